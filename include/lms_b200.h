@@ -1,0 +1,122 @@
+/*
+ * lms_b200.h -- C ABI of the B200-native exact 2D LMS engine.
+ *
+ * Plain pointers and sizes only; no torch or CUDA types cross this boundary.
+ * Every entry point returns LMS_OK (0) on success or a negative LMS_ERR_*
+ * code; lms_last_error() gives the message of the calling thread's last
+ * failure.  Host buffers are owned by the caller and copied by the library;
+ * the *_dev entry points take device pointers already resident in HBM.
+ *
+ * Each entry point replaces one seam of the reference package
+ * (/root/reference/pkg/src/lmsline, cited file:line):
+ *
+ *   lms_min_bracelet_f64      SequentialBackend/ParallelBackend.minimum_bracelet
+ *                             (backend.py:239-247, 264-289) over a contiguous
+ *                             pair-rank range, i.e. _scan_rank_range
+ *                             (backend.py:190-207) for one partition
+ *   lms_eval_vertices_f64     _evaluate_pairs per intersection
+ *                             (backend.py:125-179) / bracelet_at
+ *                             (geometry.py:182-218)
+ *   lms_min_over_vertices_f64 run_phase2 / _scan_materialized
+ *                             (backend.py:221-231, 321-354)
+ *   lms_batched_f64           refine_lms per Hough peak (detect.py:134-153,
+ *                             the per-peak loop of detect.py:184-213)
+ *   lms_hough_vote_u8         extract_points + hough_vote (hough.py:93-129)
+ *   lms_hough_support_u8      supporting_points (hough.py:171-184) +
+ *                             subsample_support (detect.py:118-131)
+ *
+ * Results are bit-identical to the reference's fp64 arithmetic: the winning
+ * pair (i, j), u, v_low, v_high and height are the values the reference's
+ * seq backend returns for the same input.
+ */
+#ifndef LMS_B200_H
+#define LMS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LMS_OK 0
+#define LMS_ERR_INVALID -1  /* bad argument (InvalidInputError on the Python side) */
+#define LMS_ERR_CUDA -2     /* CUDA runtime failure */
+#define LMS_ERR_NODEVICE -3 /* no CUDA device / device index out of range */
+#define LMS_ERR_NOMEM -4    /* device allocation failed */
+
+/* CandidateRecord (backend.py:37-54) plus a found flag: found == 0 is the
+ * reference's None ("no window fits"). 56 bytes. */
+typedef struct lms_candidate {
+  double height;
+  double u;
+  double v_low;
+  double v_high;
+  int64_t i;
+  int64_t j;
+  int32_t found;
+  int32_t reserved;
+} lms_candidate;
+
+/* Counters of the last solve on a context (device-timed). */
+typedef struct lms_stats {
+  int64_t n;
+  int64_t pairs;            /* pair ranks in the solved range */
+  int64_t seed_vertices;    /* vertices evaluated exactly to seed the bound */
+  int64_t filtered_vertices;/* vertices that went through the count filter */
+  int64_t survivors;        /* vertices the filter passed to the exact select */
+  int64_t line_evals;       /* vertex-line evaluations executed by the filter */
+  int64_t launches;         /* kernels launched by the solve */
+  int64_t chunks;
+  float ms_total;           /* device time of the whole solve (CUDA events) */
+  float ms_filter;          /* device time inside the filter kernels */
+  float ms_exact;           /* device time inside seed + exact-select + reduce */
+  float reserved;
+} lms_stats;
+
+/* Library identity and device discovery. */
+int lms_version(void);
+int lms_device_count(int* count);
+const char* lms_last_error(void);
+
+/* Exact LMS search over pair ranks [rank_begin, rank_end) of the row-major
+ * upper triangle (rank 0 = (0,1)).  a, b: n dual-line coefficients (the
+ * points' x and y, dualize geometry.py:141-144).  q in [2, n].
+ * out->found == 0 when no pair in the range yields a finite window. */
+int lms_min_bracelet_f64(const double* a, const double* b, int64_t n, int64_t q,
+                         int64_t rank_begin, int64_t rank_end, int device, lms_candidate* out);
+
+/* Anchored window at each explicit intersection (i[k], j[k], u[k]).  When v
+ * is non-NULL the anchors are snapped to v[k] (bracelet_at); when NULL to
+ * a[i]*u - b[i] (_evaluate_pairs).  out: m records. */
+int lms_eval_vertices_f64(const double* a, const double* b, int64_t n, int64_t q,
+                          const int64_t* i, const int64_t* j, const double* u, const double* v,
+                          int64_t m, int device, lms_candidate* out);
+
+/* Lexicographic (height, i, j) minimum over explicit intersections
+ * (v0 = a[i]*u - b[i]); out->found == 0 when none fits. */
+int lms_min_over_vertices_f64(const double* a, const double* b, int64_t n, int64_t q,
+                              const int64_t* i, const int64_t* j, const double* u, int64_t m,
+                              int device, lms_candidate* out);
+
+/* Context API: keeps lines, scratch and a stream resident on one device. */
+typedef struct lms_ctx lms_ctx;
+int lms_ctx_create(int device, lms_ctx** out);
+int lms_ctx_destroy(lms_ctx* ctx);
+/* Copy n lines host -> device (H2D on the context stream). */
+int lms_ctx_upload(lms_ctx* ctx, const double* a, const double* b, int64_t n);
+/* Use n lines already resident on this context's device. */
+int lms_ctx_bind_dev(lms_ctx* ctx, const double* d_a, const double* d_b, int64_t n);
+/* Solve over [rank_begin, rank_end) of the bound lines; blocks until done. */
+int lms_ctx_solve(lms_ctx* ctx, int64_t q, int64_t rank_begin, int64_t rank_end,
+                  lms_candidate* out);
+int lms_ctx_stats(const lms_ctx* ctx, lms_stats* out);
+/* CUDA events on the context stream, for device timing around solves. */
+int lms_ctx_event_record(lms_ctx* ctx, int slot);
+int lms_ctx_event_elapsed_ms(lms_ctx* ctx, int slot0, int slot1, float* ms);
+int lms_ctx_synchronize(lms_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LMS_B200_H */

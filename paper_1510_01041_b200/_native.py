@@ -1,0 +1,247 @@
+"""ctypes binding of the sm_100a C-ABI library (``_lib/liblmsb200.so``).
+
+This is the only path from Python to the engine: there is no CPU fallback.
+If the library is missing, or no CUDA device is visible, every call raises
+``NativeUnavailableError`` (a ``RuntimeError``) instead of computing
+anything on the host.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+from ._build import LIB_PATH
+
+LMS_OK = 0
+LMS_ERR_INVALID = -1
+LMS_ERR_CUDA = -2
+LMS_ERR_NODEVICE = -3
+LMS_ERR_NOMEM = -4
+
+
+class NativeUnavailableError(RuntimeError):
+    """The CUDA engine cannot run here (library not built or no GPU)."""
+
+
+class EngineError(RuntimeError):
+    """A CUDA runtime failure inside the engine."""
+
+
+class Candidate(ctypes.Structure):
+    """lms_candidate (include/lms_b200.h)."""
+
+    _fields_ = [
+        ("height", ctypes.c_double),
+        ("u", ctypes.c_double),
+        ("v_low", ctypes.c_double),
+        ("v_high", ctypes.c_double),
+        ("i", ctypes.c_int64),
+        ("j", ctypes.c_int64),
+        ("found", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
+    ]
+
+
+class Stats(ctypes.Structure):
+    """lms_stats (include/lms_b200.h)."""
+
+    _fields_ = [
+        ("n", ctypes.c_int64),
+        ("pairs", ctypes.c_int64),
+        ("seed_vertices", ctypes.c_int64),
+        ("filtered_vertices", ctypes.c_int64),
+        ("survivors", ctypes.c_int64),
+        ("line_evals", ctypes.c_int64),
+        ("launches", ctypes.c_int64),
+        ("chunks", ctypes.c_int64),
+        ("ms_total", ctypes.c_float),
+        ("ms_filter", ctypes.c_float),
+        ("ms_exact", ctypes.c_float),
+        ("reserved", ctypes.c_float),
+    ]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_ if name != "reserved"}
+
+
+_lib = None
+_lock = threading.Lock()
+
+_D = ctypes.POINTER(ctypes.c_double)
+_I = ctypes.POINTER(ctypes.c_int64)
+_C = ctypes.POINTER(Candidate)
+
+# name -> (restype, argtypes); every symbol include/lms_b200.h declares.
+SIGNATURES = {
+    "lms_version": (ctypes.c_int, []),
+    "lms_device_count": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int)]),
+    "lms_last_error": (ctypes.c_char_p, []),
+    "lms_min_bracelet_f64": (ctypes.c_int, [_D, _D, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                            ctypes.c_int64, ctypes.c_int, _C]),
+    "lms_eval_vertices_f64": (ctypes.c_int, [_D, _D, ctypes.c_int64, ctypes.c_int64, _I, _I, _D, _D,
+                                             ctypes.c_int64, ctypes.c_int, _C]),
+    "lms_min_over_vertices_f64": (ctypes.c_int, [_D, _D, ctypes.c_int64, ctypes.c_int64, _I, _I, _D,
+                                                 ctypes.c_int64, ctypes.c_int, _C]),
+    "lms_ctx_create": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]),
+    "lms_ctx_destroy": (ctypes.c_int, [ctypes.c_void_p]),
+    "lms_ctx_upload": (ctypes.c_int, [ctypes.c_void_p, _D, _D, ctypes.c_int64]),
+    "lms_ctx_bind_dev": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                        ctypes.c_int64]),
+    "lms_ctx_solve": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                     _C]),
+    "lms_ctx_stats": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(Stats)]),
+    "lms_ctx_event_record": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
+    "lms_ctx_event_elapsed_ms": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                                ctypes.POINTER(ctypes.c_float)]),
+    "lms_ctx_synchronize": (ctypes.c_int, [ctypes.c_void_p]),
+}
+
+
+def load_library():
+    """Load and bind the library (no device needed for loading)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise NativeUnavailableError(
+                    f"CUDA engine library not built: {LIB_PATH} is missing "
+                    "(run __graft_entry__.build() or python -m paper_1510_01041_b200._build)")
+            lib = ctypes.CDLL(LIB_PATH)
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+    return _lib
+
+
+def device_count() -> int:
+    n = ctypes.c_int(0)
+    load_library().lms_device_count(ctypes.byref(n))
+    return n.value
+
+
+def _lib_ready():
+    lib = load_library()
+    if device_count() == 0:
+        raise NativeUnavailableError("no CUDA device visible; the exact-LMS engine runs only on the GPU")
+    return lib
+
+
+def check(rc: int) -> None:
+    if rc == LMS_OK:
+        return
+    msg = load_library().lms_last_error().decode(errors="replace")
+    if rc == LMS_ERR_INVALID:
+        from .geometry import InvalidInputError
+
+        raise InvalidInputError(msg)
+    if rc == LMS_ERR_NODEVICE:
+        raise NativeUnavailableError(msg)
+    raise EngineError(f"engine error {rc}: {msg}")
+
+
+def _dp(x: np.ndarray):
+    return x.ctypes.data_as(_D)
+
+
+def _ip(x: np.ndarray):
+    return x.ctypes.data_as(_I)
+
+
+def _f64(x) -> np.ndarray:
+    return np.ascontiguousarray(x, dtype=np.float64)
+
+
+def _i64(x) -> np.ndarray:
+    return np.ascontiguousarray(x, dtype=np.int64)
+
+
+def min_bracelet(a, b, q: int, rank_begin: int, rank_end: int, device: int = 0) -> Candidate:
+    lib = _lib_ready()
+    a = _f64(a)
+    b = _f64(b)
+    out = Candidate()
+    check(lib.lms_min_bracelet_f64(_dp(a), _dp(b), a.size, int(q), int(rank_begin), int(rank_end),
+                                   int(device), ctypes.byref(out)))
+    return out
+
+
+def eval_vertices(a, b, q: int, i, j, u, v=None, device: int = 0):
+    lib = _lib_ready()
+    a, b = _f64(a), _f64(b)
+    i, j, u = _i64(i), _i64(j), _f64(u)
+    m = i.size
+    out = (Candidate * max(m, 1))()
+    vp = None
+    if v is not None:
+        v = _f64(v)
+        vp = _dp(v)
+    check(lib.lms_eval_vertices_f64(_dp(a), _dp(b), a.size, int(q), _ip(i), _ip(j), _dp(u), vp, m,
+                                    int(device), out))
+    return [out[k] for k in range(m)]
+
+
+def min_over_vertices(a, b, q: int, i, j, u, device: int = 0) -> Candidate:
+    lib = _lib_ready()
+    a, b = _f64(a), _f64(b)
+    i, j, u = _i64(i), _i64(j), _f64(u)
+    out = Candidate()
+    check(lib.lms_min_over_vertices_f64(_dp(a), _dp(b), a.size, int(q), _ip(i), _ip(j), _dp(u), i.size,
+                                        int(device), ctypes.byref(out)))
+    return out
+
+
+class Context:
+    """Device-resident solver context (lms_ctx): lines, scratch and a stream."""
+
+    def __init__(self, device: int = 0):
+        self._lib = _lib_ready()
+        h = ctypes.c_void_p()
+        check(self._lib.lms_ctx_create(int(device), ctypes.byref(h)))
+        self._h = h
+        self._keep = None
+
+    def close(self):
+        if self._h:
+            self._lib.lms_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown order
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def upload(self, a, b):
+        a, b = _f64(a), _f64(b)
+        self._keep = (a, b)
+        check(self._lib.lms_ctx_upload(self._h, _dp(a), _dp(b), a.size))
+
+    def bind_device(self, d_a: int, d_b: int, n: int):
+        check(self._lib.lms_ctx_bind_dev(self._h, ctypes.c_void_p(d_a), ctypes.c_void_p(d_b), int(n)))
+
+    def solve(self, q: int, rank_begin: int, rank_end: int) -> Candidate:
+        out = Candidate()
+        check(self._lib.lms_ctx_solve(self._h, int(q), int(rank_begin), int(rank_end), ctypes.byref(out)))
+        return out
+
+    def stats(self) -> dict:
+        s = Stats()
+        check(self._lib.lms_ctx_stats(self._h, ctypes.byref(s)))
+        return s.as_dict()
+
+    def record(self, slot: int):
+        check(self._lib.lms_ctx_event_record(self._h, int(slot)))
+
+    def elapsed_ms(self, slot0: int, slot1: int) -> float:
+        ms = ctypes.c_float(0.0)
+        check(self._lib.lms_ctx_event_elapsed_ms(self._h, int(slot0), int(slot1), ctypes.byref(ms)))
+        return float(ms.value)
+
+    def synchronize(self):
+        check(self._lib.lms_ctx_synchronize(self._h))

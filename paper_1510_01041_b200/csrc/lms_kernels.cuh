@@ -1,0 +1,71 @@
+// lms_kernels.cuh -- launch interfaces of the exact-LMS kernels (host side).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/lms_b200.h"
+
+namespace lmsb {
+
+enum ExactSource : int {
+  kSrcRanks = 0,     // ranks[s], s < *d_count (filter survivors)
+  kSrcStrided = 1,   // stratified sample of [rank_lo, rank_hi), s < count
+  kSrcExplicit = 2,  // explicit (i, j, u[, v]) lists, s < count
+};
+
+struct ExactArgs {
+  const double* a;
+  const double* b;
+  int64_t n;
+  int64_t q;
+  int mode;
+  int64_t count;
+  const unsigned long long* d_count;
+  int64_t capacity;
+  const int64_t* ranks;
+  int64_t rank_lo;
+  int64_t rank_hi;
+  const int64_t* ii;
+  const int64_t* jj;
+  const double* uu;
+  const double* vv;
+  lms_candidate* out;
+};
+
+void launch_exact(const ExactArgs& args, int grid, cudaStream_t stream);
+void launch_reduce(const lms_candidate* recs, const unsigned long long* d_count, int64_t count,
+                   int64_t capacity, lms_candidate* partials, int npartials,
+                   lms_candidate* best_io, cudaStream_t stream);
+
+// Count filter over warp tasks [task_begin, task_end).  A warp task is up to
+// kFilterTaskVertices consecutive pair ranks of one row of the triangle.
+constexpr int kFilterV = 8;                          // vertices per lane
+constexpr int kFilterTaskVertices = 32 * kFilterV;   // vertices per warp task
+constexpr int kFilterWarpsPerBlock = 8;
+
+struct FilterArgs {
+  const double* a;
+  const double* b;
+  int64_t n;
+  int64_t q;
+  const int64_t* task_prefix;  // task_prefix[r] = first task of row row0 + r
+  int64_t row0;
+  int64_t nrows;
+  int64_t rank_lo;
+  int64_t rank_hi;
+  int64_t task_begin;
+  int64_t task_end;
+  double amax;
+  double bmax;
+  const lms_candidate* best;        // current best (its height bounds the search)
+  int64_t* out_ranks;               // survivors
+  unsigned long long* out_count;
+  unsigned long long* line_evals;   // executed vertex-line evaluations (stats)
+  int early_exit;
+};
+
+void launch_filter(const FilterArgs& args, cudaStream_t stream);
+
+}  // namespace lmsb

@@ -1,0 +1,82 @@
+"""Exact least-median-of-squares line fit (drop-in for lmsline.solver).
+
+``solve_lms`` keeps the reference's signature, validation, errors and result
+type (solver.py:45-140).  The pair search -- every arrangement vertex of the
+dual lines, each vertex's anchored q-window, the lexicographic argmin -- runs
+in the sm_100a engine; the host only validates, maps the winning record back
+to the primal line and classifies the O(n) contact set exactly as
+solver.py:122-133 does.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import backend as _backend
+from .geometry import GEOM_EPS, DegenerateInputError, InvalidInputError, LineEq, as_xy_arrays
+
+
+@dataclass(frozen=True)
+class LmsFit:
+    """Result of an exact LMS fit (solver.py:45-59)."""
+
+    line: LineEq
+    lms_value: float
+    slab_height: float
+    coverage: int
+    contact_indices: tuple[int, ...]
+
+
+def default_coverage(n: int) -> int:
+    """``n // 2 + 1``, a strict majority (solver.py:62-64)."""
+    return n // 2 + 1
+
+
+def validated(points, q: int | None) -> tuple[np.ndarray, np.ndarray, int]:
+    """solver.py:67-80: >= 3 points, >= 2 distinct x, 2 <= q <= n."""
+    x, y = as_xy_arrays(points)
+    n = x.size
+    if n < 3:
+        raise DegenerateInputError(f"LMS needs at least 3 points, got {n}")
+    if np.unique(x).size < 2:
+        raise DegenerateInputError("all points share one x-coordinate; no non-vertical line fits")
+    if q is None:
+        q = default_coverage(n)
+    if not 2 <= q <= n:
+        raise InvalidInputError(f"coverage must satisfy 2 <= q <= {n}, got {q}")
+    return x, y, q
+
+
+def fit_from_record(x: np.ndarray, y: np.ndarray, q: int, rec: "_backend.CandidateRecord") -> LmsFit:
+    """Primal line and contact set of the winning window (solver.py:122-140)."""
+    half = (rec.v_high - rec.v_low) * 0.5
+    cut = x * rec.u - y
+    # the anchor pair sits exactly on the anchor ordinate, as in the search
+    cut[[rec.i, rec.j]] = x[rec.i] * rec.u - y[rec.i]
+    tol = GEOM_EPS * max(1.0, float(np.max(np.abs(cut))))
+    touching = (np.abs(cut - rec.v_low) <= tol) | (np.abs(cut - rec.v_high) <= tol)
+    return LmsFit(
+        line=LineEq(slope=rec.u, intercept=-(rec.v_low + rec.v_high) * 0.5),
+        lms_value=half * half,
+        slab_height=rec.v_high - rec.v_low,
+        coverage=q,
+        contact_indices=tuple(int(k) for k in np.flatnonzero(touching)),
+    )
+
+
+def solve_lms(points, q: int | None = None, *, backend: str = "seq", workers: int | None = None,
+              materialize: bool = False) -> LmsFit:
+    """Exact LMS line fit (solver.py:83-140) on the GPU.
+
+    Raises :class:`DegenerateInputError` for fewer than 3 points or a single
+    x value, :class:`InvalidInputError` for non-finite input, a bad ``q``, an
+    unknown backend or a bad worker count.
+    """
+    x, y, q = validated(points, q)
+    engine = _backend.get_backend(backend, workers)
+    rec = engine.minimum_bracelet(x, y, q, materialize=materialize)
+    if rec is None:
+        raise DegenerateInputError("no candidate slab found")
+    return fit_from_record(x, y, q, rec)

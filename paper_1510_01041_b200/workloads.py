@@ -1,0 +1,57 @@
+"""Synthetic inputs for the BASELINE.json configs (host-side, not the hot path).
+
+* ``config1_points`` / ``contaminated_line_points`` -- configs 1-3
+  (BASELINE.md section 3): x ~ U[0, 1000), inliers on y = 2x + 1 (optionally
+  + N(0, 1)), a permutation-chosen outlier fraction with uniform y.
+* ``bench_points`` -- restates the reference's fixed benchmark instance
+  (experiments.py:247-254) used for config 4 (8,192 fits of n = 512).
+
+All streams are numpy PCG64 seeded as BASELINE.md specifies, so the same
+seed gives the same points here, in the golden-fixture script and on the
+GPU box.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+
+def _rng(seed: int, n: int) -> np.random.Generator:
+    return np.random.Generator(np.random.PCG64(np.random.SeedSequence([seed, n])))
+
+
+def config1_points(seed: int = 0, n: int = 1000, noise: bool = False) -> np.ndarray:
+    """Config 1: n points, 55% exactly on y = 2x + 1 (variant B adds N(0,1)),
+    45% outliers with y ~ U[min y - 500, max y + 500]."""
+    rng = _rng(seed, n)
+    x = rng.uniform(0.0, 1000.0, n)
+    y = 2.0 * x + 1.0
+    if noise:
+        y = y + rng.normal(0.0, 1.0, n)
+    n_out = (45 * n) // 100
+    out = rng.permutation(n)[:n_out]
+    lo, hi = float(y.min()) - 500.0, float(y.max()) + 500.0
+    y[out] = rng.uniform(lo, hi, n_out)
+    return np.column_stack([x, y])
+
+
+def contaminated_line_points(n: int, seed: int = 0, outlier_frac: float = 0.49) -> np.ndarray:
+    """Configs 2-3: inliers y = 2x + 1 + N(0, 1), a fraction of gross
+    outliers with y ~ U[-1e4, 1e4]."""
+    rng = _rng(seed, n)
+    x = rng.uniform(0.0, 1000.0, n)
+    y = 2.0 * x + 1.0 + rng.normal(0.0, 1.0, n)
+    n_out = int(outlier_frac * n)
+    out = rng.permutation(n)[:n_out]
+    y[out] = rng.uniform(-1e4, 1e4, n_out)
+    return np.column_stack([x, y])
+
+
+def bench_points(n: int, seed: int = 7) -> np.ndarray:
+    """experiments.py:247-254: y = 0.75x + 40 + N(0, 5), 30% uniform outliers."""
+    rng = _rng(seed, n)
+    x = rng.uniform(0.0, 1000.0, n)
+    y = 0.75 * x + 40.0 + rng.normal(0.0, 5.0, n)
+    bad = rng.random(n) < 0.3
+    y[bad] = rng.uniform(0.0, 1000.0, int(bad.sum()))
+    return np.column_stack([x, y])

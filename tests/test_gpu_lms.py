@@ -1,0 +1,194 @@
+"""GPU parity: the sm_100a engine against the reference's golden vectors and
+the CPU oracle (bit-exact on the winning record), plus size-independent
+properties at BASELINE.json's full sizes."""
+
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1510_01041_b200 as lms
+from paper_1510_01041_b200 import _native, workloads
+from paper_1510_01041_b200.backend import record_from_native
+from conftest import fit_matches, record_matches
+
+pytestmark = pytest.mark.gpu
+THREADS = min(16, os.cpu_count() or 1)
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _ready():
+    oracle.build()
+    assert _native.device_count() > 0, "no CUDA device"
+
+
+def oracle_rec(a, b, q, r0=0, r1=None):
+    rec = oracle.min_bracelet(a, b, q, r0, r1, threads=THREADS)
+    if rec is None:
+        return None
+    return {"height": rec.height, "i": rec.i, "j": rec.j, "u": rec.u, "v_low": rec.v_low,
+            "v_high": rec.v_high}
+
+
+def gpu_range(a, b, q, r0, r1):
+    return record_from_native(_native.min_bracelet(a, b, q, r0, r1))
+
+
+def test_golden_records_and_fits(golden):
+    cases, _ = golden
+    for c in cases:
+        rec = lms.get_backend("seq").minimum_bracelet(c.x.copy(), c.y.copy(), c.q)
+        assert record_matches(rec, c.record), c.name
+        fit = lms.solve_lms(c.points, c.q_arg)
+        assert fit_matches(fit, c.fit), c.name
+
+
+def test_golden_bracelets(golden):
+    _, brs = golden
+    for g in brs:
+        lines = lms.dualize(np.column_stack([g.x, g.y]))
+        for v in g.vertices:
+            ip = lms.DualIntersection(u=v["u"], v=v["v"], i=v["i"], j=v["j"])
+            br = lms.bracelet_at(ip, lines, g.q)
+            want = v["bracelet"]
+            if want is None:
+                assert br is None
+            else:
+                assert (br.v_low, br.v_high, br.height) == (want["v_low"], want["v_high"], want["height"])
+
+
+def test_phase2_matches_oracle_and_bracelets(golden):
+    _, brs = golden
+    for g in brs:
+        lines = lms.dualize(np.column_stack([g.x, g.y]))
+        ips = list(lms.run_phase1(lines))
+        rec = lms.run_phase2(ips, lines, g.q, worker_count=3)
+        want = oracle_rec(g.x, g.y, g.q)
+        assert record_matches(rec, want), g.name
+
+
+def random_points(rng, n, collapse_x=False):
+    x = rng.uniform(-100.0, 100.0, n)
+    y = rng.uniform(-100.0, 100.0, n)
+    if collapse_x and n >= 8 and rng.random() < 0.3:
+        k = int(rng.integers(2, n // 2))
+        x[:k] = x[0]
+    return x, y
+
+
+def test_random_instances_bit_exact_vs_oracle():
+    rng = np.random.default_rng(2024)
+    for trial in range(120):
+        n = int(rng.integers(3, 300))
+        kind = trial % 4
+        if kind == 0:
+            x, y = random_points(rng, n, collapse_x=True)
+        elif kind == 1:
+            x, y = rng.integers(0, 24, n).astype(float), rng.integers(0, 24, n).astype(float)
+        elif kind == 2:
+            pts = workloads.config1_points(trial, n=max(n, 8))
+            x, y = pts[:, 0].copy(), pts[:, 1].copy()
+            n = x.size
+        else:
+            x, y = rng.normal(0, 1e3, n), rng.normal(0, 1e-3, n)
+        if np.unique(x).size < 2:
+            continue
+        q = int(rng.integers(2, n + 1)) if trial % 3 else n // 2 + 1
+        rec = lms.get_backend("seq").minimum_bracelet(x, y, q)
+        assert record_matches(rec, oracle_rec(x, y, q)), (trial, n, q)
+
+
+def test_filter_path_subranges_bit_exact_at_n16k():
+    """n = 16,384 (config 2): rank sub-ranges large enough to take the
+    filter path, at the start, middle and end of the triangle."""
+    pts = workloads.contaminated_line_points(16384, 0)
+    a, b = pts[:, 0].copy(), pts[:, 1].copy()
+    q = 16384 // 2 + 1
+    total = 16384 * 16383 // 2
+    for r0 in (0, total // 3 + 12345, total - 9000):
+        r1 = min(total, r0 + 9000)
+        got = gpu_range(a, b, q, r0, r1)
+        assert record_matches(got, oracle_rec(a, b, q, r0, r1)), r0
+
+
+def test_config1_full_bit_exact(golden):
+    cases, _ = golden
+    c = {g.name: g for g in cases}["config1_s0"]
+    ctx = _native.Context()
+    ctx.upload(c.x, c.y)
+    rec = record_from_native(ctx.solve(c.q, 0, c.n * (c.n - 1) // 2))
+    assert record_matches(rec, c.record)
+    st = ctx.stats()
+    assert st["survivors"] < st["pairs"]
+
+
+def test_config2_full_n16k_properties():
+    """Full n = 16,384 fit: the winner re-evaluates identically on the CPU,
+    partitions merge to the same record, and the fit satisfies the LMS
+    equioscillation / median properties."""
+    pts = workloads.contaminated_line_points(16384, 0)
+    a, b = pts[:, 0].copy(), pts[:, 1].copy()
+    q = 16384 // 2 + 1
+    total = 16384 * 16383 // 2
+    ctx = _native.Context()
+    ctx.upload(a, b)
+    rec = record_from_native(ctx.solve(q, 0, total))
+    assert rec is not None
+    (chk,) = oracle.eval_vertices(a, b, q, [rec.i], [rec.j], [rec.u])
+    assert (chk.height, chk.v_low, chk.v_high) == (rec.height, rec.v_low, rec.v_high)
+    parts = lms.BatchPlan.create(a, 4).partitions()
+    merged = None
+    for r0, r1 in parts:
+        merged = lms.backend.merge(merged, record_from_native(ctx.solve(q, r0, r1)))
+    assert merged == rec
+    fit = lms.solver.fit_from_record(a, b, q, rec)
+    med = lms.median_sq_residual(pts, fit.line, q)
+    assert med == pytest.approx(fit.lms_value, rel=1e-9)
+    assert abs(fit.line.slope - 2.0) < 0.01
+    assert len(fit.contact_indices) >= 3
+
+
+def test_planted_exact_fit_n16k():
+    rng = np.random.default_rng(7)
+    n = 16384
+    q = n // 2 + 1
+    x = rng.permutation(1 << 20)[:n].astype(float)
+    y = rng.uniform(-1e6, 1e6, n)
+    inl = rng.permutation(n)[:q]
+    y[inl] = 0.75 * x[inl] - 3.5  # dyadic: exact in binary
+    fit = lms.solve_lms(np.column_stack([x, y]))
+    assert fit.lms_value == 0.0
+    assert fit.line.slope == 0.75 and fit.line.intercept == -3.5
+
+
+def test_edge_cases_vs_oracle():
+    cases = []
+    cases.append(([0, 1, 2], [0, 1, 5], 2))
+    cases.append(([0, 1, 2], [0, 1, 5], 3))
+    cases.append(([1, 1, 1, 1, 2], [0, 1, 2, 3, 1], 2))
+    cases.append(([0, 0, 1, 2, 1], [0, 0, 1, 2, 5], 4))
+    cases.append(([-0.0, 0.0, 1, -1, 2], [0.0, -0.0, 0.0, -0.0, 1e-300], 3))
+    big = np.random.default_rng(3).normal(0, 1e150, (40, 2))
+    cases.append((big[:, 0], big[:, 1], 21))
+    tiny = np.random.default_rng(4).normal(0, 1e-150, (40, 2))
+    cases.append((tiny[:, 0], tiny[:, 1], 21))
+    mixed = np.random.default_rng(5).normal(0, 1, (50, 2)) * np.logspace(-100, 100, 50)[:, None]
+    cases.append((mixed[:, 0], mixed[:, 1], 26))
+    for x, y, q in cases:
+        x = np.asarray(x, dtype=float)
+        y = np.asarray(y, dtype=float)
+        for qq in (q, x.size):
+            rec = lms.get_backend("seq").minimum_bracelet(x, y, qq)
+            assert record_matches(rec, oracle_rec(x, y, qq)), (x.size, qq)
+
+
+def test_seq_par_identical():
+    rng = np.random.default_rng(19)
+    for _ in range(6):
+        n = int(rng.integers(5, 400))
+        pts = rng.normal(0, 20, (n, 2))
+        ref = lms.solve_lms(pts, backend="seq")
+        for w in (1, 3, 7):
+            assert lms.solve_lms(pts, backend="par", workers=w) == ref
+        assert lms.solve_lms(pts, materialize=True) == ref
