@@ -1,0 +1,369 @@
+#!/usr/bin/env python
+"""Benchmark of the exact 2D LMS fit (BASELINE.json metric, config 2).
+
+One step = one complete exact LMS fit of n = 16,384 points (49% gross
+outliers, q = n//2 + 1, fp64): seed, count filter over all n(n-1)/2
+arrangement vertices, exact re-evaluation of the survivors, argmin.  With
+N > 1 processes (torchrun) the vertex-rank space of the SAME fit is split
+into N contiguous partitions and the per-rank records are combined with one
+NCCL all_gather each step (strong scaling).
+
+Prints one JSON line on rank 0.  ``value`` is vertex-line evaluations per
+second in the reference's counting (n * n(n-1)/2 per fit / device time);
+``time_to_fit_s`` is the per-fit device time.  ``--impl reference`` times
+the CPU restatement of the reference's algorithm (oracle/, C++ port with
+std::nth_element in place of np.sort, all host threads) on a bounded sample
+of the same workload and extrapolates to the same metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "exact 2D LMS vertex-line evals/s (time-to-fit) at n=16384, fp64"
+UNIT = "vertex-line evals/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--n", type=int, default=16384)
+    p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--cpu-vertices-per-thread", type=int, default=3000)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+def workload(n: int, seed: int):
+    from paper_1510_01041_b200 import workloads
+
+    pts = workloads.contaminated_line_points(n, seed)
+    return pts, n // 2 + 1
+
+
+def config(n: int, world: int) -> dict:
+    return {
+        "workload": f"config2: exact LMS fit, n={n} points, 49% gross outliers, q=n//2+1, fp64",
+        "n": n,
+        "pairs": n * (n - 1) // 2,
+        "q": n // 2 + 1,
+        "partitioning": f"contiguous vertex-rank partitions x{world}, one NCCL all_gather per fit",
+        "l2": "flushed between timed steps (256 MiB write); the 256 KiB line set is re-read from "
+              "L2 within a fit by design",
+    }
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi-equivalent NVML sampling of SM clocks / throttle reasons."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nv = None
+            return self
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self._stop.wait(0.05)
+
+    def stop(self) -> dict:
+        self._stop.set()
+        if self._t:
+            self._t.join()
+        med = statistics.median(self.samples) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------------- cpu baseline
+def cpu_baseline(a, b, q, n, per_thread: int) -> dict:
+    """Oracle (C++ restatement of the reference's scan) on 16 evenly spaced
+    rank slices of the same fit, all host threads."""
+    import oracle
+
+    oracle.build()
+    threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    total = n * (n - 1) // 2
+    slices = 16
+    per_slice = max(1, (per_thread * threads) // slices)
+    t0 = time.perf_counter()
+    verts = 0
+    for s in range(slices):
+        r0 = (s * total) // slices
+        r1 = min(total, r0 + per_slice)
+        oracle.min_bracelet(a, b, q, r0, r1, threads=threads)
+        verts += r1 - r0
+    dt = time.perf_counter() - t0
+    rate = n * verts / dt
+    return {
+        "value": rate,
+        "unit": UNIT,
+        "cores": threads,
+        "kind": "port",
+        "sample": f"{verts} vertices ({slices} evenly spaced rank slices of the n={n} fit) x {n} lines "
+                  f"in {dt:.2f}s; full fit extrapolates to {n * total / rate:.0f}s",
+        "time_to_fit_s_extrapolated": n * total / rate,
+    }
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    pts, q = workload(args.n, args.seed)
+    a, b = pts[:, 0].copy(), pts[:, 1].copy()
+    for _ in range(max(0, min(args.warmup, 1))):
+        cpu_baseline(a, b, q, args.n, max(50, args.cpu_vertices_per_thread // 10))
+    vals = []
+    last = None
+    for _ in range(args.steps):
+        last = cpu_baseline(a, b, q, args.n, max(50, args.cpu_vertices_per_thread // 3))
+        vals.append(last["value"])
+    value = float(statistics.median(vals))
+    n = args.n
+    total = n * (n - 1) // 2
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": args.gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": 1e3 * n * total / value,
+        "time_to_fit_s": n * total / value,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (workloads.contaminated_line_points, seed 0)",
+        "config": config(n, 1),
+        "cpu_baseline": {**last, "value": value},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "CPU restatement of the reference's exact scan (oracle/lms_oracle.cpp), each step a "
+                "bounded rank sample of the fit extrapolated to the full fit; the reference package "
+                "itself is pure Python+numpy with no GPU path",
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------- ours
+def load_profile_traffic():
+    path = os.path.join(ROOT, "profiles", "filter_ncu_summary.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return d.get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def run_ours(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    import torch
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1510_01041_b200 import _native, distributed, solve_lms
+    from paper_1510_01041_b200.backend import record_from_native
+
+    n = args.n
+    pts, q = workload(n, args.seed)
+    a, b = pts[:, 0].copy(), pts[:, 1].copy()
+    total = n * (n - 1) // 2
+    r0, r1 = distributed.partition(total, world, rank)
+
+    ctx = _native.Context(local)
+    ctx.upload(a, b)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+
+    def step():
+        rec = record_from_native(ctx.solve(q, r0, r1)) if r1 > r0 else None
+        if world > 1:
+            rec = distributed.combine(distributed.all_gather_records(rec, device=torch.device("cuda", local)))
+        return rec
+
+    for _ in range(args.warmup):
+        step()
+
+    sampler = ClockSampler(local).start()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    dev_ms = 0.0
+    filt_ms = 0.0
+    evals_exec = 0
+    launches = 0
+    survivors = 0
+    recs = []
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        ctx.record(0)
+        rec = step()
+        ctx.record(1)
+        dev_ms += ctx.elapsed_ms(0, 1)
+        st = ctx.stats()
+        filt_ms += st["ms_filter"]
+        evals_exec += st["line_evals"]
+        launches += st["launches"]
+        survivors += st["survivors"]
+        recs.append(rec)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clocks = sampler.stop()
+
+    t_max = dev_ms
+    if dist:
+        tt = torch.tensor([dev_ms], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_max = float(tt.item())
+    ms_per_step = t_max / args.steps
+    value = args.steps * n * total / (t_max / 1e3)
+    assert all(r == recs[0] for r in recs), "non-deterministic result across steps"
+
+    # ---- e2e through the public API (host arrays in, LmsFit out), wall clock
+    e2e_s = 0.0
+    for _ in range(max(1, args.steps)):
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        if world == 1:
+            fit = solve_lms(pts)
+        else:
+            from paper_1510_01041_b200.solver import fit_from_record, validated
+
+            x, y, qq = validated(pts, None)
+            rec = distributed.solve_distributed(x, y, qq)
+            fit = fit_from_record(x, y, qq, rec)
+        e2e_s += time.perf_counter() - t0
+        assert fit.coverage == q
+    if dist:
+        tt = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = float(tt.item())
+    e2e_value = max(1, args.steps) * n * total / e2e_s
+
+    # ---- roofline of the dominant kernel (the FP64 count filter)
+    dfma_rate = _native.probe_fp64_rate(local)
+    achieved = 2.0 * evals_exec / (filt_ms / 1e3) / 1e12 if filt_ms > 0 else 0.0
+    peak = dfma_rate / 1e12  # non-FMA FP64 op rate: one DMUL or DADD (1 flop) per pipe slot
+    roofline = {
+        "bound": "fp64",
+        "kernel": "filter_kernel",
+        "achieved": achieved,
+        "peak": peak,
+        "unit": "TFLOP/s",
+        "frac": achieved / peak if peak else None,
+        "traffic": load_profile_traffic(),
+        "algorithmic": "2 FP64 flops (u*a_k - b_k) per EXECUTED vertex-line eval "
+                       "(early-exited lines not counted) / filter kernel event time",
+        "peak_source": "measured in-run: DFMA issue-rate probe (lms_probe_fp64_rate), non-FMA "
+                       "op peak = DFMA/s; MEASURED_PEAKS.json has no FP64 figure",
+        "filter_share_of_step": filt_ms / dev_ms if dev_ms else None,
+        "executed_evals_per_step": evals_exec / args.steps,
+        "reference_evals_per_step": n * total,
+    }
+
+    out = None
+    if rank == 0:
+        best = recs[0]
+        out = {
+            "metric": METRIC,
+            "value": value,
+            "unit": UNIT,
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_per_step,
+            "time_to_fit_s": ms_per_step / 1e3,
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic (workloads.contaminated_line_points, seed 0)",
+            "config": config(n, world),
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 16 * n,
+                    "d2h_bytes_per_step": 56 + (8 * 7 * world if world > 1 else 0),
+                    "seconds_per_fit": e2e_s / max(1, args.steps),
+                    "path": "solve_lms(points) -> LmsFit" if world == 1 else
+                            "distributed.solve_distributed + fit_from_record"},
+            "gpu_launches": launches,
+            "roofline": roofline,
+            "clocks": clocks,
+            "survivors_per_step": survivors / args.steps,
+            "result": {"i": best.i, "j": best.j, "height": best.height, "u": best.u},
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline(a, b, q, n, args.cpu_vertices_per_thread)
+        print(json.dumps(out), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

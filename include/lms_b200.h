@@ -115,6 +115,11 @@ int lms_ctx_event_record(lms_ctx* ctx, int slot);
 int lms_ctx_event_elapsed_ms(lms_ctx* ctx, int slot0, int slot1, float* ms);
 int lms_ctx_synchronize(lms_ctx* ctx);
 
+/* Diagnostics: measured FP64 pipe issue rate of `device` (DFMA per second,
+ * all SMs busy, 8 independent chains per thread).  bench.py's roofline
+ * denominator for the FP64-bound filter kernel. */
+int lms_probe_fp64_rate(int device, double* dfma_per_second);
+
 #ifdef __cplusplus
 }
 #endif

@@ -5,7 +5,7 @@ Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
 as the checker or the timed CPU baseline.  The product package
 (``paper_1510_01041_b200``) never imports it.
 
-It wraps ``lms_oracle.c`` (a C restatement of the reference's
+It wraps ``lms_oracle.cpp`` (a C restatement of the reference's
 ``_scan_rank_range`` / ``_evaluate_pairs`` / ``_merge``, see the file header
 for the file:line map) and restates the solver's primal mapping and contact
 set (``solver.py:115-140``) in numpy, so that an oracle ``LmsFit`` can be

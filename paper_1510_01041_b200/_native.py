@@ -98,6 +98,7 @@ SIGNATURES = {
     "lms_ctx_event_elapsed_ms": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                                 ctypes.POINTER(ctypes.c_float)]),
     "lms_ctx_synchronize": (ctypes.c_int, [ctypes.c_void_p]),
+    "lms_probe_fp64_rate": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_double)]),
 }
 
 
@@ -194,6 +195,14 @@ def min_over_vertices(a, b, q: int, i, j, u, device: int = 0) -> Candidate:
     check(lib.lms_min_over_vertices_f64(_dp(a), _dp(b), a.size, int(q), _ip(i), _ip(j), _dp(u), i.size,
                                         int(device), ctypes.byref(out)))
     return out
+
+
+def probe_fp64_rate(device: int = 0) -> float:
+    """Measured DFMA issue rate (per second) of the FP64 pipe on `device`."""
+    lib = _lib_ready()
+    r = ctypes.c_double(0.0)
+    check(lib.lms_probe_fp64_rate(int(device), ctypes.byref(r)))
+    return r.value
 
 
 class Context:
