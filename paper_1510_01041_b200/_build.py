@@ -17,7 +17,8 @@ CSRC = os.path.join(PKG_DIR, "csrc")
 LIB_DIR = os.path.join(PKG_DIR, "_lib")
 LIB_PATH = os.path.join(LIB_DIR, "liblmsb200.so")
 
-SOURCES = ["lms_engine.cu", "lms_exact.cu", "lms_filter.cu", "lms_probe.cu"]
+SOURCES = ["lms_engine.cu", "lms_exact.cu", "lms_filter.cu", "lms_filter32.cu", "lms_filter32m.cu",
+           "lms_probe.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -28,8 +29,9 @@ def nvcc() -> str:
     return cand
 
 
-def build(verbose: bool = False, extra: list[str] | None = None) -> str:
-    os.makedirs(LIB_DIR, exist_ok=True)
+def build(verbose: bool = False, extra: list[str] | None = None, out: str | None = None) -> str:
+    out = out or LIB_PATH
+    os.makedirs(os.path.dirname(out), exist_ok=True)
     objs = []
     common = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
               "-I", os.path.join(ROOT, "include"), "--expt-relaxed-constexpr"]
@@ -38,15 +40,15 @@ def build(verbose: bool = False, extra: list[str] | None = None) -> str:
     if extra:
         common += extra
     for src in SOURCES:
-        obj = os.path.join(LIB_DIR, src.replace(".cu", ".o"))
+        obj = os.path.join(os.path.dirname(out), src.replace(".cu", ".o"))
         subprocess.run([*common, "-c", os.path.join(CSRC, src), "-o", obj], check=True)
         objs.append(obj)
-    tmp = LIB_PATH + ".tmp"
+    tmp = out + ".tmp"
     subprocess.run([nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-cudart", "static"], check=True)
-    os.replace(tmp, LIB_PATH)
+    os.replace(tmp, out)
     for o in objs:
         os.remove(o)
-    return LIB_PATH
+    return out
 
 
 if __name__ == "__main__":

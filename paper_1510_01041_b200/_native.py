@@ -107,11 +107,12 @@ def load_library():
     global _lib
     with _lock:
         if _lib is None:
-            if not os.path.exists(LIB_PATH):
+            path = os.environ.get("LMSB_LIB_PATH", LIB_PATH)  # dev override for A/B builds
+            if not os.path.exists(path):
                 raise NativeUnavailableError(
-                    f"CUDA engine library not built: {LIB_PATH} is missing "
+                    f"CUDA engine library not built: {path} is missing "
                     "(run __graft_entry__.build() or python -m paper_1510_01041_b200._build)")
-            lib = ctypes.CDLL(LIB_PATH)
+            lib = ctypes.CDLL(path)
             for name, (res, args) in SIGNATURES.items():
                 fn = getattr(lib, name)
                 fn.restype = res

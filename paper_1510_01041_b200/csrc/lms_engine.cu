@@ -19,6 +19,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -57,6 +58,14 @@ constexpr int64_t kSeeds = 2048;            // exact seed vertices per solve
 constexpr int64_t kExhaustive = 4096;       // ranges this small skip the filter
 constexpr int64_t kChunkVertices = 1 << 24; // filter chunk (and survivor capacity)
 constexpr int kNumEvents = 16;
+
+// Count-filter variants: all-FP64 (lms_filter.cu), FP16 compare + mma.sync
+// counting (lms_filter32.cu), FP16 compare + integer-mask counting
+// (lms_filter32m.cu).
+constexpr int kFilterFp64 = 1;
+constexpr int kFilterMma = 2;
+constexpr int kFilterMask = 3;
+constexpr int kDefaultFilter = kFilterMask;
 
 template <typename T>
 int grow(T** ptr, int64_t* cap, int64_t need) {
@@ -107,6 +116,7 @@ struct lms_ctx {
   int64_t cap_uu = 0, cap_vv = 0;
   lms_candidate* h_best = nullptr;  // pinned
   lms_stats stats{};
+  int filter_variant = 0;  // LMSB_FILTER=fp64|mma|mask (A/B switch; see kDefaultFilter)
   std::mutex mu;
 };
 
@@ -119,6 +129,11 @@ int ctx_init(lms_ctx* c, int device) {
   if (device < 0 || device >= count)
     return set_error(LMS_ERR_NODEVICE, "device %d out of range (%d devices)", device, count);
   c->device = device;
+  const char* fv = getenv("LMSB_FILTER");
+  c->filter_variant = kDefaultFilter;
+  if (fv && std::strcmp(fv, "fp64") == 0) c->filter_variant = kFilterFp64;
+  if (fv && std::strcmp(fv, "mma") == 0) c->filter_variant = kFilterMma;
+  if (fv && std::strcmp(fv, "mask") == 0) c->filter_variant = kFilterMask;
   CUDA_TRY(cudaSetDevice(device));
   CUDA_TRY(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device));
   CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
@@ -243,6 +258,10 @@ int ctx_solve(lms_ctx* c, int64_t q, int64_t R0, int64_t R1, lms_candidate* out)
 
   int64_t nchunks = 0;
   if (!exhaustive) {
+    const int variant = c->filter_variant;
+    const int64_t task_vertices = variant == kFilterFp64   ? lmsb::kFilterTaskVertices
+                                  : variant == kFilterMask ? lmsb::kFilter32mTaskVertices
+                                                           : lmsb::kFilter32TaskVertices;
     // Warp tasks per row of the range.
     int64_t i0, j0, i1, j1;
     lmsb::decode_rank(n, R0, &i0, &j0);
@@ -255,7 +274,7 @@ int ctx_solve(lms_ctx* c, int64_t q, int64_t R0, int64_t R1, lms_candidate* out)
       const int64_t lo = std::max(lmsb::row_offset(n, i), R0);
       const int64_t hi = std::min(lmsb::row_offset(n, i) + (n - 1 - i), R1);
       prefix[r] = acc;
-      acc += (hi - lo + lmsb::kFilterTaskVertices - 1) / lmsb::kFilterTaskVertices;
+      acc += (hi - lo + task_vertices - 1) / task_vertices;
     }
     prefix[nrows] = acc;
     const int64_t ntasks = acc;
@@ -263,7 +282,7 @@ int ctx_solve(lms_ctx* c, int64_t q, int64_t R0, int64_t R1, lms_candidate* out)
     if (rc) return rc;
     CUDA_TRY(cudaMemcpyAsync(c->d_task_prefix, prefix.data(), sizeof(int64_t) * (nrows + 1),
                              cudaMemcpyHostToDevice, c->stream));
-    const int64_t chunk_tasks = kChunkVertices / lmsb::kFilterTaskVertices;
+    const int64_t chunk_tasks = kChunkVertices / task_vertices;
     nchunks = (ntasks + chunk_tasks - 1) / chunk_tasks;
     const int64_t cap = std::min<int64_t>(kChunkVertices, span);
     rc = grow(&c->d_ranks, &c->cap_ranks, cap);
@@ -300,7 +319,9 @@ int ctx_solve(lms_ctx* c, int64_t q, int64_t R0, int64_t R1, lms_candidate* out)
       fa.line_evals = c->d_counters + 1;
       fa.early_exit = 1;
       CUDA_TRY(cudaEventRecord(c->ev_chunk[2 * ch], c->stream));
-      lmsb::launch_filter(fa, c->stream);
+      if (variant == kFilterFp64) lmsb::launch_filter(fa, c->stream);
+      else if (variant == kFilterMask) lmsb::launch_filter32m(fa, c->stream);
+      else lmsb::launch_filter32(fa, c->stream);
       CUDA_TRY(cudaEventRecord(c->ev_chunk[2 * ch + 1], c->stream));
       lmsb::ExactArgs xa = ea;
       xa.mode = lmsb::kSrcRanks;
@@ -314,7 +335,7 @@ int ctx_solve(lms_ctx* c, int64_t q, int64_t R0, int64_t R1, lms_candidate* out)
                           c->d_best, c->stream);
       CUDA_TRY(cudaGetLastError());
       st.launches += 4;
-      st.filtered_vertices += (fa.task_end - fa.task_begin) * lmsb::kFilterTaskVertices;
+      st.filtered_vertices += (fa.task_end - fa.task_begin) * task_vertices;
     }
     st.filtered_vertices = std::min(st.filtered_vertices, span);
   }

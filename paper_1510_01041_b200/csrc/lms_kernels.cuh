@@ -68,4 +68,26 @@ struct FilterArgs {
 
 void launch_filter(const FilterArgs& args, cudaStream_t stream);
 
+// FP32-FMA / FP16-compare / mma.sync-count variant (lms_filter32.cu).
+#ifndef LMSB_F32_TILES
+#define LMSB_F32_TILES 4
+#endif
+constexpr int kFilter32Tiles = LMSB_F32_TILES;             // 16-vertex MMA row tiles per warp
+constexpr int kFilter32TaskVertices = 16 * kFilter32Tiles; // vertices per warp task
+
+void launch_filter32(const FilterArgs& args, cudaStream_t stream);
+
+// Packed-FP16 compare / integer-mask counting variant (lms_filter32m.cu).
+#ifndef LMSB_F32M_V
+#define LMSB_F32M_V 4
+#endif
+#ifndef LMSB_F32M_MIN_BLOCKS
+#define LMSB_F32M_MIN_BLOCKS 3
+#endif
+constexpr int kFilter32mV = LMSB_F32M_V;                    // vertices per lane
+constexpr int kFilter32mMinBlocks = LMSB_F32M_MIN_BLOCKS;
+constexpr int kFilter32mTaskVertices = 32 * kFilter32mV;    // vertices per warp task
+
+void launch_filter32m(const FilterArgs& args, cudaStream_t stream);
+
 }  // namespace lmsb
