@@ -299,22 +299,25 @@ def run_ours(args):
         e2e_s = float(tt.item())
     e2e_value = max(1, args.steps) * n * total / e2e_s
 
-    # ---- roofline of the dominant kernel (the FP64 count filter)
-    dfma_rate = _native.probe_fp64_rate(local)
+    # ---- roofline of the dominant kernel (the count filter)
+    fma_rate = _native.probe_fp32_rate(local)  # FP32 FMA lanes / s, measured in-run
     achieved = 2.0 * evals_exec / (filt_ms / 1e3) / 1e12 if filt_ms > 0 else 0.0
-    peak = dfma_rate / 1e12  # non-FMA FP64 op rate: one DMUL or DADD (1 flop) per pipe slot
+    peak = 2.0 * fma_rate / 1e12
     roofline = {
-        "bound": "fp64",
-        "kernel": "filter_kernel",
+        "bound": "fp32",
+        "kernel": "filter32m_kernel (FFMA2 + FP16 window compares + integer-mask counts)",
         "achieved": achieved,
         "peak": peak,
         "unit": "TFLOP/s",
         "frac": achieved / peak if peak else None,
         "traffic": load_profile_traffic(),
-        "algorithmic": "2 FP64 flops (u*a_k - b_k) per EXECUTED vertex-line eval "
+        "algorithmic": "2 FP32 flops (the FMA u*A_k - B_k) per EXECUTED vertex-line eval "
                        "(early-exited lines not counted) / filter kernel event time",
-        "peak_source": "measured in-run: DFMA issue-rate probe (lms_probe_fp64_rate), non-FMA "
-                       "op peak = DFMA/s; MEASURED_PEAKS.json has no FP64 figure",
+        "peak_source": "measured in-run: FFMA2 chain probe (lms_probe_fp32_rate), 2 flops per FMA "
+                       "lane; MEASURED_PEAKS.json has no FP32 CUDA-core figure",
+        "note": "the filter issues 5 datapath ops per vertex and line pair (FFMA2, F2FP, HADD2, "
+                "2x HSET2), all sharing the 0.5 warp-instr/clk/SMSP rate measured for these "
+                "ops; frac is the FMA share of that datapath, see DESIGN.md",
         "filter_share_of_step": filt_ms / dev_ms if dev_ms else None,
         "executed_evals_per_step": evals_exec / args.steps,
         "reference_evals_per_step": n * total,

@@ -119,6 +119,9 @@ int lms_ctx_synchronize(lms_ctx* ctx);
  * all SMs busy, 8 independent chains per thread).  bench.py's roofline
  * denominator for the FP64-bound filter kernel. */
 int lms_probe_fp64_rate(int device, double* dfma_per_second);
+/* Measured FP32 FMA lane rate (FFMA2 packed chains, all SMs busy): the
+ * roofline denominator of the default FP32/FP16 count filter. */
+int lms_probe_fp32_rate(int device, double* fma_lanes_per_second);
 
 #ifdef __cplusplus
 }

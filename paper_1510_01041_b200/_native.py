@@ -99,6 +99,7 @@ SIGNATURES = {
                                                 ctypes.POINTER(ctypes.c_float)]),
     "lms_ctx_synchronize": (ctypes.c_int, [ctypes.c_void_p]),
     "lms_probe_fp64_rate": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_double)]),
+    "lms_probe_fp32_rate": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_double)]),
 }
 
 
@@ -203,6 +204,14 @@ def probe_fp64_rate(device: int = 0) -> float:
     lib = _lib_ready()
     r = ctypes.c_double(0.0)
     check(lib.lms_probe_fp64_rate(int(device), ctypes.byref(r)))
+    return r.value
+
+
+def probe_fp32_rate(device: int = 0) -> float:
+    """Measured FP32 FMA lanes per second (FFMA2 chains) on `device`."""
+    lib = _lib_ready()
+    r = ctypes.c_double(0.0)
+    check(lib.lms_probe_fp32_rate(int(device), ctypes.byref(r)))
     return r.value
 
 

@@ -117,6 +117,17 @@ struct lms_ctx {
   lms_candidate* h_best = nullptr;  // pinned
   lms_stats stats{};
   int filter_variant = 0;  // LMSB_FILTER=fp64|mma|mask (A/B switch; see kDefaultFilter)
+  bool line_order = true;  // far-first streaming order (LMSB_ORDER=0 disables)
+  // far-first order buffers (lms_order.cu)
+  float* d_keys = nullptr;
+  int64_t cap_keys = 0;
+  int* d_idx = nullptr;
+  int64_t cap_idx = 0;
+  double* d_pa = nullptr;
+  double* d_pb = nullptr;
+  int64_t cap_pa = 0, cap_pb = 0;
+  unsigned char* d_sort_tmp = nullptr;
+  int64_t cap_sort_tmp = 0;
   std::mutex mu;
 };
 
@@ -134,6 +145,8 @@ int ctx_init(lms_ctx* c, int device) {
   if (fv && std::strcmp(fv, "fp64") == 0) c->filter_variant = kFilterFp64;
   if (fv && std::strcmp(fv, "mma") == 0) c->filter_variant = kFilterMma;
   if (fv && std::strcmp(fv, "mask") == 0) c->filter_variant = kFilterMask;
+  const char* ov = getenv("LMSB_ORDER");
+  c->line_order = !(ov && std::strcmp(ov, "0") == 0);
   CUDA_TRY(cudaSetDevice(device));
   CUDA_TRY(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device));
   CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
@@ -167,6 +180,11 @@ void ctx_release(lms_ctx* c) {
   cudaFree(c->d_jj);
   cudaFree(c->d_uu);
   cudaFree(c->d_vv);
+  cudaFree(c->d_keys);
+  cudaFree(c->d_idx);
+  cudaFree(c->d_pa);
+  cudaFree(c->d_pb);
+  cudaFree(c->d_sort_tmp);
   if (c->h_best) cudaFreeHost(c->h_best);
   if (c->stream) cudaStreamDestroy(c->stream);
 }
@@ -257,6 +275,36 @@ int ctx_solve(lms_ctx* c, int64_t q, int64_t R0, int64_t R1, lms_candidate* out)
   CUDA_TRY(cudaEventRecord(c->ev_seed, c->stream));
 
   int64_t nchunks = 0;
+  const double* la = c->a;
+  const double* lb = c->b;
+  if (!exhaustive && c->line_order) {
+    // Far-first streaming order from the seed's best line (lms_order.cu).
+    const size_t tmp = lmsb::order_temp_bytes(n);
+    if ((rc = grow(&c->d_keys, &c->cap_keys, 2 * n))) return rc;
+    if ((rc = grow(&c->d_idx, &c->cap_idx, 2 * n))) return rc;
+    if ((rc = grow(&c->d_pa, &c->cap_pa, n))) return rc;
+    if ((rc = grow(&c->d_pb, &c->cap_pb, n))) return rc;
+    if ((rc = grow(&c->d_sort_tmp, &c->cap_sort_tmp, (int64_t)tmp))) return rc;
+    lmsb::OrderArgs oa{};
+    oa.a = c->a;
+    oa.b = c->b;
+    oa.n = n;
+    oa.best = c->d_best;
+    oa.keys_in = c->d_keys;
+    oa.keys_out = c->d_keys + n;
+    oa.idx_in = c->d_idx;
+    oa.idx_out = c->d_idx + n;
+    oa.temp = c->d_sort_tmp;
+    oa.temp_bytes = (size_t)c->cap_sort_tmp;
+    oa.pa = c->d_pa;
+    oa.pb = c->d_pb;
+    if (lmsb::launch_line_order(oa, c->stream) != 0)
+      return set_error(LMS_ERR_CUDA, "line order sort failed");
+    CUDA_TRY(cudaGetLastError());
+    st.launches += 3;
+    la = c->d_pa;
+    lb = c->d_pb;
+  }
   if (!exhaustive) {
     const int variant = c->filter_variant;
     const int64_t task_vertices = variant == kFilterFp64   ? lmsb::kFilterTaskVertices
@@ -302,6 +350,8 @@ int ctx_solve(lms_ctx* c, int64_t q, int64_t R0, int64_t R1, lms_candidate* out)
       lmsb::FilterArgs fa{};
       fa.a = c->a;
       fa.b = c->b;
+      fa.la = la;
+      fa.lb = lb;
       fa.n = n;
       fa.q = q;
       fa.task_prefix = c->d_task_prefix;
@@ -329,6 +379,7 @@ int ctx_solve(lms_ctx* c, int64_t q, int64_t R0, int64_t R1, lms_candidate* out)
       xa.d_count = c->d_counters + 2 + ch;
       xa.capacity = cap;
       xa.ranks = c->d_ranks;
+      xa.bound = c->d_best;
       xa.out = c->d_recs;
       lmsb::launch_exact(xa, exact_grid(c, -1), c->stream);
       lmsb::launch_reduce(c->d_recs, c->d_counters + 2 + ch, 0, cap, c->d_partials, c->sms,

@@ -43,6 +43,8 @@ struct SelectShared {
   int state[2];  // -1 inactive, 0 searching, 1 unique element pending, 2 done
   unsigned red_lt[kExactWarps];
   unsigned red_le[kExactWarps];
+  unsigned red_up[kExactWarps];
+  unsigned red_dn[kExactWarps];
 };
 
 __device__ __forceinline__ double snapped_cut(const double* __restrict__ a,
@@ -96,32 +98,52 @@ __device__ void pick_digit(SelectShared& sm, int t, int level) {
 
 // Exact anchored window at (i, j, u) with anchors snapped to v0.  Must be
 // called by all threads of the CTA; thread 0's return value is meaningful.
+// When `bound` is finite the vertex is evaluated only if one of its windows
+// can reach height <= bound; pass 0 counts, with the reference's own
+// arithmetic, the lines x >= v0 with fl(x - v0) <= bound (resp. x <= v0 with
+// fl(v0 - x) <= bound).  h_up <= bound iff that count reaches q, because
+// fl(x - v0) is monotone in x and vs[up] is the q-th smallest x >= v0
+// (backend.py:153,159); otherwise no select is needed and the vertex is
+// reported as not found (it cannot win against a record of height bound).
 __device__ lms_candidate exact_vertex(const double* __restrict__ a, const double* __restrict__ b,
                                       int64_t n, int64_t q, int64_t i, int64_t j, double u,
-                                      double v0, SelectShared& sm) {
+                                      double v0, double bound, SelectShared& sm) {
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
 
-  // Pass 0: rank counts of v0 in the snapped cut.
-  unsigned lt = 0, le = 0;
+  // Pass 0: rank counts of v0 in the snapped cut (+ window counts vs bound).
+  unsigned lt = 0, le = 0, wu = 0, wd = 0;
   for (int64_t k = tid; k < n; k += kExactThreads) {
     double x = snapped_cut(a, b, k, i, j, u, v0);
     lt += x < v0;
     le += x <= v0;
+    wu += x >= v0 && __dsub_rn(x, v0) <= bound;
+    wd += x <= v0 && __dsub_rn(v0, x) <= bound;
   }
   lt = __reduce_add_sync(0xffffffffu, lt);
   le = __reduce_add_sync(0xffffffffu, le);
+  wu = __reduce_add_sync(0xffffffffu, wu);
+  wd = __reduce_add_sync(0xffffffffu, wd);
   if (lane == 0) {
     sm.red_lt[warp] = lt;
     sm.red_le[warp] = le;
+    sm.red_up[warp] = wu;
+    sm.red_dn[warp] = wd;
   }
   __syncthreads();
-  int64_t c_lt = 0, c_le = 0;
+  int64_t c_lt = 0, c_le = 0, c_up = 0, c_dn = 0;
 #pragma unroll
   for (int w = 0; w < kExactWarps; ++w) {
     c_lt += sm.red_lt[w];
     c_le += sm.red_le[w];
+    c_up += sm.red_up[w];
+    c_dn += sm.red_dn[w];
+  }
+  if (isfinite(bound) && c_up < q && c_dn < q) {
+    __syncthreads();
+    lms_candidate none = cand_none();
+    return none;
   }
   const int64_t down = c_le - q;        // k_hi - (q - 1)
   const int64_t up = c_lt + q - 1;      // k_lo + (q - 1)
@@ -203,6 +225,11 @@ __global__ void __launch_bounds__(kExactThreads) exact_kernel(ExactArgs args) {
   if (args.mode == kSrcRanks) count = (int64_t)*args.d_count;
   if (count > args.capacity) count = args.capacity;
   const int64_t n = args.n;
+  double bound = INFINITY;
+  if (args.bound) {
+    const lms_candidate bc = *args.bound;
+    if (bc.found) bound = bc.height;
+  }
   for (int64_t s = blockIdx.x; s < count; s += gridDim.x) {
     int64_t i, j;
     double u, v0;
@@ -229,7 +256,7 @@ __global__ void __launch_bounds__(kExactThreads) exact_kernel(ExactArgs args) {
       v0 = cut_value(u, ai, args.b[i]);
     }
     lms_candidate c = cand_none();
-    if (valid) c = exact_vertex(args.a, args.b, n, args.q, i, j, u, v0, sm);
+    if (valid) c = exact_vertex(args.a, args.b, n, args.q, i, j, u, v0, bound, sm);
     if (threadIdx.x == 0) args.out[s] = c;
   }
 }

@@ -111,8 +111,8 @@ __global__ void __launch_bounds__(kFilterWarpsPerBlock * 32)
 
   ShiftedLine* my = slab[wib];
   int64_t k0 = 0;
-  double ak = lane < n ? __ldg(args.a + lane) : 0.0;
-  double bk = lane < n ? __ldg(args.b + lane) : 0.0;
+  double ak = lane < n ? __ldg(args.la + lane) : 0.0;
+  double bk = lane < n ? __ldg(args.lb + lane) : 0.0;
   int64_t evals = 0;
   for (; k0 < n; k0 += 32) {
     // Stage this chunk's shifted lines; padding lines are NaN (never count).
@@ -131,8 +131,8 @@ __global__ void __launch_bounds__(kFilterWarpsPerBlock * 32)
     // Prefetch the next chunk while this one is consumed.
     const int64_t kn = k0 + 32 + lane;
     if (kn < n) {
-      ak = __ldg(args.a + kn);
-      bk = __ldg(args.b + kn);
+      ak = __ldg(args.la + kn);
+      bk = __ldg(args.lb + kn);
     }
     __syncwarp();
     my[lane] = s;

@@ -203,11 +203,11 @@ __global__ void __launch_bounds__(kFilterWarpsPerBlock * 32, kFilter32MinBlocks)
   double2 ak2 = make_double2(0.0, 0.0), bk2 = make_double2(0.0, 0.0);
   auto load_pair = [&](int64_t k) {
     if (k + 1 < n) {
-      ak2 = __ldg(reinterpret_cast<const double2*>(args.a + k));
-      bk2 = __ldg(reinterpret_cast<const double2*>(args.b + k));
+      ak2 = __ldg(reinterpret_cast<const double2*>(args.la + k));
+      bk2 = __ldg(reinterpret_cast<const double2*>(args.lb + k));
     } else if (k < n) {
-      ak2 = make_double2(__ldg(args.a + k), 0.0);
-      bk2 = make_double2(__ldg(args.b + k), 0.0);
+      ak2 = make_double2(__ldg(args.la + k), 0.0);
+      bk2 = make_double2(__ldg(args.lb + k), 0.0);
     }
   };
   load_pair(2 * lane);

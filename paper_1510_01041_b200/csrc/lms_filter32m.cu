@@ -37,6 +37,25 @@ struct __align__(16) LinePair {
   float2 Bn;  // (-Bu_k, -Bu_k+1)
 };
 
+// Accumulation of a half2 mask word.  IMAD (mad.lo c, m, 1, c) issues on the
+// FMA pipe, IADD3 on the ALU pipe that F2FP and HSET2 already load; the
+// LMSB_F32M_ACC policy picks the split (0: both IADD3, 1: up IMAD / down
+// IADD3, 2: both IMAD).
+#ifndef LMSB_F32M_ACC
+#define LMSB_F32M_ACC 1
+#endif
+__device__ __forceinline__ void acc_imad(uint32_t& c, uint32_t m) {
+  asm volatile("mad.lo.u32 %0, %1, 1, %0;" : "+r"(c) : "r"(m));
+}
+__device__ __forceinline__ void acc_up(uint32_t& c, uint32_t m) {
+  if (LMSB_F32M_ACC >= 1) acc_imad(c, m);
+  else c += m;
+}
+__device__ __forceinline__ void acc_dn(uint32_t& c, uint32_t m) {
+  if (LMSB_F32M_ACC >= 2) acc_imad(c, m);
+  else c += m;
+}
+
 __device__ __forceinline__ uint32_t mask_total(uint32_t sum) {
   const uint32_t ue = (0x10000u - (sum & 0xFFFFu)) & 0xFFFFu;
   const uint32_t uo = (ue - ((sum + ue) >> 16)) & 0xFFFFu;
@@ -122,11 +141,11 @@ __global__ void __launch_bounds__(kFilterWarpsPerBlock * 32, kFilter32mMinBlocks
   double2 ak2 = make_double2(0.0, 0.0), bk2 = make_double2(0.0, 0.0);
   auto load_pair = [&](int64_t k) {
     if (k + 1 < n) {
-      ak2 = __ldg(reinterpret_cast<const double2*>(args.a + k));
-      bk2 = __ldg(reinterpret_cast<const double2*>(args.b + k));
+      ak2 = __ldg(reinterpret_cast<const double2*>(args.la + k));
+      bk2 = __ldg(reinterpret_cast<const double2*>(args.lb + k));
     } else if (k < n) {
-      ak2 = make_double2(__ldg(args.a + k), 0.0);
-      bk2 = make_double2(__ldg(args.b + k), 0.0);
+      ak2 = make_double2(__ldg(args.la + k), 0.0);
+      bk2 = make_double2(__ldg(args.lb + k), 0.0);
     }
   };
   load_pair(2 * lane);
@@ -160,8 +179,8 @@ __global__ void __launch_bounds__(kFilterWarpsPerBlock * 32, kFilter32mMinBlocks
         const float2 t = __ffma2_rn(L.A, make_float2(u32[s], u32[s]), L.Bn);
         const __half2 hu = __floats2half2_rn(t.x, t.y);
         const __half2 hd = __hadd2(hu, hn2);
-        cu[s] += __hle2_mask(__habs2(hu), w2[s]);
-        cd[s] += __hle2_mask(__habs2(hd), w2[s]);
+        acc_up(cu[s], __hle2_mask(__habs2(hu), w2[s]));
+        acc_dn(cd[s], __hle2_mask(__habs2(hd), w2[s]));
       }
     }
     evals += (n - k0) < 64 ? (n - k0) : 64;

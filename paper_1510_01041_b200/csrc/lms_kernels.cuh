@@ -31,6 +31,7 @@ struct ExactArgs {
   const int64_t* jj;
   const double* uu;
   const double* vv;
+  const lms_candidate* bound;  // optional: skip vertices that cannot beat bound->height
   lms_candidate* out;
 };
 
@@ -46,8 +47,10 @@ constexpr int kFilterTaskVertices = 32 * kFilterV;   // vertices per warp task
 constexpr int kFilterWarpsPerBlock = 8;
 
 struct FilterArgs {
-  const double* a;
+  const double* a;   // lines in input order (anchors i, j)
   const double* b;
+  const double* la;  // lines in streaming order (lms_order.cu); may alias a/b
+  const double* lb;
   int64_t n;
   int64_t q;
   const int64_t* task_prefix;  // task_prefix[r] = first task of row row0 + r
@@ -89,5 +92,23 @@ constexpr int kFilter32mMinBlocks = LMSB_F32M_MIN_BLOCKS;
 constexpr int kFilter32mTaskVertices = 32 * kFilter32mV;    // vertices per warp task
 
 void launch_filter32m(const FilterArgs& args, cudaStream_t stream);
+
+// Far-first line streaming order (lms_order.cu).
+struct OrderArgs {
+  const double* a;
+  const double* b;
+  int64_t n;
+  const lms_candidate* best;
+  float* keys_in;
+  float* keys_out;
+  int* idx_in;
+  int* idx_out;
+  void* temp;
+  size_t temp_bytes;
+  double* pa;
+  double* pb;
+};
+size_t order_temp_bytes(int64_t n);
+int launch_line_order(const OrderArgs& o, cudaStream_t stream);
 
 }  // namespace lmsb
