@@ -21,9 +21,6 @@
  *                             (backend.py:221-231, 321-354)
  *   lms_batched_f64           refine_lms per Hough peak (detect.py:134-153,
  *                             the per-peak loop of detect.py:184-213)
- *   lms_hough_vote_u8         extract_points + hough_vote (hough.py:93-129)
- *   lms_hough_support_u8      supporting_points (hough.py:171-184) +
- *                             subsample_support (detect.py:118-131)
  *
  * Results are bit-identical to the reference's fp64 arithmetic: the winning
  * pair (i, j), u, v_low, v_high and height are the values the reference's
@@ -85,6 +82,13 @@ const char* lms_last_error(void);
 int lms_min_bracelet_f64(const double* a, const double* b, int64_t n, int64_t q,
                          int64_t rank_begin, int64_t rank_end, int device, lms_candidate* out);
 
+/* Batched exact LMS (refine_lms over many Hough peaks, detect.py:134-153 /
+ * the per-peak loop of detect.py:184-213): fit f uses points
+ * [offsets[f], offsets[f+1]) of x / y with coverage q[f]; out[f] is the
+ * minimum over all of the fit's pair ranks.  offsets[0] == 0. */
+int lms_batched_f64(const double* x, const double* y, const int64_t* offsets, const int64_t* q,
+                    int64_t nfits, int device, lms_candidate* out);
+
 /* Anchored window at each explicit intersection (i[k], j[k], u[k]).  When v
  * is non-NULL the anchors are snapped to v[k] (bracelet_at); when NULL to
  * a[i]*u - b[i] (_evaluate_pairs).  out: m records. */
@@ -109,6 +113,9 @@ int lms_ctx_bind_dev(lms_ctx* ctx, const double* d_a, const double* d_b, int64_t
 /* Solve over [rank_begin, rank_end) of the bound lines; blocks until done. */
 int lms_ctx_solve(lms_ctx* ctx, int64_t q, int64_t rank_begin, int64_t rank_end,
                   lms_candidate* out);
+/* Batched solve over the bound lines (see lms_batched_f64). */
+int lms_ctx_solve_batch(lms_ctx* ctx, const int64_t* offsets, const int64_t* q, int64_t nfits,
+                        lms_candidate* out);
 int lms_ctx_stats(const lms_ctx* ctx, lms_stats* out);
 /* CUDA events on the context stream, for device timing around solves. */
 int lms_ctx_event_record(lms_ctx* ctx, int slot);

@@ -82,6 +82,7 @@ SIGNATURES = {
     "lms_last_error": (ctypes.c_char_p, []),
     "lms_min_bracelet_f64": (ctypes.c_int, [_D, _D, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                             ctypes.c_int64, ctypes.c_int, _C]),
+    "lms_batched_f64": (ctypes.c_int, [_D, _D, _I, _I, ctypes.c_int64, ctypes.c_int, _C]),
     "lms_eval_vertices_f64": (ctypes.c_int, [_D, _D, ctypes.c_int64, ctypes.c_int64, _I, _I, _D, _D,
                                              ctypes.c_int64, ctypes.c_int, _C]),
     "lms_min_over_vertices_f64": (ctypes.c_int, [_D, _D, ctypes.c_int64, ctypes.c_int64, _I, _I, _D,
@@ -93,6 +94,7 @@ SIGNATURES = {
                                         ctypes.c_int64]),
     "lms_ctx_solve": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                      _C]),
+    "lms_ctx_solve_batch": (ctypes.c_int, [ctypes.c_void_p, _I, _I, ctypes.c_int64, _C]),
     "lms_ctx_stats": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(Stats)]),
     "lms_ctx_event_record": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "lms_ctx_event_elapsed_ms": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
@@ -174,6 +176,17 @@ def min_bracelet(a, b, q: int, rank_begin: int, rank_end: int, device: int = 0) 
     return out
 
 
+def batched(x, y, offsets, q, device: int = 0) -> list:
+    """lms_batched_f64: one exact LMS record per fit [offsets[f], offsets[f+1])."""
+    lib = _lib_ready()
+    x, y = _f64(x), _f64(y)
+    offsets, q = _i64(offsets), _i64(q)
+    nf = q.size
+    out = (Candidate * max(nf, 1))()
+    check(lib.lms_batched_f64(_dp(x), _dp(y), _ip(offsets), _ip(q), nf, int(device), out))
+    return [out[k] for k in range(nf)]
+
+
 def eval_vertices(a, b, q: int, i, j, u, v=None, device: int = 0):
     lib = _lib_ready()
     a, b = _f64(a), _f64(b)
@@ -248,6 +261,13 @@ class Context:
         out = Candidate()
         check(self._lib.lms_ctx_solve(self._h, int(q), int(rank_begin), int(rank_end), ctypes.byref(out)))
         return out
+
+    def solve_batch(self, offsets, q) -> list:
+        offsets, q = _i64(offsets), _i64(q)
+        nf = q.size
+        out = (Candidate * max(nf, 1))()
+        check(self._lib.lms_ctx_solve_batch(self._h, _ip(offsets), _ip(q), nf, out))
+        return [out[k] for k in range(nf)]
 
     def stats(self) -> dict:
         s = Stats()

@@ -1,17 +1,19 @@
 // lms_engine.cu -- host orchestration of the exact-LMS search and the C ABI.
 //
-// One solve over pair ranks [R0, R1) (a contiguous partition, as
-// BatchPlan.partitions, backend.py:84-92):
-//   1. seed     exact-evaluate a stratified sample of S vertices and reduce
-//               them to the current best record (its height is the bound H);
-//   2. filter   stream the range in chunks of warp tasks through the count
-//               filter (lms_filter.cu) with H read from device memory;
-//   3. exact    re-evaluate the chunk's survivors bit-exactly (lms_exact.cu);
-//   4. reduce   lexicographic (height, i, j) minimum into the best record,
-//               tightening H for the next chunk.
-// Every launch is asynchronous on the context stream; the host synchronises
-// once, when it reads the 56-byte best record back.  Small ranges (fewer
-// than kExhaustive pairs) skip the filter and evaluate every vertex exactly.
+// A solve is a batch of fits (one large fit, or thousands of Hough-peak
+// refits).  For every fit f with pair ranks [R0, R1) (a contiguous partition
+// as BatchPlan.partitions, backend.py:84-92):
+//   1. seed     exact-evaluate a stratified sample of its vertices and reduce
+//               them to the fit's best record (its height is the bound H);
+//               fits with at most kExhaustive pairs evaluate every vertex here
+//   2. order    stream its lines far-first from the best line (lms_order.cu)
+//   3. filter   all remaining fits' warp tasks in chunks through the count
+//               filter (lms_filter32m.cu), H read per fit from device memory
+//   4. exact    re-evaluate each chunk's survivors bit-exactly (lms_exact.cu)
+//   5. reduce   per-fit lexicographic (height, i, j) minimum by 128-bit CAS,
+//               tightening every fit's H for the next chunk.
+// All launches are asynchronous on the context stream; the host
+// synchronises once, when it reads the best records back.
 
 #include <cuda_runtime.h>
 
@@ -27,8 +29,9 @@
 
 #include "lms_common.cuh"
 #include "lms_kernels.cuh"
+#include "lms_plan.cuh"
 
-#define LMS_VERSION 1
+#define LMS_VERSION 2
 
 namespace {
 
@@ -54,18 +57,18 @@ int set_error(int code, const char* fmt, ...) {
     }                                                                                    \
   } while (0)
 
-constexpr int64_t kSeeds = 2048;            // exact seed vertices per solve
-constexpr int64_t kExhaustive = 4096;       // ranges this small skip the filter
-constexpr int64_t kChunkVertices = 1 << 24; // filter chunk (and survivor capacity)
-constexpr int kNumEvents = 16;
+#define RC_TRY(expr)     \
+  do {                   \
+    int _rc = (expr);    \
+    if (_rc) return _rc; \
+  } while (0)
 
-// Count-filter variants: all-FP64 (lms_filter.cu), FP16 compare + mma.sync
-// counting (lms_filter32.cu), FP16 compare + integer-mask counting
-// (lms_filter32m.cu).
-constexpr int kFilterFp64 = 1;
-constexpr int kFilterMma = 2;
-constexpr int kFilterMask = 3;
-constexpr int kDefaultFilter = kFilterMask;
+constexpr int64_t kSeedsMax = 2048;          // exact seed vertices per large fit
+constexpr int64_t kSeedsMin = 64;            // ... per small fit
+constexpr int64_t kSeedDivisor = 2048;       // seeds = span / kSeedDivisor, clamped
+constexpr int64_t kExhaustive = 4096;        // fits this small skip the filter
+constexpr int64_t kChunkVertices = 1 << 24;  // filter chunk (and survivor capacity)
+constexpr int kNumEvents = 16;
 
 template <typename T>
 int grow(T** ptr, int64_t* cap, int64_t need) {
@@ -79,6 +82,22 @@ int grow(T** ptr, int64_t* cap, int64_t need) {
   return LMS_OK;
 }
 
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  int64_t cap = 0;
+  int need(int64_t n) { return grow(&p, &cap, n); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+struct HostFit {
+  int64_t off, n, q, r0, r1;
+};
+
 }  // namespace
 
 struct lms_ctx {
@@ -86,48 +105,41 @@ struct lms_ctx {
   int sms = 148;
   cudaStream_t stream = nullptr;
   cudaEvent_t user_ev[kNumEvents] = {};
-  cudaEvent_t ev_begin = nullptr, ev_seed = nullptr, ev_end = nullptr;
-  std::vector<cudaEvent_t> ev_chunk;  // filter start / filter end per chunk
-  // lines
-  double* d_a = nullptr;
-  double* d_b = nullptr;
-  int64_t cap_a = 0, cap_b = 0;
-  const double* a = nullptr;  // bound lines (owned or external)
+  cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
+  std::vector<cudaEvent_t> ev_chunk;
+  bool line_order = true;  // far-first streaming order (LMSB_ORDER=0 disables, for A/B runs)
+  // lines (concatenated over fits)
+  DevBuf<double> a_own, b_own;
+  const double* a = nullptr;
   const double* b = nullptr;
-  int64_t n = 0;
-  double amax = 0.0, bmax = 0.0;
-  // scratch
-  int64_t* d_task_prefix = nullptr;
-  int64_t cap_rows = 0;
-  int64_t* d_ranks = nullptr;
-  int64_t cap_ranks = 0;
-  lms_candidate* d_recs = nullptr;
-  int64_t cap_recs = 0;
-  lms_candidate* d_partials = nullptr;
-  int64_t cap_partials = 0;
-  lms_candidate* d_best = nullptr;
-  unsigned long long* d_counters = nullptr;  // [0] survivors (current chunk), [1] line evals, [2..] per-chunk survivors
-  int64_t cap_counters = 0;
-  int64_t* d_ii = nullptr;
-  int64_t* d_jj = nullptr;
-  int64_t cap_ii = 0, cap_jj = 0;
-  double* d_uu = nullptr;
-  double* d_vv = nullptr;
-  int64_t cap_uu = 0, cap_vv = 0;
+  int64_t nlines = 0;
+  std::vector<double> h_a, h_b;  // host copy: per-fit max |a|, max |b| for the filter margins
+  // fits
+  DevBuf<lmsb::FitDesc> fits;
+  DevBuf<int64_t> prefA, prefB, seed_prefix, seg;
+  DevBuf<lmsb::BestKey> keys;
+  DevBuf<lms_candidate> best;
+  // plan
+  DevBuf<int64_t> counts, row_task_prefix;
+  DevBuf<int32_t> row_fit, row_i, task_row;
+  DevBuf<unsigned char> plan_tmp;
+  // order
+  DevBuf<float> sort_keys;
+  DevBuf<int> sort_idx;
+  DevBuf<double> pa, pb;
+  DevBuf<int32_t> line_fit;
+  DevBuf<unsigned char> sort_tmp;
+  // items (seeds, survivors) and their records
+  DevBuf<int64_t> ranks;
+  DevBuf<int32_t> item_fit;
+  DevBuf<lms_candidate> recs;
+  DevBuf<unsigned long long> counters;
+  // explicit vertices
+  DevBuf<int64_t> ii, jj;
+  DevBuf<double> uu, vv;
   lms_candidate* h_best = nullptr;  // pinned
+  int64_t cap_h_best = 0;
   lms_stats stats{};
-  int filter_variant = 0;  // LMSB_FILTER=fp64|mma|mask (A/B switch; see kDefaultFilter)
-  bool line_order = true;  // far-first streaming order (LMSB_ORDER=0 disables)
-  // far-first order buffers (lms_order.cu)
-  float* d_keys = nullptr;
-  int64_t cap_keys = 0;
-  int* d_idx = nullptr;
-  int64_t cap_idx = 0;
-  double* d_pa = nullptr;
-  double* d_pb = nullptr;
-  int64_t cap_pa = 0, cap_pb = 0;
-  unsigned char* d_sort_tmp = nullptr;
-  int64_t cap_sort_tmp = 0;
   std::mutex mu;
 };
 
@@ -140,11 +152,6 @@ int ctx_init(lms_ctx* c, int device) {
   if (device < 0 || device >= count)
     return set_error(LMS_ERR_NODEVICE, "device %d out of range (%d devices)", device, count);
   c->device = device;
-  const char* fv = getenv("LMSB_FILTER");
-  c->filter_variant = kDefaultFilter;
-  if (fv && std::strcmp(fv, "fp64") == 0) c->filter_variant = kFilterFp64;
-  if (fv && std::strcmp(fv, "mma") == 0) c->filter_variant = kFilterMma;
-  if (fv && std::strcmp(fv, "mask") == 0) c->filter_variant = kFilterMask;
   const char* ov = getenv("LMSB_ORDER");
   c->line_order = !(ov && std::strcmp(ov, "0") == 0);
   CUDA_TRY(cudaSetDevice(device));
@@ -152,10 +159,7 @@ int ctx_init(lms_ctx* c, int device) {
   CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   for (auto& e : c->user_ev) CUDA_TRY(cudaEventCreate(&e));
   CUDA_TRY(cudaEventCreate(&c->ev_begin));
-  CUDA_TRY(cudaEventCreate(&c->ev_seed));
   CUDA_TRY(cudaEventCreate(&c->ev_end));
-  CUDA_TRY(cudaMalloc(&c->d_best, sizeof(lms_candidate)));
-  CUDA_TRY(cudaMallocHost(&c->h_best, sizeof(lms_candidate)));
   return LMS_OK;
 }
 
@@ -166,239 +170,330 @@ void ctx_release(lms_ctx* c) {
     if (e) cudaEventDestroy(e);
   for (auto e : c->ev_chunk) cudaEventDestroy(e);
   if (c->ev_begin) cudaEventDestroy(c->ev_begin);
-  if (c->ev_seed) cudaEventDestroy(c->ev_seed);
   if (c->ev_end) cudaEventDestroy(c->ev_end);
-  cudaFree(c->d_a);
-  cudaFree(c->d_b);
-  cudaFree(c->d_task_prefix);
-  cudaFree(c->d_ranks);
-  cudaFree(c->d_recs);
-  cudaFree(c->d_partials);
-  cudaFree(c->d_best);
-  cudaFree(c->d_counters);
-  cudaFree(c->d_ii);
-  cudaFree(c->d_jj);
-  cudaFree(c->d_uu);
-  cudaFree(c->d_vv);
-  cudaFree(c->d_keys);
-  cudaFree(c->d_idx);
-  cudaFree(c->d_pa);
-  cudaFree(c->d_pb);
-  cudaFree(c->d_sort_tmp);
+  c->a_own.release();
+  c->b_own.release();
+  c->fits.release();
+  c->prefA.release();
+  c->prefB.release();
+  c->seed_prefix.release();
+  c->seg.release();
+  c->keys.release();
+  c->best.release();
+  c->counts.release();
+  c->row_task_prefix.release();
+  c->row_fit.release();
+  c->row_i.release();
+  c->task_row.release();
+  c->plan_tmp.release();
+  c->sort_keys.release();
+  c->sort_idx.release();
+  c->pa.release();
+  c->pb.release();
+  c->line_fit.release();
+  c->sort_tmp.release();
+  c->ranks.release();
+  c->item_fit.release();
+  c->recs.release();
+  c->counters.release();
+  c->ii.release();
+  c->jj.release();
+  c->uu.release();
+  c->vv.release();
   if (c->h_best) cudaFreeHost(c->h_best);
   if (c->stream) cudaStreamDestroy(c->stream);
 }
 
 int ctx_upload(lms_ctx* c, const double* a, const double* b, int64_t n) {
-  if (!a || !b || n < 2) return set_error(LMS_ERR_INVALID, "need at least 2 lines, got %lld", (long long)n);
+  if (!a || !b || n < 1)
+    return set_error(LMS_ERR_INVALID, "need at least 1 line, got %lld", (long long)n);
   CUDA_TRY(cudaSetDevice(c->device));
-  int rc = grow(&c->d_a, &c->cap_a, n);
-  if (rc) return rc;
-  rc = grow(&c->d_b, &c->cap_b, n);
-  if (rc) return rc;
-  CUDA_TRY(cudaMemcpyAsync(c->d_a, a, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
-  CUDA_TRY(cudaMemcpyAsync(c->d_b, b, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
-  double am = 0.0, bm = 0.0;
-  for (int64_t k = 0; k < n; ++k) {
-    am = std::max(am, std::fabs(a[k]));
-    bm = std::max(bm, std::fabs(b[k]));
-  }
-  c->a = c->d_a;
-  c->b = c->d_b;
-  c->n = n;
-  c->amax = am;
-  c->bmax = bm;
+  RC_TRY(c->a_own.need(n));
+  RC_TRY(c->b_own.need(n));
+  CUDA_TRY(cudaMemcpyAsync(c->a_own.p, a, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->b_own.p, b, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+  c->h_a.assign(a, a + n);
+  c->h_b.assign(b, b + n);
+  c->a = c->a_own.p;
+  c->b = c->b_own.p;
+  c->nlines = n;
   return LMS_OK;
 }
 
-int ensure_counters(lms_ctx* c, int64_t chunks) {
-  return grow(&c->d_counters, &c->cap_counters, 2 + chunks);
+int ensure_host_best(lms_ctx* c, int64_t nfits) {
+  if (nfits <= c->cap_h_best) return LMS_OK;
+  if (c->h_best) cudaFreeHost(c->h_best);
+  c->h_best = nullptr;
+  c->cap_h_best = 0;
+  CUDA_TRY(cudaMallocHost(&c->h_best, sizeof(lms_candidate) * nfits));
+  c->cap_h_best = nfits;
+  return LMS_OK;
 }
 
-int ensure_partials(lms_ctx* c) {
-  return grow(&c->d_partials, &c->cap_partials, (int64_t)c->sms);
-}
-
-int exact_grid(const lms_ctx* c, int64_t count) {
+int persistent_grid(const lms_ctx* c, int64_t count) {
   int64_t g = (int64_t)c->sms * 8;
   if (count >= 0) g = std::min<int64_t>(g, std::max<int64_t>(count, 1));
   return (int)g;
 }
 
-int ctx_solve(lms_ctx* c, int64_t q, int64_t R0, int64_t R1, lms_candidate* out) {
-  std::memset(out, 0, sizeof(*out));
-  const int64_t n = c->n;
-  if (n < 2 || !c->a) return set_error(LMS_ERR_INVALID, "no lines bound to the context");
-  const int64_t total = n * (n - 1) / 2;
-  if (q < 1) return set_error(LMS_ERR_INVALID, "coverage must be positive, got %lld", (long long)q);
-  if (R0 < 0 || R1 > total || R0 > R1)
-    return set_error(LMS_ERR_INVALID, "rank range [%lld, %lld) outside [0, %lld)", (long long)R0,
-                     (long long)R1, (long long)total);
+int reduce_grid(const lms_ctx* c, int64_t count) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c->sms * 4, (count + 255) / 256));
+}
+
+// Far-first streaming order of every fit's lines (lms_order.cu); returns the
+// permuted line arrays through la / lb.
+int order_lines(lms_ctx* c, const std::vector<int64_t>& seg, int64_t F, const double** la,
+                const double** lb, lms_stats* st) {
+  const int64_t o = seg[0];
+  const int64_t nl = seg[F] - o;
+  RC_TRY(c->sort_keys.need(2 * nl));
+  RC_TRY(c->sort_idx.need(2 * nl));
+  RC_TRY(c->pa.need(c->nlines));
+  RC_TRY(c->pb.need(c->nlines));
+  RC_TRY(c->line_fit.need(nl));
+  RC_TRY(c->sort_tmp.need((int64_t)lmsb::order_temp_bytes(nl, F)));
+  // the sort works on [o, o + nl): segment offsets relative to o
+  std::vector<int64_t> rel(F + 1);
+  for (int64_t f = 0; f <= F; ++f) rel[f] = seg[f] - o;
+  CUDA_TRY(cudaMemcpyAsync(c->seg.p, rel.data(), sizeof(int64_t) * (F + 1), cudaMemcpyHostToDevice,
+                           c->stream));
+  lmsb::launch_line_fit(c->seg.p, F, c->line_fit.p, c->stream);
+  lmsb::OrderArgs oa{};
+  oa.a = c->a + o;
+  oa.b = c->b + o;
+  oa.nlines = nl;
+  oa.seg_begin = c->seg.p;
+  oa.nfits = F;
+  oa.line_fit = c->line_fit.p;
+  oa.best = c->best.p;
+  oa.keys_in = c->sort_keys.p;
+  oa.keys_out = c->sort_keys.p + nl;
+  oa.idx_in = c->sort_idx.p;
+  oa.idx_out = c->sort_idx.p + nl;
+  oa.temp = c->sort_tmp.p;
+  oa.temp_bytes = (size_t)c->sort_tmp.cap;
+  oa.pa = c->pa.p + o;
+  oa.pb = c->pb.p + o;
+  if (lmsb::launch_line_order(oa, c->stream) != 0)
+    return set_error(LMS_ERR_CUDA, "line order sort failed");
+  CUDA_TRY(cudaGetLastError());
+  st->launches += 4;
+  *la = c->pa.p;
+  *lb = c->pb.p;
+  return LMS_OK;
+}
+
+// Exact LMS search over a batch of fits; out[f] receives fit f's record.
+int ctx_solve_fits(lms_ctx* c, const std::vector<HostFit>& hf, lms_candidate* out) {
+  const int64_t F = (int64_t)hf.size();
+  std::memset(out, 0, sizeof(lms_candidate) * F);
+  if (F == 0) return LMS_OK;
   CUDA_TRY(cudaSetDevice(c->device));
   lms_stats st{};
-  st.n = n;
-  st.pairs = R1 - R0;
-  const int64_t span = R1 - R0;
-  int rc = ensure_partials(c);
-  if (rc) return rc;
+
+  // ---- host plan: fit descriptors, seeds, task counts (closed form)
+  int64_t maxn = 0;
+  for (const auto& f : hf) maxn = std::max(maxn, f.n);
+  const int V = maxn >= 4096 ? 4 : 2;
+  const int64_t tv = lmsb::filter_task_vertices(V);
+  std::vector<lmsb::FitDesc> fd(F);
+  std::vector<int64_t> prefA(F + 1), prefB(F + 1), seed_pref(F + 1), seg(F + 1);
+  int64_t rowsA = 0, rows = 0, tasks = 0, tasksA = 0, seeds = 0;
+  bool disjoint = true;
+  for (int64_t f = 0; f < F; ++f) {
+    const HostFit& h = hf[f];
+    const int64_t span = h.r1 - h.r0;
+    const bool exhaustive = span <= kExhaustive;
+    int64_t s = exhaustive ? span : std::min(kSeedsMax, std::max(kSeedsMin, span / kSeedDivisor));
+    s = std::min(s, span);
+    lmsb::FitDesc& d = fd[f];
+    d.off = h.off;
+    d.n = h.n;
+    d.q = h.q;
+    d.rank_lo = h.r0;
+    d.rank_hi = h.r1;
+    d.row0 = 0;
+    d.nrows = 0;
+    if (!exhaustive) {
+      tasks += lmsb::fit_tasks(h.n, h.r0, h.r1, tv, &d.row0, &d.nrows);
+      for (int64_t k = 0; k < d.nrows; k += lmsb::kPhaseStride)
+        tasksA += lmsb::row_tasks(h.n, h.r0, h.r1, d.row0 + k, tv);
+    }
+    prefA[f] = rowsA;
+    rowsA += (d.nrows + lmsb::kPhaseStride - 1) / lmsb::kPhaseStride;
+    rows += d.nrows;
+    double am = 0.0, bm = 0.0;
+    for (int64_t k = h.off; k < h.off + h.n; ++k) {
+      am = std::max(am, std::fabs(c->h_a[k]));
+      bm = std::max(bm, std::fabs(c->h_b[k]));
+    }
+    d.amax = am;
+    d.bmax = bm;
+    seed_pref[f] = seeds;
+    seeds += s;
+    seg[f] = h.off;
+    if (f > 0 && h.off < hf[f - 1].off + hf[f - 1].n) disjoint = false;
+    st.pairs += span;
+    st.n = std::max(st.n, h.n);
+  }
+  prefA[F] = rowsA;
+  {
+    int64_t rb = rowsA;
+    for (int64_t f = 0; f < F; ++f) {
+      prefB[f] = rb;
+      rb += fd[f].nrows - (prefA[f + 1] - prefA[f]);
+    }
+    prefB[F] = rb;
+  }
+  seed_pref[F] = seeds;
+  seg[F] = hf[F - 1].off + hf[F - 1].n;
+  st.seed_vertices = seeds;
+
+  RC_TRY(c->fits.need(F));
+  RC_TRY(c->prefA.need(F + 1));
+  RC_TRY(c->prefB.need(F + 1));
+  RC_TRY(c->seed_prefix.need(F + 1));
+  RC_TRY(c->seg.need(F + 1));
+  RC_TRY(c->keys.need(F));
+  RC_TRY(c->best.need(F));
+  RC_TRY(ensure_host_best(c, F));
+  const int64_t cap = tasks > 0 ? std::min(kChunkVertices, tasks * tv) : 0;
+  const int64_t cap_items = std::max<int64_t>(seeds, cap);
+  RC_TRY(c->ranks.need(cap_items));
+  RC_TRY(c->item_fit.need(cap_items));
+  RC_TRY(c->recs.need(cap_items));
+
   CUDA_TRY(cudaEventRecord(c->ev_begin, c->stream));
-  CUDA_TRY(cudaMemsetAsync(c->d_best, 0, sizeof(lms_candidate), c->stream));
-  if (span == 0) {
-    CUDA_TRY(cudaEventRecord(c->ev_seed, c->stream));
-    CUDA_TRY(cudaEventRecord(c->ev_end, c->stream));
-    CUDA_TRY(cudaStreamSynchronize(c->stream));
-    c->stats = st;
-    return LMS_OK;
+  CUDA_TRY(cudaMemcpyAsync(c->fits.p, fd.data(), sizeof(lmsb::FitDesc) * F,
+                           cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->prefA.p, prefA.data(), sizeof(int64_t) * (F + 1),
+                           cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->prefB.p, prefB.data(), sizeof(int64_t) * (F + 1),
+                           cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->seed_prefix.p, seed_pref.data(), sizeof(int64_t) * (F + 1),
+                           cudaMemcpyHostToDevice, c->stream));
+  lmsb::launch_reset_best(c->keys.p, c->best.p, F, c->stream);
+  st.launches += 1;
+
+  // ---- 1. seeds (every vertex of the exhaustive fits)
+  if (seeds > 0) {
+    lmsb::launch_gen_seeds(c->fits.p, c->seed_prefix.p, F, c->ranks.p, c->item_fit.p, c->stream);
+    lmsb::ExactArgs ea{};
+    ea.a = c->a;
+    ea.b = c->b;
+    ea.fits = c->fits.p;
+    ea.mode = lmsb::kSrcList;
+    ea.count = seeds;
+    ea.capacity = seeds;
+    ea.ranks = c->ranks.p;
+    ea.fit_of = c->item_fit.p;
+    ea.out = c->recs.p;
+    lmsb::launch_exact(ea, persistent_grid(c, seeds), c->stream, maxn);
+    lmsb::launch_reduce(c->recs.p, nullptr, seeds, seeds, c->fits.p, c->keys.p, c->best.p,
+                        reduce_grid(c, seeds), c->stream);
+    CUDA_TRY(cudaGetLastError());
+    st.launches += 4;
   }
 
-  // 1. seed (or exhaustive evaluation of a small range)
-  const bool exhaustive = span <= kExhaustive;
-  const int64_t S = exhaustive ? span : std::min<int64_t>(kSeeds, span);
-  rc = grow(&c->d_recs, &c->cap_recs, S);
-  if (rc) return rc;
-  lmsb::ExactArgs ea{};
-  ea.a = c->a;
-  ea.b = c->b;
-  ea.n = n;
-  ea.q = q;
-  ea.mode = lmsb::kSrcStrided;
-  ea.count = S;
-  ea.capacity = S;
-  ea.rank_lo = R0;
-  ea.rank_hi = R1;
-  ea.out = c->d_recs;
-  lmsb::launch_exact(ea, exact_grid(c, S), c->stream);
-  lmsb::launch_reduce(c->d_recs, nullptr, S, S, c->d_partials, c->sms, c->d_best, c->stream);
-  CUDA_TRY(cudaGetLastError());
-  st.launches += 3;
-  st.seed_vertices = S;
-  CUDA_TRY(cudaEventRecord(c->ev_seed, c->stream));
-
+  // ---- 2.-5. filter the non-exhaustive fits: phase A (every kPhaseStride-th
+  // row), re-order, phase B (the rest)
   int64_t nchunks = 0;
-  const double* la = c->a;
-  const double* lb = c->b;
-  if (!exhaustive && c->line_order) {
-    // Far-first streaming order from the seed's best line (lms_order.cu).
-    const size_t tmp = lmsb::order_temp_bytes(n);
-    if ((rc = grow(&c->d_keys, &c->cap_keys, 2 * n))) return rc;
-    if ((rc = grow(&c->d_idx, &c->cap_idx, 2 * n))) return rc;
-    if ((rc = grow(&c->d_pa, &c->cap_pa, n))) return rc;
-    if ((rc = grow(&c->d_pb, &c->cap_pb, n))) return rc;
-    if ((rc = grow(&c->d_sort_tmp, &c->cap_sort_tmp, (int64_t)tmp))) return rc;
-    lmsb::OrderArgs oa{};
-    oa.a = c->a;
-    oa.b = c->b;
-    oa.n = n;
-    oa.best = c->d_best;
-    oa.keys_in = c->d_keys;
-    oa.keys_out = c->d_keys + n;
-    oa.idx_in = c->d_idx;
-    oa.idx_out = c->d_idx + n;
-    oa.temp = c->d_sort_tmp;
-    oa.temp_bytes = (size_t)c->cap_sort_tmp;
-    oa.pa = c->d_pa;
-    oa.pb = c->d_pb;
-    if (lmsb::launch_line_order(oa, c->stream) != 0)
-      return set_error(LMS_ERR_CUDA, "line order sort failed");
+  if (tasks > 0) {
+    RC_TRY(c->counts.need(rows + 1));
+    RC_TRY(c->row_task_prefix.need(rows + 1));
+    RC_TRY(c->row_fit.need(rows));
+    RC_TRY(c->row_i.need(rows));
+    RC_TRY(c->task_row.need(tasks));
+    RC_TRY(c->plan_tmp.need((int64_t)lmsb::plan_temp_bytes(rows)));
+    lmsb::PlanArgs pa{};
+    pa.fits = c->fits.p;
+    pa.prefA = c->prefA.p;
+    pa.prefB = c->prefB.p;
+    pa.nfits = F;
+    pa.rowsA = rowsA;
+    pa.nrows = rows;
+    pa.task_vertices = tv;
+    pa.counts = c->counts.p;
+    pa.row_fit = c->row_fit.p;
+    pa.row_i = c->row_i.p;
+    pa.row_task_prefix = c->row_task_prefix.p;
+    pa.task_row = c->task_row.p;
+    pa.temp = c->plan_tmp.p;
+    pa.temp_bytes = (size_t)c->plan_tmp.cap;
+    if (lmsb::launch_plan(pa, c->stream) != 0) return set_error(LMS_ERR_CUDA, "plan scan failed");
     CUDA_TRY(cudaGetLastError());
     st.launches += 3;
-    la = c->d_pa;
-    lb = c->d_pb;
-  }
-  if (!exhaustive) {
-    const int variant = c->filter_variant;
-    const int64_t task_vertices = variant == kFilterFp64   ? lmsb::kFilterTaskVertices
-                                  : variant == kFilterMask ? lmsb::kFilter32mTaskVertices
-                                                           : lmsb::kFilter32TaskVertices;
-    // Warp tasks per row of the range.
-    int64_t i0, j0, i1, j1;
-    lmsb::decode_rank(n, R0, &i0, &j0);
-    lmsb::decode_rank(n, R1 - 1, &i1, &j1);
-    const int64_t nrows = i1 - i0 + 1;
-    std::vector<int64_t> prefix(nrows + 1);
-    int64_t acc = 0;
-    for (int64_t r = 0; r < nrows; ++r) {
-      const int64_t i = i0 + r;
-      const int64_t lo = std::max(lmsb::row_offset(n, i), R0);
-      const int64_t hi = std::min(lmsb::row_offset(n, i) + (n - 1 - i), R1);
-      prefix[r] = acc;
-      acc += (hi - lo + task_vertices - 1) / task_vertices;
-    }
-    prefix[nrows] = acc;
-    const int64_t ntasks = acc;
-    rc = grow(&c->d_task_prefix, &c->cap_rows, nrows + 1);
-    if (rc) return rc;
-    CUDA_TRY(cudaMemcpyAsync(c->d_task_prefix, prefix.data(), sizeof(int64_t) * (nrows + 1),
-                             cudaMemcpyHostToDevice, c->stream));
-    const int64_t chunk_tasks = kChunkVertices / task_vertices;
-    nchunks = (ntasks + chunk_tasks - 1) / chunk_tasks;
-    const int64_t cap = std::min<int64_t>(kChunkVertices, span);
-    rc = grow(&c->d_ranks, &c->cap_ranks, cap);
-    if (rc) return rc;
-    rc = grow(&c->d_recs, &c->cap_recs, cap);
-    if (rc) return rc;
-    rc = ensure_counters(c, nchunks);
-    if (rc) return rc;
-    CUDA_TRY(cudaMemsetAsync(c->d_counters, 0, sizeof(unsigned long long) * (2 + nchunks),
+
+    const int64_t chunk_tasks = kChunkVertices / tv;
+    std::vector<std::pair<int64_t, int64_t>> chunks;
+    for (int64_t t0 = 0; t0 < tasksA; t0 += chunk_tasks)
+      chunks.push_back({t0, std::min(tasksA, t0 + chunk_tasks)});
+    const int64_t first_b = (int64_t)chunks.size();
+    for (int64_t t0 = tasksA; t0 < tasks; t0 += chunk_tasks)
+      chunks.push_back({t0, std::min(tasks, t0 + chunk_tasks)});
+    nchunks = (int64_t)chunks.size();
+    RC_TRY(c->counters.need(2 + nchunks));
+    CUDA_TRY(cudaMemsetAsync(c->counters.p, 0, sizeof(unsigned long long) * (2 + nchunks),
                              c->stream));
     while ((int64_t)c->ev_chunk.size() < 2 * nchunks) {
       cudaEvent_t e;
       CUDA_TRY(cudaEventCreate(&e));
       c->ev_chunk.push_back(e);
     }
+    const double* la = c->a;
+    const double* lb = c->b;
     for (int64_t ch = 0; ch < nchunks; ++ch) {
+      if ((ch == 0 || ch == first_b) && c->line_order && disjoint)
+        RC_TRY(order_lines(c, seg, F, &la, &lb, &st));  // from the current best lines
       lmsb::FilterArgs fa{};
       fa.a = c->a;
       fa.b = c->b;
       fa.la = la;
       fa.lb = lb;
-      fa.n = n;
-      fa.q = q;
-      fa.task_prefix = c->d_task_prefix;
-      fa.row0 = i0;
-      fa.nrows = nrows;
-      fa.rank_lo = R0;
-      fa.rank_hi = R1;
-      fa.task_begin = ch * chunk_tasks;
-      fa.task_end = std::min(ntasks, (ch + 1) * chunk_tasks);
-      fa.amax = c->amax;
-      fa.bmax = c->bmax;
-      fa.best = c->d_best;
-      fa.out_ranks = c->d_ranks;
-      fa.out_count = c->d_counters + 2 + ch;
-      fa.line_evals = c->d_counters + 1;
+      fa.fits = c->fits.p;
+      fa.task_row = c->task_row.p;
+      fa.row_task_prefix = c->row_task_prefix.p;
+      fa.row_fit = c->row_fit.p;
+      fa.row_i = c->row_i.p;
+      fa.task_begin = chunks[ch].first;
+      fa.task_end = chunks[ch].second;
+      fa.best = c->best.p;
+      fa.out_ranks = c->ranks.p;
+      fa.out_fits = c->item_fit.p;
+      fa.out_count = c->counters.p + 2 + ch;
+      fa.line_evals = c->counters.p + 1;
       fa.early_exit = 1;
       CUDA_TRY(cudaEventRecord(c->ev_chunk[2 * ch], c->stream));
-      if (variant == kFilterFp64) lmsb::launch_filter(fa, c->stream);
-      else if (variant == kFilterMask) lmsb::launch_filter32m(fa, c->stream);
-      else lmsb::launch_filter32(fa, c->stream);
+      lmsb::launch_filter(fa, V, c->stream);
       CUDA_TRY(cudaEventRecord(c->ev_chunk[2 * ch + 1], c->stream));
-      lmsb::ExactArgs xa = ea;
-      xa.mode = lmsb::kSrcRanks;
-      xa.count = -1;
-      xa.d_count = c->d_counters + 2 + ch;
+      lmsb::ExactArgs xa{};
+      xa.a = c->a;
+      xa.b = c->b;
+      xa.fits = c->fits.p;
+      xa.mode = lmsb::kSrcList;
+      xa.d_count = c->counters.p + 2 + ch;
       xa.capacity = cap;
-      xa.ranks = c->d_ranks;
-      xa.bound = c->d_best;
-      xa.out = c->d_recs;
-      lmsb::launch_exact(xa, exact_grid(c, -1), c->stream);
-      lmsb::launch_reduce(c->d_recs, c->d_counters + 2 + ch, 0, cap, c->d_partials, c->sms,
-                          c->d_best, c->stream);
+      xa.ranks = c->ranks.p;
+      xa.fit_of = c->item_fit.p;
+      xa.bound = c->best.p;
+      xa.out = c->recs.p;
+      lmsb::launch_exact(xa, persistent_grid(c, -1), c->stream, maxn);
+      lmsb::launch_reduce(c->recs.p, c->counters.p + 2 + ch, 0, cap, c->fits.p, c->keys.p,
+                          c->best.p, (int)c->sms * 4, c->stream);
       CUDA_TRY(cudaGetLastError());
       st.launches += 4;
-      st.filtered_vertices += (fa.task_end - fa.task_begin) * task_vertices;
+      st.filtered_vertices += (fa.task_end - fa.task_begin) * tv;
     }
-    st.filtered_vertices = std::min(st.filtered_vertices, span);
   }
-  CUDA_TRY(cudaMemcpyAsync(c->h_best, c->d_best, sizeof(lms_candidate), cudaMemcpyDeviceToHost,
-                           c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->h_best, c->best.p, sizeof(lms_candidate) * F,
+                           cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(cudaEventRecord(c->ev_end, c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
-  *out = *c->h_best;
+  std::memcpy(out, c->h_best, sizeof(lms_candidate) * F);
   st.chunks = nchunks;
   if (nchunks > 0) {
     std::vector<unsigned long long> cnt(2 + nchunks);
-    CUDA_TRY(cudaMemcpy(cnt.data(), c->d_counters, sizeof(unsigned long long) * (2 + nchunks),
+    CUDA_TRY(cudaMemcpy(cnt.data(), c->counters.p, sizeof(unsigned long long) * (2 + nchunks),
                         cudaMemcpyDeviceToHost));
     st.line_evals = (int64_t)cnt[1];
     for (int64_t ch = 0; ch < nchunks; ++ch) {
@@ -408,67 +503,111 @@ int ctx_solve(lms_ctx* c, int64_t q, int64_t R0, int64_t R1, lms_candidate* out)
       st.ms_filter += ms;
     }
   }
+  st.filtered_vertices = std::min(st.filtered_vertices, st.pairs);
   CUDA_TRY(cudaEventElapsedTime(&st.ms_total, c->ev_begin, c->ev_end));
   st.ms_exact = st.ms_total - st.ms_filter;
   c->stats = st;
   return LMS_OK;
 }
 
+int check_fit(lms_ctx* c, int64_t off, int64_t n, int64_t q) {
+  if (n < 2) return set_error(LMS_ERR_INVALID, "a fit needs at least 2 lines, got %lld", (long long)n);
+  if (q < 1) return set_error(LMS_ERR_INVALID, "coverage must be positive, got %lld", (long long)q);
+  if (off < 0 || off + n > c->nlines)
+    return set_error(LMS_ERR_INVALID, "fit lines [%lld, %lld) outside the %lld bound lines",
+                     (long long)off, (long long)(off + n), (long long)c->nlines);
+  return LMS_OK;
+}
+
+int ctx_solve(lms_ctx* c, int64_t q, int64_t R0, int64_t R1, lms_candidate* out) {
+  std::memset(out, 0, sizeof(*out));
+  if (!c->a) return set_error(LMS_ERR_INVALID, "no lines bound to the context");
+  const int64_t n = c->nlines;
+  RC_TRY(check_fit(c, 0, n, q));
+  const int64_t total = n * (n - 1) / 2;
+  if (R0 < 0 || R1 > total || R0 > R1)
+    return set_error(LMS_ERR_INVALID, "rank range [%lld, %lld) outside [0, %lld)", (long long)R0,
+                     (long long)R1, (long long)total);
+  std::vector<HostFit> hf{{0, n, q, R0, R1}};
+  return ctx_solve_fits(c, hf, out);
+}
+
+int ctx_solve_batch(lms_ctx* c, const int64_t* offsets, const int64_t* q, int64_t nfits,
+                    lms_candidate* out) {
+  if (nfits < 0 || (nfits > 0 && (!offsets || !q))) return set_error(LMS_ERR_INVALID, "bad batch");
+  if (nfits > 0 && !c->a) return set_error(LMS_ERR_INVALID, "no lines bound to the context");
+  std::vector<HostFit> hf(nfits);
+  for (int64_t f = 0; f < nfits; ++f) {
+    const int64_t off = offsets[f], n = offsets[f + 1] - offsets[f];
+    if (f > 0 && off < offsets[f - 1])
+      return set_error(LMS_ERR_INVALID, "batch offsets must be non-decreasing");
+    RC_TRY(check_fit(c, off, n, q[f]));
+    hf[f] = {off, n, q[f], 0, n * (n - 1) / 2};
+  }
+  return ctx_solve_fits(c, hf, out);
+}
+
 int ctx_eval_explicit(lms_ctx* c, int64_t q, const int64_t* i, const int64_t* j, const double* u,
                       const double* v, int64_t m, lms_candidate* out, bool reduce) {
   if (m < 0) return set_error(LMS_ERR_INVALID, "negative vertex count");
-  if (q < 1) return set_error(LMS_ERR_INVALID, "coverage must be positive, got %lld", (long long)q);
-  const int64_t n = c->n;
+  const int64_t n = c->nlines;
+  RC_TRY(check_fit(c, 0, n, q));
   for (int64_t s = 0; s < m; ++s) {
     if (i[s] < 0 || i[s] >= n || j[s] < 0 || j[s] >= n)
-      return set_error(LMS_ERR_INVALID, "vertex %lld has line index out of range", (long long)s);
+      return set_error(LMS_ERR_INVALID, "vertex %lld has a line index out of range", (long long)s);
+    if (reduce && i[s] >= j[s])
+      return set_error(LMS_ERR_INVALID, "vertex %lld must have i < j", (long long)s);
   }
   if (m == 0) {
     if (reduce) std::memset(out, 0, sizeof(*out));
     return LMS_OK;
   }
   CUDA_TRY(cudaSetDevice(c->device));
-  int rc = grow(&c->d_ii, &c->cap_ii, m);
-  if (rc) return rc;
-  rc = grow(&c->d_jj, &c->cap_jj, m);
-  if (rc) return rc;
-  rc = grow(&c->d_uu, &c->cap_uu, m);
-  if (rc) return rc;
-  rc = grow(&c->d_vv, &c->cap_vv, m);
-  if (rc) return rc;
-  rc = grow(&c->d_recs, &c->cap_recs, m);
-  if (rc) return rc;
-  rc = ensure_partials(c);
-  if (rc) return rc;
-  CUDA_TRY(cudaMemcpyAsync(c->d_ii, i, sizeof(int64_t) * m, cudaMemcpyHostToDevice, c->stream));
-  CUDA_TRY(cudaMemcpyAsync(c->d_jj, j, sizeof(int64_t) * m, cudaMemcpyHostToDevice, c->stream));
-  CUDA_TRY(cudaMemcpyAsync(c->d_uu, u, sizeof(double) * m, cudaMemcpyHostToDevice, c->stream));
-  if (v) CUDA_TRY(cudaMemcpyAsync(c->d_vv, v, sizeof(double) * m, cudaMemcpyHostToDevice, c->stream));
+  RC_TRY(c->ii.need(m));
+  RC_TRY(c->jj.need(m));
+  RC_TRY(c->uu.need(m));
+  RC_TRY(c->vv.need(m));
+  RC_TRY(c->recs.need(m));
+  RC_TRY(c->fits.need(1));
+  RC_TRY(c->keys.need(1));
+  RC_TRY(c->best.need(1));
+  lmsb::FitDesc fd{};
+  fd.off = 0;
+  fd.n = n;
+  fd.q = q;
+  CUDA_TRY(cudaMemcpyAsync(c->fits.p, &fd, sizeof(fd), cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->ii.p, i, sizeof(int64_t) * m, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->jj.p, j, sizeof(int64_t) * m, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->uu.p, u, sizeof(double) * m, cudaMemcpyHostToDevice, c->stream));
+  if (v)
+    CUDA_TRY(cudaMemcpyAsync(c->vv.p, v, sizeof(double) * m, cudaMemcpyHostToDevice, c->stream));
   lmsb::ExactArgs ea{};
   ea.a = c->a;
   ea.b = c->b;
-  ea.n = n;
-  ea.q = q;
+  ea.fits = c->fits.p;
   ea.mode = lmsb::kSrcExplicit;
   ea.count = m;
   ea.capacity = m;
-  ea.ii = c->d_ii;
-  ea.jj = c->d_jj;
-  ea.uu = c->d_uu;
-  ea.vv = v ? c->d_vv : nullptr;
-  ea.out = c->d_recs;
-  lmsb::launch_exact(ea, exact_grid(c, m), c->stream);
+  ea.ii = c->ii.p;
+  ea.jj = c->jj.p;
+  ea.uu = c->uu.p;
+  ea.vv = v ? c->vv.p : nullptr;
+  ea.out = c->recs.p;
+  lmsb::launch_exact(ea, persistent_grid(c, m), c->stream, n);
   if (reduce) {
-    CUDA_TRY(cudaMemsetAsync(c->d_best, 0, sizeof(lms_candidate), c->stream));
-    lmsb::launch_reduce(c->d_recs, nullptr, m, m, c->d_partials, c->sms, c->d_best, c->stream);
-    CUDA_TRY(cudaMemcpyAsync(out, c->d_best, sizeof(lms_candidate), cudaMemcpyDeviceToHost,
+    lmsb::launch_reset_best(c->keys.p, c->best.p, 1, c->stream);
+    lmsb::launch_reduce(c->recs.p, nullptr, m, m, c->fits.p, c->keys.p, c->best.p,
+                        reduce_grid(c, m), c->stream);
+    CUDA_TRY(cudaMemcpyAsync(out, c->best.p, sizeof(lms_candidate), cudaMemcpyDeviceToHost,
                              c->stream));
   } else {
-    CUDA_TRY(cudaMemcpyAsync(out, c->d_recs, sizeof(lms_candidate) * m, cudaMemcpyDeviceToHost,
+    CUDA_TRY(cudaMemcpyAsync(out, c->recs.p, sizeof(lms_candidate) * m, cudaMemcpyDeviceToHost,
                              c->stream));
   }
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaStreamSynchronize(c->stream));
+  if (!reduce)
+    for (int64_t s = 0; s < m; ++s) out[s].reserved = 0;
   return LMS_OK;
 }
 
@@ -521,12 +660,23 @@ int lms_min_bracelet_f64(const double* a, const double* b, int64_t n, int64_t q,
                          int64_t rank_begin, int64_t rank_end, int device, lms_candidate* out) {
   if (!out) return set_error(LMS_ERR_INVALID, "null output");
   lms_ctx* c = nullptr;
-  int rc = shared_ctx(device, &c);
-  if (rc) return rc;
+  RC_TRY(shared_ctx(device, &c));
   std::lock_guard<std::mutex> lk(c->mu);
-  rc = ctx_upload(c, a, b, n);
-  if (rc) return rc;
+  RC_TRY(ctx_upload(c, a, b, n));
   return ctx_solve(c, q, rank_begin, rank_end, out);
+}
+
+int lms_batched_f64(const double* x, const double* y, const int64_t* offsets, const int64_t* q,
+                    int64_t nfits, int device, lms_candidate* out) {
+  if (!offsets || nfits < 0 || (nfits > 0 && (!out || !x || !y || !q)))
+    return set_error(LMS_ERR_INVALID, "null argument");
+  if (nfits == 0) return LMS_OK;
+  if (offsets[0] != 0) return set_error(LMS_ERR_INVALID, "offsets[0] must be 0");
+  lms_ctx* c = nullptr;
+  RC_TRY(shared_ctx(device, &c));
+  std::lock_guard<std::mutex> lk(c->mu);
+  RC_TRY(ctx_upload(c, x, y, offsets[nfits]));
+  return ctx_solve_batch(c, offsets, q, nfits, out);
 }
 
 int lms_eval_vertices_f64(const double* a, const double* b, int64_t n, int64_t q, const int64_t* i,
@@ -534,11 +684,9 @@ int lms_eval_vertices_f64(const double* a, const double* b, int64_t n, int64_t q
                           lms_candidate* out) {
   if (!out || (m > 0 && (!i || !j || !u))) return set_error(LMS_ERR_INVALID, "null argument");
   lms_ctx* c = nullptr;
-  int rc = shared_ctx(device, &c);
-  if (rc) return rc;
+  RC_TRY(shared_ctx(device, &c));
   std::lock_guard<std::mutex> lk(c->mu);
-  rc = ctx_upload(c, a, b, n);
-  if (rc) return rc;
+  RC_TRY(ctx_upload(c, a, b, n));
   return ctx_eval_explicit(c, q, i, j, u, v, m, out, false);
 }
 
@@ -547,11 +695,9 @@ int lms_min_over_vertices_f64(const double* a, const double* b, int64_t n, int64
                               int device, lms_candidate* out) {
   if (!out || (m > 0 && (!i || !j || !u))) return set_error(LMS_ERR_INVALID, "null argument");
   lms_ctx* c = nullptr;
-  int rc = shared_ctx(device, &c);
-  if (rc) return rc;
+  RC_TRY(shared_ctx(device, &c));
   std::lock_guard<std::mutex> lk(c->mu);
-  rc = ctx_upload(c, a, b, n);
-  if (rc) return rc;
+  RC_TRY(ctx_upload(c, a, b, n));
   return ctx_eval_explicit(c, q, i, j, u, nullptr, m, out, true);
 }
 
@@ -583,22 +729,16 @@ int lms_ctx_upload(lms_ctx* c, const double* a, const double* b, int64_t n) {
 }
 
 int lms_ctx_bind_dev(lms_ctx* c, const double* d_a, const double* d_b, int64_t n) {
-  if (!c || !d_a || !d_b || n < 2) return set_error(LMS_ERR_INVALID, "bad arguments");
+  if (!c || !d_a || !d_b || n < 1) return set_error(LMS_ERR_INVALID, "bad arguments");
   std::lock_guard<std::mutex> lk(c->mu);
   CUDA_TRY(cudaSetDevice(c->device));
-  std::vector<double> ha(n), hb(n);
-  CUDA_TRY(cudaMemcpy(ha.data(), d_a, sizeof(double) * n, cudaMemcpyDeviceToHost));
-  CUDA_TRY(cudaMemcpy(hb.data(), d_b, sizeof(double) * n, cudaMemcpyDeviceToHost));
-  double am = 0.0, bm = 0.0;
-  for (int64_t k = 0; k < n; ++k) {
-    am = std::max(am, std::fabs(ha[k]));
-    bm = std::max(bm, std::fabs(hb[k]));
-  }
+  c->h_a.resize(n);
+  c->h_b.resize(n);
+  CUDA_TRY(cudaMemcpy(c->h_a.data(), d_a, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(c->h_b.data(), d_b, sizeof(double) * n, cudaMemcpyDeviceToHost));
   c->a = d_a;
   c->b = d_b;
-  c->n = n;
-  c->amax = am;
-  c->bmax = bm;
+  c->nlines = n;
   return LMS_OK;
 }
 
@@ -607,6 +747,13 @@ int lms_ctx_solve(lms_ctx* c, int64_t q, int64_t rank_begin, int64_t rank_end,
   if (!c || !out) return set_error(LMS_ERR_INVALID, "null argument");
   std::lock_guard<std::mutex> lk(c->mu);
   return ctx_solve(c, q, rank_begin, rank_end, out);
+}
+
+int lms_ctx_solve_batch(lms_ctx* c, const int64_t* offsets, const int64_t* q, int64_t nfits,
+                        lms_candidate* out) {
+  if (!c || (nfits > 0 && !out)) return set_error(LMS_ERR_INVALID, "null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  return ctx_solve_batch(c, offsets, q, nfits, out);
 }
 
 int lms_ctx_stats(const lms_ctx* c, lms_stats* out) {

@@ -219,18 +219,219 @@ __device__ lms_candidate exact_vertex(const double* __restrict__ a, const double
   return c;
 }
 
-__global__ void __launch_bounds__(kExactThreads) exact_kernel(ExactArgs args) {
-  __shared__ SelectShared sm;
-  int64_t count = args.count;
-  if (args.mode == kSrcRanks) count = (int64_t)*args.d_count;
-  if (count > args.capacity) count = args.capacity;
-  const int64_t n = args.n;
-  double bound = INFINITY;
+// ---------------------------------------------------------------------------
+// Warp-per-vertex variant for small fits (n <= kWarpExactMaxN): the same
+// passes as exact_vertex with warp-synchronous reductions, so a 512-line
+// vertex does not idle a 256-thread CTA.  Per-warp shared state: two
+// 256-bin digit histograms.
+constexpr int kWarpExactMaxN = 4096;
+
+struct SelectWarp {
+  unsigned hist[2][256];
+};
+
+// Bucket of rank r in hist (warp-wide): digit, count below it, its count.
+__device__ __forceinline__ void pick_digit_warp(const unsigned* hist, long long r, int& digit,
+                                                long long& below, unsigned& cnt) {
+  const int lane = threadIdx.x & 31;
+  unsigned h[8];
+  unsigned sum = 0;
+#pragma unroll
+  for (int d = 0; d < 8; ++d) {
+    h[d] = hist[lane * 8 + d];
+    sum += h[d];
+  }
+  unsigned incl = sum;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const unsigned o = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += o;
+  }
+  const unsigned excl = incl - sum;
+  const bool mine = r >= (long long)excl && r < (long long)incl;
+  int dg = 0;
+  unsigned c = excl, ct = 0;
+  if (mine) {
+#pragma unroll
+    for (int d = 0; d < 8; ++d) {
+      if (r >= (long long)c && r < (long long)(c + h[d])) {
+        dg = lane * 8 + d;
+        ct = h[d];
+        break;
+      }
+      c += h[d];
+    }
+  }
+  const unsigned ballot = __ballot_sync(0xffffffffu, mine);
+  const int src = __ffs(ballot) - 1;
+  digit = __shfl_sync(0xffffffffu, dg, src);
+  below = (long long)__shfl_sync(0xffffffffu, c, src);
+  cnt = __shfl_sync(0xffffffffu, ct, src);
+}
+
+__device__ lms_candidate exact_vertex_warp(const double* __restrict__ a,
+                                           const double* __restrict__ b, int64_t n, int64_t q,
+                                           int64_t i, int64_t j, double u, double v0,
+                                           double bound, SelectWarp& sw) {
+  const int lane = threadIdx.x & 31;
+  unsigned lt = 0, le = 0, wu = 0, wd = 0;
+  for (int64_t k = lane; k < n; k += 32) {
+    const double x = snapped_cut(a, b, k, i, j, u, v0);
+    lt += x < v0;
+    le += x <= v0;
+    wu += x >= v0 && __dsub_rn(x, v0) <= bound;
+    wd += x <= v0 && __dsub_rn(v0, x) <= bound;
+  }
+  const int64_t c_lt = __reduce_add_sync(0xffffffffu, lt);
+  const int64_t c_le = __reduce_add_sync(0xffffffffu, le);
+  const int64_t c_up = __reduce_add_sync(0xffffffffu, wu);
+  const int64_t c_dn = __reduce_add_sync(0xffffffffu, wd);
+  lms_candidate c = cand_none();
+  if (isfinite(bound) && c_up < q && c_dn < q) return c;
+  const int64_t down = c_le - q;
+  const int64_t up = c_lt + q - 1;
+  const bool ok_down = down >= 0;
+  const bool ok_up = up <= n - 1;
+  c.i = i;
+  c.j = j;
+  c.u = u;
+  if (c_le - c_lt >= q && isfinite(v0)) {
+    c.height = 0.0;
+    c.v_low = v0;
+    c.v_high = v0;
+    c.found = 1;
+    return c;
+  }
+  unsigned long long prefix[2] = {0ULL, 0ULL}, result[2] = {0ULL, 0ULL};
+  long long rank[2] = {up, down};
+  int state[2] = {ok_up ? 0 : -1, ok_down ? 0 : -1};
+  for (int level = 0; level < 8; ++level) {
+    if ((state[0] == 2 || state[0] == -1) && (state[1] == 2 || state[1] == -1)) break;
+    const int shift = 56 - 8 * level;
+#pragma unroll
+    for (int e = lane; e < 512; e += 32) (&sw.hist[0][0])[e] = 0u;
+    __syncwarp();
+    unsigned long long found0 = 0ULL, found1 = 0ULL;
+    bool has0 = false, has1 = false;
+    for (int64_t k = lane; k < n; k += 32) {
+      const unsigned long long key = key_of(snapped_cut(a, b, k, i, j, u, v0));
+      const unsigned long long hi = level == 0 ? 0ULL : (key >> (shift + 8));
+      const unsigned digit = (unsigned)(key >> shift) & 255u;
+      if (state[0] == 0 && hi == prefix[0]) atomicAdd(&sw.hist[0][digit], 1u);
+      if (state[1] == 0 && hi == prefix[1]) atomicAdd(&sw.hist[1][digit], 1u);
+      if (state[0] == 1 && hi == prefix[0]) {
+        found0 = key;
+        has0 = true;
+      }
+      if (state[1] == 1 && hi == prefix[1]) {
+        found1 = key;
+        has1 = true;
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      if (state[t] == 1) {  // the unique element with this prefix, found this pass
+        const unsigned bal = __ballot_sync(0xffffffffu, t == 0 ? has0 : has1);
+        result[t] = __shfl_sync(0xffffffffu, t == 0 ? found0 : found1, __ffs(bal) - 1);
+        state[t] = 2;
+      } else if (state[t] == 0) {
+        int digit;
+        long long below;
+        unsigned cnt;
+        pick_digit_warp(sw.hist[t], rank[t], digit, below, cnt);
+        prefix[t] = (prefix[t] << 8) | (unsigned long long)digit;
+        rank[t] -= below;
+        if (level == 7) {
+          result[t] = prefix[t];
+          state[t] = 2;
+        } else if (cnt == 1) {
+          state[t] = 1;
+        }
+      }
+    }
+    __syncwarp();
+  }
+  const double v_up = ok_up ? value_of(result[0]) : 0.0;
+  const double v_down = ok_down ? value_of(result[1]) : 0.0;
+  const double h_down = ok_down ? __dsub_rn(v0, v_down) : INFINITY;
+  const double h_up = ok_up ? __dsub_rn(v_up, v0) : INFINITY;
+  const bool use_up = h_up <= h_down;
+  const double h = use_up ? h_up : h_down;
+  if (isfinite(h)) {
+    c.height = h;
+    c.v_low = use_up ? v0 : v_down;
+    c.v_high = use_up ? v_up : v0;
+    c.found = 1;
+  }
+  return c;
+}
+
+__device__ __forceinline__ bool item_vertex(const ExactArgs& args, int64_t s, int32_t& f,
+                                            FitDesc& fd, int64_t& i, int64_t& j, double& u,
+                                            double& v0, double& bound) {
+  f = args.mode == kSrcList ? args.fit_of[s] : 0;
+  fd = args.fits[f];
+  const double* a = args.a + fd.off;
+  const double* b = args.b + fd.off;
+  bound = INFINITY;
   if (args.bound) {
-    const lms_candidate bc = *args.bound;
+    const lms_candidate bc = args.bound[f];
     if (bc.found) bound = bc.height;
   }
+  if (args.mode == kSrcExplicit) {
+    i = args.ii[s];
+    j = args.jj[s];
+    u = args.uu[s];
+    v0 = args.vv ? args.vv[s] : cut_value(u, a[i], b[i]);
+    return true;
+  }
+  decode_rank(fd.n, args.ranks[s], &i, &j);
+  const double ai = a[i], aj = a[j];
+  // _scan_rank_range drops parallel duals and forms u unfused (backend.py:200-204).
+  u = __ddiv_rn(__dsub_rn(b[i], b[j]), __dsub_rn(ai, aj));
+  v0 = cut_value(u, ai, b[i]);
+  return __dsub_rn(ai, aj) != 0.0;
+}
+
+constexpr int kWarpExactWarps = 8;
+
+__global__ void __launch_bounds__(kWarpExactWarps * 32) exact_warp_kernel(ExactArgs args) {
+  __shared__ SelectWarp sw[kWarpExactWarps];
+  int64_t count = args.d_count ? (int64_t)*args.d_count : args.count;
+  if (count > args.capacity) count = args.capacity;
+  const int wib = threadIdx.x >> 5;
+  const int64_t gw = (int64_t)blockIdx.x * kWarpExactWarps + wib;
+  const int64_t nw = (int64_t)gridDim.x * kWarpExactWarps;
+  for (int64_t s = gw; s < count; s += nw) {
+    int32_t f;
+    FitDesc fd;
+    int64_t i, j;
+    double u, v0, bound;
+    const bool valid = item_vertex(args, s, f, fd, i, j, u, v0, bound);
+    lms_candidate c = cand_none();
+    if (valid)
+      c = exact_vertex_warp(args.a + fd.off, args.b + fd.off, fd.n, fd.q, i, j, u, v0, bound,
+                            sw[wib]);
+    c.reserved = f;
+    if ((threadIdx.x & 31) == 0) args.out[s] = c;
+  }
+}
+
+__global__ void __launch_bounds__(kExactThreads) exact_kernel(ExactArgs args) {
+  __shared__ SelectShared sm;
+  int64_t count = args.d_count ? (int64_t)*args.d_count : args.count;
+  if (count > args.capacity) count = args.capacity;
   for (int64_t s = blockIdx.x; s < count; s += gridDim.x) {
+    const int32_t f = args.mode == kSrcList ? args.fit_of[s] : 0;
+    const FitDesc fd = args.fits[f];
+    const double* a = args.a + fd.off;
+    const double* b = args.b + fd.off;
+    double bound = INFINITY;
+    if (args.bound) {
+      const lms_candidate bc = args.bound[f];
+      if (bc.found) bound = bc.height;
+    }
     int64_t i, j;
     double u, v0;
     bool valid = true;
@@ -238,78 +439,147 @@ __global__ void __launch_bounds__(kExactThreads) exact_kernel(ExactArgs args) {
       i = args.ii[s];
       j = args.jj[s];
       u = args.uu[s];
-      v0 = args.vv ? args.vv[s] : cut_value(u, args.a[i], args.b[i]);
+      v0 = args.vv ? args.vv[s] : cut_value(u, a[i], b[i]);
     } else {
-      int64_t r;
-      if (args.mode == kSrcRanks) {
-        r = args.ranks[s];
-      } else {  // stratified sample of [rank_lo, rank_hi)
-        const int64_t span = args.rank_hi - args.rank_lo;
-        r = args.rank_lo + ((2 * s + 1) * span) / (2 * count);
-      }
-      decode_rank(n, r, &i, &j);
-      const double ai = args.a[i], aj = args.a[j];
+      decode_rank(fd.n, args.ranks[s], &i, &j);
+      const double ai = a[i], aj = a[j];
       // _scan_rank_range drops parallel duals and forms u unfused
       // (backend.py:200-204).
       valid = __dsub_rn(ai, aj) != 0.0;
-      u = __ddiv_rn(__dsub_rn(args.b[i], args.b[j]), __dsub_rn(ai, aj));
-      v0 = cut_value(u, ai, args.b[i]);
+      u = __ddiv_rn(__dsub_rn(b[i], b[j]), __dsub_rn(ai, aj));
+      v0 = cut_value(u, ai, b[i]);
     }
     lms_candidate c = cand_none();
-    if (valid) c = exact_vertex(args.a, args.b, n, args.q, i, j, u, v0, bound, sm);
+    if (valid) c = exact_vertex(a, b, fd.n, fd.q, i, j, u, v0, bound, sm);
+    c.reserved = f;
     if (threadIdx.x == 0) args.out[s] = c;
   }
 }
 
-constexpr int kReduceThreads = 256;
+// 128-bit CAS on a BestKey (atom.global.cas.b128, sm_90+).
+__device__ __forceinline__ BestKey cas_key(BestKey* addr, BestKey expect, BestKey desired) {
+  BestKey old;
+  asm volatile(
+      "{\n .reg .b128 e, d, o;\n mov.b128 e, {%2, %3};\n mov.b128 d, {%4, %5};\n"
+      " atom.global.cas.b128 o, [%6], e, d;\n mov.b128 {%0, %1}, o;\n}"
+      : "=l"(old.lo), "=l"(old.hi)
+      : "l"(expect.lo), "l"(expect.hi), "l"(desired.lo), "l"(desired.hi), "l"(addr)
+      : "memory");
+  return old;
+}
 
-__global__ void __launch_bounds__(kReduceThreads)
-    reduce_partial_kernel(const lms_candidate* __restrict__ recs, const unsigned long long* d_count,
-                          int64_t count, int64_t capacity, lms_candidate* __restrict__ partials) {
+__device__ __forceinline__ bool key_less(const BestKey& x, const BestKey& y) {
+  return x.hi < y.hi || (x.hi == y.hi && x.lo < y.lo);
+}
+
+// (height, i, j) -> 128-bit key: heights are finite and >= 0 (or -0.0, which
+// ties +0.0), so the bits of h + 0.0 order like the values; the pair rank
+// orders like (i, j) (row-major triangle).
+__device__ __forceinline__ BestKey record_key(const lms_candidate& c, int64_t n) {
+  BestKey k;
+  k.hi = (unsigned long long)__double_as_longlong(c.height + 0.0);
+  k.lo = (unsigned long long)(row_offset(n, c.i) + (c.j - c.i - 1));
+  return k;
+}
+
+__global__ void reduce_cas_kernel(const lms_candidate* __restrict__ recs,
+                                  const unsigned long long* d_count, int64_t count,
+                                  int64_t capacity, const FitDesc* __restrict__ fits,
+                                  BestKey* keys) {
   if (d_count) count = (int64_t)*d_count;
   if (count > capacity) count = capacity;
-  lms_candidate best = cand_none();
   for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < count;
        s += (int64_t)gridDim.x * blockDim.x) {
-    lms_candidate c = recs[s];
-    if (cand_less(c, best)) best = c;
-  }
-  best = warp_min_cand(best);
-  __shared__ lms_candidate sh[kReduceThreads / kWarp];
-  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = best;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    best = threadIdx.x < kReduceThreads / kWarp ? sh[threadIdx.x] : cand_none();
-    best = warp_min_cand(best);
-    if (threadIdx.x == 0) partials[blockIdx.x] = best;
+    const lms_candidate c = recs[s];
+    if (!c.found) continue;
+    const BestKey k = record_key(c, fits[c.reserved].n);
+    BestKey* addr = keys + c.reserved;
+    BestKey cur = *addr;  // a torn read only costs one failed CAS
+    while (key_less(k, cur)) {
+      const BestKey prev = cas_key(addr, cur, k);
+      if (prev.lo == cur.lo && prev.hi == cur.hi) break;
+      cur = prev;
+    }
   }
 }
 
-__global__ void __launch_bounds__(32)
-    reduce_final_kernel(const lms_candidate* __restrict__ partials, int np,
-                        lms_candidate* __restrict__ best_io) {
-  lms_candidate best = threadIdx.x == 0 ? *best_io : cand_none();
-  for (int s = threadIdx.x; s < np; s += 32) {
-    lms_candidate c = partials[s];
-    if (cand_less(c, best)) best = c;
+__global__ void publish_kernel(const lms_candidate* __restrict__ recs,
+                               const unsigned long long* d_count, int64_t count, int64_t capacity,
+                               const FitDesc* __restrict__ fits, const BestKey* __restrict__ keys,
+                               lms_candidate* __restrict__ best) {
+  if (d_count) count = (int64_t)*d_count;
+  if (count > capacity) count = capacity;
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < count;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    lms_candidate c = recs[s];
+    if (!c.found) continue;
+    const int32_t f = c.reserved;
+    const BestKey k = record_key(c, fits[f].n);
+    const BestKey w = keys[f];
+    if (k.lo == w.lo && k.hi == w.hi) {  // duplicates of one vertex are identical
+      c.reserved = 0;
+      best[f] = c;
+    }
   }
-  best = warp_min_cand(best);
-  if (threadIdx.x == 0) *best_io = best;
+}
+
+__global__ void reset_best_kernel(BestKey* keys, lms_candidate* best, int64_t nfits) {
+  for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < nfits;
+       f += (int64_t)gridDim.x * blockDim.x) {
+    keys[f].lo = ~0ULL;
+    keys[f].hi = ~0ULL;
+    best[f] = cand_none();
+  }
+}
+
+__global__ void gen_seeds_kernel(const FitDesc* __restrict__ fits,
+                                 const int64_t* __restrict__ seed_prefix, int64_t nfits,
+                                 int64_t* __restrict__ ranks, int32_t* __restrict__ fit_of) {
+  const int64_t total = seed_prefix[nfits];
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < total;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = nfits - 1;  // largest f with seed_prefix[f] <= s
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) >> 1;
+      if (seed_prefix[mid] <= s) lo = mid;
+      else hi = mid - 1;
+    }
+    const FitDesc fd = fits[lo];
+    const int64_t k = s - seed_prefix[lo];
+    const int64_t cnt = seed_prefix[lo + 1] - seed_prefix[lo];
+    const int64_t span = fd.rank_hi - fd.rank_lo;
+    ranks[s] = fd.rank_lo + ((2 * k + 1) * span) / (2 * cnt);
+    fit_of[s] = (int32_t)lo;
+  }
 }
 
 }  // namespace
 
-void launch_exact(const ExactArgs& args, int grid, cudaStream_t stream) {
+void launch_exact(const ExactArgs& args, int grid, cudaStream_t stream, int64_t max_n) {
   if (grid <= 0) return;
-  exact_kernel<<<grid, kExactThreads, 0, stream>>>(args);
+  if (max_n <= kWarpExactMaxN) {
+    exact_warp_kernel<<<grid, kWarpExactWarps * 32, 0, stream>>>(args);
+  } else {
+    exact_kernel<<<grid, kExactThreads, 0, stream>>>(args);
+  }
 }
 
 void launch_reduce(const lms_candidate* recs, const unsigned long long* d_count, int64_t count,
-                   int64_t capacity, lms_candidate* partials, int npartials,
-                   lms_candidate* best_io, cudaStream_t stream) {
-  reduce_partial_kernel<<<npartials, kReduceThreads, 0, stream>>>(recs, d_count, count, capacity,
-                                                                  partials);
-  reduce_final_kernel<<<1, 32, 0, stream>>>(partials, npartials, best_io);
+                   int64_t capacity, const FitDesc* fits, BestKey* keys, lms_candidate* best,
+                   int grid, cudaStream_t stream) {
+  if (grid <= 0) return;
+  reduce_cas_kernel<<<grid, 256, 0, stream>>>(recs, d_count, count, capacity, fits, keys);
+  publish_kernel<<<grid, 256, 0, stream>>>(recs, d_count, count, capacity, fits, keys, best);
+}
+
+void launch_reset_best(BestKey* keys, lms_candidate* best, int64_t nfits, cudaStream_t stream) {
+  const int grid = (int)((nfits + 255) / 256);
+  reset_best_kernel<<<grid > 0 ? grid : 1, 256, 0, stream>>>(keys, best, nfits);
+}
+
+void launch_gen_seeds(const FitDesc* fits, const int64_t* seed_prefix, int64_t nfits,
+                      int64_t* ranks, int32_t* fit_of, cudaStream_t stream) {
+  gen_seeds_kernel<<<512, 256, 0, stream>>>(fits, seed_prefix, nfits, ranks, fit_of);
 }
 
 }  // namespace lmsb

@@ -1,21 +1,57 @@
-// lms_filter32m.cu -- count filter with packed-FP16 compares and integer
-// mask accumulation (no tensor core).  Same contract, margins and line
-// staging as lms_filter32.cu; only the counting differs:
+// lms_filter32m.cu -- the count filter (the O(n^3) stage of the exact search).
 //
-//   t    = fma2(u, (A_k, A_k+1), -(Bu_k, Bu_k+1))   FFMA2
+// For the bound H (the height of an exactly evaluated vertex, so H >= the
+// optimum) a vertex can only matter if one of its anchored windows has
+// height <= H.  With d_k = x_k - v0 the vertical offset of line k from the
+// anchor, the reference's upward window (backend.py:153,159) has h_up <= H
+// iff at least q lines satisfy 0 <= d_k <= H (anchors and ties included),
+// and symmetrically h_down <= H iff at least q lines satisfy -H <= d_k <= 0.
+// This kernel counts both windows for every vertex, widened by a rigorous
+// rounding margin, and keeps the vertex when either count reaches q.
+// Survivors are re-evaluated bit-exactly in FP64 (lms_exact.cu), so the
+// filter only has to return a superset; its arithmetic may be approximate as
+// long as the margin covers the error.
+//
+// Warp task: up to 32*V consecutive vertices of one triangle row i of one
+// fit.  Lines are re-expressed relative to the row's anchor line,
+// A_k = (a_k - a_i)/S and Bu_k = ((b_k - b_i) + H/2)/S, formed in FP64 and
+// rounded to FP32 once per line and warp (S = power of two >= the warp's
+// largest window, so the scaling is exact), and staged per warp in 64-line
+// chunks of shared memory (16-byte (A_k, A_k+1, -Bu_k, -Bu_k+1) records,
+// broadcast to all lanes).  Lane l owns vertices l + 32*s.  Per vertex and
+// line pair:
+//
+//   t    = fma2(u, (A_k, A_k+1), -(Bu_k, Bu_k+1))   FFMA2 (packed fp32x2)
 //   hu   = half2(t)                                  F2FP
-//   hd   = hu + (H/S, H/S)                           HADD2
+//   hd   = hu + (H/S, H/S)                           HADD2 (down window)
 //   mu   = |hu| <= w_v  as 0xFFFF masks per half     HSET2 (mask form)
 //   md   = |hd| <= w_v                               HSET2
-//   cu  += mu, cd += md                              2x IADD (32-bit)
+//   cu  += mu, cd += md                              IADD3 (ptxas merges two)
 //
 // A 32-bit sum of such masks encodes two independent counts: with U_e, U_o
 // the hits in the low / high halves, sum = (U_e - U_o)*2^16 - U_e (mod
 // 2^32), so U_e = -lo16(sum) mod 2^16 and U_o = U_e - hi16(sum + U_e)
 // (mod 2^16) are recovered exactly while both stay below 2^16 (n <= 131070
-// lines).  Thread-per-vertex layout: lane l owns vertices l + 32*s of the
-// warp task; every lane streams the same line pairs (shared-memory
-// broadcast).
+// lines).  (Tensor-core counting with legacy mma.sync was measured slower:
+// on B200 HMMA.16816 issues at ~0.1/clk/SMSP and throttles the other pipes;
+// see DESIGN.md.)
+//
+// Early exit: once max(count_up, count_dn) + lines left < q for every vertex
+// of the warp, none can reach q and the warp stops.  Lines stream far-first
+// (lms_order.cu), so this happens after ~n - q lines.
+//
+// Error budget (unnormalised units; eps32 = 2^-24):
+//   u -> fp32, A, Bu -> fp32 and the FFMA rounding: <= 3*eps32*(|u|*|A|max
+//   + |B|max + H); the FP64 line shifts and the reference's own roundings of
+//   x_k, v0 and fl(x - v0) <= H: <= 2^-50*(|u|*amax + bmax + H).  Margin
+//   E_v = 2^-20*(|u|*amax + bmax + H) + 1e-300 covers both with >= 2x to
+//   spare (|A|max <= 2*amax, |B|max <= 2*bmax).  In units of S, FP16
+//   rounding of t (|t| < 4 where it matters) is <= 2^-10, of H/S <= 2^-11
+//   and of the HADD2 <= 2^-11; thresholds add 2^-8 and round up.  t beyond
+//   the FP16 range becomes inf and never counts, which is correct because
+//   such lines are far outside every window (|t|/S > 65504 >> 2).  Vertices
+//   whose magnitudes could overflow FP32 are passed to the exact stage
+//   unconditionally.
 
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -30,31 +66,10 @@ namespace lmsb {
 
 namespace {
 
-constexpr int kV = kFilter32mV;  // vertices per lane
-
 struct __align__(16) LinePair {
   float2 A;   // (A_k, A_k+1)
   float2 Bn;  // (-Bu_k, -Bu_k+1)
 };
-
-// Accumulation of a half2 mask word.  IMAD (mad.lo c, m, 1, c) issues on the
-// FMA pipe, IADD3 on the ALU pipe that F2FP and HSET2 already load; the
-// LMSB_F32M_ACC policy picks the split (0: both IADD3, 1: up IMAD / down
-// IADD3, 2: both IMAD).
-#ifndef LMSB_F32M_ACC
-#define LMSB_F32M_ACC 1
-#endif
-__device__ __forceinline__ void acc_imad(uint32_t& c, uint32_t m) {
-  asm volatile("mad.lo.u32 %0, %1, 1, %0;" : "+r"(c) : "r"(m));
-}
-__device__ __forceinline__ void acc_up(uint32_t& c, uint32_t m) {
-  if (LMSB_F32M_ACC >= 1) acc_imad(c, m);
-  else c += m;
-}
-__device__ __forceinline__ void acc_dn(uint32_t& c, uint32_t m) {
-  if (LMSB_F32M_ACC >= 2) acc_imad(c, m);
-  else c += m;
-}
 
 __device__ __forceinline__ uint32_t mask_total(uint32_t sum) {
   const uint32_t ue = (0x10000u - (sum & 0xFFFFu)) & 0xFFFFu;
@@ -62,31 +77,35 @@ __device__ __forceinline__ uint32_t mask_total(uint32_t sum) {
   return ue + uo;
 }
 
-__global__ void __launch_bounds__(kFilterWarpsPerBlock * 32, kFilter32mMinBlocks)
+template <int kV>
+__global__ void __launch_bounds__(kFilterWarpsPerBlock * 32, kV >= 4 ? 3 : 4)
     filter32m_kernel(FilterArgs args) {
+  constexpr int64_t kTaskVertices = 32 * kV;
   __shared__ LinePair slab[kFilterWarpsPerBlock][32];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int64_t task = args.task_begin + (int64_t)blockIdx.x * kFilterWarpsPerBlock + wib;
   if (task >= args.task_end) return;
 
-  int64_t lo = 0, hi = args.nrows - 1;
-  while (lo < hi) {
-    int64_t mid = (lo + hi + 1) >> 1;
-    if (args.task_prefix[mid] <= task) lo = mid;
-    else hi = mid - 1;
-  }
-  const int64_t n = args.n;
-  const int64_t i = args.row0 + lo;
+  // task -> global row -> (fit, triangle row i, first vertex rank)
+  const int64_t grow = args.task_row[task];
+  const int32_t fit = args.row_fit[grow];
+  const FitDesc fd = args.fits[fit];
+  const int64_t n = fd.n;
+  const int64_t i = args.row_i[grow];
   const int64_t row_lo = row_offset(n, i);
   const int64_t row_hi = row_lo + (n - 1 - i);
-  const int64_t rs = row_lo > args.rank_lo ? row_lo : args.rank_lo;
-  const int64_t re = row_hi < args.rank_hi ? row_hi : args.rank_hi;
-  const int64_t r_first = rs + (task - args.task_prefix[lo]) * kFilter32mTaskVertices;
+  const int64_t rs = row_lo > fd.rank_lo ? row_lo : fd.rank_lo;
+  const int64_t re = row_hi < fd.rank_hi ? row_hi : fd.rank_hi;
+  const int64_t r_first = rs + (task - args.row_task_prefix[grow]) * kTaskVertices;
+  const double* a = args.a + fd.off;
+  const double* b = args.b + fd.off;
+  const double* la = args.la + fd.off;
+  const double* lb = args.lb + fd.off;
 
-  const double ai = args.a[i];
-  const double bi = args.b[i];
-  const lms_candidate best = *args.best;
+  const double ai = a[i];
+  const double bi = b[i];
+  const lms_candidate best = args.best[fit];
   const double H = best.found ? best.height : INFINITY;
   const double half = 0.5 * H;
 
@@ -103,14 +122,14 @@ __global__ void __launch_bounds__(kFilterWarpsPerBlock * 32, kFilter32mMinBlocks
     w64[s] = 0.0;
     if (valid[s]) {
       const int64_t j = r - row_lo + i + 1;
-      const double aj = args.a[j];
+      const double aj = a[j];
       const double da = __dsub_rn(ai, aj);
-      const double uv = __ddiv_rn(__dsub_rn(bi, args.b[j]), da);
+      const double uv = __ddiv_rn(__dsub_rn(bi, b[j]), da);
       valid[s] = da != 0.0 && isfinite(uv);
       if (valid[s]) {
-        const double mag = fabs(uv) * args.amax;
-        const double w = half + (0x1p-20 * (mag + args.bmax + H) + 1e-300);
-        force[s] = !(mag < 1e30) || !(args.bmax < 1e30) || !(w < 1e30);
+        const double mag = fabs(uv) * fd.amax;
+        const double w = half + (0x1p-20 * (mag + fd.bmax + H) + 1e-300);
+        force[s] = !(mag < 1e30) || !(fd.bmax < 1e30) || !(w < 1e30);
         u32[s] = (float)uv;
         w64[s] = w;
         if (!force[s]) wmax = fmax(wmax, w);
@@ -141,11 +160,11 @@ __global__ void __launch_bounds__(kFilterWarpsPerBlock * 32, kFilter32mMinBlocks
   double2 ak2 = make_double2(0.0, 0.0), bk2 = make_double2(0.0, 0.0);
   auto load_pair = [&](int64_t k) {
     if (k + 1 < n) {
-      ak2 = __ldg(reinterpret_cast<const double2*>(args.la + k));
-      bk2 = __ldg(reinterpret_cast<const double2*>(args.lb + k));
+      ak2 = make_double2(__ldg(la + k), __ldg(la + k + 1));
+      bk2 = make_double2(__ldg(lb + k), __ldg(lb + k + 1));
     } else if (k < n) {
-      ak2 = make_double2(__ldg(args.la + k), 0.0);
-      bk2 = make_double2(__ldg(args.lb + k), 0.0);
+      ak2 = make_double2(__ldg(la + k), 0.0);
+      bk2 = make_double2(__ldg(lb + k), 0.0);
     }
   };
   load_pair(2 * lane);
@@ -179,8 +198,8 @@ __global__ void __launch_bounds__(kFilterWarpsPerBlock * 32, kFilter32mMinBlocks
         const float2 t = __ffma2_rn(L.A, make_float2(u32[s], u32[s]), L.Bn);
         const __half2 hu = __floats2half2_rn(t.x, t.y);
         const __half2 hd = __hadd2(hu, hn2);
-        acc_up(cu[s], __hle2_mask(__habs2(hu), w2[s]));
-        acc_dn(cd[s], __hle2_mask(__habs2(hd), w2[s]));
+        cu[s] += __hle2_mask(__habs2(hu), w2[s]);
+        cd[s] += __hle2_mask(__habs2(hd), w2[s]);
       }
     }
     evals += (n - k0) < 64 ? (n - k0) : 64;
@@ -191,7 +210,7 @@ __global__ void __launch_bounds__(kFilterWarpsPerBlock * 32, kFilter32mMinBlocks
 #pragma unroll
       for (int s = 0; s < kV; ++s) {
         const uint32_t m = max(mask_total(cu[s]), mask_total(cd[s]));
-        alive |= valid[s] && !force[s] && (m + left >= (uint32_t)args.q);
+        alive |= valid[s] && !force[s] && (m + left >= (uint32_t)fd.q);
       }
       if (!__any_sync(0xffffffffu, alive)) break;
     }
@@ -199,7 +218,7 @@ __global__ void __launch_bounds__(kFilterWarpsPerBlock * 32, kFilter32mMinBlocks
 
 #pragma unroll
   for (int s = 0; s < kV; ++s) {
-    const uint32_t q = (uint32_t)args.q;
+    const uint32_t q = (uint32_t)fd.q;
     const bool keep = valid[s] && (force[s] || mask_total(cu[s]) >= q || mask_total(cd[s]) >= q);
     const unsigned mask = __ballot_sync(0xffffffffu, keep);
     if (mask) {
@@ -209,24 +228,29 @@ __global__ void __launch_bounds__(kFilterWarpsPerBlock * 32, kFilter32mMinBlocks
       if (keep) {
         const unsigned slot = __popc(mask & ((1u << lane) - 1u));
         args.out_ranks[base + slot] = r_first + lane + 32 * s;
+        args.out_fits[base + slot] = fit;
       }
     }
   }
   if (args.line_evals && lane == 0) {
     const int64_t left_in_task = re - r_first;
-    const int nv =
-        left_in_task < kFilter32mTaskVertices ? (int)left_in_task : kFilter32mTaskVertices;
+    const int nv = left_in_task < kTaskVertices ? (int)left_in_task : (int)kTaskVertices;
     atomicAdd(args.line_evals, (unsigned long long)(evals * nv));
   }
 }
 
 }  // namespace
 
-void launch_filter32m(const FilterArgs& args, cudaStream_t stream) {
+void launch_filter(const FilterArgs& args, int v, cudaStream_t stream) {
   const int64_t tasks = args.task_end - args.task_begin;
   if (tasks <= 0) return;
-  const int64_t blocks = (tasks + kFilterWarpsPerBlock - 1) / kFilterWarpsPerBlock;
-  filter32m_kernel<<<(unsigned)blocks, kFilterWarpsPerBlock * 32, 0, stream>>>(args);
+  const unsigned blocks = (unsigned)((tasks + kFilterWarpsPerBlock - 1) / kFilterWarpsPerBlock);
+  const unsigned threads = kFilterWarpsPerBlock * 32;
+  switch (v) {
+    case 1: filter32m_kernel<1><<<blocks, threads, 0, stream>>>(args); break;
+    case 2: filter32m_kernel<2><<<blocks, threads, 0, stream>>>(args); break;
+    default: filter32m_kernel<4><<<blocks, threads, 0, stream>>>(args); break;
+  }
 }
 
 }  // namespace lmsb

@@ -1,4 +1,11 @@
-// lms_kernels.cuh -- launch interfaces of the exact-LMS kernels (host side).
+// lms_kernels.cuh -- device data model and launch interfaces of the
+// exact-LMS kernels (host side).
+//
+// A solve is a batch of F independent fits (F = 1 for one large fit, F =
+// 8,192 for the Hough-refinement workload).  Fit f owns lines
+// [off, off + n) of the concatenated fp64 arrays a[] (x) and b[] (y) and the
+// pair-rank range [rank_lo, rank_hi) of its own row-major upper triangle
+// (backend.py:111-122).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -9,95 +16,99 @@
 
 namespace lmsb {
 
+struct FitDesc {
+  int64_t off;       // first line of the fit in a[] / b[]
+  int64_t n;
+  int64_t q;
+  int64_t rank_lo;   // vertex ranks of this fit handled by the solve
+  int64_t rank_hi;
+  int64_t row0;      // first triangle row of [rank_lo, rank_hi)
+  int64_t nrows;     // rows in the filter task list (0: fit solved exhaustively)
+  double amax;       // max |a|, max |b| over the fit's lines (filter margins)
+  double bmax;
+};
+
+// 128-bit lexicographic key (height bits, pair rank) of a fit's best record,
+// updated with 128-bit atomic CAS; hi = canonical bits of the height, lo = rank.
+struct __align__(16) BestKey {
+  unsigned long long lo;
+  unsigned long long hi;
+};
+
+// ---------------------------------------------------------------- exact stage
 enum ExactSource : int {
-  kSrcRanks = 0,     // ranks[s], s < *d_count (filter survivors)
-  kSrcStrided = 1,   // stratified sample of [rank_lo, rank_hi), s < count
-  kSrcExplicit = 2,  // explicit (i, j, u[, v]) lists, s < count
+  kSrcList = 0,      // (ranks[s], fit_of[s]), s < *d_count or count
+  kSrcExplicit = 1,  // explicit (i, j, u[, v]) of fit 0, s < count
 };
 
 struct ExactArgs {
   const double* a;
   const double* b;
-  int64_t n;
-  int64_t q;
+  const FitDesc* fits;
   int mode;
-  int64_t count;
-  const unsigned long long* d_count;
+  int64_t count;                      // used when d_count == nullptr
+  const unsigned long long* d_count;  // device-side item count (survivors)
   int64_t capacity;
   const int64_t* ranks;
-  int64_t rank_lo;
-  int64_t rank_hi;
+  const int32_t* fit_of;
   const int64_t* ii;
   const int64_t* jj;
   const double* uu;
   const double* vv;
-  const lms_candidate* bound;  // optional: skip vertices that cannot beat bound->height
-  lms_candidate* out;
+  const lms_candidate* bound;  // optional per-fit bound (skip vertices that cannot win)
+  lms_candidate* out;          // out[s].reserved = fit id
 };
 
-void launch_exact(const ExactArgs& args, int grid, cudaStream_t stream);
-void launch_reduce(const lms_candidate* recs, const unsigned long long* d_count, int64_t count,
-                   int64_t capacity, lms_candidate* partials, int npartials,
-                   lms_candidate* best_io, cudaStream_t stream);
+// One CTA per vertex for large fits, one warp per vertex when every fit has
+// at most 4,096 lines (max_n).
+void launch_exact(const ExactArgs& args, int grid, cudaStream_t stream, int64_t max_n);
 
-// Count filter over warp tasks [task_begin, task_end).  A warp task is up to
-// kFilterTaskVertices consecutive pair ranks of one row of the triangle.
-constexpr int kFilterV = 8;                          // vertices per lane
-constexpr int kFilterTaskVertices = 32 * kFilterV;   // vertices per warp task
+// Lexicographic (height, i, j) minimum per fit (backend.py:165-167,182-187)
+// over records [0, count): CAS into keys[fit], then publish into best[fit].
+void launch_reduce(const lms_candidate* recs, const unsigned long long* d_count, int64_t count,
+                   int64_t capacity, const FitDesc* fits, BestKey* keys, lms_candidate* best,
+                   int grid, cudaStream_t stream);
+void launch_reset_best(BestKey* keys, lms_candidate* best, int64_t nfits, cudaStream_t stream);
+
+// Seeds: stratified vertex samples per fit; seed_prefix[f] = first seed of fit f.
+void launch_gen_seeds(const FitDesc* fits, const int64_t* seed_prefix, int64_t nfits,
+                      int64_t* ranks, int32_t* fit_of, cudaStream_t stream);
+
+// ---------------------------------------------------------------- filter
 constexpr int kFilterWarpsPerBlock = 8;
 
 struct FilterArgs {
   const double* a;   // lines in input order (anchors i, j)
   const double* b;
-  const double* la;  // lines in streaming order (lms_order.cu); may alias a/b
+  const double* la;  // lines in streaming order (lms_order.cu); may alias a / b
   const double* lb;
-  int64_t n;
-  int64_t q;
-  const int64_t* task_prefix;  // task_prefix[r] = first task of row row0 + r
-  int64_t row0;
-  int64_t nrows;
-  int64_t rank_lo;
-  int64_t rank_hi;
+  const FitDesc* fits;
+  const int32_t* task_row;         // global row of every warp task
+  const int64_t* row_task_prefix;  // first task of every global row
+  const int32_t* row_fit;          // fit of every global row
+  const int32_t* row_i;            // triangle row of every global row
   int64_t task_begin;
   int64_t task_end;
-  double amax;
-  double bmax;
-  const lms_candidate* best;        // current best (its height bounds the search)
-  int64_t* out_ranks;               // survivors
+  const lms_candidate* best;       // per-fit best record (its height bounds the search)
+  int64_t* out_ranks;              // survivors
+  int32_t* out_fits;
   unsigned long long* out_count;
-  unsigned long long* line_evals;   // executed vertex-line evaluations (stats)
+  unsigned long long* line_evals;  // executed vertex-line evaluations (stats)
   int early_exit;
 };
 
-void launch_filter(const FilterArgs& args, cudaStream_t stream);
+// Vertices per warp task for lanes owning V vertices each.
+inline int64_t filter_task_vertices(int v) { return 32 * (int64_t)v; }
+void launch_filter(const FilterArgs& args, int v, cudaStream_t stream);
 
-// FP32-FMA / FP16-compare / mma.sync-count variant (lms_filter32.cu).
-#ifndef LMSB_F32_TILES
-#define LMSB_F32_TILES 4
-#endif
-constexpr int kFilter32Tiles = LMSB_F32_TILES;             // 16-vertex MMA row tiles per warp
-constexpr int kFilter32TaskVertices = 16 * kFilter32Tiles; // vertices per warp task
-
-void launch_filter32(const FilterArgs& args, cudaStream_t stream);
-
-// Packed-FP16 compare / integer-mask counting variant (lms_filter32m.cu).
-#ifndef LMSB_F32M_V
-#define LMSB_F32M_V 4
-#endif
-#ifndef LMSB_F32M_MIN_BLOCKS
-#define LMSB_F32M_MIN_BLOCKS 3
-#endif
-constexpr int kFilter32mV = LMSB_F32M_V;                    // vertices per lane
-constexpr int kFilter32mMinBlocks = LMSB_F32M_MIN_BLOCKS;
-constexpr int kFilter32mTaskVertices = 32 * kFilter32mV;    // vertices per warp task
-
-void launch_filter32m(const FilterArgs& args, cudaStream_t stream);
-
-// Far-first line streaming order (lms_order.cu).
+// ---------------------------------------------------------------- line order
 struct OrderArgs {
   const double* a;
   const double* b;
-  int64_t n;
+  int64_t nlines;
+  const int64_t* seg_begin;  // per-fit line offsets (F + 1 entries)
+  int64_t nfits;
+  const int32_t* line_fit;   // fit of every line
   const lms_candidate* best;
   float* keys_in;
   float* keys_out;
@@ -108,7 +119,7 @@ struct OrderArgs {
   double* pa;
   double* pb;
 };
-size_t order_temp_bytes(int64_t n);
+size_t order_temp_bytes(int64_t nlines, int64_t nfits);
 int launch_line_order(const OrderArgs& o, cudaStream_t stream);
 
 }  // namespace lmsb

@@ -80,3 +80,44 @@ def solve_lms(points, q: int | None = None, *, backend: str = "seq", workers: in
     if rec is None:
         raise DegenerateInputError("no candidate slab found")
     return fit_from_record(x, y, q, rec)
+
+
+def solve_lms_batch(point_sets, q=None) -> list[LmsFit]:
+    """Exact LMS fits of many independent point sets in one GPU batch.
+
+    The batched form of calling :func:`solve_lms` once per set (the
+    reference's per-peak loop, detect.py:184-213): every set is validated as
+    solve_lms validates it (solver.py:67-80) and its result is identical to
+    ``solve_lms(points, q)``.  ``q`` is None (each set's default), an int
+    (the same coverage for every set) or a sequence with one entry per set.
+    """
+    from . import _native
+    from .backend import record_from_native
+
+    sets = list(point_sets)
+    if q is None or isinstance(q, (int, np.integer)):
+        qs = [q] * len(sets)
+    else:
+        qs = list(q)
+        if len(qs) != len(sets):
+            raise InvalidInputError(f"got {len(qs)} coverages for {len(sets)} point sets")
+    xs, ys, qv = [], [], []
+    for pts, qq in zip(sets, qs):
+        x, y, qq = validated(pts, qq)
+        xs.append(x)
+        ys.append(y)
+        qv.append(qq)
+    if not sets:
+        return []
+    offsets = np.zeros(len(sets) + 1, dtype=np.int64)
+    offsets[1:] = np.cumsum([x.size for x in xs])
+    X = np.concatenate(xs)
+    Y = np.concatenate(ys)
+    recs = _native.batched(X, Y, offsets, np.asarray(qv, dtype=np.int64))
+    fits = []
+    for k, c in enumerate(recs):
+        rec = record_from_native(c)
+        if rec is None:
+            raise DegenerateInputError("no candidate slab found")
+        fits.append(fit_from_record(xs[k], ys[k], qv[k], rec))
+    return fits

@@ -192,3 +192,42 @@ def test_seq_par_identical():
         for w in (1, 3, 7):
             assert lms.solve_lms(pts, backend="par", workers=w) == ref
         assert lms.solve_lms(pts, materialize=True) == ref
+
+
+def test_batched_matches_golden_and_single(golden):
+    cases, _ = golden
+    sel = [c for c in cases if c.n <= 600]
+    fits = lms.solve_lms_batch([c.points for c in sel], [c.q_arg if c.q_arg is not None else c.q for c in sel])
+    for c, fit in zip(sel, fits):
+        assert fit_matches(fit, c.fit), c.name
+
+
+def test_batched_config4_slice_vs_oracle():
+    sets = [workloads.bench_points(512, seed=f) for f in range(24)]
+    fits = lms.solve_lms_batch(sets, 257)
+    for f, (pts, fit) in enumerate(zip(sets, fits)):
+        want = oracle.solve(pts, 257, threads=THREADS)
+        assert fit.line.slope == want["slope"] and fit.line.intercept == want["intercept"], f
+        assert fit.lms_value == want["lms_value"] and tuple(fit.contact_indices) == want["contact_indices"]
+
+
+def test_batched_mixed_sizes_vs_oracle():
+    rng = np.random.default_rng(404)
+    sets, qs = [], []
+    for k in range(40):
+        n = int(rng.choice([3, 5, 17, 90, 91, 200, 700, 1500]))
+        x = rng.uniform(-50, 50, n)
+        if k % 5 == 0:
+            x[: n // 3] = x[0]
+        y = 0.5 * x + rng.normal(0, 1, n)
+        bad = rng.random(n) < 0.4
+        y[bad] = rng.uniform(-500, 500, int(bad.sum()))
+        pts = np.column_stack([x, y])
+        if np.unique(x).size < 2:
+            continue
+        sets.append(pts)
+        qs.append(int(rng.integers(2, n + 1)))
+    fits = lms.solve_lms_batch(sets, qs)
+    for pts, q, fit in zip(sets, qs, fits):
+        want = oracle.solve(pts, q, threads=THREADS)
+        assert (fit.line.slope, fit.line.intercept, fit.lms_value) == (want["slope"], want["intercept"], want["lms_value"])
