@@ -21,6 +21,9 @@
  *                             (backend.py:221-231, 321-354)
  *   lms_batched_f64           refine_lms per Hough peak (detect.py:134-153,
  *                             the per-peak loop of detect.py:184-213)
+ *   lms_hough_vote_u8         extract_points + hough_vote (hough.py:93-129)
+ *   lms_hough_vote_points     hough_vote of a point list (hough.py:112-129)
+ *   lms_hough_support         supporting_points (hough.py:171-184)
  *
  * Results are bit-identical to the reference's fp64 arithmetic: the winning
  * pair (i, j), u, v_low, v_high and height are the values the reference's
@@ -88,6 +91,32 @@ int lms_min_bracelet_f64(const double* a, const double* b, int64_t n, int64_t q,
  * minimum over all of the fit's pair ranks.  offsets[0] == 0. */
 int lms_batched_f64(const double* x, const double* y, const int64_t* offsets, const int64_t* q,
                     int64_t nfits, int device, lms_candidate* out);
+
+/* extract_points + hough_vote (hough.py:93-129): the lit pixels (value >=
+ * threshold) of the height x width uint8 image, in row-major scan order,
+ * vote once per theta bin; acc[n_rho * n_theta] (rho-major, as
+ * HoughAccumulator.bins) receives the counts, *npoints the number of lit
+ * pixels.  cos_t / sin_t are the cosines / sines of the theta bin centres
+ * (np.cos / np.sin of np.radians, as hough.py:124-125).  The lit pixels stay
+ * on the device for lms_hough_support. */
+int lms_hough_vote_u8(const uint8_t* img, int64_t height, int64_t width, int threshold,
+                      const double* cos_t, const double* sin_t, int64_t n_theta, double rho_max,
+                      double delta_rho, int64_t n_rho, int device, int64_t* acc,
+                      int64_t* npoints);
+/* hough_vote over explicit points (x[k], y[k]) (hough.py:112-129). */
+int lms_hough_vote_points(const double* x, const double* y, int64_t npts, const double* cos_t,
+                          const double* sin_t, int64_t n_theta, double rho_max, double delta_rho,
+                          int64_t n_rho, int device, int64_t* acc);
+/* supporting_points (hough.py:171-184) of the points of the last vote on
+ * `device`, for npeaks peaks: peak p's members are the points whose rho bin
+ * at (cos_p[p], sin_p[p]) (math.cos / math.sin of math.radians, as
+ * hough.py:181-183) equals rbin_p[p], in scan order, written to
+ * out[offsets[p] .. offsets[p+1]) as pixel indices (image votes) or point
+ * ordinals (point votes).  offsets has npeaks + 1 entries and is always
+ * filled; LMS_ERR_INVALID when the members exceed `capacity`. */
+int lms_hough_support(const double* cos_p, const double* sin_p, const int64_t* rbin_p,
+                      int64_t npeaks, double rho_max, double delta_rho, int64_t n_rho, int device,
+                      int64_t* offsets, int64_t* out, int64_t capacity);
 
 /* Anchored window at each explicit intersection (i[k], j[k], u[k]).  When v
  * is non-NULL the anchors are snapped to v[k] (bracelet_at); when NULL to

@@ -83,6 +83,14 @@ SIGNATURES = {
     "lms_min_bracelet_f64": (ctypes.c_int, [_D, _D, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                             ctypes.c_int64, ctypes.c_int, _C]),
     "lms_batched_f64": (ctypes.c_int, [_D, _D, _I, _I, ctypes.c_int64, ctypes.c_int, _C]),
+    "lms_hough_vote_u8": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
+                                         _D, _D, ctypes.c_int64, ctypes.c_double, ctypes.c_double,
+                                         ctypes.c_int64, ctypes.c_int, _I, _I]),
+    "lms_hough_vote_points": (ctypes.c_int, [_D, _D, ctypes.c_int64, _D, _D, ctypes.c_int64,
+                                             ctypes.c_double, ctypes.c_double, ctypes.c_int64,
+                                             ctypes.c_int, _I]),
+    "lms_hough_support": (ctypes.c_int, [_D, _D, _I, ctypes.c_int64, ctypes.c_double, ctypes.c_double,
+                                         ctypes.c_int64, ctypes.c_int, _I, _I, ctypes.c_int64]),
     "lms_eval_vertices_f64": (ctypes.c_int, [_D, _D, ctypes.c_int64, ctypes.c_int64, _I, _I, _D, _D,
                                              ctypes.c_int64, ctypes.c_int, _C]),
     "lms_min_over_vertices_f64": (ctypes.c_int, [_D, _D, ctypes.c_int64, ctypes.c_int64, _I, _I, _D,
@@ -185,6 +193,51 @@ def batched(x, y, offsets, q, device: int = 0) -> list:
     out = (Candidate * max(nf, 1))()
     check(lib.lms_batched_f64(_dp(x), _dp(y), _ip(offsets), _ip(q), nf, int(device), out))
     return [out[k] for k in range(nf)]
+
+
+def hough_vote_image(img, threshold: int, cos_t, sin_t, rho_max: float, delta_rho: float,
+                     n_rho: int, device: int = 0):
+    """lms_hough_vote_u8 -> (acc int64[n_rho, n_theta], number of lit pixels)."""
+    lib = _lib_ready()
+    img = np.ascontiguousarray(img, dtype=np.uint8)
+    h, w = img.shape
+    cos_t, sin_t = _f64(cos_t), _f64(sin_t)
+    n_theta = cos_t.size
+    acc = np.zeros((n_rho, n_theta), dtype=np.int64)
+    npts = ctypes.c_int64(0)
+    check(lib.lms_hough_vote_u8(img.ctypes.data_as(ctypes.c_void_p), h, w, int(threshold), _dp(cos_t),
+                                _dp(sin_t), n_theta, float(rho_max), float(delta_rho), int(n_rho),
+                                int(device), _ip(acc), ctypes.byref(npts)))
+    return acc, npts.value
+
+
+def hough_vote_points(x, y, cos_t, sin_t, rho_max: float, delta_rho: float, n_rho: int,
+                      device: int = 0) -> np.ndarray:
+    """lms_hough_vote_points -> acc int64[n_rho, n_theta]."""
+    lib = _lib_ready()
+    x, y, cos_t, sin_t = _f64(x), _f64(y), _f64(cos_t), _f64(sin_t)
+    n_theta = cos_t.size
+    acc = np.zeros((n_rho, n_theta), dtype=np.int64)
+    check(lib.lms_hough_vote_points(_dp(x), _dp(y), x.size, _dp(cos_t), _dp(sin_t), n_theta,
+                                    float(rho_max), float(delta_rho), int(n_rho), int(device), _ip(acc)))
+    return acc
+
+
+def hough_support(cos_p, sin_p, rbin_p, rho_max: float, delta_rho: float, n_rho: int,
+                  capacity: int, device: int = 0):
+    """lms_hough_support on the last vote's points -> (offsets[P+1], ids)."""
+    lib = _lib_ready()
+    cos_p, sin_p, rbin_p = _f64(cos_p), _f64(sin_p), _i64(rbin_p)
+    npk = cos_p.size
+    offsets = np.zeros(npk + 1, dtype=np.int64)
+    out = np.empty(max(int(capacity), 1), dtype=np.int64)
+    rc = lib.lms_hough_support(_dp(cos_p), _dp(sin_p), _ip(rbin_p), npk, float(rho_max),
+                               float(delta_rho), int(n_rho), int(device), _ip(offsets), _ip(out),
+                               int(capacity))
+    if rc == LMS_ERR_INVALID and offsets[-1] > capacity:
+        return hough_support(cos_p, sin_p, rbin_p, rho_max, delta_rho, n_rho, int(offsets[-1]), device)
+    check(rc)
+    return offsets, out[: offsets[-1]]
 
 
 def eval_vertices(a, b, q: int, i, j, u, v=None, device: int = 0):

@@ -28,6 +28,7 @@
 #include <vector>
 
 #include "lms_common.cuh"
+#include "lms_hough.cuh"
 #include "lms_kernels.cuh"
 #include "lms_plan.cuh"
 
@@ -139,6 +140,16 @@ struct lms_ctx {
   DevBuf<double> uu, vv;
   lms_candidate* h_best = nullptr;  // pinned
   int64_t cap_h_best = 0;
+  // Hough: the points of the last vote (image pixels or explicit x/y)
+  DevBuf<uint8_t> img;
+  DevBuf<int64_t> pix, pcount;
+  DevBuf<double> pxs, pys;
+  DevBuf<unsigned char> ext_tmp, scan_tmp;
+  DevBuf<unsigned long long> acc, masks;
+  DevBuf<double> tcos, tsin;
+  DevBuf<int64_t> rbin, scounts, soffsets, sout;
+  int hough_mode = 0;  // 0 none, 1 image pixels, 2 explicit points
+  int64_t hough_npts = 0, hough_width = 1;
   lms_stats stats{};
   std::mutex mu;
 };
@@ -200,6 +211,21 @@ void ctx_release(lms_ctx* c) {
   c->jj.release();
   c->uu.release();
   c->vv.release();
+  c->img.release();
+  c->pix.release();
+  c->pcount.release();
+  c->pxs.release();
+  c->pys.release();
+  c->ext_tmp.release();
+  c->scan_tmp.release();
+  c->acc.release();
+  c->masks.release();
+  c->tcos.release();
+  c->tsin.release();
+  c->rbin.release();
+  c->scounts.release();
+  c->soffsets.release();
+  c->sout.release();
   if (c->h_best) cudaFreeHost(c->h_best);
   if (c->stream) cudaStreamDestroy(c->stream);
 }
@@ -611,6 +637,154 @@ int ctx_eval_explicit(lms_ctx* c, int64_t q, const int64_t* i, const int64_t* j,
   return LMS_OK;
 }
 
+
+// ---------------------------------------------------------------- Hough
+
+int check_hough(int64_t n_theta, double rho_max, double drho, int64_t n_rho) {
+  if (n_theta < 1 || n_rho < 1 || !(drho > 0.0) || !(rho_max > 0.0))
+    return set_error(LMS_ERR_INVALID, "Hough bin widths and rho range must be positive");
+  if (n_theta * n_rho > (int64_t)1 << 31)
+    return set_error(LMS_ERR_INVALID, "Hough accumulator too large");
+  return LMS_OK;
+}
+
+int ctx_vote(lms_ctx* c, const double* cos_t, const double* sin_t, int64_t n_theta,
+             double rho_max, double drho, int64_t n_rho, int64_t* acc_out) {
+  const int64_t nb = n_theta * n_rho;
+  RC_TRY(c->acc.need(nb));
+  RC_TRY(c->tcos.need(n_theta));
+  RC_TRY(c->tsin.need(n_theta));
+  CUDA_TRY(cudaMemcpyAsync(c->tcos.p, cos_t, sizeof(double) * n_theta, cudaMemcpyHostToDevice,
+                           c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->tsin.p, sin_t, sizeof(double) * n_theta, cudaMemcpyHostToDevice,
+                           c->stream));
+  CUDA_TRY(cudaMemsetAsync(c->acc.p, 0, sizeof(unsigned long long) * nb, c->stream));
+  if (c->hough_npts > 0)
+    lmsb::hough_vote(c->hough_mode == 1 ? c->pix.p : nullptr, c->hough_mode == 2 ? c->pxs.p : nullptr,
+                     c->hough_mode == 2 ? c->pys.p : nullptr, c->hough_npts, c->hough_width,
+                     c->tcos.p, c->tsin.p, (int)n_theta, rho_max, drho, n_rho, c->acc.p, c->sms,
+                     c->stream);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpyAsync(acc_out, c->acc.p, sizeof(int64_t) * nb, cudaMemcpyDeviceToHost,
+                           c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return LMS_OK;
+}
+
+int ctx_vote_image(lms_ctx* c, const uint8_t* img, int64_t height, int64_t width, int threshold,
+                   const double* cos_t, const double* sin_t, int64_t n_theta, double rho_max,
+                   double drho, int64_t n_rho, int64_t* acc_out, int64_t* npoints) {
+  if (!img || height < 0 || width < 0) return set_error(LMS_ERR_INVALID, "bad image");
+  RC_TRY(check_hough(n_theta, rho_max, drho, n_rho));
+  CUDA_TRY(cudaSetDevice(c->device));
+  const int64_t npix = height * width;
+  RC_TRY(c->img.need(std::max<int64_t>(npix, 1)));
+  RC_TRY(c->pix.need(std::max<int64_t>(npix, 1)));
+  RC_TRY(c->pcount.need(1));
+  RC_TRY(c->ext_tmp.need((int64_t)lmsb::extract_temp_bytes(std::max<int64_t>(npix, 1))));
+  int64_t npts = 0;
+  if (npix > 0) {
+    CUDA_TRY(cudaMemcpyAsync(c->img.p, img, npix, cudaMemcpyHostToDevice, c->stream));
+    size_t tb = (size_t)c->ext_tmp.cap;
+    if (lmsb::hough_extract(c->img.p, npix, threshold, c->pix.p, c->pcount.p, c->ext_tmp.p, &tb,
+                            c->stream) != 0)
+      return set_error(LMS_ERR_CUDA, "pixel compaction failed");
+    CUDA_TRY(cudaMemcpyAsync(&npts, c->pcount.p, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                             c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+  }
+  c->hough_mode = 1;
+  c->hough_npts = npts;
+  c->hough_width = std::max<int64_t>(width, 1);
+  *npoints = npts;
+  return ctx_vote(c, cos_t, sin_t, n_theta, rho_max, drho, n_rho, acc_out);
+}
+
+int ctx_vote_points(lms_ctx* c, const double* x, const double* y, int64_t npts,
+                    const double* cos_t, const double* sin_t, int64_t n_theta, double rho_max,
+                    double drho, int64_t n_rho, int64_t* acc_out) {
+  if (npts < 0 || (npts > 0 && (!x || !y))) return set_error(LMS_ERR_INVALID, "bad points");
+  RC_TRY(check_hough(n_theta, rho_max, drho, n_rho));
+  CUDA_TRY(cudaSetDevice(c->device));
+  RC_TRY(c->pxs.need(std::max<int64_t>(npts, 1)));
+  RC_TRY(c->pys.need(std::max<int64_t>(npts, 1)));
+  if (npts > 0) {
+    CUDA_TRY(cudaMemcpyAsync(c->pxs.p, x, sizeof(double) * npts, cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(c->pys.p, y, sizeof(double) * npts, cudaMemcpyHostToDevice, c->stream));
+  }
+  c->hough_mode = 2;
+  c->hough_npts = npts;
+  c->hough_width = 1;
+  return ctx_vote(c, cos_t, sin_t, n_theta, rho_max, drho, n_rho, acc_out);
+}
+
+int ctx_support(lms_ctx* c, const double* cos_p, const double* sin_p, const int64_t* rbin_p,
+                int64_t npeaks, double rho_max, double drho, int64_t n_rho, int64_t* offsets,
+                int64_t* out, int64_t capacity) {
+  if (npeaks < 0 || !offsets || (npeaks > 0 && (!cos_p || !sin_p || !rbin_p)))
+    return set_error(LMS_ERR_INVALID, "bad peaks");
+  if (c->hough_mode == 0) return set_error(LMS_ERR_INVALID, "no points: call a vote first");
+  RC_TRY(check_hough(1, rho_max, drho, n_rho));
+  CUDA_TRY(cudaSetDevice(c->device));
+  const int64_t npts = c->hough_npts;
+  const int64_t nb = lmsb::support_blocks(npts);
+  offsets[0] = 0;
+  if (npts == 0 || npeaks == 0) {
+    for (int64_t p = 0; p < npeaks; ++p) offsets[p + 1] = 0;
+    return LMS_OK;
+  }
+  RC_TRY(c->masks.need(npts));
+  RC_TRY(c->scounts.need(64 * nb + 1));
+  RC_TRY(c->soffsets.need(64 * nb + 1));
+  RC_TRY(c->rbin.need(64));
+  RC_TRY(c->tcos.need(64));
+  RC_TRY(c->tsin.need(64));
+  RC_TRY(c->scan_tmp.need((int64_t)lmsb::support_scan_temp_bytes(64 * nb + 1)));
+  std::vector<int64_t> goff(64 * nb + 1);
+  int64_t total = 0;
+  for (int64_t g0 = 0; g0 < npeaks; g0 += 64) {
+    const int np = (int)std::min<int64_t>(64, npeaks - g0);
+    CUDA_TRY(cudaMemcpyAsync(c->tcos.p, cos_p + g0, sizeof(double) * np, cudaMemcpyHostToDevice,
+                             c->stream));
+    CUDA_TRY(cudaMemcpyAsync(c->tsin.p, sin_p + g0, sizeof(double) * np, cudaMemcpyHostToDevice,
+                             c->stream));
+    CUDA_TRY(cudaMemcpyAsync(c->rbin.p, rbin_p + g0, sizeof(int64_t) * np, cudaMemcpyHostToDevice,
+                             c->stream));
+    CUDA_TRY(cudaMemsetAsync(c->scounts.p, 0, sizeof(int64_t) * (np * nb + 1), c->stream));
+    RC_TRY(c->sout.need(std::max<int64_t>(1, capacity - total)));
+    // pass 1 + scan + pass 2 into a device buffer sized by the caller's
+    // capacity; rerun once with a grown buffer if the members did not fit
+    const int64_t m = (int64_t)np * nb + 1;
+    int64_t group_total = 0;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      if (lmsb::hough_support(c->hough_mode == 1 ? c->pix.p : nullptr,
+                              c->hough_mode == 2 ? c->pxs.p : nullptr,
+                              c->hough_mode == 2 ? c->pys.p : nullptr, npts, c->hough_width,
+                              c->tcos.p, c->tsin.p, c->rbin.p, np, rho_max, drho, n_rho,
+                              c->masks.p, c->scounts.p, c->soffsets.p, c->scan_tmp.p,
+                              (size_t)c->scan_tmp.cap, c->sout.p, c->stream) != 0)
+        return set_error(LMS_ERR_CUDA, "support scan failed");
+      CUDA_TRY(cudaGetLastError());
+      CUDA_TRY(cudaMemcpyAsync(goff.data(), c->soffsets.p, sizeof(int64_t) * m,
+                               cudaMemcpyDeviceToHost, c->stream));
+      CUDA_TRY(cudaStreamSynchronize(c->stream));
+      group_total = goff[m - 1];
+      if (group_total <= c->sout.cap) break;
+      RC_TRY(c->sout.need(group_total));  // grown: write again
+    }
+    for (int q = 0; q < np; ++q) offsets[g0 + q + 1] = total + goff[(int64_t)(q + 1) * nb];
+    if (out && total + group_total <= capacity && group_total > 0)
+      CUDA_TRY(cudaMemcpyAsync(out + total, c->sout.p, sizeof(int64_t) * group_total,
+                               cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    total += group_total;
+  }
+  if (total > capacity)
+    return set_error(LMS_ERR_INVALID, "support output capacity %lld < %lld members",
+                     (long long)capacity, (long long)total);
+  return LMS_OK;
+}
+
 // One cached context per device for the one-shot entry points.
 std::mutex g_ctx_mu;
 std::vector<lms_ctx*> g_ctx;
@@ -677,6 +851,38 @@ int lms_batched_f64(const double* x, const double* y, const int64_t* offsets, co
   std::lock_guard<std::mutex> lk(c->mu);
   RC_TRY(ctx_upload(c, x, y, offsets[nfits]));
   return ctx_solve_batch(c, offsets, q, nfits, out);
+}
+
+int lms_hough_vote_u8(const uint8_t* img, int64_t height, int64_t width, int threshold,
+                      const double* cos_t, const double* sin_t, int64_t n_theta, double rho_max,
+                      double delta_rho, int64_t n_rho, int device, int64_t* acc,
+                      int64_t* npoints) {
+  if (!acc || !npoints || !cos_t || !sin_t) return set_error(LMS_ERR_INVALID, "null argument");
+  lms_ctx* c = nullptr;
+  RC_TRY(shared_ctx(device, &c));
+  std::lock_guard<std::mutex> lk(c->mu);
+  return ctx_vote_image(c, img, height, width, threshold, cos_t, sin_t, n_theta, rho_max,
+                        delta_rho, n_rho, acc, npoints);
+}
+
+int lms_hough_vote_points(const double* x, const double* y, int64_t npts, const double* cos_t,
+                          const double* sin_t, int64_t n_theta, double rho_max, double delta_rho,
+                          int64_t n_rho, int device, int64_t* acc) {
+  if (!acc || !cos_t || !sin_t) return set_error(LMS_ERR_INVALID, "null argument");
+  lms_ctx* c = nullptr;
+  RC_TRY(shared_ctx(device, &c));
+  std::lock_guard<std::mutex> lk(c->mu);
+  return ctx_vote_points(c, x, y, npts, cos_t, sin_t, n_theta, rho_max, delta_rho, n_rho, acc);
+}
+
+int lms_hough_support(const double* cos_p, const double* sin_p, const int64_t* rbin_p,
+                      int64_t npeaks, double rho_max, double delta_rho, int64_t n_rho, int device,
+                      int64_t* offsets, int64_t* out, int64_t capacity) {
+  lms_ctx* c = nullptr;
+  RC_TRY(shared_ctx(device, &c));
+  std::lock_guard<std::mutex> lk(c->mu);
+  return ctx_support(c, cos_p, sin_p, rbin_p, npeaks, rho_max, delta_rho, n_rho, offsets, out,
+                     capacity);
 }
 
 int lms_eval_vertices_f64(const double* a, const double* b, int64_t n, int64_t q, const int64_t* i,

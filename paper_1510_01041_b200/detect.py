@@ -1,0 +1,244 @@
+"""Line detection: Hough peaks refined by LMS (drop-in for lmsline.detect).
+
+``detect_lines`` keeps the reference's signature, methods and result type
+(detect.py:156-214) but runs as one device pipeline: the image is uploaded
+once, lit pixels are compacted and vote on the GPU, the (small) accumulator
+comes back for ``find_peaks``, every peak's support is gathered on the GPU
+in scan order, and all peaks' LMS refits run as ONE batched exact solve
+(``solve_lms_batch``) instead of the reference's per-peak Python loop.
+Supports are returned as :class:`SupportPoints`, a lazy, tuple-comparable
+sequence of ``Point2`` backed by the pixel indices (the reference's
+``tuple[Point2, ...]`` of ~30k objects per peak costs seconds to build).
+"""
+
+from __future__ import annotations
+
+import math
+from collections.abc import Sequence
+from dataclasses import dataclass
+
+import numpy as np
+
+from .geometry import DegenerateInputError, InvalidInputError, LineEq, Point2
+from .hough import (
+    HoughAccumulator,
+    HoughParams,
+    find_peaks,
+    line_to_polar,
+    lit_mask_u8,
+    needs_axis_swap,
+    polar_to_frame_fit,
+)
+from .solver import LmsFit, solve_lms, solve_lms_batch
+
+METHOD_SHT = "sht"
+METHOD_OLS = "ols"
+METHOD_LMS = "lms"
+METHODS = (METHOD_SHT, METHOD_OLS, METHOD_LMS)
+
+DEFAULT_THRESHOLD = 128
+DEFAULT_MIN_VOTES = 2
+
+LMS_SUPPORT_CAP = 256
+"""Support subsample size for the LMS refit (detect.py:43)."""
+
+
+class SupportPoints(Sequence):
+    """Lazy ``Point2`` sequence of one peak's support, in scan order.
+
+    Compares equal to any sequence with the same points (so to the
+    reference's tuples) and hashes like the equivalent tuple.
+    """
+
+    __slots__ = ("_x", "_y")
+
+    def __init__(self, x: np.ndarray, y: np.ndarray):
+        self._x = np.asarray(x, dtype=float)
+        self._y = np.asarray(y, dtype=float)
+
+    @classmethod
+    def from_pixels(cls, ids: np.ndarray, width: int) -> "SupportPoints":
+        ids = np.asarray(ids, dtype=np.int64)
+        return cls((ids % width).astype(float), (ids // width).astype(float))
+
+    @property
+    def xy(self) -> tuple[np.ndarray, np.ndarray]:
+        return self._x, self._y
+
+    def __len__(self) -> int:
+        return int(self._x.size)
+
+    def __getitem__(self, k):
+        if isinstance(k, slice):
+            return SupportPoints(self._x[k], self._y[k])
+        return Point2(float(self._x[k]), float(self._y[k]))
+
+    def __iter__(self):
+        for x, y in zip(self._x.tolist(), self._y.tolist()):
+            yield Point2(x, y)
+
+    def __eq__(self, other) -> bool:
+        if isinstance(other, SupportPoints):
+            return np.array_equal(self._x, other._x) and np.array_equal(self._y, other._y)
+        if isinstance(other, Sequence) and not isinstance(other, (str, bytes)):
+            return len(other) == len(self) and all(a == b for a, b in zip(self, other))
+        return NotImplemented
+
+    def __hash__(self) -> int:
+        return hash(tuple(self))
+
+    def __repr__(self) -> str:
+        return f"SupportPoints({len(self)} points)"
+
+
+@dataclass(frozen=True)
+class LineDetection:
+    """One detected line (detect.py:52-88)."""
+
+    method: str
+    rho: float
+    theta: float
+    slope: float
+    intercept: float
+    axis_swapped: bool
+    support: Sequence
+    lms_value: float | None = None
+
+    @property
+    def image_slope(self) -> float:
+        if not self.axis_swapped:
+            return self.slope
+        if self.slope == 0.0:
+            return math.inf
+        return 1.0 / self.slope
+
+    @property
+    def image_intercept(self) -> float:
+        if not self.axis_swapped:
+            return self.intercept
+        if self.slope == 0.0:
+            return math.nan
+        return -self.intercept / self.slope
+
+
+def _support_xy(support) -> tuple[np.ndarray, np.ndarray]:
+    if isinstance(support, SupportPoints):
+        return support.xy
+    pts = list(support)
+    x = np.fromiter((p.x for p in pts), dtype=float, count=len(pts))
+    y = np.fromiter((p.y for p in pts), dtype=float, count=len(pts))
+    return x, y
+
+
+def _design_xy(x: np.ndarray, y: np.ndarray, axis_swapped: bool) -> tuple[np.ndarray, np.ndarray]:
+    return (y, x) if axis_swapped else (x, y)
+
+
+def refine_ols(support, axis_swapped: bool = False) -> LineEq:
+    """Closed-form least squares in the given frame (detect.py:98-115)."""
+    t, z = _design_xy(*_support_xy(support), axis_swapped)
+    if t.size < 2:
+        raise DegenerateInputError(f"least squares needs at least 2 points, got {t.size}")
+    if not (np.isfinite(t).all() and np.isfinite(z).all()):
+        raise InvalidInputError("support coordinates must be finite")
+    t_mean = t.mean()
+    z_mean = z.mean()
+    dt = t - t_mean
+    denom = float(dt @ dt)
+    if denom == 0.0:
+        raise DegenerateInputError("support is constant along the regression axis")
+    slope = float(dt @ (z - z_mean)) / denom
+    return LineEq(slope=slope, intercept=float(z_mean - slope * t_mean))
+
+
+def _subsample_index(m: int, cap: int) -> np.ndarray:
+    return (np.arange(cap, dtype=np.int64) * m) // cap
+
+
+def subsample_support(support, cap: int):
+    """Even-stride thinning to at most ``cap`` points, scan order kept
+    (detect.py:118-131)."""
+    pts = list(support)
+    if cap < 3:
+        raise InvalidInputError(f"support cap must be at least 3, got {cap}")
+    m = len(pts)
+    if m <= cap:
+        return pts
+    return [pts[int(k)] for k in _subsample_index(m, cap)]
+
+
+def _thinned_xy(support, cap: int | None) -> tuple[np.ndarray, np.ndarray]:
+    x, y = _support_xy(support)
+    if cap is not None:
+        if cap < 3:
+            raise InvalidInputError(f"support cap must be at least 3, got {cap}")
+        if x.size > cap:
+            idx = _subsample_index(x.size, cap)
+            x, y = x[idx], y[idx]
+    return x, y
+
+
+def refine_lms(support, q: int | None = None, axis_swapped: bool = False, *, backend: str = "seq",
+               workers: int | None = None, support_cap: int | None = None) -> LmsFit:
+    """Exact LMS line through the (optionally thinned) support in the given
+    frame (detect.py:134-153)."""
+    t, z = _design_xy(*_thinned_xy(support, support_cap), axis_swapped)
+    return solve_lms(np.column_stack([t, z]), q, backend=backend, workers=workers)
+
+
+def detect_lines(image: np.ndarray, params: HoughParams, method: str = METHOD_LMS, max_peaks: int = 1,
+                 *, threshold: int = DEFAULT_THRESHOLD, min_votes: int = DEFAULT_MIN_VOTES,
+                 q: int | None = None, backend: str = "seq", workers: int | None = None,
+                 support_cap: int | None = LMS_SUPPORT_CAP) -> list[LineDetection]:
+    """Detect up to ``max_peaks`` lines (detect.py:156-214) on the GPU."""
+    from . import _native
+    from .backend import get_backend
+
+    if method not in METHODS:
+        raise InvalidInputError(f"unknown method {method!r}; expected one of {METHODS}")
+    img, thr = lit_mask_u8(image, threshold)
+    c, s = params.vote_trig()
+    bins, npoints = _native.hough_vote_image(img, thr, c, s, params.rho_max, params.delta_rho,
+                                             params.n_rho)
+    if npoints == 0:
+        return []
+    peaks = find_peaks(HoughAccumulator(bins=bins, params=params), max_peaks, min_votes)
+    if not peaks:
+        return []
+    trig = [params.support_trig(p.theta_bin) for p in peaks]
+    offsets, ids = _native.hough_support([t[0] for t in trig], [t[1] for t in trig],
+                                         [p.rho_bin for p in peaks], params.rho_max,
+                                         params.delta_rho, params.n_rho,
+                                         capacity=sum(p.votes for p in peaks))
+    width = img.shape[1]
+    supports = [SupportPoints.from_pixels(ids[offsets[k]: offsets[k + 1]], width)
+                for k in range(len(peaks))]
+    swapped = [needs_axis_swap(p.theta) for p in peaks]
+
+    lms_fits: list[LmsFit] = []
+    if method == METHOD_LMS:
+        get_backend(backend, workers)  # same name / worker validation as solve_lms
+        designs = []
+        for sup, sw in zip(supports, swapped):
+            t, z = _design_xy(*_thinned_xy(sup, support_cap), sw)
+            designs.append(np.column_stack([t, z]))
+        lms_fits = solve_lms_batch(designs, q)
+
+    out: list[LineDetection] = []
+    for k, (peak, sup, sw) in enumerate(zip(peaks, supports, swapped)):
+        lms_value = None
+        if method == METHOD_SHT:
+            rho, theta = peak.rho, peak.theta
+            slope, intercept, sw = polar_to_frame_fit(rho, theta)
+        elif method == METHOD_OLS:
+            fit = refine_ols(sup, sw)
+            slope, intercept = fit.slope, fit.intercept
+            rho, theta = line_to_polar(slope, intercept, sw)
+        else:
+            fit = lms_fits[k]
+            slope, intercept = fit.line.slope, fit.line.intercept
+            lms_value = fit.lms_value
+            rho, theta = line_to_polar(slope, intercept, sw)
+        out.append(LineDetection(method=method, rho=rho, theta=theta, slope=slope, intercept=intercept,
+                                 axis_swapped=sw, support=sup, lms_value=lms_value))
+    return out

@@ -55,3 +55,34 @@ def bench_points(n: int, seed: int = 7) -> np.ndarray:
     bad = rng.random(n) < 0.3
     y[bad] = rng.uniform(0.0, 1000.0, int(bad.sum()))
     return np.column_stack([x, y])
+
+
+def line_image(width: int = 4096, height: int = 4096, lines: int = 64, salt: float = 0.30,
+               sampling: float = 0.5, seed: int = 0) -> np.ndarray:
+    """Config 5 input: a uint8 image (0 / 255) with ``lines`` random lines
+    (normal angle in [20, 160) degrees, passing within width/4 of the
+    centre, pixels kept with probability ``sampling``) plus salt noise.
+
+    Stands in for the reference's gen_synthetic + np.maximum composition
+    (synth.py:132-191, test_detect.py:246-257); the exact raster differs, the
+    workload shape (4096^2 pixels, ~5.1 M lit points at 30% salt) does not.
+    """
+    rng = np.random.Generator(np.random.PCG64(np.random.SeedSequence([seed, 0])))
+    img = np.zeros((height, width), dtype=np.uint8)
+    cx, cy = width / 2.0, height / 2.0
+    for _ in range(lines):
+        th = np.radians(rng.uniform(20.0, 160.0))
+        off = rng.uniform(-width / 4.0, width / 4.0)
+        # normal form x cos th + y sin th = rho through a point near the centre
+        px, py = cx + off * np.cos(th), cy + off * np.sin(th)
+        dx, dy = -np.sin(th), np.cos(th)  # direction along the line
+        t = np.arange(-2.0 * max(width, height), 2.0 * max(width, height), 0.5)
+        xs = np.rint(px + t * dx).astype(np.int64)
+        ys = np.rint(py + t * dy).astype(np.int64)
+        ok = (xs >= 0) & (xs < width) & (ys >= 0) & (ys < height)
+        xs, ys = xs[ok], ys[ok]
+        keep = rng.random(xs.size) < sampling
+        img[ys[keep], xs[keep]] = 255
+    noise = np.random.Generator(np.random.PCG64(np.random.SeedSequence([seed, 1])))
+    img[noise.random((height, width)) < salt] = 255
+    return img

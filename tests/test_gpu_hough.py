@@ -1,0 +1,104 @@
+"""GPU Hough vote / support / detect_lines against the reference's golden
+vectors and, at config-5 scale, against the numpy oracle."""
+
+import math
+
+import numpy as np
+import pytest
+
+from oracle import hough_oracle
+import paper_1510_01041_b200 as lms
+from paper_1510_01041_b200 import _native, workloads
+from test_oracle_hough import f, image_of, load, params_of
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def cases():
+    assert _native.device_count() > 0
+    return load()
+
+
+def test_vote_points_and_support_match_reference(cases):
+    for c in cases:
+        p = params_of(c)
+        pts = lms.extract_points(image_of(c))
+        acc = lms.hough_vote(pts, p)
+        want = np.zeros((p.n_rho, p.n_theta), dtype=np.int64)
+        for r, t, v in c["bins"]:
+            want[r, t] = v
+        assert np.array_equal(acc.bins, want), c["name"]
+        peaks = lms.find_peaks(acc, c["max_peaks"], c["min_votes"])
+        for pk, sup in zip(peaks, c["supports"]):
+            got = lms.supporting_points(pts, pk, p)
+            assert got == [pts[k] for k in sup], c["name"]
+
+
+def test_detect_lines_matches_reference(cases):
+    for c in cases:
+        p = params_of(c)
+        img = image_of(c)
+        for method in ("lms", "ols", "sht"):
+            want = c["detect"][method]
+            if isinstance(want, dict):
+                with pytest.raises(ValueError):
+                    lms.detect_lines(img, p, method, c["max_peaks"], min_votes=c["min_votes"], q=c["q"],
+                                     support_cap=c["support_cap"])
+                continue
+            got = lms.detect_lines(img, p, method, c["max_peaks"], min_votes=c["min_votes"], q=c["q"],
+                                   support_cap=c["support_cap"])
+            assert len(got) == len(want), (c["name"], method)
+            pts = lms.extract_points(img)
+            for d, w, sup in zip(got, want, c["supports"]):
+                assert (d.rho, d.theta, d.slope, d.intercept) == (f(w["rho"]), f(w["theta"]), f(w["slope"]),
+                                                                  f(w["intercept"])), (c["name"], method)
+                assert d.axis_swapped == w["axis_swapped"]
+                assert d.lms_value == f(w["lms_value"])
+                assert len(d.support) == w["support_len"]
+                assert d.support == tuple(pts[k] for k in sup)
+
+
+def test_refine_lms_with_cap_matches_reference(cases):
+    for c in cases:
+        p = params_of(c)
+        pts = lms.extract_points(image_of(c))
+        for pk, sup, want in zip(c["peaks"], c["supports"], c["refits"]):
+            if want is None or "error" in want:
+                continue
+            fit = lms.refine_lms([pts[k] for k in sup], None, lms.needs_axis_swap(f(pk[4])), support_cap=64)
+            assert (fit.line.slope, fit.line.intercept, fit.lms_value) == \
+                (f(want["slope"]), f(want["intercept"]), f(want["lms_value"]))
+
+
+def test_config5_scale_vote_and_support_vs_oracle():
+    img = workloads.line_image(2048, 2048, lines=24, salt=0.10, seed=5)
+    p = lms.HoughParams.for_image(2048, 2048, 20.0, 20.0)
+    c, s = p.vote_trig()
+    bins, npts = _native.hough_vote_image(img, 128, c, s, p.rho_max, p.delta_rho, p.n_rho)
+    lit = np.flatnonzero(img >= 128)
+    assert npts == lit.size
+    x = (lit % 2048).astype(float)
+    y = (lit // 2048).astype(float)
+    want = hough_oracle.vote(x, y, p.delta_rho, p.delta_theta, p.rho_max)
+    assert np.array_equal(bins, want)
+    peaks = lms.find_peaks(lms.HoughAccumulator(bins=bins, params=p), 70, 2)
+    trig = [p.support_trig(k.theta_bin) for k in peaks]
+    offsets, ids = _native.hough_support([t[0] for t in trig], [t[1] for t in trig],
+                                         [k.rho_bin for k in peaks], p.rho_max, p.delta_rho, p.n_rho,
+                                         capacity=10)  # forces the grow-and-retry path
+    for q, k in enumerate(peaks[:12]):
+        ords = hough_oracle.support(x, y, k.theta_bin, k.rho_bin, p.delta_rho, p.delta_theta, p.rho_max)
+        assert np.array_equal(ids[offsets[q]:offsets[q + 1]], lit[ords])
+    assert all(offsets[q + 1] - offsets[q] == k.votes for q, k in enumerate(peaks))
+
+
+def test_detect_lines_deterministic_and_batched_equals_single():
+    img = workloads.line_image(1024, 1024, lines=6, salt=0.02, seed=9)
+    p = lms.HoughParams.for_image(1024, 1024, 20.0, 10.0)
+    a = lms.detect_lines(img, p, "lms", 6)
+    b = lms.detect_lines(img, p, "lms", 6, backend="par", workers=3)
+    assert a == b
+    for d in a:
+        fit = lms.refine_lms(d.support, None, d.axis_swapped, support_cap=256)
+        assert (fit.line.slope, fit.line.intercept, fit.lms_value) == (d.slope, d.intercept, d.lms_value)
