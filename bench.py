@@ -45,6 +45,7 @@ def parse():
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--cpu-vertices-per-thread", type=int, default=3000)
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-extra", action="store_true", help="skip the configs 1/4/5 side measurements")
     return p.parse_args()
 
 
@@ -193,6 +194,59 @@ def run_reference(args):
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+# --------------------------------------------------------------------------- configs 1, 4, 5
+def other_configs(device: int, reps: int = 3) -> dict:
+    """Device / end-to-end times of BASELINE.json configs 1, 4 and 5 (median
+    of `reps` after one warm-up), reported beside the headline config 2."""
+    import paper_1510_01041_b200 as lms
+    from paper_1510_01041_b200 import _native, workloads
+
+    res = {}
+    ctx = _native.Context(device)
+
+    def timed(fn):
+        fn()
+        ms = []
+        for _ in range(reps):
+            ctx.record(2)
+            fn()
+            ctx.record(3)
+            ms.append(ctx.elapsed_ms(2, 3))
+        return statistics.median(ms)
+
+    # config 1: n = 1000, exact inliers on y = 2x + 1, 45% outliers, q = 501
+    pts = workloads.config1_points(0)
+    ctx.upload(pts[:, 0], pts[:, 1])
+    ms = timed(lambda: ctx.solve(501, 0, 1000 * 999 // 2))
+    res["config1"] = {"workload": "n=1000, 45% outliers, q=501", "ms_per_fit": ms,
+                      "evals_per_s": 1000 * 499500 / (ms / 1e3)}
+    # config 4: 8,192 fits of bench_points(512) (experiments.py:247-254)
+    F, m = 8192, 512
+    sets = [workloads.bench_points(m, seed=f) for f in range(F)]
+    X = np.concatenate([t[:, 0] for t in sets])
+    Y = np.concatenate([t[:, 1] for t in sets])
+    offs = np.arange(F + 1, dtype=np.int64) * m
+    qs = np.full(F, m // 2 + 1, dtype=np.int64)
+    ctx.upload(X, Y)
+    ms = timed(lambda: ctx.solve_batch(offs, qs))
+    res["config4"] = {"workload": "8192 fits x n=512 (bench_points), q=257", "ms_per_batch": ms,
+                      "evals_per_s": F * m * (m * (m - 1) // 2) / (ms / 1e3)}
+    # config 5: detect_lines end to end (host image in, LineDetections out)
+    img = workloads.line_image(4096, 4096, 64, 0.30, seed=0)
+    params = lms.HoughParams.for_image(4096, 4096, 20.0, 20.0)
+    lms.detect_lines(img, params, "lms", 64)
+    walls = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        dets = lms.detect_lines(img, params, "lms", 64)
+        walls.append(time.perf_counter() - t0)
+    res["config5"] = {"workload": "detect_lines, 4096^2 image, 64 lines, 30% salt, 64 peaks, cap 256",
+                      "e2e_ms": 1e3 * statistics.median(walls), "peaks": len(dets),
+                      "lit_points": int((img >= 128).sum())}
+    ctx.close()
+    return res
 
 
 # --------------------------------------------------------------------------- ours
@@ -352,6 +406,8 @@ def run_ours(args):
             "survivors_per_step": survivors / args.steps,
             "result": {"i": best.i, "j": best.j, "height": best.height, "u": best.u},
         }
+        if world == 1 and not args.no_extra:
+            out["other_configs"] = other_configs(local)
         if world == 1 and not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(a, b, q, n, args.cpu_vertices_per_thread)
         print(json.dumps(out), flush=True)

@@ -21,6 +21,7 @@
  *                             (backend.py:221-231, 321-354)
  *   lms_batched_f64           refine_lms per Hough peak (detect.py:134-153,
  *                             the per-peak loop of detect.py:184-213)
+ *   lms_primal_brute_f64      oracle_lms, the primal brute force (solver.py:143-196)
  *   lms_hough_vote_u8         extract_points + hough_vote (hough.py:93-129)
  *   lms_hough_vote_points     hough_vote of a point list (hough.py:112-129)
  *   lms_hough_support         supporting_points (hough.py:171-184)
@@ -91,6 +92,13 @@ int lms_min_bracelet_f64(const double* a, const double* b, int64_t n, int64_t q,
  * minimum over all of the fit's pair ranks.  offsets[0] == 0. */
 int lms_batched_f64(const double* x, const double* y, const int64_t* offsets, const int64_t* q,
                     int64_t nfits, int device, lms_candidate* out);
+
+/* oracle_lms (solver.py:143-196), the reference's independent primal brute
+ * force: per pair slope, sorted intercepts, narrowest q-window (first
+ * minimal); lexicographic (span, i, j) minimum.  out->height = span,
+ * out->u = slope, out->v_low / v_high = the window's intercepts.  n <= 16384. */
+int lms_primal_brute_f64(const double* x, const double* y, int64_t n, int64_t q, int device,
+                         lms_candidate* out);
 
 /* extract_points + hough_vote (hough.py:93-129): the lit pixels (value >=
  * threshold) of the height x width uint8 image, in row-major scan order,

@@ -83,6 +83,7 @@ SIGNATURES = {
     "lms_min_bracelet_f64": (ctypes.c_int, [_D, _D, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                             ctypes.c_int64, ctypes.c_int, _C]),
     "lms_batched_f64": (ctypes.c_int, [_D, _D, _I, _I, ctypes.c_int64, ctypes.c_int, _C]),
+    "lms_primal_brute_f64": (ctypes.c_int, [_D, _D, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, _C]),
     "lms_hough_vote_u8": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
                                          _D, _D, ctypes.c_int64, ctypes.c_double, ctypes.c_double,
                                          ctypes.c_int64, ctypes.c_int, _I, _I]),
@@ -193,6 +194,15 @@ def batched(x, y, offsets, q, device: int = 0) -> list:
     out = (Candidate * max(nf, 1))()
     check(lib.lms_batched_f64(_dp(x), _dp(y), _ip(offsets), _ip(q), nf, int(device), out))
     return [out[k] for k in range(nf)]
+
+
+def primal_brute(x, y, q: int, device: int = 0) -> Candidate:
+    """lms_primal_brute_f64 (oracle_lms, solver.py:143-196)."""
+    lib = _lib_ready()
+    x, y = _f64(x), _f64(y)
+    out = Candidate()
+    check(lib.lms_primal_brute_f64(_dp(x), _dp(y), x.size, int(q), int(device), ctypes.byref(out)))
+    return out
 
 
 def hough_vote_image(img, threshold: int, cos_t, sin_t, rho_max: float, delta_rho: float,

@@ -31,6 +31,7 @@
 #include "lms_hough.cuh"
 #include "lms_kernels.cuh"
 #include "lms_plan.cuh"
+#include "lms_primal.cuh"
 
 #define LMS_VERSION 2
 
@@ -638,6 +639,38 @@ int ctx_eval_explicit(lms_ctx* c, int64_t q, const int64_t* i, const int64_t* j,
 }
 
 
+// ---------------------------------------------------------------- primal brute force
+
+int ctx_primal(lms_ctx* c, int64_t q, lms_candidate* out) {
+  std::memset(out, 0, sizeof(*out));
+  const int64_t n = c->nlines;
+  RC_TRY(check_fit(c, 0, n, q));
+  if (n > lmsb::kPrimalMaxN)
+    return set_error(LMS_ERR_INVALID, "the primal brute force is limited to n <= %lld, got %lld",
+                     (long long)lmsb::kPrimalMaxN, (long long)n);
+  CUDA_TRY(cudaSetDevice(c->device));
+  const int64_t P = n * (n - 1) / 2;
+  RC_TRY(c->recs.need(P));
+  RC_TRY(c->fits.need(1));
+  RC_TRY(c->keys.need(1));
+  RC_TRY(c->best.need(1));
+  lmsb::FitDesc fd{};
+  fd.n = n;
+  fd.q = q;
+  CUDA_TRY(cudaMemcpyAsync(c->fits.p, &fd, sizeof(fd), cudaMemcpyHostToDevice, c->stream));
+  if (lmsb::launch_primal(c->a, c->b, n, q, c->recs.p, persistent_grid(c, P), c->stream) != 0)
+    return set_error(LMS_ERR_CUDA, "primal kernel shared memory configuration failed");
+  lmsb::launch_reset_best(c->keys.p, c->best.p, 1, c->stream);
+  lmsb::launch_reduce(c->recs.p, nullptr, P, P, c->fits.p, c->keys.p, c->best.p, reduce_grid(c, P),
+                      c->stream);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpyAsync(out, c->best.p, sizeof(lms_candidate), cudaMemcpyDeviceToHost,
+                           c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return LMS_OK;
+}
+
+
 // ---------------------------------------------------------------- Hough
 
 int check_hough(int64_t n_theta, double rho_max, double drho, int64_t n_rho) {
@@ -851,6 +884,16 @@ int lms_batched_f64(const double* x, const double* y, const int64_t* offsets, co
   std::lock_guard<std::mutex> lk(c->mu);
   RC_TRY(ctx_upload(c, x, y, offsets[nfits]));
   return ctx_solve_batch(c, offsets, q, nfits, out);
+}
+
+int lms_primal_brute_f64(const double* x, const double* y, int64_t n, int64_t q, int device,
+                         lms_candidate* out) {
+  if (!out) return set_error(LMS_ERR_INVALID, "null output");
+  lms_ctx* c = nullptr;
+  RC_TRY(shared_ctx(device, &c));
+  std::lock_guard<std::mutex> lk(c->mu);
+  RC_TRY(ctx_upload(c, x, y, n));
+  return ctx_primal(c, q, out);
 }
 
 int lms_hough_vote_u8(const uint8_t* img, int64_t height, int64_t width, int threshold,

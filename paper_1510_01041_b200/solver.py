@@ -82,6 +82,32 @@ def solve_lms(points, q: int | None = None, *, backend: str = "seq", workers: in
     return fit_from_record(x, y, q, rec)
 
 
+def oracle_lms(points, q: int | None = None) -> LmsFit:
+    """The reference's independent primal brute force (solver.py:143-196),
+    evaluated on the GPU: every pair's slope, all its sorted intercepts, the
+    narrowest q-window (first on ties); lexicographic (span, i, j) winner;
+    the line through the window's midpoint.  Limited to n <= 16,384.
+    """
+    from . import _native
+
+    x, y, q = validated(points, q)
+    c = _native.primal_brute(x, y, q)
+    if not c.found:
+        raise DegenerateInputError("no candidate slope found")
+    slope, c_low, c_high = c.u, c.v_low, c.v_high
+    half = (c_high - c_low) * 0.5
+    c_all = y - slope * x
+    tol = GEOM_EPS * max(1.0, float(np.max(np.abs(c_all))))
+    on_edge = (np.abs(c_all - c_low) <= tol) | (np.abs(c_all - c_high) <= tol)
+    return LmsFit(
+        line=LineEq(slope=slope, intercept=(c_low + c_high) * 0.5),
+        lms_value=half * half,
+        slab_height=c_high - c_low,
+        coverage=q,
+        contact_indices=tuple(int(k) for k in np.flatnonzero(on_edge)),
+    )
+
+
 def solve_lms_batch(point_sets, q=None) -> list[LmsFit]:
     """Exact LMS fits of many independent point sets in one GPU batch.
 

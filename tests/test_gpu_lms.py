@@ -231,3 +231,27 @@ def test_batched_mixed_sizes_vs_oracle():
     for pts, q, fit in zip(sets, qs, fits):
         want = oracle.solve(pts, q, threads=THREADS)
         assert (fit.line.slope, fit.line.intercept, fit.lms_value) == (want["slope"], want["intercept"], want["lms_value"])
+
+
+def test_oracle_lms_matches_reference_primal_brute_force():
+    import gzip
+    import json
+
+    path = os.path.join(os.path.dirname(__file__), "golden", "primal_golden.json.gz")
+    with gzip.open(path, "rt") as fh:
+        cases = json.load(fh)["cases"]
+    for c in cases:
+        pts = np.column_stack([[float.fromhex(v) for v in c["x"]], [float.fromhex(v) for v in c["y"]]])
+        fit = lms.oracle_lms(pts, c["q"])
+        want = {k: (float.fromhex(v) if isinstance(v, str) else v) for k, v in c["fit"].items()}
+        want["contact_indices"] = tuple(want["contact_indices"])
+        assert fit_matches(fit, want), c["name"]
+
+
+def test_solver_and_primal_agree_at_moderate_n():
+    rng = np.random.default_rng(909)
+    for n in (100, 300):
+        pts = workloads.contaminated_line_points(n, int(rng.integers(1000)))
+        a, b = lms.solve_lms(pts), lms.oracle_lms(pts)
+        assert a.lms_value == pytest.approx(b.lms_value, rel=1e-9)
+        assert a.line.slope == pytest.approx(b.line.slope, rel=1e-9, abs=1e-12)
