@@ -72,6 +72,13 @@ typedef struct lms_stats {
   float ms_filter;          /* device time inside the filter kernels */
   float ms_exact;           /* device time inside seed + exact-select + reduce */
   float reserved;
+  /* slope-band stage (lms_band.cu); zero when the count filter ran instead */
+  int64_t bands;            /* slope bands the fit's vertices were grouped into */
+  int64_t bands_searched;   /* bands whose lower bound admitted the bound H */
+  float ms_partition;       /* sample + band histogram + scatter */
+  float ms_bound;           /* per-band sorted keys and lower bounds */
+  float ms_band_filter;     /* band-seeded exact records + window counts + exact survivors */
+  float reserved2;
 } lms_stats;
 
 /* Library identity and device discovery. */

@@ -17,7 +17,7 @@ CSRC = os.path.join(PKG_DIR, "csrc")
 LIB_DIR = os.path.join(PKG_DIR, "_lib")
 LIB_PATH = os.path.join(LIB_DIR, "liblmsb200.so")
 
-SOURCES = ["lms_engine.cu", "lms_exact.cu", "lms_filter32m.cu", "lms_order.cu", "lms_plan.cu",
+SOURCES = ["lms_engine.cu", "lms_band.cu", "lms_exact.cu", "lms_filter32m.cu", "lms_order.cu", "lms_plan.cu",
            "lms_hough.cu", "lms_primal.cu", "lms_probe.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -39,10 +39,15 @@ def build(verbose: bool = False, extra: list[str] | None = None, out: str | None
         common += ["-Xptxas", "-v"]
     if extra:
         common += extra
-    for src in SOURCES:
+    from concurrent.futures import ThreadPoolExecutor
+
+    def compile_one(src: str) -> str:
         obj = os.path.join(os.path.dirname(out), src.replace(".cu", ".o"))
         subprocess.run([*common, "-c", os.path.join(CSRC, src), "-o", obj], check=True)
-        objs.append(obj)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 1)) as pool:
+        objs = list(pool.map(compile_one, SOURCES))
     tmp = out + ".tmp"
     subprocess.run([nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-cudart", "static"], check=True)
     os.replace(tmp, out)

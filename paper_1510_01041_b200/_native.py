@@ -62,10 +62,16 @@ class Stats(ctypes.Structure):
         ("ms_filter", ctypes.c_float),
         ("ms_exact", ctypes.c_float),
         ("reserved", ctypes.c_float),
+        ("bands", ctypes.c_int64),
+        ("bands_searched", ctypes.c_int64),
+        ("ms_partition", ctypes.c_float),
+        ("ms_bound", ctypes.c_float),
+        ("ms_band_filter", ctypes.c_float),
+        ("reserved2", ctypes.c_float),
     ]
 
     def as_dict(self) -> dict:
-        return {name: getattr(self, name) for name, _ in self._fields_ if name != "reserved"}
+        return {name: getattr(self, name) for name, _ in self._fields_ if not name.startswith("reserved")}
 
 
 _lib = None

@@ -27,6 +27,7 @@
 #include <string>
 #include <vector>
 
+#include "lms_band.cuh"
 #include "lms_common.cuh"
 #include "lms_hough.cuh"
 #include "lms_kernels.cuh"
@@ -149,6 +150,18 @@ struct lms_ctx {
   DevBuf<unsigned long long> acc, masks;
   DevBuf<double> tcos, tsin;
   DevBuf<int64_t> rbin, scounts, soffsets, sout;
+  // slope bands (lms_band.cu)
+  int band_mode = 1;             // LMSB_BAND=0 disables (count-filter path, for A/B runs)
+  int64_t band_vertices = 16384; // target vertices per band (LMSB_BAND_VERTICES)
+  DevBuf<float> bsample, bbounds;
+  DevBuf<uint16_t> bid;
+  DevBuf<unsigned long long> bcounts, boffsets, bcursor, bscal;
+  DevBuf<uint32_t> bmembers;
+  DevBuf<unsigned char> btemp;
+  DevBuf<double> blb, bulo, buhi;
+  DevBuf<int32_t> blist;
+  std::vector<unsigned long long> h_boff;
+  std::vector<double> h_blb;
   int hough_mode = 0;  // 0 none, 1 image pixels, 2 explicit points
   int64_t hough_npts = 0, hough_width = 1;
   lms_stats stats{};
@@ -166,6 +179,10 @@ int ctx_init(lms_ctx* c, int device) {
   c->device = device;
   const char* ov = getenv("LMSB_ORDER");
   c->line_order = !(ov && std::strcmp(ov, "0") == 0);
+  const char* bm = getenv("LMSB_BAND");
+  c->band_mode = (bm && std::strcmp(bm, "0") == 0) ? 0 : 1;
+  const char* bv = getenv("LMSB_BAND_VERTICES");
+  if (bv && atoll(bv) >= 256) c->band_vertices = atoll(bv);
   CUDA_TRY(cudaSetDevice(device));
   CUDA_TRY(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device));
   CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
@@ -227,6 +244,19 @@ void ctx_release(lms_ctx* c) {
   c->scounts.release();
   c->soffsets.release();
   c->sout.release();
+  c->bsample.release();
+  c->bbounds.release();
+  c->bid.release();
+  c->bcounts.release();
+  c->boffsets.release();
+  c->bcursor.release();
+  c->bscal.release();
+  c->bmembers.release();
+  c->btemp.release();
+  c->blb.release();
+  c->bulo.release();
+  c->buhi.release();
+  c->blist.release();
   if (c->h_best) cudaFreeHost(c->h_best);
   if (c->stream) cudaStreamDestroy(c->stream);
 }
@@ -307,6 +337,224 @@ int order_lines(lms_ctx* c, const std::vector<int64_t>& seg, int64_t F, const do
   st->launches += 4;
   *la = c->pa.p;
   *lb = c->pb.p;
+  return LMS_OK;
+}
+
+// Slope-band search of one large fit (lms_band.cu), after the stratified
+// seeds have put a first record into best[0]: partition the fit's vertices
+// into slope bands, bound every band, seed H from the vertices of the
+// lowest-bound bands, then count windows band by band (lowest bound first)
+// and re-evaluate the survivors exactly.  *used = false when the fit has
+// vertices outside the band stage's fp32 key range (the caller then runs
+// the count filter instead).
+int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st, bool* used) {
+  *used = false;
+  const int64_t span = h.r1 - h.r0;
+  const int K = (int)std::max<int64_t>(
+      1, std::min<int64_t>(lmsb::kBandMaxK, (span + c->band_vertices - 1) / c->band_vertices));
+  const int64_t S = std::min<int64_t>(span, std::min<int64_t>(1 << 20, std::max<int64_t>(64 * K, 1 << 16)));
+  RC_TRY(c->bsample.need(2 * S));
+  RC_TRY(c->bbounds.need(K));
+  RC_TRY(c->bid.need(span + 16));
+  RC_TRY(c->bcounts.need(K + 1));
+  RC_TRY(c->boffsets.need(K + 1));
+  RC_TRY(c->bcursor.need(K));
+  RC_TRY(c->bscal.need(8));
+  RC_TRY(c->bmembers.need(span));
+  RC_TRY(c->btemp.need((int64_t)std::max(lmsb::band_sample_temp_bytes(S), lmsb::band_scan_temp_bytes(K))));
+  RC_TRY(c->blb.need(K));
+  RC_TRY(c->bulo.need(K));
+  RC_TRY(c->buhi.need(K));
+  RC_TRY(c->blist.need(K));
+
+  lmsb::BandFit bf{};
+  bf.a = c->a + h.off;
+  bf.b = c->b + h.off;
+  bf.n = h.n;
+  bf.q = h.q;
+  bf.R0 = h.r0;
+  bf.span = span;
+  double alo = INFINITY, ahi = -INFINITY, am = 0.0, bmx = 0.0;
+  for (int64_t k = h.off; k < h.off + h.n; ++k) {
+    alo = std::min(alo, c->h_a[k]);
+    ahi = std::max(ahi, c->h_a[k]);
+    am = std::max(am, std::fabs(c->h_a[k]));
+    bmx = std::max(bmx, std::fabs(c->h_b[k]));
+  }
+  bf.c = 0.5 * alo + 0.5 * ahi;
+  bf.dev = std::max(ahi - bf.c, bf.c - alo) * (1.0 + 0x1p-40) + 1e-300;
+  bf.amax = am;
+  bf.bmax = bmx;
+  if (!(am < 1e30) || !(bmx < 1e30)) return LMS_OK;
+
+  unsigned long long* sc = c->bscal.p;  // [0] nvalid [1] nforce [2] seed count [3..] wave counts
+  lmsb::BandPartition bp{};
+  bp.S = S;
+  bp.K = K;
+  bp.sample = c->bsample.p;
+  bp.sample_sorted = c->bsample.p + S;
+  bp.nvalid = sc;
+  bp.bounds = c->bbounds.p;
+  bp.bid = c->bid.p;
+  bp.counts = c->bcounts.p;
+  bp.offsets = c->boffsets.p;
+  bp.cursor = c->bcursor.p;
+  bp.nforce = sc + 1;
+  bp.members = c->bmembers.p;
+  bp.temp = c->btemp.p;
+  bp.temp_bytes = (size_t)c->btemp.cap;
+  while (c->ev_chunk.size() < 8) {
+    cudaEvent_t e;
+    CUDA_TRY(cudaEventCreate(&e));
+    c->ev_chunk.push_back(e);
+  }
+  CUDA_TRY(cudaEventRecord(c->ev_chunk[0], c->stream));
+  if (lmsb::launch_band_partition(bf, bp, c->sms, c->stream) != 0)
+    return set_error(LMS_ERR_CUDA, "band partition failed");
+  CUDA_TRY(cudaGetLastError());
+  st->launches += 7;
+  CUDA_TRY(cudaEventRecord(c->ev_chunk[1], c->stream));
+
+  lmsb::BandArgs ba{};
+  ba.offsets = c->boffsets.p;
+  ba.members = c->bmembers.p;
+  ba.list = c->blist.p;
+  ba.lb = c->blb.p;
+  ba.ulo = c->bulo.p;
+  ba.uhi = c->buhi.p;
+  ba.best = c->best.p;
+  ba.out_ranks = c->ranks.p;
+  ba.out_fits = c->item_fit.p;
+  ba.fit = 0;
+  lmsb::launch_band(bf, ba, 0, K, c->stream);
+  CUDA_TRY(cudaGetLastError());
+  st->launches += 1;
+  CUDA_TRY(cudaEventRecord(c->ev_chunk[2], c->stream));
+  c->h_boff.resize(K + 1);
+  c->h_blb.resize(K);
+  unsigned long long hsc[2] = {0, 0};
+  CUDA_TRY(cudaMemcpyAsync(c->h_boff.data(), c->boffsets.p, sizeof(unsigned long long) * (K + 1),
+                           cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->h_blb.data(), c->blb.p, sizeof(double) * K, cudaMemcpyDeviceToHost,
+                           c->stream));
+  CUDA_TRY(cudaMemcpyAsync(hsc, sc, sizeof(hsc), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  if (hsc[1] > 0) return LMS_OK;  // vertices beyond the key range: count filter instead
+  *used = true;
+
+  // bands in ascending bound order
+  std::vector<int32_t> order;
+  order.reserve(K);
+  for (int k = 0; k < K; ++k)
+    if (c->h_boff[k + 1] > c->h_boff[k]) order.push_back(k);
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int32_t x, int32_t y) { return c->h_blb[x] < c->h_blb[y]; });
+  const int nb = (int)order.size();
+  st->bands = K;
+
+  // capacity: the largest wave (bands of up to kChunkVertices vertices, or one bigger band)
+  int64_t maxband = 0;
+  for (int32_t k : order) maxband = std::max<int64_t>(maxband, (int64_t)(c->h_boff[k + 1] - c->h_boff[k]));
+  constexpr int kSeedBands = 4, kSeedPerBand = 1024;
+  const int64_t cap = std::max<int64_t>({std::min<int64_t>(kChunkVertices, span), maxband,
+                                         (int64_t)kSeedBands * kSeedPerBand});
+  RC_TRY(c->ranks.need(cap));
+  RC_TRY(c->item_fit.need(cap));
+  RC_TRY(c->recs.need(cap));
+  ba.out_ranks = c->ranks.p;
+  ba.out_fits = c->item_fit.p;
+  CUDA_TRY(cudaMemcpyAsync(c->blist.p, order.data(), sizeof(int32_t) * nb, cudaMemcpyHostToDevice,
+                           c->stream));
+
+  // seeds from the most promising bands
+  const int sb = std::min(nb, kSeedBands);
+  CUDA_TRY(cudaMemsetAsync(sc + 2, 0, sizeof(unsigned long long), c->stream));
+  lmsb::launch_band_seeds(bf, c->boffsets.p, c->bmembers.p, c->blist.p, sb, kSeedPerBand,
+                          c->ranks.p, c->item_fit.p, 0, sc + 2, c->stream);
+  {
+    lmsb::ExactArgs xa{};
+    xa.a = c->a;
+    xa.b = c->b;
+    xa.fits = c->fits.p;
+    xa.mode = lmsb::kSrcList;
+    xa.d_count = sc + 2;
+    xa.capacity = cap;
+    xa.ranks = c->ranks.p;
+    xa.fit_of = c->item_fit.p;
+    xa.bound = c->best.p;
+    xa.out = c->recs.p;
+    lmsb::launch_exact(xa, persistent_grid(c, -1), c->stream, h.n);
+    lmsb::launch_reduce(c->recs.p, sc + 2, 0, cap, c->fits.p, c->keys.p, c->best.p,
+                        (int)c->sms * 4, c->stream);
+    CUDA_TRY(cudaGetLastError());
+    st->launches += 3;
+  }
+  lms_candidate hb{};
+  CUDA_TRY(cudaMemcpyAsync(&hb, c->best.p, sizeof(hb), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  const double H = hb.found ? hb.height : INFINITY;
+  CUDA_TRY(cudaEventRecord(c->ev_chunk[3], c->stream));
+
+  // waves of bands whose bound admits H
+  std::vector<std::pair<int, int>> waves;
+  {
+    int w0 = 0;
+    int64_t acc = 0;
+    int e = 0;
+    for (; e < nb; ++e) {
+      const int32_t k = order[e];
+      if (!(c->h_blb[k] <= H * (1.0 + 0x1p-19))) break;  // sorted: the rest cannot reach H
+      const int64_t sz = (int64_t)(c->h_boff[k + 1] - c->h_boff[k]);
+      if (acc > 0 && acc + sz > cap) {
+        waves.push_back({w0, e});
+        w0 = e;
+        acc = 0;
+      }
+      acc += sz;
+    }
+    if (e > w0) waves.push_back({w0, e});
+    st->bands_searched = e;
+  }
+  const int nw = (int)waves.size();
+  RC_TRY(c->bscal.need(3 + nw + 1));
+  sc = c->bscal.p;
+  CUDA_TRY(cudaMemsetAsync(sc + 3, 0, sizeof(unsigned long long) * (nw + 1), c->stream));
+  for (int w = 0; w < nw; ++w) {
+    ba.list = c->blist.p + waves[w].first;
+    ba.out_count = sc + 3 + w;
+    lmsb::launch_band(bf, ba, 1, waves[w].second - waves[w].first, c->stream);
+    lmsb::ExactArgs xa{};
+    xa.a = c->a;
+    xa.b = c->b;
+    xa.fits = c->fits.p;
+    xa.mode = lmsb::kSrcList;
+    xa.d_count = sc + 3 + w;
+    xa.capacity = cap;
+    xa.ranks = c->ranks.p;
+    xa.fit_of = c->item_fit.p;
+    xa.bound = c->best.p;
+    xa.out = c->recs.p;
+    lmsb::launch_exact(xa, persistent_grid(c, -1), c->stream, h.n);
+    lmsb::launch_reduce(c->recs.p, sc + 3 + w, 0, cap, c->fits.p, c->keys.p, c->best.p,
+                        (int)c->sms * 4, c->stream);
+    CUDA_TRY(cudaGetLastError());
+    st->launches += 3;
+  }
+  CUDA_TRY(cudaEventRecord(c->ev_chunk[4], c->stream));
+  std::vector<unsigned long long> wc(nw + 1, 0);
+  CUDA_TRY(cudaMemcpyAsync(wc.data(), sc + 3, sizeof(unsigned long long) * (nw + 1),
+                           cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  for (int w = 0; w < nw; ++w) st->survivors += (int64_t)wc[w];
+  st->chunks = nw;
+  float ms = 0.f;
+  CUDA_TRY(cudaEventElapsedTime(&ms, c->ev_chunk[0], c->ev_chunk[1]));
+  st->ms_partition = ms;
+  CUDA_TRY(cudaEventElapsedTime(&ms, c->ev_chunk[1], c->ev_chunk[2]));
+  st->ms_bound = ms;
+  CUDA_TRY(cudaEventElapsedTime(&ms, c->ev_chunk[3], c->ev_chunk[4]));
+  st->ms_band_filter = ms;
+  st->filtered_vertices = span;
   return LMS_OK;
 }
 
@@ -422,10 +670,15 @@ int ctx_solve_fits(lms_ctx* c, const std::vector<HostFit>& hf, lms_candidate* ou
     st.launches += 4;
   }
 
+  // ---- band path: one large fit with lines in shared-memory range
+  bool banded = false;
+  if (F == 1 && c->band_mode && tasks > 0 && hf[0].n <= lmsb::kBandMaxN && hf[0].n <= 65536)
+    RC_TRY(band_solve(c, hf[0], &st, &banded));
+
   // ---- 2.-5. filter the non-exhaustive fits: phase A (every kPhaseStride-th
   // row), re-order, phase B (the rest)
   int64_t nchunks = 0;
-  if (tasks > 0) {
+  if (tasks > 0 && !banded) {
     RC_TRY(c->counts.need(rows + 1));
     RC_TRY(c->row_task_prefix.need(rows + 1));
     RC_TRY(c->row_fit.need(rows));
@@ -517,7 +770,7 @@ int ctx_solve_fits(lms_ctx* c, const std::vector<HostFit>& hf, lms_candidate* ou
   CUDA_TRY(cudaEventRecord(c->ev_end, c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   std::memcpy(out, c->h_best, sizeof(lms_candidate) * F);
-  st.chunks = nchunks;
+  if (!banded) st.chunks = nchunks;
   if (nchunks > 0) {
     std::vector<unsigned long long> cnt(2 + nchunks);
     CUDA_TRY(cudaMemcpy(cnt.data(), c->counters.p, sizeof(unsigned long long) * (2 + nchunks),
@@ -532,7 +785,7 @@ int ctx_solve_fits(lms_ctx* c, const std::vector<HostFit>& hf, lms_candidate* ou
   }
   st.filtered_vertices = std::min(st.filtered_vertices, st.pairs);
   CUDA_TRY(cudaEventElapsedTime(&st.ms_total, c->ev_begin, c->ev_end));
-  st.ms_exact = st.ms_total - st.ms_filter;
+  st.ms_exact = st.ms_total - st.ms_filter - st.ms_partition - st.ms_bound - st.ms_band_filter;
   c->stats = st;
   return LMS_OK;
 }

@@ -255,3 +255,59 @@ def test_solver_and_primal_agree_at_moderate_n():
         a, b = lms.solve_lms(pts), lms.oracle_lms(pts)
         assert a.lms_value == pytest.approx(b.lms_value, rel=1e-9)
         assert a.line.slope == pytest.approx(b.line.slope, rel=1e-9, abs=1e-12)
+
+
+def _ctx_with(env: dict):
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        return _native.Context()
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+def test_band_path_matches_count_filter_path_config2():
+    """The slope-band stage (default) and the count-filter path give the
+    identical record on the full n = 16,384 fit, and on partitions."""
+    pts = workloads.contaminated_line_points(16384, 0)
+    a, b = pts[:, 0].copy(), pts[:, 1].copy()
+    q = 16384 // 2 + 1
+    total = 16384 * 16383 // 2
+    band = _ctx_with({"LMSB_BAND": "1"})
+    filt = _ctx_with({"LMSB_BAND": "0"})
+    for c in (band, filt):
+        c.upload(a, b)
+    for r0, r1 in ((0, total), (0, total // 3), (total // 3, total)):
+        got = band.solve(q, r0, r1)
+        st = band.stats()
+        assert st["bands"] > 0, "band stage did not run"
+        want = filt.solve(q, r0, r1)
+        assert filt.stats()["bands"] == 0
+        assert record_from_native(got) == record_from_native(want), (r0, r1)
+
+
+def test_band_path_bit_exact_vs_oracle_mid_n():
+    """Band stage at n in the thousands (many bands, small ones) against
+    the CPU oracle, including noisy, exact-inlier and integer-grid inputs."""
+    rng = np.random.default_rng(99)
+    for trial in range(6):
+        n = int(rng.integers(600, 1500))
+        if trial % 3 == 0:
+            pts = workloads.contaminated_line_points(n, trial)
+        elif trial % 3 == 1:
+            pts = workloads.config1_points(trial, n=n)
+        else:
+            pts = np.column_stack([rng.integers(0, 60, n), rng.integers(0, 60, n)]).astype(float)
+        x, y = pts[:, 0].copy(), pts[:, 1].copy()
+        q = n // 2 + 1 if trial % 2 == 0 else int(rng.integers(2, n + 1))
+        ctx = _ctx_with({"LMSB_BAND": "1", "LMSB_BAND_VERTICES": "2048"})
+        ctx.upload(x, y)
+        total = n * (n - 1) // 2
+        got = record_from_native(ctx.solve(q, 0, total))
+        assert ctx.stats()["bands"] > 1
+        want = oracle_rec(x, y, q)
+        assert record_matches(got, want), (trial, n, q)
