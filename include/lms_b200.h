@@ -79,6 +79,8 @@ typedef struct lms_stats {
   float ms_bound;           /* per-band sorted keys and lower bounds */
   float ms_band_filter;     /* band-seeded exact records + window counts + exact survivors */
   float reserved2;
+  double seed_height;       /* the bound H the band stage collected with */
+  int64_t band_survivors;   /* collected vertices whose band window counts reached q */
 } lms_stats;
 
 /* Library identity and device discovery. */

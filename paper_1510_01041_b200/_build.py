@@ -46,13 +46,17 @@ def build(verbose: bool = False, extra: list[str] | None = None, out: str | None
         subprocess.run([*common, "-c", os.path.join(CSRC, src), "-o", obj], check=True)
         return obj
 
-    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 1)) as pool:
-        objs = list(pool.map(compile_one, SOURCES))
-    tmp = out + ".tmp"
-    subprocess.run([nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-cudart", "static"], check=True)
-    os.replace(tmp, out)
-    for o in objs:
-        os.remove(o)
+    objs = [os.path.join(os.path.dirname(out), s.replace(".cu", ".o")) for s in SOURCES]
+    try:
+        with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 1)) as pool:
+            list(pool.map(compile_one, SOURCES))
+        tmp = out + ".tmp"
+        subprocess.run([nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-cudart", "static"], check=True)
+        os.replace(tmp, out)
+    finally:
+        for o in objs:
+            if os.path.exists(o):
+                os.remove(o)
     return out
 
 

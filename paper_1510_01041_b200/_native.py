@@ -68,6 +68,8 @@ class Stats(ctypes.Structure):
         ("ms_bound", ctypes.c_float),
         ("ms_band_filter", ctypes.c_float),
         ("reserved2", ctypes.c_float),
+        ("seed_height", ctypes.c_double),
+        ("band_survivors", ctypes.c_int64),
     ]
 
     def as_dict(self) -> dict:

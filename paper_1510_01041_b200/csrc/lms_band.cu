@@ -3,9 +3,9 @@
 // The reference evaluates every arrangement vertex against every line
 // (backend.py:125-179, O(n) per vertex after an O(n log n) sort).  The count
 // filter (lms_filter32m.cu) needs > n - q line tests before it can reject a
-// vertex.  This stage rejects almost every vertex in O(log n) instead, by
-// grouping vertices of similar slope into bands that share one sorted view
-// of the lines.
+// vertex.  This stage rejects whole groups of vertices at once and the rest
+// in O(log n) each, by grouping vertices of similar slope into bands that
+// share one sorted view of the lines.
 //
 // Geometry.  Re-centre the dual lines on c (the middle of the a-range):
 // y'_k(u) = (a_k - c) u - b_k differs from the cut value u a_k - b_k by the
@@ -16,38 +16,42 @@
 // v0 = a_i u - b_i and z = v0 - c u has h_up <= H only if at least q lines
 // have y'_k - z in [0, H] (backend.py:153,159; anchors and ties included),
 // hence only if at least q of the band's sorted keys m_k lie in
-// [z - D_v - E_v, z + H + D_v + E_v] (and symmetrically for h_down).  Two
-// binary searches in the band's sorted keys (shared memory) count that.
+// [z - D_v - E_v, z + H + D_v + E_v] (and symmetrically for h_down).  Binary
+// searches in the band's sorted keys (shared memory) count that.
 //
 // Band lower bound.  If v has height h, q keys lie in an interval of width
 // h + 2 D_v + 2 E_v, so h >= W_q - 2 D_max - 2 E_max with W_q the narrowest
-// q-window of the sorted keys.  Bands whose bound exceeds the current H are
-// skipped without touching their vertices; the lowest bounds also point at
-// the bands where the optimum lives (their vertices seed H).
+// q-window of the sorted keys.  Bands whose bound exceeds H are never
+// touched again; the lowest bounds point at the bands where the optimum
+// lives, and the sampled vertices of those bands seed H.
 //
-// Error budget (eps = 2^-53, amax = max|a|, bmax = max|b|): the reference's
-// roundings of u a_k - b_k, v0 and fl(x - v0) <= H move membership by at
-// most 2^-49 (|u| amax + bmax + H); the fp64 z = fl(v0 - fl(c u)) adds
-// 2^-50 (2 |u| amax + bmax); keys are fp64-formed and rounded to fp32 once:
-// <= 2^-23 (|uM| dev + bmax).  E_v = 2^-20 (|u| amax + bmax + H + |uM| dev)
-// + 1e-300 covers the sum with a wide margin; D is computed from an
-// upward-padded dev, window ends are rounded outward to fp32.  Survivors are
-// re-evaluated bit-exactly (lms_exact.cu), so the band stage only has to
-// return a superset.
+// Error budget (amax = max|a|, bmax = max|b|): the reference's roundings of
+// u a_k - b_k, v0 and fl(x - v0) <= H move membership by at most
+// 2^-49 (|u| amax + bmax + H); z = fl(v0 - fl(c u)) adds 2^-50 (2|u| amax +
+// bmax); keys are fp64-formed and rounded to fp32 once: <= 2^-23 (|uM| dev +
+// bmax).  E_v = 2^-20 (|u| amax + bmax + H + |uM| dev) + 1e-300 covers the
+// sum with a wide margin; dev and the band half-width are padded upward and
+// window ends are rounded outward to fp32.  Survivors are re-evaluated
+// bit-exactly (lms_exact.cu), so this stage only has to return a superset.
 //
-// Pipeline per fit (rank range [R0, R0 + span)):
-//   sample   stratified vertex slopes -> CUB sort -> K-1 quantile boundaries
-//   hist     every vertex: u, band id (binary search of the boundaries)
-//   scatter  vertices (packed i << 16 | j) grouped by band
-//   bound    per band: sort the n keys, W_q, lower bound, slope extent
-//   filter   per band in bound order (skip if bound > H): count windows of
-//            every vertex, emit survivors for the exact stage
+// Pipeline per fit (pair ranks [R0, R0 + span)):
+//   sample   S stratified vertex slopes -> CUB sort -> K-1 boundaries: the
+//            sample minimum, quantiles, just above the sample maximum (so the
+//            two outer bands hold only the extremes)
+//   bound    per inner band: slope extent from its boundaries, sorted keys,
+//            W_q, lower bound (one CTA per band, no vertex touched)
+//   seeds    the samples that fall in the lowest-bound bands (exact stage)
+//   collect  one pass over all vertices: those in bands whose bound admits
+//            H (and any beyond the fp32 key range) are appended, then
+//            grouped by band (CUB radix sort on the band id)
+//   filter   per collected band: window counts of every member; survivors
+//            go to the exact stage
 
 #include <cub/block/block_radix_sort.cuh>
 #include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cfloat>
 #include <cmath>
 #include <cstdint>
@@ -59,9 +63,9 @@ namespace lmsb {
 
 namespace {
 
-constexpr uint16_t kBidDrop = 0xFFFF;   // a_i == a_j or non-finite slope (never a window)
-constexpr uint16_t kBidForce = 0xFFFE;  // magnitudes beyond the fp32 key range
-constexpr int kRun = 16;                // consecutive ranks per thread in hist / scatter
+constexpr int kCollectThreads = 512;
+constexpr unsigned kSeedPerBand = 160;  // sampled vertices per seed band
+constexpr int kRun = 32;  // ranks per lane per warp segment (lane-interleaved)
 
 __device__ __forceinline__ float band_key(double u) {
   // monotone non-decreasing map of the slope to fp32 (clamped, so ordered)
@@ -69,55 +73,24 @@ __device__ __forceinline__ float band_key(double u) {
   return fminf(fmaxf(f, -FLT_MAX), FLT_MAX);
 }
 
-// slope and class of vertex (i, j), exactly as _scan_rank_range (backend.py:203-205)
-__device__ __forceinline__ int classify(const BandFit& bf, int64_t i, int64_t j, double* pu) {
-  const double da = __dsub_rn(bf.a[i], bf.a[j]);
+// slope and class of vertex (i, j) exactly as _scan_rank_range forms it
+// (backend.py:200-205): 0 never a window (a_i == a_j or non-finite u),
+// 1 banded, 2 beyond the fp32 key range (always passed to the exact stage)
+__device__ __forceinline__ int classify(const BandFit& bf, double ai, double bi, double aj,
+                                        double bj, double* pu) {
+  const double da = __dsub_rn(ai, aj);
   if (da == 0.0) return 0;
-  const double u = __ddiv_rn(__dsub_rn(bf.b[i], bf.b[j]), da);
+  const double u = __ddiv_rn(__dsub_rn(bi, bj), da);
   if (!isfinite(u)) return 0;
   *pu = u;
-  if (!(fabs(u) * bf.amax < 1e30) || !(bf.bmax < 1e30) || !(bf.amax < 1e30)) return 2;
-  return 1;
+  return fabs(u) * bf.amax < 1e30 ? 1 : 2;
 }
 
-// first rank of a thread's run and its (i, j)
-__device__ __forceinline__ void run_start(const BandFit& bf, int64_t r, int64_t* i, int64_t* j) {
-  decode_rank(bf.n, r, i, j);
+__device__ __forceinline__ int64_t sample_rank(const BandFit& bf, int64_t S, int64_t s) {
+  return bf.R0 + ((2 * s + 1) * bf.span) / (2 * S);
 }
 
-__device__ __forceinline__ void step_pair(int64_t n, int64_t* i, int64_t* j) {
-  if (++*j >= n) {
-    ++*i;
-    *j = *i + 1;
-  }
-}
-
-__global__ void band_sample_kernel(BandFit bf, int64_t S, float* __restrict__ keys,
-                                   unsigned long long* __restrict__ nvalid) {
-  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < S;
-       s += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = bf.R0 + ((2 * s + 1) * bf.span) / (2 * S);
-    int64_t i, j;
-    decode_rank(bf.n, r, &i, &j);
-    double u = 0.0;
-    const int cls = classify(bf, i, j, &u);
-    const bool ok = cls == 1;
-    keys[s] = ok ? band_key(u) : INFINITY;
-    const unsigned m = __ballot_sync(__activemask(), ok);
-    if ((threadIdx.x & 31) == __ffs(__activemask()) - 1 && m)
-      atomicAdd(nvalid, (unsigned long long)__popc(m));
-  }
-}
-
-__global__ void band_bounds_kernel(const float* __restrict__ sorted,
-                                   const unsigned long long* __restrict__ nvalid, int K,
-                                   float* __restrict__ bounds) {
-  const int64_t sv = (int64_t)*nvalid;
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x + 1; k < K; k += gridDim.x * blockDim.x)
-    bounds[k - 1] = sv > 0 ? sorted[(k * sv) / K] : INFINITY;
-}
-
-// number of boundaries <= key (upper bound), i.e. the band index
+// number of boundaries <= key, i.e. the band index
 __device__ __forceinline__ int band_of(const float* __restrict__ bnd, int nb, float key) {
   int lo = 0, hi = nb;
   while (lo < hi) {
@@ -128,80 +101,33 @@ __device__ __forceinline__ int band_of(const float* __restrict__ bnd, int nb, fl
   return lo;
 }
 
-__global__ void __launch_bounds__(512) band_hist_kernel(BandFit bf, int K,
-                                                        const float* __restrict__ bounds,
-                                                        uint16_t* __restrict__ bid,
-                                                        unsigned long long* __restrict__ counts,
-                                                        unsigned long long* __restrict__ nforce) {
-  extern __shared__ unsigned char smem_raw[];
-  float* bnd = reinterpret_cast<float*>(smem_raw);
-  unsigned* hist = reinterpret_cast<unsigned*>(bnd + K);
-  for (int k = threadIdx.x; k < K; k += blockDim.x) {
-    if (k < K - 1) bnd[k] = bounds[k];
-    hist[k] = 0;
-  }
-  __syncthreads();
-  const int64_t runs = (bf.span + kRun - 1) / kRun;
-  unsigned forced = 0;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < runs;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r0 = t * kRun;
-    const int64_t cnt = bf.span - r0 < kRun ? bf.span - r0 : kRun;
+__global__ void band_sample_kernel(BandFit bf, int64_t S, float* __restrict__ keys,
+                                   unsigned long long* __restrict__ nvalid) {
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < S;
+       s += (int64_t)gridDim.x * blockDim.x) {
     int64_t i, j;
-    run_start(bf, bf.R0 + r0, &i, &j);
-    uint32_t w[kRun / 2];
-#pragma unroll
-    for (int e = 0; e < kRun; ++e) {
-      uint16_t id = kBidDrop;
-      if (e < cnt) {
-        double u = 0.0;
-        const int cls = classify(bf, i, j, &u);
-        if (cls == 1) {
-          const int k = band_of(bnd, K - 1, band_key(u));
-          id = (uint16_t)k;
-          atomicAdd(hist + k, 1u);
-        } else if (cls == 2) {
-          id = kBidForce;
-          ++forced;
-        }
-        step_pair(bf.n, &i, &j);
-      }
-      if (e & 1) w[e >> 1] |= (uint32_t)id << 16;
-      else w[e >> 1] = id;
-    }
-    if (cnt == kRun) {
-      uint4* dst = reinterpret_cast<uint4*>(bid + r0);
-      dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
-      dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
-    } else {
-      for (int e = 0; e < cnt; ++e) bid[r0 + e] = (uint16_t)(w[e >> 1] >> (16 * (e & 1)));
-    }
+    decode_rank(bf.n, sample_rank(bf, S, s), &i, &j);
+    double u = 0.0;
+    const bool ok = classify(bf, bf.a[i], bf.b[i], bf.a[j], bf.b[j], &u) == 1;
+    keys[s] = ok ? band_key(u) : INFINITY;
+    if (ok) atomicAdd(nvalid, 1ull);
   }
-  if (forced) atomicAdd(nforce, (unsigned long long)forced);
-  __syncthreads();
-  for (int k = threadIdx.x; k < K; k += blockDim.x)
-    if (hist[k]) atomicAdd(counts + k, (unsigned long long)hist[k]);
 }
 
-__global__ void __launch_bounds__(512) band_scatter_kernel(BandFit bf,
-                                                           const uint16_t* __restrict__ bid,
-                                                           unsigned long long* __restrict__ cursor,
-                                                           uint32_t* __restrict__ members) {
-  const int64_t runs = (bf.span + kRun - 1) / kRun;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < runs;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r0 = t * kRun;
-    const int64_t cnt = bf.span - r0 < kRun ? bf.span - r0 : kRun;
-    int64_t i, j;
-    run_start(bf, bf.R0 + r0, &i, &j);
-    for (int e = 0; e < cnt; ++e) {
-      const uint16_t id = bid[r0 + e];
-      if (id < kBidForce) {
-        const unsigned long long pos = atomicAdd(cursor + id, 1ull);
-        members[pos] = ((uint32_t)i << 16) | (uint32_t)j;
-      }
-      step_pair(bf.n, &i, &j);
+// K >= 3 bands from the sorted valid samples s[0 .. sv): boundary 0 = s[0],
+// boundary K-2 = just above s[sv-1], boundaries 1..K-3 = quantiles.
+__global__ void band_bounds_kernel(const float* __restrict__ sorted,
+                                   const unsigned long long* __restrict__ nvalid, int K,
+                                   float* __restrict__ bounds) {
+  const int64_t sv = (int64_t)*nvalid;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < K - 1; k += gridDim.x * blockDim.x) {
+    float v = INFINITY;
+    if (sv > 0) {
+      if (k == 0) v = sorted[0];
+      else if (k == K - 2) v = nextafterf(sorted[sv - 1], INFINITY);
+      else v = sorted[(k * sv) / (K - 2)];
     }
+    bounds[k] = v;
   }
 }
 
@@ -214,7 +140,6 @@ struct BandShared {
     float keys[kThreads * kItems];
   };
   double red[2][kThreads / 32];
-  unsigned long long base;
 };
 
 __device__ __forceinline__ int lower_idx(const float* __restrict__ k, int n, float x) {
@@ -255,27 +180,94 @@ __device__ __forceinline__ double slack_base(const BandFit& bf, double umag, dou
   return 0x1p-20 * (umag * bf.amax + bf.bmax + fabs(uM) * bf.dev);
 }
 
-// mode 0: slope extent + lower bound of every band; mode 1: count windows
-template <int kThreads, int kItems, int kMode>
-__global__ void __launch_bounds__(kThreads, 1) band_kernel(BandFit bf, BandArgs ba) {
+// Slope extent of an inner band from its boundaries: members satisfy
+// b_{k-1} <= fl32(u) < b_k, so prev(b_{k-1}) < u < b_k.  false for the outer
+// bands (their extent comes from the members).
+__device__ __forceinline__ bool boundary_extent(const float* __restrict__ bounds, int K, int band,
+                                                double* uL, double* uR) {
+  if (band <= 0 || band >= K - 1) return false;
+  const float lo = bounds[band - 1], hi = bounds[band];
+  *uL = (double)nextafterf(lo, -INFINITY);
+  *uR = (double)hi;
+  return isfinite(*uL) && isfinite(*uR) && *uL <= *uR;
+}
+
+__device__ __forceinline__ bool keys_in_range(const BandFit& bf, double uL, double uR) {
+  return fmax(fabs(uL), fabs(uR)) * bf.dev + bf.bmax < 1e37;
+}
+
+// sorted keys m_k = (a_k - c) uM - b_k of the band into sh.keys (the input
+// arrangement is irrelevant to a sort, so lines are loaded striped, i.e.
+// coalesced, and the result is written striped, i.e. bank-conflict free)
+template <int kThreads, int kItems>
+__device__ __forceinline__ void band_keys(const BandFit& bf, double uM,
+                                          BandShared<kThreads, kItems>& sh) {
+  const int tid = threadIdx.x;
+  const int n = (int)bf.n;
+  float keys[kItems];
+#pragma unroll
+  for (int e = 0; e < kItems; ++e) {
+    const int k = e * kThreads + tid;
+    keys[e] = k < n ? (float)__dsub_rn(__dmul_rn(__dsub_rn(__ldg(bf.a + k), bf.c), uM), __ldg(bf.b + k))
+                    : INFINITY;
+  }
+  typename BandShared<kThreads, kItems>::Sort(sh.sort).SortBlockedToStriped(keys);
+  __syncthreads();
+#pragma unroll
+  for (int e = 0; e < kItems; ++e) sh.keys[e * kThreads + tid] = keys[e];
+  __syncthreads();
+}
+
+// mode 0: lower bound of every inner band (grid = K)
+template <int kThreads, int kItems>
+__global__ void __launch_bounds__(kThreads, 1) band_bound_kernel(BandFit bf, BandArgs ba) {
   using SH = BandShared<kThreads, kItems>;
   extern __shared__ __align__(16) unsigned char band_smem[];
   SH& sh = *reinterpret_cast<SH*>(band_smem);
-  const int band = kMode == 0 ? (int)blockIdx.x : ba.list[blockIdx.x];
-  const int64_t m0 = (int64_t)ba.offsets[band];
-  const int64_t m1 = (int64_t)ba.offsets[band + 1];
-  const int n = (int)bf.n;
-  const int tid = threadIdx.x;
-  if (m1 <= m0) {
-    if (kMode == 0 && tid == 0) {
-      ba.lb[band] = INFINITY;
-      ba.ulo[band] = 0.0;
-      ba.uhi[band] = 0.0;
+  const int band = (int)blockIdx.x;
+  double uL, uR;
+  if (!boundary_extent(ba.bounds, ba.K, band, &uL, &uR) || !keys_in_range(bf, uL, uR)) {
+    if (threadIdx.x == 0) {
+      ba.lb[band] = -INFINITY;  // outer / unbounded: always collected
+      ba.wq[band] = INFINITY;
     }
     return;
   }
-  double uL, uR, H = INFINITY;
-  if (kMode == 0) {
+  const double uM = 0.5 * uL + 0.5 * uR;
+  const double dmax = bf.dev * fmax(uR - uM, uM - uL) * (1.0 + 0x1p-40);
+  band_keys<kThreads, kItems>(bf, uM, sh);
+  const int n = (int)bf.n, q = (int)bf.q;
+  double w = INFINITY;
+  for (int k = threadIdx.x; k + q - 1 < n; k += kThreads)
+    w = fmin(w, (double)sh.keys[k + q - 1] - (double)sh.keys[k]);
+  w = block_min<kThreads>(w, sh.red[0]);
+  if (threadIdx.x == 0) {
+    const double e = slack_base(bf, fmax(fabs(uL), fabs(uR)), uM) + 1e-300;
+    ba.lb[band] = (w - 2.0 * dmax - 2.0 * e) * (1.0 - 0x1p-40);
+    ba.wq[band] = w;
+  }
+}
+
+// mode 1: window counts of every collected member of the listed bands
+template <int kThreads, int kItems>
+__global__ void __launch_bounds__(kThreads, 1) band_filter_kernel(BandFit bf, BandArgs ba) {
+  using SH = BandShared<kThreads, kItems>;
+  extern __shared__ __align__(16) unsigned char band_smem[];
+  SH& sh = *reinterpret_cast<SH*>(band_smem);
+  const int band = ba.list[blockIdx.x];
+  const int64_t m0 = ba.start[band];
+  const int64_t m1 = ba.end[band];
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  if (m1 <= m0) return;
+  double H = INFINITY;
+  {
+    const lms_candidate best = *ba.best;
+    if (best.found) H = best.height;
+  }
+  bool all = band >= ba.K;  // the beyond-range pseudo band: every member survives
+  double uL = 0.0, uR = 0.0;
+  if (!all && !boundary_extent(ba.bounds, ba.K, band, &uL, &uR)) {
     double lo = INFINITY, hi = -INFINITY;
     for (int64_t s = m0 + tid; s < m1; s += kThreads) {
       const uint32_t p = ba.members[s];
@@ -286,46 +278,15 @@ __global__ void __launch_bounds__(kThreads, 1) band_kernel(BandFit bf, BandArgs 
     }
     uL = block_min<kThreads>(lo, sh.red[0]);
     uR = -block_min<kThreads>(-hi, sh.red[1]);
-  } else {
-    uL = ba.ulo[band];
-    uR = ba.uhi[band];
-    const lms_candidate best = *ba.best;
-    if (best.found) H = best.height;
-    if (ba.lb[band] > H * (1.0 + 0x1p-19)) return;  // no vertex of the band can reach H
+  }
+  if (!all) {
+    if (ba.lb[band] > H * (1.0 + 0x1p-19)) return;  // H tightened since collection
+    all = !(isfinite(uL) && isfinite(uR)) || !keys_in_range(bf, uL, uR);
   }
   const double uM = 0.5 * uL + 0.5 * uR;
-  const double half_w = fmax(uR - uM, uM - uL) * (1.0 + 0x1p-40);
-  const double dmax = bf.dev * half_w;
-
-  // the band's keys m_k = (a_k - c) uM - b_k, sorted
-  float keys[kItems];
-#pragma unroll
-  for (int e = 0; e < kItems; ++e) {
-    const int k = tid * kItems + e;
-    keys[e] = k < n ? (float)__dsub_rn(__dmul_rn(__dsub_rn(bf.a[k], bf.c), uM), bf.b[k]) : INFINITY;
-  }
-  typename SH::Sort(sh.sort).Sort(keys);
-  __syncthreads();
-#pragma unroll
-  for (int e = 0; e < kItems; ++e) sh.keys[tid * kItems + e] = keys[e];
-  __syncthreads();
+  if (!all) band_keys<kThreads, kItems>(bf, uM, sh);
   const float* K = sh.keys;
-  const int q = (int)bf.q;
-
-  if constexpr (kMode == 0) {
-    double w = INFINITY;
-    for (int k = tid; k + q - 1 < n; k += kThreads)
-      w = fmin(w, (double)K[k + q - 1] - (double)K[k]);
-    w = block_min<kThreads>(w, sh.red[0]);
-    if (tid == 0) {
-      const double umag = fmax(fabs(uL), fabs(uR));
-      const double e = slack_base(bf, umag, uM) + 1e-300;
-      ba.lb[band] = (w - 2.0 * dmax - 2.0 * e) * (1.0 - 0x1p-40);
-      ba.ulo[band] = uL;
-      ba.uhi[band] = uR;
-    }
-  } else {
-  // mode 1: every vertex of the band
+  const int n = (int)bf.n, q = (int)bf.q;
   for (int64_t s0 = m0; s0 < m1; s0 += kThreads) {
     const int64_t s = s0 + tid;
     bool keep = false;
@@ -333,26 +294,28 @@ __global__ void __launch_bounds__(kThreads, 1) band_kernel(BandFit bf, BandArgs 
     if (s < m1) {
       const uint32_t p = ba.members[s];
       const int64_t i = p >> 16, j = p & 0xFFFF;
-      const double ai = bf.a[i], bi = bf.b[i];
-      const double u = __ddiv_rn(__dsub_rn(bi, bf.b[j]), __dsub_rn(ai, bf.a[j]));
-      const double v0 = cut_value(u, ai, bi);
-      const double z = __dsub_rn(v0, __dmul_rn(bf.c, u));
-      const double D = bf.dev * fabs(u - uM) * (1.0 + 0x1p-40);
-      const double E = slack_base(bf, fabs(u), uM) + 0x1p-20 * H + 1e-300;
-      const double pad = D + E;
-      const int top = upper_idx(K, n, __double2float_ru(z + H + pad));
-      const int bot = lower_idx(K, n, __double2float_rd(z - H - pad));
-      if (top - bot >= q) {
-        const int up_lo = lower_idx(K, n, __double2float_rd(z - pad));
-        const int dn_hi = upper_idx(K, n, __double2float_ru(z + pad));
-        keep = (top - up_lo >= q) || (dn_hi - bot >= q);
-      }
       rank = row_offset(bf.n, i) + (j - i - 1);
+      keep = all;
+      if (!all) {
+        const double ai = bf.a[i], bi = bf.b[i];
+        const double u = __ddiv_rn(__dsub_rn(bi, bf.b[j]), __dsub_rn(ai, bf.a[j]));
+        const double v0 = cut_value(u, ai, bi);
+        const double z = __dsub_rn(v0, __dmul_rn(bf.c, u));
+        const double D = bf.dev * fabs(u - uM) * (1.0 + 0x1p-40);
+        const double E = slack_base(bf, fabs(u), uM) + 0x1p-20 * H + 1e-300;
+        const double pad = D + E;
+        const int top = upper_idx(K, n, __double2float_ru(z + H + pad));
+        const int bot = lower_idx(K, n, __double2float_rd(z - H - pad));
+        if (top - bot >= q) {
+          const int up_lo = lower_idx(K, n, __double2float_rd(z - pad));
+          const int dn_hi = upper_idx(K, n, __double2float_ru(z + pad));
+          keep = (top - up_lo >= q) || (dn_hi - bot >= q);
+        }
+      }
     }
     const unsigned mask = __ballot_sync(0xffffffffu, keep);
     if (mask) {
       unsigned long long base = 0;
-      const int lane = tid & 31;
       if (lane == 0) base = atomicAdd(ba.out_count, (unsigned long long)__popc(mask));
       base = __shfl_sync(0xffffffffu, base, 0);
       if (keep) {
@@ -362,51 +325,289 @@ __global__ void __launch_bounds__(kThreads, 1) band_kernel(BandFit bf, BandArgs 
       }
     }
   }
+}
+
+// seeds: the sampled vertices of the flagged (lowest-bound) bands; also the
+// sample count of every band (collection size estimate)
+__global__ void band_seed_kernel(BandFit bf, int64_t S, const float* __restrict__ keys,
+                                 const float* __restrict__ bounds, int K,
+                                 const uint8_t* __restrict__ flag,
+                                 unsigned* __restrict__ sample_counts, int64_t* __restrict__ ranks,
+                                 int32_t* __restrict__ fits, int32_t fit, int64_t cap,
+                                 unsigned long long* __restrict__ count) {
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < S;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const float key = keys[s];
+    if (!(key <= FLT_MAX)) continue;  // not a banded sample
+    const int band = band_of(bounds, K - 1, key);
+    const unsigned seen = atomicAdd(sample_counts + band, 1u);
+    if (flag[band] && seen < kSeedPerBand) {
+      const unsigned long long pos = atomicAdd(count, 1ull);
+      if ((int64_t)pos < cap) {
+        ranks[pos] = sample_rank(bf, S, s);
+        fits[pos] = fit;
+      }
+    }
   }
 }
 
-template <int kThreads, int kItems, int kMode>
-void launch_band_m(const BandFit& bf, const BandArgs& ba, int grid, cudaStream_t st) {
-  constexpr size_t smem = sizeof(BandShared<kThreads, kItems>);
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(band_kernel<kThreads, kItems, kMode>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = true;
+// one pass over all vertices: append (band, i << 16 | j) of every vertex in
+// a flagged band, and (K, ...) of every vertex beyond the fp32 key range.
+//
+// Pre-test: the flagged bands form a few slope runs; a vertex is tested
+// against them with an fp32 slope u32 = fl32(num) / fl32(da) (num = b_i - b_j,
+// da = a_i - a_j, the reference's own fp64 differences), whose relative
+// error is below 3 * 2^-24, against runs widened by 2^-18 relative (host
+// side, BandRuns).  Vertices with tiny differences (fp32 underflow) or a
+// non-finite u32 always pass.  Passing vertices are queued per warp and
+// processed 32 at a time (no divergence): the fp64 slope exactly as the
+// reference forms it, the band by binary search, the flag.
+//
+// Enumeration: a warp walks a segment of 32 * kRun consecutive ranks, lane l
+// owning ranks base + l + 32 e; (i, j) is decoded once per segment and
+// advanced along the row-major triangle (backend.py:111-122).
+__device__ __forceinline__ void advance_pair(int n, int step, int& i, int& j) {
+  j += step;
+  while (j >= n && i < n - 2) {
+    const int over = j - n;
+    ++i;
+    j = i + 1 + over;
   }
-  band_kernel<kThreads, kItems, kMode><<<grid, kThreads, smem, st>>>(bf, ba);
+}
+
+__global__ void __launch_bounds__(kCollectThreads) band_collect_kernel(
+    BandFit bf, const float* __restrict__ bounds, int K, const uint8_t* __restrict__ flag,
+    BandRuns runs, uint32_t* __restrict__ out_keys, uint32_t* __restrict__ out_vals, int64_t cap,
+    unsigned long long* __restrict__ count) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int kWarps = kCollectThreads / 32;
+  uint32_t* queue = reinterpret_cast<uint32_t*>(smem_raw);  // [kWarps][64]
+  float* bnd = reinterpret_cast<float*>(queue + kWarps * 64);
+  uint8_t* fl = reinterpret_cast<uint8_t*>(bnd + K);
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+    if (k < K - 1) bnd[k] = bounds[k];
+    fl[k] = flag[k];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  uint32_t* q = queue + (threadIdx.x >> 5) * 64;
+  int qn = 0;
+  const int n = (int)bf.n;
+  const int64_t seg = 32 * kRun;
+  const int64_t nseg = (bf.span + seg - 1) / seg;
+  const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+
+  // exact band lookup of 32 queued vertices (lanes >= cnt idle), append
+  auto drain = [&](int cnt) {
+    bool take = false;
+    uint32_t key = 0, val = 0;
+    if (lane < cnt) {
+      val = q[lane];
+      const int i = val >> 16, j = val & 0xFFFF;
+      double u = 0.0;
+      const int cls = classify(bf, __ldg(bf.a + i), __ldg(bf.b + i), __ldg(bf.a + j),
+                               __ldg(bf.b + j), &u);
+      if (cls == 1) {
+        const int band = band_of(bnd, K - 1, band_key(u));
+        take = fl[band] != 0;
+        key = (uint32_t)band;
+      } else if (cls == 2) {
+        take = true;
+        key = (uint32_t)K;
+      }
+    }
+    const unsigned mask = __ballot_sync(0xffffffffu, take);
+    if (mask) {
+      const int leader = __ffs(mask) - 1;
+      unsigned long long b0 = 0;
+      if (lane == leader) b0 = atomicAdd(count, (unsigned long long)__popc(mask));
+      b0 = __shfl_sync(0xffffffffu, b0, leader);
+      if (take) {
+        const unsigned long long pos = b0 + __popc(mask & ((1u << lane) - 1u));
+        if ((int64_t)pos < cap) {
+          out_keys[pos] = key;
+          out_vals[pos] = val;
+        }
+      }
+    }
+  };
+
+  for (int64_t g = warp0; g < nseg; g += nwarps) {
+    const int64_t base = g * seg;
+    int i0 = 0, j0 = 0;
+    if (lane == 0) {
+      int64_t i64, j64;
+      decode_rank(bf.n, bf.R0 + base, &i64, &j64);
+      i0 = (int)i64;
+      j0 = (int)j64;
+    }
+    int i = __shfl_sync(0xffffffffu, i0, 0);
+    int j = __shfl_sync(0xffffffffu, j0, 0);
+    advance_pair(n, lane, i, j);
+    double ai = __ldg(bf.a + i), bi = __ldg(bf.b + i);
+    int64_t r = base + lane;
+#pragma unroll 1
+    for (int e = 0; e < kRun; ++e, r += 32) {
+      bool cand = false;
+      if (r < bf.span) {
+        const double da = __dsub_rn(ai, __ldg(bf.a + j));
+        const double num = __dsub_rn(bi, __ldg(bf.b + j));
+        if (da != 0.0) {
+          const float u32 = (float)num / (float)da;
+          cand = !(fabsf(u32) <= FLT_MAX) || fabs(da) < 1e-30 || (num != 0.0 && fabs(num) < 1e-30);
+#pragma unroll
+          for (int k = 0; k < kMaxRuns; ++k)
+            if (k < runs.count) cand |= (u32 >= runs.lo[k]) & (u32 <= runs.hi[k]);
+        }
+      }
+      const unsigned cm = __ballot_sync(0xffffffffu, cand);
+      if (cand) q[qn + __popc(cm & ((1u << lane) - 1u))] = ((uint32_t)i << 16) | (uint32_t)j;
+      qn += __popc(cm);
+      __syncwarp();
+      if (qn >= 32) {
+        drain(32);
+        __syncwarp();
+        if (lane < qn - 32) q[lane] = q[32 + lane];
+        __syncwarp();
+        qn -= 32;
+      }
+      const int i_old = i;
+      advance_pair(n, 32, i, j);
+      if (i != i_old) {
+        ai = __ldg(bf.a + i);
+        bi = __ldg(bf.b + i);
+      }
+    }
+  }
+  if (qn > 0) drain(qn);
+}
+
+// Exact-slope window counts of the band filter's survivors, in fp32: with
+// A_k = fl32(a_k - c), B_k = fl32(b_k) and t_k = fma(A_k, fl32(u), -B_k), a
+// line in the reference's upward window satisfies t_k in [z - E, z + H + E]
+// (downward: [z - H - E, z + E]) where E = 2^-20 (3 amax |u| + 2 bmax + H)
+// + 1e-37 covers the fp32 roundings of A, B, u and the FMA (<= 2^-22 (dev |u|
+// + bmax) + subnormal steps) and the reference's own (see the file header).
+// Removes the band padding D_v, so only vertices whose windows really can
+// reach H go on to the exact select.
+constexpr int kCountThreads = 256;
+constexpr int kCountChunk = 2048;
+
+__global__ void band_lines32_kernel(BandFit bf, float2* __restrict__ lines) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < bf.n;
+       k += (int64_t)gridDim.x * blockDim.x)
+    lines[k] = make_float2((float)__dsub_rn(bf.a[k], bf.c), (float)bf.b[k]);
+}
+
+__global__ void __launch_bounds__(kCountThreads) band_count_kernel(
+    BandFit bf, const float2* __restrict__ lines, const lms_candidate* __restrict__ best,
+    const int64_t* __restrict__ in_ranks, const unsigned long long* __restrict__ in_count,
+    int64_t* __restrict__ out_ranks, int32_t* __restrict__ out_fits, int32_t fit,
+    unsigned long long* __restrict__ out_count) {
+  __shared__ float2 sl[kCountChunk];
+  const int64_t total = (int64_t)*in_count;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int n = (int)bf.n;
+  const int q = (int)bf.q;
+  double H = INFINITY;
+  {
+    const lms_candidate b0 = *best;
+    if (b0.found) H = b0.height;
+  }
+  for (int64_t t0 = (int64_t)blockIdx.x * kCountThreads; t0 < total;
+       t0 += (int64_t)gridDim.x * kCountThreads) {
+    const int64_t s = t0 + tid;
+    const bool live = s < total;
+    int64_t rank = 0;
+    bool force = !isfinite(H) || (bf.amax > 0.0 && bf.amax < 1e-30) ||
+                 (bf.bmax > 0.0 && bf.bmax < 1e-30);
+    float u32 = 0.f, upLo = 1.f, upHi = 0.f, dnLo = 1.f, dnHi = 0.f;
+    if (live) {
+      rank = in_ranks[s];
+      int64_t i, j;
+      decode_rank(bf.n, rank, &i, &j);
+      const double ai = bf.a[i], bi = bf.b[i];
+      const double u = __ddiv_rn(__dsub_rn(bi, bf.b[j]), __dsub_rn(ai, bf.a[j]));
+      const double v0 = cut_value(u, ai, bi);
+      const double z = __dsub_rn(v0, __dmul_rn(bf.c, u));
+      const double mag = fabs(u) * bf.amax;
+      force = force || !(mag + bf.bmax + H < 1e36);
+      const double E = 0x1p-20 * (3.0 * mag + 2.0 * bf.bmax + H) + 1e-37;
+      u32 = (float)u;
+      upLo = __double2float_rd(z - E);
+      upHi = __double2float_ru(z + H + E);
+      dnLo = __double2float_rd(z - H - E);
+      dnHi = __double2float_ru(z + E);
+    }
+    int cu = 0, cd = 0;
+    for (int k0 = 0; k0 < n; k0 += kCountChunk) {
+      const int cnt = n - k0 < kCountChunk ? n - k0 : kCountChunk;
+      __syncthreads();
+      for (int k = tid; k < cnt; k += kCountThreads) sl[k] = lines[k0 + k];
+      __syncthreads();
+#pragma unroll 8
+      for (int k = 0; k < cnt; ++k) {
+        const float2 L = sl[k];
+        const float t = fmaf(L.x, u32, -L.y);
+        cu += (t >= upLo) & (t <= upHi);
+        cd += (t >= dnLo) & (t <= dnHi);
+      }
+    }
+    const bool keep = live && (force || cu >= q || cd >= q);
+    const unsigned mask = __ballot_sync(0xffffffffu, keep);
+    if (mask) {
+      unsigned long long base = 0;
+      if (lane == 0) base = atomicAdd(out_count, (unsigned long long)__popc(mask));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (keep) {
+        const unsigned slot = __popc(mask & ((1u << lane) - 1u));
+        out_ranks[base + slot] = rank;
+        out_fits[base + slot] = fit;
+      }
+    }
+  }
+}
+
+__global__ void band_runs_kernel(const uint32_t* __restrict__ keys, int64_t m,
+                                 int64_t* __restrict__ start, int64_t* __restrict__ end) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < m;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t k = keys[p];
+    if (p == 0 || keys[p - 1] != k) start[k] = p;
+    if (p == m - 1 || keys[p + 1] != k) end[k] = p + 1;
+  }
+}
+
+template <typename Kern>
+void set_smem(Kern kern, size_t smem, bool* done) {
+  if (!*done) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    *done = true;
+  }
 }
 
 template <int kThreads, int kItems>
 void launch_band_t(const BandFit& bf, const BandArgs& ba, int mode, int grid, cudaStream_t st) {
-  if (mode == 0) launch_band_m<kThreads, kItems, 0>(bf, ba, grid, st);
-  else launch_band_m<kThreads, kItems, 1>(bf, ba, grid, st);
-}
-
-__global__ void band_seed_kernel(BandFit bf, const unsigned long long* __restrict__ offsets,
-                                 const uint32_t* __restrict__ members,
-                                 const int32_t* __restrict__ list, int nb, int per_band,
-                                 int64_t* __restrict__ ranks, int32_t* __restrict__ fits,
-                                 int32_t fit, unsigned long long* __restrict__ count) {
-  const int e = blockIdx.x;
-  if (e >= nb) return;
-  const int band = list[e];
-  const int64_t m0 = (int64_t)offsets[band], cnt = (int64_t)offsets[band + 1] - m0;
-  const int64_t take = cnt < per_band ? cnt : per_band;
-  for (int64_t t = threadIdx.x; t < take; t += blockDim.x) {
-    const uint32_t p = members[m0 + (t * cnt) / take];
-    const int64_t i = p >> 16, j = p & 0xFFFF;
-    const unsigned long long pos = atomicAdd(count, 1ull);
-    ranks[pos] = row_offset(bf.n, i) + (j - i - 1);
-    fits[pos] = fit;
+  constexpr size_t smem = sizeof(BandShared<kThreads, kItems>);
+  static bool c0 = false, c1 = false;
+  if (mode == 0) {
+    set_smem(band_bound_kernel<kThreads, kItems>, smem, &c0);
+    band_bound_kernel<kThreads, kItems><<<grid, kThreads, smem, st>>>(bf, ba);
+  } else {
+    set_smem(band_filter_kernel<kThreads, kItems>, smem, &c1);
+    band_filter_kernel<kThreads, kItems><<<grid, kThreads, smem, st>>>(bf, ba);
   }
 }
 
+int bits_for(int64_t v) {
+  int b = 1;
+  while (b < 32 && ((int64_t)1 << b) <= v) ++b;
+  return b;
+}
+
 }  // namespace
-
-int band_max_n() { return kBandMaxN; }
-
-size_t band_hist_smem(int K) { return (size_t)K * (sizeof(float) + sizeof(unsigned)); }
 
 size_t band_sample_temp_bytes(int64_t S) {
   size_t bytes = 0;
@@ -414,42 +615,25 @@ size_t band_sample_temp_bytes(int64_t S) {
   return bytes;
 }
 
-size_t band_scan_temp_bytes(int K) {
+size_t band_group_temp_bytes(int64_t m) {
   size_t bytes = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, bytes, (const unsigned long long*)nullptr,
-                                (unsigned long long*)nullptr, K + 1);
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                  (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)m);
   return bytes;
 }
 
-int launch_band_partition(const BandFit& bf, const BandPartition& bp, int sms, cudaStream_t st) {
-  // 1. quantile boundaries from a stratified sample of slopes
-  cudaMemsetAsync(bp.nvalid, 0, sizeof(unsigned long long), st);
-  band_sample_kernel<<<sms * 4, 256, 0, st>>>(bf, bp.S, bp.sample, bp.nvalid);
-  size_t bytes = bp.temp_bytes;
-  if (cub::DeviceRadixSort::SortKeys(bp.temp, bytes, bp.sample, bp.sample_sorted, (int)bp.S, 0,
-                                     32, st) != cudaSuccess)
+size_t band_collect_smem(int K) {
+  return (size_t)(kCollectThreads / 32) * 64 * sizeof(uint32_t) + (size_t)K * (sizeof(float) + sizeof(uint8_t)) + 16;
+}
+
+int launch_band_sample(const BandFit& bf, const BandWork& w, int sms, cudaStream_t st) {
+  cudaMemsetAsync(w.nvalid, 0, sizeof(unsigned long long), st);
+  band_sample_kernel<<<sms * 4, 256, 0, st>>>(bf, w.S, w.sample, w.nvalid);
+  size_t bytes = w.temp_bytes;
+  if (cub::DeviceRadixSort::SortKeys(w.temp, bytes, w.sample, w.sample_sorted, (int)w.S, 0, 32,
+                                     st) != cudaSuccess)
     return -1;
-  if (bp.K > 1) band_bounds_kernel<<<(bp.K + 255) / 256, 256, 0, st>>>(bp.sample_sorted, bp.nvalid,
-                                                                        bp.K, bp.bounds);
-  // 2. band of every vertex + histogram
-  cudaMemsetAsync(bp.counts, 0, sizeof(unsigned long long) * (bp.K + 1), st);
-  cudaMemsetAsync(bp.nforce, 0, sizeof(unsigned long long), st);
-  const size_t smem = band_hist_smem(bp.K);
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(band_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)band_hist_smem(kBandMaxK));
-    configured = true;
-  }
-  band_hist_kernel<<<sms * 2, 512, smem, st>>>(bf, bp.K, bp.bounds, bp.bid, bp.counts, bp.nforce);
-  // 3. offsets, then group the vertices by band
-  bytes = bp.temp_bytes;
-  if (cub::DeviceScan::ExclusiveSum(bp.temp, bytes, bp.counts, bp.offsets, bp.K + 1, st) !=
-      cudaSuccess)
-    return -1;
-  cudaMemcpyAsync(bp.cursor, bp.offsets, sizeof(unsigned long long) * bp.K,
-                  cudaMemcpyDeviceToDevice, st);
-  band_scatter_kernel<<<sms * 4, 512, 0, st>>>(bf, bp.bid, bp.cursor, bp.members);
+  band_bounds_kernel<<<(w.K + 255) / 256, 256, 0, st>>>(w.sample_sorted, w.nvalid, w.K, w.bounds);
   return 0;
 }
 
@@ -460,13 +644,43 @@ void launch_band(const BandFit& bf, const BandArgs& ba, int mode, int grid, cuda
   else launch_band_t<1024, 16>(bf, ba, mode, grid, st);
 }
 
-void launch_band_seeds(const BandFit& bf, const unsigned long long* offsets,
-                       const uint32_t* members, const int32_t* list, int nb, int per_band,
-                       int64_t* ranks, int32_t* fits, int32_t fit, unsigned long long* count,
-                       cudaStream_t st) {
-  if (nb <= 0) return;
-  band_seed_kernel<<<nb, 256, 0, st>>>(bf, offsets, members, list, nb, per_band, ranks, fits, fit,
-                                       count);
+void launch_band_seeds(const BandFit& bf, const BandWork& w, int64_t* ranks, int32_t* fits,
+                       int32_t fit, int64_t cap, unsigned long long* count, cudaStream_t st) {
+  cudaMemsetAsync(w.sample_counts, 0, sizeof(unsigned) * w.K, st);
+  cudaMemsetAsync(count, 0, sizeof(unsigned long long), st);
+  const int grid = (int)std::min<int64_t>((w.S + 255) / 256, 1184);
+  band_seed_kernel<<<grid, 256, 0, st>>>(bf, w.S, w.sample, w.bounds, w.K, w.flag,
+                                         w.sample_counts, ranks, fits, fit, cap, count);
+}
+
+void launch_band_collect(const BandFit& bf, const BandWork& w, const BandRuns& runs, int64_t cap,
+                         int sms, cudaStream_t st) {
+  static bool done = false;
+  set_smem(band_collect_kernel, band_collect_smem(kBandMaxK), &done);
+  cudaMemsetAsync(w.ncollect, 0, sizeof(unsigned long long), st);
+  band_collect_kernel<<<sms * 4, kCollectThreads, band_collect_smem(w.K), st>>>(
+      bf, w.bounds, w.K, w.flag, runs, w.ckeys, w.cvals, cap, w.ncollect);
+}
+
+void launch_band_count(const BandFit& bf, const BandCount& bc, int sms, cudaStream_t st) {
+  band_lines32_kernel<<<(int)((bf.n + 255) / 256), 256, 0, st>>>(bf, bc.lines);
+  cudaMemsetAsync(bc.out_count, 0, sizeof(unsigned long long), st);
+  band_count_kernel<<<sms * 8, kCountThreads, 0, st>>>(bf, bc.lines, bc.best, bc.in_ranks,
+                                                       bc.in_count, bc.out_ranks, bc.out_fits,
+                                                       bc.fit, bc.out_count);
+}
+
+int launch_band_group(const BandWork& w, int64_t m, cudaStream_t st) {
+  cudaMemsetAsync(w.start, 0, sizeof(int64_t) * (w.K + 1), st);
+  cudaMemsetAsync(w.end, 0, sizeof(int64_t) * (w.K + 1), st);
+  if (m <= 0) return 0;
+  size_t bytes = w.temp_bytes;
+  if (cub::DeviceRadixSort::SortPairs(w.temp, bytes, w.ckeys, w.ckeys_alt, w.cvals, w.members,
+                                      (int)m, 0, bits_for(w.K), st) != cudaSuccess)
+    return -1;
+  band_runs_kernel<<<(int)std::min<int64_t>((m + 255) / 256, 4096), 256, 0, st>>>(
+      w.ckeys_alt, m, w.start, w.end);
+  return 0;
 }
 
 }  // namespace lmsb

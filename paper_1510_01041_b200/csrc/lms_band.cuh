@@ -9,10 +9,10 @@
 
 namespace lmsb {
 
-// Lines per fit the band stage handles (its sorted keys live in shared memory).
+// Lines per fit the band stage handles (the sorted keys of a band live in
+// shared memory; member vertices pack (i, j) into 16 + 16 bits).
 constexpr int kBandMaxN = 16384;
-// Most bands per fit (band ids are 16-bit; the hist kernel keeps K boundaries
-// and K counters in shared memory).
+// Most bands per fit (the collect kernel keeps K boundaries in shared memory).
 constexpr int kBandMaxK = 16384;
 
 struct BandFit {
@@ -25,30 +25,45 @@ struct BandFit {
   double amax, bmax;
 };
 
-struct BandPartition {
+// Device scratch of one banded solve.
+struct BandWork {
   int64_t S;  // slope samples
-  int K;      // bands
-  float* sample;
-  float* sample_sorted;
+  int K;      // bands (>= 3)
+  float* sample;          // S keys in sample order
+  float* sample_sorted;   // S
   unsigned long long* nvalid;
-  float* bounds;                 // K - 1
-  uint16_t* bid;                 // span
-  unsigned long long* counts;    // K + 1
-  unsigned long long* offsets;   // K + 1
-  unsigned long long* cursor;    // K
-  unsigned long long* nforce;
-  uint32_t* members;             // span: packed (i << 16 | j), grouped by band
+  float* bounds;          // K - 1
+  unsigned* sample_counts;// K
+  uint8_t* flag;          // K: band selected (seeds / collection)
+  uint32_t* ckeys;        // collected (band, packed i<<16|j), capacity cap
+  uint32_t* cvals;
+  uint32_t* ckeys_alt;    // grouped copies
+  uint32_t* members;
+  unsigned long long* ncollect;
+  int64_t* start;         // K + 1: members of band k are [start[k], end[k]); band K =
+  int64_t* end;           //        vertices beyond the fp32 key range
   void* temp;
   size_t temp_bytes;
 };
 
+// Slope runs of the flagged bands (collect pre-test), at most kMaxRuns: fp32
+// bounds widened by 2^-18 relative + 1e-37 and rounded outward (-inf / +inf:
+// open end).
+constexpr int kMaxRuns = 8;
+struct BandRuns {
+  int count;
+  float lo[kMaxRuns], hi[kMaxRuns];
+};
+
 struct BandArgs {
-  const unsigned long long* offsets;
+  int K;
+  const float* bounds;
+  const int64_t* start;
+  const int64_t* end;
   const uint32_t* members;
-  const int32_t* list;  // mode 1: bands to filter (blockIdx -> band)
-  double* lb;           // per band lower bound of any vertex height
-  double* ulo;          // per band slope extent
-  double* uhi;
+  const int32_t* list;        // filter: bands to process (blockIdx -> band)
+  double* lb;                 // per band lower bound of any vertex height (-inf: unknown)
+  double* wq;                 // per band narrowest q-window of the keys at the band centre
   const lms_candidate* best;  // the fit's current best record (H)
   int64_t* out_ranks;
   int32_t* out_fits;
@@ -56,16 +71,29 @@ struct BandArgs {
   unsigned long long* out_count;
 };
 
-int band_max_n();
+// fp32 exact-slope window counts of the band filter's survivors
+struct BandCount {
+  float2* lines;  // n scratch: (fl32(a_k - c), fl32(b_k))
+  const lms_candidate* best;
+  const int64_t* in_ranks;
+  const unsigned long long* in_count;
+  int64_t* out_ranks;
+  int32_t* out_fits;
+  int32_t fit;
+  unsigned long long* out_count;
+};
+
 size_t band_sample_temp_bytes(int64_t S);
-size_t band_scan_temp_bytes(int K);
-size_t band_hist_smem(int K);
-int launch_band_partition(const BandFit& bf, const BandPartition& bp, int sms, cudaStream_t st);
-// mode 0: grid = K (bounds of every band); mode 1: grid = bands in `list`
+size_t band_group_temp_bytes(int64_t m);
+size_t band_collect_smem(int K);
+int launch_band_sample(const BandFit& bf, const BandWork& w, int sms, cudaStream_t st);
+// mode 0: grid = K (lower bound of every band); mode 1: grid = bands in ba.list
 void launch_band(const BandFit& bf, const BandArgs& ba, int mode, int grid, cudaStream_t st);
-void launch_band_seeds(const BandFit& bf, const unsigned long long* offsets,
-                       const uint32_t* members, const int32_t* list, int nb, int per_band,
-                       int64_t* ranks, int32_t* fits, int32_t fit, unsigned long long* count,
-                       cudaStream_t st);
+void launch_band_seeds(const BandFit& bf, const BandWork& w, int64_t* ranks, int32_t* fits,
+                       int32_t fit, int64_t cap, unsigned long long* count, cudaStream_t st);
+void launch_band_collect(const BandFit& bf, const BandWork& w, const BandRuns& runs, int64_t cap,
+                         int sms, cudaStream_t st);
+int launch_band_group(const BandWork& w, int64_t m, cudaStream_t st);
+void launch_band_count(const BandFit& bf, const BandCount& bc, int sms, cudaStream_t st);
 
 }  // namespace lmsb

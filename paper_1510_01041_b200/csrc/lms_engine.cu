@@ -154,13 +154,17 @@ struct lms_ctx {
   int band_mode = 1;             // LMSB_BAND=0 disables (count-filter path, for A/B runs)
   int64_t band_vertices = 16384; // target vertices per band (LMSB_BAND_VERTICES)
   DevBuf<float> bsample, bbounds;
-  DevBuf<uint16_t> bid;
-  DevBuf<unsigned long long> bcounts, boffsets, bcursor, bscal;
-  DevBuf<uint32_t> bmembers;
+  DevBuf<unsigned> bscnt;
+  DevBuf<uint8_t> bflag;
+  DevBuf<uint32_t> bck, bcv, bcka, bmem;
+  DevBuf<unsigned long long> bscal;
+  DevBuf<int64_t> bstart, bend;
   DevBuf<unsigned char> btemp;
-  DevBuf<double> blb, bulo, buhi;
+  DevBuf<double> blb, bwq;
   DevBuf<int32_t> blist;
-  std::vector<unsigned long long> h_boff;
+  DevBuf<int64_t> branks2;
+  DevBuf<int32_t> bfits2;
+  DevBuf<float2> blines32;
   std::vector<double> h_blb;
   int hough_mode = 0;  // 0 none, 1 image pixels, 2 explicit points
   int64_t hough_npts = 0, hough_width = 1;
@@ -246,17 +250,22 @@ void ctx_release(lms_ctx* c) {
   c->sout.release();
   c->bsample.release();
   c->bbounds.release();
-  c->bid.release();
-  c->bcounts.release();
-  c->boffsets.release();
-  c->bcursor.release();
+  c->bscnt.release();
+  c->bflag.release();
+  c->bck.release();
+  c->bcv.release();
+  c->bcka.release();
+  c->bmem.release();
   c->bscal.release();
-  c->bmembers.release();
+  c->bstart.release();
+  c->bend.release();
   c->btemp.release();
   c->blb.release();
-  c->bulo.release();
-  c->buhi.release();
+  c->bwq.release();
   c->blist.release();
+  c->branks2.release();
+  c->bfits2.release();
+  c->blines32.release();
   if (c->h_best) cudaFreeHost(c->h_best);
   if (c->stream) cudaStreamDestroy(c->stream);
 }
@@ -340,32 +349,33 @@ int order_lines(lms_ctx* c, const std::vector<int64_t>& seg, int64_t F, const do
   return LMS_OK;
 }
 
-// Slope-band search of one large fit (lms_band.cu), after the stratified
-// seeds have put a first record into best[0]: partition the fit's vertices
-// into slope bands, bound every band, seed H from the vertices of the
-// lowest-bound bands, then count windows band by band (lowest bound first)
-// and re-evaluate the survivors exactly.  *used = false when the fit has
-// vertices outside the band stage's fp32 key range (the caller then runs
-// the count filter instead).
-int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st, bool* used) {
-  *used = false;
+// Slope-band search of one large fit (lms_band.cu): bound every slope band,
+// seed H from the samples of the lowest-bound bands, collect the vertices of
+// the bands whose bound admits H, count their windows, and re-evaluate the
+// survivors exactly.  best[0] must be reset; the caller checked that the
+// fit's magnitudes are finite and n <= kBandMaxN.
+int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   const int64_t span = h.r1 - h.r0;
   const int K = (int)std::max<int64_t>(
-      1, std::min<int64_t>(lmsb::kBandMaxK, (span + c->band_vertices - 1) / c->band_vertices));
-  const int64_t S = std::min<int64_t>(span, std::min<int64_t>(1 << 20, std::max<int64_t>(64 * K, 1 << 16)));
+      3, std::min<int64_t>(lmsb::kBandMaxK, (span + c->band_vertices - 1) / c->band_vertices));
+  const int64_t S =
+      std::min<int64_t>(span, std::min<int64_t>(1 << 20, std::max<int64_t>(64 * K, 1 << 16)));
+  constexpr int kSeedBands = 8;
+  const int64_t seed_cap = S;
   RC_TRY(c->bsample.need(2 * S));
   RC_TRY(c->bbounds.need(K));
-  RC_TRY(c->bid.need(span + 16));
-  RC_TRY(c->bcounts.need(K + 1));
-  RC_TRY(c->boffsets.need(K + 1));
-  RC_TRY(c->bcursor.need(K));
-  RC_TRY(c->bscal.need(8));
-  RC_TRY(c->bmembers.need(span));
-  RC_TRY(c->btemp.need((int64_t)std::max(lmsb::band_sample_temp_bytes(S), lmsb::band_scan_temp_bytes(K))));
+  RC_TRY(c->bscnt.need(K));
+  RC_TRY(c->bflag.need(K + 1));
+  RC_TRY(c->bscal.need(5));
+  RC_TRY(c->bstart.need(K + 1));
+  RC_TRY(c->bend.need(K + 1));
   RC_TRY(c->blb.need(K));
-  RC_TRY(c->bulo.need(K));
-  RC_TRY(c->buhi.need(K));
-  RC_TRY(c->blist.need(K));
+  RC_TRY(c->bwq.need(K));
+  RC_TRY(c->blist.need(K + 1));
+  RC_TRY(c->btemp.need((int64_t)lmsb::band_sample_temp_bytes(S)));
+  RC_TRY(c->ranks.need(seed_cap));
+  RC_TRY(c->item_fit.need(seed_cap));
+  RC_TRY(c->recs.need(seed_cap));
 
   lmsb::BandFit bf{};
   bf.a = c->a + h.off;
@@ -385,176 +395,231 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st, bool* used) {
   bf.dev = std::max(ahi - bf.c, bf.c - alo) * (1.0 + 0x1p-40) + 1e-300;
   bf.amax = am;
   bf.bmax = bmx;
-  if (!(am < 1e30) || !(bmx < 1e30)) return LMS_OK;
 
-  unsigned long long* sc = c->bscal.p;  // [0] nvalid [1] nforce [2] seed count [3..] wave counts
-  lmsb::BandPartition bp{};
-  bp.S = S;
-  bp.K = K;
-  bp.sample = c->bsample.p;
-  bp.sample_sorted = c->bsample.p + S;
-  bp.nvalid = sc;
-  bp.bounds = c->bbounds.p;
-  bp.bid = c->bid.p;
-  bp.counts = c->bcounts.p;
-  bp.offsets = c->boffsets.p;
-  bp.cursor = c->bcursor.p;
-  bp.nforce = sc + 1;
-  bp.members = c->bmembers.p;
-  bp.temp = c->btemp.p;
-  bp.temp_bytes = (size_t)c->btemp.cap;
+  // [0] valid samples [1] collected [2] seeds [3] band survivors [4] count survivors
+  unsigned long long* sc = c->bscal.p;
+  lmsb::BandWork w{};
+  w.S = S;
+  w.K = K;
+  w.sample = c->bsample.p;
+  w.sample_sorted = c->bsample.p + S;
+  w.nvalid = sc;
+  w.bounds = c->bbounds.p;
+  w.sample_counts = c->bscnt.p;
+  w.flag = c->bflag.p;
+  w.ncollect = sc + 1;
+  w.start = c->bstart.p;
+  w.end = c->bend.p;
+  w.temp = c->btemp.p;
+  w.temp_bytes = (size_t)c->btemp.cap;
   while (c->ev_chunk.size() < 8) {
     cudaEvent_t e;
     CUDA_TRY(cudaEventCreate(&e));
     c->ev_chunk.push_back(e);
   }
-  CUDA_TRY(cudaEventRecord(c->ev_chunk[0], c->stream));
-  if (lmsb::launch_band_partition(bf, bp, c->sms, c->stream) != 0)
-    return set_error(LMS_ERR_CUDA, "band partition failed");
-  CUDA_TRY(cudaGetLastError());
-  st->launches += 7;
-  CUDA_TRY(cudaEventRecord(c->ev_chunk[1], c->stream));
+  auto exact_list = [&](unsigned long long* d_count, int64_t cap, const int64_t* ranks,
+                        const int32_t* fits) -> int {
+    lmsb::ExactArgs xa{};
+    xa.a = c->a;
+    xa.b = c->b;
+    xa.fits = c->fits.p;
+    xa.mode = lmsb::kSrcList;
+    xa.d_count = d_count;
+    xa.capacity = cap;
+    xa.ranks = ranks;
+    xa.fit_of = fits;
+    xa.bound = c->best.p;
+    xa.out = c->recs.p;
+    lmsb::launch_exact(xa, persistent_grid(c, -1), c->stream, h.n);
+    lmsb::launch_reduce(c->recs.p, d_count, 0, cap, c->fits.p, c->keys.p, c->best.p,
+                        (int)c->sms * 4, c->stream);
+    CUDA_TRY(cudaGetLastError());
+    st->launches += 3;
+    return LMS_OK;
+  };
 
+  // ---- sample, boundaries, per-band lower bounds
+  CUDA_TRY(cudaEventRecord(c->ev_chunk[0], c->stream));
+  if (lmsb::launch_band_sample(bf, w, c->sms, c->stream) != 0)
+    return set_error(LMS_ERR_CUDA, "band sample sort failed");
   lmsb::BandArgs ba{};
-  ba.offsets = c->boffsets.p;
-  ba.members = c->bmembers.p;
-  ba.list = c->blist.p;
+  ba.K = K;
+  ba.bounds = c->bbounds.p;
+  ba.start = c->bstart.p;
+  ba.end = c->bend.p;
   ba.lb = c->blb.p;
-  ba.ulo = c->bulo.p;
-  ba.uhi = c->buhi.p;
+  ba.wq = c->bwq.p;
   ba.best = c->best.p;
-  ba.out_ranks = c->ranks.p;
-  ba.out_fits = c->item_fit.p;
   ba.fit = 0;
   lmsb::launch_band(bf, ba, 0, K, c->stream);
   CUDA_TRY(cudaGetLastError());
-  st->launches += 1;
-  CUDA_TRY(cudaEventRecord(c->ev_chunk[2], c->stream));
-  c->h_boff.resize(K + 1);
-  c->h_blb.resize(K);
-  unsigned long long hsc[2] = {0, 0};
-  CUDA_TRY(cudaMemcpyAsync(c->h_boff.data(), c->boffsets.p, sizeof(unsigned long long) * (K + 1),
-                           cudaMemcpyDeviceToHost, c->stream));
-  CUDA_TRY(cudaMemcpyAsync(c->h_blb.data(), c->blb.p, sizeof(double) * K, cudaMemcpyDeviceToHost,
+  st->launches += 5;
+  CUDA_TRY(cudaEventRecord(c->ev_chunk[1], c->stream));
+  std::vector<double>& lb = c->h_blb;
+  lb.resize(K);
+  std::vector<float> hbnd(K - 1);
+  std::vector<double> wq(K);
+  CUDA_TRY(cudaMemcpyAsync(wq.data(), c->bwq.p, sizeof(double) * K, cudaMemcpyDeviceToHost,
                            c->stream));
-  CUDA_TRY(cudaMemcpyAsync(hsc, sc, sizeof(hsc), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(lb.data(), c->blb.p, sizeof(double) * K, cudaMemcpyDeviceToHost,
+                           c->stream));
+  CUDA_TRY(cudaMemcpyAsync(hbnd.data(), c->bbounds.p, sizeof(float) * (K - 1),
+                           cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
-  if (hsc[1] > 0) return LMS_OK;  // vertices beyond the key range: count filter instead
-  *used = true;
-
-  // bands in ascending bound order
-  std::vector<int32_t> order;
-  order.reserve(K);
-  for (int k = 0; k < K; ++k)
-    if (c->h_boff[k + 1] > c->h_boff[k]) order.push_back(k);
-  std::stable_sort(order.begin(), order.end(),
-                   [&](int32_t x, int32_t y) { return c->h_blb[x] < c->h_blb[y]; });
-  const int nb = (int)order.size();
+  std::vector<int32_t> order(K);
+  for (int k = 0; k < K; ++k) order[k] = k;
+  std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return lb[x] < lb[y]; });
   st->bands = K;
 
-  // capacity: the largest wave (bands of up to kChunkVertices vertices, or one bigger band)
-  int64_t maxband = 0;
-  for (int32_t k : order) maxband = std::max<int64_t>(maxband, (int64_t)(c->h_boff[k + 1] - c->h_boff[k]));
-  constexpr int kSeedBands = 4, kSeedPerBand = 1024;
-  const int64_t cap = std::max<int64_t>({std::min<int64_t>(kChunkVertices, span), maxband,
-                                         (int64_t)kSeedBands * kSeedPerBand});
-  RC_TRY(c->ranks.need(cap));
-  RC_TRY(c->item_fit.need(cap));
-  RC_TRY(c->recs.need(cap));
-  ba.out_ranks = c->ranks.p;
-  ba.out_fits = c->item_fit.p;
-  CUDA_TRY(cudaMemcpyAsync(c->blist.p, order.data(), sizeof(int32_t) * nb, cudaMemcpyHostToDevice,
-                           c->stream));
-
-  // seeds from the most promising bands
-  const int sb = std::min(nb, kSeedBands);
-  CUDA_TRY(cudaMemsetAsync(sc + 2, 0, sizeof(unsigned long long), c->stream));
-  lmsb::launch_band_seeds(bf, c->boffsets.p, c->bmembers.p, c->blist.p, sb, kSeedPerBand,
-                          c->ranks.p, c->item_fit.p, 0, sc + 2, c->stream);
+  // ---- seeds: the samples of the bands with the narrowest q-windows at their
+  // centre slope (the bands an LMS line of that slope would come from)
+  std::vector<uint8_t> flag(K + 1, 0);
   {
-    lmsb::ExactArgs xa{};
-    xa.a = c->a;
-    xa.b = c->b;
-    xa.fits = c->fits.p;
-    xa.mode = lmsb::kSrcList;
-    xa.d_count = sc + 2;
-    xa.capacity = cap;
-    xa.ranks = c->ranks.p;
-    xa.fit_of = c->item_fit.p;
-    xa.bound = c->best.p;
-    xa.out = c->recs.p;
-    lmsb::launch_exact(xa, persistent_grid(c, -1), c->stream, h.n);
-    lmsb::launch_reduce(c->recs.p, sc + 2, 0, cap, c->fits.p, c->keys.p, c->best.p,
-                        (int)c->sms * 4, c->stream);
-    CUDA_TRY(cudaGetLastError());
-    st->launches += 3;
+    std::vector<int32_t> byw(K);
+    for (int k = 0; k < K; ++k) byw[k] = k;
+    std::stable_sort(byw.begin(), byw.end(), [&](int32_t x, int32_t y) { return wq[x] < wq[y]; });
+    for (int e = 0; e < K && e < kSeedBands; ++e)
+      if (std::isfinite(wq[byw[e]])) flag[byw[e]] = 1;
   }
+  CUDA_TRY(cudaMemcpyAsync(c->bflag.p, flag.data(), K, cudaMemcpyHostToDevice, c->stream));
+  lmsb::launch_band_seeds(bf, w, c->ranks.p, c->item_fit.p, 0, seed_cap, sc + 2, c->stream);
+  RC_TRY(exact_list(sc + 2, seed_cap, c->ranks.p, c->item_fit.p));
   lms_candidate hb{};
+  std::vector<unsigned> scnt(K);
   CUDA_TRY(cudaMemcpyAsync(&hb, c->best.p, sizeof(hb), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(scnt.data(), c->bscnt.p, sizeof(unsigned) * K, cudaMemcpyDeviceToHost,
+                           c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   const double H = hb.found ? hb.height : INFINITY;
+  st->seed_height = H;
+
+  // ---- collect the vertices of the bands whose bound admits H
+  std::vector<int32_t> list;
+  double est = 0.0;
+  for (int e = 0; e < K; ++e) {
+    const int32_t k = order[e];
+    if (!(lb[k] <= H * (1.0 + 0x1p-19))) break;  // ascending: the rest cannot reach H
+    list.push_back(k);
+    est += (double)scnt[k] + 2.0;
+  }
+  st->bands_searched = (int64_t)list.size();
+  std::fill(flag.begin(), flag.end(), 0);
+  for (int32_t k : list) flag[k] = 1;
+  list.push_back(K);  // vertices beyond the key range
+  int64_t cap = std::min<int64_t>(span, (int64_t)(2.0 * est * (double)span / (double)S) + 65536);
+  CUDA_TRY(cudaMemcpyAsync(c->bflag.p, flag.data(), K, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->blist.p, list.data(), sizeof(int32_t) * list.size(),
+                           cudaMemcpyHostToDevice, c->stream));
+  // slope runs of the flagged bands for the collect pre-test, merged across the
+  // smallest gaps down to kMaxRuns
+  std::vector<std::pair<int, int>> rr;
+  for (int k = 0; k < K; ++k) {
+    if (!flag[k]) continue;
+    if (!rr.empty() && rr.back().second == k - 1) rr.back().second = k;
+    else rr.push_back({k, k});
+  }
+  while ((int)rr.size() > lmsb::kMaxRuns) {
+    size_t best = 0;
+    for (size_t e = 1; e + 1 < rr.size(); ++e)
+      if (rr[e + 1].first - rr[e].second < rr[best + 1].first - rr[best].second) best = e;
+    rr[best].second = rr[best + 1].second;
+    rr.erase(rr.begin() + best + 1);
+  }
+  lmsb::BandRuns runs{};
+  runs.count = (int)rr.size();
+  for (int e = 0; e < runs.count; ++e) {
+    const int k0 = rr[e].first, k1 = rr[e].second;
+    const double lo = k0 == 0 ? -INFINITY : (double)std::nextafter(hbnd[k0 - 1], -INFINITY);
+    const double hi = k1 == K - 1 ? INFINITY : (double)hbnd[k1];
+    runs.lo[e] = -INFINITY;
+    runs.hi[e] = INFINITY;
+    if (std::isfinite(lo)) {
+      const double w = lo - (0x1p-18 * std::fabs(lo) + 1e-37);
+      float f = (float)w;
+      if ((double)f > w) f = std::nextafter(f, -INFINITY);
+      runs.lo[e] = f;
+    }
+    if (std::isfinite(hi)) {
+      const double w = hi + (0x1p-18 * std::fabs(hi) + 1e-37);
+      float f = (float)w;
+      if ((double)f < w) f = std::nextafter(f, INFINITY);
+      runs.hi[e] = f;
+    }
+  }
+  CUDA_TRY(cudaEventRecord(c->ev_chunk[2], c->stream));
+  unsigned long long m = 0;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    RC_TRY(c->bck.need(cap));
+    RC_TRY(c->bcv.need(cap));
+    w.ckeys = c->bck.p;
+    w.cvals = c->bcv.p;
+    lmsb::launch_band_collect(bf, w, runs, cap, c->sms, c->stream);
+    CUDA_TRY(cudaGetLastError());
+    st->launches += 1;
+    CUDA_TRY(cudaMemcpyAsync(&m, sc + 1, sizeof(m), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    if ((int64_t)m <= cap) break;
+    cap = (int64_t)m;  // estimate too small: collect again with the exact size
+  }
+  RC_TRY(c->bcka.need((int64_t)m));
+  RC_TRY(c->bmem.need((int64_t)m));
+  RC_TRY(c->btemp.need((int64_t)std::max(lmsb::band_sample_temp_bytes(S),
+                                         lmsb::band_group_temp_bytes((int64_t)m))));
+  w.ckeys_alt = c->bcka.p;
+  w.members = c->bmem.p;
+  w.temp = c->btemp.p;
+  w.temp_bytes = (size_t)c->btemp.cap;
+  if (lmsb::launch_band_group(w, (int64_t)m, c->stream) != 0)
+    return set_error(LMS_ERR_CUDA, "band grouping sort failed");
+  CUDA_TRY(cudaGetLastError());
+  st->launches += 3;
   CUDA_TRY(cudaEventRecord(c->ev_chunk[3], c->stream));
 
-  // waves of bands whose bound admits H
-  std::vector<std::pair<int, int>> waves;
-  {
-    int w0 = 0;
-    int64_t acc = 0;
-    int e = 0;
-    for (; e < nb; ++e) {
-      const int32_t k = order[e];
-      if (!(c->h_blb[k] <= H * (1.0 + 0x1p-19))) break;  // sorted: the rest cannot reach H
-      const int64_t sz = (int64_t)(c->h_boff[k + 1] - c->h_boff[k]);
-      if (acc > 0 && acc + sz > cap) {
-        waves.push_back({w0, e});
-        w0 = e;
-        acc = 0;
-      }
-      acc += sz;
-    }
-    if (e > w0) waves.push_back({w0, e});
-    st->bands_searched = e;
-  }
-  const int nw = (int)waves.size();
-  RC_TRY(c->bscal.need(3 + nw + 1));
-  sc = c->bscal.p;
-  CUDA_TRY(cudaMemsetAsync(sc + 3, 0, sizeof(unsigned long long) * (nw + 1), c->stream));
-  for (int w = 0; w < nw; ++w) {
-    ba.list = c->blist.p + waves[w].first;
-    ba.out_count = sc + 3 + w;
-    lmsb::launch_band(bf, ba, 1, waves[w].second - waves[w].first, c->stream);
-    lmsb::ExactArgs xa{};
-    xa.a = c->a;
-    xa.b = c->b;
-    xa.fits = c->fits.p;
-    xa.mode = lmsb::kSrcList;
-    xa.d_count = sc + 3 + w;
-    xa.capacity = cap;
-    xa.ranks = c->ranks.p;
-    xa.fit_of = c->item_fit.p;
-    xa.bound = c->best.p;
-    xa.out = c->recs.p;
-    lmsb::launch_exact(xa, persistent_grid(c, -1), c->stream, h.n);
-    lmsb::launch_reduce(c->recs.p, sc + 3 + w, 0, cap, c->fits.p, c->keys.p, c->best.p,
-                        (int)c->sms * 4, c->stream);
+  // ---- window counts of the collected vertices, exact survivors
+  const int64_t scap = std::max<int64_t>((int64_t)m, 1);
+  RC_TRY(c->ranks.need(scap));
+  RC_TRY(c->item_fit.need(scap));
+  RC_TRY(c->recs.need(scap));
+  RC_TRY(c->branks2.need(scap));
+  RC_TRY(c->bfits2.need(scap));
+  RC_TRY(c->blines32.need(h.n));
+  ba.members = c->bmem.p;
+  ba.list = c->blist.p;
+  ba.out_ranks = c->ranks.p;
+  ba.out_fits = c->item_fit.p;
+  ba.out_count = sc + 3;
+  CUDA_TRY(cudaMemsetAsync(sc + 3, 0, 2 * sizeof(unsigned long long), c->stream));
+  if (m > 0) {
+    lmsb::launch_band(bf, ba, 1, (int)list.size(), c->stream);
+    lmsb::BandCount bc{};
+    bc.lines = c->blines32.p;
+    bc.best = c->best.p;
+    bc.in_ranks = c->ranks.p;
+    bc.in_count = sc + 3;
+    bc.out_ranks = c->branks2.p;
+    bc.out_fits = c->bfits2.p;
+    bc.fit = 0;
+    bc.out_count = sc + 4;
+    lmsb::launch_band_count(bf, bc, c->sms, c->stream);
     CUDA_TRY(cudaGetLastError());
-    st->launches += 3;
+    st->launches += 4;
+    RC_TRY(exact_list(sc + 4, scap, c->branks2.p, c->bfits2.p));
   }
   CUDA_TRY(cudaEventRecord(c->ev_chunk[4], c->stream));
-  std::vector<unsigned long long> wc(nw + 1, 0);
-  CUDA_TRY(cudaMemcpyAsync(wc.data(), sc + 3, sizeof(unsigned long long) * (nw + 1),
-                           cudaMemcpyDeviceToHost, c->stream));
+  unsigned long long nsurv[2] = {0, 0};
+  CUDA_TRY(cudaMemcpyAsync(nsurv, sc + 3, sizeof(nsurv), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
-  for (int w = 0; w < nw; ++w) st->survivors += (int64_t)wc[w];
-  st->chunks = nw;
+  st->survivors = (int64_t)nsurv[1];
+  st->band_survivors = (int64_t)nsurv[0];
+  st->filtered_vertices = (int64_t)m;
+  st->chunks = 1;
   float ms = 0.f;
   CUDA_TRY(cudaEventElapsedTime(&ms, c->ev_chunk[0], c->ev_chunk[1]));
-  st->ms_partition = ms;
-  CUDA_TRY(cudaEventElapsedTime(&ms, c->ev_chunk[1], c->ev_chunk[2]));
   st->ms_bound = ms;
+  CUDA_TRY(cudaEventElapsedTime(&ms, c->ev_chunk[2], c->ev_chunk[3]));
+  st->ms_partition = ms;
   CUDA_TRY(cudaEventElapsedTime(&ms, c->ev_chunk[3], c->ev_chunk[4]));
   st->ms_band_filter = ms;
-  st->filtered_vertices = span;
   return LMS_OK;
 }
 
@@ -575,12 +640,20 @@ int ctx_solve_fits(lms_ctx* c, const std::vector<HostFit>& hf, lms_candidate* ou
   std::vector<int64_t> prefA(F + 1), prefB(F + 1), seed_pref(F + 1), seg(F + 1);
   int64_t rowsA = 0, rows = 0, tasks = 0, tasksA = 0, seeds = 0;
   bool disjoint = true;
+  bool banded = false;
   for (int64_t f = 0; f < F; ++f) {
     const HostFit& h = hf[f];
     const int64_t span = h.r1 - h.r0;
     const bool exhaustive = span <= kExhaustive;
+    double am = 0.0, bm = 0.0;
+    for (int64_t k = h.off; k < h.off + h.n; ++k) {
+      am = std::max(am, std::fabs(c->h_a[k]));
+      bm = std::max(bm, std::fabs(c->h_b[k]));
+    }
+    if (F == 1 && c->band_mode && !exhaustive && h.n <= lmsb::kBandMaxN && am < 1e30 && bm < 1e30)
+      banded = true;  // slope-band stage instead of seeds + count filter
     int64_t s = exhaustive ? span : std::min(kSeedsMax, std::max(kSeedsMin, span / kSeedDivisor));
-    s = std::min(s, span);
+    s = banded ? 0 : std::min(s, span);
     lmsb::FitDesc& d = fd[f];
     d.off = h.off;
     d.n = h.n;
@@ -589,7 +662,7 @@ int ctx_solve_fits(lms_ctx* c, const std::vector<HostFit>& hf, lms_candidate* ou
     d.rank_hi = h.r1;
     d.row0 = 0;
     d.nrows = 0;
-    if (!exhaustive) {
+    if (!exhaustive && !banded) {
       tasks += lmsb::fit_tasks(h.n, h.r0, h.r1, tv, &d.row0, &d.nrows);
       for (int64_t k = 0; k < d.nrows; k += lmsb::kPhaseStride)
         tasksA += lmsb::row_tasks(h.n, h.r0, h.r1, d.row0 + k, tv);
@@ -597,11 +670,6 @@ int ctx_solve_fits(lms_ctx* c, const std::vector<HostFit>& hf, lms_candidate* ou
     prefA[f] = rowsA;
     rowsA += (d.nrows + lmsb::kPhaseStride - 1) / lmsb::kPhaseStride;
     rows += d.nrows;
-    double am = 0.0, bm = 0.0;
-    for (int64_t k = h.off; k < h.off + h.n; ++k) {
-      am = std::max(am, std::fabs(c->h_a[k]));
-      bm = std::max(bm, std::fabs(c->h_b[k]));
-    }
     d.amax = am;
     d.bmax = bm;
     seed_pref[f] = seeds;
@@ -671,9 +739,7 @@ int ctx_solve_fits(lms_ctx* c, const std::vector<HostFit>& hf, lms_candidate* ou
   }
 
   // ---- band path: one large fit with lines in shared-memory range
-  bool banded = false;
-  if (F == 1 && c->band_mode && tasks > 0 && hf[0].n <= lmsb::kBandMaxN && hf[0].n <= 65536)
-    RC_TRY(band_solve(c, hf[0], &st, &banded));
+  if (banded) RC_TRY(band_solve(c, hf[0], &st));
 
   // ---- 2.-5. filter the non-exhaustive fits: phase A (every kPhaseStride-th
   // row), re-order, phase B (the rest)
