@@ -66,6 +66,7 @@ namespace {
 constexpr int kCollectThreads = 512;
 constexpr unsigned kSeedPerBand = 160;  // sampled vertices per seed band
 constexpr int kRun = 32;  // ranks per lane per warp segment (lane-interleaved)
+constexpr int kSlopeBits = 17;  // within-band slope order bits of a collected key
 
 __device__ __forceinline__ float band_key(double u) {
   // monotone non-decreasing map of the slope to fp32 (clamped, so ordered)
@@ -248,17 +249,29 @@ __global__ void __launch_bounds__(kThreads, 1) band_bound_kernel(BandFit bf, Ban
   }
 }
 
-// mode 1: window counts of every collected member of the listed bands
+// mode 1: window counts of the collected members, one CTA per chunk of up to
+// kChunk members of a listed band (members are slope-ordered within their
+// band, so a chunk spans a narrow slope range and gets its own centre uM,
+// sorted keys, padding D and lower bound)
 template <int kThreads, int kItems>
 __global__ void __launch_bounds__(kThreads, 1) band_filter_kernel(BandFit bf, BandArgs ba) {
   using SH = BandShared<kThreads, kItems>;
   extern __shared__ __align__(16) unsigned char band_smem[];
   SH& sh = *reinterpret_cast<SH*>(band_smem);
-  const int band = ba.list[blockIdx.x];
-  const int64_t m0 = ba.start[band];
-  const int64_t m1 = ba.end[band];
   const int tid = threadIdx.x;
   const int lane = tid & 31;
+  // chunk -> (listed band, chunk index)
+  const int64_t cidx = blockIdx.x;
+  if (cidx >= ba.chunk_prefix[ba.nlist]) return;
+  int lo = 0, hi = ba.nlist - 1;  // largest e with chunk_prefix[e] <= cidx
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (ba.chunk_prefix[mid] <= cidx) lo = mid;
+    else hi = mid - 1;
+  }
+  const int band = ba.list[lo];
+  const int64_t m0 = ba.start[band] + (cidx - ba.chunk_prefix[lo]) * ba.chunk;
+  const int64_t m1 = min(ba.end[band], m0 + ba.chunk);
   if (m1 <= m0) return;
   double H = INFINITY;
   {
@@ -266,27 +279,34 @@ __global__ void __launch_bounds__(kThreads, 1) band_filter_kernel(BandFit bf, Ba
     if (best.found) H = best.height;
   }
   bool all = band >= ba.K;  // the beyond-range pseudo band: every member survives
+  if (!all && ba.lb[band] > H * (1.0 + 0x1p-19)) return;  // H tightened since collection
   double uL = 0.0, uR = 0.0;
-  if (!all && !boundary_extent(ba.bounds, ba.K, band, &uL, &uR)) {
-    double lo = INFINITY, hi = -INFINITY;
+  if (!all) {
+    double l = INFINITY, h = -INFINITY;
     for (int64_t s = m0 + tid; s < m1; s += kThreads) {
       const uint32_t p = ba.members[s];
       const int64_t i = p >> 16, j = p & 0xFFFF;
       const double u = __ddiv_rn(__dsub_rn(bf.b[i], bf.b[j]), __dsub_rn(bf.a[i], bf.a[j]));
-      lo = fmin(lo, u);
-      hi = fmax(hi, u);
+      l = fmin(l, u);
+      h = fmax(h, u);
     }
-    uL = block_min<kThreads>(lo, sh.red[0]);
-    uR = -block_min<kThreads>(-hi, sh.red[1]);
-  }
-  if (!all) {
-    if (ba.lb[band] > H * (1.0 + 0x1p-19)) return;  // H tightened since collection
+    uL = block_min<kThreads>(l, sh.red[0]);
+    uR = -block_min<kThreads>(-h, sh.red[1]);
     all = !(isfinite(uL) && isfinite(uR)) || !keys_in_range(bf, uL, uR);
   }
   const double uM = 0.5 * uL + 0.5 * uR;
-  if (!all) band_keys<kThreads, kItems>(bf, uM, sh);
   const float* K = sh.keys;
   const int n = (int)bf.n, q = (int)bf.q;
+  if (!all) {
+    band_keys<kThreads, kItems>(bf, uM, sh);
+    // the chunk's own lower bound (as band_bound_kernel, with its narrower extent)
+    double w = INFINITY;
+    for (int k = tid; k + q - 1 < n; k += kThreads) w = fmin(w, (double)K[k + q - 1] - (double)K[k]);
+    w = block_min<kThreads>(w, sh.red[0]);
+    const double dmax = bf.dev * fmax(uR - uM, uM - uL) * (1.0 + 0x1p-40);
+    const double e = slack_base(bf, fmax(fabs(uL), fabs(uR)), uM) + 0x1p-20 * H + 1e-300;
+    if ((w - 2.0 * dmax - 2.0 * e) * (1.0 - 0x1p-40) > H) return;
+  }
   for (int64_t s0 = m0; s0 < m1; s0 += kThreads) {
     const int64_t s = s0 + tid;
     bool keep = false;
@@ -324,6 +344,22 @@ __global__ void __launch_bounds__(kThreads, 1) band_filter_kernel(BandFit bf, Ba
         ba.out_fits[base + slot] = ba.fit;
       }
     }
+  }
+}
+
+// chunk_prefix[e] = first chunk of listed band e (single block; nlist small)
+__global__ void band_chunks_kernel(const int32_t* __restrict__ list, int nlist,
+                                   const int64_t* __restrict__ start,
+                                   const int64_t* __restrict__ end, int64_t chunk,
+                                   int64_t* __restrict__ prefix) {
+  if (threadIdx.x == 0) {
+    int64_t acc = 0;
+    for (int e = 0; e < nlist; ++e) {
+      prefix[e] = acc;
+      const int64_t sz = end[list[e]] - start[list[e]];
+      acc += (sz + chunk - 1) / chunk;
+    }
+    prefix[nlist] = acc;
   }
 }
 
@@ -409,12 +445,21 @@ __global__ void __launch_bounds__(kCollectThreads) band_collect_kernel(
       const int cls = classify(bf, __ldg(bf.a + i), __ldg(bf.b + i), __ldg(bf.a + j),
                                __ldg(bf.b + j), &u);
       if (cls == 1) {
-        const int band = band_of(bnd, K - 1, band_key(u));
+        const float bk = band_key(u);
+        const int band = band_of(bnd, K - 1, bk);
         take = fl[band] != 0;
-        key = (uint32_t)band;
+        // members of a band ordered by slope: kSlopeBits of fixed-point position
+        // between the band's boundaries (monotone in u; 0 in the outer bands)
+        uint32_t t = 0;
+        if (band > 0 && band < K - 1) {
+          const float lo = bnd[band - 1], w = bnd[band] - lo;
+          const float f = w > 0.f ? (bk - lo) / w * (float)(1 << kSlopeBits) : 0.f;
+          t = (uint32_t)fminf(fmaxf(f, 0.f), (float)((1 << kSlopeBits) - 1));
+        }
+        key = ((uint32_t)band << kSlopeBits) | t;
       } else if (cls == 2) {
         take = true;
-        key = (uint32_t)K;
+        key = (uint32_t)K << kSlopeBits;
       }
     }
     const unsigned mask = __ballot_sync(0xffffffffu, take);
@@ -491,8 +536,8 @@ __global__ void __launch_bounds__(kCollectThreads) band_collect_kernel(
 // + bmax) + subnormal steps) and the reference's own (see the file header).
 // Removes the band padding D_v, so only vertices whose windows really can
 // reach H go on to the exact select.
-constexpr int kCountThreads = 256;
-constexpr int kCountChunk = 2048;
+constexpr int kCountThreads = 512;
+constexpr int kCountWarps = kCountThreads / 32;
 
 __global__ void band_lines32_kernel(BandFit bf, float2* __restrict__ lines) {
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < bf.n;
@@ -500,25 +545,34 @@ __global__ void band_lines32_kernel(BandFit bf, float2* __restrict__ lines) {
     lines[k] = make_float2((float)__dsub_rn(bf.a[k], bf.c), (float)bf.b[k]);
 }
 
+// Persistent: all n lines staged once per CTA in shared memory; a tile is 32
+// survivors (one per lane), every warp counts its slice of the lines for all
+// 32, and the slices' counts are summed in shared memory.
 __global__ void __launch_bounds__(kCountThreads) band_count_kernel(
     BandFit bf, const float2* __restrict__ lines, const lms_candidate* __restrict__ best,
     const int64_t* __restrict__ in_ranks, const unsigned long long* __restrict__ in_count,
     int64_t* __restrict__ out_ranks, int32_t* __restrict__ out_fits, int32_t fit,
-    unsigned long long* __restrict__ out_count) {
-  __shared__ float2 sl[kCountChunk];
+    unsigned long long* __restrict__ out_count, int32_t* __restrict__ out_margin) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float2* sl = reinterpret_cast<float2*>(smem_raw);
+  unsigned* cnt = reinterpret_cast<unsigned*>(sl + bf.n);  // [2][32]
   const int64_t total = (int64_t)*in_count;
   const int tid = threadIdx.x;
   const int lane = tid & 31;
+  const int warp = tid >> 5;
   const int n = (int)bf.n;
   const int q = (int)bf.q;
+  if ((int64_t)blockIdx.x * 32 >= total) return;
+  for (int k = tid; k < n; k += kCountThreads) sl[k] = lines[k];
   double H = INFINITY;
   {
     const lms_candidate b0 = *best;
     if (b0.found) H = b0.height;
   }
-  for (int64_t t0 = (int64_t)blockIdx.x * kCountThreads; t0 < total;
-       t0 += (int64_t)gridDim.x * kCountThreads) {
-    const int64_t s = t0 + tid;
+  const int per = (n + kCountWarps - 1) / kCountWarps;
+  const int k0 = warp * per, k1 = min(n, k0 + per);
+  for (int64_t t0 = (int64_t)blockIdx.x * 32; t0 < total; t0 += (int64_t)gridDim.x * 32) {
+    const int64_t s = t0 + lane;
     const bool live = s < total;
     int64_t rank = 0;
     bool force = !isfinite(H) || (bf.amax > 0.0 && bf.amax < 1e-30) ||
@@ -541,32 +595,37 @@ __global__ void __launch_bounds__(kCountThreads) band_count_kernel(
       dnLo = __double2float_rd(z - H - E);
       dnHi = __double2float_ru(z + E);
     }
-    int cu = 0, cd = 0;
-    for (int k0 = 0; k0 < n; k0 += kCountChunk) {
-      const int cnt = n - k0 < kCountChunk ? n - k0 : kCountChunk;
-      __syncthreads();
-      for (int k = tid; k < cnt; k += kCountThreads) sl[k] = lines[k0 + k];
-      __syncthreads();
+    if (tid < 64) cnt[tid] = 0u;
+    __syncthreads();  // also orders the line staging before first use
+    unsigned cu = 0, cd = 0;
 #pragma unroll 8
-      for (int k = 0; k < cnt; ++k) {
-        const float2 L = sl[k];
-        const float t = fmaf(L.x, u32, -L.y);
-        cu += (t >= upLo) & (t <= upHi);
-        cd += (t >= dnLo) & (t <= dnHi);
+    for (int k = k0; k < k1; ++k) {
+      const float2 L = sl[k];
+      const float t = fmaf(L.x, u32, -L.y);
+      cu += (t >= upLo) & (t <= upHi);
+      cd += (t >= dnLo) & (t <= dnHi);
+    }
+    atomicAdd(cnt + lane, cu);
+    atomicAdd(cnt + 32 + lane, cd);
+    __syncthreads();
+    if (warp == 0) {
+      const int tu = (int)cnt[lane], td = (int)cnt[32 + lane];
+      const bool keep = live && (force || tu >= q || td >= q);
+      const unsigned mask = __ballot_sync(0xffffffffu, keep);
+      if (mask) {
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(out_count, (unsigned long long)__popc(mask));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (keep) {
+          const unsigned slot = __popc(mask & ((1u << lane) - 1u));
+          out_ranks[base + slot] = rank;
+          out_fits[base + slot] = fit;
+          // lines inside the better window beyond q: more means a lower height
+          if (out_margin) out_margin[base + slot] = force ? 0x7fffffff : max(tu, td) - q;
+        }
       }
     }
-    const bool keep = live && (force || cu >= q || cd >= q);
-    const unsigned mask = __ballot_sync(0xffffffffu, keep);
-    if (mask) {
-      unsigned long long base = 0;
-      if (lane == 0) base = atomicAdd(out_count, (unsigned long long)__popc(mask));
-      base = __shfl_sync(0xffffffffu, base, 0);
-      if (keep) {
-        const unsigned slot = __popc(mask & ((1u << lane) - 1u));
-        out_ranks[base + slot] = rank;
-        out_fits[base + slot] = fit;
-      }
-    }
+    __syncthreads();
   }
 }
 
@@ -574,9 +633,9 @@ __global__ void band_runs_kernel(const uint32_t* __restrict__ keys, int64_t m,
                                  int64_t* __restrict__ start, int64_t* __restrict__ end) {
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < m;
        p += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t k = keys[p];
-    if (p == 0 || keys[p - 1] != k) start[k] = p;
-    if (p == m - 1 || keys[p + 1] != k) end[k] = p + 1;
+    const uint32_t k = keys[p] >> kSlopeBits;
+    if (p == 0 || (keys[p - 1] >> kSlopeBits) != k) start[k] = p;
+    if (p == m - 1 || (keys[p + 1] >> kSlopeBits) != k) end[k] = p + 1;
   }
 }
 
@@ -639,6 +698,9 @@ int launch_band_sample(const BandFit& bf, const BandWork& w, int sms, cudaStream
 
 void launch_band(const BandFit& bf, const BandArgs& ba, int mode, int grid, cudaStream_t st) {
   if (grid <= 0) return;
+  if (mode == 1)
+    band_chunks_kernel<<<1, 32, 0, st>>>(ba.list, ba.nlist, ba.start, ba.end, ba.chunk,
+                                         ba.chunk_prefix);
   if (bf.n <= 1024) launch_band_t<256, 4>(bf, ba, mode, grid, st);
   else if (bf.n <= 4096) launch_band_t<512, 8>(bf, ba, mode, grid, st);
   else launch_band_t<1024, 16>(bf, ba, mode, grid, st);
@@ -663,11 +725,33 @@ void launch_band_collect(const BandFit& bf, const BandWork& w, const BandRuns& r
 }
 
 void launch_band_count(const BandFit& bf, const BandCount& bc, int sms, cudaStream_t st) {
-  band_lines32_kernel<<<(int)((bf.n + 255) / 256), 256, 0, st>>>(bf, bc.lines);
+  if (bc.make_lines) band_lines32_kernel<<<(int)((bf.n + 255) / 256), 256, 0, st>>>(bf, bc.lines);
   cudaMemsetAsync(bc.out_count, 0, sizeof(unsigned long long), st);
-  band_count_kernel<<<sms * 8, kCountThreads, 0, st>>>(bf, bc.lines, bc.best, bc.in_ranks,
-                                                       bc.in_count, bc.out_ranks, bc.out_fits,
-                                                       bc.fit, bc.out_count);
+  const size_t smem = (size_t)bf.n * sizeof(float2) + 64 * sizeof(unsigned);
+  static bool done = false;
+  set_smem(band_count_kernel, (size_t)kBandMaxN * sizeof(float2) + 64 * sizeof(unsigned), &done);
+  band_count_kernel<<<sms, kCountThreads, smem, st>>>(bf, bc.lines, bc.best, bc.in_ranks,
+                                                      bc.in_count, bc.out_ranks, bc.out_fits,
+                                                      bc.fit, bc.out_count, bc.out_margin);
+}
+
+size_t band_order_temp_bytes(int64_t m) {
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, (const int32_t*)nullptr,
+                                            (int32_t*)nullptr, (const int64_t*)nullptr,
+                                            (int64_t*)nullptr, (int)m);
+  return bytes;
+}
+
+int launch_band_order(const int32_t* margin_in, int32_t* margin_out, const int64_t* ranks_in,
+                      int64_t* ranks_out, int64_t m, void* temp, size_t temp_bytes,
+                      cudaStream_t st) {
+  if (m <= 0) return 0;
+  size_t bytes = temp_bytes;
+  return cub::DeviceRadixSort::SortPairsDescending(temp, bytes, margin_in, margin_out, ranks_in,
+                                                   ranks_out, (int)m, 0, 32, st) == cudaSuccess
+             ? 0
+             : -1;
 }
 
 int launch_band_group(const BandWork& w, int64_t m, cudaStream_t st) {
@@ -676,7 +760,7 @@ int launch_band_group(const BandWork& w, int64_t m, cudaStream_t st) {
   if (m <= 0) return 0;
   size_t bytes = w.temp_bytes;
   if (cub::DeviceRadixSort::SortPairs(w.temp, bytes, w.ckeys, w.ckeys_alt, w.cvals, w.members,
-                                      (int)m, 0, bits_for(w.K), st) != cudaSuccess)
+                                      (int)m, 0, kSlopeBits + bits_for(w.K), st) != cudaSuccess)
     return -1;
   band_runs_kernel<<<(int)std::min<int64_t>((m + 255) / 256, 4096), 256, 0, st>>>(
       w.ckeys_alt, m, w.start, w.end);

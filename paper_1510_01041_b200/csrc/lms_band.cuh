@@ -61,7 +61,10 @@ struct BandArgs {
   const int64_t* start;
   const int64_t* end;
   const uint32_t* members;
-  const int32_t* list;        // filter: bands to process (blockIdx -> band)
+  const int32_t* list;        // filter: bands to process
+  int nlist;
+  int64_t chunk;              // filter: members per CTA
+  int64_t* chunk_prefix;      // nlist + 1 scratch: first chunk of every listed band
   double* lb;                 // per band lower bound of any vertex height (-inf: unknown)
   double* wq;                 // per band narrowest q-window of the keys at the band centre
   const lms_candidate* best;  // the fit's current best record (H)
@@ -81,13 +84,20 @@ struct BandCount {
   int32_t* out_fits;
   int32_t fit;
   unsigned long long* out_count;
+  int32_t* out_margin;  // optional: max(window counts) - q per survivor
+  bool make_lines;      // fill `lines` first
 };
 
 size_t band_sample_temp_bytes(int64_t S);
+size_t band_order_temp_bytes(int64_t m);
+// survivors by descending margin (CUB radix sort)
+int launch_band_order(const int32_t* margin_in, int32_t* margin_out, const int64_t* ranks_in,
+                      int64_t* ranks_out, int64_t m, void* temp, size_t temp_bytes,
+                      cudaStream_t st);
 size_t band_group_temp_bytes(int64_t m);
 size_t band_collect_smem(int K);
 int launch_band_sample(const BandFit& bf, const BandWork& w, int sms, cudaStream_t st);
-// mode 0: grid = K (lower bound of every band); mode 1: grid = bands in ba.list
+// mode 0: grid = K (lower bound of every band); mode 1: grid >= chunks of the listed bands
 void launch_band(const BandFit& bf, const BandArgs& ba, int mode, int grid, cudaStream_t st);
 void launch_band_seeds(const BandFit& bf, const BandWork& w, int64_t* ranks, int32_t* fits,
                        int32_t fit, int64_t cap, unsigned long long* count, cudaStream_t st);

@@ -152,7 +152,8 @@ struct lms_ctx {
   DevBuf<int64_t> rbin, scounts, soffsets, sout;
   // slope bands (lms_band.cu)
   int band_mode = 1;             // LMSB_BAND=0 disables (count-filter path, for A/B runs)
-  int64_t band_vertices = 16384; // target vertices per band (LMSB_BAND_VERTICES)
+  int64_t band_vertices = 131072; // target vertices per band (LMSB_BAND_VERTICES)
+  int64_t band_chunk = 4096;     // collected members per filter CTA (LMSB_BAND_CHUNK)
   DevBuf<float> bsample, bbounds;
   DevBuf<unsigned> bscnt;
   DevBuf<uint8_t> bflag;
@@ -163,7 +164,8 @@ struct lms_ctx {
   DevBuf<double> blb, bwq;
   DevBuf<int32_t> blist;
   DevBuf<int64_t> branks2;
-  DevBuf<int32_t> bfits2;
+  DevBuf<int32_t> bfits2, bmargin;
+  DevBuf<int64_t> bchunks;
   DevBuf<float2> blines32;
   std::vector<double> h_blb;
   int hough_mode = 0;  // 0 none, 1 image pixels, 2 explicit points
@@ -187,6 +189,8 @@ int ctx_init(lms_ctx* c, int device) {
   c->band_mode = (bm && std::strcmp(bm, "0") == 0) ? 0 : 1;
   const char* bv = getenv("LMSB_BAND_VERTICES");
   if (bv && atoll(bv) >= 256) c->band_vertices = atoll(bv);
+  const char* bc = getenv("LMSB_BAND_CHUNK");
+  if (bc && atoll(bc) >= 32) c->band_chunk = atoll(bc);
   CUDA_TRY(cudaSetDevice(device));
   CUDA_TRY(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device));
   CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
@@ -265,6 +269,8 @@ void ctx_release(lms_ctx* c) {
   c->blist.release();
   c->branks2.release();
   c->bfits2.release();
+  c->bmargin.release();
+  c->bchunks.release();
   c->blines32.release();
   if (c->h_best) cudaFreeHost(c->h_best);
   if (c->stream) cudaStreamDestroy(c->stream);
@@ -417,6 +423,8 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     CUDA_TRY(cudaEventCreate(&e));
     c->ev_chunk.push_back(e);
   }
+  // exact select + reduce of a survivor list: d_count on the device, or the
+  // first `cap` entries when d_count is null
   auto exact_list = [&](unsigned long long* d_count, int64_t cap, const int64_t* ranks,
                         const int32_t* fits) -> int {
     lmsb::ExactArgs xa{};
@@ -425,14 +433,15 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     xa.fits = c->fits.p;
     xa.mode = lmsb::kSrcList;
     xa.d_count = d_count;
+    xa.count = cap;
     xa.capacity = cap;
     xa.ranks = ranks;
     xa.fit_of = fits;
     xa.bound = c->best.p;
     xa.out = c->recs.p;
     lmsb::launch_exact(xa, persistent_grid(c, -1), c->stream, h.n);
-    lmsb::launch_reduce(c->recs.p, d_count, 0, cap, c->fits.p, c->keys.p, c->best.p,
-                        (int)c->sms * 4, c->stream);
+    lmsb::launch_reduce(c->recs.p, d_count, d_count ? 0 : cap, cap, c->fits.p, c->keys.p,
+                        c->best.p, (int)c->sms * 4, c->stream);
     CUDA_TRY(cudaGetLastError());
     st->launches += 3;
     return LMS_OK;
@@ -575,22 +584,31 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   st->launches += 3;
   CUDA_TRY(cudaEventRecord(c->ev_chunk[3], c->stream));
 
-  // ---- window counts of the collected vertices, exact survivors
+  // ---- window counts of the collected vertices; fp32 counts at each
+  // survivor's own slope; exact select of the most promising few (tightens H),
+  // counts again against the tightened H, exact select of the rest
   const int64_t scap = std::max<int64_t>((int64_t)m, 1);
   RC_TRY(c->ranks.need(scap));
   RC_TRY(c->item_fit.need(scap));
   RC_TRY(c->recs.need(scap));
-  RC_TRY(c->branks2.need(scap));
+  RC_TRY(c->branks2.need(2 * scap));
   RC_TRY(c->bfits2.need(scap));
+  RC_TRY(c->bmargin.need(2 * scap));
   RC_TRY(c->blines32.need(h.n));
+  RC_TRY(c->bchunks.need((int64_t)list.size() + 1));
   ba.members = c->bmem.p;
   ba.list = c->blist.p;
+  ba.nlist = (int)list.size();
+  ba.chunk = c->band_chunk;
+  ba.chunk_prefix = c->bchunks.p;
   ba.out_ranks = c->ranks.p;
   ba.out_fits = c->item_fit.p;
   ba.out_count = sc + 3;
   CUDA_TRY(cudaMemsetAsync(sc + 3, 0, 2 * sizeof(unsigned long long), c->stream));
+  unsigned long long m2 = 0, m3 = 0, m1 = 0;
   if (m > 0) {
-    lmsb::launch_band(bf, ba, 1, (int)list.size(), c->stream);
+    lmsb::launch_band(bf, ba, 1, (int)(((int64_t)m + ba.chunk - 1) / ba.chunk + ba.nlist),
+                      c->stream);
     lmsb::BandCount bc{};
     bc.lines = c->blines32.p;
     bc.best = c->best.p;
@@ -600,17 +618,49 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     bc.out_fits = c->bfits2.p;
     bc.fit = 0;
     bc.out_count = sc + 4;
+    bc.out_margin = c->bmargin.p;
+    bc.make_lines = true;
     lmsb::launch_band_count(bf, bc, c->sms, c->stream);
     CUDA_TRY(cudaGetLastError());
     st->launches += 4;
-    RC_TRY(exact_list(sc + 4, scap, c->branks2.p, c->bfits2.p));
+    unsigned long long cnts[2] = {0, 0};
+    CUDA_TRY(cudaMemcpyAsync(cnts, sc + 3, sizeof(cnts), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    m1 = cnts[0];
+    m2 = cnts[1];
+  }
+  if (m2 > 0) {
+    constexpr int64_t kFirstWave = 128;
+    int64_t* sorted = c->branks2.p + scap;
+    RC_TRY(c->btemp.need((int64_t)std::max(lmsb::band_order_temp_bytes((int64_t)m2),
+                                           (size_t)c->btemp.cap)));
+    if (lmsb::launch_band_order(c->bmargin.p, c->bmargin.p + scap, c->branks2.p, sorted,
+                                (int64_t)m2, c->btemp.p, (size_t)c->btemp.cap, c->stream) != 0)
+      return set_error(LMS_ERR_CUDA, "survivor ordering sort failed");
+    RC_TRY(exact_list(nullptr, std::min<int64_t>(kFirstWave, (int64_t)m2), sorted, c->bfits2.p));
+    if ((int64_t)m2 > kFirstWave) {
+      lmsb::BandCount bc{};
+      bc.lines = c->blines32.p;
+      bc.best = c->best.p;
+      bc.in_ranks = sorted + kFirstWave;
+      bc.in_count = sc + 4;  // the rest of the ordered survivors (staged below)
+      bc.out_ranks = c->ranks.p;
+      bc.out_fits = c->item_fit.p;
+      bc.fit = 0;
+      bc.out_count = sc + 3;
+      bc.out_margin = nullptr;
+      bc.make_lines = false;
+      const unsigned long long rest = m2 - kFirstWave;
+      CUDA_TRY(cudaMemcpyAsync(sc + 4, &rest, sizeof(rest), cudaMemcpyHostToDevice, c->stream));
+      lmsb::launch_band_count(bf, bc, c->sms, c->stream);
+      RC_TRY(exact_list(sc + 3, scap, c->ranks.p, c->item_fit.p));
+      CUDA_TRY(cudaMemcpyAsync(&m3, sc + 3, sizeof(m3), cudaMemcpyDeviceToHost, c->stream));
+    }
   }
   CUDA_TRY(cudaEventRecord(c->ev_chunk[4], c->stream));
-  unsigned long long nsurv[2] = {0, 0};
-  CUDA_TRY(cudaMemcpyAsync(nsurv, sc + 3, sizeof(nsurv), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
-  st->survivors = (int64_t)nsurv[1];
-  st->band_survivors = (int64_t)nsurv[0];
+  st->survivors = (int64_t)std::min<unsigned long long>(m2, 128) + (int64_t)m3;
+  st->band_survivors = (int64_t)m1;
   st->filtered_vertices = (int64_t)m;
   st->chunks = 1;
   float ms = 0.f;
