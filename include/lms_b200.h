@@ -77,8 +77,8 @@ typedef struct lms_stats {
   int64_t bands_searched;   /* bands whose lower bound admitted the bound H */
   float ms_partition;       /* sample + band histogram + scatter */
   float ms_bound;           /* per-band sorted keys and lower bounds */
-  float ms_band_filter;     /* band-seeded exact records + window counts + exact survivors */
-  float reserved2;
+  float ms_band_filter;     /* chunk window counts + fp32 counts + exact survivors */
+  float ms_collect;         /* the collect pass alone (last attempt) */
   double seed_height;       /* the bound H the band stage collected with */
   int64_t band_survivors;   /* collected vertices whose band window counts reached q */
 } lms_stats;

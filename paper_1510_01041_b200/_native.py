@@ -67,7 +67,7 @@ class Stats(ctypes.Structure):
         ("ms_partition", ctypes.c_float),
         ("ms_bound", ctypes.c_float),
         ("ms_band_filter", ctypes.c_float),
-        ("reserved2", ctypes.c_float),
+        ("ms_collect", ctypes.c_float),
         ("seed_height", ctypes.c_double),
         ("band_survivors", ctypes.c_int64),
     ]

@@ -71,6 +71,7 @@ constexpr int64_t kSeedsMin = 64;            // ... per small fit
 constexpr int64_t kSeedDivisor = 2048;       // seeds = span / kSeedDivisor, clamped
 constexpr int64_t kExhaustive = 4096;        // fits this small skip the filter
 constexpr int64_t kChunkVertices = 1 << 24;  // filter chunk (and survivor capacity)
+constexpr int64_t kBandMinSpan = 1 << 21;    // smaller fits: seeds + count filter are faster
 constexpr int kNumEvents = 16;
 
 template <typename T>
@@ -151,7 +152,7 @@ struct lms_ctx {
   DevBuf<double> tcos, tsin;
   DevBuf<int64_t> rbin, scounts, soffsets, sout;
   // slope bands (lms_band.cu)
-  int band_mode = 1;             // LMSB_BAND=0 disables (count-filter path, for A/B runs)
+  int band_mode = 1;  // LMSB_BAND: 0 count-filter path only, 1 auto (large fits), 2 always
   int64_t band_vertices = 131072; // target vertices per band (LMSB_BAND_VERTICES)
   int64_t band_chunk = 4096;     // collected members per filter CTA (LMSB_BAND_CHUNK)
   DevBuf<float> bsample, bbounds;
@@ -186,7 +187,7 @@ int ctx_init(lms_ctx* c, int device) {
   const char* ov = getenv("LMSB_ORDER");
   c->line_order = !(ov && std::strcmp(ov, "0") == 0);
   const char* bm = getenv("LMSB_BAND");
-  c->band_mode = (bm && std::strcmp(bm, "0") == 0) ? 0 : 1;
+  c->band_mode = bm ? std::max(0, std::min(2, atoi(bm))) : 1;
   const char* bv = getenv("LMSB_BAND_VERTICES");
   if (bv && atoll(bv) >= 256) c->band_vertices = atoll(bv);
   const char* bc = getenv("LMSB_BAND_CHUNK");
@@ -562,7 +563,9 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     RC_TRY(c->bcv.need(cap));
     w.ckeys = c->bck.p;
     w.cvals = c->bcv.p;
+    CUDA_TRY(cudaEventRecord(c->ev_chunk[5], c->stream));
     lmsb::launch_band_collect(bf, w, runs, cap, c->sms, c->stream);
+    CUDA_TRY(cudaEventRecord(c->ev_chunk[6], c->stream));
     CUDA_TRY(cudaGetLastError());
     st->launches += 1;
     CUDA_TRY(cudaMemcpyAsync(&m, sc + 1, sizeof(m), cudaMemcpyDeviceToHost, c->stream));
@@ -670,6 +673,8 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   st->ms_partition = ms;
   CUDA_TRY(cudaEventElapsedTime(&ms, c->ev_chunk[3], c->ev_chunk[4]));
   st->ms_band_filter = ms;
+  CUDA_TRY(cudaEventElapsedTime(&ms, c->ev_chunk[5], c->ev_chunk[6]));
+  st->ms_collect = ms;
   return LMS_OK;
 }
 
@@ -700,7 +705,8 @@ int ctx_solve_fits(lms_ctx* c, const std::vector<HostFit>& hf, lms_candidate* ou
       am = std::max(am, std::fabs(c->h_a[k]));
       bm = std::max(bm, std::fabs(c->h_b[k]));
     }
-    if (F == 1 && c->band_mode && !exhaustive && h.n <= lmsb::kBandMaxN && am < 1e30 && bm < 1e30)
+    if (F == 1 && !exhaustive && h.n <= lmsb::kBandMaxN && am < 1e30 && bm < 1e30 &&
+        (c->band_mode == 2 || (c->band_mode == 1 && span >= kBandMinSpan)))
       banded = true;  // slope-band stage instead of seeds + count filter
     int64_t s = exhaustive ? span : std::min(kSeedsMax, std::max(kSeedsMin, span / kSeedDivisor));
     s = banded ? 0 : std::min(s, span);

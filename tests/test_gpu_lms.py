@@ -304,10 +304,43 @@ def test_band_path_bit_exact_vs_oracle_mid_n():
             pts = np.column_stack([rng.integers(0, 60, n), rng.integers(0, 60, n)]).astype(float)
         x, y = pts[:, 0].copy(), pts[:, 1].copy()
         q = n // 2 + 1 if trial % 2 == 0 else int(rng.integers(2, n + 1))
-        ctx = _ctx_with({"LMSB_BAND": "1", "LMSB_BAND_VERTICES": "2048"})
+        ctx = _ctx_with({"LMSB_BAND": "2", "LMSB_BAND_VERTICES": "2048"})
         ctx.upload(x, y)
         total = n * (n - 1) // 2
         got = record_from_native(ctx.solve(q, 0, total))
         assert ctx.stats()["bands"] > 1
         want = oracle_rec(x, y, q)
         assert record_matches(got, want), (trial, n, q)
+
+
+def test_band_path_matches_count_filter_varied_inputs():
+    """Forced band stage vs the count-filter path (itself pinned to the
+    oracle) on n = 2,000-6,000 inputs with ties, duplicate x, exact inliers,
+    huge outliers, vertical and horizontal structure."""
+    rng = np.random.default_rng(5)
+    cases = []
+    n = 3000
+    cases.append(workloads.config1_points(3, n=n))                      # exact inliers: h = 0 ties
+    x = rng.integers(0, 200, n).astype(float)                            # duplicate x, integer grid
+    cases.append(np.column_stack([x, rng.integers(0, 200, n).astype(float)]))
+    x = rng.uniform(0, 1, n)
+    y = np.where(rng.random(n) < 0.6, 3.0 - 0.5 * x, rng.uniform(-1e6, 1e6, n))
+    cases.append(np.column_stack([x, y]))                                # breakdown: 1e6 outliers
+    x = rng.normal(0, 1e3, 4000)
+    cases.append(np.column_stack([x, rng.normal(0, 1e-3, 4000)]))        # near-horizontal
+    x = np.concatenate([np.full(1500, 7.0), rng.uniform(0, 10, 1500)])   # vertical majority
+    cases.append(np.column_stack([x, rng.uniform(0, 10, 3000)]))
+    cases.append(workloads.contaminated_line_points(6000, 4))
+    band = _ctx_with({"LMSB_BAND": "2"})
+    filt = _ctx_with({"LMSB_BAND": "0"})
+    for k, pts in enumerate(cases):
+        a, b = pts[:, 0].copy(), pts[:, 1].copy()
+        m = a.size
+        for q in (m // 2 + 1, max(2, m // 4), m - 3):
+            total = m * (m - 1) // 2
+            band.upload(a, b)
+            filt.upload(a, b)
+            got = record_from_native(band.solve(q, 0, total))
+            assert band.stats()["bands"] > 0
+            want = record_from_native(filt.solve(q, 0, total))
+            assert got == want, (k, q)
