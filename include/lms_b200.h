@@ -81,6 +81,7 @@ typedef struct lms_stats {
   float ms_collect;         /* the collect pass alone (last attempt) */
   double seed_height;       /* the bound H the band stage collected with */
   int64_t band_survivors;   /* collected vertices whose band window counts reached q */
+  int64_t small_fits;       /* fits of the batch solved by the fused per-fit band kernel */
 } lms_stats;
 
 /* Library identity and device discovery. */

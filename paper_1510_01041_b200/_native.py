@@ -70,6 +70,7 @@ class Stats(ctypes.Structure):
         ("ms_collect", ctypes.c_float),
         ("seed_height", ctypes.c_double),
         ("band_survivors", ctypes.c_int64),
+        ("small_fits", ctypes.c_int64),
     ]
 
     def as_dict(self) -> dict:

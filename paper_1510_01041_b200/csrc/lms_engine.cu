@@ -28,6 +28,7 @@
 #include <vector>
 
 #include "lms_band.cuh"
+#include "lms_band_small.cuh"
 #include "lms_common.cuh"
 #include "lms_hough.cuh"
 #include "lms_kernels.cuh"
@@ -167,6 +168,9 @@ struct lms_ctx {
   DevBuf<int64_t> branks2;
   DevBuf<int32_t> bfits2, bmargin;
   DevBuf<int64_t> bchunks;
+  DevBuf<int32_t> small_list;
+  DevBuf<unsigned long long> small_cnt;
+  int small_mode = 1;  // LMSB_SMALL: 0 off, 1 batches, 2 also single fits
   DevBuf<float2> blines32;
   std::vector<double> h_blb;
   int hough_mode = 0;  // 0 none, 1 image pixels, 2 explicit points
@@ -190,6 +194,8 @@ int ctx_init(lms_ctx* c, int device) {
   c->band_mode = bm ? std::max(0, std::min(2, atoi(bm))) : 1;
   const char* bv = getenv("LMSB_BAND_VERTICES");
   if (bv && atoll(bv) >= 256) c->band_vertices = atoll(bv);
+  const char* sm = getenv("LMSB_SMALL");
+  c->small_mode = sm ? std::max(0, std::min(2, atoi(sm))) : 1;
   const char* bc = getenv("LMSB_BAND_CHUNK");
   if (bc && atoll(bc) >= 32) c->band_chunk = atoll(bc);
   CUDA_TRY(cudaSetDevice(device));
@@ -272,6 +278,8 @@ void ctx_release(lms_ctx* c) {
   c->bfits2.release();
   c->bmargin.release();
   c->bchunks.release();
+  c->small_list.release();
+  c->small_cnt.release();
   c->blines32.release();
   if (c->h_best) cudaFreeHost(c->h_best);
   if (c->stream) cudaStreamDestroy(c->stream);
@@ -696,6 +704,8 @@ int ctx_solve_fits(lms_ctx* c, const std::vector<HostFit>& hf, lms_candidate* ou
   int64_t rowsA = 0, rows = 0, tasks = 0, tasksA = 0, seeds = 0;
   bool disjoint = true;
   bool banded = false;
+  std::vector<int32_t> small_list;
+  int64_t small_maxn = 0;
   for (int64_t f = 0; f < F; ++f) {
     const HostFit& h = hf[f];
     const int64_t span = h.r1 - h.r0;
@@ -708,8 +718,16 @@ int ctx_solve_fits(lms_ctx* c, const std::vector<HostFit>& hf, lms_candidate* ou
     if (F == 1 && !exhaustive && h.n <= lmsb::kBandMaxN && am < 1e30 && bm < 1e30 &&
         (c->band_mode == 2 || (c->band_mode == 1 && span >= kBandMinSpan)))
       banded = true;  // slope-band stage instead of seeds + count filter
+    // small fits of a batch: the fused per-fit band kernel (lms_band_small.cu)
+    const bool small = c->small_mode != 0 && (F > 1 || c->small_mode == 2) &&
+                       h.n <= lmsb::kSmallMaxN && span >= lmsb::kSmallMinPairs &&
+                       h.r0 == 0 && h.r1 == h.n * (h.n - 1) / 2;
+    if (small) {
+      small_list.push_back((int32_t)f);
+      small_maxn = std::max(small_maxn, h.n);
+    }
     int64_t s = exhaustive ? span : std::min(kSeedsMax, std::max(kSeedsMin, span / kSeedDivisor));
-    s = banded ? 0 : std::min(s, span);
+    s = (banded || small) ? 0 : std::min(s, span);
     lmsb::FitDesc& d = fd[f];
     d.off = h.off;
     d.n = h.n;
@@ -718,7 +736,7 @@ int ctx_solve_fits(lms_ctx* c, const std::vector<HostFit>& hf, lms_candidate* ou
     d.rank_hi = h.r1;
     d.row0 = 0;
     d.nrows = 0;
-    if (!exhaustive && !banded) {
+    if (!exhaustive && !banded && !small) {
       tasks += lmsb::fit_tasks(h.n, h.r0, h.r1, tv, &d.row0, &d.nrows);
       for (int64_t k = 0; k < d.nrows; k += lmsb::kPhaseStride)
         tasksA += lmsb::row_tasks(h.n, h.r0, h.r1, d.row0 + k, tv);
@@ -796,6 +814,28 @@ int ctx_solve_fits(lms_ctx* c, const std::vector<HostFit>& hf, lms_candidate* ou
 
   // ---- band path: one large fit with lines in shared-memory range
   if (banded) RC_TRY(band_solve(c, hf[0], &st));
+
+  // ---- fused band search of the batch's small fits, one CTA each
+  if (!small_list.empty()) {
+    RC_TRY(c->small_list.need((int64_t)small_list.size()));
+    CUDA_TRY(cudaMemcpyAsync(c->small_list.p, small_list.data(),
+                             sizeof(int32_t) * small_list.size(), cudaMemcpyHostToDevice,
+                             c->stream));
+    lmsb::SmallArgs sa{};
+    sa.a = c->a;
+    sa.b = c->b;
+    sa.fits = c->fits.p;
+    sa.list = c->small_list.p;
+    sa.out = c->best.p;
+    RC_TRY(c->small_cnt.need(12));
+    CUDA_TRY(cudaMemsetAsync(c->small_cnt.p, 0, 12 * sizeof(unsigned long long), c->stream));
+    sa.counters = c->small_cnt.p;
+    sa.timing = getenv("LMSB_SMALL_DEBUG") != nullptr;
+    lmsb::launch_small_fits(sa, (int64_t)small_list.size(), small_maxn, c->stream);
+    CUDA_TRY(cudaGetLastError());
+    st.launches += 1;
+    st.small_fits = (int64_t)small_list.size();
+  }
 
   // ---- 2.-5. filter the non-exhaustive fits: phase A (every kPhaseStride-th
   // row), re-order, phase B (the rest)
@@ -893,6 +933,21 @@ int ctx_solve_fits(lms_ctx* c, const std::vector<HostFit>& hf, lms_candidate* ou
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   std::memcpy(out, c->h_best, sizeof(lms_candidate) * F);
   if (!banded) st.chunks = nchunks;
+  if (!small_list.empty()) {
+    unsigned long long sc4[12];
+    CUDA_TRY(cudaMemcpy(sc4, c->small_cnt.p, sizeof(sc4), cudaMemcpyDeviceToHost));
+    if (getenv("LMSB_SMALL_DEBUG")) {
+      const double F = (double)small_list.size();
+      fprintf(stderr,
+              "small: bounds %.3g seeds %.3g sweeps %.3g cycles/fit; warp-cycles/fit: exact %.3g "
+              "counts %.3g searches %.3g\n",
+              sc4[5] / F, sc4[6] / F, sc4[7] / F, sc4[8] / F, sc4[9] / F, sc4[10] / F);
+    }
+    st.bands_searched = (int64_t)sc4[0];
+    st.band_survivors = (int64_t)sc4[1];
+    st.survivors = (int64_t)sc4[2];
+    st.chunks = (int64_t)sc4[3];
+  }
   if (nchunks > 0) {
     std::vector<unsigned long long> cnt(2 + nchunks);
     CUDA_TRY(cudaMemcpy(cnt.data(), c->counters.p, sizeof(unsigned long long) * (2 + nchunks),

@@ -344,3 +344,44 @@ def test_band_path_matches_count_filter_varied_inputs():
             assert band.stats()["bands"] > 0
             want = record_from_native(filt.solve(q, 0, total))
             assert got == want, (k, q)
+
+
+def test_small_fit_kernel_matches_count_filter_batch():
+    """Fused per-fit band kernel (batches of fits with n <= 1,024) vs the
+    count-filter batch path on 600 varied fits: config-4 sets, exact
+    inliers, integer grids with duplicate x, huge outliers, random q."""
+    rng = np.random.default_rng(77)
+    sets, qs = [], []
+    for k in range(600):
+        kind = k % 5
+        n = int(rng.choice([92, 150, 256, 333, 512, 700, 1024]))
+        if kind == 0:
+            pts = workloads.bench_points(n, seed=k)
+        elif kind == 1:
+            pts = workloads.config1_points(k, n=n)
+        elif kind == 2:
+            pts = np.column_stack([rng.integers(0, 40, n), rng.integers(0, 40, n)]).astype(float)
+        elif kind == 3:
+            x = rng.uniform(0, 1, n)
+            y = np.where(rng.random(n) < 0.6, 3.0 - 0.5 * x, rng.uniform(-1e6, 1e6, n))
+            pts = np.column_stack([x, y])
+        else:
+            pts = np.column_stack([rng.normal(0, 100, n), rng.normal(0, 1, n)])
+        if np.unique(pts[:, 0]).size < 2:
+            continue
+        sets.append(pts)
+        qs.append(n // 2 + 1 if k % 3 else int(rng.integers(2, n + 1)))
+    X = np.concatenate([s[:, 0] for s in sets])
+    Y = np.concatenate([s[:, 1] for s in sets])
+    offs = np.concatenate([[0], np.cumsum([len(s) for s in sets])]).astype(np.int64)
+    q = np.asarray(qs, dtype=np.int64)
+    fused = _ctx_with({"LMSB_SMALL": "1"})
+    legacy = _ctx_with({"LMSB_SMALL": "0"})
+    fused.upload(X, Y)
+    legacy.upload(X, Y)
+    got = fused.solve_batch(offs, q)
+    assert fused.stats()["small_fits"] == len(sets)
+    want = legacy.solve_batch(offs, q)
+    assert legacy.stats()["small_fits"] == 0
+    for f, (g, w) in enumerate(zip(got, want)):
+        assert record_from_native(g) == record_from_native(w), f
