@@ -63,6 +63,9 @@ namespace lmsb {
 
 namespace {
 
+#ifndef LMSB_RADIX_BITS
+#define LMSB_RADIX_BITS 4
+#endif
 constexpr int kCollectThreads = 512;
 constexpr unsigned kSeedPerBand = 160;  // sampled vertices per seed band
 constexpr int kRun = 32;  // ranks per lane per warp segment (lane-interleaved)
@@ -135,7 +138,7 @@ __global__ void band_bounds_kernel(const float* __restrict__ sorted,
 // ------------------------------------------------------------------ per band
 template <int kThreads, int kItems>
 struct BandShared {
-  using Sort = cub::BlockRadixSort<float, kThreads, kItems>;
+  using Sort = cub::BlockRadixSort<float, kThreads, kItems, cub::NullType, LMSB_RADIX_BITS>;
   union {
     typename Sort::TempStorage sort;
     float keys[kThreads * kItems];
@@ -499,7 +502,8 @@ __global__ void __launch_bounds__(kCollectThreads) band_collect_kernel(
         const double da = __dsub_rn(ai, __ldg(bf.a + j));
         const double num = __dsub_rn(bi, __ldg(bf.b + j));
         if (da != 0.0) {
-          const float u32 = (float)num / (float)da;
+          // |da| in [1e-30, 2e30] here or cand below: __fdividef is within 2 ulp
+          const float u32 = __fdividef((float)num, (float)da);
           cand = !(fabsf(u32) <= FLT_MAX) || fabs(da) < 1e-30 || (num != 0.0 && fabs(num) < 1e-30);
 #pragma unroll
           for (int k = 0; k < kMaxRuns; ++k)
