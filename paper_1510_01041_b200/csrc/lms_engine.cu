@@ -710,15 +710,8 @@ int ctx_solve_fits(lms_ctx* c, const std::vector<HostFit>& hf, lms_candidate* ou
     const HostFit& h = hf[f];
     const int64_t span = h.r1 - h.r0;
     const bool exhaustive = span <= kExhaustive;
-    double am = 0.0, bm = 0.0;
-    for (int64_t k = h.off; k < h.off + h.n; ++k) {
-      am = std::max(am, std::fabs(c->h_a[k]));
-      bm = std::max(bm, std::fabs(c->h_b[k]));
-    }
-    if (F == 1 && !exhaustive && h.n <= lmsb::kBandMaxN && am < 1e30 && bm < 1e30 &&
-        (c->band_mode == 2 || (c->band_mode == 1 && span >= kBandMinSpan)))
-      banded = true;  // slope-band stage instead of seeds + count filter
-    // small fits of a batch: the fused per-fit band kernel (lms_band_small.cu)
+    // small fits of a batch: the fused per-fit band kernel (lms_band_small.cu),
+    // which derives its own magnitudes on the device
     const bool small = c->small_mode != 0 && (F > 1 || c->small_mode == 2) &&
                        h.n <= lmsb::kSmallMaxN && span >= lmsb::kSmallMinPairs &&
                        h.r0 == 0 && h.r1 == h.n * (h.n - 1) / 2;
@@ -726,6 +719,16 @@ int ctx_solve_fits(lms_ctx* c, const std::vector<HostFit>& hf, lms_candidate* ou
       small_list.push_back((int32_t)f);
       small_maxn = std::max(small_maxn, h.n);
     }
+    double am = 0.0, bm = 0.0;
+    if (!small) {
+      for (int64_t k = h.off; k < h.off + h.n; ++k) {
+        am = std::max(am, std::fabs(c->h_a[k]));
+        bm = std::max(bm, std::fabs(c->h_b[k]));
+      }
+    }
+    if (F == 1 && !exhaustive && !small && h.n <= lmsb::kBandMaxN && am < 1e30 && bm < 1e30 &&
+        (c->band_mode == 2 || (c->band_mode == 1 && span >= kBandMinSpan)))
+      banded = true;  // slope-band stage instead of seeds + count filter
     int64_t s = exhaustive ? span : std::min(kSeedsMax, std::max(kSeedsMin, span / kSeedDivisor));
     s = (banded || small) ? 0 : std::min(s, span);
     lmsb::FitDesc& d = fd[f];
