@@ -49,6 +49,7 @@
 
 #include <cub/block/block_radix_sort.cuh>
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_segmented_radix_sort.cuh>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -67,7 +68,8 @@ namespace {
 #define LMSB_RADIX_BITS 4
 #endif
 constexpr int kCollectThreads = 512;
-constexpr unsigned kSeedPerBand = 160;  // sampled vertices per seed band
+constexpr int kEdge = 5;  // keys kept around each end of a band's narrowest q-window
+constexpr unsigned kSeedPerBand = 64;  // sampled vertices per seed band
 constexpr int kRun = 32;  // ranks per lane per warp segment (lane-interleaved)
 constexpr int kSlopeBits = 17;  // within-band slope order bits of a collected key
 
@@ -144,6 +146,7 @@ struct BandShared {
     float keys[kThreads * kItems];
   };
   double red[2][kThreads / 32];
+  int kstar;
 };
 
 __device__ __forceinline__ int lower_idx(const float* __restrict__ k, int n, float x) {
@@ -222,6 +225,19 @@ __device__ __forceinline__ void band_keys(const BandFit& bf, double uM,
   __syncthreads();
 }
 
+// keys around the narrowest q-window [K[k*], K[k*+q-1]] of a band: the lines
+// there bound the best window at the band's centre slope; pairs among them
+// seed H (band_edge_seed_kernel)
+__device__ __forceinline__ void write_edges(const float* K, int n, int q, int ks, float* e) {
+#pragma unroll
+  for (int t = 0; t < kEdge; ++t) {
+    const int lo = min(max(ks + t - kEdge / 2, 0), n - 1);
+    const int hi = min(max(ks + q - 1 + t - kEdge / 2, 0), n - 1);
+    e[t] = K[lo];
+    e[kEdge + t] = K[hi];
+  }
+}
+
 // mode 0: lower bound of every inner band (grid = K)
 template <int kThreads, int kItems>
 __global__ void __launch_bounds__(kThreads, 1) band_bound_kernel(BandFit bf, BandArgs ba) {
@@ -244,8 +260,16 @@ __global__ void __launch_bounds__(kThreads, 1) band_bound_kernel(BandFit bf, Ban
   double w = INFINITY;
   for (int k = threadIdx.x; k + q - 1 < n; k += kThreads)
     w = fmin(w, (double)sh.keys[k + q - 1] - (double)sh.keys[k]);
+  if (threadIdx.x == 0) sh.kstar = n;
   w = block_min<kThreads>(w, sh.red[0]);
+  for (int k = threadIdx.x; k + q - 1 < n; k += kThreads)
+    if ((double)sh.keys[k + q - 1] - (double)sh.keys[k] == w) {
+      atomicMin(&sh.kstar, k);
+      break;
+    }
+  __syncthreads();
   if (threadIdx.x == 0) {
+    if (ba.edge && sh.kstar < n) write_edges(sh.keys, n, q, sh.kstar, ba.edge + (int64_t)band * 2 * kEdge);
     const double e = slack_base(bf, fmax(fabs(uL), fabs(uR)), uM) + 1e-300;
     ba.lb[band] = (w - 2.0 * dmax - 2.0 * e) * (1.0 - 0x1p-40);
     ba.wq[band] = w;
@@ -559,7 +583,8 @@ __global__ void __launch_bounds__(kCountThreads) band_count_kernel(
     unsigned long long* __restrict__ out_count, int32_t* __restrict__ out_margin) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float2* sl = reinterpret_cast<float2*>(smem_raw);
-  unsigned* cnt = reinterpret_cast<unsigned*>(sl + bf.n);  // [2][32]
+  const int nst = (int)min(bf.n, (int64_t)kBandMaxN);  // lines staged at once
+  unsigned* cnt = reinterpret_cast<unsigned*>(sl + nst);  // [2][32]
   const int64_t total = (int64_t)*in_count;
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -567,14 +592,16 @@ __global__ void __launch_bounds__(kCountThreads) band_count_kernel(
   const int n = (int)bf.n;
   const int q = (int)bf.q;
   if ((int64_t)blockIdx.x * 32 >= total) return;
-  for (int k = tid; k < n; k += kCountThreads) sl[k] = lines[k];
+  const bool resident = n <= nst;
+  if (resident)
+    for (int k = tid; k < n; k += kCountThreads) sl[k] = lines[k];
   double H = INFINITY;
   {
     const lms_candidate b0 = *best;
     if (b0.found) H = b0.height;
   }
-  const int per = (n + kCountWarps - 1) / kCountWarps;
-  const int k0 = warp * per, k1 = min(n, k0 + per);
+  const int per = (nst + kCountWarps - 1) / kCountWarps;
+  const int k0 = warp * per, k1 = min(nst, k0 + per);
   for (int64_t t0 = (int64_t)blockIdx.x * 32; t0 < total; t0 += (int64_t)gridDim.x * 32) {
     const int64_t s = t0 + lane;
     const bool live = s < total;
@@ -602,12 +629,21 @@ __global__ void __launch_bounds__(kCountThreads) band_count_kernel(
     if (tid < 64) cnt[tid] = 0u;
     __syncthreads();  // also orders the line staging before first use
     unsigned cu = 0, cd = 0;
+    for (int c0 = 0; c0 < n; c0 += nst) {
+      const int cn = min(nst, n - c0);
+      if (!resident) {
+        __syncthreads();
+        for (int k = tid; k < cn; k += kCountThreads) sl[k] = lines[c0 + k];
+        __syncthreads();
+      }
+      const int e1 = min(k1, cn);
 #pragma unroll 8
-    for (int k = k0; k < k1; ++k) {
-      const float2 L = sl[k];
-      const float t = fmaf(L.x, u32, -L.y);
-      cu += (t >= upLo) & (t <= upHi);
-      cd += (t >= dnLo) & (t <= dnHi);
+      for (int k = k0; k < e1; ++k) {
+        const float2 L = sl[k];
+        const float t = fmaf(L.x, u32, -L.y);
+        cu += (t >= upLo) & (t <= upHi);
+        cd += (t >= dnLo) & (t <= dnHi);
+      }
     }
     atomicAdd(cnt + lane, cu);
     atomicAdd(cnt + 32 + lane, cd);
@@ -633,6 +669,53 @@ __global__ void __launch_bounds__(kCountThreads) band_count_kernel(
   }
 }
 
+// Seeds from the narrowest q-window of each listed band: the lines whose
+// keys (recomputed exactly as the bound kernel formed them) lie among the
+// kEdge keys around either end of the window, paired within each end.
+__global__ void __launch_bounds__(256) band_edge_seed_kernel(BandFit bf, BandArgs ba,
+                                                            const int32_t* __restrict__ bands,
+                                                            int64_t* __restrict__ ranks,
+                                                            int32_t* __restrict__ fits,
+                                                            int64_t cap,
+                                                            unsigned long long* __restrict__ count) {
+  constexpr int kGroup = 16;
+  __shared__ int grp[2][kGroup];
+  __shared__ int ng[2];
+  const int band = bands[blockIdx.x];
+  double uL, uR;
+  if (band < 0 || !boundary_extent(ba.bounds, ba.K, band, &uL, &uR) || !keys_in_range(bf, uL, uR))
+    return;
+  const double uM = 0.5 * uL + 0.5 * uR;
+  const float* e = ba.edge + (int64_t)band * 2 * kEdge;
+  if (threadIdx.x < 2) ng[threadIdx.x] = 0;
+  __syncthreads();
+  const int n = (int)bf.n;
+  for (int k = threadIdx.x; k < n; k += blockDim.x) {
+    const float key = (float)__dsub_rn(__dmul_rn(__dsub_rn(__ldg(bf.a + k), bf.c), uM), __ldg(bf.b + k));
+#pragma unroll
+    for (int g = 0; g < 2; ++g)
+      if (key >= e[g * kEdge] && key <= e[g * kEdge + kEdge - 1]) {
+        const int slot = atomicAdd(&ng[g], 1);
+        if (slot < kGroup) grp[g][slot] = k;
+      }
+  }
+  __syncthreads();
+  for (int g = 0; g < 2; ++g) {
+    const int m = min(ng[g], kGroup);
+    for (int t = threadIdx.x; t < m * m; t += blockDim.x) {
+      int x = grp[g][t / m], y = grp[g][t % m];
+      if (x >= y) continue;
+      const int64_t r = row_offset(bf.n, x) + (y - x - 1);
+      if (r < bf.R0 || r >= bf.R0 + bf.span) continue;
+      const unsigned long long pos = atomicAdd(count, 1ull);
+      if ((int64_t)pos < cap) {
+        ranks[pos] = r;
+        fits[pos] = ba.fit;
+      }
+    }
+  }
+}
+
 __global__ void band_runs_kernel(const uint32_t* __restrict__ keys, int64_t m,
                                  int64_t* __restrict__ start, int64_t* __restrict__ end) {
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < m;
@@ -640,6 +723,185 @@ __global__ void band_runs_kernel(const uint32_t* __restrict__ keys, int64_t m,
     const uint32_t k = keys[p] >> kSlopeBits;
     if (p == 0 || (keys[p - 1] >> kSlopeBits) != k) start[k] = p;
     if (p == m - 1 || (keys[p + 1] >> kSlopeBits) != k) end[k] = p + 1;
+  }
+}
+
+// ------------------------------------------------------------------ n > kBandMaxN
+// The n keys of a band no longer fit shared memory.  Bounds: the keys of a
+// batch of bands are written to global memory, sorted by a CUB segmented
+// radix sort and scanned for W_q (band_wq_kernel).  Filter: every chunk CTA
+// reads its band's sorted keys back and quantises them to 16 bits between the
+// band's extreme keys (sorted order is preserved; a window [lo, hi] is
+// widened to whole quantisation steps, so counts stay a superset), and
+// counts with the band's own centre (no per-chunk sort).
+
+__global__ void band_keys_global_kernel(BandFit bf, const float* __restrict__ bounds, int K,
+                                        int band0, int nb, float* __restrict__ keys) {
+  const int n = (int)bf.n;
+  for (int e = blockIdx.y; e < nb; e += gridDim.y) {
+    const int band = band0 + e;
+    double uL, uR;
+    const bool ok = boundary_extent(bounds, K, band, &uL, &uR) && keys_in_range(bf, uL, uR);
+    const double uM = 0.5 * uL + 0.5 * uR;
+    float* dst = keys + (int64_t)e * n;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+      dst[k] = ok ? (float)__dsub_rn(__dmul_rn(__dsub_rn(__ldg(bf.a + k), bf.c), uM), __ldg(bf.b + k))
+                  : 0.f;
+  }
+}
+
+__global__ void __launch_bounds__(1024) band_wq_kernel(BandFit bf, BandArgs ba, int band0,
+                                                      const float* __restrict__ sorted,
+                                                      float* __restrict__ store) {
+  __shared__ double red[32];
+  __shared__ int kstar;
+  const int band = band0 + blockIdx.x;
+  const int n = (int)bf.n, q = (int)bf.q;
+  double uL, uR;
+  if (!boundary_extent(ba.bounds, ba.K, band, &uL, &uR) || !keys_in_range(bf, uL, uR)) {
+    if (threadIdx.x == 0) {
+      ba.lb[band] = -INFINITY;
+      ba.wq[band] = INFINITY;
+    }
+    return;
+  }
+  const float* K = sorted + (int64_t)blockIdx.x * n;
+  double w = INFINITY;
+  for (int k = threadIdx.x; k + q - 1 < n; k += blockDim.x) w = fmin(w, (double)K[k + q - 1] - (double)K[k]);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) w = fmin(w, __shfl_xor_sync(0xffffffffu, w, off));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = w;
+  if (threadIdx.x == 0) kstar = n;
+  __syncthreads();
+  w = red[0];
+  for (int t = 1; t < (int)(blockDim.x >> 5); ++t) w = fmin(w, red[t]);
+  for (int k = threadIdx.x; k + q - 1 < n; k += blockDim.x)
+    if ((double)K[k + q - 1] - (double)K[k] == w) {
+      atomicMin(&kstar, k);
+      break;
+    }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (ba.edge && kstar < n) write_edges(K, n, q, kstar, ba.edge + (int64_t)band * 2 * kEdge);
+    const double uM = 0.5 * uL + 0.5 * uR;
+    const double dmax = bf.dev * fmax(uR - uM, uM - uL) * (1.0 + 0x1p-40);
+    const double e = slack_base(bf, fmax(fabs(uL), fabs(uR)), uM) + 1e-300;
+    ba.lb[band] = (w - 2.0 * dmax - 2.0 * e) * (1.0 - 0x1p-40);
+    ba.wq[band] = w;
+  }
+  // keep the sorted keys of the band for the filter (admitted bands only use them)
+  if (store) {
+    float* dst = store + (int64_t)band * n;
+    for (int k = threadIdx.x; k < n; k += blockDim.x) dst[k] = K[k];
+  }
+}
+
+constexpr int kBigThreads = 1024;
+
+__global__ void __launch_bounds__(kBigThreads, 1) band_filter_big_kernel(BandFit bf, BandArgs ba,
+                                                                        const float* __restrict__ keys) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint16_t* K16 = reinterpret_cast<uint16_t*>(smem_raw);
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int64_t cidx = blockIdx.x;
+  if (cidx >= ba.chunk_prefix[ba.nlist]) return;
+  int lo = 0, hi = ba.nlist - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (ba.chunk_prefix[mid] <= cidx) lo = mid;
+    else hi = mid - 1;
+  }
+  const int band = ba.list[lo];
+  const int64_t m0 = ba.start[band] + (cidx - ba.chunk_prefix[lo]) * ba.chunk;
+  const int64_t m1 = min(ba.end[band], m0 + ba.chunk);
+  if (m1 <= m0) return;
+  double H = INFINITY;
+  {
+    const lms_candidate best = *ba.best;
+    if (best.found) H = best.height;
+  }
+  const int n = (int)bf.n, q = (int)bf.q;
+  bool all = band >= ba.K;
+  double uL = 0.0, uR = 0.0;
+  if (!all) {
+    if (ba.lb[band] > H * (1.0 + 0x1p-19)) return;
+    all = !boundary_extent(ba.bounds, ba.K, band, &uL, &uR) || !keys_in_range(bf, uL, uR);
+  }
+  const double uM = 0.5 * uL + 0.5 * uR;
+  double kmin = 0.0, res = 1.0;
+  if (!all) {
+    const float* Kg = keys + (int64_t)band * n;
+    kmin = (double)Kg[0];
+    const double kmax = (double)Kg[n - 1];
+    res = fmax((kmax - kmin) / 65535.0, 1e-300) * (1.0 + 0x1p-30);
+    for (int k = tid; k < n; k += kBigThreads) {
+      const double t = floor(((double)Kg[k] - kmin) / res);
+      K16[k] = (uint16_t)fmin(fmax(t, 0.0), 65535.0);
+    }
+    __syncthreads();
+  }
+  auto q16 = [&](double x, bool up) -> int {
+    // whole quantisation steps around x, one extra step either side for rounding
+    const double t = floor((x - kmin) / res);
+    const double v = up ? t + 1.0 : t - 1.0;
+    return (int)fmin(fmax(v, -1.0), 65536.0);
+  };
+  auto lower16 = [&](int x) {  // first index with K16 >= x
+    int a = 0, b = n;
+    while (a < b) {
+      const int mid = (a + b) >> 1;
+      if ((int)K16[mid] < x) a = mid + 1;
+      else b = mid;
+    }
+    return a;
+  };
+  auto upper16 = [&](int x) {  // first index with K16 > x
+    int a = 0, b = n;
+    while (a < b) {
+      const int mid = (a + b) >> 1;
+      if ((int)K16[mid] <= x) a = mid + 1;
+      else b = mid;
+    }
+    return a;
+  };
+  for (int64_t s0 = m0; s0 < m1; s0 += kBigThreads) {
+    const int64_t s = s0 + tid;
+    bool keep = false;
+    int64_t rank = 0;
+    if (s < m1) {
+      const uint32_t p = ba.members[s];
+      const int64_t i = p >> 16, j = p & 0xFFFF;
+      rank = row_offset(bf.n, i) + (j - i - 1);
+      keep = all;
+      if (!all) {
+        const double ai = bf.a[i], bi = bf.b[i];
+        const double u = __ddiv_rn(__dsub_rn(bi, bf.b[j]), __dsub_rn(ai, bf.a[j]));
+        const double v0 = cut_value(u, ai, bi);
+        const double z = __dsub_rn(v0, __dmul_rn(bf.c, u));
+        const double D = bf.dev * fabs(u - uM) * (1.0 + 0x1p-40);
+        const double E = slack_base(bf, fabs(u), uM) + 0x1p-20 * H + 1e-300;
+        const double pad = D + E;
+        const int top = upper16(q16(z + H + pad, true));
+        const int bot = lower16(q16(z - H - pad, false));
+        if (top - bot >= q) {
+          const int up_lo = lower16(q16(z - pad, false));
+          const int dn_hi = upper16(q16(z + pad, true));
+          keep = (top - up_lo >= q) || (dn_hi - bot >= q);
+        }
+      }
+    }
+    const unsigned mask = __ballot_sync(0xffffffffu, keep);
+    if (mask) {
+      unsigned long long base = 0;
+      if (lane == 0) base = atomicAdd(ba.out_count, (unsigned long long)__popc(mask));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (keep) {
+        const unsigned slot = __popc(mask & ((1u << lane) - 1u));
+        ba.out_ranks[base + slot] = rank;
+        ba.out_fits[base + slot] = ba.fit;
+      }
+    }
   }
 }
 
@@ -710,6 +972,55 @@ void launch_band(const BandFit& bf, const BandArgs& ba, int mode, int grid, cuda
   else launch_band_t<1024, 16>(bf, ba, mode, grid, st);
 }
 
+size_t band_big_sort_temp_bytes(int nb, int64_t n) {
+  size_t bytes = 0;
+  cub::DeviceSegmentedRadixSort::SortKeys(nullptr, bytes, (const float*)nullptr, (float*)nullptr,
+                                          (int)(nb * n), nb, (const int64_t*)nullptr,
+                                          (const int64_t*)nullptr);
+  return bytes;
+}
+
+__global__ void seg_offsets_kernel(int64_t* off, int nb, int64_t n) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e <= nb; e += gridDim.x * blockDim.x)
+    off[e] = (int64_t)e * n;
+}
+
+int launch_band_bound_big(const BandFit& bf, const BandArgs& ba, const BandBig& bg,
+                          cudaStream_t st) {
+  const int64_t n = bf.n;
+  seg_offsets_kernel<<<(bg.batch + 256) / 256, 256, 0, st>>>(bg.seg, bg.batch, n);
+  for (int b0 = 0; b0 < ba.K; b0 += bg.batch) {
+    const int nb = std::min(bg.batch, ba.K - b0);
+    dim3 grid((unsigned)std::min<int64_t>((n + 255) / 256, 64), (unsigned)std::min(nb, 65535));
+    band_keys_global_kernel<<<grid, 256, 0, st>>>(bf, ba.bounds, ba.K, b0, nb, bg.keys);
+    size_t bytes = bg.temp_bytes;
+    if (cub::DeviceSegmentedRadixSort::SortKeys(bg.temp, bytes, bg.keys, bg.keys_alt,
+                                                (int)(nb * n), nb, bg.seg, bg.seg + 1, 0, 32,
+                                                st) != cudaSuccess)
+      return -1;
+    band_wq_kernel<<<nb, 1024, 0, st>>>(bf, ba, b0, bg.keys_alt, bg.store);
+  }
+  return 0;
+}
+
+void launch_band_filter_big(const BandFit& bf, const BandArgs& ba, const float* store, int grid,
+                            cudaStream_t st) {
+  if (grid <= 0) return;
+  band_chunks_kernel<<<1, 32, 0, st>>>(ba.list, ba.nlist, ba.start, ba.end, ba.chunk,
+                                       ba.chunk_prefix);
+  const size_t smem = (size_t)bf.n * sizeof(uint16_t);
+  static bool done = false;
+  set_smem(band_filter_big_kernel, (size_t)kBandMaxBigN * sizeof(uint16_t), &done);
+  band_filter_big_kernel<<<grid, kBigThreads, smem, st>>>(bf, ba, store);
+}
+
+void launch_band_edge_seeds(const BandFit& bf, const BandArgs& ba, const int32_t* bands, int nb,
+                            int64_t* ranks, int32_t* fits, int64_t cap,
+                            unsigned long long* count, cudaStream_t st) {
+  if (nb > 0 && ba.edge)
+    band_edge_seed_kernel<<<nb, 256, 0, st>>>(bf, ba, bands, ranks, fits, cap, count);
+}
+
 void launch_band_seeds(const BandFit& bf, const BandWork& w, int64_t* ranks, int32_t* fits,
                        int32_t fit, int64_t cap, unsigned long long* count, cudaStream_t st) {
   cudaMemsetAsync(w.sample_counts, 0, sizeof(unsigned) * w.K, st);
@@ -731,7 +1042,7 @@ void launch_band_collect(const BandFit& bf, const BandWork& w, const BandRuns& r
 void launch_band_count(const BandFit& bf, const BandCount& bc, int sms, cudaStream_t st) {
   if (bc.make_lines) band_lines32_kernel<<<(int)((bf.n + 255) / 256), 256, 0, st>>>(bf, bc.lines);
   cudaMemsetAsync(bc.out_count, 0, sizeof(unsigned long long), st);
-  const size_t smem = (size_t)bf.n * sizeof(float2) + 64 * sizeof(unsigned);
+  const size_t smem = (size_t)std::min<int64_t>(bf.n, kBandMaxN) * sizeof(float2) + 64 * sizeof(unsigned);
   static bool done = false;
   set_smem(band_count_kernel, (size_t)kBandMaxN * sizeof(float2) + 64 * sizeof(unsigned), &done);
   band_count_kernel<<<sms, kCountThreads, smem, st>>>(bf, bc.lines, bc.best, bc.in_ranks,

@@ -12,6 +12,9 @@ namespace lmsb {
 // Lines per fit the band stage handles (the sorted keys of a band live in
 // shared memory; member vertices pack (i, j) into 16 + 16 bits).
 constexpr int kBandMaxN = 16384;
+// Lines per fit of the large-n band path (global segmented sorts for the
+// bounds, 16-bit quantised keys in the filter; pair indices pack 16 + 16 bits).
+constexpr int kBandMaxBigN = 65536;
 // Most bands per fit (the collect kernel keeps K boundaries in shared memory).
 constexpr int kBandMaxK = 16384;
 
@@ -67,6 +70,7 @@ struct BandArgs {
   int64_t* chunk_prefix;      // nlist + 1 scratch: first chunk of every listed band
   double* lb;                 // per band lower bound of any vertex height (-inf: unknown)
   double* wq;                 // per band narrowest q-window of the keys at the band centre
+  float* edge;                // per band 2 * 5 keys around the ends of that window (optional)
   const lms_candidate* best;  // the fit's current best record (H)
   int64_t* out_ranks;
   int32_t* out_fits;
@@ -88,6 +92,22 @@ struct BandCount {
   bool make_lines;      // fill `lines` first
 };
 
+// large-n bounds: keys of `batch` bands at a time in global memory
+struct BandBig {
+  int batch;
+  float* keys;      // batch * n
+  float* keys_alt;  // batch * n
+  float* store;     // K * n: every band's sorted keys, kept for the filter
+  int64_t* seg;     // batch + 1
+  void* temp;
+  size_t temp_bytes;
+};
+size_t band_big_sort_temp_bytes(int nb, int64_t n);
+int launch_band_bound_big(const BandFit& bf, const BandArgs& ba, const BandBig& bg,
+                          cudaStream_t st);
+void launch_band_filter_big(const BandFit& bf, const BandArgs& ba, const float* store, int grid,
+                            cudaStream_t st);
+
 size_t band_sample_temp_bytes(int64_t S);
 size_t band_order_temp_bytes(int64_t m);
 // survivors by descending margin (CUB radix sort)
@@ -99,6 +119,10 @@ size_t band_collect_smem(int K);
 int launch_band_sample(const BandFit& bf, const BandWork& w, int sms, cudaStream_t st);
 // mode 0: grid = K (lower bound of every band); mode 1: grid >= chunks of the listed bands
 void launch_band(const BandFit& bf, const BandArgs& ba, int mode, int grid, cudaStream_t st);
+// pairs of lines at the ends of the listed bands' narrowest q-windows
+void launch_band_edge_seeds(const BandFit& bf, const BandArgs& ba, const int32_t* bands, int nb,
+                            int64_t* ranks, int32_t* fits, int64_t cap,
+                            unsigned long long* count, cudaStream_t st);
 void launch_band_seeds(const BandFit& bf, const BandWork& w, int64_t* ranks, int32_t* fits,
                        int32_t fit, int64_t cap, unsigned long long* count, cudaStream_t st);
 void launch_band_collect(const BandFit& bf, const BandWork& w, const BandRuns& runs, int64_t cap,

@@ -156,6 +156,7 @@ struct lms_ctx {
   int band_mode = 1;  // LMSB_BAND: 0 count-filter path only, 1 auto (large fits), 2 always
   int64_t band_vertices = 131072; // target vertices per band (LMSB_BAND_VERTICES)
   int64_t band_chunk = 4096;     // collected members per filter CTA (LMSB_BAND_CHUNK)
+  int64_t big_mult = 8;          // n > 16,384: vertices per band >= big_mult * n (LMSB_BIG_MULT)
   DevBuf<float> bsample, bbounds;
   DevBuf<unsigned> bscnt;
   DevBuf<uint8_t> bflag;
@@ -164,10 +165,13 @@ struct lms_ctx {
   DevBuf<int64_t> bstart, bend;
   DevBuf<unsigned char> btemp;
   DevBuf<double> blb, bwq;
+  DevBuf<float> bedge;
   DevBuf<int32_t> blist;
   DevBuf<int64_t> branks2;
   DevBuf<int32_t> bfits2, bmargin;
   DevBuf<int64_t> bchunks;
+  DevBuf<float> bbig_keys, bbig_store;
+  DevBuf<int64_t> bbig_seg;
   DevBuf<int32_t> small_list;
   DevBuf<unsigned long long> small_cnt;
   int small_mode = 1;  // LMSB_SMALL: 0 off, 1 batches, 2 also single fits
@@ -194,6 +198,8 @@ int ctx_init(lms_ctx* c, int device) {
   c->band_mode = bm ? std::max(0, std::min(2, atoi(bm))) : 1;
   const char* bv = getenv("LMSB_BAND_VERTICES");
   if (bv && atoll(bv) >= 256) c->band_vertices = atoll(bv);
+  const char* bmul = getenv("LMSB_BIG_MULT");
+  if (bmul && atoll(bmul) >= 1) c->big_mult = atoll(bmul);
   const char* sm = getenv("LMSB_SMALL");
   c->small_mode = sm ? std::max(0, std::min(2, atoi(sm))) : 1;
   const char* bc = getenv("LMSB_BAND_CHUNK");
@@ -273,11 +279,15 @@ void ctx_release(lms_ctx* c) {
   c->btemp.release();
   c->blb.release();
   c->bwq.release();
+  c->bedge.release();
   c->blist.release();
   c->branks2.release();
   c->bfits2.release();
   c->bmargin.release();
   c->bchunks.release();
+  c->bbig_keys.release();
+  c->bbig_store.release();
+  c->bbig_seg.release();
   c->small_list.release();
   c->small_cnt.release();
   c->blines32.release();
@@ -368,11 +378,13 @@ int order_lines(lms_ctx* c, const std::vector<int64_t>& seg, int64_t F, const do
 // seed H from the samples of the lowest-bound bands, collect the vertices of
 // the bands whose bound admits H, count their windows, and re-evaluate the
 // survivors exactly.  best[0] must be reset; the caller checked that the
-// fit's magnitudes are finite and n <= kBandMaxN.
+// fit's magnitudes are finite and n <= kBandMaxBigN.
 int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   const int64_t span = h.r1 - h.r0;
-  const int K = (int)std::max<int64_t>(
-      3, std::min<int64_t>(lmsb::kBandMaxK, (span + c->band_vertices - 1) / c->band_vertices));
+  // large n: bands of >= 32 n vertices (their keys are sorted in global memory)
+  const bool big = h.n > lmsb::kBandMaxN;
+  const int64_t bv = big ? std::max<int64_t>(c->band_vertices, c->big_mult * h.n) : c->band_vertices;
+  const int K = (int)std::max<int64_t>(3, std::min<int64_t>(lmsb::kBandMaxK, (span + bv - 1) / bv));
   const int64_t S =
       std::min<int64_t>(span, std::min<int64_t>(1 << 20, std::max<int64_t>(64 * K, 1 << 16)));
   constexpr int kSeedBands = 8;
@@ -467,11 +479,34 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   ba.end = c->bend.p;
   ba.lb = c->blb.p;
   ba.wq = c->bwq.p;
+  RC_TRY(c->bedge.need((int64_t)K * 10));
+  ba.edge = c->bedge.p;
   ba.best = c->best.p;
   ba.fit = 0;
-  lmsb::launch_band(bf, ba, 0, K, c->stream);
+  if (big) {
+    constexpr int kBatch = 256;
+    RC_TRY(c->bbig_keys.need((int64_t)kBatch * h.n * 2));
+    RC_TRY(c->bbig_store.need((int64_t)K * h.n));
+    RC_TRY(c->bbig_seg.need(kBatch + 1));
+    RC_TRY(c->btemp.need((int64_t)std::max(lmsb::band_sample_temp_bytes(S),
+                                           lmsb::band_big_sort_temp_bytes(kBatch, h.n))));
+    lmsb::BandBig bg{};
+    bg.batch = kBatch;
+    bg.keys = c->bbig_keys.p;
+    bg.keys_alt = c->bbig_keys.p + (int64_t)kBatch * h.n;
+    bg.store = c->bbig_store.p;
+    bg.seg = c->bbig_seg.p;
+    bg.temp = c->btemp.p;
+    bg.temp_bytes = (size_t)c->btemp.cap;
+    if (lmsb::launch_band_bound_big(bf, ba, bg, c->stream) != 0)
+      return set_error(LMS_ERR_CUDA, "large-n band bound sort failed");
+    st->launches += 4 * ((K + kBatch - 1) / kBatch);
+  } else {
+    lmsb::launch_band(bf, ba, 0, K, c->stream);
+    st->launches += 1;
+  }
   CUDA_TRY(cudaGetLastError());
-  st->launches += 5;
+  st->launches += 4;
   CUDA_TRY(cudaEventRecord(c->ev_chunk[1], c->stream));
   std::vector<double>& lb = c->h_blb;
   lb.resize(K);
@@ -492,14 +527,26 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   // ---- seeds: the samples of the bands with the narrowest q-windows at their
   // centre slope (the bands an LMS line of that slope would come from)
   std::vector<uint8_t> flag(K + 1, 0);
+  std::vector<int32_t> seed_bands;
   {
     std::vector<int32_t> byw(K);
     for (int k = 0; k < K; ++k) byw[k] = k;
     std::stable_sort(byw.begin(), byw.end(), [&](int32_t x, int32_t y) { return wq[x] < wq[y]; });
     for (int e = 0; e < K && e < kSeedBands; ++e)
-      if (std::isfinite(wq[byw[e]])) flag[byw[e]] = 1;
+      if (std::isfinite(wq[byw[e]])) {
+        flag[byw[e]] = 1;
+        seed_bands.push_back(byw[e]);
+      }
   }
   CUDA_TRY(cudaMemcpyAsync(c->bflag.p, flag.data(), K, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->blist.p, seed_bands.data(), sizeof(int32_t) * seed_bands.size(),
+                           cudaMemcpyHostToDevice, c->stream));
+  // the window-edge pairs first (usually within a few ulps of the optimum),
+  // then the sampled vertices of the same bands against that bound
+  CUDA_TRY(cudaMemsetAsync(sc + 2, 0, sizeof(unsigned long long), c->stream));
+  lmsb::launch_band_edge_seeds(bf, ba, c->blist.p, (int)seed_bands.size(), c->ranks.p,
+                               c->item_fit.p, seed_cap, sc + 2, c->stream);
+  RC_TRY(exact_list(sc + 2, seed_cap, c->ranks.p, c->item_fit.p));
   lmsb::launch_band_seeds(bf, w, c->ranks.p, c->item_fit.p, 0, seed_cap, sc + 2, c->stream);
   RC_TRY(exact_list(sc + 2, seed_cap, c->ranks.p, c->item_fit.p));
   lms_candidate hb{};
@@ -618,8 +665,9 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   CUDA_TRY(cudaMemsetAsync(sc + 3, 0, 2 * sizeof(unsigned long long), c->stream));
   unsigned long long m2 = 0, m3 = 0, m1 = 0;
   if (m > 0) {
-    lmsb::launch_band(bf, ba, 1, (int)(((int64_t)m + ba.chunk - 1) / ba.chunk + ba.nlist),
-                      c->stream);
+    const int fgrid = (int)(((int64_t)m + ba.chunk - 1) / ba.chunk + ba.nlist);
+    if (big) lmsb::launch_band_filter_big(bf, ba, c->bbig_store.p, fgrid, c->stream);
+    else lmsb::launch_band(bf, ba, 1, fgrid, c->stream);
     lmsb::BandCount bc{};
     bc.lines = c->blines32.p;
     bc.best = c->best.p;
@@ -726,7 +774,7 @@ int ctx_solve_fits(lms_ctx* c, const std::vector<HostFit>& hf, lms_candidate* ou
         bm = std::max(bm, std::fabs(c->h_b[k]));
       }
     }
-    if (F == 1 && !exhaustive && !small && h.n <= lmsb::kBandMaxN && am < 1e30 && bm < 1e30 &&
+    if (F == 1 && !exhaustive && !small && h.n <= lmsb::kBandMaxBigN && am < 1e30 && bm < 1e30 &&
         (c->band_mode == 2 || (c->band_mode == 1 && span >= kBandMinSpan)))
       banded = true;  // slope-band stage instead of seeds + count filter
     int64_t s = exhaustive ? span : std::min(kSeedsMax, std::max(kSeedsMin, span / kSeedDivisor));

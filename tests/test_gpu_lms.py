@@ -385,3 +385,42 @@ def test_small_fit_kernel_matches_count_filter_batch():
     assert legacy.stats()["small_fits"] == 0
     for f, (g, w) in enumerate(zip(got, want)):
         assert record_from_native(g) == record_from_native(w), f
+
+
+def test_band_path_large_n_matches_count_filter():
+    """n > 16,384 takes the large-n band path (global segmented sorts, 16-bit
+    quantised keys): same record as the count-filter path."""
+    for n, seed in ((20000, 1), (24000, 2)):
+        pts = workloads.contaminated_line_points(n, seed)
+        a, b = pts[:, 0].copy(), pts[:, 1].copy()
+        q = n // 2 + 1
+        total = n * (n - 1) // 2
+        band = _ctx_with({"LMSB_BAND": "1"})
+        filt = _ctx_with({"LMSB_BAND": "0"})
+        band.upload(a, b)
+        filt.upload(a, b)
+        got = record_from_native(band.solve(q, 0, total))
+        assert band.stats()["bands"] > 0
+        want = record_from_native(filt.solve(q, 0, total))
+        assert got == want, n
+
+
+def test_config3_n65536_band_path_properties():
+    """Config 3 (n = 65,536) on one GPU: the winner re-evaluates identically
+    on the CPU oracle and two rank partitions merge to the same record."""
+    n = 65536
+    pts = workloads.contaminated_line_points(n, 0)
+    a, b = pts[:, 0].copy(), pts[:, 1].copy()
+    q = n // 2 + 1
+    total = n * (n - 1) // 2
+    ctx = _native.Context()
+    ctx.upload(a, b)
+    rec = record_from_native(ctx.solve(q, 0, total))
+    assert ctx.stats()["bands"] > 0
+    (chk,) = oracle.eval_vertices(a, b, q, [rec.i], [rec.j], [rec.u])
+    assert (chk.height, chk.v_low, chk.v_high) == (rec.height, rec.v_low, rec.v_high)
+    half = total // 2
+    merged = lms.backend.merge(record_from_native(ctx.solve(q, 0, half)),
+                               record_from_native(ctx.solve(q, half, total)))
+    assert merged == rec
+    assert abs(rec.u - 2.0) < 0.01
