@@ -50,36 +50,63 @@ class SupportPoints(Sequence):
     reference's tuples) and hashes like the equivalent tuple.
     """
 
-    __slots__ = ("_x", "_y")
+    __slots__ = ("_xy", "_ids", "_width")
 
     def __init__(self, x: np.ndarray, y: np.ndarray):
-        self._x = np.asarray(x, dtype=float)
-        self._y = np.asarray(y, dtype=float)
+        self._xy = (np.asarray(x, dtype=float), np.asarray(y, dtype=float))
+        self._ids = None
+        self._width = 0
 
     @classmethod
     def from_pixels(cls, ids: np.ndarray, width: int) -> "SupportPoints":
-        ids = np.asarray(ids, dtype=np.int64)
-        return cls((ids % width).astype(float), (ids // width).astype(float))
+        """Backed by pixel indices (row-major, ``width`` columns); the float
+        coordinates are formed on first use."""
+        sp = cls.__new__(cls)
+        sp._xy = None
+        sp._ids = np.asarray(ids, dtype=np.int64)
+        sp._width = int(width)
+        return sp
+
+    @staticmethod
+    def _pixel_xy(ids: np.ndarray, width: int) -> tuple[np.ndarray, np.ndarray]:
+        row, col = np.divmod(ids, width)
+        return col.astype(float), row.astype(float)
 
     @property
     def xy(self) -> tuple[np.ndarray, np.ndarray]:
-        return self._x, self._y
+        if self._xy is None:
+            self._xy = self._pixel_xy(self._ids, self._width)
+        return self._xy
+
+    def thinned_xy(self, cap: int) -> tuple[np.ndarray, np.ndarray]:
+        """Coordinates of the even-stride subsample (detect.py:118-131)
+        without materialising the whole support."""
+        m = len(self)
+        if m <= cap:
+            return self.xy
+        idx = _subsample_index(m, cap)
+        if self._xy is None:
+            return self._pixel_xy(self._ids[idx], self._width)
+        return self._xy[0][idx], self._xy[1][idx]
 
     def __len__(self) -> int:
-        return int(self._x.size)
+        return int(self._ids.size if self._xy is None else self._xy[0].size)
 
     def __getitem__(self, k):
+        x, y = self.xy
         if isinstance(k, slice):
-            return SupportPoints(self._x[k], self._y[k])
-        return Point2(float(self._x[k]), float(self._y[k]))
+            return SupportPoints(x[k], y[k])
+        return Point2(float(x[k]), float(y[k]))
 
     def __iter__(self):
-        for x, y in zip(self._x.tolist(), self._y.tolist()):
-            yield Point2(x, y)
+        x, y = self.xy
+        for xv, yv in zip(x.tolist(), y.tolist()):
+            yield Point2(xv, yv)
 
     def __eq__(self, other) -> bool:
         if isinstance(other, SupportPoints):
-            return np.array_equal(self._x, other._x) and np.array_equal(self._y, other._y)
+            (ax, ay), (bx, by) = self.xy, other.xy
+            return np.array_equal(ax, bx) and np.array_equal(ay, by)
         if isinstance(other, Sequence) and not isinstance(other, (str, bytes)):
             return len(other) == len(self) and all(a == b for a, b in zip(self, other))
         return NotImplemented
@@ -168,10 +195,12 @@ def subsample_support(support, cap: int):
 
 
 def _thinned_xy(support, cap: int | None) -> tuple[np.ndarray, np.ndarray]:
+    if cap is not None and cap < 3:
+        raise InvalidInputError(f"support cap must be at least 3, got {cap}")
+    if cap is not None and isinstance(support, SupportPoints):
+        return support.thinned_xy(cap)
     x, y = _support_xy(support)
     if cap is not None:
-        if cap < 3:
-            raise InvalidInputError(f"support cap must be at least 3, got {cap}")
         if x.size > cap:
             idx = _subsample_index(x.size, cap)
             x, y = x[idx], y[idx]
