@@ -548,7 +548,7 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
                                c->item_fit.p, seed_cap, sc + 2, c->stream);
   RC_TRY(exact_list(sc + 2, seed_cap, c->ranks.p, c->item_fit.p));
   lmsb::launch_band_seeds(bf, w, c->ranks.p, c->item_fit.p, 0, seed_cap, sc + 2, c->stream);
-  RC_TRY(exact_list(sc + 2, seed_cap, c->ranks.p, c->item_fit.p));
+  RC_TRY(exact_list(sc + 2, seed_cap, c->ranks.p, c->item_fit.p));  // pruned against the edges' H
   lms_candidate hb{};
   std::vector<unsigned> scnt(K);
   CUDA_TRY(cudaMemcpyAsync(&hb, c->best.p, sizeof(hb), cudaMemcpyDeviceToHost, c->stream));
@@ -663,7 +663,6 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   ba.out_fits = c->item_fit.p;
   ba.out_count = sc + 3;
   CUDA_TRY(cudaMemsetAsync(sc + 3, 0, 2 * sizeof(unsigned long long), c->stream));
-  unsigned long long m2 = 0, m3 = 0, m1 = 0;
   if (m > 0) {
     const int fgrid = (int)(((int64_t)m + ba.chunk - 1) / ba.chunk + ba.nlist);
     if (big) lmsb::launch_band_filter_big(bf, ba, c->bbig_store.p, fgrid, c->stream);
@@ -677,49 +676,21 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     bc.out_fits = c->bfits2.p;
     bc.fit = 0;
     bc.out_count = sc + 4;
-    bc.out_margin = c->bmargin.p;
+    bc.out_margin = nullptr;
     bc.make_lines = true;
     lmsb::launch_band_count(bf, bc, c->sms, c->stream);
     CUDA_TRY(cudaGetLastError());
     st->launches += 4;
-    unsigned long long cnts[2] = {0, 0};
-    CUDA_TRY(cudaMemcpyAsync(cnts, sc + 3, sizeof(cnts), cudaMemcpyDeviceToHost, c->stream));
-    CUDA_TRY(cudaStreamSynchronize(c->stream));
-    m1 = cnts[0];
-    m2 = cnts[1];
-  }
-  if (m2 > 0) {
-    constexpr int64_t kFirstWave = 128;
-    int64_t* sorted = c->branks2.p + scap;
-    RC_TRY(c->btemp.need((int64_t)std::max(lmsb::band_order_temp_bytes((int64_t)m2),
-                                           (size_t)c->btemp.cap)));
-    if (lmsb::launch_band_order(c->bmargin.p, c->bmargin.p + scap, c->branks2.p, sorted,
-                                (int64_t)m2, c->btemp.p, (size_t)c->btemp.cap, c->stream) != 0)
-      return set_error(LMS_ERR_CUDA, "survivor ordering sort failed");
-    RC_TRY(exact_list(nullptr, std::min<int64_t>(kFirstWave, (int64_t)m2), sorted, c->bfits2.p));
-    if ((int64_t)m2 > kFirstWave) {
-      lmsb::BandCount bc{};
-      bc.lines = c->blines32.p;
-      bc.best = c->best.p;
-      bc.in_ranks = sorted + kFirstWave;
-      bc.in_count = sc + 4;  // the rest of the ordered survivors (staged below)
-      bc.out_ranks = c->ranks.p;
-      bc.out_fits = c->item_fit.p;
-      bc.fit = 0;
-      bc.out_count = sc + 3;
-      bc.out_margin = nullptr;
-      bc.make_lines = false;
-      const unsigned long long rest = m2 - kFirstWave;
-      CUDA_TRY(cudaMemcpyAsync(sc + 4, &rest, sizeof(rest), cudaMemcpyHostToDevice, c->stream));
-      lmsb::launch_band_count(bf, bc, c->sms, c->stream);
-      RC_TRY(exact_list(sc + 3, scap, c->ranks.p, c->item_fit.p));
-      CUDA_TRY(cudaMemcpyAsync(&m3, sc + 3, sizeof(m3), cudaMemcpyDeviceToHost, c->stream));
-    }
+    // the window-edge seeds put H at (or within a few ulps of) the optimum, so
+    // the exact stage's pass 0 prunes every survivor that cannot tie it
+    RC_TRY(exact_list(sc + 4, scap, c->branks2.p, c->bfits2.p));
   }
   CUDA_TRY(cudaEventRecord(c->ev_chunk[4], c->stream));
+  unsigned long long cnts[2] = {0, 0};
+  CUDA_TRY(cudaMemcpyAsync(cnts, sc + 3, sizeof(cnts), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
-  st->survivors = (int64_t)std::min<unsigned long long>(m2, 128) + (int64_t)m3;
-  st->band_survivors = (int64_t)m1;
+  st->survivors = (int64_t)cnts[1];
+  st->band_survivors = (int64_t)cnts[0];
   st->filtered_vertices = (int64_t)m;
   st->chunks = 1;
   float ms = 0.f;

@@ -33,7 +33,10 @@ namespace lmsb {
 
 namespace {
 
-constexpr int kExactThreads = 256;
+#ifndef LMSB_EXACT_THREADS
+#define LMSB_EXACT_THREADS 256
+#endif
+constexpr int kExactThreads = LMSB_EXACT_THREADS;
 constexpr int kExactWarps = kExactThreads / kWarp;
 
 struct SelectShared {
