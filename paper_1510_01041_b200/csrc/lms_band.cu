@@ -438,10 +438,17 @@ __device__ __forceinline__ void advance_pair(int n, int step, int& i, int& j) {
   }
 }
 
+template <int kR>
 __global__ void __launch_bounds__(kCollectThreads) band_collect_kernel(
     BandFit bf, const float* __restrict__ bounds, int K, const uint8_t* __restrict__ flag,
     BandRuns runs, uint32_t* __restrict__ out_keys, uint32_t* __restrict__ out_vals, int64_t cap,
     unsigned long long* __restrict__ count) {
+  float rlo[kR], rhi[kR];
+#pragma unroll
+  for (int k = 0; k < kR; ++k) {
+    rlo[k] = runs.lo[k];
+    rhi[k] = runs.hi[k];
+  }
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int kWarps = kCollectThreads / 32;
   uint32_t* queue = reinterpret_cast<uint32_t*>(smem_raw);  // [kWarps][64]
@@ -530,8 +537,7 @@ __global__ void __launch_bounds__(kCollectThreads) band_collect_kernel(
           const float u32 = __fdividef((float)num, (float)da);
           cand = !(fabsf(u32) <= FLT_MAX) || fabs(da) < 1e-30 || (num != 0.0 && fabs(num) < 1e-30);
 #pragma unroll
-          for (int k = 0; k < kMaxRuns; ++k)
-            if (k < runs.count) cand |= (u32 >= runs.lo[k]) & (u32 <= runs.hi[k]);
+          for (int k = 0; k < kR; ++k) cand |= (u32 >= rlo[k]) & (u32 <= rhi[k]);
         }
       }
       const unsigned cm = __ballot_sync(0xffffffffu, cand);
@@ -1032,11 +1038,27 @@ void launch_band_seeds(const BandFit& bf, const BandWork& w, int64_t* ranks, int
 
 void launch_band_collect(const BandFit& bf, const BandWork& w, const BandRuns& runs, int64_t cap,
                          int sms, cudaStream_t st) {
-  static bool done = false;
-  set_smem(band_collect_kernel, band_collect_smem(kBandMaxK), &done);
   cudaMemsetAsync(w.ncollect, 0, sizeof(unsigned long long), st);
-  band_collect_kernel<<<sms * 4, kCollectThreads, band_collect_smem(w.K), st>>>(
-      bf, w.bounds, w.K, w.flag, runs, w.ckeys, w.cvals, cap, w.ncollect);
+  switch (runs.count) {
+#define LMSB_COLLECT(R)                                                                       \
+  case R: {                                                                                   \
+    static bool done = false;                                                                 \
+    set_smem(band_collect_kernel<R>, band_collect_smem(kBandMaxK), &done);                    \
+    band_collect_kernel<R><<<sms * 4, kCollectThreads, band_collect_smem(w.K), st>>>(         \
+        bf, w.bounds, w.K, w.flag, runs, w.ckeys, w.cvals, cap, w.ncollect);                  \
+    break;                                                                                    \
+  }
+    LMSB_COLLECT(1)
+    LMSB_COLLECT(2)
+    LMSB_COLLECT(3)
+    LMSB_COLLECT(4)
+    LMSB_COLLECT(5)
+    LMSB_COLLECT(6)
+    LMSB_COLLECT(7)
+    default:
+    LMSB_COLLECT(8)
+#undef LMSB_COLLECT
+  }
 }
 
 void launch_band_count(const BandFit& bf, const BandCount& bc, int sms, cudaStream_t st) {

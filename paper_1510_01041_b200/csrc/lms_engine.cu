@@ -592,6 +592,11 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   }
   lmsb::BandRuns runs{};
   runs.count = (int)rr.size();
+  if (runs.count == 0) {  // nothing flagged: an empty run (only beyond-range vertices)
+    runs.count = 1;
+    runs.lo[0] = INFINITY;
+    runs.hi[0] = -INFINITY;
+  }
   for (int e = 0; e < runs.count; ++e) {
     const int k0 = rr[e].first, k1 = rr[e].second;
     const double lo = k0 == 0 ? -INFINITY : (double)std::nextafter(hbnd[k0 - 1], -INFINITY);
