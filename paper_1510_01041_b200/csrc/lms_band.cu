@@ -678,7 +678,7 @@ __global__ void __launch_bounds__(kCountThreads) band_count_kernel(
 // Seeds from the narrowest q-window of each listed band: the lines whose
 // keys (recomputed exactly as the bound kernel formed them) lie among the
 // kEdge keys around either end of the window, paired within each end.
-__global__ void __launch_bounds__(256) band_edge_seed_kernel(BandFit bf, BandArgs ba,
+__global__ void __launch_bounds__(1024) band_edge_seed_kernel(BandFit bf, BandArgs ba,
                                                             const int32_t* __restrict__ bands,
                                                             int64_t* __restrict__ ranks,
                                                             int32_t* __restrict__ fits,
@@ -1024,7 +1024,7 @@ void launch_band_edge_seeds(const BandFit& bf, const BandArgs& ba, const int32_t
                             int64_t* ranks, int32_t* fits, int64_t cap,
                             unsigned long long* count, cudaStream_t st) {
   if (nb > 0 && ba.edge)
-    band_edge_seed_kernel<<<nb, 256, 0, st>>>(bf, ba, bands, ranks, fits, cap, count);
+    band_edge_seed_kernel<<<nb, 1024, 0, st>>>(bf, ba, bands, ranks, fits, cap, count);
 }
 
 void launch_band_seeds(const BandFit& bf, const BandWork& w, int64_t* ranks, int32_t* fits,

@@ -439,7 +439,7 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   w.end = c->bend.p;
   w.temp = c->btemp.p;
   w.temp_bytes = (size_t)c->btemp.cap;
-  while (c->ev_chunk.size() < 8) {
+  while (c->ev_chunk.size() < 10) {
     cudaEvent_t e;
     CUDA_TRY(cudaEventCreate(&e));
     c->ev_chunk.push_back(e);
@@ -460,6 +460,7 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     xa.fit_of = fits;
     xa.bound = c->best.p;
     xa.out = c->recs.p;
+    xa.cached = 1;  // seeds and band survivors: few vertices, latency-bound
     lmsb::launch_exact(xa, persistent_grid(c, -1), c->stream, h.n);
     lmsb::launch_reduce(c->recs.p, d_count, d_count ? 0 : cap, cap, c->fits.p, c->keys.p,
                         c->best.p, (int)c->sms * 4, c->stream);
@@ -549,6 +550,7 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   RC_TRY(exact_list(sc + 2, seed_cap, c->ranks.p, c->item_fit.p));
   lmsb::launch_band_seeds(bf, w, c->ranks.p, c->item_fit.p, 0, seed_cap, sc + 2, c->stream);
   RC_TRY(exact_list(sc + 2, seed_cap, c->ranks.p, c->item_fit.p));  // pruned against the edges' H
+  CUDA_TRY(cudaEventRecord(c->ev_chunk[7], c->stream));
   lms_candidate hb{};
   std::vector<unsigned> scnt(K);
   CUDA_TRY(cudaMemcpyAsync(&hb, c->best.p, sizeof(hb), cudaMemcpyDeviceToHost, c->stream));
@@ -707,6 +709,18 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   st->ms_band_filter = ms;
   CUDA_TRY(cudaEventElapsedTime(&ms, c->ev_chunk[5], c->ev_chunk[6]));
   st->ms_collect = ms;
+  if (getenv("LMSB_BAND_DEBUG")) {
+    float t[6];
+    cudaEventElapsedTime(&t[0], c->ev_chunk[0], c->ev_chunk[1]);
+    cudaEventElapsedTime(&t[1], c->ev_chunk[1], c->ev_chunk[7]);
+    cudaEventElapsedTime(&t[2], c->ev_chunk[7], c->ev_chunk[2]);
+    cudaEventElapsedTime(&t[3], c->ev_chunk[2], c->ev_chunk[3]);
+    cudaEventElapsedTime(&t[4], c->ev_chunk[3], c->ev_chunk[4]);
+    cudaEventElapsedTime(&t[5], c->ev_begin, c->ev_chunk[0]);
+    fprintf(stderr,
+            "band: pre %.3f bound %.3f seeds %.3f gap %.3f collect+group %.3f filter+count+exact %.3f ms\n",
+            t[5], t[0], t[1], t[2], t[3], t[4]);
+  }
   return LMS_OK;
 }
 

@@ -39,21 +39,25 @@ namespace {
 constexpr int kExactThreads = LMSB_EXACT_THREADS;
 constexpr int kExactWarps = kExactThreads / kWarp;
 
-struct SelectShared {
+template <int kW>
+struct SelectSharedT {
   unsigned hist[2][256];
   unsigned long long prefix[2];
   long long rank[2];
   unsigned long long result[2];
   int state[2];  // -1 inactive, 0 searching, 1 unique element pending, 2 done
-  unsigned red_lt[kExactWarps];
-  unsigned red_le[kExactWarps];
-  unsigned red_up[kExactWarps];
-  unsigned red_dn[kExactWarps];
+  unsigned red_lt[kW];
+  unsigned red_le[kW];
+  unsigned red_up[kW];
+  unsigned red_dn[kW];
 };
+using SelectShared = SelectSharedT<kExactWarps>;
+
 
 
 // Warp `t` picks the digit bucket containing rank[t] from hist[t].
-__device__ void pick_digit(SelectShared& sm, int t, int level) {
+template <class SM>
+__device__ void pick_digit(SM& sm, int t, int level) {
   const int lane = threadIdx.x & 31;
   unsigned h[8];
   unsigned sum = 0;
@@ -104,17 +108,24 @@ __device__ void pick_digit(SelectShared& sm, int t, int level) {
 // fl(x - v0) is monotone in x and vs[up] is the q-th smallest x >= v0
 // (backend.py:153,159); otherwise no select is needed and the vertex is
 // reported as not found (it cannot win against a record of height bound).
-__device__ lms_candidate exact_vertex(const double* __restrict__ a, const double* __restrict__ b,
-                                      int64_t n, int64_t q, int64_t i, int64_t j, double u,
-                                      double v0, double bound, SelectShared& sm) {
+// kCached: pass 0 keeps the order-preserving keys of the cut in shared
+// memory (n <= kExactCacheN) and the select passes read them from there
+// instead of recomputing the cut from the L2-resident lines.
+template <int kT, bool kCached, class SM>
+__device__ lms_candidate exact_vertex_t(const double* __restrict__ a,
+                                        const double* __restrict__ b, int64_t n, int64_t q,
+                                        int64_t i, int64_t j, double u, double v0, double bound,
+                                        SM& sm, unsigned long long* cache) {
+  constexpr int kW = kT / kWarp;
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
 
   // Pass 0: rank counts of v0 in the snapped cut (+ window counts vs bound).
   unsigned lt = 0, le = 0, wu = 0, wd = 0;
-  for (int64_t k = tid; k < n; k += kExactThreads) {
+  for (int64_t k = tid; k < n; k += kT) {
     double x = snapped_cut(a, b, k, i, j, u, v0);
+    if (kCached) cache[k] = key_of(x);
     lt += x < v0;
     le += x <= v0;
     wu += x >= v0 && __dsub_rn(x, v0) <= bound;
@@ -133,7 +144,7 @@ __device__ lms_candidate exact_vertex(const double* __restrict__ a, const double
   __syncthreads();
   int64_t c_lt = 0, c_le = 0, c_up = 0, c_dn = 0;
 #pragma unroll
-  for (int w = 0; w < kExactWarps; ++w) {
+  for (int w = 0; w < kW; ++w) {
     c_lt += sm.red_lt[w];
     c_le += sm.red_le[w];
     c_up += sm.red_up[w];
@@ -181,10 +192,10 @@ __device__ lms_candidate exact_vertex(const double* __restrict__ a, const double
     if ((s0 == 2 || s0 == -1) && (s1 == 2 || s1 == -1)) break;
     const unsigned long long p0 = sm.prefix[0];
     const unsigned long long p1 = sm.prefix[1];
-    for (int e = tid; e < 512; e += kExactThreads) (&sm.hist[0][0])[e] = 0u;
+    for (int e = tid; e < 512; e += kT) (&sm.hist[0][0])[e] = 0u;
     __syncthreads();
-    for (int64_t k = tid; k < n; k += kExactThreads) {
-      const unsigned long long key = key_of(snapped_cut(a, b, k, i, j, u, v0));
+    for (int64_t k = tid; k < n; k += kT) {
+      const unsigned long long key = kCached ? cache[k] : key_of(snapped_cut(a, b, k, i, j, u, v0));
       const unsigned long long hi = level == 0 ? 0ULL : (key >> (shift + 8));
       const unsigned digit = (unsigned)(key >> shift) & 255u;
       if (s0 == 0 && hi == p0) atomicAdd(&sm.hist[0][digit], 1u);
@@ -216,6 +227,13 @@ __device__ lms_candidate exact_vertex(const double* __restrict__ a, const double
   }
   __syncthreads();
   return c;
+}
+
+__device__ __forceinline__ lms_candidate exact_vertex(const double* __restrict__ a,
+                                                     const double* __restrict__ b, int64_t n,
+                                                     int64_t q, int64_t i, int64_t j, double u,
+                                                     double v0, double bound, SelectShared& sm) {
+  return exact_vertex_t<kExactThreads, false>(a, b, n, q, i, j, u, v0, bound, sm, nullptr);
 }
 
 __device__ __forceinline__ bool item_vertex(const ExactArgs& args, int64_t s, int32_t& f,
@@ -304,6 +322,34 @@ __global__ void __launch_bounds__(kExactThreads) exact_kernel(ExactArgs args) {
     if (valid) c = exact_vertex(a, b, fd.n, fd.q, i, j, u, v0, bound, sm);
     c.reserved = f;
     if (threadIdx.x == 0) args.out[s] = c;
+  }
+}
+
+constexpr int kCachedThreads = 1024;
+
+// One vertex per CTA with its cut's keys cached in shared memory: few
+// vertices (seeds, band survivors) finish in a fraction of the time the
+// L2-streaming exact_kernel needs per vertex.
+__global__ void __launch_bounds__(kCachedThreads, 1) exact_cached_kernel(ExactArgs args) {
+  using SM = SelectSharedT<kCachedThreads / kWarp>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SM& sm = *reinterpret_cast<SM*>(smem_raw);
+  unsigned long long* cache = reinterpret_cast<unsigned long long*>(smem_raw + ((sizeof(SM) + 15) & ~size_t(15)));
+  int64_t count = args.d_count ? (int64_t)*args.d_count : args.count;
+  if (count > args.capacity) count = args.capacity;
+  for (int64_t s = blockIdx.x; s < count; s += gridDim.x) {
+    int32_t f;
+    FitDesc fd;
+    int64_t i, j;
+    double u, v0, bound;
+    const bool valid = item_vertex(args, s, f, fd, i, j, u, v0, bound);
+    lms_candidate c = cand_none();
+    if (valid)
+      c = exact_vertex_t<kCachedThreads, true>(args.a + fd.off, args.b + fd.off, fd.n, fd.q, i, j,
+                                               u, v0, bound, sm, cache);
+    c.reserved = f;
+    if (threadIdx.x == 0) args.out[s] = c;
+    __syncthreads();
   }
 }
 
@@ -408,6 +454,21 @@ __global__ void gen_seeds_kernel(const FitDesc* __restrict__ fits,
 
 void launch_exact(const ExactArgs& args, int grid, cudaStream_t stream, int64_t max_n) {
   if (grid <= 0) return;
+  if (args.cached && max_n <= kExactCacheN && max_n > kWarpExactMaxN) {
+    using SM = SelectSharedT<kCachedThreads / kWarp>;
+    const size_t smem = ((sizeof(SM) + 15) & ~size_t(15)) + sizeof(unsigned long long) * max_n;
+    static bool done = false;
+    if (!done) {
+      cudaFuncSetAttribute(exact_cached_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(((sizeof(SM) + 15) & ~size_t(15)) +
+                                 sizeof(unsigned long long) * kExactCacheN));
+      done = true;
+    }
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    exact_cached_kernel<<<sms, kCachedThreads, smem, stream>>>(args);
+    return;
+  }
   if (max_n <= kWarpExactMaxN) {
     exact_warp_kernel<<<grid, kWarpExactWarps * 32, 0, stream>>>(args);
   } else {

@@ -57,7 +57,11 @@ struct ExactArgs {
   const double* vv;
   const lms_candidate* bound;  // optional per-fit bound (skip vertices that cannot win)
   lms_candidate* out;          // out[s].reserved = fit id
+  int cached;                  // few vertices: one CTA each, cut keys cached in shared memory
 };
+
+// Largest fit whose cut keys the cached exact kernel keeps in shared memory.
+constexpr int64_t kExactCacheN = 16384;
 
 // One CTA per vertex for large fits, one warp per vertex when every fit has
 // at most 4,096 lines (max_n).
