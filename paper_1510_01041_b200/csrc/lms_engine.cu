@@ -824,12 +824,15 @@ int ctx_solve_fits(lms_ctx* c, const std::vector<HostFit>& hf, lms_candidate* ou
   CUDA_TRY(cudaEventRecord(c->ev_begin, c->stream));
   CUDA_TRY(cudaMemcpyAsync(c->fits.p, fd.data(), sizeof(lmsb::FitDesc) * F,
                            cudaMemcpyHostToDevice, c->stream));
-  CUDA_TRY(cudaMemcpyAsync(c->prefA.p, prefA.data(), sizeof(int64_t) * (F + 1),
-                           cudaMemcpyHostToDevice, c->stream));
-  CUDA_TRY(cudaMemcpyAsync(c->prefB.p, prefB.data(), sizeof(int64_t) * (F + 1),
-                           cudaMemcpyHostToDevice, c->stream));
-  CUDA_TRY(cudaMemcpyAsync(c->seed_prefix.p, seed_pref.data(), sizeof(int64_t) * (F + 1),
-                           cudaMemcpyHostToDevice, c->stream));
+  if (tasks > 0) {  // the count filter's task plan
+    CUDA_TRY(cudaMemcpyAsync(c->prefA.p, prefA.data(), sizeof(int64_t) * (F + 1),
+                             cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(c->prefB.p, prefB.data(), sizeof(int64_t) * (F + 1),
+                             cudaMemcpyHostToDevice, c->stream));
+  }
+  if (seeds > 0)
+    CUDA_TRY(cudaMemcpyAsync(c->seed_prefix.p, seed_pref.data(), sizeof(int64_t) * (F + 1),
+                             cudaMemcpyHostToDevice, c->stream));
   lmsb::launch_reset_best(c->keys.p, c->best.p, F, c->stream);
   st.launches += 1;
 
