@@ -424,3 +424,39 @@ def test_config3_n65536_band_path_properties():
                                record_from_native(ctx.solve(q, half, total)))
     assert merged == rec
     assert abs(rec.u - 2.0) < 0.01
+
+
+@pytest.mark.parametrize("block", range(4))
+def test_band_path_random_sweep_vs_count_filter(block):
+    """Forced band stage vs the count-filter path on 40 random instances per
+    block: mixtures of lines, clusters, heavy-tailed noise, rounded
+    coordinates (ties) and random q."""
+    rng = np.random.default_rng(1000 + block)
+    band = _ctx_with({"LMSB_BAND": "2", "LMSB_BAND_VERTICES": str(int(rng.choice([4096, 16384, 65536])))})
+    filt = _ctx_with({"LMSB_BAND": "0"})
+    for t in range(40):
+        n = int(rng.integers(2100, 3600))
+        kind = t % 5
+        x = rng.uniform(-1, 1, n) * 10 ** rng.uniform(0, 4)
+        if kind == 0:
+            y = rng.normal(0, 1, n) + rng.uniform(-3, 3) * x
+        elif kind == 1:
+            y = np.where(rng.random(n) < 0.5, 0.3 * x + 5, -2.0 * x + rng.standard_cauchy(n))
+        elif kind == 2:
+            x = np.round(x)
+            y = np.round(rng.normal(0, 50, n))
+        elif kind == 3:
+            c = rng.integers(0, 5, n)
+            y = c * 100.0 + rng.normal(0, 1, n) + 0.1 * x
+        else:
+            y = np.where(rng.random(n) < 0.3, 7.0, rng.normal(0, 1e4, n))
+        if np.unique(x).size < 2:
+            continue
+        q = int(rng.integers(2, n + 1)) if t % 2 else n // 2 + 1
+        total = n * (n - 1) // 2
+        band.upload(x, y)
+        filt.upload(x, y)
+        got = record_from_native(band.solve(q, 0, total))
+        assert band.stats()["bands"] > 0
+        want = record_from_native(filt.solve(q, 0, total))
+        assert got == want, (block, t, n, q)
