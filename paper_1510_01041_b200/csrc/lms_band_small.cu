@@ -53,6 +53,7 @@ constexpr int kSamples = kMaxBands * kSamplesPerBand;  // 2,048
 constexpr int kSampleItems = kSamples / kThreads;
 constexpr int kSeedsPerBand = 16;
 constexpr int kSeedBands = 2;
+constexpr int kEdge = 5;  // keys kept around each end of a band's narrowest q-window
 constexpr int kSlots = 16;    // admitted bands whose keys are resident at once
 constexpr int kSegRun = 16;   // ranks per lane per warp segment
 constexpr int kMaxRuns = 8;   // slope runs tested before a band lookup
@@ -77,6 +78,9 @@ struct SmallShared {
   };
   float bounds[kMaxBands - 1];
   double lb[kMaxBands], um[kMaxBands], wq[kMaxBands];
+  float edge[kMaxBands][2 * 5];  // keys around the ends of each band's narrowest q-window
+  int egrp[2][16];               // edge-seed line groups
+  int negrp[2];
   int16_t band_slot[kMaxBands];
   int admitted[kMaxBands];
   int nadmitted;
@@ -339,6 +343,20 @@ __global__ void __launch_bounds__(kThreads, 2) small_fit_kernel(SmallArgs args) 
     for (int l = lane; l + q - 1 < n; l += 32) w = fmin(w, (double)ks[l + q - 1] - (double)ks[l]);
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) w = fmin(w, __shfl_xor_sync(0xffffffffu, w, off));
+    {  // the narrowest window's position, its end keys for the edge seeds
+      int ks_ = n;
+      for (int l = lane; l + q - 1 < n; l += 32)
+        if ((double)ks[l + q - 1] - (double)ks[l] == w) {
+          ks_ = l;
+          break;
+        }
+      ks_ = __reduce_min_sync(0xffffffffu, (unsigned)ks_);
+      if (lane < 2 * kEdge && ks_ < n) {
+        const int t = lane % kEdge;
+        const int at = (lane < kEdge ? ks_ : ks_ + q - 1) + t - kEdge / 2;
+        sh.edge[k][lane] = ks[min(max(at, 0), n - 1)];
+      }
+    }
     if (lane == 0) {
       const double dmax = dev * fmax(uR - uM, uM - uL) * (1.0 + 0x1p-40);
       const double e = 0x1p-20 * (fmax(fabs(uL), fabs(uR)) * am + bm + fabs(uM) * dev) + 1e-300;
@@ -387,6 +405,34 @@ __global__ void __launch_bounds__(kThreads, 2) small_fit_kernel(SmallArgs args) 
     }
   }
   __syncthreads();
+  // window-edge pairs of the seed bands first: lines whose keys sit among the
+  // kEdge keys around either end of the band's narrowest q-window, paired
+  // within each end (the optimum's anchors are window-end lines)
+  for (int t = 0; t < kSeedBands; ++t) {
+    const int band = sh.seed_band[t];
+    if (band < 0) continue;  // uniform
+    if (tid < 2) sh.negrp[tid] = 0;
+    __syncthreads();
+    const double uM = sh.um[band];
+    for (int l = tid; l < n; l += kThreads) {
+      const float key = (float)__dsub_rn(__dmul_rn(__dsub_rn(sh.a[l], c), uM), sh.b[l]);
+#pragma unroll
+      for (int g = 0; g < 2; ++g)
+        if (key >= sh.edge[band][g * kEdge] && key <= sh.edge[band][g * kEdge + kEdge - 1]) {
+          const int slot = atomicAdd(&sh.negrp[g], 1);
+          if (slot < 16) sh.egrp[g][slot] = l;
+        }
+    }
+    __syncthreads();
+    for (int g = 0; g < 2; ++g) {
+      const int m = min(sh.negrp[g], 16);
+      for (int pr = warp; pr < m * m; pr += kWarps) {
+        const int x = sh.egrp[g][pr / m], y = sh.egrp[g][pr % m];
+        if (x < y) exact_one(x, y);
+      }
+    }
+    __syncthreads();
+  }
   {
     const int sv = sh.nvalid;
     for (int t = warp; t < kSeedBands * kSeedsPerBand; t += kWarps) {
