@@ -200,7 +200,7 @@ def run_reference(args):
 
 # --------------------------------------------------------------------------- configs 1, 4, 5
 def other_configs(device: int, reps: int = 3) -> dict:
-    """Device / end-to-end times of BASELINE.json configs 1, 4 and 5 (median
+    """Device / end-to-end times of BASELINE.json configs 1, 3, 4 and 5 (median
     of `reps` after one warm-up), reported beside the headline config 2."""
     import paper_1510_01041_b200 as lms
     from paper_1510_01041_b200 import _native, workloads
@@ -224,6 +224,14 @@ def other_configs(device: int, reps: int = 3) -> dict:
     ms = timed(lambda: ctx.solve(501, 0, 1000 * 999 // 2))
     res["config1"] = {"workload": "n=1000, 45% outliers, q=501", "ms_per_fit": ms,
                       "evals_per_s": 1000 * 499500 / (ms / 1e3)}
+    # config 3: n = 65,536 on this one GPU (the multi-GPU case shards this rank space)
+    n3 = 65536
+    pts3 = workloads.contaminated_line_points(n3, 0)
+    ctx.upload(pts3[:, 0], pts3[:, 1])
+    P3 = n3 * (n3 - 1) // 2
+    ms = timed(lambda: ctx.solve(n3 // 2 + 1, 0, P3))
+    res["config3"] = {"workload": "n=65536, 49% outliers, q=32769, one GPU (all 2,147,450,880 pairs)",
+                      "ms_per_fit": ms, "evals_per_s": n3 * P3 / (ms / 1e3)}
     # config 4: 8,192 fits of bench_points(512) (experiments.py:247-254)
     F, m = 8192, 512
     sets = [workloads.bench_points(m, seed=f) for f in range(F)]
