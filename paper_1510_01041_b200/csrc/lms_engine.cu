@@ -460,7 +460,11 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     xa.fit_of = fits;
     xa.bound = c->best.p;
     xa.out = c->recs.p;
-    xa.cached = 1;  // seeds and band survivors: few vertices, latency-bound
+    // few vertices (seeds, band survivors): latency-bound, one CTA per vertex
+    // with its cut cached; a long list (degenerate q, loose bounds) streams
+    // everything beyond the first 8 per SM
+    xa.cached = 1;
+    xa.cached_end = (int64_t)c->sms * 8;
     lmsb::launch_exact(xa, persistent_grid(c, -1), c->stream, h.n);
     lmsb::launch_reduce(c->recs.p, d_count, d_count ? 0 : cap, cap, c->fits.p, c->keys.p,
                         c->best.p, (int)c->sms * 4, c->stream);

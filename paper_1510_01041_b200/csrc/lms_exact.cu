@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(kExactThreads) exact_kernel(ExactArgs args) {
   __shared__ SelectShared sm;
   int64_t count = args.d_count ? (int64_t)*args.d_count : args.count;
   if (count > args.capacity) count = args.capacity;
-  for (int64_t s = blockIdx.x; s < count; s += gridDim.x) {
+  for (int64_t s = args.begin + blockIdx.x; s < count; s += gridDim.x) {
     const int32_t f = args.mode == kSrcList ? args.fit_of[s] : 0;
     const FitDesc fd = args.fits[f];
     const double* a = args.a + fd.off;
@@ -337,6 +337,7 @@ __global__ void __launch_bounds__(kCachedThreads, 1) exact_cached_kernel(ExactAr
   unsigned long long* cache = reinterpret_cast<unsigned long long*>(smem_raw + ((sizeof(SM) + 15) & ~size_t(15)));
   int64_t count = args.d_count ? (int64_t)*args.d_count : args.count;
   if (count > args.capacity) count = args.capacity;
+  if (args.cached_end > 0 && count > args.cached_end) count = args.cached_end;
   for (int64_t s = blockIdx.x; s < count; s += gridDim.x) {
     int32_t f;
     FitDesc fd;
@@ -467,6 +468,12 @@ void launch_exact(const ExactArgs& args, int grid, cudaStream_t stream, int64_t 
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     exact_cached_kernel<<<sms, kCachedThreads, smem, stream>>>(args);
+    if (args.cached_end <= 0) return;
+    // the rest of a long list (beyond cached_end) streams
+    ExactArgs rest = args;
+    rest.begin = args.cached_end;
+    rest.cached = 0;
+    exact_kernel<<<grid, kExactThreads, 0, stream>>>(rest);
     return;
   }
   if (max_n <= kWarpExactMaxN) {

@@ -58,6 +58,8 @@ struct ExactArgs {
   const lms_candidate* bound;  // optional per-fit bound (skip vertices that cannot win)
   lms_candidate* out;          // out[s].reserved = fit id
   int cached;                  // few vertices: one CTA each, cut keys cached in shared memory
+  int64_t cached_end;          // cached: items beyond this go to the streaming kernel (0: none)
+  int64_t begin;               // streaming kernel: first item
 };
 
 // Largest fit whose cut keys the cached exact kernel keeps in shared memory.

@@ -460,3 +460,20 @@ def test_band_path_random_sweep_vs_count_filter(block):
         assert band.stats()["bands"] > 0
         want = record_from_native(filt.solve(q, 0, total))
         assert got == want, (block, t, n, q)
+
+
+def test_band_path_degenerate_q_many_ties():
+    """q = 2: every vertex has height 0, the band stage admits everything and
+    the exact stage sees a huge tied list; the winner is the smallest pair."""
+    n = 3000
+    pts = workloads.contaminated_line_points(n, 9)
+    a, b = pts[:, 0].copy(), pts[:, 1].copy()
+    total = n * (n - 1) // 2
+    band = _ctx_with({"LMSB_BAND": "2"})
+    filt = _ctx_with({"LMSB_BAND": "0"})
+    band.upload(a, b)
+    filt.upload(a, b)
+    for q in (2, 3):
+        got = record_from_native(band.solve(q, 0, total))
+        want = record_from_native(filt.solve(q, 0, total))
+        assert got == want, q
