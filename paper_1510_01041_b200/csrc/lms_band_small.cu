@@ -45,6 +45,9 @@ namespace lmsb {
 
 namespace {
 
+#ifndef LMSB_SMALL_MINB
+#define LMSB_SMALL_MINB 2
+#endif
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxBands = 128;
@@ -63,18 +66,27 @@ struct SmallShared {
   static constexpr int kNP = 32 * kItems;  // padded lines (one warp sorts a band)
   using SampleSort = cub::BlockRadixSort<float, kThreads, kSampleItems, int>;
   double a[kNP], b[kNP];
-  float2 l32[kNP];
   float4 l2[kNP / 2];         // (A_k, A_k+1, -B_k, -B_k+1) for the packed counts
   float rlo[kMaxRuns], rhi[kMaxRuns];  // slope runs of the current sweep (widened)
   int nruns;
-  float wkeys[kWarps][kNP];   // per-warp sort output
-  float slot[kSlots][kNP];    // resident keys of admitted bands
+  // phase-disjoint storage: the bound phase sorts into wkeys, the seeds and
+  // sweeps select with sw; the samples live until the seeds, the admitted
+  // bands' keys (slots) only in the sweeps
   union {
-    typename SampleSort::TempStorage ssort;
+    float wkeys[kWarps][kNP];   // per-warp sort output (bound phase)
+    SelectWarp sw[kWarps];      // exact select state (seeds, sweeps)
+  };
+  union {
     struct {
-      float skey[kSamples];
-      int sidx[kSamples];
-    } s;
+      union {
+        typename SampleSort::TempStorage ssort;
+        struct {
+          float skey[kSamples];
+          int sidx[kSamples];
+        } s;
+      };
+    };
+    float slot[kSlots][kNP];    // resident keys of admitted bands (sweeps)
   };
   float bounds[kMaxBands - 1];
   double lb[kMaxBands], um[kMaxBands], wq[kMaxBands];
@@ -85,7 +97,6 @@ struct SmallShared {
   int admitted[kMaxBands];
   int nadmitted;
   int seed_band[kSeedBands];
-  SelectWarp sw[kWarps];
   uint32_t queue[kWarps][64];   // fp32-count queue
   uint32_t squeue[kWarps][64];  // in-run vertices awaiting band lookup + padded counts
   lms_candidate wbest[kWarps];
@@ -211,7 +222,7 @@ __device__ __forceinline__ void band_keys_warp(const SmallShared<kItems>& sh, in
 }
 
 template <int kItems>
-__global__ void __launch_bounds__(kThreads, 2) small_fit_kernel(SmallArgs args) {
+__global__ void __launch_bounds__(kThreads, LMSB_SMALL_MINB) small_fit_kernel(SmallArgs args) {
   using SH = SmallShared<kItems>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SH& sh = *reinterpret_cast<SH*>(smem_raw);
@@ -241,8 +252,6 @@ __global__ void __launch_bounds__(kThreads, 2) small_fit_kernel(SmallArgs args) 
   bm = -block_min<kItems>(-bm, sh, 1);
   const double c = 0.5 * alo + 0.5 * ahi;
   const double dev = fmax(ahi - c, c - alo) * (1.0 + 0x1p-40) + 1e-300;
-  for (int k = tid; k < n; k += kThreads)
-    sh.l32[k] = make_float2((float)__dsub_rn(sh.a[k], c), (float)sh.b[k]);
   for (int p2 = tid; p2 < SH::kNP / 2; p2 += kThreads) {
     const int k = 2 * p2;
     float4 r = make_float4(0.f, 0.f, __int_as_float(0x7fc00000), __int_as_float(0x7fc00000));
