@@ -1273,7 +1273,7 @@ int ctx_support(lms_ctx* c, const double* cos_p, const double* sin_p, const int6
                               c->hough_mode == 2 ? c->pys.p : nullptr, npts, c->hough_width,
                               c->tcos.p, c->tsin.p, c->rbin.p, np, rho_max, drho, n_rho,
                               c->masks.p, c->scounts.p, c->soffsets.p, c->scan_tmp.p,
-                              (size_t)c->scan_tmp.cap, c->sout.p, c->stream) != 0)
+                              (size_t)c->scan_tmp.cap, c->sout.p, c->sout.cap, c->stream) != 0)
         return set_error(LMS_ERR_CUDA, "support scan failed");
       CUDA_TRY(cudaGetLastError());
       CUDA_TRY(cudaMemcpyAsync(goff.data(), c->soffsets.p, sizeof(int64_t) * m,

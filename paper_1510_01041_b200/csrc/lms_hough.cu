@@ -58,6 +58,32 @@ __device__ __forceinline__ int64_t rho_bin(double x, double y, double c, double 
   return r;
 }
 
+// rho_bin through an fp32 estimate: rho32 = x c + y s with every operand
+// rounded to fp32 is within E = 2^-19 (|x c| + |y s| + |rho32| + rho_max) +
+// 1e-30 of the reference's fp64 rho (fp32 operand / product / sum roundings
+// <= 4 * 2^-24 of the magnitudes), and the fp32 bin coordinates of rho32 -+ E
+// bracket the fp64 one (their own roundings add 2^-23 relative, inside E's
+// slack).  When both ends floor to the same bin that bin is exact; otherwise
+// (within E of a bin edge, or non-finite) the fp64 path decides.
+__device__ __forceinline__ int64_t rho_bin_fast(double x, double y, const double* c, const double* s,
+                                                float c32, float s32, double rho_max,
+                                                float rho_max32, double drho, float inv_drho32,
+                                                int64_t n_rho) {
+  const float x32 = (float)x, y32 = (float)y;
+  const float xc = x32 * c32, ys = y32 * s32;
+  const float rho32 = xc + ys;
+  const float E = 0x1p-19f * (fabsf(xc) + fabsf(ys) + fabsf(rho32) + rho_max32) + 1e-30f;
+  const float glo = floorf((rho32 - E + rho_max32) * inv_drho32);
+  const float ghi = floorf((rho32 + E + rho_max32) * inv_drho32);
+  if (glo == ghi && fabsf(glo) < 0x1p22f) {
+    int64_t r = (int64_t)glo;
+    if (r < 0) r = 0;
+    if (r > n_rho - 1) r = n_rho - 1;
+    return r;
+  }
+  return rho_bin(x, y, *c, *s, rho_max, drho, n_rho);
+}
+
 // A point is either a pixel index (x = p % width, y = p / width) or an
 // explicit (x, y) pair (xs != nullptr).
 struct PointSrc {
@@ -79,6 +105,7 @@ struct PointSrc {
 };
 
 constexpr int kVoteThreads = 256;
+constexpr int kMaxTheta = 512;  // theta bins with fp32 trig staged in shared memory
 
 __global__ void __launch_bounds__(kVoteThreads)
     vote_kernel(PointSrc src, int64_t npts, const double* __restrict__ cos_t,
@@ -86,7 +113,13 @@ __global__ void __launch_bounds__(kVoteThreads)
                 double rho_max, double drho, int64_t n_rho, int use_smem,
                 unsigned long long* __restrict__ acc) {
   extern __shared__ unsigned int hist[];
+  __shared__ float2 cs32[kMaxTheta];
   const int64_t nbins = n_rho * n_theta;
+  const float rho_max32 = (float)rho_max;
+  const float inv_drho32 = (float)(1.0 / drho);
+  for (int t = threadIdx.x; t < n_theta && t < kMaxTheta; t += blockDim.x)
+    cs32[t] = make_float2((float)cos_t[t], (float)sin_t[t]);
+  __syncthreads();
   if (use_smem) {
     for (int64_t e = threadIdx.x; e < nbins; e += blockDim.x) hist[e] = 0u;
     __syncthreads();
@@ -96,7 +129,9 @@ __global__ void __launch_bounds__(kVoteThreads)
     double x, y;
     src.get(k, x, y);
     for (int t = 0; t < n_theta; ++t) {
-      const int64_t r = rho_bin(x, y, cos_t[t], sin_t[t], rho_max, drho, n_rho);
+      const float2 cs = t < kMaxTheta ? cs32[t] : make_float2((float)cos_t[t], (float)sin_t[t]);
+      const int64_t r = rho_bin_fast(x, y, cos_t + t, sin_t + t, cs.x, cs.y, rho_max, rho_max32,
+                                     drho, inv_drho32, n_rho);
       const int64_t bin = r * n_theta + t;
       if (use_smem) atomicAdd(&hist[bin], 1u);
       else atomicAdd(&acc[bin], 1ULL);
@@ -123,12 +158,27 @@ struct PeakArgs {
   int64_t n_rho;
 };
 
-__device__ __forceinline__ unsigned long long member_mask(double x, double y, const PeakArgs& pk) {
-  unsigned long long m = 0ULL;
-  for (int q = 0; q < pk.npeaks; ++q) {
-    const int64_t r = rho_bin(x, y, pk.cos_p[q], pk.sin_p[q], pk.rho_max, pk.drho, pk.n_rho);
-    if (r == pk.rbin_p[q]) m |= 1ULL << q;
+// Peaks sharing a theta bin share their support trig (support_trig of the
+// bin, hough.py:181-182): one rho bin per distinct (cos, sin) slot, then one
+// compare per peak.
+__device__ __forceinline__ unsigned long long member_mask(double x, double y, const PeakArgs& pk,
+                                                         const float2* __restrict__ cs32,
+                                                         const int* __restrict__ slot_peak,
+                                                         int nslot,
+                                                         const int* __restrict__ peak_slot,
+                                                         const int* __restrict__ rb) {
+  const float rho_max32 = (float)pk.rho_max;
+  const float inv_drho32 = (float)(1.0 / pk.drho);
+  int bins[64];
+#pragma unroll 4
+  for (int t = 0; t < nslot; ++t) {
+    const int q = slot_peak[t];
+    bins[t] = (int)rho_bin_fast(x, y, pk.cos_p + q, pk.sin_p + q, cs32[t].x, cs32[t].y,
+                                pk.rho_max, rho_max32, pk.drho, inv_drho32, pk.n_rho);
   }
+  unsigned long long m = 0ULL;
+  for (int q = 0; q < pk.npeaks; ++q)
+    if (bins[peak_slot[q]] == rb[q]) m |= 1ULL << q;
   return m;
 }
 
@@ -139,7 +189,27 @@ __global__ void __launch_bounds__(kSupThreads)
                          unsigned long long* __restrict__ masks,
                          int64_t* __restrict__ counts, int64_t nblocks) {
   __shared__ unsigned int cnt[64];
-  if (threadIdx.x < 64) cnt[threadIdx.x] = 0u;
+  __shared__ float2 cs32[64];
+  __shared__ int rb[64], peak_slot[64], slot_peak[64];
+  __shared__ int nslot;
+  if (threadIdx.x < 64) {
+    cnt[threadIdx.x] = 0u;
+    if (threadIdx.x < pk.npeaks) rb[threadIdx.x] = (int)pk.rbin_p[threadIdx.x];
+  }
+  if (threadIdx.x == 0) {
+    int ns = 0;
+    for (int q = 0; q < pk.npeaks; ++q) {
+      int t = 0;
+      while (t < ns && !(pk.cos_p[slot_peak[t]] == pk.cos_p[q] && pk.sin_p[slot_peak[t]] == pk.sin_p[q])) ++t;
+      if (t == ns) {
+        slot_peak[ns] = q;
+        cs32[ns] = make_float2((float)pk.cos_p[q], (float)pk.sin_p[q]);
+        ++ns;
+      }
+      peak_slot[q] = t;
+    }
+    nslot = ns;
+  }
   __syncthreads();
   const int64_t base = (int64_t)blockIdx.x * kSupChunk;
   for (int it = 0; it < kSupItems; ++it) {
@@ -148,7 +218,7 @@ __global__ void __launch_bounds__(kSupThreads)
     if (k < npts) {
       double x, y;
       src.get(k, x, y);
-      m = member_mask(x, y, pk);
+      m = member_mask(x, y, pk, cs32, slot_peak, nslot, peak_slot, rb);
       masks[k] = m;
     }
     while (m) {
@@ -162,48 +232,44 @@ __global__ void __launch_bounds__(kSupThreads)
 }
 
 // Pass 2: ordered write of each block's members; offsets = exclusive scan of
-// counts, so peak q's block b writes from offsets[q * nblocks + b].
+// counts, so peak q's block b writes from offsets[q * nblocks + b].  The
+// block's masks are staged in shared memory and each warp walks them in scan
+// order for its share of the peaks (ballot + popc positions, no block-wide
+// barriers per peak).
 __global__ void __launch_bounds__(kSupThreads)
     support_write_kernel(PointSrc src, int64_t npts, const unsigned long long* __restrict__ masks,
                          const int64_t* __restrict__ offsets, int64_t nblocks, int npeaks,
-                         int64_t* __restrict__ out) {
-  __shared__ int64_t run[64];
-  __shared__ unsigned int warp_cnt[kSupThreads / 32];
+                         int64_t* __restrict__ out, int64_t cap) {
+  __shared__ unsigned long long sm[kSupChunk];
   __shared__ unsigned long long tile_or;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  if (threadIdx.x < npeaks) run[threadIdx.x] = offsets[(int64_t)threadIdx.x * nblocks + blockIdx.x];
   const int64_t base = (int64_t)blockIdx.x * kSupChunk;
-  for (int it = 0; it < kSupItems; ++it) {
-    const int64_t k = base + (int64_t)it * kSupThreads + threadIdx.x;
+  if (threadIdx.x == 0) tile_or = 0ULL;
+  __syncthreads();
+  unsigned long long orv = 0ULL;
+  for (int e = threadIdx.x; e < kSupChunk; e += kSupThreads) {
+    const int64_t k = base + e;
     const unsigned long long m = k < npts ? masks[k] : 0ULL;
-    unsigned long long wor = m;
+    sm[e] = m;
+    orv |= m;
+  }
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) wor |= __shfl_xor_sync(0xffffffffu, wor, off);
-    if (threadIdx.x == 0) tile_or = 0ULL;
-    __syncthreads();
-    if (lane == 0 && wor) atomicOr(&tile_or, wor);
-    __syncthreads();
-    unsigned long long todo = tile_or;
-    __syncthreads();  // everyone has read tile_or before it is reset
-    while (todo) {
-      const int q = __ffsll((long long)todo) - 1;
-      todo &= todo - 1;
-      const bool mine = (m >> q) & 1ULL;
+  for (int off = 16; off > 0; off >>= 1) orv |= __shfl_xor_sync(0xffffffffu, orv, off);
+  if (lane == 0 && orv) atomicOr(&tile_or, orv);
+  __syncthreads();
+  const unsigned long long todo = tile_or;
+  const int64_t nvalid = npts - base < kSupChunk ? npts - base : kSupChunk;
+  for (int q = warp; q < npeaks; q += kSupThreads / 32) {
+    if (!((todo >> q) & 1ULL)) continue;
+    int64_t pos = offsets[(int64_t)q * nblocks + blockIdx.x];
+    for (int e0 = 0; e0 < nvalid; e0 += 32) {
+      const int e = e0 + lane;
+      const bool mine = e < nvalid && ((sm[e] >> q) & 1ULL);
       const unsigned bal = __ballot_sync(0xffffffffu, mine);
-      if (lane == 0) warp_cnt[warp] = __popc(bal);
-      __syncthreads();
-      int64_t pos = run[q];
-      for (int w = 0; w < warp; ++w) pos += warp_cnt[w];
-      pos += __popc(bal & ((1u << lane) - 1u));
-      if (mine) out[pos] = src.id(k);
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        unsigned int tot = 0;
-        for (int w = 0; w < kSupThreads / 32; ++w) tot += warp_cnt[w];
-        run[q] += tot;
-      }
-      __syncthreads();
+      const int64_t at = pos + __popc(bal & ((1u << lane) - 1u));
+      if (mine && at < cap) out[at] = src.id(base + e);  // beyond cap: the host regrows and reruns
+      pos += __popc(bal);
     }
   }
 }
@@ -228,7 +294,7 @@ void hough_vote(const int64_t* d_pix, const double* d_x, const double* d_y, int6
   const int64_t nbins = n_rho * n_theta;
   const size_t smem = (size_t)nbins * sizeof(unsigned int);
   const int use_smem = smem <= 96 * 1024;
-  if (use_smem && smem > 48 * 1024)
+  if (use_smem && smem + kMaxTheta * sizeof(float2) > 40 * 1024)
     cudaFuncSetAttribute(vote_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int64_t blocks = (npts + kVoteThreads - 1) / kVoteThreads;
   if (blocks > (int64_t)sms * 4) blocks = (int64_t)sms * 4;
@@ -243,7 +309,7 @@ int hough_support(const int64_t* d_pix, const double* d_x, const double* d_y, in
                   int64_t width, const double* d_cos, const double* d_sin, const int64_t* d_rbin,
                   int npeaks, double rho_max, double drho, int64_t n_rho,
                   unsigned long long* d_masks, int64_t* d_counts, int64_t* d_offsets, void* temp,
-                  size_t temp_bytes, int64_t* d_out, cudaStream_t stream) {
+                  size_t temp_bytes, int64_t* d_out, int64_t out_cap, cudaStream_t stream) {
   const int64_t nb = support_blocks(npts);
   if (nb == 0 || npeaks == 0) return 0;
   const PointSrc src{d_pix, d_x, d_y, width};
@@ -256,7 +322,7 @@ int hough_support(const int64_t* d_pix, const double* d_x, const double* d_y, in
   if (cub::DeviceScan::ExclusiveSum(temp, bytes, d_counts, d_offsets, m, stream) != cudaSuccess)
     return -1;
   support_write_kernel<<<(unsigned)nb, kSupThreads, 0, stream>>>(src, npts, d_masks, d_offsets,
-                                                                 nb, npeaks, d_out);
+                                                                 nb, npeaks, d_out, out_cap);
   return 0;
 }
 

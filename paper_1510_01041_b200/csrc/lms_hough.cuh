@@ -28,7 +28,7 @@ int hough_support(const int64_t* d_pix, const double* d_x, const double* d_y, in
                   int64_t width, const double* d_cos, const double* d_sin, const int64_t* d_rbin,
                   int npeaks, double rho_max, double drho, int64_t n_rho,
                   unsigned long long* d_masks, int64_t* d_counts, int64_t* d_offsets, void* temp,
-                  size_t temp_bytes, int64_t* d_out, cudaStream_t stream);
+                  size_t temp_bytes, int64_t* d_out, int64_t out_cap, cudaStream_t stream);
 size_t support_scan_temp_bytes(int64_t m);
 
 }  // namespace lmsb
