@@ -40,7 +40,7 @@ def validated(points, q: int | None) -> tuple[np.ndarray, np.ndarray, int]:
     n = x.size
     if n < 3:
         raise DegenerateInputError(f"LMS needs at least 3 points, got {n}")
-    if np.unique(x).size < 2:
+    if not x.min() < x.max():  # fewer than two distinct x (x is finite here)
         raise DegenerateInputError("all points share one x-coordinate; no non-vertical line fits")
     if q is None:
         q = default_coverage(n)
