@@ -10,6 +10,10 @@
  * Each entry point replaces one seam of the reference package
  * (/root/reference/pkg/src/lmsline, cited file:line):
  *
+ *   lms_min_bracelet_materialized_f64
+ *                             minimum_bracelet(..., materialize=True), i.e.
+ *                             _materialized_inputs + _scan_materialized
+ *                             (backend.py:210-231): the two-kernel flow
  *   lms_min_bracelet_f64      SequentialBackend/ParallelBackend.minimum_bracelet
  *                             (backend.py:239-247, 264-289) over a contiguous
  *                             pair-rank range, i.e. _scan_rank_range
@@ -96,6 +100,14 @@ const char* lms_last_error(void);
 int lms_min_bracelet_f64(const double* a, const double* b, int64_t n, int64_t q,
                          int64_t rank_begin, int64_t rank_end, int device, lms_candidate* out);
 
+/* The materialised two-kernel flow over the same rank range (materialize=True,
+ * backend.py:210-231): K1 writes every non-parallel pair's (i, j, u), K2
+ * evaluates every one exactly; no pruning filter.  Same record as
+ * lms_min_bracelet_f64. */
+int lms_min_bracelet_materialized_f64(const double* a, const double* b, int64_t n, int64_t q,
+                                      int64_t rank_begin, int64_t rank_end, int device,
+                                      lms_candidate* out);
+
 /* Batched exact LMS (refine_lms over many Hough peaks, detect.py:134-153 /
  * the per-peak loop of detect.py:184-213): fit f uses points
  * [offsets[f], offsets[f+1]) of x / y with coverage q[f]; out[f] is the
@@ -160,6 +172,10 @@ int lms_ctx_bind_dev(lms_ctx* ctx, const double* d_a, const double* d_b, int64_t
 /* Solve over [rank_begin, rank_end) of the bound lines; blocks until done. */
 int lms_ctx_solve(lms_ctx* ctx, int64_t q, int64_t rank_begin, int64_t rank_end,
                   lms_candidate* out);
+/* Materialised two-kernel solve over the bound lines (see
+ * lms_min_bracelet_materialized_f64). */
+int lms_ctx_solve_materialized(lms_ctx* ctx, int64_t q, int64_t rank_begin, int64_t rank_end,
+                               lms_candidate* out);
 /* Batched solve over the bound lines (see lms_batched_f64). */
 int lms_ctx_solve_batch(lms_ctx* ctx, const int64_t* offsets, const int64_t* q, int64_t nfits,
                         lms_candidate* out);

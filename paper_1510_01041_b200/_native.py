@@ -91,6 +91,9 @@ SIGNATURES = {
     "lms_last_error": (ctypes.c_char_p, []),
     "lms_min_bracelet_f64": (ctypes.c_int, [_D, _D, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                             ctypes.c_int64, ctypes.c_int, _C]),
+    "lms_min_bracelet_materialized_f64": (ctypes.c_int, [_D, _D, ctypes.c_int64, ctypes.c_int64,
+                                                         ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
+                                                         _C]),
     "lms_batched_f64": (ctypes.c_int, [_D, _D, _I, _I, ctypes.c_int64, ctypes.c_int, _C]),
     "lms_primal_brute_f64": (ctypes.c_int, [_D, _D, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, _C]),
     "lms_hough_vote_u8": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
@@ -112,6 +115,8 @@ SIGNATURES = {
                                         ctypes.c_int64]),
     "lms_ctx_solve": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                      _C]),
+    "lms_ctx_solve_materialized": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                                                  ctypes.c_int64, _C]),
     "lms_ctx_solve_batch": (ctypes.c_int, [ctypes.c_void_p, _I, _I, ctypes.c_int64, _C]),
     "lms_ctx_stats": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(Stats)]),
     "lms_ctx_event_record": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
@@ -191,6 +196,18 @@ def min_bracelet(a, b, q: int, rank_begin: int, rank_end: int, device: int = 0) 
     out = Candidate()
     check(lib.lms_min_bracelet_f64(_dp(a), _dp(b), a.size, int(q), int(rank_begin), int(rank_end),
                                    int(device), ctypes.byref(out)))
+    return out
+
+
+def min_bracelet_materialized(a, b, q: int, rank_begin: int, rank_end: int,
+                              device: int = 0) -> Candidate:
+    """lms_min_bracelet_materialized_f64: the two-kernel K1/K2 flow."""
+    lib = _lib_ready()
+    a = _f64(a)
+    b = _f64(b)
+    out = Candidate()
+    check(lib.lms_min_bracelet_materialized_f64(_dp(a), _dp(b), a.size, int(q), int(rank_begin),
+                                                int(rank_end), int(device), ctypes.byref(out)))
     return out
 
 
@@ -332,6 +349,13 @@ class Context:
     def solve(self, q: int, rank_begin: int, rank_end: int) -> Candidate:
         out = Candidate()
         check(self._lib.lms_ctx_solve(self._h, int(q), int(rank_begin), int(rank_end), ctypes.byref(out)))
+        return out
+
+    def solve_materialized(self, q: int, rank_begin: int, rank_end: int) -> Candidate:
+        """The two-kernel K1/K2 flow (materialize=True) over the bound lines."""
+        out = Candidate()
+        check(self._lib.lms_ctx_solve_materialized(self._h, int(q), int(rank_begin), int(rank_end),
+                                                   ctypes.byref(out)))
         return out
 
     def solve_batch(self, offsets, q) -> list:

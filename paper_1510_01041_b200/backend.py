@@ -14,9 +14,12 @@ particular ``"gpu"`` is not a backend, exactly as in the reference
   the worker count), solves them concurrently and merges the partition
   minima with the exact lexicographic key (backend.py:182-187), so the result
   is bit-identical to ``seq`` for any worker or device count.
-* ``materialize=True`` is accepted for API compatibility; the engine streams
-  vertices either way and the result is the same (backend.py:210-231 states
-  the same equivalence for the reference).
+* ``materialize=True`` runs the materialised two-kernel flow of the
+  reference (``_materialized_inputs`` + ``_scan_materialized``,
+  backend.py:210-231; the paper's K1 -> K2): every non-parallel pair becomes
+  an explicit (i, j, u) triple on the device and each one is evaluated
+  exactly, without the pruning stages.  The record is the same as the
+  streaming engine's (the reference states the same equivalence).
 """
 
 from __future__ import annotations
@@ -110,8 +113,11 @@ def merge(best: CandidateRecord | None, cand: CandidateRecord | None) -> Candida
 
 
 def solve_range(a: np.ndarray, b: np.ndarray, q: int, rank_begin: int, rank_end: int,
-                device: int = 0) -> CandidateRecord | None:
+                device: int = 0, materialize: bool = False) -> CandidateRecord | None:
     """Exact minimum over one contiguous rank range on one GPU."""
+    if materialize:
+        return record_from_native(_native.min_bracelet_materialized(a, b, q, rank_begin, rank_end,
+                                                                    device))
     return record_from_native(_native.min_bracelet(a, b, q, rank_begin, rank_end, device))
 
 
@@ -123,7 +129,7 @@ class SequentialBackend:
     def minimum_bracelet(self, a: np.ndarray, b: np.ndarray, q: int, *,
                          materialize: bool = False) -> CandidateRecord | None:
         n = int(a.size)
-        return solve_range(a, b, q, 0, n * (n - 1) // 2, 0)
+        return solve_range(a, b, q, 0, n * (n - 1) // 2, 0, materialize)
 
 
 class ParallelBackend:
@@ -140,9 +146,10 @@ class ParallelBackend:
         plan = BatchPlan.create(a, devices)
         parts = plan.partitions()
         if len(parts) <= 1:
-            return solve_range(a, b, q, *parts[0], 0) if parts else None
+            return solve_range(a, b, q, *parts[0], 0, materialize) if parts else None
         with ThreadPoolExecutor(max_workers=len(parts)) as pool:
-            results = list(pool.map(lambda kp: solve_range(a, b, q, kp[1][0], kp[1][1], kp[0] % devices),
+            results = list(pool.map(lambda kp: solve_range(a, b, q, kp[1][0], kp[1][1], kp[0] % devices,
+                                                           materialize),
                                     enumerate(parts)))
         best: CandidateRecord | None = None
         for rec in results:

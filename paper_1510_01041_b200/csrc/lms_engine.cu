@@ -1037,6 +1037,78 @@ int ctx_solve(lms_ctx* c, int64_t q, int64_t R0, int64_t R1, lms_candidate* out)
   return ctx_solve_fits(c, hf, out);
 }
 
+// The materialised two-kernel flow (_scan_materialized, backend.py:221-231;
+// the paper's K1 -> K2): chunks of 2^22 pair ranks are materialised as
+// explicit (i, j, u) triples (K1) and every triple is evaluated exactly (K2,
+// exact stage in explicit mode with the running best as its bound), then
+// reduced.  No band or count filter: every vertex is counted exactly, so it
+// doubles as an independent cross-check of the pruned search.
+int ctx_solve_materialized(lms_ctx* c, int64_t q, int64_t R0, int64_t R1, lms_candidate* out) {
+  std::memset(out, 0, sizeof(*out));
+  if (!c->a) return set_error(LMS_ERR_INVALID, "no lines bound to the context");
+  const int64_t n = c->nlines;
+  RC_TRY(check_fit(c, 0, n, q));
+  const int64_t total = n * (n - 1) / 2;
+  if (R0 < 0 || R1 > total || R0 > R1)
+    return set_error(LMS_ERR_INVALID, "rank range [%lld, %lld) outside [0, %lld)", (long long)R0,
+                     (long long)R1, (long long)total);
+  CUDA_TRY(cudaSetDevice(c->device));
+  constexpr int64_t kMatChunk = 1 << 22;
+  const int64_t cap = std::min<int64_t>(kMatChunk, std::max<int64_t>(R1 - R0, 1));
+  RC_TRY(c->ii.need(cap));
+  RC_TRY(c->jj.need(cap));
+  RC_TRY(c->uu.need(cap));
+  RC_TRY(c->recs.need(cap));
+  RC_TRY(c->fits.need(1));
+  RC_TRY(c->keys.need(1));
+  RC_TRY(c->best.need(1));
+  RC_TRY(c->counters.need(1));
+  lmsb::FitDesc fd{};
+  fd.n = n;
+  fd.q = q;
+  fd.rank_lo = R0;
+  fd.rank_hi = R1;
+  lms_stats st{};
+  st.n = n;
+  st.pairs = R1 - R0;
+  CUDA_TRY(cudaEventRecord(c->ev_begin, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->fits.p, &fd, sizeof(fd), cudaMemcpyHostToDevice, c->stream));
+  lmsb::launch_reset_best(c->keys.p, c->best.p, 1, c->stream);
+  for (int64_t r = R0; r < R1; r += cap) {
+    const int64_t cnt = std::min<int64_t>(cap, R1 - r);
+    CUDA_TRY(cudaMemsetAsync(c->counters.p, 0, sizeof(unsigned long long), c->stream));
+    lmsb::launch_materialize(c->a, c->b, n, r, cnt, c->ii.p, c->jj.p, c->uu.p, c->counters.p,
+                             c->sms, c->stream);
+    lmsb::ExactArgs ea{};
+    ea.a = c->a;
+    ea.b = c->b;
+    ea.fits = c->fits.p;
+    ea.mode = lmsb::kSrcExplicit;
+    ea.d_count = c->counters.p;
+    ea.capacity = cap;
+    ea.ii = c->ii.p;
+    ea.jj = c->jj.p;
+    ea.uu = c->uu.p;
+    ea.bound = c->best.p;
+    ea.out = c->recs.p;
+    lmsb::launch_exact(ea, persistent_grid(c, -1), c->stream, n);
+    lmsb::launch_reduce(c->recs.p, c->counters.p, 0, cap, c->fits.p, c->keys.p, c->best.p,
+                        (int)c->sms * 4, c->stream);
+    CUDA_TRY(cudaGetLastError());
+    st.launches += 5;
+    st.chunks += 1;
+  }
+  CUDA_TRY(cudaMemcpyAsync(out, c->best.p, sizeof(lms_candidate), cudaMemcpyDeviceToHost,
+                           c->stream));
+  CUDA_TRY(cudaEventRecord(c->ev_end, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  CUDA_TRY(cudaEventElapsedTime(&st.ms_total, c->ev_begin, c->ev_end));
+  st.ms_exact = st.ms_total;
+  st.filtered_vertices = 0;
+  c->stats = st;
+  return LMS_OK;
+}
+
 int ctx_solve_batch(lms_ctx* c, const int64_t* offsets, const int64_t* q, int64_t nfits,
                     lms_candidate* out) {
   if (nfits < 0 || (nfits > 0 && (!offsets || !q))) return set_error(LMS_ERR_INVALID, "bad batch");
@@ -1349,6 +1421,24 @@ int lms_min_bracelet_f64(const double* a, const double* b, int64_t n, int64_t q,
   std::lock_guard<std::mutex> lk(c->mu);
   RC_TRY(ctx_upload(c, a, b, n));
   return ctx_solve(c, q, rank_begin, rank_end, out);
+}
+
+int lms_min_bracelet_materialized_f64(const double* a, const double* b, int64_t n, int64_t q,
+                                      int64_t rank_begin, int64_t rank_end, int device,
+                                      lms_candidate* out) {
+  if (!out) return set_error(LMS_ERR_INVALID, "null output");
+  lms_ctx* c = nullptr;
+  RC_TRY(shared_ctx(device, &c));
+  std::lock_guard<std::mutex> lk(c->mu);
+  RC_TRY(ctx_upload(c, a, b, n));
+  return ctx_solve_materialized(c, q, rank_begin, rank_end, out);
+}
+
+int lms_ctx_solve_materialized(lms_ctx* c, int64_t q, int64_t rank_begin, int64_t rank_end,
+                               lms_candidate* out) {
+  if (!c || !out) return set_error(LMS_ERR_INVALID, "null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  return ctx_solve_materialized(c, q, rank_begin, rank_end, out);
 }
 
 int lms_batched_f64(const double* x, const double* y, const int64_t* offsets, const int64_t* q,

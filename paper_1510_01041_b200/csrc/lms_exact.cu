@@ -354,6 +354,43 @@ __global__ void __launch_bounds__(kCachedThreads, 1) exact_cached_kernel(ExactAr
   }
 }
 
+// K1 of the materialised two-kernel flow (_materialized_inputs,
+// backend.py:210-219; the paper's intersection kernel): every pair of ranks
+// [r0, r0 + count) with a_i != a_j becomes an explicit (i, j, u) triple,
+// u = (b_i - b_j) / (a_i - a_j) unfused; compacted in any order (the
+// lexicographic reduce does not depend on it).
+__global__ void materialize_kernel(const double* __restrict__ a, const double* __restrict__ b,
+                                   int64_t n, int64_t r0, int64_t count, int64_t* __restrict__ ii,
+                                   int64_t* __restrict__ jj, double* __restrict__ uu,
+                                   unsigned long long* __restrict__ nout) {
+  const int lane = threadIdx.x & 31;
+  const int64_t cend = ((count + 31) / 32) * 32;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < cend;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    bool keep = false;
+    int64_t i = 0, j = 0;
+    double u = 0.0;
+    if (t < count) {
+      decode_rank(n, r0 + t, &i, &j);
+      const double da = __dsub_rn(a[i], a[j]);
+      keep = da != 0.0;
+      u = __ddiv_rn(__dsub_rn(b[i], b[j]), da);
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if (m) {
+      unsigned long long base = 0;
+      if (lane == 0) base = atomicAdd(nout, (unsigned long long)__popc(m));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (keep) {
+        const unsigned long long pos = base + __popc(m & ((1u << lane) - 1u));
+        ii[pos] = i;
+        jj[pos] = j;
+        uu[pos] = u;
+      }
+    }
+  }
+}
+
 // 128-bit CAS on a BestKey (atom.global.cas.b128, sm_90+).
 __device__ __forceinline__ BestKey cas_key(BestKey* addr, BestKey expect, BestKey desired) {
   BestKey old;
@@ -494,6 +531,13 @@ void launch_reduce(const lms_candidate* recs, const unsigned long long* d_count,
 void launch_reset_best(BestKey* keys, lms_candidate* best, int64_t nfits, cudaStream_t stream) {
   const int grid = (int)((nfits + 255) / 256);
   reset_best_kernel<<<grid > 0 ? grid : 1, 256, 0, stream>>>(keys, best, nfits);
+}
+
+void launch_materialize(const double* a, const double* b, int64_t n, int64_t r0, int64_t count,
+                        int64_t* ii, int64_t* jj, double* uu, unsigned long long* nout, int sms,
+                        cudaStream_t stream) {
+  if (count <= 0) return;
+  materialize_kernel<<<sms * 8, 256, 0, stream>>>(a, b, n, r0, count, ii, jj, uu, nout);
 }
 
 void launch_gen_seeds(const FitDesc* fits, const int64_t* seed_prefix, int64_t nfits,

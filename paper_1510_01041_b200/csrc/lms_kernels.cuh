@@ -76,6 +76,12 @@ void launch_reduce(const lms_candidate* recs, const unsigned long long* d_count,
                    int grid, cudaStream_t stream);
 void launch_reset_best(BestKey* keys, lms_candidate* best, int64_t nfits, cudaStream_t stream);
 
+// K1 of the materialised flow: explicit (i, j, u) of the non-parallel pairs
+// of ranks [r0, r0 + count), compacted; *nout counts them (zeroed by caller).
+void launch_materialize(const double* a, const double* b, int64_t n, int64_t r0, int64_t count,
+                        int64_t* ii, int64_t* jj, double* uu, unsigned long long* nout, int sms,
+                        cudaStream_t stream);
+
 // Seeds: stratified vertex samples per fit; seed_prefix[f] = first seed of fit f.
 void launch_gen_seeds(const FitDesc* fits, const int64_t* seed_prefix, int64_t nfits,
                       int64_t* ranks, int32_t* fit_of, cudaStream_t stream);

@@ -477,3 +477,47 @@ def test_band_path_degenerate_q_many_ties():
         got = record_from_native(band.solve(q, 0, total))
         want = record_from_native(filt.solve(q, 0, total))
         assert got == want, q
+
+
+def test_materialized_two_kernel_flow_matches():
+    """materialize=True (K1 materialises every (i, j, u), K2 evaluates each
+    exactly, no pruning) gives the streaming engine's record: vs the oracle
+    at small n, vs the band stage on a full n = 8,192 fit."""
+    rng = np.random.default_rng(31)
+    for t in range(6):
+        n = int(rng.integers(20, 400))
+        pts = workloads.config1_points(t, n=n) if t % 2 else workloads.contaminated_line_points(n, t)
+        x, y = pts[:, 0].copy(), pts[:, 1].copy()
+        q = n // 2 + 1
+        got = lms.get_backend("seq").minimum_bracelet(x, y, q, materialize=True)
+        assert record_matches(got, oracle_rec(x, y, q)), t
+    n = 8192
+    pts = workloads.contaminated_line_points(n, 5)
+    a, b = pts[:, 0].copy(), pts[:, 1].copy()
+    q = n // 2 + 1
+    total = n * (n - 1) // 2
+    ctx = _native.Context()
+    ctx.upload(a, b)
+    full = record_from_native(ctx.solve_materialized(q, 0, total))
+    band = record_from_native(ctx.solve(q, 0, total))
+    assert ctx.stats()["bands"] > 0
+    assert full == band
+    fit = lms.solve_lms(pts, materialize=True)
+    assert fit.line.slope == full.u
+
+
+def test_config2_full_fit_matches_unpruned_materialized_flow():
+    """BASELINE config 2 at full size (n = 16,384): the pruned slope-band
+    search returns exactly the record of the unpruned K1/K2 flow, which
+    evaluates all 134,209,536 vertices with the reference's arithmetic."""
+    n = 16384
+    pts = workloads.contaminated_line_points(n, 0)
+    a, b = pts[:, 0].copy(), pts[:, 1].copy()
+    q = n // 2 + 1
+    total = n * (n - 1) // 2
+    ctx = _native.Context()
+    ctx.upload(a, b)
+    band = record_from_native(ctx.solve(q, 0, total))
+    assert ctx.stats()["bands"] > 0
+    full = record_from_native(ctx.solve_materialized(q, 0, total))
+    assert full == band
