@@ -581,12 +581,6 @@ __global__ void __launch_bounds__(kThreads, LMSB_SMALL_MINB) small_fit_kernel(Sm
     }
     __syncthreads();
     const int nruns = sh.nruns;
-    float rlo[kMaxRuns], rhi[kMaxRuns];
-#pragma unroll
-    for (int w = 0; w < kMaxRuns; ++w) {
-      rlo[w] = sh.rlo[w];
-      rhi[w] = sh.rhi[w];
-    }
     const float amf = (float)am;
     // band lookup and padded window counts of queued in-run vertices, lane per
     // vertex; vertices of keyless bands go straight to the fp32 counts
@@ -693,10 +687,9 @@ __global__ void __launch_bounds__(kThreads, LMSB_SMALL_MINB) small_fit_kernel(Sm
                   (num != 0.0 && fabs(num) < 1e-30)) {
                 cand[t] = first;  // beyond the fp32 tests (first sweep only)
               } else {
-                bool inrun = false;
-#pragma unroll
-                for (int w = 0; w < kMaxRuns; ++w)
-                  if (w < nruns) inrun |= (u32 >= rlo[w]) & (u32 <= rhi[w]);
+                bool inrun = false;  // runs from shared memory (broadcast reads)
+#pragma unroll 1
+                for (int w = 0; w < nruns; ++w) inrun |= (u32 >= sh.rlo[w]) & (u32 <= sh.rhi[w]);
                 slot_id[t] = inrun ? 0 : -1;  // band lookup deferred to search()
               }
             }
