@@ -586,7 +586,7 @@ __global__ void __launch_bounds__(kCountThreads) band_count_kernel(
     BandFit bf, const float2* __restrict__ lines, const lms_candidate* __restrict__ best,
     const int64_t* __restrict__ in_ranks, const unsigned long long* __restrict__ in_count,
     int64_t* __restrict__ out_ranks, int32_t* __restrict__ out_fits, int32_t fit,
-    unsigned long long* __restrict__ out_count, int32_t* __restrict__ out_margin) {
+    unsigned long long* __restrict__ out_count) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float2* sl = reinterpret_cast<float2*>(smem_raw);
   const int nst = (int)min(bf.n, (int64_t)kBandMaxN);  // lines staged at once
@@ -599,8 +599,15 @@ __global__ void __launch_bounds__(kCountThreads) band_count_kernel(
   const int q = (int)bf.q;
   if ((int64_t)blockIdx.x * 32 >= total) return;
   const bool resident = n <= nst;
-  if (resident)
-    for (int k = tid; k < n; k += kCountThreads) sl[k] = lines[k];
+  if (resident) {
+    // TMA bulk copy of the whole line set (8 n bytes; an odd last line by hand)
+    __shared__ __align__(8) uint64_t bar;
+    if (tid == 0) mbar_init(&bar, 1);
+    __syncthreads();
+    const uint32_t bytes = (uint32_t)(n & ~1) * (uint32_t)sizeof(float2);
+    if (bytes) bulk_stage(sl, lines, bytes, &bar, 0);
+    if ((n & 1) && tid == 0) sl[n - 1] = lines[n - 1];
+  }
   double H = INFINITY;
   {
     const lms_candidate b0 = *best;
@@ -666,8 +673,6 @@ __global__ void __launch_bounds__(kCountThreads) band_count_kernel(
           const unsigned slot = __popc(mask & ((1u << lane) - 1u));
           out_ranks[base + slot] = rank;
           out_fits[base + slot] = fit;
-          // lines inside the better window beyond q: more means a lower height
-          if (out_margin) out_margin[base + slot] = force ? 0x7fffffff : max(tu, td) - q;
         }
       }
     }
@@ -1069,27 +1074,9 @@ void launch_band_count(const BandFit& bf, const BandCount& bc, int sms, cudaStre
   set_smem(band_count_kernel, (size_t)kBandMaxN * sizeof(float2) + 64 * sizeof(unsigned), &done);
   band_count_kernel<<<sms, kCountThreads, smem, st>>>(bf, bc.lines, bc.best, bc.in_ranks,
                                                       bc.in_count, bc.out_ranks, bc.out_fits,
-                                                      bc.fit, bc.out_count, bc.out_margin);
+                                                      bc.fit, bc.out_count);
 }
 
-size_t band_order_temp_bytes(int64_t m) {
-  size_t bytes = 0;
-  cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, (const int32_t*)nullptr,
-                                            (int32_t*)nullptr, (const int64_t*)nullptr,
-                                            (int64_t*)nullptr, (int)m);
-  return bytes;
-}
-
-int launch_band_order(const int32_t* margin_in, int32_t* margin_out, const int64_t* ranks_in,
-                      int64_t* ranks_out, int64_t m, void* temp, size_t temp_bytes,
-                      cudaStream_t st) {
-  if (m <= 0) return 0;
-  size_t bytes = temp_bytes;
-  return cub::DeviceRadixSort::SortPairsDescending(temp, bytes, margin_in, margin_out, ranks_in,
-                                                   ranks_out, (int)m, 0, 32, st) == cudaSuccess
-             ? 0
-             : -1;
-}
 
 int launch_band_group(const BandWork& w, int64_t m, cudaStream_t st) {
   cudaMemsetAsync(w.start, 0, sizeof(int64_t) * (w.K + 1), st);

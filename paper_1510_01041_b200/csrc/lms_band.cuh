@@ -88,7 +88,6 @@ struct BandCount {
   int32_t* out_fits;
   int32_t fit;
   unsigned long long* out_count;
-  int32_t* out_margin;  // optional: max(window counts) - q per survivor
   bool make_lines;      // fill `lines` first
 };
 
@@ -109,11 +108,6 @@ void launch_band_filter_big(const BandFit& bf, const BandArgs& ba, const float* 
                             cudaStream_t st);
 
 size_t band_sample_temp_bytes(int64_t S);
-size_t band_order_temp_bytes(int64_t m);
-// survivors by descending margin (CUB radix sort)
-int launch_band_order(const int32_t* margin_in, int32_t* margin_out, const int64_t* ranks_in,
-                      int64_t* ranks_out, int64_t m, void* temp, size_t temp_bytes,
-                      cudaStream_t st);
 size_t band_group_temp_bytes(int64_t m);
 size_t band_collect_smem(int K);
 int launch_band_sample(const BandFit& bf, const BandWork& w, int sms, cudaStream_t st);

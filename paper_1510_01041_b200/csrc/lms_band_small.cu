@@ -65,7 +65,8 @@ template <int kItems>
 struct SmallShared {
   static constexpr int kNP = 32 * kItems;  // padded lines (one warp sorts a band)
   using SampleSort = cub::BlockRadixSort<float, kThreads, kSampleItems, int>;
-  double a[kNP], b[kNP];
+  alignas(16) double a[kNP];
+  alignas(16) double b[kNP];
   float4 l2[kNP / 2];         // (A_k, A_k+1, -B_k, -B_k+1) for the packed counts
   float rlo[kMaxRuns], rhi[kMaxRuns];  // slope runs of the current sweep (widened)
   int nruns;
@@ -102,6 +103,7 @@ struct SmallShared {
   lms_candidate wbest[kWarps];
   double red[2][kWarps];
   unsigned long long hbits;  // current bound H (bits of a non-negative double)
+  uint64_t bar;              // mbarrier of the line bulk copies
   int nvalid;
   unsigned long long cnt[12];  // admitted bands, queued, exact, sweeps; phase cycles (stats)
 };
@@ -237,10 +239,26 @@ __global__ void __launch_bounds__(kThreads, LMSB_SMALL_MINB) small_fit_kernel(Sm
 
   // ---- lines, centre, magnitudes
   double alo = INFINITY, ahi = -INFINITY, am = 0.0, bm = 0.0;
+  // the fit's lines: TMA bulk copies when 16-byte aligned (even n, aligned
+  // offset), element loads otherwise
+  const bool bulk = ((reinterpret_cast<uintptr_t>(ga) | reinterpret_cast<uintptr_t>(gb)) & 15) == 0 &&
+                    (n & 1) == 0;
+  if (bulk) {
+    if (tid == 0) mbar_init(&sh.bar, 1);
+    __syncthreads();
+    if (tid == 0) {
+      mbar_expect_tx(&sh.bar, 2u * 8u * (uint32_t)n);
+      bulk_g2s(sh.a, ga, 8u * (uint32_t)n, &sh.bar);
+      bulk_g2s(sh.b, gb, 8u * (uint32_t)n, &sh.bar);
+    }
+    mbar_wait(&sh.bar, 0);
+  }
   for (int k = tid; k < n; k += kThreads) {
-    const double ak = ga[k], bk = gb[k];
-    sh.a[k] = ak;
-    sh.b[k] = bk;
+    const double ak = bulk ? sh.a[k] : ga[k], bk = bulk ? sh.b[k] : gb[k];
+    if (!bulk) {
+      sh.a[k] = ak;
+      sh.b[k] = bk;
+    }
     alo = fmin(alo, ak);
     ahi = fmax(ahi, ak);
     am = fmax(am, fabs(ak));

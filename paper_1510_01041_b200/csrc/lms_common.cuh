@@ -105,4 +105,56 @@ __device__ __forceinline__ lms_candidate warp_min_cand(lms_candidate c) {
   return c;
 }
 
+// ---------------------------------------------------------------- bulk copy
+// 1-D TMA bulk copies global -> shared (cp.async.bulk, completion counted on
+// an mbarrier in transaction bytes).  Sizes and both addresses must be
+// multiples of 16 bytes.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+// One thread stages `bytes` (multiple of 16, both pointers 16-byte aligned)
+// into shared memory with bulk copies of <= 64 KB; every thread of the CTA
+// then waits for the transaction count.  `bar` must be initialised (count 1)
+// and visible to the CTA; `phase` alternates per use.
+__device__ __forceinline__ void bulk_stage(void* dst, const void* src, uint32_t bytes,
+                                           uint64_t* bar, uint32_t phase) {
+  if (threadIdx.x == 0) {
+    mbar_expect_tx(bar, bytes);
+    for (uint32_t off = 0; off < bytes; off += 65536u) {
+      const uint32_t len = bytes - off < 65536u ? bytes - off : 65536u;
+      bulk_g2s(static_cast<char*>(dst) + off, static_cast<const char*>(src) + off, len, bar);
+    }
+  }
+  mbar_wait(bar, phase);
+}
+
 }  // namespace lmsb

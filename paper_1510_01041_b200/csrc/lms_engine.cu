@@ -168,7 +168,7 @@ struct lms_ctx {
   DevBuf<float> bedge;
   DevBuf<int32_t> blist;
   DevBuf<int64_t> branks2;
-  DevBuf<int32_t> bfits2, bmargin;
+  DevBuf<int32_t> bfits2;
   DevBuf<int64_t> bchunks;
   DevBuf<float> bbig_keys, bbig_store;
   DevBuf<int64_t> bbig_seg;
@@ -283,7 +283,6 @@ void ctx_release(lms_ctx* c) {
   c->blist.release();
   c->branks2.release();
   c->bfits2.release();
-  c->bmargin.release();
   c->bchunks.release();
   c->bbig_keys.release();
   c->bbig_store.release();
@@ -660,9 +659,8 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   RC_TRY(c->ranks.need(scap));
   RC_TRY(c->item_fit.need(scap));
   RC_TRY(c->recs.need(scap));
-  RC_TRY(c->branks2.need(2 * scap));
+  RC_TRY(c->branks2.need(scap));
   RC_TRY(c->bfits2.need(scap));
-  RC_TRY(c->bmargin.need(2 * scap));
   RC_TRY(c->blines32.need(h.n));
   RC_TRY(c->bchunks.need((int64_t)list.size() + 1));
   ba.members = c->bmem.p;
@@ -687,7 +685,6 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     bc.out_fits = c->bfits2.p;
     bc.fit = 0;
     bc.out_count = sc + 4;
-    bc.out_margin = nullptr;
     bc.make_lines = true;
     lmsb::launch_band_count(bf, bc, c->sms, c->stream);
     CUDA_TRY(cudaGetLastError());
