@@ -521,3 +521,52 @@ def test_config2_full_fit_matches_unpruned_materialized_flow():
     assert ctx.stats()["bands"] > 0
     full = record_from_native(ctx.solve_materialized(q, 0, total))
     assert full == band
+
+
+@pytest.mark.parametrize("scale", [(1e-8, 1e8), (1e12, 1.0), (1.0, 1e-12), (3e5, 3e5)])
+def test_band_and_filter_paths_vs_unpruned_at_extreme_scales(scale):
+    """The fp32 pre-tests of both pruned searches carry magnitude-scaled
+    margins: at extreme coordinate scales they still return the record of
+    the unpruned K1/K2 flow (exact arithmetic only)."""
+    sx, sy = scale
+    rng = np.random.default_rng(int(np.log10(sx * sy + 1e-300) + 400))
+    n = 2500
+    pts = workloads.contaminated_line_points(n, 3)
+    x = (pts[:, 0] + rng.uniform(0, 1e-3, n)) * sx
+    y = pts[:, 1] * sy
+    q = n // 2 + 1
+    total = n * (n - 1) // 2
+    ref = _native.Context()
+    ref.upload(x, y)
+    want = record_from_native(ref.solve_materialized(q, 0, total))
+    for env in ({"LMSB_BAND": "2"}, {"LMSB_BAND": "0"}):
+        ctx = _ctx_with(env)
+        ctx.upload(x, y)
+        got = record_from_native(ctx.solve(q, 0, total))
+        assert got == want, (scale, env)
+
+
+def test_small_fit_kernel_vs_unpruned_at_extreme_scales():
+    """Fused small-fit kernel at extreme coordinate scales (and odd n, which
+    takes the element-load path instead of the bulk copy) against the
+    unpruned K1/K2 flow of every fit."""
+    rng = np.random.default_rng(8)
+    sets = []
+    for k, (sx, sy) in enumerate([(1e-8, 1e8), (1e12, 1.0), (1.0, 1e-12), (3e5, 3e5)] * 6):
+        n = int(rng.choice([257, 300, 511, 512, 999]))
+        pts = workloads.bench_points(n, seed=100 + k)
+        sets.append(np.column_stack([(pts[:, 0] + rng.uniform(0, 1e-3, n)) * sx, pts[:, 1] * sy]))
+    X = np.concatenate([s[:, 0] for s in sets])
+    Y = np.concatenate([s[:, 1] for s in sets])
+    offs = np.concatenate([[0], np.cumsum([len(s) for s in sets])]).astype(np.int64)
+    q = np.asarray([len(s) // 2 + 1 for s in sets], dtype=np.int64)
+    ctx = _ctx_with({"LMSB_SMALL": "1"})
+    ctx.upload(X, Y)
+    got = ctx.solve_batch(offs, q)
+    assert ctx.stats()["small_fits"] == len(sets)
+    ref = _native.Context()
+    for f, s in enumerate(sets):
+        ref.upload(s[:, 0], s[:, 1])
+        m = len(s)
+        want = record_from_native(ref.solve_materialized(int(q[f]), 0, m * (m - 1) // 2))
+        assert record_from_native(got[f]) == want, f
