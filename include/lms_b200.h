@@ -86,6 +86,7 @@ typedef struct lms_stats {
   double seed_height;       /* the bound H the band stage collected with */
   int64_t band_survivors;   /* collected vertices whose band window counts reached q */
   int64_t small_fits;       /* fits of the batch solved by the fused per-fit band kernel */
+  int64_t direct_groups;    /* sub-band regions of the direct grouping (0: radix-sort path) */
 } lms_stats;
 
 /* Library identity and device discovery. */

@@ -71,6 +71,7 @@ class Stats(ctypes.Structure):
         ("seed_height", ctypes.c_double),
         ("band_survivors", ctypes.c_int64),
         ("small_fits", ctypes.c_int64),
+        ("direct_groups", ctypes.c_int64),
     ]
 
     def as_dict(self) -> dict:

@@ -296,9 +296,10 @@ __global__ void __launch_bounds__(kThreads, 1) band_filter_kernel(BandFit bf, Ba
     if (ba.chunk_prefix[mid] <= cidx) lo = mid;
     else hi = mid - 1;
   }
-  const int band = ba.list[lo];
-  const int64_t m0 = ba.start[band] + (cidx - ba.chunk_prefix[lo]) * ba.chunk;
-  const int64_t m1 = min(ba.end[band], m0 + ba.chunk);
+  const int grp = ba.list[lo];
+  const int band = ba.group_band ? ba.group_band[grp] : grp;
+  const int64_t m0 = ba.start[grp] + (cidx - ba.chunk_prefix[lo]) * ba.chunk;
+  const int64_t m1 = min(ba.end[grp], m0 + ba.chunk);
   if (m1 <= m0) return;
   double H = INFINITY;
   {
@@ -727,6 +728,157 @@ __global__ void __launch_bounds__(1024) band_edge_seed_kernel(BandFit bf, BandAr
   }
 }
 
+// ---------------------------------------------------------- direct grouping
+// Instead of appending (band, slope position, pair) and radix-sorting, the
+// collect pass can write every collected vertex straight into a region of
+// its sub-band: each admitted band is split into S_e sub-bands at quantiles
+// of its sampled slopes (band_subbounds_kernel), each sub-band gets a region
+// sized from the sample counts, and a vertex lands in its sub-band's region
+// (atomic cursor).  A region overflow is reported; the host then falls back
+// to the sorting path.  Sub-bands are narrow slope ranges, so they serve as
+// the filter's chunks directly.
+
+// inner sub-band boundaries of admitted band entry e: S_e - 1 quantiles of its
+// samples, stored from sub[sb_first[e] - e]
+__global__ void band_subbounds_kernel(const float* __restrict__ sorted,
+                                      const unsigned long long* __restrict__ nvalid,
+                                      const float* __restrict__ bounds, int K,
+                                      const int32_t* __restrict__ list,
+                                      const int32_t* __restrict__ sb_first, int nadm,
+                                      float* __restrict__ sub) {
+  const int e = blockIdx.x;
+  if (e >= nadm) return;
+  const int k = list[e];
+  const int S = sb_first[e + 1] - sb_first[e];
+  if (S <= 1 || k >= K) return;
+  const int sv = (int)*nvalid;
+  auto lower = [&](float x) {
+    int a = 0, b = sv;
+    while (a < b) {
+      const int mid = (a + b) >> 1;
+      if (sorted[mid] < x) a = mid + 1;
+      else b = mid;
+    }
+    return a;
+  };
+  const int lo = k > 0 ? lower(bounds[k - 1]) : 0;
+  const int hi = k < K - 1 ? lower(bounds[k]) : sv;
+  for (int t = threadIdx.x + 1; t < S; t += blockDim.x)
+    sub[sb_first[e] - e + t - 1] = hi > lo ? sorted[lo + ((int64_t)t * (hi - lo)) / S] : INFINITY;
+}
+
+template <int kR>
+__global__ void __launch_bounds__(kCollectThreads) band_collect_direct_kernel(
+    BandFit bf, const float* __restrict__ bounds, int K, BandRuns runs, BandDirect dg) {
+  float rlo[kR], rhi[kR];
+#pragma unroll
+  for (int k = 0; k < kR; ++k) {
+    rlo[k] = runs.lo[k];
+    rhi[k] = runs.hi[k];
+  }
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int kWarps = kCollectThreads / 32;
+  uint32_t* queue = reinterpret_cast<uint32_t*>(smem_raw);  // [kWarps][64]
+  float* bnd = reinterpret_cast<float*>(queue + kWarps * 64);
+  float* sub = bnd + K;
+  int32_t* sbf = reinterpret_cast<int32_t*>(sub + dg.nsub);
+  int16_t* slot = reinterpret_cast<int16_t*>(sbf + dg.nadm + 1);
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+    if (k < K - 1) bnd[k] = bounds[k];
+    slot[k] = dg.slot[k];
+  }
+  for (int t = threadIdx.x; t < dg.nsub; t += blockDim.x) sub[t] = dg.sub[t];
+  for (int t = threadIdx.x; t <= dg.nadm; t += blockDim.x) sbf[t] = dg.sb_first[t];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  uint32_t* q = queue + (threadIdx.x >> 5) * 64;
+  int qn = 0;
+  const int n = (int)bf.n;
+  const int64_t seg = 32 * kRun;
+  const int64_t nseg = (bf.span + seg - 1) / seg;
+  const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+
+  auto drain = [&](int cnt) {
+    int g = -1;
+    uint32_t val = 0;
+    if (lane < cnt) {
+      val = q[lane];
+      const int i = val >> 16, j = val & 0xFFFF;
+      double u = 0.0;
+      const int cls = classify(bf, __ldg(bf.a + i), __ldg(bf.b + i), __ldg(bf.a + j),
+                               __ldg(bf.b + j), &u);
+      if (cls == 1) {
+        const float bk = band_key(u);
+        const int e = slot[band_of(bnd, K - 1, bk)];
+        if (e >= 0) {
+          const int f0 = sbf[e], S = sbf[e + 1] - f0;
+          g = f0 + (S > 1 ? band_of(sub + f0 - e, S - 1, bk) : 0);
+        }
+      } else if (cls == 2) {
+        g = dg.force_group;
+      }
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, g);
+    const int leader = __ffs(peers) - 1;
+    unsigned long long b0 = 0;
+    if (g >= 0 && lane == leader) b0 = atomicAdd(dg.cursor + g, (unsigned long long)__popc(peers));
+    b0 = __shfl_sync(0xffffffffu, b0, leader);
+    if (g >= 0) {
+      const unsigned long long pos = b0 + __popc(peers & ((1u << lane) - 1u));
+      if ((int64_t)pos < dg.cap[g]) dg.members[dg.rstart[g] + pos] = val;
+    }
+  };
+
+  for (int64_t gi = warp0; gi < nseg; gi += nwarps) {
+    const int64_t base = gi * seg;
+    int i0 = 0, j0 = 0;
+    if (lane == 0) {
+      int64_t i64, j64;
+      decode_rank(bf.n, bf.R0 + base, &i64, &j64);
+      i0 = (int)i64;
+      j0 = (int)j64;
+    }
+    int i = __shfl_sync(0xffffffffu, i0, 0);
+    int j = __shfl_sync(0xffffffffu, j0, 0);
+    advance_pair(n, lane, i, j);
+    double ai = __ldg(bf.a + i), bi = __ldg(bf.b + i);
+    int64_t r = base + lane;
+#pragma unroll 1
+    for (int e = 0; e < kRun; ++e, r += 32) {
+      bool cand = false;
+      if (r < bf.span) {
+        const double da = __dsub_rn(ai, __ldg(bf.a + j));
+        const double num = __dsub_rn(bi, __ldg(bf.b + j));
+        if (da != 0.0) {
+          const float u32 = __fdividef((float)num, (float)da);
+          cand = !(fabsf(u32) <= FLT_MAX) || fabs(da) < 1e-30 || (num != 0.0 && fabs(num) < 1e-30);
+#pragma unroll
+          for (int k = 0; k < kR; ++k) cand |= (u32 >= rlo[k]) & (u32 <= rhi[k]);
+        }
+      }
+      const unsigned cm = __ballot_sync(0xffffffffu, cand);
+      if (cand) q[qn + __popc(cm & ((1u << lane) - 1u))] = ((uint32_t)i << 16) | (uint32_t)j;
+      qn += __popc(cm);
+      __syncwarp();
+      if (qn >= 32) {
+        drain(32);
+        __syncwarp();
+        if (lane < qn - 32) q[lane] = q[32 + lane];
+        __syncwarp();
+        qn -= 32;
+      }
+      const int i_old = i;
+      advance_pair(n, 32, i, j);
+      if (i != i_old) {
+        ai = __ldg(bf.a + i);
+        bi = __ldg(bf.b + i);
+      }
+    }
+  }
+  if (qn > 0) drain(qn);
+}
+
 __global__ void band_runs_kernel(const uint32_t* __restrict__ keys, int64_t m,
                                  int64_t* __restrict__ start, int64_t* __restrict__ end) {
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < m;
@@ -823,9 +975,10 @@ __global__ void __launch_bounds__(kBigThreads, 1) band_filter_big_kernel(BandFit
     if (ba.chunk_prefix[mid] <= cidx) lo = mid;
     else hi = mid - 1;
   }
-  const int band = ba.list[lo];
-  const int64_t m0 = ba.start[band] + (cidx - ba.chunk_prefix[lo]) * ba.chunk;
-  const int64_t m1 = min(ba.end[band], m0 + ba.chunk);
+  const int grp = ba.list[lo];
+  const int band = ba.group_band ? ba.group_band[grp] : grp;
+  const int64_t m0 = ba.start[grp] + (cidx - ba.chunk_prefix[lo]) * ba.chunk;
+  const int64_t m1 = min(ba.end[grp], m0 + ba.chunk);
   if (m1 <= m0) return;
   double H = INFINITY;
   {
@@ -1077,6 +1230,40 @@ void launch_band_count(const BandFit& bf, const BandCount& bc, int sms, cudaStre
                                                       bc.fit, bc.out_count);
 }
 
+
+size_t band_direct_smem(int K, int nsub, int nadm) {
+  return (size_t)(kCollectThreads / 32) * 64 * sizeof(uint32_t) + (size_t)K * sizeof(float) +
+         (size_t)nsub * sizeof(float) + (size_t)(nadm + 1) * sizeof(int32_t) +
+         (size_t)K * sizeof(int16_t) + 16;
+}
+
+void launch_band_collect_direct(const BandFit& bf, const BandWork& w, const BandRuns& runs,
+                                const BandDirect& dg, int sms, cudaStream_t st) {
+  band_subbounds_kernel<<<std::max(dg.nadm, 1), 128, 0, st>>>(w.sample_sorted, w.nvalid, w.bounds,
+                                                              w.K, dg.list, dg.sb_first, dg.nadm,
+                                                              dg.sub);
+  const size_t smem = band_direct_smem(w.K, dg.nsub, dg.nadm);
+  switch (runs.count) {
+#define LMSB_DIRECT(R)                                                                        \
+  case R: {                                                                                   \
+    cudaFuncSetAttribute(band_collect_direct_kernel<R>,                                       \
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);             \
+    band_collect_direct_kernel<R><<<sms * 4, kCollectThreads, smem, st>>>(bf, w.bounds, w.K,  \
+                                                                          runs, dg);          \
+    break;                                                                                    \
+  }
+    LMSB_DIRECT(1)
+    LMSB_DIRECT(2)
+    LMSB_DIRECT(3)
+    LMSB_DIRECT(4)
+    LMSB_DIRECT(5)
+    LMSB_DIRECT(6)
+    LMSB_DIRECT(7)
+    default:
+    LMSB_DIRECT(8)
+#undef LMSB_DIRECT
+  }
+}
 
 int launch_band_group(const BandWork& w, int64_t m, cudaStream_t st) {
   cudaMemsetAsync(w.start, 0, sizeof(int64_t) * (w.K + 1), st);

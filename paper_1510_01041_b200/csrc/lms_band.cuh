@@ -58,13 +58,29 @@ struct BandRuns {
   float lo[kMaxRuns], hi[kMaxRuns];
 };
 
+// Direct grouping of the collected vertices into sub-band regions.
+struct BandDirect {
+  int nadm;                   // admitted band entries
+  const int32_t* list;        // nadm: their bands
+  const int32_t* sb_first;    // nadm + 1: first sub-band of each entry
+  int nsub;                   // inner sub-boundaries (sum of S_e - 1)
+  float* sub;                 // nsub, filled by the collect launcher
+  const int16_t* slot;        // K: admitted entry of a band, or -1
+  int force_group;            // sub-band id of the beyond-range vertices
+  unsigned long long* cursor; // groups: members written (may exceed cap)
+  const int64_t* cap;         // groups: region capacity
+  const int64_t* rstart;      // groups: region start in members
+  uint32_t* members;
+};
+
 struct BandArgs {
   int K;
   const float* bounds;
   const int64_t* start;
   const int64_t* end;
   const uint32_t* members;
-  const int32_t* list;        // filter: bands to process
+  const int32_t* list;        // filter: groups to process (bands, or sub-bands with group_band)
+  const int32_t* group_band;  // optional: band of every group
   int nlist;
   int64_t chunk;              // filter: members per CTA
   int64_t* chunk_prefix;      // nlist + 1 scratch: first chunk of every listed band
@@ -122,6 +138,9 @@ void launch_band_seeds(const BandFit& bf, const BandWork& w, int64_t* ranks, int
 void launch_band_collect(const BandFit& bf, const BandWork& w, const BandRuns& runs, int64_t cap,
                          int sms, cudaStream_t st);
 int launch_band_group(const BandWork& w, int64_t m, cudaStream_t st);
+size_t band_direct_smem(int K, int nsub, int nadm);
+void launch_band_collect_direct(const BandFit& bf, const BandWork& w, const BandRuns& runs,
+                                const BandDirect& dg, int sms, cudaStream_t st);
 void launch_band_count(const BandFit& bf, const BandCount& bc, int sms, cudaStream_t st);
 
 }  // namespace lmsb

@@ -172,7 +172,15 @@ struct lms_ctx {
   DevBuf<int64_t> bchunks;
   DevBuf<float> bbig_keys, bbig_store;
   DevBuf<int64_t> bbig_seg;
-  DevBuf<int32_t> small_list;
+  DevBuf<int32_t> small_list, dg_i32;
+  DevBuf<int64_t> dg_i64;
+  DevBuf<unsigned long long> dg_cursor;
+  DevBuf<float> dg_sub;
+  DevBuf<int16_t> dg_slot;
+  // LMSB_BAND_DIRECT=1: collect straight into sub-band regions (no radix sort);
+  // slower on config 2 (sub-bands are wider than slope-sorted chunks), kept
+  // for A/B runs
+  int band_direct = 0;
   DevBuf<unsigned long long> small_cnt;
   int small_mode = 1;  // LMSB_SMALL: 0 off, 1 batches, 2 also single fits
   DevBuf<float2> blines32;
@@ -198,6 +206,8 @@ int ctx_init(lms_ctx* c, int device) {
   c->band_mode = bm ? std::max(0, std::min(2, atoi(bm))) : 1;
   const char* bv = getenv("LMSB_BAND_VERTICES");
   if (bv && atoll(bv) >= 256) c->band_vertices = atoll(bv);
+  const char* bd = getenv("LMSB_BAND_DIRECT");
+  c->band_direct = (bd && std::strcmp(bd, "1") == 0) ? 1 : 0;
   const char* bmul = getenv("LMSB_BIG_MULT");
   if (bmul && atoll(bmul) >= 1) c->big_mult = atoll(bmul);
   const char* sm = getenv("LMSB_SMALL");
@@ -288,6 +298,11 @@ void ctx_release(lms_ctx* c) {
   c->bbig_store.release();
   c->bbig_seg.release();
   c->small_list.release();
+  c->dg_i32.release();
+  c->dg_i64.release();
+  c->dg_cursor.release();
+  c->dg_sub.release();
+  c->dg_slot.release();
   c->small_cnt.release();
   c->blines32.release();
   if (c->h_best) cudaFreeHost(c->h_best);
@@ -623,6 +638,127 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   }
   CUDA_TRY(cudaEventRecord(c->ev_chunk[2], c->stream));
   unsigned long long m = 0;
+  // direct grouping into sub-band regions (falls back to the sorting path on a
+  // region overflow)
+  bool direct = false;
+  int ngroups = 0;
+  std::vector<int64_t> gstart, gend;
+  if (c->band_direct) {
+    const int nadm = (int)list.size() - 1;  // the last entry is the beyond-range pseudo band
+    std::vector<int32_t> sbf(nadm + 1, 0);
+    std::vector<int64_t> gcap;
+    std::vector<int32_t> gband;
+    std::vector<int16_t> slot(K, -1);
+    const double per_sample = (double)span / (double)S;
+    for (int e = 0; e < nadm; ++e) {
+      const int32_t k = list[e];
+      slot[k] = (int16_t)e;
+      const double est = (double)scnt[k] * per_sample;
+      int Se = (int)std::ceil(est / (double)c->band_chunk);
+      Se = std::max(1, std::min({Se, 64, (int)(scnt[k] / 4)}));
+      sbf[e + 1] = sbf[e] + Se;
+      // sub-band quantiles rest on ~16-32 samples each: room for 4x the mean
+      const int64_t cap_g = (int64_t)std::min(est + 1.0, 4.0 * est / Se) + 4096;
+      for (int t = 0; t < Se; ++t) {
+        gcap.push_back(cap_g);
+        gband.push_back(k);
+      }
+    }
+    const int G = sbf[nadm];
+    gcap.push_back(65536);  // beyond-range vertices
+    gband.push_back(K);
+    ngroups = G + 1;
+    std::vector<int64_t> rstart(ngroups + 1, 0);
+    for (int g = 0; g < ngroups; ++g) rstart[g + 1] = rstart[g] + gcap[g];
+    const int64_t total_cap = rstart[ngroups];
+    const int nsub = G - nadm;
+    if (nadm < 32767 && total_cap < ((int64_t)1 << 31) &&
+        lmsb::band_direct_smem(K, nsub, nadm) <= 200 * 1024) {
+      RC_TRY(c->bmem.need(total_cap));
+      RC_TRY(c->dg_i32.need((int64_t)(nadm + 1) + 2 * (int64_t)ngroups + 1));
+      RC_TRY(c->dg_i64.need(2 * (int64_t)ngroups + 2));
+      RC_TRY(c->dg_cursor.need(ngroups));
+      RC_TRY(c->dg_sub.need(std::max(nsub, 1)));
+      RC_TRY(c->dg_slot.need(K));
+      RC_TRY(c->bstart.need(std::max<int64_t>(ngroups, K + 1)));
+      RC_TRY(c->bend.need(std::max<int64_t>(ngroups, K + 1)));
+      w.start = c->bstart.p;
+      w.end = c->bend.p;
+      ba.start = c->bstart.p;
+      ba.end = c->bend.p;
+      int32_t* d_list = c->blist.p;  // list[0..nadm) already uploaded
+      int32_t* d_sbf = c->dg_i32.p;
+      int32_t* d_gband = d_sbf + (nadm + 1);
+      int32_t* d_glist = d_gband + ngroups;
+      int64_t* d_cap = c->dg_i64.p;
+      int64_t* d_rstart = d_cap + ngroups;
+      std::vector<int32_t> glist(ngroups);
+      for (int g = 0; g < ngroups; ++g) glist[g] = g;
+      CUDA_TRY(cudaMemcpyAsync(d_sbf, sbf.data(), sizeof(int32_t) * (nadm + 1),
+                               cudaMemcpyHostToDevice, c->stream));
+      CUDA_TRY(cudaMemcpyAsync(d_gband, gband.data(), sizeof(int32_t) * ngroups,
+                               cudaMemcpyHostToDevice, c->stream));
+      CUDA_TRY(cudaMemcpyAsync(d_glist, glist.data(), sizeof(int32_t) * ngroups,
+                               cudaMemcpyHostToDevice, c->stream));
+      CUDA_TRY(cudaMemcpyAsync(d_cap, gcap.data(), sizeof(int64_t) * ngroups,
+                               cudaMemcpyHostToDevice, c->stream));
+      CUDA_TRY(cudaMemcpyAsync(d_rstart, rstart.data(), sizeof(int64_t) * ngroups,
+                               cudaMemcpyHostToDevice, c->stream));
+      CUDA_TRY(cudaMemcpyAsync(c->dg_slot.p, slot.data(), sizeof(int16_t) * K,
+                               cudaMemcpyHostToDevice, c->stream));
+      CUDA_TRY(cudaMemsetAsync(c->dg_cursor.p, 0, sizeof(unsigned long long) * ngroups, c->stream));
+      lmsb::BandDirect dg{};
+      dg.nadm = nadm;
+      dg.list = d_list;
+      dg.sb_first = d_sbf;
+      dg.nsub = nsub;
+      dg.sub = c->dg_sub.p;
+      dg.slot = c->dg_slot.p;
+      dg.force_group = G;
+      dg.cursor = c->dg_cursor.p;
+      dg.cap = d_cap;
+      dg.rstart = d_rstart;
+      dg.members = c->bmem.p;
+      CUDA_TRY(cudaEventRecord(c->ev_chunk[5], c->stream));
+      lmsb::launch_band_collect_direct(bf, w, runs, dg, c->sms, c->stream);
+      CUDA_TRY(cudaEventRecord(c->ev_chunk[6], c->stream));
+      CUDA_TRY(cudaGetLastError());
+      st->launches += 2;
+      std::vector<unsigned long long> cur(ngroups);
+      CUDA_TRY(cudaMemcpyAsync(cur.data(), c->dg_cursor.p, sizeof(unsigned long long) * ngroups,
+                               cudaMemcpyDeviceToHost, c->stream));
+      CUDA_TRY(cudaStreamSynchronize(c->stream));
+      bool overflow = false;
+      gstart.assign(ngroups, 0);
+      gend.assign(ngroups, 0);
+      for (int g = 0; g < ngroups; ++g) {
+        overflow |= (int64_t)cur[g] > gcap[g];
+        m += cur[g];
+        gstart[g] = rstart[g];
+        gend[g] = rstart[g] + std::min<int64_t>((int64_t)cur[g], gcap[g]);
+      }
+      if (overflow && getenv("LMSB_BAND_DEBUG")) {
+        for (int g = 0; g < ngroups; ++g)
+          if ((int64_t)cur[g] > gcap[g])
+            fprintf(stderr, "band direct: group %d (band %d) %llu > cap %lld\n", g, gband[g],
+                    (unsigned long long)cur[g], (long long)gcap[g]);
+      }
+      if (!overflow) {
+        direct = true;
+        CUDA_TRY(cudaMemcpyAsync(c->bstart.p, gstart.data(), sizeof(int64_t) * ngroups,
+                                 cudaMemcpyHostToDevice, c->stream));
+        CUDA_TRY(cudaMemcpyAsync(c->bend.p, gend.data(), sizeof(int64_t) * ngroups,
+                                 cudaMemcpyHostToDevice, c->stream));
+        ba.list = d_glist;
+        ba.group_band = d_gband;
+        ba.nlist = ngroups;
+        st->direct_groups = ngroups;
+      } else {
+        m = 0;
+      }
+    }
+  }
+  if (!direct) {
   for (int attempt = 0; attempt < 2; ++attempt) {
     RC_TRY(c->bck.need(cap));
     RC_TRY(c->bcv.need(cap));
@@ -650,6 +786,7 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     return set_error(LMS_ERR_CUDA, "band grouping sort failed");
   CUDA_TRY(cudaGetLastError());
   st->launches += 3;
+  }
   CUDA_TRY(cudaEventRecord(c->ev_chunk[3], c->stream));
 
   // ---- window counts of the collected vertices; fp32 counts at each
@@ -662,10 +799,12 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   RC_TRY(c->branks2.need(scap));
   RC_TRY(c->bfits2.need(scap));
   RC_TRY(c->blines32.need(h.n));
-  RC_TRY(c->bchunks.need((int64_t)list.size() + 1));
+  RC_TRY(c->bchunks.need((int64_t)std::max<size_t>(list.size(), (size_t)ngroups) + 1));
   ba.members = c->bmem.p;
-  ba.list = c->blist.p;
-  ba.nlist = (int)list.size();
+  if (!direct) {
+    ba.list = c->blist.p;
+    ba.nlist = (int)list.size();
+  }
   ba.chunk = c->band_chunk;
   ba.chunk_prefix = c->bchunks.p;
   ba.out_ranks = c->ranks.p;

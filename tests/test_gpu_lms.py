@@ -570,3 +570,20 @@ def test_small_fit_kernel_vs_unpruned_at_extreme_scales():
         m = len(s)
         want = record_from_native(ref.solve_materialized(int(q[f]), 0, m * (m - 1) // 2))
         assert record_from_native(got[f]) == want, f
+
+
+def test_band_direct_grouping_matches():
+    """The direct sub-band grouping variant of the collect pass
+    (LMSB_BAND_DIRECT=1) returns the same records as the default."""
+    for n, seed in ((16384, 0), (3000, 2)):
+        pts = workloads.contaminated_line_points(n, seed)
+        a, b = pts[:, 0].copy(), pts[:, 1].copy()
+        q = n // 2 + 1
+        total = n * (n - 1) // 2
+        d = _ctx_with({"LMSB_BAND": "2", "LMSB_BAND_DIRECT": "1"})
+        s = _ctx_with({"LMSB_BAND": "2"})
+        d.upload(a, b)
+        s.upload(a, b)
+        got = record_from_native(d.solve(q, 0, total))
+        assert d.stats()["direct_groups"] > 0
+        assert got == record_from_native(s.solve(q, 0, total))
