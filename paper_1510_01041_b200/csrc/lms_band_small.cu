@@ -45,12 +45,18 @@ namespace lmsb {
 
 namespace {
 
+#ifndef LMSB_SMALL_BAND_VERTS
+#define LMSB_SMALL_BAND_VERTS 512
+#endif
 #ifndef LMSB_SMALL_MINB
 #define LMSB_SMALL_MINB 2
 #endif
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kMaxBands = 128;
+#ifndef LMSB_SMALL_MAX_BANDS
+#define LMSB_SMALL_MAX_BANDS 128
+#endif
+constexpr int kMaxBands = LMSB_SMALL_MAX_BANDS;
 constexpr int kSamplesPerBand = 16;
 constexpr int kSamples = kMaxBands * kSamplesPerBand;  // 2,048
 constexpr int kSampleItems = kSamples / kThreads;
@@ -235,7 +241,7 @@ __global__ void __launch_bounds__(kThreads, LMSB_SMALL_MINB) small_fit_kernel(Sm
   const double* ga = args.a + fd.off;
   const double* gb = args.b + fd.off;
   const int64_t P = (int64_t)n * (n - 1) / 2;
-  const int K = (int)min((int64_t)kMaxBands, max((int64_t)16, P / 1024));
+  const int K = (int)min((int64_t)kMaxBands, max((int64_t)16, P / LMSB_SMALL_BAND_VERTS));
 
   // ---- lines, centre, magnitudes
   double alo = INFINITY, ahi = -INFINITY, am = 0.0, bm = 0.0;
