@@ -1187,8 +1187,7 @@ void launch_band_edge_seeds(const BandFit& bf, const BandArgs& ba, const int32_t
 
 void launch_band_seeds(const BandFit& bf, const BandWork& w, int64_t* ranks, int32_t* fits,
                        int32_t fit, int64_t cap, unsigned long long* count, cudaStream_t st) {
-  cudaMemsetAsync(w.sample_counts, 0, sizeof(unsigned) * w.K, st);
-  cudaMemsetAsync(count, 0, sizeof(unsigned long long), st);
+  cudaMemsetAsync(w.sample_counts, 0, sizeof(unsigned) * w.K, st);  // appends after *count
   const int grid = (int)std::min<int64_t>((w.S + 255) / 256, 1184);
   band_seed_kernel<<<grid, 256, 0, st>>>(bf, w.S, w.sample, w.bounds, w.K, w.flag,
                                          w.sample_counts, ranks, fits, fit, cap, count);

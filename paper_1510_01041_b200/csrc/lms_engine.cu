@@ -560,14 +560,13 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   CUDA_TRY(cudaMemcpyAsync(c->bflag.p, flag.data(), K, cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(cudaMemcpyAsync(c->blist.p, seed_bands.data(), sizeof(int32_t) * seed_bands.size(),
                            cudaMemcpyHostToDevice, c->stream));
-  // the window-edge pairs first (usually within a few ulps of the optimum),
-  // then the sampled vertices of the same bands against that bound
+  // the window-edge pairs (usually the optimum itself) and, as a safety net,
+  // up to 64 sampled vertices of the same bands, in one exact launch
   CUDA_TRY(cudaMemsetAsync(sc + 2, 0, sizeof(unsigned long long), c->stream));
   lmsb::launch_band_edge_seeds(bf, ba, c->blist.p, (int)seed_bands.size(), c->ranks.p,
                                c->item_fit.p, seed_cap, sc + 2, c->stream);
-  RC_TRY(exact_list(sc + 2, seed_cap, c->ranks.p, c->item_fit.p));
   lmsb::launch_band_seeds(bf, w, c->ranks.p, c->item_fit.p, 0, seed_cap, sc + 2, c->stream);
-  RC_TRY(exact_list(sc + 2, seed_cap, c->ranks.p, c->item_fit.p));  // pruned against the edges' H
+  RC_TRY(exact_list(sc + 2, seed_cap, c->ranks.p, c->item_fit.p));
   CUDA_TRY(cudaEventRecord(c->ev_chunk[7], c->stream));
   lms_candidate hb{};
   std::vector<unsigned> scnt(K);
