@@ -69,7 +69,7 @@ namespace {
 #endif
 constexpr int kCollectThreads = 512;
 constexpr int kEdge = 5;  // keys kept around each end of a band's narrowest q-window
-constexpr unsigned kSeedPerBand = 64;  // sampled vertices per seed band
+constexpr unsigned kSeedPerBand = 16;  // sampled vertices per seed band (safety net)
 constexpr int kRun = 32;  // ranks per lane per warp segment (lane-interleaved)
 constexpr int kSlopeBits = 17;  // within-band slope order bits of a collected key
 
