@@ -119,6 +119,7 @@ struct lms_ctx {
   const double* b = nullptr;
   int64_t nlines = 0;
   std::vector<double> h_a, h_b;  // host copy: per-fit max |a|, max |b| for the filter margins
+  double s_alo = 0, s_ahi = 0, s_am = 0, s_bm = 0;  // range / magnitudes of all bound lines
   // fits
   DevBuf<lmsb::FitDesc> fits;
   DevBuf<int64_t> prefA, prefB, seed_prefix, seg;
@@ -309,6 +310,43 @@ void ctx_release(lms_ctx* c) {
   if (c->stream) cudaStreamDestroy(c->stream);
 }
 
+// Range and magnitudes of lines [off, off + n) (the whole bound set is cached
+// at upload).
+void line_stats(const lms_ctx* c, int64_t off, int64_t n, double* alo, double* ahi, double* am,
+                double* bm) {
+  if (off == 0 && n == c->nlines) {
+    *alo = c->s_alo;
+    *ahi = c->s_ahi;
+    *am = c->s_am;
+    *bm = c->s_bm;
+    return;
+  }
+  double lo = INFINITY, hi = -INFINITY, ma = 0.0, mb = 0.0;
+  for (int64_t k = off; k < off + n; ++k) {
+    lo = std::min(lo, c->h_a[k]);
+    hi = std::max(hi, c->h_a[k]);
+    ma = std::max(ma, std::fabs(c->h_a[k]));
+    mb = std::max(mb, std::fabs(c->h_b[k]));
+  }
+  *alo = lo;
+  *ahi = hi;
+  *am = ma;
+  *bm = mb;
+}
+
+void cache_line_stats(lms_ctx* c) {
+  c->s_alo = INFINITY;
+  c->s_ahi = -INFINITY;
+  c->s_am = 0.0;
+  c->s_bm = 0.0;
+  for (int64_t k = 0; k < c->nlines; ++k) {
+    c->s_alo = std::min(c->s_alo, c->h_a[k]);
+    c->s_ahi = std::max(c->s_ahi, c->h_a[k]);
+    c->s_am = std::max(c->s_am, std::fabs(c->h_a[k]));
+    c->s_bm = std::max(c->s_bm, std::fabs(c->h_b[k]));
+  }
+}
+
 int ctx_upload(lms_ctx* c, const double* a, const double* b, int64_t n) {
   if (!a || !b || n < 1)
     return set_error(LMS_ERR_INVALID, "need at least 1 line, got %lld", (long long)n);
@@ -322,6 +360,7 @@ int ctx_upload(lms_ctx* c, const double* a, const double* b, int64_t n) {
   c->a = c->a_own.p;
   c->b = c->b_own.p;
   c->nlines = n;
+  cache_line_stats(c);
   return LMS_OK;
 }
 
@@ -425,13 +464,8 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   bf.q = h.q;
   bf.R0 = h.r0;
   bf.span = span;
-  double alo = INFINITY, ahi = -INFINITY, am = 0.0, bmx = 0.0;
-  for (int64_t k = h.off; k < h.off + h.n; ++k) {
-    alo = std::min(alo, c->h_a[k]);
-    ahi = std::max(ahi, c->h_a[k]);
-    am = std::max(am, std::fabs(c->h_a[k]));
-    bmx = std::max(bmx, std::fabs(c->h_b[k]));
-  }
+  double alo, ahi, am, bmx;
+  line_stats(c, h.off, h.n, &alo, &ahi, &am, &bmx);
   bf.c = 0.5 * alo + 0.5 * ahi;
   bf.dev = std::max(ahi - bf.c, bf.c - alo) * (1.0 + 0x1p-40) + 1e-300;
   bf.amax = am;
@@ -898,10 +932,8 @@ int ctx_solve_fits(lms_ctx* c, const std::vector<HostFit>& hf, lms_candidate* ou
     }
     double am = 0.0, bm = 0.0;
     if (!small) {
-      for (int64_t k = h.off; k < h.off + h.n; ++k) {
-        am = std::max(am, std::fabs(c->h_a[k]));
-        bm = std::max(bm, std::fabs(c->h_b[k]));
-      }
+      double alo_, ahi_;
+      line_stats(c, h.off, h.n, &alo_, &ahi_, &am, &bm);
     }
     if (F == 1 && !exhaustive && !small && h.n <= lmsb::kBandMaxBigN && am < 1e30 && bm < 1e30 &&
         (c->band_mode == 2 || (c->band_mode == 1 && span >= kBandMinSpan)))
@@ -1691,6 +1723,7 @@ int lms_ctx_bind_dev(lms_ctx* c, const double* d_a, const double* d_b, int64_t n
   c->a = d_a;
   c->b = d_b;
   c->nlines = n;
+  cache_line_stats(c);
   return LMS_OK;
 }
 
