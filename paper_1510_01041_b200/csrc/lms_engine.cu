@@ -144,6 +144,8 @@ struct lms_ctx {
   DevBuf<int64_t> ii, jj;
   DevBuf<double> uu, vv;
   lms_candidate* h_best = nullptr;  // pinned
+  unsigned char* pin = nullptr;      // pinned staging of the band stage's small readbacks
+  size_t cap_pin = 0;
   int64_t cap_h_best = 0;
   // Hough: the points of the last vote (image pixels or explicit x/y)
   DevBuf<uint8_t> img;
@@ -307,6 +309,7 @@ void ctx_release(lms_ctx* c) {
   c->small_cnt.release();
   c->blines32.release();
   if (c->h_best) cudaFreeHost(c->h_best);
+  if (c->pin) cudaFreeHost(c->pin);
   if (c->stream) cudaStreamDestroy(c->stream);
 }
 
@@ -361,6 +364,16 @@ int ctx_upload(lms_ctx* c, const double* a, const double* b, int64_t n) {
   c->b = c->b_own.p;
   c->nlines = n;
   cache_line_stats(c);
+  return LMS_OK;
+}
+
+int ensure_pinned(lms_ctx* c, size_t bytes) {
+  if (bytes <= c->cap_pin) return LMS_OK;
+  if (c->pin) cudaFreeHost(c->pin);
+  c->pin = nullptr;
+  c->cap_pin = 0;
+  CUDA_TRY(cudaMallocHost(&c->pin, bytes));
+  c->cap_pin = bytes;
   return LMS_OK;
 }
 
@@ -561,17 +574,25 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   CUDA_TRY(cudaGetLastError());
   st->launches += 4;
   CUDA_TRY(cudaEventRecord(c->ev_chunk[1], c->stream));
-  std::vector<double>& lb = c->h_blb;
-  lb.resize(K);
-  std::vector<float> hbnd(K - 1);
-  std::vector<double> wq(K);
-  CUDA_TRY(cudaMemcpyAsync(wq.data(), c->bwq.p, sizeof(double) * K, cudaMemcpyDeviceToHost,
+  // small readbacks through pinned staging (truly asynchronous copies)
+  RC_TRY(ensure_pinned(c, (size_t)K * (2 * sizeof(double) + sizeof(float) + sizeof(unsigned)) +
+                              sizeof(lms_candidate) + 64));
+  double* p_lb = reinterpret_cast<double*>(c->pin);
+  double* p_wq = p_lb + K;
+  lms_candidate* p_hb = reinterpret_cast<lms_candidate*>(p_wq + K);
+  float* p_bnd = reinterpret_cast<float*>(p_hb + 1);
+  unsigned* p_scnt = reinterpret_cast<unsigned*>(p_bnd + K);
+  CUDA_TRY(cudaMemcpyAsync(p_wq, c->bwq.p, sizeof(double) * K, cudaMemcpyDeviceToHost,
                            c->stream));
-  CUDA_TRY(cudaMemcpyAsync(lb.data(), c->blb.p, sizeof(double) * K, cudaMemcpyDeviceToHost,
+  CUDA_TRY(cudaMemcpyAsync(p_lb, c->blb.p, sizeof(double) * K, cudaMemcpyDeviceToHost,
                            c->stream));
-  CUDA_TRY(cudaMemcpyAsync(hbnd.data(), c->bbounds.p, sizeof(float) * (K - 1),
-                           cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(p_bnd, c->bbounds.p, sizeof(float) * (K - 1), cudaMemcpyDeviceToHost,
+                           c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
+  std::vector<double>& lb = c->h_blb;
+  lb.assign(p_lb, p_lb + K);
+  const std::vector<float> hbnd(p_bnd, p_bnd + (K - 1));
+  const std::vector<double> wq(p_wq, p_wq + K);
   std::vector<int32_t> order(K);
   for (int k = 0; k < K; ++k) order[k] = k;
   std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return lb[x] < lb[y]; });
@@ -602,12 +623,13 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   lmsb::launch_band_seeds(bf, w, c->ranks.p, c->item_fit.p, 0, seed_cap, sc + 2, c->stream);
   RC_TRY(exact_list(sc + 2, seed_cap, c->ranks.p, c->item_fit.p));
   CUDA_TRY(cudaEventRecord(c->ev_chunk[7], c->stream));
-  lms_candidate hb{};
-  std::vector<unsigned> scnt(K);
-  CUDA_TRY(cudaMemcpyAsync(&hb, c->best.p, sizeof(hb), cudaMemcpyDeviceToHost, c->stream));
-  CUDA_TRY(cudaMemcpyAsync(scnt.data(), c->bscnt.p, sizeof(unsigned) * K, cudaMemcpyDeviceToHost,
+  CUDA_TRY(cudaMemcpyAsync(p_hb, c->best.p, sizeof(lms_candidate), cudaMemcpyDeviceToHost,
+                           c->stream));
+  CUDA_TRY(cudaMemcpyAsync(p_scnt, c->bscnt.p, sizeof(unsigned) * K, cudaMemcpyDeviceToHost,
                            c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
+  const lms_candidate hb = *p_hb;
+  const std::vector<unsigned> scnt(p_scnt, p_scnt + K);
   const double H = hb.found ? hb.height : INFINITY;
   st->seed_height = H;
 
@@ -802,8 +824,10 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     CUDA_TRY(cudaEventRecord(c->ev_chunk[6], c->stream));
     CUDA_TRY(cudaGetLastError());
     st->launches += 1;
-    CUDA_TRY(cudaMemcpyAsync(&m, sc + 1, sizeof(m), cudaMemcpyDeviceToHost, c->stream));
+    unsigned long long* p_m = reinterpret_cast<unsigned long long*>(c->pin);
+    CUDA_TRY(cudaMemcpyAsync(p_m, sc + 1, sizeof(m), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
+    m = *p_m;
     if ((int64_t)m <= cap) break;
     cap = (int64_t)m;  // estimate too small: collect again with the exact size
   }
