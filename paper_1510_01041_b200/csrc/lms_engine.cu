@@ -575,8 +575,14 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   st->launches += 4;
   CUDA_TRY(cudaEventRecord(c->ev_chunk[1], c->stream));
   // small readbacks through pinned staging (truly asynchronous copies)
-  RC_TRY(ensure_pinned(c, (size_t)K * (2 * sizeof(double) + sizeof(float) + sizeof(unsigned)) +
-                              sizeof(lms_candidate) + 64));
+  const size_t pin_rb = ((size_t)K * (2 * sizeof(double) + sizeof(float) + sizeof(unsigned)) +
+                        sizeof(lms_candidate) + 64 + 255) & ~(size_t)255;
+  RC_TRY(ensure_pinned(c, pin_rb + (size_t)(K + 1) * (2 + 2 * sizeof(int32_t)) + 1024));
+  // upload staging after the readbacks: flags x2, seed bands, collected bands
+  uint8_t* u_flag1 = c->pin + pin_rb;
+  uint8_t* u_flag2 = u_flag1 + (K + 1);
+  int32_t* u_seed = reinterpret_cast<int32_t*>(((uintptr_t)(u_flag2 + (K + 1)) + 15) & ~(uintptr_t)15);
+  int32_t* u_list = u_seed + 64;
   double* p_lb = reinterpret_cast<double*>(c->pin);
   double* p_wq = p_lb + K;
   lms_candidate* p_hb = reinterpret_cast<lms_candidate*>(p_wq + K);
@@ -612,8 +618,10 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
         seed_bands.push_back(byw[e]);
       }
   }
-  CUDA_TRY(cudaMemcpyAsync(c->bflag.p, flag.data(), K, cudaMemcpyHostToDevice, c->stream));
-  CUDA_TRY(cudaMemcpyAsync(c->blist.p, seed_bands.data(), sizeof(int32_t) * seed_bands.size(),
+  std::memcpy(u_flag1, flag.data(), K);
+  std::copy(seed_bands.begin(), seed_bands.end(), u_seed);
+  CUDA_TRY(cudaMemcpyAsync(c->bflag.p, u_flag1, K, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->blist.p, u_seed, sizeof(int32_t) * seed_bands.size(),
                            cudaMemcpyHostToDevice, c->stream));
   // the window-edge pairs (usually the optimum itself) and, as a safety net,
   // up to 64 sampled vertices of the same bands, in one exact launch
@@ -647,8 +655,10 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   for (int32_t k : list) flag[k] = 1;
   list.push_back(K);  // vertices beyond the key range
   int64_t cap = std::min<int64_t>(span, (int64_t)(2.0 * est * (double)span / (double)S) + 65536);
-  CUDA_TRY(cudaMemcpyAsync(c->bflag.p, flag.data(), K, cudaMemcpyHostToDevice, c->stream));
-  CUDA_TRY(cudaMemcpyAsync(c->blist.p, list.data(), sizeof(int32_t) * list.size(),
+  std::memcpy(u_flag2, flag.data(), K);
+  std::copy(list.begin(), list.end(), u_list);
+  CUDA_TRY(cudaMemcpyAsync(c->bflag.p, u_flag2, K, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->blist.p, u_list, sizeof(int32_t) * list.size(),
                            cudaMemcpyHostToDevice, c->stream));
   // slope runs of the flagged bands for the collect pre-test, merged across the
   // smallest gaps down to kMaxRuns
@@ -890,8 +900,9 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     RC_TRY(exact_list(sc + 4, scap, c->branks2.p, c->bfits2.p));
   }
   CUDA_TRY(cudaEventRecord(c->ev_chunk[4], c->stream));
-  unsigned long long cnts[2] = {0, 0};
-  CUDA_TRY(cudaMemcpyAsync(cnts, sc + 3, sizeof(cnts), cudaMemcpyDeviceToHost, c->stream));
+  unsigned long long* cnts = reinterpret_cast<unsigned long long*>(c->pin);  // readbacks done
+  CUDA_TRY(cudaMemcpyAsync(cnts, sc + 3, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                           c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   st->survivors = (int64_t)cnts[1];
   st->band_survivors = (int64_t)cnts[0];
