@@ -64,7 +64,9 @@ def config(n: int, world: int) -> dict:
         "n": n,
         "pairs": n * (n - 1) // 2,
         "q": n // 2 + 1,
-        "partitioning": f"contiguous vertex-rank partitions x{world}, one NCCL all_gather per fit",
+        "partitioning": (f"contiguous vertex-rank partitions x{world}; sharded band search: each rank "
+                         "bounds 1/N of the slope bands, NCCL all_gather of the band table, then of "
+                         "the per-rank records") if world > 1 else "one GPU, whole pair space",
         "l2": "flushed between timed steps (256 MiB write); the 256 KiB line set is re-read from "
               "L2 within a fit by design",
     }
@@ -296,10 +298,9 @@ def run_ours(args):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
 
     def step():
-        rec = record_from_native(ctx.solve(q, r0, r1)) if r1 > r0 else None
-        if world > 1:
-            rec = distributed.combine(distributed.all_gather_records(rec, device=torch.device("cuda", local)))
-        return rec
+        if world > 1:  # sharded band search: band-table all_gather, record all_gather
+            return distributed.solve_sharded(ctx, q, device=torch.device("cuda", local))
+        return record_from_native(ctx.solve(q, r0, r1))
 
     for _ in range(args.warmup):
         step()
@@ -427,7 +428,7 @@ def run_ours(args):
                     "d2h_bytes_per_step": 56 + (8 * 7 * world if world > 1 else 0),
                     "seconds_per_fit": e2e_s / max(1, args.steps),
                     "path": "solve_lms(points) -> LmsFit" if world == 1 else
-                            "distributed.solve_distributed + fit_from_record"},
+                            "distributed.solve_distributed (sharded band search) + fit_from_record"},
             "gpu_launches": launches,
             "roofline": roofline,
             "clocks": clocks,

@@ -173,6 +173,35 @@ int lms_ctx_bind_dev(lms_ctx* ctx, const double* d_a, const double* d_b, int64_t
 /* Solve over [rank_begin, rank_end) of the bound lines; blocks until done. */
 int lms_ctx_solve(lms_ctx* ctx, int64_t q, int64_t rank_begin, int64_t rank_end,
                   lms_candidate* out);
+/* Sharded band search (multi-GPU, one context per GPU).
+ * Replaces the per-partition _scan_rank_range call of a multi-worker run
+ * (backend.py:190-207, partitions backend.py:84-92) when the partitions are
+ * GPUs that can exchange a small per-band table.  Shard s of S searches the
+ * pair ranks [lo, hi) of the ceil split of [0, n(n-1)/2) (distributed.partition).
+ *   1. lms_ctx_shard_plan: every shard samples the whole pair space (the same
+ *      samples, band boundaries and K on every shard) and bounds only its slice
+ *      [band_begin, band_end) of the K slope bands (ceil split of K): per band
+ *      its lower bound, narrowest q-window and LMS_BAND_EDGE_KEYS window-edge
+ *      keys, written to the caller's arrays (capacity bands).  *seed is the
+ *      best exactly evaluated vertex at the ends of the slice's narrowest
+ *      windows (any vertex of the fit; not found if none).  nbands = 0: the
+ *      fit is not searched by bands; skip the exchange.
+ *   2. the caller all-gathers the slices (NCCL over NVLink) into K-band arrays
+ *      and takes the lexicographic minimum of the seeds.
+ *   3. lms_ctx_shard_search: starts from that seed (H = its height) and
+ *      searches the shard's rank range against the full band table.  *out is
+ *      the minimum over the shard's range and the seed (which may lie outside
+ *      the range), so the lexicographic minimum of all shards' records is the
+ *      fit's record (backend.py:182-187), bit-identical to one lms_ctx_solve
+ *      over [0, n(n-1)/2).  A search on the context that ran the plan reuses
+ *      the plan's samples and band boundaries. */
+#define LMS_BAND_EDGE_KEYS 10
+int lms_ctx_shard_plan(lms_ctx* ctx, int64_t q, int32_t nshards, int32_t shard, int64_t capacity,
+                       int64_t* nbands, int64_t* band_begin, int64_t* band_end, double* lower_bound,
+                       double* window, float* edge_keys, lms_candidate* seed);
+int lms_ctx_shard_search(lms_ctx* ctx, int64_t q, int32_t nshards, int32_t shard, int64_t nbands,
+                         const double* lower_bound, const double* window, const float* edge_keys,
+                         const lms_candidate* seed, lms_candidate* out);
 /* Materialised two-kernel solve over the bound lines (see
  * lms_min_bracelet_materialized_f64). */
 int lms_ctx_solve_materialized(lms_ctx* ctx, int64_t q, int64_t rank_begin, int64_t rank_end,

@@ -34,6 +34,14 @@ class EngineError(RuntimeError):
 class Candidate(ctypes.Structure):
     """lms_candidate (include/lms_b200.h)."""
 
+    @classmethod
+    def of(cls, rec) -> "Candidate":
+        """From a CandidateRecord (None: not found)."""
+        if rec is None:
+            return cls()
+        return cls(height=rec.height, u=rec.u, v_low=rec.v_low, v_high=rec.v_high, i=rec.i, j=rec.j,
+                   found=1)
+
     _fields_ = [
         ("height", ctypes.c_double),
         ("u", ctypes.c_double),
@@ -78,6 +86,29 @@ class Stats(ctypes.Structure):
         return {name: getattr(self, name) for name, _ in self._fields_ if not name.startswith("reserved")}
 
 
+MAX_BANDS = 16384       # kBandMaxK (lms_band.cuh)
+BAND_EDGE_KEYS = 10     # LMS_BAND_EDGE_KEYS
+BAND_TABLE_COLS = 2 + BAND_EDGE_KEYS // 2
+
+
+def pack_band_table(lb, wq, edge) -> np.ndarray:
+    """(m, BAND_TABLE_COLS) float64 rows: lb, wq, then the fp32 edge keys' bytes."""
+    m = len(lb)
+    t = np.empty((m, BAND_TABLE_COLS), dtype=np.float64)
+    t[:, 0] = lb
+    t[:, 1] = wq
+    t[:, 2:] = np.ascontiguousarray(edge, dtype=np.float32).reshape(m, BAND_EDGE_KEYS).view(np.float64)
+    return t
+
+
+def unpack_band_table(table):
+    t = np.ascontiguousarray(table, dtype=np.float64).reshape(-1, BAND_TABLE_COLS)
+    lb = np.ascontiguousarray(t[:, 0])
+    wq = np.ascontiguousarray(t[:, 1])
+    edge = np.ascontiguousarray(t[:, 2:]).view(np.float32).reshape(len(t), BAND_EDGE_KEYS)
+    return lb, wq, np.ascontiguousarray(edge)
+
+
 _lib = None
 _lock = threading.Lock()
 
@@ -119,6 +150,12 @@ SIGNATURES = {
     "lms_ctx_solve_materialized": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
                                                   ctypes.c_int64, _C]),
     "lms_ctx_solve_batch": (ctypes.c_int, [ctypes.c_void_p, _I, _I, ctypes.c_int64, _C]),
+    "lms_ctx_shard_plan": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
+                                          ctypes.c_int32, ctypes.c_int64, _I, _I, _I, _D, _D,
+                                          ctypes.POINTER(ctypes.c_float), _C]),
+    "lms_ctx_shard_search": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
+                                            ctypes.c_int32, ctypes.c_int64, _D, _D,
+                                            ctypes.POINTER(ctypes.c_float), _C, _C]),
     "lms_ctx_stats": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(Stats)]),
     "lms_ctx_event_record": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "lms_ctx_event_elapsed_ms": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
@@ -350,6 +387,39 @@ class Context:
     def solve(self, q: int, rank_begin: int, rank_end: int) -> Candidate:
         out = Candidate()
         check(self._lib.lms_ctx_solve(self._h, int(q), int(rank_begin), int(rank_end), ctypes.byref(out)))
+        return out
+
+    def shard_plan(self, q: int, nshards: int, shard: int):
+        """Bounds of this shard's slice of the slope bands (lms_ctx_shard_plan).
+
+        Returns ``(K, k0, k1, table, seed)`` with ``table`` a float64 array of
+        shape ``(k1 - k0, BAND_TABLE_COLS)``: lower bound, narrowest q-window
+        and the window-edge keys (fp32, packed two per column); ``seed`` is the
+        best vertex at the ends of the slice's narrowest windows (a Candidate).
+        ``K == 0``: the fit is not searched by bands (no exchange needed).
+        """
+        cap = -(-MAX_BANDS // max(1, int(nshards)))
+        lb = np.empty(cap, dtype=np.float64)
+        wq = np.empty(cap, dtype=np.float64)
+        edge = np.empty((cap, BAND_EDGE_KEYS), dtype=np.float32)
+        K, k0, k1 = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        seed = Candidate()
+        check(self._lib.lms_ctx_shard_plan(
+            self._h, int(q), int(nshards), int(shard), cap, ctypes.byref(K), ctypes.byref(k0),
+            ctypes.byref(k1), lb.ctypes.data_as(_D), wq.ctypes.data_as(_D),
+            edge.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), ctypes.byref(seed)))
+        m = k1.value - k0.value
+        return K.value, k0.value, k1.value, pack_band_table(lb[:m], wq[:m], edge[:m]), seed
+
+    def shard_search(self, q: int, nshards: int, shard: int, table, seed=None) -> Candidate:
+        """Search this shard's rank range against the full band table (all K
+        bands), starting from ``seed`` (the minimum of all shards' plan seeds)."""
+        lb, wq, edge = unpack_band_table(table)
+        out = Candidate()
+        check(self._lib.lms_ctx_shard_search(
+            self._h, int(q), int(nshards), int(shard), len(lb), lb.ctypes.data_as(_D),
+            wq.ctypes.data_as(_D), edge.ctypes.data_as(ctypes.POINTER(ctypes.c_float)),
+            ctypes.byref(seed) if seed is not None else None, ctypes.byref(out)))
         return out
 
     def solve_materialized(self, q: int, rank_begin: int, rank_end: int) -> Candidate:

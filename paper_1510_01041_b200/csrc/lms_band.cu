@@ -54,6 +54,7 @@
 
 #include <algorithm>
 #include <cfloat>
+#include <climits>
 #include <cmath>
 #include <cstdint>
 
@@ -68,7 +69,6 @@ namespace {
 #define LMSB_RADIX_BITS 4
 #endif
 constexpr int kCollectThreads = 512;
-constexpr int kEdge = 5;  // keys kept around each end of a band's narrowest q-window
 constexpr unsigned kSeedPerBand = 16;  // sampled vertices per seed band (safety net)
 constexpr int kRun = 32;  // ranks per lane per warp segment (lane-interleaved)
 constexpr int kSlopeBits = 17;  // within-band slope order bits of a collected key
@@ -93,7 +93,7 @@ __device__ __forceinline__ int classify(const BandFit& bf, double ai, double bi,
 }
 
 __device__ __forceinline__ int64_t sample_rank(const BandFit& bf, int64_t S, int64_t s) {
-  return bf.R0 + ((2 * s + 1) * bf.span) / (2 * S);
+  return bf.P0 + ((2 * s + 1) * bf.pspan) / (2 * S);
 }
 
 // number of boundaries <= key, i.e. the band index
@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(kThreads, 1) band_bound_kernel(BandFit bf, Ban
   using SH = BandShared<kThreads, kItems>;
   extern __shared__ __align__(16) unsigned char band_smem[];
   SH& sh = *reinterpret_cast<SH*>(band_smem);
-  const int band = (int)blockIdx.x;
+  const int band = ba.band0 + (int)blockIdx.x;
   double uL, uR;
   if (!boundary_extent(ba.bounds, ba.K, band, &uL, &uR) || !keys_in_range(bf, uL, uR)) {
     if (threadIdx.x == 0) {
@@ -718,7 +718,7 @@ __global__ void __launch_bounds__(1024) band_edge_seed_kernel(BandFit bf, BandAr
       int x = grp[g][t / m], y = grp[g][t % m];
       if (x >= y) continue;
       const int64_t r = row_offset(bf.n, x) + (y - x - 1);
-      if (r < bf.R0 || r >= bf.R0 + bf.span) continue;
+      if (r < bf.P0 || r >= bf.P0 + bf.pspan) continue;
       const unsigned long long pos = atomicAdd(count, 1ull);
       if ((int64_t)pos < cap) {
         ranks[pos] = r;
@@ -899,10 +899,11 @@ __global__ void band_runs_kernel(const uint32_t* __restrict__ keys, int64_t m,
 // counts with the band's own centre (no per-chunk sort).
 
 __global__ void band_keys_global_kernel(BandFit bf, const float* __restrict__ bounds, int K,
-                                        int band0, int nb, float* __restrict__ keys) {
+                                        int band0, const int32_t* __restrict__ ids, int nb,
+                                        float* __restrict__ keys) {
   const int n = (int)bf.n;
   for (int e = blockIdx.y; e < nb; e += gridDim.y) {
-    const int band = band0 + e;
+    const int band = ids ? ids[band0 + e] : band0 + e;
     double uL, uR;
     const bool ok = boundary_extent(bounds, K, band, &uL, &uR) && keys_in_range(bf, uL, uR);
     const double uM = 0.5 * uL + 0.5 * uR;
@@ -914,11 +915,12 @@ __global__ void band_keys_global_kernel(BandFit bf, const float* __restrict__ bo
 }
 
 __global__ void __launch_bounds__(1024) band_wq_kernel(BandFit bf, BandArgs ba, int band0,
+                                                      const int32_t* __restrict__ ids,
                                                       const float* __restrict__ sorted,
                                                       float* __restrict__ store) {
   __shared__ double red[32];
   __shared__ int kstar;
-  const int band = band0 + blockIdx.x;
+  const int band = ids ? ids[band0 + blockIdx.x] : band0 + (int)blockIdx.x;
   const int n = (int)bf.n, q = (int)bf.q;
   double uL, uR;
   if (!boundary_extent(ba.bounds, ba.K, band, &uL, &uR) || !keys_in_range(bf, uL, uR)) {
@@ -1149,20 +1151,20 @@ __global__ void seg_offsets_kernel(int64_t* off, int nb, int64_t n) {
     off[e] = (int64_t)e * n;
 }
 
-int launch_band_bound_big(const BandFit& bf, const BandArgs& ba, const BandBig& bg,
-                          cudaStream_t st) {
+int launch_band_bound_big(const BandFit& bf, const BandArgs& ba, const BandBig& bg, int k0,
+                          int k1, const int32_t* ids, cudaStream_t st) {
   const int64_t n = bf.n;
   seg_offsets_kernel<<<(bg.batch + 256) / 256, 256, 0, st>>>(bg.seg, bg.batch, n);
-  for (int b0 = 0; b0 < ba.K; b0 += bg.batch) {
-    const int nb = std::min(bg.batch, ba.K - b0);
+  for (int b0 = k0; b0 < k1; b0 += bg.batch) {
+    const int nb = std::min(bg.batch, k1 - b0);
     dim3 grid((unsigned)std::min<int64_t>((n + 255) / 256, 64), (unsigned)std::min(nb, 65535));
-    band_keys_global_kernel<<<grid, 256, 0, st>>>(bf, ba.bounds, ba.K, b0, nb, bg.keys);
+    band_keys_global_kernel<<<grid, 256, 0, st>>>(bf, ba.bounds, ba.K, b0, ids, nb, bg.keys);
     size_t bytes = bg.temp_bytes;
     if (cub::DeviceSegmentedRadixSort::SortKeys(bg.temp, bytes, bg.keys, bg.keys_alt,
                                                 (int)(nb * n), nb, bg.seg, bg.seg + 1, 0, 32,
                                                 st) != cudaSuccess)
       return -1;
-    band_wq_kernel<<<nb, 1024, 0, st>>>(bf, ba, b0, bg.keys_alt, bg.store);
+    band_wq_kernel<<<nb, 1024, 0, st>>>(bf, ba, b0, ids, bg.keys_alt, bg.store);
   }
   return 0;
 }
@@ -1176,6 +1178,61 @@ void launch_band_filter_big(const BandFit& bf, const BandArgs& ba, const float* 
   static bool done = false;
   set_smem(band_filter_big_kernel, (size_t)kBandMaxBigN * sizeof(uint16_t), &done);
   band_filter_big_kernel<<<grid, kBigThreads, smem, st>>>(bf, ba, store);
+}
+
+__global__ void __launch_bounds__(1024) band_top_kernel(const double* __restrict__ wq, int k0,
+                                                       int k1, int K, int T,
+                                                       int32_t* __restrict__ list,
+                                                       uint8_t* __restrict__ flag) {
+  __shared__ double rv[32];
+  __shared__ int rk[32];
+  __shared__ int chosen[16];
+  for (int k = threadIdx.x; k < K; k += blockDim.x) flag[k] = 0;
+  __syncthreads();
+  for (int t = 0; t < T; ++t) {
+    double v = INFINITY;
+    int bk = INT_MAX;
+    for (int k = k0 + (int)threadIdx.x; k < k1; k += blockDim.x) {
+      bool taken = false;
+      for (int e = 0; e < t; ++e) taken |= chosen[e] == k;
+      const double x = wq[k];
+      if (!taken && x < v) {
+        v = x;
+        bk = k;
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, v, off);
+      const int ok = __shfl_xor_sync(0xffffffffu, bk, off);
+      if (ov < v || (ov == v && ok < bk)) {
+        v = ov;
+        bk = ok;
+      }
+    }
+    if ((threadIdx.x & 31) == 0) {
+      rv[threadIdx.x >> 5] = v;
+      rk[threadIdx.x >> 5] = bk;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+        if (rv[w] < v || (rv[w] == v && rk[w] < bk)) {
+          v = rv[w];
+          bk = rk[w];
+        }
+      const int pick = v < INFINITY ? bk : -1;
+      chosen[t] = pick;
+      list[t] = pick;
+      if (pick >= 0) flag[pick] = 1;
+    }
+    __syncthreads();
+  }
+}
+
+void launch_band_top(const double* wq, int k0, int k1, int K, int T, int32_t* list, uint8_t* flag,
+                     cudaStream_t st) {
+  band_top_kernel<<<1, 1024, 0, st>>>(wq, k0, k1, K, T < 16 ? T : 16, list, flag);
 }
 
 void launch_band_edge_seeds(const BandFit& bf, const BandArgs& ba, const int32_t* bands, int nb,

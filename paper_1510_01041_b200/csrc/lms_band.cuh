@@ -22,7 +22,9 @@ struct BandFit {
   const double* a;  // the fit's lines (input order)
   const double* b;
   int64_t n, q;
-  int64_t R0, span;  // pair ranks [R0, R0 + span)
+  int64_t R0, span;  // pair ranks [R0, R0 + span) searched
+  int64_t P0, pspan; // plan range [P0, P0 + pspan): slope samples, band boundaries and seed
+                     // pairs (the search range, unless one shard of a sharded solve)
   double c;          // centre of the a-range
   double dev;        // >= max_k |a_k - c|
   double amax, bmax;
@@ -48,6 +50,9 @@ struct BandWork {
   void* temp;
   size_t temp_bytes;
 };
+
+// keys kept around each end of a band's narrowest q-window (2 * kEdge per band)
+constexpr int kEdge = 5;
 
 // Slope runs of the flagged bands (collect pre-test), at most kMaxRuns: fp32
 // bounds widened by 2^-18 relative + 1e-37 and rounded outward (-inf / +inf:
@@ -75,6 +80,7 @@ struct BandDirect {
 
 struct BandArgs {
   int K;
+  int band0;                  // bound launch (mode 0): first band, block b bounds band0 + b
   const float* bounds;
   const int64_t* start;
   const int64_t* end;
@@ -118,8 +124,10 @@ struct BandBig {
   size_t temp_bytes;
 };
 size_t band_big_sort_temp_bytes(int nb, int64_t n);
-int launch_band_bound_big(const BandFit& bf, const BandArgs& ba, const BandBig& bg,
-                          cudaStream_t st);
+// bounds (and stored sorted keys) of bands [k0, k1), or of bands ids[k0 .. k1)
+// when ids (device) is given
+int launch_band_bound_big(const BandFit& bf, const BandArgs& ba, const BandBig& bg, int k0,
+                          int k1, const int32_t* ids, cudaStream_t st);
 void launch_band_filter_big(const BandFit& bf, const BandArgs& ba, const float* store, int grid,
                             cudaStream_t st);
 
@@ -127,8 +135,13 @@ size_t band_sample_temp_bytes(int64_t S);
 size_t band_group_temp_bytes(int64_t m);
 size_t band_collect_smem(int K);
 int launch_band_sample(const BandFit& bf, const BandWork& w, int sms, cudaStream_t st);
-// mode 0: grid = K (lower bound of every band); mode 1: grid >= chunks of the listed bands
+// mode 0: grid = bands [ba.band0, ba.band0 + grid) (their lower bounds); mode 1: grid >=
+// chunks of the listed bands
 void launch_band(const BandFit& bf, const BandArgs& ba, int mode, int grid, cudaStream_t st);
+// the T bands of [k0, k1) with the narrowest finite q-windows into list[0 .. T)
+// (-1: none), flagged in flag[0 .. K) (cleared first)
+void launch_band_top(const double* wq, int k0, int k1, int K, int T, int32_t* list, uint8_t* flag,
+                     cudaStream_t st);
 // pairs of lines at the ends of the listed bands' narrowest q-windows
 void launch_band_edge_seeds(const BandFit& bf, const BandArgs& ba, const int32_t* bands, int nb,
                             int64_t* ranks, int32_t* fits, int64_t cap,

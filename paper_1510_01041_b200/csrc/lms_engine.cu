@@ -103,6 +103,46 @@ struct HostFit {
   int64_t off, n, q, r0, r1;
 };
 
+// One shard of a sharded band search (lms_ctx_shard_plan / _search): the
+// band plan (samples, boundaries, seeds) covers the whole pair space
+// [P0, P1); the shard bounds only its slice [k0, k1) of the bands (plan) or
+// takes every band's bound from the caller (search) and searches its own
+// rank range.
+struct ShardSpec {
+  int mode = 0;          // 1 plan, 2 search
+  int64_t P0 = 0, P1 = 0;
+  int nshards = 1, shard = 0;
+  int64_t K = 0, k0 = 0, k1 = 0;  // plan: set by band_solve
+  int64_t cap = 0;                // plan: capacity of the output slice
+  double* lb_out = nullptr;
+  double* wq_out = nullptr;
+  float* edge_out = nullptr;
+  lms_candidate seed_out{};       // plan: best seed of the slice's narrowest windows
+  int64_t K_in = 0;               // search: bands of the caller's arrays
+  const double* lb_in = nullptr;
+  const double* wq_in = nullptr;
+  const float* edge_in = nullptr;
+  lms_candidate seed_in{};        // search: best seed over all shards
+};
+
+// Host side of the last shard plan run on a context (its device keeps the
+// samples and boundaries), reused by a search of the same fit.
+struct ShardPlanState {
+  bool valid = false;
+  uint64_t gen = 0;
+  int64_t n = 0, q = 0, K = 0, S = 0, P0 = 0, pspan = 0;
+  std::vector<float> h_bnd;
+  std::vector<unsigned> h_scnt;
+};
+
+// contiguous share `s` of `total` items over `parts` (ceil split, as
+// distributed.partition / BatchPlan.partitions, backend.py:84-92)
+inline void share_of(int64_t total, int64_t parts, int64_t s, int64_t* lo, int64_t* hi) {
+  const int64_t size = std::max<int64_t>(1, (total + parts - 1) / parts);
+  *lo = std::min(total, s * size);
+  *hi = std::min(total, *lo + size);
+}
+
 }  // namespace
 
 struct lms_ctx {
@@ -188,6 +228,9 @@ struct lms_ctx {
   int small_mode = 1;  // LMSB_SMALL: 0 off, 1 batches, 2 also single fits
   DevBuf<float2> blines32;
   std::vector<double> h_blb;
+  ShardSpec* shard = nullptr;  // set for the duration of a shard plan / search call
+  ShardPlanState splan;
+  uint64_t gen = 0;            // bumped whenever the bound lines change
   int hough_mode = 0;  // 0 none, 1 image pixels, 2 explicit points
   int64_t hough_npts = 0, hough_width = 1;
   lms_stats stats{};
@@ -338,6 +381,7 @@ void line_stats(const lms_ctx* c, int64_t off, int64_t n, double* alo, double* a
 }
 
 void cache_line_stats(lms_ctx* c) {
+  ++c->gen;
   c->s_alo = INFINITY;
   c->s_ahi = -INFINITY;
   c->s_am = 0.0;
@@ -447,12 +491,25 @@ int order_lines(lms_ctx* c, const std::vector<int64_t>& seg, int64_t F, const do
 // fit's magnitudes are finite and n <= kBandMaxBigN.
 int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   const int64_t span = h.r1 - h.r0;
+  ShardSpec* sh = c->shard;
+  const int64_t P0 = sh ? sh->P0 : h.r0;
+  const int64_t pspan = sh ? sh->P1 - sh->P0 : span;
   // large n: bands of >= 32 n vertices (their keys are sorted in global memory)
   const bool big = h.n > lmsb::kBandMaxN;
   const int64_t bv = big ? std::max<int64_t>(c->band_vertices, c->big_mult * h.n) : c->band_vertices;
-  const int K = (int)std::max<int64_t>(3, std::min<int64_t>(lmsb::kBandMaxK, (span + bv - 1) / bv));
+  const int K = (int)std::max<int64_t>(3, std::min<int64_t>(lmsb::kBandMaxK, (pspan + bv - 1) / bv));
   const int64_t S =
-      std::min<int64_t>(span, std::min<int64_t>(1 << 20, std::max<int64_t>(64 * K, 1 << 16)));
+      std::min<int64_t>(pspan, std::min<int64_t>(1 << 20, std::max<int64_t>(64 * K, 1 << 16)));
+  // bands bounded here: all, or the shard's slice (plan), or none (search:
+  // every band's bound comes from the caller)
+  int64_t k0 = 0, k1 = K;
+  if (sh && sh->mode == 1) share_of(K, sh->nshards, sh->shard, &k0, &k1);
+  if (sh && sh->mode == 2) {
+    if (sh->K_in != K)
+      return set_error(LMS_ERR_INVALID, "shard search: %lld bands given, the plan has %d",
+                       (long long)sh->K_in, K);
+    k0 = k1 = 0;
+  }
   constexpr int kSeedBands = 8;
   const int64_t seed_cap = S;
   RC_TRY(c->bsample.need(2 * S));
@@ -464,7 +521,7 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   RC_TRY(c->bend.need(K + 1));
   RC_TRY(c->blb.need(K));
   RC_TRY(c->bwq.need(K));
-  RC_TRY(c->blist.need(K + 1));
+  RC_TRY(c->blist.need(std::max(K + 1, 16)));
   RC_TRY(c->btemp.need((int64_t)lmsb::band_sample_temp_bytes(S)));
   RC_TRY(c->ranks.need(seed_cap));
   RC_TRY(c->item_fit.need(seed_cap));
@@ -477,6 +534,8 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   bf.q = h.q;
   bf.R0 = h.r0;
   bf.span = span;
+  bf.P0 = P0;
+  bf.pspan = pspan;
   double alo, ahi, am, bmx;
   line_stats(c, h.off, h.n, &alo, &ahi, &am, &bmx);
   bf.c = 0.5 * alo + 0.5 * ahi;
@@ -536,19 +595,30 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
 
   // ---- sample, boundaries, per-band lower bounds
   CUDA_TRY(cudaEventRecord(c->ev_chunk[0], c->stream));
-  if (lmsb::launch_band_sample(bf, w, c->sms, c->stream) != 0)
-    return set_error(LMS_ERR_CUDA, "band sample sort failed");
+  // a shard search reuses its context's plan (samples, boundaries, counts)
+  // when the same fit was planned on it last
+  ShardPlanState& sp = c->splan;
+  const bool reuse = sh && sh->mode == 2 && sp.valid && sp.gen == c->gen && sp.n == h.n &&
+                     sp.q == h.q && sp.K == K && sp.S == S && sp.P0 == P0 && sp.pspan == pspan;
+  if (!reuse) {
+    sp.valid = false;
+    if (lmsb::launch_band_sample(bf, w, c->sms, c->stream) != 0)
+      return set_error(LMS_ERR_CUDA, "band sample sort failed");
+    st->launches += 4;
+  }
   lmsb::BandArgs ba{};
   ba.K = K;
+  ba.band0 = (int)k0;
   ba.bounds = c->bbounds.p;
   ba.start = c->bstart.p;
   ba.end = c->bend.p;
   ba.lb = c->blb.p;
   ba.wq = c->bwq.p;
-  RC_TRY(c->bedge.need((int64_t)K * 10));
+  RC_TRY(c->bedge.need((int64_t)K * 2 * lmsb::kEdge));
   ba.edge = c->bedge.p;
   ba.best = c->best.p;
   ba.fit = 0;
+  lmsb::BandBig bg{};
   if (big) {
     constexpr int kBatch = 256;
     RC_TRY(c->bbig_keys.need((int64_t)kBatch * h.n * 2));
@@ -556,7 +626,6 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     RC_TRY(c->bbig_seg.need(kBatch + 1));
     RC_TRY(c->btemp.need((int64_t)std::max(lmsb::band_sample_temp_bytes(S),
                                            lmsb::band_big_sort_temp_bytes(kBatch, h.n))));
-    lmsb::BandBig bg{};
     bg.batch = kBatch;
     bg.keys = c->bbig_keys.p;
     bg.keys_alt = c->bbig_keys.p + (int64_t)kBatch * h.n;
@@ -564,20 +633,24 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     bg.seg = c->bbig_seg.p;
     bg.temp = c->btemp.p;
     bg.temp_bytes = (size_t)c->btemp.cap;
-    if (lmsb::launch_band_bound_big(bf, ba, bg, c->stream) != 0)
-      return set_error(LMS_ERR_CUDA, "large-n band bound sort failed");
-    st->launches += 4 * ((K + kBatch - 1) / kBatch);
-  } else {
-    lmsb::launch_band(bf, ba, 0, K, c->stream);
+    if (k1 > k0) {
+      if (lmsb::launch_band_bound_big(bf, ba, bg, (int)k0, (int)k1, nullptr, c->stream) != 0)
+        return set_error(LMS_ERR_CUDA, "large-n band bound sort failed");
+      st->launches += 4 * ((k1 - k0 + kBatch - 1) / kBatch);
+    }
+  } else if (k1 > k0) {
+    lmsb::launch_band(bf, ba, 0, (int)(k1 - k0), c->stream);
     st->launches += 1;
   }
   CUDA_TRY(cudaGetLastError());
-  st->launches += 4;
-  CUDA_TRY(cudaEventRecord(c->ev_chunk[1], c->stream));
   // small readbacks through pinned staging (truly asynchronous copies)
   const size_t pin_rb = ((size_t)K * (2 * sizeof(double) + sizeof(float) + sizeof(unsigned)) +
                         sizeof(lms_candidate) + 64 + 255) & ~(size_t)255;
-  RC_TRY(ensure_pinned(c, pin_rb + (size_t)(K + 1) * (2 + 2 * sizeof(int32_t)) + 1024));
+  const size_t pin_up = (size_t)(K + 1) * (2 + 2 * sizeof(int32_t)) + 1024;
+  // a search's band table goes up through pinned staging as well
+  const size_t pin_tab = (sh && sh->mode == 2) ? (size_t)K * (2 * sizeof(double) +
+                                                              2 * lmsb::kEdge * sizeof(float)) : 0;
+  RC_TRY(ensure_pinned(c, pin_rb + pin_up + pin_tab));
   // upload staging after the readbacks: flags x2, seed bands, collected bands
   uint8_t* u_flag1 = c->pin + pin_rb;
   uint8_t* u_flag2 = u_flag1 + (K + 1);
@@ -588,57 +661,164 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   lms_candidate* p_hb = reinterpret_cast<lms_candidate*>(p_wq + K);
   float* p_bnd = reinterpret_cast<float*>(p_hb + 1);
   unsigned* p_scnt = reinterpret_cast<unsigned*>(p_bnd + K);
-  CUDA_TRY(cudaMemcpyAsync(p_wq, c->bwq.p, sizeof(double) * K, cudaMemcpyDeviceToHost,
-                           c->stream));
-  CUDA_TRY(cudaMemcpyAsync(p_lb, c->blb.p, sizeof(double) * K, cudaMemcpyDeviceToHost,
-                           c->stream));
-  CUDA_TRY(cudaMemcpyAsync(p_bnd, c->bbounds.p, sizeof(float) * (K - 1), cudaMemcpyDeviceToHost,
-                           c->stream));
-  CUDA_TRY(cudaStreamSynchronize(c->stream));
+
+  if (sh && sh->mode == 1) {
+    // ---- plan: seeds from the slice's narrowest windows (picked on the
+    // device, no extra round trip), then one readback of the slice's bounds,
+    // the seed record, the boundaries and the sample counts
+    const int T = std::max(2, (kSeedBands + sh->nshards - 1) / sh->nshards);
+    lmsb::launch_band_top(c->bwq.p, (int)k0, (int)k1, K, T, c->blist.p, c->bflag.p, c->stream);
+    CUDA_TRY(cudaMemsetAsync(sc + 2, 0, sizeof(unsigned long long), c->stream));
+    lmsb::launch_band_edge_seeds(bf, ba, c->blist.p, T, c->ranks.p, c->item_fit.p, seed_cap,
+                                 sc + 2, c->stream);
+    lmsb::launch_band_seeds(bf, w, c->ranks.p, c->item_fit.p, 0, seed_cap, sc + 2, c->stream);
+    RC_TRY(exact_list(sc + 2, seed_cap, c->ranks.p, c->item_fit.p));
+    st->launches += 3;
+    const int64_t m = k1 - k0;
+    if (m > sh->cap)
+      return set_error(LMS_ERR_INVALID, "shard plan: %lld bands exceed the capacity %lld",
+                       (long long)m, (long long)sh->cap);
+    CUDA_TRY(cudaMemcpyAsync(p_lb, c->blb.p + k0, sizeof(double) * m, cudaMemcpyDeviceToHost,
+                             c->stream));
+    CUDA_TRY(cudaMemcpyAsync(p_wq, c->bwq.p + k0, sizeof(double) * m, cudaMemcpyDeviceToHost,
+                             c->stream));
+    CUDA_TRY(cudaMemcpyAsync(sh->edge_out, c->bedge.p + k0 * 2 * lmsb::kEdge,
+                             sizeof(float) * m * 2 * lmsb::kEdge, cudaMemcpyDeviceToHost,
+                             c->stream));
+    CUDA_TRY(cudaMemcpyAsync(p_hb, c->best.p, sizeof(lms_candidate), cudaMemcpyDeviceToHost,
+                             c->stream));
+    CUDA_TRY(cudaMemcpyAsync(p_bnd, c->bbounds.p, sizeof(float) * (K - 1), cudaMemcpyDeviceToHost,
+                             c->stream));
+    CUDA_TRY(cudaMemcpyAsync(p_scnt, c->bscnt.p, sizeof(unsigned) * K, cudaMemcpyDeviceToHost,
+                             c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    std::memcpy(sh->lb_out, p_lb, sizeof(double) * m);
+    std::memcpy(sh->wq_out, p_wq, sizeof(double) * m);
+    sh->seed_out = *p_hb;
+    sh->K = K;
+    sh->k0 = k0;
+    sh->k1 = k1;
+    sp.h_bnd.assign(p_bnd, p_bnd + (K - 1));
+    sp.h_scnt.assign(p_scnt, p_scnt + K);
+    sp.valid = true;
+    sp.gen = c->gen;
+    sp.n = h.n;
+    sp.q = h.q;
+    sp.K = K;
+    sp.S = S;
+    sp.P0 = P0;
+    sp.pspan = pspan;
+    st->bands = K;
+    st->seed_height = sh->seed_out.found ? sh->seed_out.height : INFINITY;
+    CUDA_TRY(cudaEventRecord(c->ev_chunk[1], c->stream));
+    return LMS_OK;
+  }
+
   std::vector<double>& lb = c->h_blb;
-  lb.assign(p_lb, p_lb + K);
-  const std::vector<float> hbnd(p_bnd, p_bnd + (K - 1));
-  const std::vector<double> wq(p_wq, p_wq + K);
+  std::vector<float> hbnd;
+  std::vector<double> wq;
+  std::vector<unsigned> scnt;
+  double H = INFINITY;
+  std::vector<uint8_t> flag(K + 1, 0);
+  if (sh && sh->mode == 2) {
+    // ---- search: every band's bound and the global seed record from the
+    // caller (the exchanged plan); boundaries and counts from this context's
+    // plan, or recomputed
+    double* t_lb = reinterpret_cast<double*>(c->pin + pin_rb + pin_up);
+    double* t_wq = t_lb + K;
+    float* t_edge = reinterpret_cast<float*>(t_wq + K);
+    std::memcpy(t_lb, sh->lb_in, sizeof(double) * K);
+    std::memcpy(t_wq, sh->wq_in, sizeof(double) * K);
+    std::memcpy(t_edge, sh->edge_in, sizeof(float) * K * 2 * lmsb::kEdge);
+    CUDA_TRY(cudaMemcpyAsync(c->blb.p, t_lb, sizeof(double) * K, cudaMemcpyHostToDevice,
+                             c->stream));
+    CUDA_TRY(cudaMemcpyAsync(c->bwq.p, t_wq, sizeof(double) * K, cudaMemcpyHostToDevice,
+                             c->stream));
+    CUDA_TRY(cudaMemcpyAsync(c->bedge.p, t_edge, sizeof(float) * K * 2 * lmsb::kEdge,
+                             cudaMemcpyHostToDevice, c->stream));
+    if (sh->seed_in.found) {
+      lms_candidate* p_seed = p_hb;
+      *p_seed = sh->seed_in;
+      p_seed->reserved = 0;
+      CUDA_TRY(cudaMemcpyAsync(c->recs.p, p_seed, sizeof(lms_candidate), cudaMemcpyHostToDevice,
+                               c->stream));
+      lmsb::launch_reduce(c->recs.p, nullptr, 1, 1, c->fits.p, c->keys.p, c->best.p, 1,
+                          c->stream);
+      st->launches += 2;
+      H = sh->seed_in.height;
+    }
+    if (reuse) {
+      hbnd = sp.h_bnd;
+      scnt = sp.h_scnt;
+    } else {
+      CUDA_TRY(cudaMemsetAsync(c->bflag.p, 0, K, c->stream));
+      CUDA_TRY(cudaMemsetAsync(sc + 2, 0, sizeof(unsigned long long), c->stream));
+      lmsb::launch_band_seeds(bf, w, c->ranks.p, c->item_fit.p, 0, 0, sc + 2, c->stream);  // counts
+      st->launches += 1;
+      CUDA_TRY(cudaMemcpyAsync(p_bnd, c->bbounds.p, sizeof(float) * (K - 1),
+                               cudaMemcpyDeviceToHost, c->stream));
+      CUDA_TRY(cudaMemcpyAsync(p_scnt, c->bscnt.p, sizeof(unsigned) * K, cudaMemcpyDeviceToHost,
+                               c->stream));
+      CUDA_TRY(cudaStreamSynchronize(c->stream));
+      hbnd.assign(p_bnd, p_bnd + (K - 1));
+      scnt.assign(p_scnt, p_scnt + K);
+    }
+    lb.assign(sh->lb_in, sh->lb_in + K);
+    wq.assign(sh->wq_in, sh->wq_in + K);
+    CUDA_TRY(cudaEventRecord(c->ev_chunk[1], c->stream));
+    CUDA_TRY(cudaEventRecord(c->ev_chunk[7], c->stream));
+  } else {
+    CUDA_TRY(cudaEventRecord(c->ev_chunk[1], c->stream));
+    CUDA_TRY(cudaMemcpyAsync(p_wq, c->bwq.p, sizeof(double) * K, cudaMemcpyDeviceToHost,
+                             c->stream));
+    CUDA_TRY(cudaMemcpyAsync(p_lb, c->blb.p, sizeof(double) * K, cudaMemcpyDeviceToHost,
+                             c->stream));
+    CUDA_TRY(cudaMemcpyAsync(p_bnd, c->bbounds.p, sizeof(float) * (K - 1), cudaMemcpyDeviceToHost,
+                             c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    lb.assign(p_lb, p_lb + K);
+    hbnd.assign(p_bnd, p_bnd + (K - 1));
+    wq.assign(p_wq, p_wq + K);
+
+    // ---- seeds: the samples of the bands with the narrowest q-windows at their
+    // centre slope (the bands an LMS line of that slope would come from)
+    std::vector<int32_t> seed_bands;
+    {
+      std::vector<int32_t> byw(K);
+      for (int k = 0; k < K; ++k) byw[k] = k;
+      std::stable_sort(byw.begin(), byw.end(), [&](int32_t x, int32_t y) { return wq[x] < wq[y]; });
+      for (int e = 0; e < K && e < kSeedBands; ++e)
+        if (std::isfinite(wq[byw[e]])) {
+          flag[byw[e]] = 1;
+          seed_bands.push_back(byw[e]);
+        }
+    }
+    std::memcpy(u_flag1, flag.data(), K);
+    std::copy(seed_bands.begin(), seed_bands.end(), u_seed);
+    CUDA_TRY(cudaMemcpyAsync(c->bflag.p, u_flag1, K, cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(c->blist.p, u_seed, sizeof(int32_t) * seed_bands.size(),
+                             cudaMemcpyHostToDevice, c->stream));
+    // the window-edge pairs (usually the optimum itself) and, as a safety net,
+    // up to 16 sampled vertices of each of the same bands, in one exact launch
+    CUDA_TRY(cudaMemsetAsync(sc + 2, 0, sizeof(unsigned long long), c->stream));
+    lmsb::launch_band_edge_seeds(bf, ba, c->blist.p, (int)seed_bands.size(), c->ranks.p,
+                                 c->item_fit.p, seed_cap, sc + 2, c->stream);
+    lmsb::launch_band_seeds(bf, w, c->ranks.p, c->item_fit.p, 0, seed_cap, sc + 2, c->stream);
+    RC_TRY(exact_list(sc + 2, seed_cap, c->ranks.p, c->item_fit.p));
+    CUDA_TRY(cudaEventRecord(c->ev_chunk[7], c->stream));
+    CUDA_TRY(cudaMemcpyAsync(p_hb, c->best.p, sizeof(lms_candidate), cudaMemcpyDeviceToHost,
+                             c->stream));
+    CUDA_TRY(cudaMemcpyAsync(p_scnt, c->bscnt.p, sizeof(unsigned) * K, cudaMemcpyDeviceToHost,
+                             c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    const lms_candidate hb = *p_hb;
+    scnt.assign(p_scnt, p_scnt + K);
+    H = hb.found ? hb.height : INFINITY;
+  }
   std::vector<int32_t> order(K);
   for (int k = 0; k < K; ++k) order[k] = k;
   std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return lb[x] < lb[y]; });
   st->bands = K;
-
-  // ---- seeds: the samples of the bands with the narrowest q-windows at their
-  // centre slope (the bands an LMS line of that slope would come from)
-  std::vector<uint8_t> flag(K + 1, 0);
-  std::vector<int32_t> seed_bands;
-  {
-    std::vector<int32_t> byw(K);
-    for (int k = 0; k < K; ++k) byw[k] = k;
-    std::stable_sort(byw.begin(), byw.end(), [&](int32_t x, int32_t y) { return wq[x] < wq[y]; });
-    for (int e = 0; e < K && e < kSeedBands; ++e)
-      if (std::isfinite(wq[byw[e]])) {
-        flag[byw[e]] = 1;
-        seed_bands.push_back(byw[e]);
-      }
-  }
-  std::memcpy(u_flag1, flag.data(), K);
-  std::copy(seed_bands.begin(), seed_bands.end(), u_seed);
-  CUDA_TRY(cudaMemcpyAsync(c->bflag.p, u_flag1, K, cudaMemcpyHostToDevice, c->stream));
-  CUDA_TRY(cudaMemcpyAsync(c->blist.p, u_seed, sizeof(int32_t) * seed_bands.size(),
-                           cudaMemcpyHostToDevice, c->stream));
-  // the window-edge pairs (usually the optimum itself) and, as a safety net,
-  // up to 64 sampled vertices of the same bands, in one exact launch
-  CUDA_TRY(cudaMemsetAsync(sc + 2, 0, sizeof(unsigned long long), c->stream));
-  lmsb::launch_band_edge_seeds(bf, ba, c->blist.p, (int)seed_bands.size(), c->ranks.p,
-                               c->item_fit.p, seed_cap, sc + 2, c->stream);
-  lmsb::launch_band_seeds(bf, w, c->ranks.p, c->item_fit.p, 0, seed_cap, sc + 2, c->stream);
-  RC_TRY(exact_list(sc + 2, seed_cap, c->ranks.p, c->item_fit.p));
-  CUDA_TRY(cudaEventRecord(c->ev_chunk[7], c->stream));
-  CUDA_TRY(cudaMemcpyAsync(p_hb, c->best.p, sizeof(lms_candidate), cudaMemcpyDeviceToHost,
-                           c->stream));
-  CUDA_TRY(cudaMemcpyAsync(p_scnt, c->bscnt.p, sizeof(unsigned) * K, cudaMemcpyDeviceToHost,
-                           c->stream));
-  CUDA_TRY(cudaStreamSynchronize(c->stream));
-  const lms_candidate hb = *p_hb;
-  const std::vector<unsigned> scnt(p_scnt, p_scnt + K);
-  const double H = hb.found ? hb.height : INFINITY;
   st->seed_height = H;
 
   // ---- collect the vertices of the bands whose bound admits H
@@ -660,6 +840,13 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   CUDA_TRY(cudaMemcpyAsync(c->bflag.p, u_flag2, K, cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(cudaMemcpyAsync(c->blist.p, u_list, sizeof(int32_t) * list.size(),
                            cudaMemcpyHostToDevice, c->stream));
+  if (big && sh && sh->mode == 2 && list.size() > 1) {
+    // the chunk filter reads the admitted bands' sorted keys: rebuild them
+    // (the plan kept only its own slice's, on its own device)
+    if (lmsb::launch_band_bound_big(bf, ba, bg, 0, (int)list.size() - 1, c->blist.p, c->stream) != 0)
+      return set_error(LMS_ERR_CUDA, "large-n band key rebuild failed");
+    st->launches += 4 * (int64_t)((list.size() - 1 + bg.batch - 1) / bg.batch);
+  }
   // slope runs of the flagged bands for the collect pre-test, merged across the
   // smallest gaps down to kMaxRuns
   std::vector<std::pair<int, int>> rr;
@@ -955,7 +1142,9 @@ int ctx_solve_fits(lms_ctx* c, const std::vector<HostFit>& hf, lms_candidate* ou
   for (int64_t f = 0; f < F; ++f) {
     const HostFit& h = hf[f];
     const int64_t span = h.r1 - h.r0;
-    const bool exhaustive = span <= kExhaustive;
+    // a shard of a sharded search decides on the whole pair space, as its plan did
+    const int64_t bspan = c->shard ? c->shard->P1 - c->shard->P0 : span;
+    bool exhaustive = bspan <= kExhaustive;
     // small fits of a batch: the fused per-fit band kernel (lms_band_small.cu),
     // which derives its own magnitudes on the device
     const bool small = c->small_mode != 0 && (F > 1 || c->small_mode == 2) &&
@@ -971,8 +1160,9 @@ int ctx_solve_fits(lms_ctx* c, const std::vector<HostFit>& hf, lms_candidate* ou
       line_stats(c, h.off, h.n, &alo_, &ahi_, &am, &bm);
     }
     if (F == 1 && !exhaustive && !small && h.n <= lmsb::kBandMaxBigN && am < 1e30 && bm < 1e30 &&
-        (c->band_mode == 2 || (c->band_mode == 1 && span >= kBandMinSpan)))
+        (c->band_mode == 2 || (c->band_mode == 1 && bspan >= kBandMinSpan)))
       banded = true;  // slope-band stage instead of seeds + count filter
+    exhaustive = !banded && span <= kExhaustive;
     int64_t s = exhaustive ? span : std::min(kSeedsMax, std::max(kSeedsMin, span / kSeedDivisor));
     s = (banded || small) ? 0 : std::min(s, span);
     lmsb::FitDesc& d = fd[f];
@@ -1009,6 +1199,7 @@ int ctx_solve_fits(lms_ctx* c, const std::vector<HostFit>& hf, lms_candidate* ou
     }
     prefB[F] = rb;
   }
+  if (c->shard && c->shard->mode == 1 && !banded) return LMS_OK;  // plan: no bands
   seed_pref[F] = seeds;
   seg[F] = hf[F - 1].off + hf[F - 1].n;
   st.seed_vertices = seeds;
@@ -1063,7 +1254,13 @@ int ctx_solve_fits(lms_ctx* c, const std::vector<HostFit>& hf, lms_candidate* ou
   }
 
   // ---- band path: one large fit with lines in shared-memory range
-  if (banded) RC_TRY(band_solve(c, hf[0], &st));
+  if (banded) {
+    RC_TRY(band_solve(c, hf[0], &st));
+    if (c->shard && c->shard->mode == 1) {
+      c->stats = st;
+      return LMS_OK;  // plan: the slice's bounds are with the caller
+    }
+  }
 
   // ---- fused band search of the batch's small fits, one CTA each
   if (!small_list.empty()) {
@@ -1767,6 +1964,79 @@ int lms_ctx_solve(lms_ctx* c, int64_t q, int64_t rank_begin, int64_t rank_end,
   if (!c || !out) return set_error(LMS_ERR_INVALID, "null argument");
   std::lock_guard<std::mutex> lk(c->mu);
   return ctx_solve(c, q, rank_begin, rank_end, out);
+}
+
+int lms_ctx_shard_plan(lms_ctx* c, int64_t q, int32_t nshards, int32_t shard, int64_t capacity,
+                       int64_t* nbands, int64_t* band_begin, int64_t* band_end, double* lower_bound,
+                       double* window, float* edge_keys, lms_candidate* seed) {
+  if (!c || !nbands || !band_begin || !band_end || !seed)
+    return set_error(LMS_ERR_INVALID, "null argument");
+  std::memset(seed, 0, sizeof(*seed));
+  if (nshards < 1 || shard < 0 || shard >= nshards)
+    return set_error(LMS_ERR_INVALID, "bad shard %d of %d", shard, nshards);
+  if (capacity > 0 && (!lower_bound || !window || !edge_keys))
+    return set_error(LMS_ERR_INVALID, "null band buffers");
+  std::lock_guard<std::mutex> lk(c->mu);
+  *nbands = *band_begin = *band_end = 0;
+  if (!c->a) return set_error(LMS_ERR_INVALID, "no lines bound to the context");
+  const int64_t n = c->nlines;
+  RC_TRY(check_fit(c, 0, n, q));
+  const int64_t total = n * (n - 1) / 2;
+  ShardSpec sp;
+  sp.mode = 1;
+  sp.P0 = 0;
+  sp.P1 = total;
+  sp.nshards = nshards;
+  sp.shard = shard;
+  sp.cap = capacity;
+  sp.lb_out = lower_bound;
+  sp.wq_out = window;
+  sp.edge_out = edge_keys;
+  c->shard = &sp;
+  lms_candidate dummy;
+  std::vector<HostFit> hf{{0, n, q, 0, total}};
+  const int rc = ctx_solve_fits(c, hf, &dummy);
+  c->shard = nullptr;
+  if (rc != LMS_OK) return rc;
+  *nbands = sp.K;
+  *band_begin = sp.k0;
+  *band_end = sp.k1;
+  *seed = sp.seed_out;
+  return LMS_OK;
+}
+
+int lms_ctx_shard_search(lms_ctx* c, int64_t q, int32_t nshards, int32_t shard, int64_t nbands,
+                         const double* lower_bound, const double* window, const float* edge_keys,
+                         const lms_candidate* seed, lms_candidate* out) {
+  if (!c || !out) return set_error(LMS_ERR_INVALID, "null argument");
+  if (nshards < 1 || shard < 0 || shard >= nshards)
+    return set_error(LMS_ERR_INVALID, "bad shard %d of %d", shard, nshards);
+  if (nbands < 0 || (nbands > 0 && (!lower_bound || !window || !edge_keys)))
+    return set_error(LMS_ERR_INVALID, "null band arrays");
+  std::lock_guard<std::mutex> lk(c->mu);
+  std::memset(out, 0, sizeof(*out));
+  if (!c->a) return set_error(LMS_ERR_INVALID, "no lines bound to the context");
+  const int64_t n = c->nlines;
+  RC_TRY(check_fit(c, 0, n, q));
+  const int64_t total = n * (n - 1) / 2;
+  ShardSpec sp;
+  sp.mode = 2;
+  sp.P0 = 0;
+  sp.P1 = total;
+  sp.nshards = nshards;
+  sp.shard = shard;
+  sp.K_in = nbands;
+  sp.lb_in = lower_bound;
+  sp.wq_in = window;
+  sp.edge_in = edge_keys;
+  if (seed) sp.seed_in = *seed;
+  int64_t r0, r1;
+  share_of(total, nshards, shard, &r0, &r1);
+  c->shard = &sp;
+  std::vector<HostFit> hf{{0, n, q, r0, r1}};
+  const int rc = ctx_solve_fits(c, hf, out);
+  c->shard = nullptr;
+  return rc;
 }
 
 int lms_ctx_solve_batch(lms_ctx* c, const int64_t* offsets, const int64_t* q, int64_t nfits,

@@ -8,6 +8,12 @@ NVLink on the GPU box) and every rank takes the same lexicographic
 (height, i, j) minimum (backend.py:182-187), so the result is bit-identical
 for any world size.
 
+``solve_sharded`` is the band-search form of the same split: the slope-band
+table (one lower bound, window and edge keys per band) is computed in slices,
+one per rank, and exchanged with one more ``all_gather`` before each rank
+searches its partition, so the per-band work is divided as well instead of
+being repeated on every rank.
+
 The combine is expressed over ``torch.distributed`` so the same code runs on
 ``nccl`` (GPU tensors) and ``gloo`` (CPU tensors, used by the CPU tests).
 """
@@ -73,25 +79,94 @@ def solve_distributed(a: np.ndarray, b: np.ndarray, q: int, *, group=None,
                       device=None) -> CandidateRecord | None:
     """Solve this rank's partition and return the global exact minimum.
 
-    ``solve_range(r0, r1)`` defaults to the CUDA engine on this process's GPU
-    (``torch.cuda.current_device()``); tests substitute another exact solver
-    to exercise the partition/combine logic on CPU-only ``gloo`` groups.
+    By default the CUDA engine on this process's GPU
+    (``torch.cuda.current_device()``) runs the sharded band search
+    (``solve_sharded``).  ``solve_range(r0, r1)`` substitutes a per-partition
+    exact solver: tests use the CPU oracle to exercise the partition/combine
+    logic on CPU-only ``gloo`` groups.
     """
     import torch.distributed as dist
 
-    n = int(np.asarray(a).size)
-    total = n * (n - 1) // 2
-    r0, r1 = partition(total, dist.get_world_size(group), dist.get_rank(group))
     if solve_range is None:
         import torch
 
-        from . import _native
-
         dev = torch.cuda.current_device()
         device = device if device is not None else torch.device("cuda", dev)
-
-        def solve_range(lo, hi):  # noqa: E306
-            return record_from_native(_native.min_bracelet(a, b, q, lo, hi, dev))
-
+        ctx = _context(dev)
+        ctx.upload(a, b)
+        return solve_sharded(ctx, q, group=group, device=device)
+    n = int(np.asarray(a).size)
+    total = n * (n - 1) // 2
+    r0, r1 = partition(total, dist.get_world_size(group), dist.get_rank(group))
     rec = solve_range(r0, r1) if r1 > r0 else None
+    return combine(all_gather_records(rec, group=group, device=device))
+
+
+_contexts: dict = {}
+
+
+def _context(device: int):
+    """This process's engine context on `device` (created on first use)."""
+    if device not in _contexts:
+        from . import _native
+
+        _contexts[device] = _native.Context(device)
+    return _contexts[device]
+
+
+def band_slice(nbands: int, world: int, rank: int) -> tuple[int, int]:
+    """Bands [k0, k1) a rank bounds in a sharded plan (ceil split, as the engine's)."""
+    return partition(nbands, world, rank)
+
+
+def exchange_band_table(table: np.ndarray, nbands: int, seed: CandidateRecord | None = None,
+                        group=None, device=None) -> tuple[np.ndarray, CandidateRecord | None]:
+    """All-gather every rank's band-table slice and plan seed in one collective.
+
+    Returns the full (nbands, cols) table and the minimum of the seeds.  Each
+    rank sends one header row (its packed seed record, RECORD_FIELDS wide)
+    followed by its slice, padded to ceil(nbands / world) rows.  Slices are
+    ceil splits of [0, nbands) in rank order (band_slice), so the short or
+    empty slices are the last ones: the gathered slices read in rank order are
+    bands 0 .. nbands-1 followed by padding.
+    """
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    cols = table.shape[1]
+    assert cols == RECORD_FIELDS, "band table rows and records share one row width"
+    per = max(1, -(-nbands // world))
+    mine = torch.zeros((1 + per, cols), dtype=torch.float64)
+    mine[0] = torch.from_numpy(pack(seed))
+    if len(table):
+        mine[1: 1 + len(table)] = torch.from_numpy(np.ascontiguousarray(table))
+    if device is not None:
+        mine = mine.to(device)
+    out = torch.empty((world, 1 + per, cols), dtype=torch.float64, device=mine.device)
+    dist.all_gather_into_tensor(out.view(world * (1 + per), cols), mine, group=group)
+    out = out.cpu().numpy()
+    return out[:, 1:].reshape(world * per, cols)[:nbands].copy(), combine(out[:, 0])
+
+
+def solve_sharded(ctx, q: int, *, group=None, device=None) -> CandidateRecord | None:
+    """Sharded band search of the lines bound to ``ctx`` (this rank's GPU).
+
+    plan (this rank's band slice and seed) -> one all_gather of the band table
+    and seeds -> search of this rank's partition against the full table ->
+    all_gather of the records -> lexicographic minimum.  Same record as one
+    ``ctx.solve`` over the whole pair space.
+    """
+    import torch.distributed as dist
+
+    from ._native import Candidate
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    nbands, _, _, table, seed = ctx.shard_plan(q, world, rank)
+    full, best_seed = table[:0], None
+    if nbands:
+        full, best_seed = exchange_band_table(table, nbands, record_from_native(seed), group=group,
+                                              device=device)
+    rec = record_from_native(ctx.shard_search(q, world, rank, full, Candidate.of(best_seed)))
     return combine(all_gather_records(rec, group=group, device=device))

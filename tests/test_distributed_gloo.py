@@ -78,3 +78,47 @@ def test_pack_roundtrip_and_combine_order():
     rows = np.stack([distributed.pack(r1), distributed.pack(None), distributed.pack(r2)])
     assert distributed.unpack(rows[0]) == r1 and distributed.unpack(rows[1]) is None
     assert distributed.combine(rows) == r2  # equal height: smaller (i, j) wins
+
+
+def _table_worker(rank, world, port, nbands, out_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1510_01041_b200.backend import CandidateRecord
+
+        full = np.arange(nbands * 7, dtype=np.float64).reshape(nbands, 7) * 0.5 - 3.0
+        k0, k1 = distributed.band_slice(nbands, world, rank)
+        seed = None if rank == 0 else CandidateRecord(2.0, 10 - rank, 20, 0.5, -1.0, 1.0)
+        got, best = distributed.exchange_band_table(full[k0:k1], nbands, seed)
+        np.save(f"{out_path}.{rank}.npy", got)
+        np.save(f"{out_path}.{rank}.seed.npy", distributed.pack(best))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,nbands", [(2, 1024), (3, 1024), (3, 2), (2, 5)])
+def test_gloo_band_table_exchange(tmp_path, world, nbands):
+    """The sharded plan's all_gather reassembles every rank's band slice into
+    the full table in band order, including short and empty last slices."""
+    out = str(tmp_path / "tab")
+    mp.start_processes(_table_worker, args=(world, _free_port(), nbands, out), nprocs=world,
+                       start_method="spawn")
+    full = np.arange(nbands * 7, dtype=np.float64).reshape(nbands, 7) * 0.5 - 3.0
+    for r in range(world):
+        assert np.array_equal(np.load(f"{out}.{r}.npy"), full)
+        best = distributed.unpack(np.load(f"{out}.{r}.seed.npy"))
+        assert (best.i, best.j) == (10 - (world - 1), 20)  # equal heights: smallest (i, j)
+
+
+def test_band_table_pack_roundtrip():
+    from paper_1510_01041_b200 import _native
+
+    rng = np.random.default_rng(3)
+    lb = rng.normal(size=9)
+    wq = rng.normal(size=9)
+    edge = rng.normal(size=(9, _native.BAND_EDGE_KEYS)).astype(np.float32)
+    t = _native.pack_band_table(lb, wq, edge)
+    assert t.shape == (9, _native.BAND_TABLE_COLS)
+    l2, w2, e2 = _native.unpack_band_table(t)
+    assert np.array_equal(l2, lb) and np.array_equal(w2, wq) and np.array_equal(e2, edge)

@@ -587,3 +587,89 @@ def test_band_direct_grouping_matches():
         got = record_from_native(d.solve(q, 0, total))
         assert d.stats()["direct_groups"] > 0
         assert got == record_from_native(s.solve(q, 0, total))
+
+
+def _sharded_sequential(ctx, q, world):
+    """Every shard of a world-size `world` sharded search, run one after the
+    other on this GPU, with the band-table exchange done by concatenation
+    (what exchange_band_table's all_gather yields)."""
+    from paper_1510_01041_b200 import distributed
+
+    plans = [ctx.shard_plan(q, world, r) for r in range(world)]
+    K = plans[0][0]
+    assert all(p[0] == K for p in plans)
+    for r, p in enumerate(plans):
+        assert (p[1], p[2]) == (distributed.band_slice(K, world, r) if K else (0, 0))
+    table = np.concatenate([p[3] for p in plans]) if K else plans[0][3]
+    assert len(table) == K
+    seed = distributed.combine(np.stack([distributed.pack(record_from_native(p[4])) for p in plans]))
+    recs = [record_from_native(ctx.shard_search(q, world, r, table, _native.Candidate.of(seed)))
+            for r in range(world)]
+    return K, table, distributed.combine(np.stack([distributed.pack(x) for x in recs]))
+
+
+@pytest.mark.parametrize("n,seed", [(16384, 0), (4096, 3), (20000, 1), (1000, 2)])
+def test_sharded_band_search_matches_single_solve(n, seed):
+    """Sharded search (plan slices -> exchanged band table -> per-shard range
+    search -> combine) gives the single-GPU record for 1, 2, 3, 4 and 8
+    shards; the exchanged table equals the unsharded plan's bit for bit.
+    n = 1,000 is below the band threshold (no table, plain range solves);
+    n = 20,000 takes the large-n path (admitted bands' keys rebuilt per shard)."""
+    pts = workloads.contaminated_line_points(n, seed)
+    a, b = pts[:, 0].copy(), pts[:, 1].copy()
+    q = n // 2 + 1
+    total = n * (n - 1) // 2
+    ctx = _native.Context()
+    ctx.upload(a, b)
+    want = record_from_native(ctx.solve(q, 0, total))
+    K1, table1, got1 = _sharded_sequential(ctx, q, 1)
+    assert got1 == want
+    assert (K1 > 0) == (n >= 4096)
+    for world in (2, 3, 4, 8):
+        K, table, got = _sharded_sequential(ctx, q, world)
+        assert K == K1
+        assert table.tobytes() == table1.tobytes(), world
+        assert got == want, (n, world)
+    # a search on a context that did not run the plan (no reusable samples),
+    # and one after an unrelated solve invalidated it: same shard records
+    if K1:
+        from paper_1510_01041_b200 import distributed
+
+        plans = [ctx.shard_plan(q, 4, r) for r in range(4)]
+        table = np.concatenate([p[3] for p in plans])
+        seed = distributed.combine(np.stack([distributed.pack(record_from_native(p[4]))
+                                             for p in plans]))
+        seed = _native.Candidate.of(seed)
+        warm = [record_from_native(ctx.shard_search(q, 4, r, table, seed)) for r in range(4)]
+        fresh = _native.Context()
+        fresh.upload(a, b)
+        assert [record_from_native(fresh.shard_search(q, 4, r, table, seed))
+                for r in range(4)] == warm
+        ctx.solve(q, 0, total // 2)
+        assert record_from_native(ctx.shard_search(q, 4, 1, table, seed)) == warm[1]
+
+
+def test_sharded_band_search_degenerate_q_and_ties():
+    """q = n (whole-set windows) and a duplicated-x, many-ties input under
+    4 shards: same record as the single solve."""
+    rng = np.random.default_rng(5)
+    n = 6000
+    x = rng.integers(0, 300, n).astype(float)
+    y = np.round(2 * x + rng.integers(-3, 4, n)).astype(float)
+    total = n * (n - 1) // 2
+    ctx = _native.Context()
+    ctx.upload(x, y)
+    for q in (n // 2 + 1, n, 3):
+        want = record_from_native(ctx.solve(q, 0, total))
+        _, _, got = _sharded_sequential(ctx, q, 4)
+        assert got == want, q
+
+
+def test_shard_search_rejects_a_wrong_table():
+    pts = workloads.contaminated_line_points(4096, 0)
+    ctx = _native.Context()
+    ctx.upload(pts[:, 0].copy(), pts[:, 1].copy())
+    K, _, _, table, _ = ctx.shard_plan(2049, 1, 0)
+    assert K > 1
+    with pytest.raises(Exception):
+        ctx.shard_search(2049, 1, 0, table[:-1])
