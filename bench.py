@@ -276,6 +276,13 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # LMSB_DIST_BACKEND=gloo: a functional check of the N > 1 path with several
+    # ranks sharing the visible GPUs (CPU collectives; its timings mean nothing)
+    backend = os.environ.get("LMSB_DIST_BACKEND", "nccl")
+    import torch as _t
+
+    if backend != "nccl" and _t.cuda.device_count() > 0:
+        local %= _t.cuda.device_count()
     import torch
 
     torch.cuda.set_device(local)
@@ -283,7 +290,11 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    coll_dev = torch.device("cuda", local) if backend == "nccl" else None
     from paper_1510_01041_b200 import _native, distributed, solve_lms
     from paper_1510_01041_b200.backend import record_from_native
 
@@ -299,7 +310,7 @@ def run_ours(args):
 
     def step():
         if world > 1:  # sharded band search: band-table all_gather, record all_gather
-            return distributed.solve_sharded(ctx, q, device=torch.device("cuda", local))
+            return distributed.solve_sharded(ctx, q, device=coll_dev)
         return record_from_native(ctx.solve(q, r0, r1))
 
     for _ in range(args.warmup):
@@ -337,7 +348,7 @@ def run_ours(args):
 
     t_max = dev_ms
     if dist:
-        tt = torch.tensor([dev_ms], dtype=torch.float64, device=f"cuda:{local}")
+        tt = torch.tensor([dev_ms], dtype=torch.float64, device=coll_dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_max = float(tt.item())
     ms_per_step = t_max / args.steps
@@ -364,7 +375,7 @@ def run_ours(args):
         e2e_s += time.perf_counter() - t0
         assert fit.coverage == q
     if dist:
-        tt = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local}")
+        tt = torch.tensor([e2e_s], dtype=torch.float64, device=coll_dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_s = float(tt.item())
     e2e_value = max(1, args.steps) * n * total / e2e_s
@@ -380,13 +391,15 @@ def run_ours(args):
     sms = torch.cuda.get_device_properties(local).multi_processor_count
     peak = sms * 4 * sm_mhz * 1e6  # warp instructions / s: 4 schedulers per SM
     inst = prof.get("smsp__inst_executed.sum")
+    pairs = r1 - r0
+    if inst:  # the profile is of the whole-fit launch: scale to this rank's partition
+        inst *= pairs / total
     achieved = inst / (coll_ms / 1e3) if inst and coll_ms > 0 else None
     traffic = None
     if prof.get("dram__bytes_read.sum") is not None:
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
         traffic = (prof["dram__bytes_read.sum"] * scale.get(prof.get("dram__bytes_read.sum.unit"), 1)
                    + prof["dram__bytes_write.sum"] * scale.get(prof.get("dram__bytes_write.sum.unit"), 1))
-    pairs = r1 - r0
     roofline = {
         "bound": "issue",
         "kernel": "band_collect_kernel (fp32 slope-run pre-test of every vertex, exact band of the "

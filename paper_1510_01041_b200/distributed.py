@@ -91,7 +91,8 @@ def solve_distributed(a: np.ndarray, b: np.ndarray, q: int, *, group=None,
         import torch
 
         dev = torch.cuda.current_device()
-        device = device if device is not None else torch.device("cuda", dev)
+        if device is None and dist.get_backend(group) == "nccl":
+            device = torch.device("cuda", dev)  # NCCL collectives take device tensors
         ctx = _context(dev)
         ctx.upload(a, b)
         return solve_sharded(ctx, q, group=group, device=device)
