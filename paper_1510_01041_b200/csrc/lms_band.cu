@@ -70,13 +70,29 @@ namespace {
 #endif
 constexpr int kCollectThreads = 512;
 constexpr unsigned kSeedPerBand = 16;  // sampled vertices per seed band (safety net)
-constexpr int kRun = 32;  // ranks per lane per warp segment (lane-interleaved)
+#ifndef LMSB_COLLECT_RUN
+#define LMSB_COLLECT_RUN 64
+#endif
+constexpr int kRun = LMSB_COLLECT_RUN;  // ranks per lane per warp segment (lane-interleaved)
 constexpr int kSlopeBits = 17;  // within-band slope order bits of a collected key
 
 __device__ __forceinline__ float band_key(double u) {
   // monotone non-decreasing map of the slope to fp32 (clamped, so ordered)
   const float f = (float)u;
   return fminf(fmaxf(f, -FLT_MAX), FLT_MAX);
+}
+
+__device__ __forceinline__ float rcp_approx_ftz(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+__global__ void band_interleave_kernel(const double* __restrict__ a, const double* __restrict__ b,
+                                       int64_t n, double2* __restrict__ ab) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x)
+    ab[k] = make_double2(a[k], b[k]);
 }
 
 // slope and class of vertex (i, j) exactly as _scan_rank_range forms it
@@ -439,8 +455,11 @@ __device__ __forceinline__ void advance_pair(int n, int step, int& i, int& j) {
   }
 }
 
+#ifndef LMSB_COLLECT_MINB
+#define LMSB_COLLECT_MINB 2
+#endif
 template <int kR>
-__global__ void __launch_bounds__(kCollectThreads) band_collect_kernel(
+__global__ void __launch_bounds__(kCollectThreads, LMSB_COLLECT_MINB) band_collect_kernel(
     BandFit bf, const float* __restrict__ bounds, int K, const uint8_t* __restrict__ flag,
     BandRuns runs, uint32_t* __restrict__ out_keys, uint32_t* __restrict__ out_vals, int64_t cap,
     unsigned long long* __restrict__ count) {
@@ -513,6 +532,7 @@ __global__ void __launch_bounds__(kCollectThreads) band_collect_kernel(
     }
   };
 
+  const double2* __restrict__ ab = bf.ab;
   for (int64_t g = warp0; g < nseg; g += nwarps) {
     const int64_t base = g * seg;
     int i0 = 0, j0 = 0;
@@ -525,22 +545,32 @@ __global__ void __launch_bounds__(kCollectThreads) band_collect_kernel(
     int i = __shfl_sync(0xffffffffu, i0, 0);
     int j = __shfl_sync(0xffffffffu, j0, 0);
     advance_pair(n, lane, i, j);
-    double ai = __ldg(bf.a + i), bi = __ldg(bf.b + i);
-    int64_t r = base + lane;
+    double2 li = ab[i];
+    double2 lj = ab[min(j, n - 1)];  // j runs past n only beyond the triangle's end
+    // ranks of this lane still inside the span (all kRun in every full segment)
+    const int64_t left = bf.span - base - lane;
+    const int valid = left <= 0 ? 0 : (left >= (int64_t)32 * kRun ? kRun : (int)((left + 31) / 32));
 #pragma unroll 1
-    for (int e = 0; e < kRun; ++e, r += 32) {
-      bool cand = false;
-      if (r < bf.span) {
-        const double da = __dsub_rn(ai, __ldg(bf.a + j));
-        const double num = __dsub_rn(bi, __ldg(bf.b + j));
-        if (da != 0.0) {
-          // |da| in [1e-30, 2e30] here or cand below: __fdividef is within 2 ulp
-          const float u32 = __fdividef((float)num, (float)da);
-          cand = !(fabsf(u32) <= FLT_MAX) || fabs(da) < 1e-30 || (num != 0.0 && fabs(num) < 1e-30);
+    for (int e = 0; e < kRun; ++e) {
+      // next vertex of this lane, loaded before this one is tested (keeps a
+      // second line load in flight per warp)
+      int i2 = i, j2 = j;
+      advance_pair(n, 32, i2, j2);
+      const double2 lj2 = ab[min(j2, n - 1)];
+      const double2 li2 = i2 != i ? ab[i2] : li;
+      const double da = __dsub_rn(li.x, lj.x);
+      const double num = __dsub_rn(li.y, lj.y);
+      const float da32 = (float)da, num32 = (float)num;
+      // rcp.approx.ftz: |da32| below FLT_MIN (ftz) gives an infinite or NaN
+      // u32 (always passes); |da| <= 2e30 here (band path magnitudes < 1e30),
+      // so the reciprocal stays normal.  Error of u32 <= ~5 * 2^-24 relative
+      // unless num32 is subnormal (passes below) or u32 underflows (absolute
+      // error < 1.2e-38, inside the runs' 1e-37 absolute widening).
+      const float u32 = num32 * rcp_approx_ftz(da32);
+      bool cand = !(fabsf(u32) <= FLT_MAX) | ((fabsf(num32) < 1e-30f) & (num != 0.0));
 #pragma unroll
-          for (int k = 0; k < kR; ++k) cand |= (u32 >= rlo[k]) & (u32 <= rhi[k]);
-        }
-      }
+      for (int k = 0; k < kR; ++k) cand |= (u32 >= rlo[k]) & (u32 <= rhi[k]);
+      cand &= (da != 0.0) & (e < valid);
       const unsigned cm = __ballot_sync(0xffffffffu, cand);
       if (cand) q[qn + __popc(cm & ((1u << lane) - 1u))] = ((uint32_t)i << 16) | (uint32_t)j;
       qn += __popc(cm);
@@ -552,12 +582,10 @@ __global__ void __launch_bounds__(kCollectThreads) band_collect_kernel(
         __syncwarp();
         qn -= 32;
       }
-      const int i_old = i;
-      advance_pair(n, 32, i, j);
-      if (i != i_old) {
-        ai = __ldg(bf.a + i);
-        bi = __ldg(bf.b + i);
-      }
+      i = i2;
+      j = j2;
+      li = li2;
+      lj = lj2;
     }
   }
   if (qn > 0) drain(qn);
@@ -994,10 +1022,16 @@ __global__ void __launch_bounds__(kBigThreads, 1) band_filter_big_kernel(BandFit
     if (ba.lb[band] > H * (1.0 + 0x1p-19)) return;
     all = !boundary_extent(ba.bounds, ba.K, band, &uL, &uR) || !keys_in_range(bf, uL, uR);
   }
-  const double uM = 0.5 * uL + 0.5 * uR;
+  // the chunk's slice: its sorted keys and their centre slope
+  int64_t sl = 0;
+  double uM = 0.0;
+  if (!all) {
+    sl = ba.slice_prefix[lo] + (m0 - ba.start[grp]) / ba.slice;
+    uM = ba.slice_u[sl];
+  }
   double kmin = 0.0, res = 1.0;
   if (!all) {
-    const float* Kg = keys + (int64_t)band * n;
+    const float* Kg = keys + sl * n;
     kmin = (double)Kg[0];
     const double kmax = (double)Kg[n - 1];
     res = fmax((kmax - kmin) / 65535.0, 1e-300) * (1.0 + 0x1p-30);
@@ -1031,6 +1065,34 @@ __global__ void __launch_bounds__(kBigThreads, 1) band_filter_big_kernel(BandFit
     }
     return a;
   };
+  // Exact fp32 positions from the band's sorted keys in global memory (L2:
+  // the admitted bands' rows), searched only inside the bracket the 16-bit
+  // keys give: every key of index < lower16(t - 1) lies below x, every key of
+  // index >= upper16(t + 1) above it (t = x's quantisation step; the one-step
+  // margins absorb the roundings of the quantisation).
+  const float* __restrict__ Kg = keys + sl * n;
+  auto upper_f = [&](double x) {  // first index with key > x (x rounded up to fp32)
+    float xf = (float)x;
+    if ((double)xf < x) xf = nextafterf(xf, INFINITY);
+    int a = lower16(q16((double)xf, false)), b = upper16(q16((double)xf, true));
+    while (a < b) {
+      const int mid = (a + b) >> 1;
+      if (__ldg(Kg + mid) <= xf) a = mid + 1;
+      else b = mid;
+    }
+    return a;
+  };
+  auto lower_f = [&](double x) {  // first index with key >= x (x rounded down to fp32)
+    float xf = (float)x;
+    if ((double)xf > x) xf = nextafterf(xf, -INFINITY);
+    int a = lower16(q16((double)xf, false)), b = upper16(q16((double)xf, true));
+    while (a < b) {
+      const int mid = (a + b) >> 1;
+      if (__ldg(Kg + mid) < xf) a = mid + 1;
+      else b = mid;
+    }
+    return a;
+  };
   for (int64_t s0 = m0; s0 < m1; s0 += kBigThreads) {
     const int64_t s = s0 + tid;
     bool keep = false;
@@ -1048,12 +1110,19 @@ __global__ void __launch_bounds__(kBigThreads, 1) band_filter_big_kernel(BandFit
         const double D = bf.dev * fabs(u - uM) * (1.0 + 0x1p-40);
         const double E = slack_base(bf, fabs(u), uM) + 0x1p-20 * H + 1e-300;
         const double pad = D + E;
-        const int top = upper16(q16(z + H + pad, true));
-        const int bot = lower16(q16(z - H - pad, false));
+        // coarse: 16-bit keys in shared memory (a superset)
+        int top = upper16(q16(z + H + pad, true));
+        int bot = lower16(q16(z - H - pad, false));
         if (top - bot >= q) {
-          const int up_lo = lower16(q16(z - pad, false));
-          const int dn_hi = upper16(q16(z + pad, true));
-          keep = (top - up_lo >= q) || (dn_hi - bot >= q);
+          // exact fp32 ends (the survivors' count kernel and exact select
+          // follow, so this only has to stay a superset)
+          top = upper_f(z + H + pad);
+          bot = lower_f(z - H - pad);
+          if (top - bot >= q) {
+            const int up_lo = lower_f(z - pad);
+            const int dn_hi = upper_f(z + pad);
+            keep = (top - up_lo >= q) || (dn_hi - bot >= q);
+          }
         }
       }
     }
@@ -1169,6 +1238,96 @@ int launch_band_bound_big(const BandFit& bf, const BandArgs& ba, const BandBig& 
   return 0;
 }
 
+__global__ void band_slice_prefix_kernel(const int32_t* __restrict__ list, int nlist,
+                                         const int64_t* __restrict__ start,
+                                         const int64_t* __restrict__ end, int64_t slice,
+                                         int64_t* __restrict__ prefix) {
+  if (threadIdx.x == 0) {
+    int64_t acc = 0;
+    for (int e = 0; e < nlist; ++e) {
+      prefix[e] = acc;
+      const int64_t sz = end[list[e]] - start[list[e]];
+      acc += (sz + slice - 1) / slice;
+    }
+    prefix[nlist] = acc;
+  }
+}
+
+// exact slope of member pair p, or NaN when it is not a banded vertex
+__device__ __forceinline__ double member_slope(const BandFit& bf, uint32_t p) {
+  const int i = p >> 16, j = p & 0xFFFF;
+  double u = 0.0;
+  return classify(bf, bf.a[i], bf.b[i], bf.a[j], bf.b[j], &u) == 1 ? u : __longlong_as_double(
+                                                                            0x7FF8000000000000LL);
+}
+
+__global__ void band_slice_keys_kernel(BandFit bf, BandArgs ba, int64_t nslices_max,
+                                       float* __restrict__ keys, int64_t* __restrict__ seg_b,
+                                       int64_t* __restrict__ seg_e) {
+  const int n = (int)bf.n;
+  const int64_t total = ba.slice_prefix[ba.nlist];
+  for (int64_t s = blockIdx.y; s < nslices_max; s += gridDim.y) {
+    bool live = s < total;
+    double uC = 0.0;
+    if (live) {
+      int lo = 0, hi = ba.nlist - 1;  // listed group of slice s
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (ba.slice_prefix[mid] <= s) lo = mid;
+        else hi = mid - 1;
+      }
+      const int grp = ba.list[lo];
+      const int band = ba.group_band ? ba.group_band[grp] : grp;
+      const int64_t m0 = ba.start[grp] + (s - ba.slice_prefix[lo]) * ba.slice;
+      const int64_t m1 = min(ba.end[grp], m0 + ba.slice);
+      double uL, uR;
+      live = band < ba.K && m1 > m0 && boundary_extent(ba.bounds, ba.K, band, &uL, &uR) &&
+             keys_in_range(bf, uL, uR);  // else the filter keeps every member
+      if (live) {
+        const double uf = member_slope(bf, ba.members[m0]);
+        const double ul = member_slope(bf, ba.members[m1 - 1]);
+        // members of an inner band are banded vertices inside its extent
+        uC = fmin(fmax(0.5 * uf + 0.5 * ul, uL), uR);
+        if (!(uC == uC)) uC = 0.5 * uL + 0.5 * uR;
+      }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      seg_b[s] = s * n;
+      seg_e[s] = live ? s * n + n : s * n;
+      ba.slice_u[s] = uC;
+    }
+    if (!live) continue;
+    float* dst = keys + s * n;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+      dst[k] = (float)__dsub_rn(__dmul_rn(__dsub_rn(__ldg(bf.a + k), bf.c), uC), __ldg(bf.b + k));
+  }
+}
+
+size_t band_slice_sort_temp_bytes(int64_t nslices_max, int64_t n) {
+  size_t bytes = 0;
+  cub::DeviceSegmentedRadixSort::SortKeys(nullptr, bytes, (const float*)nullptr, (float*)nullptr,
+                                          (int)(nslices_max * n), (int)nslices_max,
+                                          (const int64_t*)nullptr, (const int64_t*)nullptr);
+  return bytes;
+}
+
+int launch_band_slices(const BandFit& bf, const BandArgs& ba, int64_t nslices_max, float* keys,
+                       float* store, int64_t* seg_begin, int64_t* seg_end, void* temp,
+                       size_t temp_bytes, cudaStream_t st) {
+  if (nslices_max <= 0) return 0;
+  band_slice_prefix_kernel<<<1, 32, 0, st>>>(ba.list, ba.nlist, ba.start, ba.end, ba.slice,
+                                             ba.slice_prefix);
+  dim3 grid((unsigned)std::min<int64_t>((bf.n + 255) / 256, 64),
+            (unsigned)std::min<int64_t>(nslices_max, 65535));
+  band_slice_keys_kernel<<<grid, 256, 0, st>>>(bf, ba, nslices_max, keys, seg_begin, seg_end);
+  size_t bytes = temp_bytes;
+  if (cub::DeviceSegmentedRadixSort::SortKeys(temp, bytes, keys, store,
+                                              (int)(nslices_max * bf.n), (int)nslices_max,
+                                              seg_begin, seg_end, 0, 32, st) != cudaSuccess)
+    return -1;
+  return 0;
+}
+
 void launch_band_filter_big(const BandFit& bf, const BandArgs& ba, const float* store, int grid,
                             cudaStream_t st) {
   if (grid <= 0) return;
@@ -1228,6 +1387,11 @@ __global__ void __launch_bounds__(1024) band_top_kernel(const double* __restrict
     }
     __syncthreads();
   }
+}
+
+void launch_band_interleave(const double* a, const double* b, int64_t n, double2* ab,
+                            cudaStream_t st) {
+  band_interleave_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 1024), 256, 0, st>>>(a, b, n, ab);
 }
 
 void launch_band_top(const double* wq, int k0, int k1, int K, int T, int32_t* list, uint8_t* flag,

@@ -28,6 +28,7 @@ struct BandFit {
   double c;          // centre of the a-range
   double dev;        // >= max_k |a_k - c|
   double amax, bmax;
+  const double2* ab;  // the lines interleaved (a_k, b_k): one 16-byte load per line
 };
 
 // Device scratch of one banded solve.
@@ -93,6 +94,11 @@ struct BandArgs {
   double* lb;                 // per band lower bound of any vertex height (-inf: unknown)
   double* wq;                 // per band narrowest q-window of the keys at the band centre
   float* edge;                // per band 2 * 5 keys around the ends of that window (optional)
+  // large n (filter): slices of up to `slice` consecutive members of each
+  // listed group, each with its own sorted keys at its own centre slope
+  int64_t slice;              // members per slice (a multiple of chunk)
+  int64_t* slice_prefix;      // nlist + 1: first slice of every listed group
+  double* slice_u;            // per slice: centre slope of its keys
   const lms_candidate* best;  // the fit's current best record (H)
   int64_t* out_ranks;
   int32_t* out_fits;
@@ -128,6 +134,13 @@ size_t band_big_sort_temp_bytes(int nb, int64_t n);
 // when ids (device) is given
 int launch_band_bound_big(const BandFit& bf, const BandArgs& ba, const BandBig& bg, int k0,
                           int k1, const int32_t* ids, cudaStream_t st);
+// large n: sorted keys (store, nslices_max * n) of every slice of the listed
+// groups at the slice's centre slope (midpoint of its first and last member's
+// slopes); slices past the real count are empty segments
+size_t band_slice_sort_temp_bytes(int64_t nslices_max, int64_t n);
+int launch_band_slices(const BandFit& bf, const BandArgs& ba, int64_t nslices_max, float* keys,
+                       float* store, int64_t* seg_begin, int64_t* seg_end, void* temp,
+                       size_t temp_bytes, cudaStream_t st);
 void launch_band_filter_big(const BandFit& bf, const BandArgs& ba, const float* store, int grid,
                             cudaStream_t st);
 
@@ -138,6 +151,9 @@ int launch_band_sample(const BandFit& bf, const BandWork& w, int sms, cudaStream
 // mode 0: grid = bands [ba.band0, ba.band0 + grid) (their lower bounds); mode 1: grid >=
 // chunks of the listed bands
 void launch_band(const BandFit& bf, const BandArgs& ba, int mode, int grid, cudaStream_t st);
+// ab[k] = (a[k], b[k]), k < n (BandFit::ab)
+void launch_band_interleave(const double* a, const double* b, int64_t n, double2* ab,
+                            cudaStream_t st);
 // the T bands of [k0, k1) with the narrowest finite q-windows into list[0 .. T)
 // (-1: none), flagged in flag[0 .. K) (cleared first)
 void launch_band_top(const double* wq, int k0, int k1, int K, int T, int32_t* list, uint8_t* flag,

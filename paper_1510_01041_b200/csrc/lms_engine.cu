@@ -214,6 +214,10 @@ struct lms_ctx {
   DevBuf<int32_t> bfits2;
   DevBuf<int64_t> bchunks;
   DevBuf<float> bbig_keys, bbig_store;
+  DevBuf<float> bslice_keys, bslice_store;
+  DevBuf<int64_t> bslice_seg, bslice_prefix;
+  DevBuf<double> bslice_u;
+  int64_t big_slice = 65536;     // n > 16,384: members per filter slice (LMSB_BIG_SLICE)
   DevBuf<int64_t> bbig_seg;
   DevBuf<int32_t> small_list, dg_i32;
   DevBuf<int64_t> dg_i64;
@@ -230,6 +234,10 @@ struct lms_ctx {
   std::vector<double> h_blb;
   ShardSpec* shard = nullptr;  // set for the duration of a shard plan / search call
   ShardPlanState splan;
+  DevBuf<double2> bab;         // interleaved lines of the last banded fit
+  uint64_t ab_gen = ~0ull;
+  int64_t ab_off = -1, ab_n = -1;
+  const double2* ab_ptr = nullptr;
   uint64_t gen = 0;            // bumped whenever the bound lines change
   int hough_mode = 0;  // 0 none, 1 image pixels, 2 explicit points
   int64_t hough_npts = 0, hough_width = 1;
@@ -256,6 +264,7 @@ int ctx_init(lms_ctx* c, int device) {
   c->band_direct = (bd && std::strcmp(bd, "1") == 0) ? 1 : 0;
   const char* bmul = getenv("LMSB_BIG_MULT");
   if (bmul && atoll(bmul) >= 1) c->big_mult = atoll(bmul);
+  if (const char* bs = getenv("LMSB_BIG_SLICE"); bs && atoll(bs) >= 1) c->big_slice = atoll(bs);
   const char* sm = getenv("LMSB_SMALL");
   c->small_mode = sm ? std::max(0, std::min(2, atoi(sm))) : 1;
   const char* bc = getenv("LMSB_BAND_CHUNK");
@@ -342,6 +351,12 @@ void ctx_release(lms_ctx* c) {
   c->bchunks.release();
   c->bbig_keys.release();
   c->bbig_store.release();
+  c->bslice_keys.release();
+  c->bslice_store.release();
+  c->bslice_seg.release();
+  c->bslice_prefix.release();
+  c->bslice_u.release();
+  c->bab.release();
   c->bbig_seg.release();
   c->small_list.release();
   c->dg_i32.release();
@@ -542,6 +557,18 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   bf.dev = std::max(ahi - bf.c, bf.c - alo) * (1.0 + 0x1p-40) + 1e-300;
   bf.amax = am;
   bf.bmax = bmx;
+  // interleaved copy of the fit's lines for the collect pass (kept while the
+  // bound lines and the fit's offset are unchanged)
+  RC_TRY(c->bab.need(h.n));
+  if (c->ab_gen != c->gen || c->ab_off != h.off || c->ab_n != h.n || c->ab_ptr != c->bab.p) {
+    lmsb::launch_band_interleave(bf.a, bf.b, h.n, c->bab.p, c->stream);
+    st->launches += 1;
+    c->ab_gen = c->gen;
+    c->ab_off = h.off;
+    c->ab_n = h.n;
+    c->ab_ptr = c->bab.p;
+  }
+  bf.ab = c->bab.p;
 
   // [0] valid samples [1] collected [2] seeds [3] band survivors [4] count survivors
   unsigned long long* sc = c->bscal.p;
@@ -622,14 +649,13 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   if (big) {
     constexpr int kBatch = 256;
     RC_TRY(c->bbig_keys.need((int64_t)kBatch * h.n * 2));
-    RC_TRY(c->bbig_store.need((int64_t)K * h.n));
     RC_TRY(c->bbig_seg.need(kBatch + 1));
     RC_TRY(c->btemp.need((int64_t)std::max(lmsb::band_sample_temp_bytes(S),
                                            lmsb::band_big_sort_temp_bytes(kBatch, h.n))));
     bg.batch = kBatch;
     bg.keys = c->bbig_keys.p;
     bg.keys_alt = c->bbig_keys.p + (int64_t)kBatch * h.n;
-    bg.store = c->bbig_store.p;
+    bg.store = nullptr;  // the filter sorts its own slices (launch_band_slices)
     bg.seg = c->bbig_seg.p;
     bg.temp = c->btemp.p;
     bg.temp_bytes = (size_t)c->btemp.cap;
@@ -840,13 +866,6 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   CUDA_TRY(cudaMemcpyAsync(c->bflag.p, u_flag2, K, cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(cudaMemcpyAsync(c->blist.p, u_list, sizeof(int32_t) * list.size(),
                            cudaMemcpyHostToDevice, c->stream));
-  if (big && sh && sh->mode == 2 && list.size() > 1) {
-    // the chunk filter reads the admitted bands' sorted keys: rebuild them
-    // (the plan kept only its own slice's, on its own device)
-    if (lmsb::launch_band_bound_big(bf, ba, bg, 0, (int)list.size() - 1, c->blist.p, c->stream) != 0)
-      return set_error(LMS_ERR_CUDA, "large-n band key rebuild failed");
-    st->launches += 4 * (int64_t)((list.size() - 1 + bg.batch - 1) / bg.batch);
-  }
   // slope runs of the flagged bands for the collect pre-test, merged across the
   // smallest gaps down to kMaxRuns
   std::vector<std::pair<int, int>> rr;
@@ -1067,7 +1086,28 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   CUDA_TRY(cudaMemsetAsync(sc + 3, 0, 2 * sizeof(unsigned long long), c->stream));
   if (m > 0) {
     const int fgrid = (int)(((int64_t)m + ba.chunk - 1) / ba.chunk + ba.nlist);
-    if (big) lmsb::launch_band_filter_big(bf, ba, c->bbig_store.p, fgrid, c->stream);
+    if (big) {
+      // sorted keys per slice of `big_slice` members at the slice's own
+      // centre slope (padding D shrinks with the slice's slope range)
+      const int64_t SB = std::max<int64_t>(ba.chunk, (c->big_slice / ba.chunk) * ba.chunk);
+      const int64_t nsl = (int64_t)m / SB + ba.nlist + 1;
+      RC_TRY(c->bslice_keys.need(nsl * h.n));
+      RC_TRY(c->bslice_store.need(nsl * h.n));
+      RC_TRY(c->bslice_seg.need(2 * nsl));
+      RC_TRY(c->bslice_prefix.need(ba.nlist + 1));
+      RC_TRY(c->bslice_u.need(nsl));
+      RC_TRY(c->btemp.need((int64_t)std::max<size_t>((size_t)c->btemp.cap,
+                                                     lmsb::band_slice_sort_temp_bytes(nsl, h.n))));
+      ba.slice = SB;
+      ba.slice_prefix = c->bslice_prefix.p;
+      ba.slice_u = c->bslice_u.p;
+      if (lmsb::launch_band_slices(bf, ba, nsl, c->bslice_keys.p, c->bslice_store.p,
+                                   c->bslice_seg.p, c->bslice_seg.p + nsl, c->btemp.p,
+                                   (size_t)c->btemp.cap, c->stream) != 0)
+        return set_error(LMS_ERR_CUDA, "large-n slice sort failed");
+      st->launches += 4;
+      lmsb::launch_band_filter_big(bf, ba, c->bslice_store.p, fgrid, c->stream);
+    }
     else lmsb::launch_band(bf, ba, 1, fgrid, c->stream);
     lmsb::BandCount bc{};
     bc.lines = c->blines32.p;
