@@ -87,6 +87,7 @@ typedef struct lms_stats {
   int64_t band_survivors;   /* collected vertices whose band window counts reached q */
   int64_t small_fits;       /* fits of the batch solved by the fused per-fit band kernel */
   int64_t direct_groups;    /* sub-band regions of the direct grouping (0: radix-sort path) */
+  int64_t bands_refined;    /* bands whose coarse bound admitted H and got the exact bound */
 } lms_stats;
 
 /* Library identity and device discovery. */
@@ -180,14 +181,17 @@ int lms_ctx_solve(lms_ctx* ctx, int64_t q, int64_t rank_begin, int64_t rank_end,
  * pair ranks [lo, hi) of the ceil split of [0, n(n-1)/2) (distributed.partition).
  *   1. lms_ctx_shard_plan: every shard samples the whole pair space (the same
  *      samples, band boundaries and K on every shard) and bounds only its slice
- *      [band_begin, band_end) of the K slope bands (ceil split of K): per band
- *      its lower bound, narrowest q-window and LMS_BAND_EDGE_KEYS window-edge
- *      keys, written to the caller's arrays (capacity bands).  *seed is the
+ *      of the K slope bands, bands shard, shard + nshards, shard + 2 nshards,
+ *      ... (*nslice of them; interleaved, so the bands near the optimum slope
+ *      spread over all shards): per band its lower bound, narrowest q-window
+ *      and LMS_BAND_EDGE_KEYS window-edge keys, written in that order to the
+ *      caller's arrays (capacity bands).  *seed is the
  *      best exactly evaluated vertex at the ends of the slice's narrowest
  *      windows (any vertex of the fit; not found if none).  nbands = 0: the
  *      fit is not searched by bands; skip the exchange.
  *   2. the caller all-gathers the slices (NCCL over NVLink) into K-band arrays
- *      and takes the lexicographic minimum of the seeds.
+ *      (band k is entry k / nshards of shard k % nshards's slice) and takes
+ *      the lexicographic minimum of the seeds.
  *   3. lms_ctx_shard_search: starts from that seed (H = its height) and
  *      searches the shard's rank range against the full band table.  *out is
  *      the minimum over the shard's range and the seed (which may lie outside
@@ -197,8 +201,8 @@ int lms_ctx_solve(lms_ctx* ctx, int64_t q, int64_t rank_begin, int64_t rank_end,
  *      the plan's samples and band boundaries. */
 #define LMS_BAND_EDGE_KEYS 10
 int lms_ctx_shard_plan(lms_ctx* ctx, int64_t q, int32_t nshards, int32_t shard, int64_t capacity,
-                       int64_t* nbands, int64_t* band_begin, int64_t* band_end, double* lower_bound,
-                       double* window, float* edge_keys, lms_candidate* seed);
+                       int64_t* nbands, int64_t* nslice, double* lower_bound, double* window,
+                       float* edge_keys, lms_candidate* seed);
 int lms_ctx_shard_search(lms_ctx* ctx, int64_t q, int32_t nshards, int32_t shard, int64_t nbands,
                          const double* lower_bound, const double* window, const float* edge_keys,
                          const lms_candidate* seed, lms_candidate* out);

@@ -80,6 +80,7 @@ class Stats(ctypes.Structure):
         ("band_survivors", ctypes.c_int64),
         ("small_fits", ctypes.c_int64),
         ("direct_groups", ctypes.c_int64),
+        ("bands_refined", ctypes.c_int64),
     ]
 
     def as_dict(self) -> dict:
@@ -151,7 +152,7 @@ SIGNATURES = {
                                                   ctypes.c_int64, _C]),
     "lms_ctx_solve_batch": (ctypes.c_int, [ctypes.c_void_p, _I, _I, ctypes.c_int64, _C]),
     "lms_ctx_shard_plan": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
-                                          ctypes.c_int32, ctypes.c_int64, _I, _I, _I, _D, _D,
+                                          ctypes.c_int32, ctypes.c_int64, _I, _I, _D, _D,
                                           ctypes.POINTER(ctypes.c_float), _C]),
     "lms_ctx_shard_search": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
                                             ctypes.c_int32, ctypes.c_int64, _D, _D,
@@ -392,24 +393,25 @@ class Context:
     def shard_plan(self, q: int, nshards: int, shard: int):
         """Bounds of this shard's slice of the slope bands (lms_ctx_shard_plan).
 
-        Returns ``(K, k0, k1, table, seed)`` with ``table`` a float64 array of
-        shape ``(k1 - k0, BAND_TABLE_COLS)``: lower bound, narrowest q-window
-        and the window-edge keys (fp32, packed two per column); ``seed`` is the
-        best vertex at the ends of the slice's narrowest windows (a Candidate).
+        Returns ``(K, table, seed)``: ``table`` is a float64 array of shape
+        ``(len(range(shard, K, nshards)), BAND_TABLE_COLS)``, one row per band
+        shard, shard + nshards, ... (lower bound, narrowest q-window, then the
+        window-edge keys, fp32 packed two per column); ``seed`` is the best
+        vertex at the ends of the slice's narrowest windows (a Candidate).
         ``K == 0``: the fit is not searched by bands (no exchange needed).
         """
         cap = -(-MAX_BANDS // max(1, int(nshards)))
         lb = np.empty(cap, dtype=np.float64)
         wq = np.empty(cap, dtype=np.float64)
         edge = np.empty((cap, BAND_EDGE_KEYS), dtype=np.float32)
-        K, k0, k1 = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        K, m = ctypes.c_int64(), ctypes.c_int64()
         seed = Candidate()
         check(self._lib.lms_ctx_shard_plan(
-            self._h, int(q), int(nshards), int(shard), cap, ctypes.byref(K), ctypes.byref(k0),
-            ctypes.byref(k1), lb.ctypes.data_as(_D), wq.ctypes.data_as(_D),
+            self._h, int(q), int(nshards), int(shard), cap, ctypes.byref(K), ctypes.byref(m),
+            lb.ctypes.data_as(_D), wq.ctypes.data_as(_D),
             edge.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), ctypes.byref(seed)))
-        m = k1.value - k0.value
-        return K.value, k0.value, k1.value, pack_band_table(lb[:m], wq[:m], edge[:m]), seed
+        m = m.value
+        return K.value, pack_band_table(lb[:m], wq[:m], edge[:m]), seed
 
     def shard_search(self, q: int, nshards: int, shard: int, table, seed=None) -> Candidate:
         """Search this shard's rank range against the full band table (all K

@@ -260,7 +260,8 @@ __global__ void __launch_bounds__(kThreads, 1) band_bound_kernel(BandFit bf, Ban
   using SH = BandShared<kThreads, kItems>;
   extern __shared__ __align__(16) unsigned char band_smem[];
   SH& sh = *reinterpret_cast<SH*>(band_smem);
-  const int band = ba.band0 + (int)blockIdx.x;
+  const int band = ba.band_ids ? ba.band_ids[ba.band0 + (int)blockIdx.x] : ba.band0 + (int)blockIdx.x;
+  if (band < 0) return;
   double uL, uR;
   if (!boundary_extent(ba.bounds, ba.K, band, &uL, &uR) || !keys_in_range(bf, uL, uR)) {
     if (threadIdx.x == 0) {
@@ -289,6 +290,110 @@ __global__ void __launch_bounds__(kThreads, 1) band_bound_kernel(BandFit bf, Ban
     const double e = slack_base(bf, fmax(fabs(uL), fabs(uR)), uM) + 1e-300;
     ba.lb[band] = (w - 2.0 * dmax - 2.0 * e) * (1.0 - 0x1p-40);
     ba.wq[band] = w;
+  }
+}
+
+// Coarse lower bound of every band without sorting: the band's keys binned
+// linearly between their extremes (kCoarseBins bins of width res); with
+// P = prefix counts, a q-window starting in bin b1 ends in a bin >= b2*(b1),
+// the first bin where P[b2 + 1] - P[b1] >= q, so
+//   W_q >= min_b1 (b2*(b1) - b1 - 3) res
+// (one bin width, plus one either side for the roundings of the binning).
+// lb = (that - 2 D_max - 2 E) as in band_bound_kernel; wq = the same
+// estimate (ranks bands for seeding only).  The exact bound (sorted keys)
+// is computed afterwards only for the bands this one cannot dismiss.
+constexpr int kCoarseBins = 49152;
+constexpr int kCoarseThreads = 1024;
+
+__global__ void __launch_bounds__(kCoarseThreads, 1) band_coarse_kernel(BandFit bf, BandArgs ba) {
+  extern __shared__ __align__(16) unsigned char band_smem[];
+  unsigned* P = reinterpret_cast<unsigned*>(band_smem);  // kCoarseBins + 1
+  __shared__ double red[2][kCoarseThreads / 32];
+  __shared__ unsigned wsum[kCoarseThreads / 32];
+  const int band = ba.band_ids ? ba.band_ids[ba.band0 + (int)blockIdx.x] : ba.band0 + (int)blockIdx.x;
+  if (band < 0) return;
+  const int tid = threadIdx.x;
+  double uL, uR;
+  if (!boundary_extent(ba.bounds, ba.K, band, &uL, &uR) || !keys_in_range(bf, uL, uR)) {
+    if (tid == 0) {
+      ba.lb[band] = -INFINITY;
+      ba.wq[band] = INFINITY;
+    }
+    return;
+  }
+  const double uM = 0.5 * uL + 0.5 * uR;
+  const double dmax = bf.dev * fmax(uR - uM, uM - uL) * (1.0 + 0x1p-40);
+  const int n = (int)bf.n, q = (int)bf.q;
+  auto key = [&](int k) {
+    return (float)__dsub_rn(__dmul_rn(__dsub_rn(__ldg(bf.a + k), bf.c), uM), __ldg(bf.b + k));
+  };
+  double lo = INFINITY, hi = -INFINITY;
+  for (int k = tid; k < n; k += kCoarseThreads) {
+    const double v = (double)key(k);
+    lo = fmin(lo, v);
+    hi = fmax(hi, v);
+  }
+  for (int b = tid; b <= kCoarseBins; b += kCoarseThreads) P[b] = 0;
+  lo = block_min<kCoarseThreads>(lo, red[0]);
+  hi = -block_min<kCoarseThreads>(-hi, red[1]);
+  const double res = fmax((hi - lo) / kCoarseBins, 1e-300) * (1.0 + 0x1p-30);
+  __syncthreads();
+  for (int k = tid; k < n; k += kCoarseThreads) {
+    const int b = (int)fmin(fmax(floor(((double)key(k) - lo) / res), 0.0), kCoarseBins - 1.0);
+    atomicAdd(P + b, 1u);
+  }
+  __syncthreads();
+  // exclusive prefix in place: P[b] = keys in bins < b, P[kCoarseBins] = n
+  constexpr int kPer = kCoarseBins / kCoarseThreads;
+  unsigned mine[kPer];
+  unsigned sum = 0;
+#pragma unroll
+  for (int e = 0; e < kPer; ++e) {
+    mine[e] = P[tid * kPer + e];
+    sum += mine[e];
+  }
+  unsigned incl = sum;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const unsigned o = __shfl_up_sync(0xffffffffu, incl, off);
+    if ((tid & 31) >= off) incl += o;
+  }
+  if ((tid & 31) == 31) wsum[tid >> 5] = incl;
+  __syncthreads();
+  unsigned base = incl - sum;
+  for (int w = 0; w < (tid >> 5); ++w) base += wsum[w];
+#pragma unroll
+  for (int e = 0; e < kPer; ++e) {
+    P[tid * kPer + e] = base;
+    base += mine[e];
+  }
+  if (tid == kCoarseThreads - 1) P[kCoarseBins] = base;
+  __syncthreads();
+  // narrowest window in bins, over the non-empty start bins; `est` is the
+  // same window with the keys spread evenly inside each bin (interpolated
+  // end position; ranks bands for seeding, which whole bins cannot)
+  double best = INFINITY, est = INFINITY;
+  for (int b1 = tid; b1 < kCoarseBins; b1 += kCoarseThreads) {
+    const unsigned p1 = P[b1];
+    if (P[b1 + 1] == p1) continue;  // empty bin
+    if (P[kCoarseBins] - p1 < (unsigned)q) continue;
+    int a = b1, z = kCoarseBins - 1;  // first b2 with P[b2 + 1] - p1 >= q
+    while (a < z) {
+      const int mid = (a + z) >> 1;
+      if (P[mid + 1] - p1 >= (unsigned)q) z = mid;
+      else a = mid + 1;
+    }
+    best = fmin(best, (double)(a - b1));
+    const double inb = (double)(p1 + (unsigned)q - P[a]) / (double)(P[a + 1] - P[a]);
+    est = fmin(est, (double)(a - b1) + inb);
+  }
+  best = block_min<kCoarseThreads>(best, red[0]);
+  est = block_min<kCoarseThreads>(est, red[1]);
+  if (tid == 0) {
+    const double w = fmax(best - 3.0, 0.0) * res;
+    const double e = slack_base(bf, fmax(fabs(uL), fabs(uR)), uM) + 1e-300;
+    ba.lb[band] = (w - 2.0 * dmax - 2.0 * e) * (1.0 - 0x1p-40);
+    ba.wq[band] = est < INFINITY ? est * res : INFINITY;
   }
 }
 
@@ -949,6 +1054,7 @@ __global__ void __launch_bounds__(1024) band_wq_kernel(BandFit bf, BandArgs ba, 
   __shared__ double red[32];
   __shared__ int kstar;
   const int band = ids ? ids[band0 + blockIdx.x] : band0 + (int)blockIdx.x;
+  if (band < 0) return;
   const int n = (int)bf.n, q = (int)bf.q;
   double uL, uR;
   if (!boundary_extent(ba.bounds, ba.K, band, &uL, &uR) || !keys_in_range(bf, uL, uR)) {
@@ -989,6 +1095,16 @@ __global__ void __launch_bounds__(1024) band_wq_kernel(BandFit bf, BandArgs ba, 
   }
 }
 
+// members per slice of a group of `cnt` members: at least kMinSlices slices
+// when the group has that many chunks (a rank of a sharded search holds few
+// members per band), at most `smax` members each, whole chunks
+constexpr int kMinSlices = 8;
+__host__ __device__ __forceinline__ int64_t group_slice(int64_t cnt, int64_t chunk, int64_t smax) {
+  int64_t s = (cnt + kMinSlices - 1) / kMinSlices;
+  s = (s + chunk - 1) / chunk * chunk;
+  return s < chunk ? chunk : (s > smax ? smax : s);
+}
+
 constexpr int kBigThreads = 1024;
 
 __global__ void __launch_bounds__(kBigThreads, 1) band_filter_big_kernel(BandFit bf, BandArgs ba,
@@ -1026,7 +1142,8 @@ __global__ void __launch_bounds__(kBigThreads, 1) band_filter_big_kernel(BandFit
   int64_t sl = 0;
   double uM = 0.0;
   if (!all) {
-    sl = ba.slice_prefix[lo] + (m0 - ba.start[grp]) / ba.slice;
+    sl = ba.slice_prefix[lo] +
+         (m0 - ba.start[grp]) / group_slice(ba.end[grp] - ba.start[grp], ba.chunk, ba.slice);
     uM = ba.slice_u[sl];
   }
   double kmin = 0.0, res = 1.0;
@@ -1240,14 +1357,15 @@ int launch_band_bound_big(const BandFit& bf, const BandArgs& ba, const BandBig& 
 
 __global__ void band_slice_prefix_kernel(const int32_t* __restrict__ list, int nlist,
                                          const int64_t* __restrict__ start,
-                                         const int64_t* __restrict__ end, int64_t slice,
-                                         int64_t* __restrict__ prefix) {
+                                         const int64_t* __restrict__ end, int64_t chunk,
+                                         int64_t slice, int64_t* __restrict__ prefix) {
   if (threadIdx.x == 0) {
     int64_t acc = 0;
     for (int e = 0; e < nlist; ++e) {
       prefix[e] = acc;
       const int64_t sz = end[list[e]] - start[list[e]];
-      acc += (sz + slice - 1) / slice;
+      const int64_t sb = group_slice(sz, chunk, slice);
+      acc += (sz + sb - 1) / sb;
     }
     prefix[nlist] = acc;
   }
@@ -1278,8 +1396,9 @@ __global__ void band_slice_keys_kernel(BandFit bf, BandArgs ba, int64_t nslices_
       }
       const int grp = ba.list[lo];
       const int band = ba.group_band ? ba.group_band[grp] : grp;
-      const int64_t m0 = ba.start[grp] + (s - ba.slice_prefix[lo]) * ba.slice;
-      const int64_t m1 = min(ba.end[grp], m0 + ba.slice);
+      const int64_t sb = group_slice(ba.end[grp] - ba.start[grp], ba.chunk, ba.slice);
+      const int64_t m0 = ba.start[grp] + (s - ba.slice_prefix[lo]) * sb;
+      const int64_t m1 = min(ba.end[grp], m0 + sb);
       double uL, uR;
       live = band < ba.K && m1 > m0 && boundary_extent(ba.bounds, ba.K, band, &uL, &uR) &&
              keys_in_range(bf, uL, uR);  // else the filter keeps every member
@@ -1315,8 +1434,8 @@ int launch_band_slices(const BandFit& bf, const BandArgs& ba, int64_t nslices_ma
                        float* store, int64_t* seg_begin, int64_t* seg_end, void* temp,
                        size_t temp_bytes, cudaStream_t st) {
   if (nslices_max <= 0) return 0;
-  band_slice_prefix_kernel<<<1, 32, 0, st>>>(ba.list, ba.nlist, ba.start, ba.end, ba.slice,
-                                             ba.slice_prefix);
+  band_slice_prefix_kernel<<<1, 32, 0, st>>>(ba.list, ba.nlist, ba.start, ba.end, ba.chunk,
+                                             ba.slice, ba.slice_prefix);
   dim3 grid((unsigned)std::min<int64_t>((bf.n + 255) / 256, 64),
             (unsigned)std::min<int64_t>(nslices_max, 65535));
   band_slice_keys_kernel<<<grid, 256, 0, st>>>(bf, ba, nslices_max, keys, seg_begin, seg_end);
@@ -1340,18 +1459,20 @@ void launch_band_filter_big(const BandFit& bf, const BandArgs& ba, const float* 
 }
 
 __global__ void __launch_bounds__(1024) band_top_kernel(const double* __restrict__ wq, int k0,
-                                                       int k1, int K, int T,
-                                                       int32_t* __restrict__ list,
+                                                       int k1, const int32_t* __restrict__ ids,
+                                                       int K, int T, int32_t* __restrict__ list,
                                                        uint8_t* __restrict__ flag) {
   __shared__ double rv[32];
   __shared__ int rk[32];
-  __shared__ int chosen[16];
+  __shared__ int chosen[64];
   for (int k = threadIdx.x; k < K; k += blockDim.x) flag[k] = 0;
   __syncthreads();
   for (int t = 0; t < T; ++t) {
     double v = INFINITY;
     int bk = INT_MAX;
-    for (int k = k0 + (int)threadIdx.x; k < k1; k += blockDim.x) {
+    for (int x0 = k0 + (int)threadIdx.x; x0 < k1; x0 += blockDim.x) {
+      const int k = ids ? ids[x0] : x0;
+      if (k < 0) continue;
       bool taken = false;
       for (int e = 0; e < t; ++e) taken |= chosen[e] == k;
       const double x = wq[k];
@@ -1389,14 +1510,22 @@ __global__ void __launch_bounds__(1024) band_top_kernel(const double* __restrict
   }
 }
 
+void launch_band_coarse(const BandFit& bf, const BandArgs& ba, int grid, cudaStream_t st) {
+  if (grid <= 0) return;
+  constexpr size_t smem = (kCoarseBins + 1) * sizeof(unsigned);
+  static bool done = false;
+  set_smem(band_coarse_kernel, smem, &done);
+  band_coarse_kernel<<<grid, kCoarseThreads, smem, st>>>(bf, ba);
+}
+
 void launch_band_interleave(const double* a, const double* b, int64_t n, double2* ab,
                             cudaStream_t st) {
   band_interleave_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 1024), 256, 0, st>>>(a, b, n, ab);
 }
 
 void launch_band_top(const double* wq, int k0, int k1, int K, int T, int32_t* list, uint8_t* flag,
-                     cudaStream_t st) {
-  band_top_kernel<<<1, 1024, 0, st>>>(wq, k0, k1, K, T < 16 ? T : 16, list, flag);
+                     cudaStream_t st, const int32_t* ids) {
+  band_top_kernel<<<1, 1024, 0, st>>>(wq, k0, k1, ids, K, T < 64 ? T : 64, list, flag);
 }
 
 void launch_band_edge_seeds(const BandFit& bf, const BandArgs& ba, const int32_t* bands, int nb,

@@ -82,6 +82,7 @@ struct BandDirect {
 struct BandArgs {
   int K;
   int band0;                  // bound launch (mode 0): first band, block b bounds band0 + b
+  const int32_t* band_ids;    // optional: block b bounds band_ids[band0 + b] (< 0: none)
   const float* bounds;
   const int64_t* start;
   const int64_t* end;
@@ -151,13 +152,16 @@ int launch_band_sample(const BandFit& bf, const BandWork& w, int sms, cudaStream
 // mode 0: grid = bands [ba.band0, ba.band0 + grid) (their lower bounds); mode 1: grid >=
 // chunks of the listed bands
 void launch_band(const BandFit& bf, const BandArgs& ba, int mode, int grid, cudaStream_t st);
+// coarse (sort-free) lower bounds of bands [ba.band0, ba.band0 + grid): binned keys
+void launch_band_coarse(const BandFit& bf, const BandArgs& ba, int grid, cudaStream_t st);
 // ab[k] = (a[k], b[k]), k < n (BandFit::ab)
 void launch_band_interleave(const double* a, const double* b, int64_t n, double2* ab,
                             cudaStream_t st);
-// the T bands of [k0, k1) with the narrowest finite q-windows into list[0 .. T)
-// (-1: none), flagged in flag[0 .. K) (cleared first)
+// the T bands of [k0, k1) (or of ids[k0 .. k1) when ids is given; entries < 0
+// skipped) with the narrowest finite q-windows into list[0 .. T) (-1: none),
+// flagged in flag[0 .. K) (cleared first); T <= 64
 void launch_band_top(const double* wq, int k0, int k1, int K, int T, int32_t* list, uint8_t* flag,
-                     cudaStream_t st);
+                     cudaStream_t st, const int32_t* ids = nullptr);
 // pairs of lines at the ends of the listed bands' narrowest q-windows
 void launch_band_edge_seeds(const BandFit& bf, const BandArgs& ba, const int32_t* bands, int nb,
                             int64_t* ranks, int32_t* fits, int64_t cap,

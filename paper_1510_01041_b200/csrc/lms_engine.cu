@@ -105,14 +105,15 @@ struct HostFit {
 
 // One shard of a sharded band search (lms_ctx_shard_plan / _search): the
 // band plan (samples, boundaries, seeds) covers the whole pair space
-// [P0, P1); the shard bounds only its slice [k0, k1) of the bands (plan) or
+// [P0, P1); the shard bounds only its slice of the bands (plan: bands
+// shard, shard + nshards, ...) or
 // takes every band's bound from the caller (search) and searches its own
 // rank range.
 struct ShardSpec {
   int mode = 0;          // 1 plan, 2 search
   int64_t P0 = 0, P1 = 0;
   int nshards = 1, shard = 0;
-  int64_t K = 0, k0 = 0, k1 = 0;  // plan: set by band_solve
+  int64_t K = 0, k0 = 0, k1 = 0;  // plan: set by band_solve (k0 = k1 = bands in the slice)
   int64_t cap = 0;                // plan: capacity of the output slice
   double* lb_out = nullptr;
   double* wq_out = nullptr;
@@ -217,7 +218,12 @@ struct lms_ctx {
   DevBuf<float> bslice_keys, bslice_store;
   DevBuf<int64_t> bslice_seg, bslice_prefix;
   DevBuf<double> bslice_u;
+  DevBuf<int32_t> bslice_ids;  // a shard plan's interleaved bands
   int64_t big_slice = 65536;     // n > 16,384: members per filter slice (LMSB_BIG_SLICE)
+  // sort-free band bounds first, exact ones where they cannot dismiss a band
+  // (LMSB_BAND_COARSE: 0 never, 1 always, 2 large n only -- for n <= 16,384
+  // one shared-memory sort per band is cheaper than binning plus a refine)
+  int band_coarse = 2;
   DevBuf<int64_t> bbig_seg;
   DevBuf<int32_t> small_list, dg_i32;
   DevBuf<int64_t> dg_i64;
@@ -265,6 +271,7 @@ int ctx_init(lms_ctx* c, int device) {
   const char* bmul = getenv("LMSB_BIG_MULT");
   if (bmul && atoll(bmul) >= 1) c->big_mult = atoll(bmul);
   if (const char* bs = getenv("LMSB_BIG_SLICE"); bs && atoll(bs) >= 1) c->big_slice = atoll(bs);
+  if (const char* bc0 = getenv("LMSB_BAND_COARSE")) c->band_coarse = std::max(0, std::min(2, atoi(bc0)));
   const char* sm = getenv("LMSB_SMALL");
   c->small_mode = sm ? std::max(0, std::min(2, atoi(sm))) : 1;
   const char* bc = getenv("LMSB_BAND_CHUNK");
@@ -356,6 +363,7 @@ void ctx_release(lms_ctx* c) {
   c->bslice_seg.release();
   c->bslice_prefix.release();
   c->bslice_u.release();
+  c->bslice_ids.release();
   c->bab.release();
   c->bbig_seg.release();
   c->small_list.release();
@@ -511,6 +519,7 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   const int64_t pspan = sh ? sh->P1 - sh->P0 : span;
   // large n: bands of >= 32 n vertices (their keys are sorted in global memory)
   const bool big = h.n > lmsb::kBandMaxN;
+  const bool coarse = c->band_coarse == 1 || (c->band_coarse == 2 && big);
   const int64_t bv = big ? std::max<int64_t>(c->band_vertices, c->big_mult * h.n) : c->band_vertices;
   const int K = (int)std::max<int64_t>(3, std::min<int64_t>(lmsb::kBandMaxK, (pspan + bv - 1) / bv));
   const int64_t S =
@@ -518,7 +527,14 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   // bands bounded here: all, or the shard's slice (plan), or none (search:
   // every band's bound comes from the caller)
   int64_t k0 = 0, k1 = K;
-  if (sh && sh->mode == 1) share_of(K, sh->nshards, sh->shard, &k0, &k1);
+  // plan: the shard's bands are interleaved (k = shard + t * nshards), so the
+  // bands near the optimum slope -- the ones that need exact bounds -- are
+  // spread over all shards
+  std::vector<int32_t> slice_ids;
+  if (sh && sh->mode == 1) {
+    for (int64_t k = sh->shard; k < K; k += sh->nshards) slice_ids.push_back((int32_t)k);
+    k0 = k1 = 0;
+  }
   if (sh && sh->mode == 2) {
     if (sh->K_in != K)
       return set_error(LMS_ERR_INVALID, "shard search: %lld bands given, the plan has %d",
@@ -536,7 +552,7 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   RC_TRY(c->bend.need(K + 1));
   RC_TRY(c->blb.need(K));
   RC_TRY(c->bwq.need(K));
-  RC_TRY(c->blist.need(std::max(K + 1, 16)));
+  RC_TRY(c->blist.need(std::max(K + 1, 128)));
   RC_TRY(c->btemp.need((int64_t)lmsb::band_sample_temp_bytes(S)));
   RC_TRY(c->ranks.need(seed_cap));
   RC_TRY(c->item_fit.need(seed_cap));
@@ -659,15 +675,37 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     bg.seg = c->bbig_seg.p;
     bg.temp = c->btemp.p;
     bg.temp_bytes = (size_t)c->btemp.cap;
-    if (k1 > k0) {
+    if (k1 > k0 && !coarse) {
       if (lmsb::launch_band_bound_big(bf, ba, bg, (int)k0, (int)k1, nullptr, c->stream) != 0)
         return set_error(LMS_ERR_CUDA, "large-n band bound sort failed");
       st->launches += 4 * ((k1 - k0 + kBatch - 1) / kBatch);
     }
-  } else if (k1 > k0) {
+  } else if (k1 > k0 && !coarse) {
     lmsb::launch_band(bf, ba, 0, (int)(k1 - k0), c->stream);
     st->launches += 1;
   }
+  if (k1 > k0 && coarse) {  // sort-free bounds; exact ones only where needed
+    lmsb::launch_band_coarse(bf, ba, (int)(k1 - k0), c->stream);
+    st->launches += 1;
+  }
+  // exact (sorted-key) bounds, window widths and edge keys of `nb` listed bands
+  // (device list; entries < 0 are skipped)
+  auto exact_bounds = [&](const int32_t* d_ids, int nb) -> int {
+    if (nb <= 0) return LMS_OK;
+    lmsb::BandArgs bx = ba;
+    bx.band0 = 0;
+    bx.band_ids = d_ids;
+    if (big) {
+      if (lmsb::launch_band_bound_big(bf, bx, bg, 0, nb, d_ids, c->stream) != 0)
+        return set_error(LMS_ERR_CUDA, "large-n band bound sort failed");
+      st->launches += 4 * ((nb + bg.batch - 1) / bg.batch);
+    } else {
+      lmsb::launch_band(bf, bx, 0, nb, c->stream);
+      st->launches += 1;
+    }
+    CUDA_TRY(cudaGetLastError());
+    return LMS_OK;
+  };
   CUDA_TRY(cudaGetLastError());
   // small readbacks through pinned staging (truly asynchronous copies)
   const size_t pin_rb = ((size_t)K * (2 * sizeof(double) + sizeof(float) + sizeof(unsigned)) +
@@ -687,29 +725,83 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   lms_candidate* p_hb = reinterpret_cast<lms_candidate*>(p_wq + K);
   float* p_bnd = reinterpret_cast<float*>(p_hb + 1);
   unsigned* p_scnt = reinterpret_cast<unsigned*>(p_bnd + K);
+  const int nsl = (int)slice_ids.size();
+  if (nsl > 0) {  // plan: bounds of the shard's interleaved slice
+    RC_TRY(c->bslice_ids.need(nsl));
+    std::memcpy(u_list, slice_ids.data(), sizeof(int32_t) * nsl);  // staging (K + 1 entries)
+    CUDA_TRY(cudaMemcpyAsync(c->bslice_ids.p, u_list, sizeof(int32_t) * nsl,
+                             cudaMemcpyHostToDevice, c->stream));
+    if (coarse) {
+      lmsb::BandArgs bx = ba;
+      bx.band0 = 0;
+      bx.band_ids = c->bslice_ids.p;
+      lmsb::launch_band_coarse(bf, bx, nsl, c->stream);
+      st->launches += 1;
+    } else {
+      RC_TRY(exact_bounds(c->bslice_ids.p, nsl));
+    }
+  }
 
   if (sh && sh->mode == 1) {
     // ---- plan: seeds from the slice's narrowest windows (picked on the
-    // device, no extra round trip), then one readback of the slice's bounds,
-    // the seed record, the boundaries and the sample counts
+    // device), exact bounds of the slice's bands this shard's seed height
+    // cannot dismiss, then one readback of the slice's table, the seed
+    // record, the boundaries and the sample counts
     const int T = std::max(2, (kSeedBands + sh->nshards - 1) / sh->nshards);
-    lmsb::launch_band_top(c->bwq.p, (int)k0, (int)k1, K, T, c->blist.p, c->bflag.p, c->stream);
-    CUDA_TRY(cudaMemsetAsync(sc + 2, 0, sizeof(unsigned long long), c->stream));
-    lmsb::launch_band_edge_seeds(bf, ba, c->blist.p, T, c->ranks.p, c->item_fit.p, seed_cap,
-                                 sc + 2, c->stream);
-    lmsb::launch_band_seeds(bf, w, c->ranks.p, c->item_fit.p, 0, seed_cap, sc + 2, c->stream);
-    RC_TRY(exact_list(sc + 2, seed_cap, c->ranks.p, c->item_fit.p));
-    st->launches += 3;
-    const int64_t m = k1 - k0;
-    if (m > sh->cap)
-      return set_error(LMS_ERR_INVALID, "shard plan: %lld bands exceed the capacity %lld",
-                       (long long)m, (long long)sh->cap);
-    CUDA_TRY(cudaMemcpyAsync(p_lb, c->blb.p + k0, sizeof(double) * m, cudaMemcpyDeviceToHost,
+    const int32_t* d_sl = c->bslice_ids.p;
+    const int32_t* d_seed = c->blist.p;
+    if (nsl > 0) {
+      if (coarse) {
+        // a pool of the narrowest coarse windows gets exact bounds (and edge
+        // keys); the T narrowest exact windows among them seed
+        constexpr int kPool = 64;
+        lmsb::launch_band_top(c->bwq.p, 0, nsl, K, kPool, c->blist.p, c->bflag.p, c->stream, d_sl);
+        RC_TRY(exact_bounds(c->blist.p, kPool));
+        lmsb::launch_band_top(c->bwq.p, 0, kPool, K, T, c->blist.p + kPool, c->bflag.p, c->stream,
+                              c->blist.p);
+        d_seed = c->blist.p + kPool;
+        st->launches += 2;
+      } else {
+        lmsb::launch_band_top(c->bwq.p, 0, nsl, K, T, c->blist.p, c->bflag.p, c->stream, d_sl);
+      }
+      CUDA_TRY(cudaMemsetAsync(sc + 2, 0, sizeof(unsigned long long), c->stream));
+      lmsb::launch_band_edge_seeds(bf, ba, d_seed, T, c->ranks.p, c->item_fit.p, seed_cap, sc + 2,
+                                   c->stream);
+      lmsb::launch_band_seeds(bf, w, c->ranks.p, c->item_fit.p, 0, seed_cap, sc + 2, c->stream);
+      RC_TRY(exact_list(sc + 2, seed_cap, c->ranks.p, c->item_fit.p));
+      st->launches += 3;
+    } else {  // no bands here: only the sample counts
+      CUDA_TRY(cudaMemsetAsync(c->bflag.p, 0, K, c->stream));
+      CUDA_TRY(cudaMemsetAsync(sc + 2, 0, sizeof(unsigned long long), c->stream));
+      lmsb::launch_band_seeds(bf, w, c->ranks.p, c->item_fit.p, 0, 0, sc + 2, c->stream);
+    }
+    if (nsl > sh->cap)
+      return set_error(LMS_ERR_INVALID, "shard plan: %d bands exceed the capacity %lld", nsl,
+                       (long long)sh->cap);
+    if (coarse && nsl > 0) {
+      // the global seed height is never above this shard's, so bands it
+      // cannot dismiss are all the search could need exactly
+      CUDA_TRY(cudaMemcpyAsync(p_hb, c->best.p, sizeof(lms_candidate), cudaMemcpyDeviceToHost,
+                               c->stream));
+      CUDA_TRY(cudaMemcpyAsync(p_lb, c->blb.p, sizeof(double) * K, cudaMemcpyDeviceToHost,
+                               c->stream));
+      CUDA_TRY(cudaStreamSynchronize(c->stream));
+      const double Hs = p_hb->found ? p_hb->height : INFINITY;
+      std::vector<int32_t> cand;
+      for (int32_t k : slice_ids)
+        if (p_lb[k] <= Hs * (1.0 + 0x1p-19) && std::isfinite(p_lb[k])) cand.push_back(k);
+      if (!cand.empty()) {
+        std::copy(cand.begin(), cand.end(), u_list);
+        CUDA_TRY(cudaMemcpyAsync(c->blist.p, u_list, sizeof(int32_t) * cand.size(),
+                                 cudaMemcpyHostToDevice, c->stream));
+        RC_TRY(exact_bounds(c->blist.p, (int)cand.size()));
+      }
+      st->bands_refined = (int64_t)cand.size();
+    }
+    std::vector<float> h_edge((size_t)K * 2 * lmsb::kEdge);
+    CUDA_TRY(cudaMemcpyAsync(p_lb, c->blb.p, sizeof(double) * K, cudaMemcpyDeviceToHost,
                              c->stream));
-    CUDA_TRY(cudaMemcpyAsync(p_wq, c->bwq.p + k0, sizeof(double) * m, cudaMemcpyDeviceToHost,
-                             c->stream));
-    CUDA_TRY(cudaMemcpyAsync(sh->edge_out, c->bedge.p + k0 * 2 * lmsb::kEdge,
-                             sizeof(float) * m * 2 * lmsb::kEdge, cudaMemcpyDeviceToHost,
+    CUDA_TRY(cudaMemcpyAsync(p_wq, c->bwq.p, sizeof(double) * K, cudaMemcpyDeviceToHost,
                              c->stream));
     CUDA_TRY(cudaMemcpyAsync(p_hb, c->best.p, sizeof(lms_candidate), cudaMemcpyDeviceToHost,
                              c->stream));
@@ -717,13 +809,20 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
                              c->stream));
     CUDA_TRY(cudaMemcpyAsync(p_scnt, c->bscnt.p, sizeof(unsigned) * K, cudaMemcpyDeviceToHost,
                              c->stream));
+    CUDA_TRY(cudaMemcpyAsync(h_edge.data(), c->bedge.p, sizeof(float) * h_edge.size(),
+                             cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
-    std::memcpy(sh->lb_out, p_lb, sizeof(double) * m);
-    std::memcpy(sh->wq_out, p_wq, sizeof(double) * m);
-    sh->seed_out = *p_hb;
+    for (int t = 0; t < nsl; ++t) {
+      const int32_t k = slice_ids[t];
+      sh->lb_out[t] = p_lb[k];
+      sh->wq_out[t] = p_wq[k];
+      std::memcpy(sh->edge_out + (size_t)t * 2 * lmsb::kEdge,
+                  h_edge.data() + (size_t)k * 2 * lmsb::kEdge, sizeof(float) * 2 * lmsb::kEdge);
+    }
+    sh->seed_out = nsl > 0 ? *p_hb : lms_candidate{};
     sh->K = K;
-    sh->k0 = k0;
-    sh->k1 = k1;
+    sh->k0 = nsl;  // bands in the slice (shard, shard + nshards, ...)
+    sh->k1 = nsl;
     sp.h_bnd.assign(p_bnd, p_bnd + (K - 1));
     sp.h_scnt.assign(p_scnt, p_scnt + K);
     sp.valid = true;
@@ -808,27 +907,43 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
 
     // ---- seeds: the samples of the bands with the narrowest q-windows at their
     // centre slope (the bands an LMS line of that slope would come from)
+    // (coarse bounds: a pool of the kSeedPool narrowest coarse windows gets
+    // exact bounds, and the kSeedBands narrowest exact windows among them
+    // are picked on the device)
+    constexpr int kSeedPool = 64;
     std::vector<int32_t> seed_bands;
     {
       std::vector<int32_t> byw(K);
       for (int k = 0; k < K; ++k) byw[k] = k;
       std::stable_sort(byw.begin(), byw.end(), [&](int32_t x, int32_t y) { return wq[x] < wq[y]; });
-      for (int e = 0; e < K && e < kSeedBands; ++e)
+      const int take = coarse ? kSeedPool : kSeedBands;
+      for (int e = 0; e < K && e < take; ++e)
         if (std::isfinite(wq[byw[e]])) {
-          flag[byw[e]] = 1;
+          if (!coarse) flag[byw[e]] = 1;
           seed_bands.push_back(byw[e]);
         }
     }
-    std::memcpy(u_flag1, flag.data(), K);
     std::copy(seed_bands.begin(), seed_bands.end(), u_seed);
-    CUDA_TRY(cudaMemcpyAsync(c->bflag.p, u_flag1, K, cudaMemcpyHostToDevice, c->stream));
     CUDA_TRY(cudaMemcpyAsync(c->blist.p, u_seed, sizeof(int32_t) * seed_bands.size(),
                              cudaMemcpyHostToDevice, c->stream));
+    const int32_t* d_seed = c->blist.p;
+    int nseed = (int)seed_bands.size();
+    if (coarse) {
+      RC_TRY(exact_bounds(c->blist.p, nseed));
+      lmsb::launch_band_top(c->bwq.p, 0, nseed, K, kSeedBands, c->blist.p + kSeedPool, c->bflag.p,
+                            c->stream, c->blist.p);
+      d_seed = c->blist.p + kSeedPool;
+      nseed = kSeedBands;
+      st->launches += 1;
+    } else {
+      std::memcpy(u_flag1, flag.data(), K);
+      CUDA_TRY(cudaMemcpyAsync(c->bflag.p, u_flag1, K, cudaMemcpyHostToDevice, c->stream));
+    }
     // the window-edge pairs (usually the optimum itself) and, as a safety net,
     // up to 16 sampled vertices of each of the same bands, in one exact launch
     CUDA_TRY(cudaMemsetAsync(sc + 2, 0, sizeof(unsigned long long), c->stream));
-    lmsb::launch_band_edge_seeds(bf, ba, c->blist.p, (int)seed_bands.size(), c->ranks.p,
-                                 c->item_fit.p, seed_cap, sc + 2, c->stream);
+    lmsb::launch_band_edge_seeds(bf, ba, d_seed, nseed, c->ranks.p, c->item_fit.p, seed_cap,
+                                 sc + 2, c->stream);
     lmsb::launch_band_seeds(bf, w, c->ranks.p, c->item_fit.p, 0, seed_cap, sc + 2, c->stream);
     RC_TRY(exact_list(sc + 2, seed_cap, c->ranks.p, c->item_fit.p));
     CUDA_TRY(cudaEventRecord(c->ev_chunk[7], c->stream));
@@ -840,6 +955,23 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     const lms_candidate hb = *p_hb;
     scnt.assign(p_scnt, p_scnt + K);
     H = hb.found ? hb.height : INFINITY;
+  }
+  if (coarse && !(sh && sh->mode == 2)) {  // (a shard's plan refined its own slice)
+    // the bands the coarse bounds cannot dismiss get their exact bound
+    std::vector<int32_t> cand;
+    for (int k = 0; k < K; ++k)
+      if (lb[k] <= H * (1.0 + 0x1p-19) && std::isfinite(lb[k])) cand.push_back(k);
+    if (!cand.empty()) {
+      std::copy(cand.begin(), cand.end(), u_list);
+      CUDA_TRY(cudaMemcpyAsync(c->blist.p, u_list, sizeof(int32_t) * cand.size(),
+                               cudaMemcpyHostToDevice, c->stream));
+      RC_TRY(exact_bounds(c->blist.p, (int)cand.size()));
+      CUDA_TRY(cudaMemcpyAsync(p_lb, c->blb.p, sizeof(double) * K, cudaMemcpyDeviceToHost,
+                               c->stream));
+      CUDA_TRY(cudaStreamSynchronize(c->stream));
+      for (int32_t k : cand) lb[k] = p_lb[k];
+    }
+    st->bands_refined = (int64_t)cand.size();
   }
   std::vector<int32_t> order(K);
   for (int k = 0; k < K; ++k) order[k] = k;
@@ -1090,7 +1222,8 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
       // sorted keys per slice of `big_slice` members at the slice's own
       // centre slope (padding D shrinks with the slice's slope range)
       const int64_t SB = std::max<int64_t>(ba.chunk, (c->big_slice / ba.chunk) * ba.chunk);
-      const int64_t nsl = (int64_t)m / SB + ba.nlist + 1;
+      // per group at most ceil(cnt / SB) or kMinSlices + 1 slices (group_slice)
+      const int64_t nsl = (int64_t)m / SB + 9 * (int64_t)ba.nlist + 1;
       RC_TRY(c->bslice_keys.need(nsl * h.n));
       RC_TRY(c->bslice_store.need(nsl * h.n));
       RC_TRY(c->bslice_seg.need(2 * nsl));
@@ -2007,9 +2140,9 @@ int lms_ctx_solve(lms_ctx* c, int64_t q, int64_t rank_begin, int64_t rank_end,
 }
 
 int lms_ctx_shard_plan(lms_ctx* c, int64_t q, int32_t nshards, int32_t shard, int64_t capacity,
-                       int64_t* nbands, int64_t* band_begin, int64_t* band_end, double* lower_bound,
+                       int64_t* nbands, int64_t* nslice, double* lower_bound,
                        double* window, float* edge_keys, lms_candidate* seed) {
-  if (!c || !nbands || !band_begin || !band_end || !seed)
+  if (!c || !nbands || !nslice || !seed)
     return set_error(LMS_ERR_INVALID, "null argument");
   std::memset(seed, 0, sizeof(*seed));
   if (nshards < 1 || shard < 0 || shard >= nshards)
@@ -2017,7 +2150,7 @@ int lms_ctx_shard_plan(lms_ctx* c, int64_t q, int32_t nshards, int32_t shard, in
   if (capacity > 0 && (!lower_bound || !window || !edge_keys))
     return set_error(LMS_ERR_INVALID, "null band buffers");
   std::lock_guard<std::mutex> lk(c->mu);
-  *nbands = *band_begin = *band_end = 0;
+  *nbands = *nslice = 0;
   if (!c->a) return set_error(LMS_ERR_INVALID, "no lines bound to the context");
   const int64_t n = c->nlines;
   RC_TRY(check_fit(c, 0, n, q));
@@ -2039,8 +2172,7 @@ int lms_ctx_shard_plan(lms_ctx* c, int64_t q, int32_t nshards, int32_t shard, in
   c->shard = nullptr;
   if (rc != LMS_OK) return rc;
   *nbands = sp.K;
-  *band_begin = sp.k0;
-  *band_end = sp.k1;
+  *nslice = sp.k0;
   *seed = sp.seed_out;
   return LMS_OK;
 }

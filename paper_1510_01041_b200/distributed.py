@@ -115,9 +115,20 @@ def _context(device: int):
     return _contexts[device]
 
 
-def band_slice(nbands: int, world: int, rank: int) -> tuple[int, int]:
-    """Bands [k0, k1) a rank bounds in a sharded plan (ceil split, as the engine's)."""
-    return partition(nbands, world, rank)
+def band_slice(nbands: int, world: int, rank: int) -> range:
+    """Bands a rank bounds in a sharded plan: rank, rank + world, ... (interleaved)."""
+    return range(rank, nbands, world)
+
+
+def interleave_band_table(slices: list, nbands: int) -> np.ndarray:
+    """Full (nbands, cols) table from the ranks' slices (band k = row k // world of
+    rank k % world's slice)."""
+    world = len(slices)
+    cols = slices[0].shape[1] if slices and slices[0].ndim == 2 else 0
+    full = np.empty((nbands, cols), dtype=np.float64)
+    for r, t in enumerate(slices):
+        full[r::world] = t[: len(range(r, nbands, world))]
+    return full
 
 
 def exchange_band_table(table: np.ndarray, nbands: int, seed: CandidateRecord | None = None,
@@ -126,10 +137,8 @@ def exchange_band_table(table: np.ndarray, nbands: int, seed: CandidateRecord | 
 
     Returns the full (nbands, cols) table and the minimum of the seeds.  Each
     rank sends one header row (its packed seed record, RECORD_FIELDS wide)
-    followed by its slice, padded to ceil(nbands / world) rows.  Slices are
-    ceil splits of [0, nbands) in rank order (band_slice), so the short or
-    empty slices are the last ones: the gathered slices read in rank order are
-    bands 0 .. nbands-1 followed by padding.
+    followed by its slice (bands rank, rank + world, ...; band_slice), padded
+    to ceil(nbands / world) rows.
     """
     import torch
     import torch.distributed as dist
@@ -147,7 +156,8 @@ def exchange_band_table(table: np.ndarray, nbands: int, seed: CandidateRecord | 
     out = torch.empty((world, 1 + per, cols), dtype=torch.float64, device=mine.device)
     dist.all_gather_into_tensor(out.view(world * (1 + per), cols), mine, group=group)
     out = out.cpu().numpy()
-    return out[:, 1:].reshape(world * per, cols)[:nbands].copy(), combine(out[:, 0])
+    full = interleave_band_table([out[r, 1:] for r in range(world)], nbands)
+    return full, combine(out[:, 0])
 
 
 def solve_sharded(ctx, q: int, *, group=None, device=None) -> CandidateRecord | None:
@@ -164,7 +174,7 @@ def solve_sharded(ctx, q: int, *, group=None, device=None) -> CandidateRecord | 
 
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    nbands, _, _, table, seed = ctx.shard_plan(q, world, rank)
+    nbands, table, seed = ctx.shard_plan(q, world, rank)
     full, best_seed = table[:0], None
     if nbands:
         full, best_seed = exchange_band_table(table, nbands, record_from_native(seed), group=group,

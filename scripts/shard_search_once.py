@@ -13,8 +13,8 @@ ctx = _native.Context()
 ctx.upload(pts[:, 0], pts[:, 1])
 q = n // 2 + 1
 plans = [ctx.shard_plan(q, R, r) for r in range(R)]
-table = np.concatenate([p[3] for p in plans])
-seed = _native.Candidate.of(distributed.combine(np.stack([distributed.pack(record_from_native(p[4])) for p in plans])))
+table = distributed.interleave_band_table([p[1] for p in plans], plans[0][0])
+seed = _native.Candidate.of(distributed.combine(np.stack([distributed.pack(record_from_native(p[2])) for p in plans])))
 for _ in range(2):
     ctx.shard_search(q, R, 0, table, seed)
 print("launches per search", ctx.stats()["launches"])

@@ -43,9 +43,9 @@ for R in (1, 2, 4, 8):
         ms_p, plan = timed(lambda: ctx.shard_plan(q, R, r))
         plans.append((ms_p, plan))
     K = plans[0][1][0]
-    table = np.concatenate([p[1][3] for p in plans])
+    table = distributed.interleave_band_table([p[1][1] for p in plans], K)
     from paper_1510_01041_b200.backend import record_from_native
-    seed = distributed.combine(np.stack([distributed.pack(record_from_native(p[1][4])) for p in plans]))
+    seed = distributed.combine(np.stack([distributed.pack(record_from_native(p[1][2])) for p in plans]))
     seed = _native.Candidate.of(seed)
     detail = []
     for r in range(R):

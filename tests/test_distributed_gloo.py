@@ -88,9 +88,9 @@ def _table_worker(rank, world, port, nbands, out_path):
         from paper_1510_01041_b200.backend import CandidateRecord
 
         full = np.arange(nbands * 7, dtype=np.float64).reshape(nbands, 7) * 0.5 - 3.0
-        k0, k1 = distributed.band_slice(nbands, world, rank)
+        mine = full[list(distributed.band_slice(nbands, world, rank))]
         seed = None if rank == 0 else CandidateRecord(2.0, 10 - rank, 20, 0.5, -1.0, 1.0)
-        got, best = distributed.exchange_band_table(full[k0:k1], nbands, seed)
+        got, best = distributed.exchange_band_table(mine, nbands, seed)
         np.save(f"{out_path}.{rank}.npy", got)
         np.save(f"{out_path}.{rank}.seed.npy", distributed.pack(best))
     finally:
