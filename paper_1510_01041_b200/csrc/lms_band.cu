@@ -74,7 +74,10 @@ constexpr unsigned kSeedPerBand = 16;  // sampled vertices per seed band (safety
 #define LMSB_COLLECT_RUN 64
 #endif
 constexpr int kRun = LMSB_COLLECT_RUN;  // ranks per lane per warp segment (lane-interleaved)
-constexpr int kSlopeBits = 17;  // within-band slope order bits of a collected key
+#ifndef LMSB_SLOPE_BITS
+#define LMSB_SLOPE_BITS 17
+#endif
+constexpr int kSlopeBits = LMSB_SLOPE_BITS;  // within-band slope order bits of a collected key
 
 __device__ __forceinline__ float band_key(double u) {
   // monotone non-decreasing map of the slope to fp32 (clamped, so ordered)

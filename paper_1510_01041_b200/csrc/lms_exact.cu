@@ -121,6 +121,8 @@ __device__ lms_candidate exact_vertex_t(const double* __restrict__ a,
   const int lane = tid & 31;
   const int warp = tid >> 5;
 
+  if (bound < 0.0) return cand_none();  // (uniform) no height can reach it
+
   // Pass 0: rank counts of v0 in the snapped cut (+ window counts vs bound).
   unsigned lt = 0, le = 0, wu = 0, wd = 0;
   for (int64_t k = tid; k < n; k += kT) {
@@ -236,6 +238,16 @@ __device__ __forceinline__ lms_candidate exact_vertex(const double* __restrict__
   return exact_vertex_t<kExactThreads, false>(a, b, n, q, i, j, u, v0, bound, sm, nullptr);
 }
 
+// Bound for vertex (i, j) against the fit's record bc: a vertex after bc in
+// (i, j) order wins only with a strictly smaller height (backend.py:182-187),
+// so its bound drops to the next double below (a negative bound: nothing to
+// evaluate, heights are >= 0 -- the many exact ties of collinear inputs).
+__device__ __forceinline__ double vertex_bound(const lms_candidate& bc, int64_t i, int64_t j) {
+  if (!bc.found) return INFINITY;
+  const bool after = i > bc.i || (i == bc.i && j > bc.j);
+  return after ? nextafter(bc.height, -INFINITY) : bc.height;
+}
+
 __device__ __forceinline__ bool item_vertex(const ExactArgs& args, int64_t s, int32_t& f,
                                             FitDesc& fd, int64_t& i, int64_t& j, double& u,
                                             double& v0, double& bound) {
@@ -244,18 +256,16 @@ __device__ __forceinline__ bool item_vertex(const ExactArgs& args, int64_t s, in
   const double* a = args.a + fd.off;
   const double* b = args.b + fd.off;
   bound = INFINITY;
-  if (args.bound) {
-    const lms_candidate bc = args.bound[f];
-    if (bc.found) bound = bc.height;
-  }
   if (args.mode == kSrcExplicit) {
     i = args.ii[s];
     j = args.jj[s];
     u = args.uu[s];
     v0 = args.vv ? args.vv[s] : cut_value(u, a[i], b[i]);
+    if (args.bound) bound = vertex_bound(args.bound[f], i, j);
     return true;
   }
   decode_rank(fd.n, args.ranks[s], &i, &j);
+  if (args.bound) bound = vertex_bound(args.bound[f], i, j);
   const double ai = a[i], aj = a[j];
   // _scan_rank_range drops parallel duals and forms u unfused (backend.py:200-204).
   u = __ddiv_rn(__dsub_rn(b[i], b[j]), __dsub_rn(ai, aj));
@@ -297,10 +307,6 @@ __global__ void __launch_bounds__(kExactThreads) exact_kernel(ExactArgs args) {
     const double* a = args.a + fd.off;
     const double* b = args.b + fd.off;
     double bound = INFINITY;
-    if (args.bound) {
-      const lms_candidate bc = args.bound[f];
-      if (bc.found) bound = bc.height;
-    }
     int64_t i, j;
     double u, v0;
     bool valid = true;
@@ -309,8 +315,10 @@ __global__ void __launch_bounds__(kExactThreads) exact_kernel(ExactArgs args) {
       j = args.jj[s];
       u = args.uu[s];
       v0 = args.vv ? args.vv[s] : cut_value(u, a[i], b[i]);
+      if (args.bound) bound = vertex_bound(args.bound[f], i, j);
     } else {
       decode_rank(fd.n, args.ranks[s], &i, &j);
+      if (args.bound) bound = vertex_bound(args.bound[f], i, j);
       const double ai = a[i], aj = a[j];
       // _scan_rank_range drops parallel duals and forms u unfused
       // (backend.py:200-204).

@@ -75,6 +75,7 @@ static __device__ __noinline__ lms_candidate exact_vertex_warp(const double* __r
                                            int64_t i, int64_t j, double u, double v0,
                                            double bound, SelectWarp& sw) {
   const int lane = threadIdx.x & 31;
+  if (bound < 0.0) return cand_none();  // (warp-uniform) no height can reach it
   unsigned lt = 0, le = 0, wu = 0, wd = 0;
   for (int64_t k = lane; k < n; k += 32) {
     const double x = snapped_cut(a, b, k, i, j, u, v0);
