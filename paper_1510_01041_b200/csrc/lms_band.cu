@@ -1108,12 +1108,19 @@ __host__ __device__ __forceinline__ int64_t group_slice(int64_t cnt, int64_t chu
   return s < chunk ? chunk : (s > smax ? smax : s);
 }
 
+// per-slice bin table of the large-n filter: kSliceBins linear bins between
+// the slice's extreme keys, P[0 .. kSliceBins] first key index of each bin
+// (rows padded to a 16-byte multiple for the bulk copy)
+constexpr int kSliceBins = 32768;
+constexpr int64_t kSliceRow = kSliceBins + 4;
+static_assert(kSliceRow == kSliceTableRow, "slice table row (lms_band.cuh)");
 constexpr int kBigThreads = 1024;
 
 __global__ void __launch_bounds__(kBigThreads, 1) band_filter_big_kernel(BandFit bf, BandArgs ba,
                                                                         const float* __restrict__ keys) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  uint16_t* K16 = reinterpret_cast<uint16_t*>(smem_raw);
+  unsigned* P = reinterpret_cast<unsigned*>(smem_raw);  // the slice's bin table
+  __shared__ __align__(8) uint64_t pbar;
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int64_t cidx = blockIdx.x;
@@ -1149,41 +1156,49 @@ __global__ void __launch_bounds__(kBigThreads, 1) band_filter_big_kernel(BandFit
          (m0 - ba.start[grp]) / group_slice(ba.end[grp] - ba.start[grp], ba.chunk, ba.slice);
     uM = ba.slice_u[sl];
   }
+  if (!all) {
+    // the chunk's own lower bound from its slice's narrowest q-window, with
+    // the chunk's slope extent (members are slope-ordered, so a chunk is a
+    // narrow part of its slice)
+    __shared__ double cred[2][kBigThreads / 32];
+    double l = INFINITY, h = -INFINITY;
+    for (int64_t s = m0 + tid; s < m1; s += kBigThreads) {
+      const uint32_t p = ba.members[s];
+      const int64_t i = p >> 16, j = p & 0xFFFF;
+      const double u = __ddiv_rn(__dsub_rn(bf.b[i], bf.b[j]), __dsub_rn(bf.a[i], bf.a[j]));
+      l = fmin(l, u);
+      h = fmax(h, u);
+    }
+    const double cl = block_min<kBigThreads>(l, cred[0]);
+    const double ch = -block_min<kBigThreads>(-h, cred[1]);
+    if (isfinite(cl) && isfinite(ch)) {
+      const double dmax = bf.dev * fmax(ch - uM, uM - cl) * (1.0 + 0x1p-40);
+      const double e = slack_base(bf, fmax(fabs(cl), fabs(ch)), uM) + 0x1p-20 * H + 1e-300;
+      if ((ba.slice_wq[sl] - 2.0 * dmax - 2.0 * e) * (1.0 - 0x1p-40) > H) return;
+    }
+  }
+  // the slice's bin table (launch_band_slices): P[b] = first key index whose
+  // bin is >= b, bins of width res from the slice's smallest key; staged by a
+  // bulk copy
   double kmin = 0.0, res = 1.0;
   if (!all) {
-    const float* Kg = keys + sl * n;
-    kmin = (double)Kg[0];
-    const double kmax = (double)Kg[n - 1];
-    res = fmax((kmax - kmin) / 65535.0, 1e-300) * (1.0 + 0x1p-30);
-    for (int k = tid; k < n; k += kBigThreads) {
-      const double t = floor(((double)Kg[k] - kmin) / res);
-      K16[k] = (uint16_t)fmin(fmax(t, 0.0), 65535.0);
-    }
+    kmin = ba.slice_kmin[sl];
+    res = ba.slice_res[sl];
+    if (tid == 0) mbar_init(&pbar, 1);
     __syncthreads();
+    bulk_stage(P, ba.slice_ptab + sl * kSliceRow, kSliceRow * sizeof(unsigned), &pbar, 0);
   }
   auto q16 = [&](double x, bool up) -> int {
-    // whole quantisation steps around x, one extra step either side for rounding
+    // whole bins around x, one extra either side for rounding
     const double t = floor((x - kmin) / res);
     const double v = up ? t + 1.0 : t - 1.0;
-    return (int)fmin(fmax(v, -1.0), 65536.0);
+    return (int)fmin(fmax(v, -1.0), (double)kSliceBins);
   };
-  auto lower16 = [&](int x) {  // first index with K16 >= x
-    int a = 0, b = n;
-    while (a < b) {
-      const int mid = (a + b) >> 1;
-      if ((int)K16[mid] < x) a = mid + 1;
-      else b = mid;
-    }
-    return a;
+  auto lower16 = [&](int x) {  // first index whose bin is >= x
+    return (int)P[min(max(x, 0), kSliceBins)];
   };
-  auto upper16 = [&](int x) {  // first index with K16 > x
-    int a = 0, b = n;
-    while (a < b) {
-      const int mid = (a + b) >> 1;
-      if ((int)K16[mid] <= x) a = mid + 1;
-      else b = mid;
-    }
-    return a;
+  auto upper16 = [&](int x) {  // first index whose bin is > x
+    return (int)P[min(max(x + 1, 0), kSliceBins)];
   };
   // Exact fp32 positions from the band's sorted keys in global memory (L2:
   // the admitted bands' rows), searched only inside the bracket the 16-bit
@@ -1425,6 +1440,58 @@ __global__ void band_slice_keys_kernel(BandFit bf, BandArgs ba, int64_t nslices_
   }
 }
 
+// narrowest q-window of every live slice's sorted keys (chunk lower bounds)
+__global__ void __launch_bounds__(1024) band_slice_wq_kernel(BandFit bf, BandArgs ba,
+                                                            int64_t nslices_max,
+                                                            const float* __restrict__ store,
+                                                            const int64_t* __restrict__ seg_b,
+                                                            const int64_t* __restrict__ seg_e) {
+  __shared__ double red[32];
+  const int n = (int)bf.n, q = (int)bf.q;
+  for (int64_t s = blockIdx.x; s < nslices_max; s += gridDim.x) {
+    double w = INFINITY;
+    if (seg_e[s] > seg_b[s]) {
+      const float* K = store + s * n;
+      for (int k = threadIdx.x; k + q - 1 < n; k += blockDim.x)
+        w = fmin(w, (double)K[k + q - 1] - (double)K[k]);
+    }
+    w = block_min<1024>(w, red);
+    if (threadIdx.x == 0) ba.slice_wq[s] = w;
+    __syncthreads();
+  }
+}
+
+// bin table of every live slice (band_filter_big_kernel): keys are sorted,
+// so bins are non-decreasing in the key index and P[b] is where bin b starts
+__global__ void __launch_bounds__(1024) band_slice_table_kernel(BandFit bf, BandArgs ba,
+                                                               int64_t nslices_max,
+                                                               const float* __restrict__ store,
+                                                               const int64_t* __restrict__ seg_b,
+                                                               const int64_t* __restrict__ seg_e) {
+  const int n = (int)bf.n;
+  for (int64_t s = blockIdx.x; s < nslices_max; s += gridDim.x) {
+    if (seg_e[s] <= seg_b[s]) continue;
+    const float* K = store + s * n;
+    unsigned* P = ba.slice_ptab + s * kSliceRow;
+    const double kmin = (double)K[0], kmax = (double)K[n - 1];
+    const double res = fmax((kmax - kmin) / kSliceBins, 1e-300) * (1.0 + 0x1p-30);
+    if (threadIdx.x == 0) {
+      ba.slice_kmin[s] = kmin;
+      ba.slice_res[s] = res;
+    }
+    auto bin = [&](int k) {
+      return (int)fmin(fmax(floor(((double)K[k] - kmin) / res), 0.0), kSliceBins - 1.0);
+    };
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+      const int bk = bin(k);
+      const int bp = k > 0 ? bin(k - 1) : -1;
+      for (int b = bp + 1; b <= bk; ++b) P[b] = (unsigned)k;
+      if (k == n - 1)
+        for (int b = bk + 1; b <= kSliceBins; ++b) P[b] = (unsigned)n;
+    }
+  }
+}
+
 size_t band_slice_sort_temp_bytes(int64_t nslices_max, int64_t n) {
   size_t bytes = 0;
   cub::DeviceSegmentedRadixSort::SortKeys(nullptr, bytes, (const float*)nullptr, (float*)nullptr,
@@ -1447,6 +1514,10 @@ int launch_band_slices(const BandFit& bf, const BandArgs& ba, int64_t nslices_ma
                                               (int)(nslices_max * bf.n), (int)nslices_max,
                                               seg_begin, seg_end, 0, 32, st) != cudaSuccess)
     return -1;
+  band_slice_wq_kernel<<<(int)std::min<int64_t>(nslices_max, 4096), 1024, 0, st>>>(
+      bf, ba, nslices_max, store, seg_begin, seg_end);
+  band_slice_table_kernel<<<(int)std::min<int64_t>(nslices_max, 4096), 1024, 0, st>>>(
+      bf, ba, nslices_max, store, seg_begin, seg_end);
   return 0;
 }
 
@@ -1455,9 +1526,9 @@ void launch_band_filter_big(const BandFit& bf, const BandArgs& ba, const float* 
   if (grid <= 0) return;
   band_chunks_kernel<<<1, 32, 0, st>>>(ba.list, ba.nlist, ba.start, ba.end, ba.chunk,
                                        ba.chunk_prefix);
-  const size_t smem = (size_t)bf.n * sizeof(uint16_t);
+  const size_t smem = kSliceRow * sizeof(unsigned);
   static bool done = false;
-  set_smem(band_filter_big_kernel, (size_t)kBandMaxBigN * sizeof(uint16_t), &done);
+  set_smem(band_filter_big_kernel, smem, &done);
   band_filter_big_kernel<<<grid, kBigThreads, smem, st>>>(bf, ba, store);
 }
 

@@ -100,6 +100,10 @@ struct BandArgs {
   int64_t slice;              // members per slice (a multiple of chunk)
   int64_t* slice_prefix;      // nlist + 1: first slice of every listed group
   double* slice_u;            // per slice: centre slope of its keys
+  double* slice_wq;           // per slice: narrowest q-window of its sorted keys
+  double* slice_kmin;         // per slice: smallest key and bin width of its bin table
+  double* slice_res;
+  unsigned* slice_ptab;       // per slice: bin table (band_slice_table_kernel)
   const lms_candidate* best;  // the fit's current best record (H)
   int64_t* out_ranks;
   int32_t* out_fits;
@@ -139,6 +143,7 @@ int launch_band_bound_big(const BandFit& bf, const BandArgs& ba, const BandBig& 
 // groups at the slice's centre slope (midpoint of its first and last member's
 // slopes); slices past the real count are empty segments
 size_t band_slice_sort_temp_bytes(int64_t nslices_max, int64_t n);
+constexpr int64_t kSliceTableRow = 32768 + 4;  // unsigned entries per slice (kSliceRow)
 int launch_band_slices(const BandFit& bf, const BandArgs& ba, int64_t nslices_max, float* keys,
                        float* store, int64_t* seg_begin, int64_t* seg_end, void* temp,
                        size_t temp_bytes, cudaStream_t st);

@@ -219,6 +219,7 @@ struct lms_ctx {
   DevBuf<int64_t> bslice_seg, bslice_prefix;
   DevBuf<double> bslice_u;
   DevBuf<int32_t> bslice_ids;  // a shard plan's interleaved bands
+  DevBuf<unsigned> bslice_ptab;
   int64_t big_slice = 65536;     // n > 16,384: members per filter slice (LMSB_BIG_SLICE)
   // sort-free band bounds first, exact ones where they cannot dismiss a band
   // (LMSB_BAND_COARSE: 0 never, 1 always, 2 large n only -- for n <= 16,384
@@ -364,6 +365,7 @@ void ctx_release(lms_ctx* c) {
   c->bslice_prefix.release();
   c->bslice_u.release();
   c->bslice_ids.release();
+  c->bslice_ptab.release();
   c->bab.release();
   c->bbig_seg.release();
   c->small_list.release();
@@ -1228,12 +1230,17 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
       RC_TRY(c->bslice_store.need(nsl * h.n));
       RC_TRY(c->bslice_seg.need(2 * nsl));
       RC_TRY(c->bslice_prefix.need(ba.nlist + 1));
-      RC_TRY(c->bslice_u.need(nsl));
+      RC_TRY(c->bslice_u.need(4 * nsl));
+      RC_TRY(c->bslice_ptab.need(nsl * lmsb::kSliceTableRow));
       RC_TRY(c->btemp.need((int64_t)std::max<size_t>((size_t)c->btemp.cap,
                                                      lmsb::band_slice_sort_temp_bytes(nsl, h.n))));
       ba.slice = SB;
       ba.slice_prefix = c->bslice_prefix.p;
       ba.slice_u = c->bslice_u.p;
+      ba.slice_wq = c->bslice_u.p + nsl;
+      ba.slice_kmin = c->bslice_u.p + 2 * nsl;
+      ba.slice_res = c->bslice_u.p + 3 * nsl;
+      ba.slice_ptab = c->bslice_ptab.p;
       if (lmsb::launch_band_slices(bf, ba, nsl, c->bslice_keys.p, c->bslice_store.p,
                                    c->bslice_seg.p, c->bslice_seg.p + nsl, c->btemp.p,
                                    (size_t)c->btemp.cap, c->stream) != 0)
