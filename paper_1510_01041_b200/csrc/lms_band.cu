@@ -69,11 +69,13 @@ namespace {
 #define LMSB_RADIX_BITS 4
 #endif
 constexpr int kCollectThreads = 512;
+constexpr int kCollectQueue = 96;  // per-warp queue: < 32 waiting + 64 per step
 constexpr unsigned kSeedPerBand = 16;  // sampled vertices per seed band (safety net)
 #ifndef LMSB_COLLECT_RUN
 #define LMSB_COLLECT_RUN 64
 #endif
 constexpr int kRun = LMSB_COLLECT_RUN;  // ranks per lane per warp segment (lane-interleaved)
+static_assert(kRun % 2 == 0, "the collect step takes two ranks per lane");
 #ifndef LMSB_SLOPE_BITS
 #define LMSB_SLOPE_BITS 17
 #endif
@@ -579,8 +581,8 @@ __global__ void __launch_bounds__(kCollectThreads, LMSB_COLLECT_MINB) band_colle
   }
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int kWarps = kCollectThreads / 32;
-  uint32_t* queue = reinterpret_cast<uint32_t*>(smem_raw);  // [kWarps][64]
-  float* bnd = reinterpret_cast<float*>(queue + kWarps * 64);
+  uint32_t* queue = reinterpret_cast<uint32_t*>(smem_raw);  // [kWarps][kCollectQueue]
+  float* bnd = reinterpret_cast<float*>(queue + kWarps * kCollectQueue);
   uint8_t* fl = reinterpret_cast<uint8_t*>(bnd + K);
   for (int k = threadIdx.x; k < K; k += blockDim.x) {
     if (k < K - 1) bnd[k] = bounds[k];
@@ -588,7 +590,7 @@ __global__ void __launch_bounds__(kCollectThreads, LMSB_COLLECT_MINB) band_colle
   }
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  uint32_t* q = queue + (threadIdx.x >> 5) * 64;
+  uint32_t* q = queue + (threadIdx.x >> 5) * kCollectQueue;
   int qn = 0;
   const int n = (int)bf.n;
   const int64_t seg = 32 * kRun;
@@ -641,6 +643,22 @@ __global__ void __launch_bounds__(kCollectThreads, LMSB_COLLECT_MINB) band_colle
   };
 
   const double2* __restrict__ ab = bf.ab;
+  // fp32 slope pre-test of vertex (i, j) against the runs
+  auto pretest = [&](const double2& li, const double2& lj) {
+    const double da = __dsub_rn(li.x, lj.x);
+    const double num = __dsub_rn(li.y, lj.y);
+    const float da32 = (float)da, num32 = (float)num;
+    // rcp.approx.ftz: |da32| below FLT_MIN (ftz) gives an infinite or NaN
+    // u32 (always passes); |da| <= 2e30 here (band path magnitudes < 1e30),
+    // so the reciprocal stays normal.  Error of u32 <= ~5 * 2^-24 relative
+    // unless num32 is subnormal (passes below) or u32 underflows (absolute
+    // error < 1.2e-38, inside the runs' 1e-37 absolute widening).
+    const float u32 = num32 * rcp_approx_ftz(da32);
+    bool cand = !(fabsf(u32) <= FLT_MAX) | ((fabsf(num32) < 1e-30f) & (num != 0.0));
+#pragma unroll
+    for (int k = 0; k < kR; ++k) cand |= (u32 >= rlo[k]) & (u32 <= rhi[k]);
+    return cand & (da != 0.0);
+  };
   for (int64_t g = warp0; g < nseg; g += nwarps) {
     const int64_t base = g * seg;
     int i0 = 0, j0 = 0;
@@ -654,46 +672,41 @@ __global__ void __launch_bounds__(kCollectThreads, LMSB_COLLECT_MINB) band_colle
     int j = __shfl_sync(0xffffffffu, j0, 0);
     advance_pair(n, lane, i, j);
     double2 li = ab[i];
-    double2 lj = ab[min(j, n - 1)];  // j runs past n only beyond the triangle's end
     // ranks of this lane still inside the span (all kRun in every full segment)
     const int64_t left = bf.span - base - lane;
     const int valid = left <= 0 ? 0 : (left >= (int64_t)32 * kRun ? kRun : (int)((left + 31) / 32));
+    // two vertices per lane per step (ranks r and r + 32): two independent
+    // load -> test chains in flight, one queue update and drain check
 #pragma unroll 1
-    for (int e = 0; e < kRun; ++e) {
-      // next vertex of this lane, loaded before this one is tested (keeps a
-      // second line load in flight per warp)
+    for (int e = 0; e < kRun; e += 2) {
       int i2 = i, j2 = j;
       advance_pair(n, 32, i2, j2);
-      const double2 lj2 = ab[min(j2, n - 1)];
-      const double2 li2 = i2 != i ? ab[i2] : li;
-      const double da = __dsub_rn(li.x, lj.x);
-      const double num = __dsub_rn(li.y, lj.y);
-      const float da32 = (float)da, num32 = (float)num;
-      // rcp.approx.ftz: |da32| below FLT_MIN (ftz) gives an infinite or NaN
-      // u32 (always passes); |da| <= 2e30 here (band path magnitudes < 1e30),
-      // so the reciprocal stays normal.  Error of u32 <= ~5 * 2^-24 relative
-      // unless num32 is subnormal (passes below) or u32 underflows (absolute
-      // error < 1.2e-38, inside the runs' 1e-37 absolute widening).
-      const float u32 = num32 * rcp_approx_ftz(da32);
-      bool cand = !(fabsf(u32) <= FLT_MAX) | ((fabsf(num32) < 1e-30f) & (num != 0.0));
-#pragma unroll
-      for (int k = 0; k < kR; ++k) cand |= (u32 >= rlo[k]) & (u32 <= rhi[k]);
-      cand &= (da != 0.0) & (e < valid);
-      const unsigned cm = __ballot_sync(0xffffffffu, cand);
-      if (cand) q[qn + __popc(cm & ((1u << lane) - 1u))] = ((uint32_t)i << 16) | (uint32_t)j;
-      qn += __popc(cm);
+      // j runs past n only beyond the triangle's end
+      const double2 ljA = ab[min(j, n - 1)];
+      const double2 ljB = ab[min(j2, n - 1)];
+      const double2 liB = i2 != i ? ab[i2] : li;
+      const bool cA = pretest(li, ljA) & (e < valid);
+      const bool cB = pretest(liB, ljB) & (e + 1 < valid);
+      const unsigned mA = __ballot_sync(0xffffffffu, cA);
+      const unsigned mB = __ballot_sync(0xffffffffu, cB);
+      const unsigned below = (1u << lane) - 1u;
+      if (cA) q[qn + __popc(mA & below)] = ((uint32_t)i << 16) | (uint32_t)j;
+      const int qB = qn + __popc(mA);
+      if (cB) q[qB + __popc(mB & below)] = ((uint32_t)i2 << 16) | (uint32_t)j2;
+      qn = qB + __popc(mB);
       __syncwarp();
-      if (qn >= 32) {
+      while (qn >= 32) {
         drain(32);
         __syncwarp();
-        if (lane < qn - 32) q[lane] = q[32 + lane];
+        for (int t = lane; t < qn - 32; t += 32) q[t] = q[32 + t];
         __syncwarp();
         qn -= 32;
       }
       i = i2;
       j = j2;
-      li = li2;
-      lj = lj2;
+      li = liB;
+      advance_pair(n, 32, i, j);
+      if (i != i2) li = ab[i];
     }
   }
   if (qn > 0) drain(qn);
@@ -1318,7 +1331,8 @@ size_t band_group_temp_bytes(int64_t m) {
 }
 
 size_t band_collect_smem(int K) {
-  return (size_t)(kCollectThreads / 32) * 64 * sizeof(uint32_t) + (size_t)K * (sizeof(float) + sizeof(uint8_t)) + 16;
+  return (size_t)(kCollectThreads / 32) * kCollectQueue * sizeof(uint32_t) +
+         (size_t)K * (sizeof(float) + sizeof(uint8_t)) + 16;
 }
 
 int launch_band_sample(const BandFit& bf, const BandWork& w, int sms, cudaStream_t st) {
