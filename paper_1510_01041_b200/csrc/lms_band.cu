@@ -69,13 +69,18 @@ namespace {
 #define LMSB_RADIX_BITS 4
 #endif
 constexpr int kCollectThreads = 512;
-constexpr int kCollectQueue = 96;  // per-warp queue: < 32 waiting + 64 per step
+#ifndef LMSB_COLLECT_STEP
+#define LMSB_COLLECT_STEP 4
+#endif
+constexpr int kCollectStep = LMSB_COLLECT_STEP;  // vertices per lane per collect step
+constexpr int kCollectQueue = 32 * (kCollectStep + 1);  // per-warp queue: < 32 waiting + a step
 constexpr unsigned kSeedPerBand = 16;  // sampled vertices per seed band (safety net)
 #ifndef LMSB_COLLECT_RUN
 #define LMSB_COLLECT_RUN 64
 #endif
 constexpr int kRun = LMSB_COLLECT_RUN;  // ranks per lane per warp segment (lane-interleaved)
-static_assert(kRun % 2 == 0, "the collect step takes two ranks per lane");
+static_assert(kRun % kCollectStep == 0, "whole collect steps per segment");
+
 #ifndef LMSB_SLOPE_BITS
 #define LMSB_SLOPE_BITS 17
 #endif
@@ -675,25 +680,36 @@ __global__ void __launch_bounds__(kCollectThreads, LMSB_COLLECT_MINB) band_colle
     // ranks of this lane still inside the span (all kRun in every full segment)
     const int64_t left = bf.span - base - lane;
     const int valid = left <= 0 ? 0 : (left >= (int64_t)32 * kRun ? kRun : (int)((left + 31) / 32));
-    // two vertices per lane per step (ranks r and r + 32): two independent
-    // load -> test chains in flight, one queue update and drain check
+    // kCollectStep vertices per lane per step (ranks r, r + 32, ...):
+    // independent load -> test chains in flight, one drain check per step
 #pragma unroll 1
-    for (int e = 0; e < kRun; e += 2) {
-      int i2 = i, j2 = j;
-      advance_pair(n, 32, i2, j2);
-      // j runs past n only beyond the triangle's end
-      const double2 ljA = ab[min(j, n - 1)];
-      const double2 ljB = ab[min(j2, n - 1)];
-      const double2 liB = i2 != i ? ab[i2] : li;
-      const bool cA = pretest(li, ljA) & (e < valid);
-      const bool cB = pretest(liB, ljB) & (e + 1 < valid);
-      const unsigned mA = __ballot_sync(0xffffffffu, cA);
-      const unsigned mB = __ballot_sync(0xffffffffu, cB);
+    for (int e = 0; e < kRun; e += kCollectStep) {
+      int vi[kCollectStep], vj[kCollectStep];
+      double2 vli[kCollectStep];
+      bool vc[kCollectStep];
+      vi[0] = i;
+      vj[0] = j;
+      vli[0] = li;
+#pragma unroll
+      for (int t = 1; t < kCollectStep; ++t) {
+        vi[t] = vi[t - 1];
+        vj[t] = vj[t - 1];
+        advance_pair(n, 32, vi[t], vj[t]);
+      }
+#pragma unroll
+      for (int t = 0; t < kCollectStep; ++t) {
+        // j runs past n only beyond the triangle's end
+        const double2 lj = ab[min(vj[t], n - 1)];
+        if (t > 0) vli[t] = vi[t] != vi[t - 1] ? ab[vi[t]] : vli[t - 1];
+        vc[t] = pretest(vli[t], lj) & (e + t < valid);
+      }
       const unsigned below = (1u << lane) - 1u;
-      if (cA) q[qn + __popc(mA & below)] = ((uint32_t)i << 16) | (uint32_t)j;
-      const int qB = qn + __popc(mA);
-      if (cB) q[qB + __popc(mB & below)] = ((uint32_t)i2 << 16) | (uint32_t)j2;
-      qn = qB + __popc(mB);
+#pragma unroll
+      for (int t = 0; t < kCollectStep; ++t) {
+        const unsigned m = __ballot_sync(0xffffffffu, vc[t]);
+        if (vc[t]) q[qn + __popc(m & below)] = ((uint32_t)vi[t] << 16) | (uint32_t)vj[t];
+        qn += __popc(m);
+      }
       __syncwarp();
       while (qn >= 32) {
         drain(32);
@@ -702,11 +718,12 @@ __global__ void __launch_bounds__(kCollectThreads, LMSB_COLLECT_MINB) band_colle
         __syncwarp();
         qn -= 32;
       }
-      i = i2;
-      j = j2;
-      li = liB;
+      i = vi[kCollectStep - 1];
+      j = vj[kCollectStep - 1];
+      li = vli[kCollectStep - 1];
+      const int i_last = i;
       advance_pair(n, 32, i, j);
-      if (i != i2) li = ab[i];
+      if (i != i_last) li = ab[i];
     }
   }
   if (qn > 0) drain(qn);
