@@ -65,6 +65,9 @@ constexpr int kSeedBands = 2;
 constexpr int kEdge = 5;  // keys kept around each end of a band's narrowest q-window
 constexpr int kSlots = 16;    // admitted bands whose keys are resident at once
 constexpr int kSegRun = 16;   // ranks per lane per warp segment
+constexpr int kSweepStep = 4; // vertices per lane per sweep step
+constexpr int kQueue = 32 * (kSweepStep + 1);  // per-warp queues: < 32 waiting + a step
+static_assert(kSegRun % kSweepStep == 0, "whole sweep steps per segment");
 constexpr int kMaxRuns = 8;   // slope runs tested before a band lookup
 
 template <int kItems>
@@ -73,6 +76,7 @@ struct SmallShared {
   using SampleSort = cub::BlockRadixSort<float, kThreads, kSampleItems, int>;
   alignas(16) double a[kNP];
   alignas(16) double b[kNP];
+  double2 ab[kNP];            // (a_k, b_k) interleaved for the sweeps
   float4 l2[kNP / 2];         // (A_k, A_k+1, -B_k, -B_k+1) for the packed counts
   float rlo[kMaxRuns], rhi[kMaxRuns];  // slope runs of the current sweep (widened)
   int nruns;
@@ -104,8 +108,8 @@ struct SmallShared {
   int admitted[kMaxBands];
   int nadmitted;
   int seed_band[kSeedBands];
-  uint32_t queue[kWarps][64];   // fp32-count queue
-  uint32_t squeue[kWarps][64];  // in-run vertices awaiting band lookup + padded counts
+  uint32_t queue[kWarps][kQueue];   // fp32-count queue
+  uint32_t squeue[kWarps][kQueue];  // in-run vertices awaiting band lookup + padded counts
   lms_candidate wbest[kWarps];
   double red[2][kWarps];
   unsigned long long hbits;  // current bound H (bits of a non-negative double)
@@ -113,6 +117,12 @@ struct SmallShared {
   int nvalid;
   unsigned long long cnt[12];  // admitted bands, queued, exact, sweeps; phase cycles (stats)
 };
+
+__device__ __forceinline__ float rcp_approx_ftz(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
 
 __device__ __forceinline__ float band_key(double u) {
   const float f = (float)u;
@@ -265,6 +275,7 @@ __global__ void __launch_bounds__(kThreads, LMSB_SMALL_MINB) small_fit_kernel(Sm
       sh.a[k] = ak;
       sh.b[k] = bk;
     }
+    sh.ab[k] = make_double2(ak, bk);
     alo = fmin(alo, ak);
     ahi = fmax(ahi, ak);
     am = fmax(am, fabs(ak));
@@ -619,7 +630,7 @@ __global__ void __launch_bounds__(kThreads, LMSB_SMALL_MINB) small_fit_kernel(Sm
         const double ai = sh.a[vi], bi = sh.b[vi];
         const double da = __dsub_rn(ai, sh.a[vj]);
         const double num = __dsub_rn(bi, sh.b[vj]);
-        const float u32 = __fdividef((float)num, (float)da);
+        const float u32 = (float)num * rcp_approx_ftz((float)da);  // as the sweep formed it
         const int band = band_of(sh.bounds, K - 1, u32);
         int slot_id = sh.band_slot[band];
         if (slot_id < 0) {
@@ -684,67 +695,73 @@ __global__ void __launch_bounds__(kThreads, LMSB_SMALL_MINB) small_fit_kernel(Sm
         j = __shfl_sync(0xffffffffu, (int)j64, 0);
         advance_pair(n, lane, i, j);
       }
-      int64_t r = base + lane;
-      constexpr int kIlp = 1;  // independent vertices per lane in flight
+      // ranks of this lane inside the fit (all kSegRun except in the last segment)
+      const int64_t left = P - base - lane;
+      const int valid = left <= 0 ? 0 : (left >= (int64_t)32 * kSegRun ? kSegRun : (int)((left + 31) / 32));
+      // kSweepStep vertices per lane per step (ranks r, r + 32, ...): independent
+      // load -> test chains, one queue update and drain check per step
 #pragma unroll 1
-      for (int e0 = 0; e0 < kSegRun; e0 += kIlp) {
-        int vi[kIlp], vj[kIlp];
-        bool cand[kIlp];  // straight to the fp32 counts
-        int slot_id[kIlp];  // padded window counts against a resident band
+      for (int e0 = 0; e0 < kSegRun; e0 += kSweepStep) {
+        int vi[kSweepStep], vj[kSweepStep];
+        bool cand[kSweepStep];  // straight to the fp32 counts
+        bool inr[kSweepStep];   // padded window counts against a resident band
+        vi[0] = i;
+        vj[0] = j;
 #pragma unroll
-        for (int t = 0; t < kIlp; ++t) {
-          vi[t] = i;
-          vj[t] = j;
-          advance_pair(n, 32, i, j);
+        for (int t = 1; t < kSweepStep; ++t) {
+          vi[t] = vi[t - 1];
+          vj[t] = vj[t - 1];
+          advance_pair(n, 32, vi[t], vj[t]);
         }
 #pragma unroll
-        for (int t = 0; t < kIlp; ++t) {
-          cand[t] = false;
-          slot_id[t] = -1;
-          if (r + 32 * t < P) {
-            const double da = __dsub_rn(sh.a[vi[t]], sh.a[vj[t]]);
-            const double num = __dsub_rn(sh.b[vi[t]], sh.b[vj[t]]);
-            if (da != 0.0) {
-              // |da| in [1e-30, 2e30]: __fdividef is within 2 ulp
-              const float u32 = __fdividef((float)num, (float)da);
-              if (huge || !(fabsf(u32) * amf < 1e29f) || fabs(da) < 1e-30 ||
-                  (num != 0.0 && fabs(num) < 1e-30)) {
-                cand[t] = first;  // beyond the fp32 tests (first sweep only)
-              } else {
-                bool inrun = false;  // runs from shared memory (broadcast reads)
+        for (int t = 0; t < kSweepStep; ++t) {
+          // j runs past n only beyond the triangle's end
+          const double2 li = sh.ab[vi[t]], lj = sh.ab[min(vj[t], n - 1)];
+          const double da = __dsub_rn(li.x, lj.x);
+          const double num = __dsub_rn(li.y, lj.y);
+          const float da32 = (float)da, num32 = (float)num;
+          // rcp.approx.ftz: a subnormal da32 gives an infinite / NaN u32,
+          // caught by the magnitude test below (the band path of lms_band.cu
+          // uses the same pre-test)
+          const float u32 = num32 * rcp_approx_ftz(da32);
+          const bool live = (da != 0.0) & (e0 + t < valid);
+          const bool beyond = huge | !(fabsf(u32) * amf < 1e29f) |
+                              ((fabsf(num32) < 1e-30f) & (num != 0.0));
+          bool inrun = false;  // runs from shared memory (broadcast reads)
 #pragma unroll 1
-                for (int w = 0; w < nruns; ++w) inrun |= (u32 >= sh.rlo[w]) & (u32 <= sh.rhi[w]);
-                slot_id[t] = inrun ? 0 : -1;  // band lookup deferred to search()
-              }
-            }
-          }
+          for (int w = 0; w < nruns; ++w) inrun |= (u32 >= sh.rlo[w]) & (u32 <= sh.rhi[w]);
+          cand[t] = live & beyond & first;  // beyond the fp32 tests (first sweep only)
+          inr[t] = live & !beyond & inrun;  // band lookup deferred to search()
         }
-        r += 32 * kIlp;
-#pragma unroll 1
-        for (int t = 0; t < kIlp; ++t) {
+        const unsigned below = (1u << lane) - 1u;
+#pragma unroll
+        for (int t = 0; t < kSweepStep; ++t) {
           const uint32_t packed = ((uint32_t)vi[t] << 16) | (uint32_t)vj[t];
-          const unsigned sm_ = __ballot_sync(0xffffffffu, slot_id[t] >= 0);
-          if (slot_id[t] >= 0) sq[sn + __popc(sm_ & ((1u << lane) - 1u))] = packed;
+          const unsigned sm_ = __ballot_sync(0xffffffffu, inr[t]);
+          if (inr[t]) sq[sn + __popc(sm_ & below)] = packed;
           sn += __popc(sm_);
           const unsigned cm = __ballot_sync(0xffffffffu, cand[t]);
-          if (cand[t]) qw[qn + __popc(cm & ((1u << lane) - 1u))] = packed;
+          if (cand[t]) qw[qn + __popc(cm & below)] = packed;
           qn += __popc(cm);
-          __syncwarp();
-          if (qn >= 32) {
-            drain(32);
-            __syncwarp();
-            if (lane < qn - 32) qw[lane] = qw[32 + lane];
-            __syncwarp();
-            qn -= 32;
-          }
-          if (sn >= 32) {
-            search(32);
-            __syncwarp();
-            if (lane < sn - 32) sq[lane] = sq[32 + lane];
-            __syncwarp();
-            sn -= 32;
-          }
         }
+        __syncwarp();
+        while (qn >= 32) {
+          drain(32);
+          __syncwarp();
+          for (int t = lane; t < qn - 32; t += 32) qw[t] = qw[32 + t];
+          __syncwarp();
+          qn -= 32;
+        }
+        while (sn >= 32) {
+          search(32);  // may append to qw (and drain it)
+          __syncwarp();
+          for (int t = lane; t < sn - 32; t += 32) sq[t] = sq[32 + t];
+          __syncwarp();
+          sn -= 32;
+        }
+        i = vi[kSweepStep - 1];
+        j = vj[kSweepStep - 1];
+        advance_pair(n, 32, i, j);
       }
     }
     if (sn > 0) {
