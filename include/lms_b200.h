@@ -102,6 +102,16 @@ const char* lms_last_error(void);
 int lms_min_bracelet_f64(const double* a, const double* b, int64_t n, int64_t q,
                          int64_t rank_begin, int64_t rank_end, int device, lms_candidate* out);
 
+/* solve_lms on the device end to end (solver.py:115-140): the exact search
+ * over all n(n-1)/2 pairs, then the fit's contact set -- indices k with
+ * |x_k u - y_k - v_low| <= tol or |x_k u - y_k - v_high| <= tol, anchors
+ * snapped, tol = GEOM_EPS max(1, max_k |x_k u - y_k|) -- ascending in
+ * contacts[0 .. min(*ncontacts, cap)).  *ncontacts may exceed cap (call again
+ * with more room).  Replaces the SequentialBackend.minimum_bracelet call plus
+ * the numpy tail of solve_lms (solver.py:115-140, backend.py:234-247). */
+int lms_solve_fit_f64(const double* a, const double* b, int64_t n, int64_t q, int device,
+                      lms_candidate* out, int64_t* contacts, int64_t cap, int64_t* ncontacts);
+
 /* The materialised two-kernel flow over the same rank range (materialize=True,
  * backend.py:210-231): K1 writes every non-parallel pair's (i, j, u), K2
  * evaluates every one exactly; no pruning filter.  Same record as

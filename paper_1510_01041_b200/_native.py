@@ -127,6 +127,8 @@ SIGNATURES = {
     "lms_min_bracelet_materialized_f64": (ctypes.c_int, [_D, _D, ctypes.c_int64, ctypes.c_int64,
                                                          ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
                                                          _C]),
+    "lms_solve_fit_f64": (ctypes.c_int, [_D, _D, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, _C, _I,
+                                         ctypes.c_int64, _I]),
     "lms_batched_f64": (ctypes.c_int, [_D, _D, _I, _I, ctypes.c_int64, ctypes.c_int, _C]),
     "lms_primal_brute_f64": (ctypes.c_int, [_D, _D, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, _C]),
     "lms_hough_vote_u8": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
@@ -236,6 +238,24 @@ def min_bracelet(a, b, q: int, rank_begin: int, rank_end: int, device: int = 0) 
     check(lib.lms_min_bracelet_f64(_dp(a), _dp(b), a.size, int(q), int(rank_begin), int(rank_end),
                                    int(device), ctypes.byref(out)))
     return out
+
+
+def solve_fit(a, b, q: int, device: int = 0):
+    """lms_solve_fit_f64: the record over all pairs and its contact indices
+    (ascending int64 array), or (not-found record, empty array)."""
+    lib = _lib_ready()
+    a = _f64(a)
+    b = _f64(b)
+    out = Candidate()
+    cap = 64
+    while True:
+        idx = np.empty(cap, dtype=np.int64)
+        cnt = ctypes.c_int64()
+        check(lib.lms_solve_fit_f64(_dp(a), _dp(b), a.size, int(q), int(device), ctypes.byref(out),
+                                    idx.ctypes.data_as(_I), cap, ctypes.byref(cnt)))
+        if cnt.value <= cap:
+            return out, idx[: cnt.value]
+        cap = int(cnt.value)
 
 
 def min_bracelet_materialized(a, b, q: int, rank_begin: int, rank_end: int,

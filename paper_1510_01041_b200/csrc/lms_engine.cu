@@ -2002,6 +2002,35 @@ int lms_min_bracelet_f64(const double* a, const double* b, int64_t n, int64_t q,
   return ctx_solve(c, q, rank_begin, rank_end, out);
 }
 
+int lms_solve_fit_f64(const double* a, const double* b, int64_t n, int64_t q, int device,
+                      lms_candidate* out, int64_t* contacts, int64_t cap, int64_t* ncontacts) {
+  if (!out || !ncontacts || (cap > 0 && !contacts)) return set_error(LMS_ERR_INVALID, "null output");
+  *ncontacts = 0;
+  lms_ctx* c = nullptr;
+  RC_TRY(shared_ctx(device, &c));
+  std::lock_guard<std::mutex> lk(c->mu);
+  RC_TRY(ctx_upload(c, a, b, n));
+  RC_TRY(ctx_solve(c, q, 0, n * (n - 1) / 2, out));
+  if (!out->found) return LMS_OK;
+  RC_TRY(c->ii.need(std::max<int64_t>(n, 1)));
+  RC_TRY(c->counters.need(2));
+  lmsb::launch_contacts(c->a, c->b, n, *out, c->counters.p, c->ii.p, n, c->sms, c->stream);
+  CUDA_TRY(cudaGetLastError());
+  unsigned long long cnt = 0;
+  CUDA_TRY(cudaMemcpyAsync(&cnt, c->counters.p + 1, sizeof(cnt), cudaMemcpyDeviceToHost,
+                           c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  const int64_t m = std::min<int64_t>((int64_t)cnt, cap);
+  if (m > 0) {
+    std::vector<int64_t> h((size_t)cnt);
+    CUDA_TRY(cudaMemcpy(h.data(), c->ii.p, sizeof(int64_t) * cnt, cudaMemcpyDeviceToHost));
+    std::sort(h.begin(), h.end());
+    std::copy(h.begin(), h.begin() + m, contacts);
+  }
+  *ncontacts = (int64_t)cnt;
+  return LMS_OK;
+}
+
 int lms_min_bracelet_materialized_f64(const double* a, const double* b, int64_t n, int64_t q,
                                       int64_t rank_begin, int64_t rank_end, int device,
                                       lms_candidate* out) {

@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <algorithm>
 #include <cstdint>
 
 #include "lms_common.cuh"
@@ -551,6 +552,62 @@ void launch_materialize(const double* a, const double* b, int64_t n, int64_t r0,
 void launch_gen_seeds(const FitDesc* fits, const int64_t* seed_prefix, int64_t nfits,
                       int64_t* ranks, int32_t* fit_of, cudaStream_t stream) {
   gen_seeds_kernel<<<512, 256, 0, stream>>>(fits, seed_prefix, nfits, ranks, fit_of);
+}
+
+// ---------------------------------------------------------------- contacts
+// solve_lms tail (solver.py:122-140): cut_k = x_k u - y_k (numpy's unfused
+// product and difference), the anchor pair snapped to x_i u - y_i;
+// tol = GEOM_EPS * max(1, max_k |cut_k|); k touches when |cut_k - v_low| <= tol
+// or |cut_k - v_high| <= tol.
+namespace {
+__device__ __forceinline__ double contact_cut(const double* a, const double* b, int64_t k,
+                                              int64_t i, int64_t j, double u) {
+  const int64_t kk = (k == j) ? i : k;
+  return cut_value(u, a[kk], b[kk]);
+}
+
+__global__ void contacts_max_kernel(const double* __restrict__ a, const double* __restrict__ b,
+                                    int64_t n, int64_t i, int64_t j, double u,
+                                    unsigned long long* __restrict__ maxbits) {
+  unsigned long long m = 0;  // bits of non-negative doubles order like their values
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long v = (unsigned long long)__double_as_longlong(fabs(contact_cut(a, b, k, i, j, u)));
+    m = v > m ? v : m;
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const unsigned long long o = __shfl_xor_sync(0xffffffffu, m, off);
+    m = o > m ? o : m;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMax(maxbits, m);
+}
+
+__global__ void contacts_collect_kernel(const double* __restrict__ a, const double* __restrict__ b,
+                                        int64_t n, int64_t i, int64_t j, double u, double v_low,
+                                        double v_high, const unsigned long long* __restrict__ maxbits,
+                                        int64_t* __restrict__ out, int64_t cap,
+                                        unsigned long long* __restrict__ count) {
+  const double tol = 1e-9 * fmax(1.0, __longlong_as_double((long long)*maxbits));
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const double x = contact_cut(a, b, k, i, j, u);
+    if (fabs(__dsub_rn(x, v_low)) <= tol || fabs(__dsub_rn(x, v_high)) <= tol) {
+      const unsigned long long pos = atomicAdd(count, 1ull);
+      if ((int64_t)pos < cap) out[pos] = k;
+    }
+  }
+}
+}  // namespace
+
+void launch_contacts(const double* a, const double* b, int64_t n, const lms_candidate& rec,
+                     unsigned long long* scratch, int64_t* out, int64_t cap, int sms,
+                     cudaStream_t st) {
+  cudaMemsetAsync(scratch, 0, 2 * sizeof(unsigned long long), st);
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)sms * 8);
+  contacts_max_kernel<<<grid, 256, 0, st>>>(a, b, n, rec.i, rec.j, rec.u, scratch);
+  contacts_collect_kernel<<<grid, 256, 0, st>>>(a, b, n, rec.i, rec.j, rec.u, rec.v_low,
+                                                rec.v_high, scratch, out, cap, scratch + 1);
 }
 
 }  // namespace lmsb

@@ -82,6 +82,12 @@ void launch_materialize(const double* a, const double* b, int64_t n, int64_t r0,
                         int64_t* ii, int64_t* jj, double* uu, unsigned long long* nout, int sms,
                         cudaStream_t stream);
 
+// Contact set of a fit's record (solve_lms tail, solver.py:122-140): indices
+// appended in any order to out (at most cap); scratch[1] = total count.
+void launch_contacts(const double* a, const double* b, int64_t n, const lms_candidate& rec,
+                     unsigned long long* scratch, int64_t* out, int64_t cap, int sms,
+                     cudaStream_t st);
+
 // Seeds: stratified vertex samples per fit; seed_prefix[f] = first seed of fit f.
 void launch_gen_seeds(const FitDesc* fits, const int64_t* seed_prefix, int64_t nfits,
                       int64_t* ranks, int32_t* fit_of, cudaStream_t stream);

@@ -76,6 +76,22 @@ def solve_lms(points, q: int | None = None, *, backend: str = "seq", workers: in
     """
     x, y, q = validated(points, q)
     engine = _backend.get_backend(backend, workers)
+    if backend == "seq" and not materialize:
+        # one device call: the search and the contact set (solver.py:115-140)
+        from . import _native
+
+        cand, contacts = _native.solve_fit(x, y, q)
+        rec = _backend.record_from_native(cand)
+        if rec is None:
+            raise DegenerateInputError("no candidate slab found")
+        half = (rec.v_high - rec.v_low) * 0.5
+        return LmsFit(
+            line=LineEq(slope=rec.u, intercept=-(rec.v_low + rec.v_high) * 0.5),
+            lms_value=half * half,
+            slab_height=rec.v_high - rec.v_low,
+            coverage=q,
+            contact_indices=tuple(contacts.tolist()),
+        )
     rec = engine.minimum_bracelet(x, y, q, materialize=materialize)
     if rec is None:
         raise DegenerateInputError("no candidate slab found")

@@ -672,3 +672,25 @@ def test_shard_search_rejects_a_wrong_table():
     assert K > 1
     with pytest.raises(Exception):
         ctx.shard_search(2049, 1, 0, table[:-1])
+
+
+def test_device_contacts_match_host_tail():
+    """solve_lms's one-call device path (search + contact set on the GPU,
+    lms_solve_fit_f64) equals the record through the backend followed by the
+    numpy tail (fit_from_record, solver.py:122-140): exact fits with hundreds
+    of contacts (the contact buffer regrows), noisy fits, duplicates."""
+    from paper_1510_01041_b200.solver import fit_from_record, validated
+
+    cases = [workloads.config1_points(0), workloads.config1_points(3),
+             workloads.contaminated_line_points(3000, 1)]
+    rng = np.random.default_rng(8)
+    x = rng.integers(0, 40, 500).astype(float)
+    cases.append(np.column_stack([x, 3 * x - 7]))  # every point on one line, duplicates
+    cases.append(np.column_stack([rng.normal(0, 1e6, 400), rng.normal(0, 1e-3, 400)]))
+    for pts in cases:
+        xx, yy, q = validated(pts, None)
+        got = lms.solve_lms(pts)
+        rec = lms.get_backend("seq").minimum_bracelet(xx, yy, q)
+        want = fit_from_record(xx, yy, q, rec)
+        assert got == want
+    assert len(lms.solve_lms(cases[3]).contact_indices) == 500
