@@ -105,6 +105,20 @@ __global__ void band_interleave_kernel(const double* __restrict__ a, const doubl
     ab[k] = make_double2(a[k], b[k]);
 }
 
+// Members per filter chunk of a group of `cnt` members: `chunk`, or (adaptive,
+// when that gives fewer) an even split into min(kMinChunks, cnt / kMinChunkMembers) chunks,
+// so a group with few members (one rank's share of a band in a sharded
+// search) still gets chunks of a narrow slope range.
+constexpr int64_t kMinChunks = 4;
+constexpr int64_t kMinChunkMembers = 2048;
+__host__ __device__ __forceinline__ int64_t chunk_size(int64_t cnt, int64_t chunk, bool adaptive) {
+  if (!adaptive || cnt <= 0) return chunk;
+  const int64_t nc = (cnt + chunk - 1) / chunk;
+  int64_t want = (cnt + kMinChunkMembers - 1) / kMinChunkMembers;
+  want = want < kMinChunks ? want : kMinChunks;
+  return nc >= want ? chunk : (cnt + want - 1) / want;
+}
+
 // slope and class of vertex (i, j) exactly as _scan_rank_range forms it
 // (backend.py:200-205): 0 never a window (a_i == a_j or non-finite u),
 // 1 banded, 2 beyond the fp32 key range (always passed to the exact stage)
@@ -429,8 +443,9 @@ __global__ void __launch_bounds__(kThreads, 1) band_filter_kernel(BandFit bf, Ba
   }
   const int grp = ba.list[lo];
   const int band = ba.group_band ? ba.group_band[grp] : grp;
-  const int64_t m0 = ba.start[grp] + (cidx - ba.chunk_prefix[lo]) * ba.chunk;
-  const int64_t m1 = min(ba.end[grp], m0 + ba.chunk);
+  const int64_t cs = chunk_size(ba.end[grp] - ba.start[grp], ba.chunk, true);
+  const int64_t m0 = ba.start[grp] + (cidx - ba.chunk_prefix[lo]) * cs;
+  const int64_t m1 = min(ba.end[grp], m0 + cs);
   if (m1 <= m0) return;
   double H = INFINITY;
   {
@@ -509,14 +524,15 @@ __global__ void __launch_bounds__(kThreads, 1) band_filter_kernel(BandFit bf, Ba
 // chunk_prefix[e] = first chunk of listed band e (single block; nlist small)
 __global__ void band_chunks_kernel(const int32_t* __restrict__ list, int nlist,
                                    const int64_t* __restrict__ start,
-                                   const int64_t* __restrict__ end, int64_t chunk,
+                                   const int64_t* __restrict__ end, int64_t chunk, bool adaptive,
                                    int64_t* __restrict__ prefix) {
   if (threadIdx.x == 0) {
     int64_t acc = 0;
     for (int e = 0; e < nlist; ++e) {
       prefix[e] = acc;
       const int64_t sz = end[list[e]] - start[list[e]];
-      acc += (sz + chunk - 1) / chunk;
+      const int64_t cs = chunk_size(sz, chunk, adaptive);
+      acc += (sz + cs - 1) / cs;
     }
     prefix[nlist] = acc;
   }
@@ -1366,7 +1382,7 @@ int launch_band_sample(const BandFit& bf, const BandWork& w, int sms, cudaStream
 void launch_band(const BandFit& bf, const BandArgs& ba, int mode, int grid, cudaStream_t st) {
   if (grid <= 0) return;
   if (mode == 1)
-    band_chunks_kernel<<<1, 32, 0, st>>>(ba.list, ba.nlist, ba.start, ba.end, ba.chunk,
+    band_chunks_kernel<<<1, 32, 0, st>>>(ba.list, ba.nlist, ba.start, ba.end, ba.chunk, true,
                                          ba.chunk_prefix);
   if (bf.n <= 1024) launch_band_t<256, 4>(bf, ba, mode, grid, st);
   else if (bf.n <= 4096) launch_band_t<512, 8>(bf, ba, mode, grid, st);
@@ -1555,7 +1571,7 @@ int launch_band_slices(const BandFit& bf, const BandArgs& ba, int64_t nslices_ma
 void launch_band_filter_big(const BandFit& bf, const BandArgs& ba, const float* store, int grid,
                             cudaStream_t st) {
   if (grid <= 0) return;
-  band_chunks_kernel<<<1, 32, 0, st>>>(ba.list, ba.nlist, ba.start, ba.end, ba.chunk,
+  band_chunks_kernel<<<1, 32, 0, st>>>(ba.list, ba.nlist, ba.start, ba.end, ba.chunk, false,
                                        ba.chunk_prefix);
   const size_t smem = kSliceRow * sizeof(unsigned);
   static bool done = false;

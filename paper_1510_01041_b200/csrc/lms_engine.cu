@@ -198,8 +198,8 @@ struct lms_ctx {
   DevBuf<int64_t> rbin, scounts, soffsets, sout;
   // slope bands (lms_band.cu)
   int band_mode = 1;  // LMSB_BAND: 0 count-filter path only, 1 auto (large fits), 2 always
-  int64_t band_vertices = 131072; // target vertices per band (LMSB_BAND_VERTICES)
-  int64_t band_chunk = 4096;     // collected members per filter CTA (LMSB_BAND_CHUNK)
+  int64_t band_vertices = 196608; // target vertices per band (LMSB_BAND_VERTICES)
+  int64_t band_chunk = 12288;    // collected members per filter CTA (LMSB_BAND_CHUNK)
   int64_t big_mult = 8;          // n > 16,384: vertices per band >= big_mult * n (LMSB_BIG_MULT)
   DevBuf<float> bsample, bbounds;
   DevBuf<unsigned> bscnt;
@@ -1219,7 +1219,8 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   ba.out_count = sc + 3;
   CUDA_TRY(cudaMemsetAsync(sc + 3, 0, 2 * sizeof(unsigned long long), c->stream));
   if (m > 0) {
-    const int fgrid = (int)(((int64_t)m + ba.chunk - 1) / ba.chunk + ba.nlist);
+    // (small path: up to kMinChunks = 4 chunks per group beyond m / chunk)
+    const int fgrid = (int)(((int64_t)m + ba.chunk - 1) / ba.chunk + 5 * (int64_t)ba.nlist);
     if (big) {
       // sorted keys per slice of `big_slice` members at the slice's own
       // centre slope (padding D shrinks with the slice's slope range)
