@@ -225,6 +225,7 @@ struct lms_ctx {
   // (LMSB_BAND_COARSE: 0 never, 1 always, 2 large n only -- for n <= 16,384
   // one shared-memory sort per band is cheaper than binning plus a refine)
   int band_coarse = 2;
+  int seed_bands = 8;            // bands whose window-edge pairs seed H (LMSB_SEED_BANDS)
   DevBuf<int64_t> bbig_seg;
   DevBuf<int32_t> small_list, dg_i32;
   DevBuf<int64_t> dg_i64;
@@ -272,6 +273,8 @@ int ctx_init(lms_ctx* c, int device) {
   const char* bmul = getenv("LMSB_BIG_MULT");
   if (bmul && atoll(bmul) >= 1) c->big_mult = atoll(bmul);
   if (const char* bs = getenv("LMSB_BIG_SLICE"); bs && atoll(bs) >= 1) c->big_slice = atoll(bs);
+  if (const char* sb = getenv("LMSB_SEED_BANDS"); sb && atoi(sb) >= 1)
+    c->seed_bands = std::min(48, atoi(sb));
   if (const char* bc0 = getenv("LMSB_BAND_COARSE")) c->band_coarse = std::max(0, std::min(2, atoi(bc0)));
   const char* sm = getenv("LMSB_SMALL");
   c->small_mode = sm ? std::max(0, std::min(2, atoi(sm))) : 1;
@@ -543,13 +546,13 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
                        (long long)sh->K_in, K);
     k0 = k1 = 0;
   }
-  constexpr int kSeedBands = 8;
+  const int kSeedBands = c->seed_bands;
   const int64_t seed_cap = S;
   RC_TRY(c->bsample.need(2 * S));
   RC_TRY(c->bbounds.need(K));
   RC_TRY(c->bscnt.need(K));
   RC_TRY(c->bflag.need(K + 1));
-  RC_TRY(c->bscal.need(5));
+  RC_TRY(c->bscal.need(6));  // [5]: running best height bits of the exact launches
   RC_TRY(c->bstart.need(K + 1));
   RC_TRY(c->bend.need(K + 1));
   RC_TRY(c->blb.need(K));
@@ -590,6 +593,7 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
 
   // [0] valid samples [1] collected [2] seeds [3] band survivors [4] count survivors
   unsigned long long* sc = c->bscal.p;
+  CUDA_TRY(cudaMemsetAsync(sc + 5, 0xFF, sizeof(unsigned long long), c->stream));  // no height yet
   lmsb::BandWork w{};
   w.S = S;
   w.K = K;
@@ -630,6 +634,7 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     // everything beyond the first 8 per SM
     xa.cached = 1;
     xa.cached_end = (int64_t)c->sms * 8;
+    xa.live_h = sc + 5;
     lmsb::launch_exact(xa, persistent_grid(c, -1), c->stream, h.n);
     lmsb::launch_reduce(c->recs.p, d_count, d_count ? 0 : cap, cap, c->fits.p, c->keys.p,
                         c->best.p, (int)c->sms * 4, c->stream);

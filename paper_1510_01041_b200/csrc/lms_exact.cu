@@ -239,6 +239,23 @@ __device__ __forceinline__ lms_candidate exact_vertex(const double* __restrict__
   return exact_vertex_t<kExactThreads, false>(a, b, n, q, i, j, u, v0, bound, sm, nullptr);
 }
 
+// Running minimum height of a single-fit exact launch (bits of a
+// non-negative double order like its value).  A vertex whose windows all
+// exceed it cannot win (a vertex of that height exists), so it is tested
+// against it; ties stay (<=), the reduce settles them by (i, j).  The bound
+// is uniform across the CTA: one read by thread 0, broadcast.
+__device__ __forceinline__ double live_bound(const unsigned long long* live_h) {
+  __shared__ double lb;
+  __syncthreads();
+  if (threadIdx.x == 0) lb = __longlong_as_double((long long)*(volatile const unsigned long long*)live_h);
+  __syncthreads();
+  return lb;
+}
+
+__device__ __forceinline__ void live_lower(unsigned long long* live_h, double h) {
+  atomicMin(live_h, (unsigned long long)__double_as_longlong(h + 0.0));
+}
+
 // Bound for vertex (i, j) against the fit's record bc: a vertex after bc in
 // (i, j) order wins only with a strictly smaller height (backend.py:182-187),
 // so its bound drops to the next double below (a negative bound: nothing to
@@ -327,10 +344,14 @@ __global__ void __launch_bounds__(kExactThreads) exact_kernel(ExactArgs args) {
       u = __ddiv_rn(__dsub_rn(b[i], b[j]), __dsub_rn(ai, aj));
       v0 = cut_value(u, ai, b[i]);
     }
+    if (args.live_h) bound = fmin(bound, live_bound(args.live_h));
     lms_candidate c = cand_none();
     if (valid) c = exact_vertex(a, b, fd.n, fd.q, i, j, u, v0, bound, sm);
     c.reserved = f;
-    if (threadIdx.x == 0) args.out[s] = c;
+    if (threadIdx.x == 0) {
+      args.out[s] = c;
+      if (args.live_h && c.found) live_lower(args.live_h, c.height);
+    }
   }
 }
 
@@ -353,12 +374,16 @@ __global__ void __launch_bounds__(kCachedThreads, 1) exact_cached_kernel(ExactAr
     int64_t i, j;
     double u, v0, bound;
     const bool valid = item_vertex(args, s, f, fd, i, j, u, v0, bound);
+    if (args.live_h) bound = fmin(bound, live_bound(args.live_h));
     lms_candidate c = cand_none();
     if (valid)
       c = exact_vertex_t<kCachedThreads, true>(args.a + fd.off, args.b + fd.off, fd.n, fd.q, i, j,
                                                u, v0, bound, sm, cache);
     c.reserved = f;
-    if (threadIdx.x == 0) args.out[s] = c;
+    if (threadIdx.x == 0) {
+      args.out[s] = c;
+      if (args.live_h && c.found) live_lower(args.live_h, c.height);
+    }
     __syncthreads();
   }
 }

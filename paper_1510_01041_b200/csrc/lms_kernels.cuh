@@ -57,6 +57,8 @@ struct ExactArgs {
   const double* vv;
   const lms_candidate* bound;  // optional per-fit bound (skip vertices that cannot win)
   lms_candidate* out;          // out[s].reserved = fit id
+  unsigned long long* live_h;  // optional (single fit): bits of the lowest height found so far;
+                               // vertices are tested against it and lower it as they finish
   int cached;                  // few vertices: one CTA each, cut keys cached in shared memory
   int64_t cached_end;          // cached: items beyond this go to the streaming kernel (0: none)
   int64_t begin;               // streaming kernel: first item
