@@ -756,10 +756,31 @@ __global__ void __launch_bounds__(kCollectThreads, LMSB_COLLECT_MINB) band_colle
 constexpr int kCountThreads = 512;
 constexpr int kCountWarps = kCountThreads / 32;
 
+// Line pairs (A_k, A_k+1, -B_k, -B_k+1) with A = fl32(a - c), B = fl32(b), as
+// float4 (the operand pairs of FFMA2); an odd n gets a pad line (0, NaN) at
+// index n, whose t is NaN and never counts
 __global__ void band_lines32_kernel(BandFit bf, float2* __restrict__ lines) {
-  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < bf.n;
-       k += (int64_t)gridDim.x * blockDim.x)
-    lines[k] = make_float2((float)__dsub_rn(bf.a[k], bf.c), (float)bf.b[k]);
+  float4* l4 = reinterpret_cast<float4*>(lines);
+  const int64_t np = (bf.n + 1) / 2;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < np;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = 2 * p;
+    float4 r = make_float4(0.f, 0.f, __int_as_float(0x7fc00000), __int_as_float(0x7fc00000));
+    r.x = (float)__dsub_rn(bf.a[k], bf.c);
+    r.z = -(float)bf.b[k];
+    if (k + 1 < bf.n) {
+      r.y = (float)__dsub_rn(bf.a[k + 1], bf.c);
+      r.w = -(float)bf.b[k + 1];
+    }
+    l4[p] = r;
+  }
+}
+
+// cnt += (x <= w), unsigned: one compare and one predicated add
+__device__ __forceinline__ void count_le(unsigned& cnt, uint32_t x, uint32_t w) {
+  asm("{\n .reg .pred p;\n setp.le.u32 p, %1, %2;\n @p add.u32 %0, %0, 1;\n}\n"
+      : "+r"(cnt)
+      : "r"(x), "r"(w));
 }
 
 // Persistent: all n lines staged once per CTA in shared memory; a tile is 32
@@ -772,7 +793,7 @@ __global__ void __launch_bounds__(kCountThreads) band_count_kernel(
     unsigned long long* __restrict__ out_count) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float2* sl = reinterpret_cast<float2*>(smem_raw);
-  const int nst = (int)min(bf.n, (int64_t)kBandMaxN);  // lines staged at once
+  const int nst = (int)min(bf.n + (bf.n & 1), (int64_t)kBandMaxN);  // lines staged at once (even)
   unsigned* cnt = reinterpret_cast<unsigned*>(sl + nst);  // [2][32]
   const int64_t total = (int64_t)*in_count;
   const int tid = threadIdx.x;
@@ -782,22 +803,23 @@ __global__ void __launch_bounds__(kCountThreads) band_count_kernel(
   const int q = (int)bf.q;
   if ((int64_t)blockIdx.x * 32 >= total) return;
   const bool resident = n <= nst;
+  const int ne = n + (n & 1);  // lines incl. the pad line, an even count
   if (resident) {
-    // TMA bulk copy of the whole line set (8 n bytes; an odd last line by hand)
+    // TMA bulk copy of the whole line set (8 ne bytes)
     __shared__ __align__(8) uint64_t bar;
     if (tid == 0) mbar_init(&bar, 1);
     __syncthreads();
-    const uint32_t bytes = (uint32_t)(n & ~1) * (uint32_t)sizeof(float2);
-    if (bytes) bulk_stage(sl, lines, bytes, &bar, 0);
-    if ((n & 1) && tid == 0) sl[n - 1] = lines[n - 1];
+    bulk_stage(sl, lines, (uint32_t)ne * (uint32_t)sizeof(float2), &bar, 0);
   }
   double H = INFINITY;
   {
     const lms_candidate b0 = *best;
     if (b0.found) H = b0.height;
   }
-  const int per = (nst + kCountWarps - 1) / kCountWarps;
-  const int k0 = warp * per, k1 = min(nst, k0 + per);
+  const float4* sl4 = reinterpret_cast<const float4*>(sl);  // two lines per entry
+  const int pairs = nst / 2;
+  const int per = (pairs + kCountWarps - 1) / kCountWarps;
+  const int p0 = warp * per, p1 = min(pairs, p0 + per);
   for (int64_t t0 = (int64_t)blockIdx.x * 32; t0 < total; t0 += (int64_t)gridDim.x * 32) {
     const int64_t s = t0 + lane;
     const bool live = s < total;
@@ -822,23 +844,36 @@ __global__ void __launch_bounds__(kCountThreads) band_count_kernel(
       dnLo = __double2float_rd(z - H - E);
       dnHi = __double2float_ru(z + E);
     }
+    // lo <= t <= hi implies fl(t - lo) in [+0, fl_ru(hi - lo)] (monotone
+    // rounding): one unsigned compare of the bits per window (negatives and
+    // NaN fail).  A lower end of +0 becomes -0 so that t = -0 gives +0.
+    if (upLo == 0.f) upLo = -0.f;
+    if (dnLo == 0.f) dnLo = -0.f;
+    const uint32_t wu = live ? __float_as_uint(__fsub_ru(upHi, upLo)) : 0u;
+    const uint32_t wd = live ? __float_as_uint(__fsub_ru(dnHi, dnLo)) : 0u;
+    const float2 u2 = make_float2(u32, u32);
+    const float2 nlu = make_float2(-upLo, -upLo), nld = make_float2(-dnLo, -dnLo);
     if (tid < 64) cnt[tid] = 0u;
     __syncthreads();  // also orders the line staging before first use
     unsigned cu = 0, cd = 0;
-    for (int c0 = 0; c0 < n; c0 += nst) {
-      const int cn = min(nst, n - c0);
+    for (int c0 = 0; c0 < ne; c0 += nst) {
+      const int cn = min(nst, ne - c0);  // even
       if (!resident) {
         __syncthreads();
         for (int k = tid; k < cn; k += kCountThreads) sl[k] = lines[c0 + k];
         __syncthreads();
       }
-      const int e1 = min(k1, cn);
+      const int e1 = min(p1, cn / 2);
 #pragma unroll 8
-      for (int k = k0; k < e1; ++k) {
-        const float2 L = sl[k];
-        const float t = fmaf(L.x, u32, -L.y);
-        cu += (t >= upLo) & (t <= upHi);
-        cd += (t >= dnLo) & (t <= dnHi);
+      for (int p = p0; p < e1; ++p) {
+        const float4 L = sl4[p];
+        const float2 t = __ffma2_rn(make_float2(L.x, L.y), u2, make_float2(L.z, L.w));
+        const float2 du = __fadd2_rn(t, nlu);
+        const float2 dd = __fadd2_rn(t, nld);
+        count_le(cu, __float_as_uint(du.x), wu);
+        count_le(cu, __float_as_uint(du.y), wu);
+        count_le(cd, __float_as_uint(dd.x), wd);
+        count_le(cd, __float_as_uint(dd.y), wd);
       }
     }
     atomicAdd(cnt + lane, cu);
@@ -1690,9 +1725,10 @@ void launch_band_collect(const BandFit& bf, const BandWork& w, const BandRuns& r
 }
 
 void launch_band_count(const BandFit& bf, const BandCount& bc, int sms, cudaStream_t st) {
-  if (bc.make_lines) band_lines32_kernel<<<(int)((bf.n + 255) / 256), 256, 0, st>>>(bf, bc.lines);
+  if (bc.make_lines) band_lines32_kernel<<<(int)((bf.n + 256) / 256), 256, 0, st>>>(bf, bc.lines);
   cudaMemsetAsync(bc.out_count, 0, sizeof(unsigned long long), st);
-  const size_t smem = (size_t)std::min<int64_t>(bf.n, kBandMaxN) * sizeof(float2) + 64 * sizeof(unsigned);
+  const size_t smem = (size_t)std::min<int64_t>(bf.n + (bf.n & 1), kBandMaxN) * sizeof(float2) +
+                      64 * sizeof(unsigned);
   static bool done = false;
   set_smem(band_count_kernel, (size_t)kBandMaxN * sizeof(float2) + 64 * sizeof(unsigned), &done);
   band_count_kernel<<<sms, kCountThreads, smem, st>>>(bf, bc.lines, bc.best, bc.in_ranks,

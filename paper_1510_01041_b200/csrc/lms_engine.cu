@@ -1210,7 +1210,7 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   RC_TRY(c->recs.need(scap));
   RC_TRY(c->branks2.need(scap));
   RC_TRY(c->bfits2.need(scap));
-  RC_TRY(c->blines32.need(h.n));
+  RC_TRY(c->blines32.need(h.n + 2));
   RC_TRY(c->bchunks.need((int64_t)std::max<size_t>(list.size(), (size_t)ngroups) + 1));
   ba.members = c->bmem.p;
   if (!direct) {
