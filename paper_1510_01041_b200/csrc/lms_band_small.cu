@@ -118,6 +118,13 @@ struct SmallShared {
   unsigned long long cnt[12];  // admitted bands, queued, exact, sweeps; phase cycles (stats)
 };
 
+// cnt += (x <= w), unsigned: one compare and one predicated add
+__device__ __forceinline__ void count_le(unsigned& cnt, uint32_t x, uint32_t w) {
+  asm("{\n .reg .pred p;\n setp.le.u32 p, %1, %2;\n @p add.u32 %0, %0, 1;\n}\n"
+      : "+r"(cnt)
+      : "r"(x), "r"(w));
+}
+
 __device__ __forceinline__ float rcp_approx_ftz(float x) {
   float r;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
@@ -541,25 +548,29 @@ __global__ void __launch_bounds__(kThreads, LMSB_SMALL_MINB) small_fit_kernel(Sm
       } else {
         const double E = 0x1p-20 * (3.0 * mag + 2.0 * bm + H) + 1e-37;
         const float u32 = (float)u;
-        const float upLo = __double2float_rd(z - E), upHi = __double2float_ru(z + H + E);
-        const float dnLo = __double2float_rd(z - H - E), dnHi = __double2float_ru(z + E);
+        float upLo = __double2float_rd(z - E), upHi = __double2float_ru(z + H + E);
+        float dnLo = __double2float_rd(z - H - E), dnHi = __double2float_ru(z + E);
+        if (upLo == 0.f) upLo = -0.f;  // so that t = -0 gives fl(t - lo) = +0
+        if (dnLo == 0.f) dnLo = -0.f;
         // lo <= t <= hi implies fl(t - lo) in [+0, fl(hi - lo)] (monotone rounding),
         // tested as one unsigned compare of the bits (negatives and NaN fail)
         const uint32_t wu = __float_as_uint(__fsub_ru(upHi, upLo));
         const uint32_t wd = __float_as_uint(__fsub_ru(dnHi, dnLo));
         const float2 u2 = make_float2(u32, u32);
         const float2 nlu = make_float2(-upLo, -upLo), nld = make_float2(-dnLo, -dnLo);
-        int cu = 0, cd = 0;
+        unsigned cu = 0, cd = 0;
 #pragma unroll 4
         for (int p2 = 0; p2 < (n + 1) / 2; ++p2) {
           const float4 R = sh.l2[p2];
           const float2 t = __ffma2_rn(make_float2(R.x, R.y), u2, make_float2(R.z, R.w));
           const float2 du = __fadd2_rn(t, nlu);
           const float2 dd = __fadd2_rn(t, nld);
-          cu += (__float_as_uint(du.x) <= wu) + (__float_as_uint(du.y) <= wu);
-          cd += (__float_as_uint(dd.x) <= wd) + (__float_as_uint(dd.y) <= wd);
+          count_le(cu, __float_as_uint(du.x), wu);
+          count_le(cu, __float_as_uint(du.y), wu);
+          count_le(cd, __float_as_uint(dd.x), wd);
+          count_le(cd, __float_as_uint(dd.y), wd);
         }
-        pass = cu >= q || cd >= q;
+        pass = (int)cu >= q || (int)cd >= q;
       }
     }
     if (args.timing && lane == 0) atomicAdd(&sh.cnt[9], (unsigned long long)(clock64() - td));
