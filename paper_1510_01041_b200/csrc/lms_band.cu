@@ -209,6 +209,21 @@ __device__ __forceinline__ int upper_idx(const float* __restrict__ k, int n, flo
   return lo;
 }
 
+// Two branch-free binary searches in lockstep (independent loads in flight):
+// *lo = first index with k >= xl, *up = first index with k > xu (n >= 1).
+__device__ __forceinline__ void lower_upper(const float* __restrict__ k, int n, float xl, float xu,
+                                            int* lo, int* up) {
+  int bl = 0, bu = 0, len = n;
+  while (len > 1) {
+    const int half = len >> 1;
+    bl = k[bl + half] < xl ? bl + half : bl;
+    bu = k[bu + half] <= xu ? bu + half : bu;
+    len -= half;
+  }
+  *lo = bl + (k[bl] < xl);
+  *up = bu + (k[bu] <= xu);
+}
+
 template <int kThreads>
 __device__ __forceinline__ double block_min(double v, double* red) {
 #pragma unroll
@@ -217,9 +232,12 @@ __device__ __forceinline__ double block_min(double v, double* red) {
   __syncthreads();
   if ((threadIdx.x & 31) == 0) red[w] = v;
   __syncthreads();
-  double r = red[0];
-#pragma unroll 1
-  for (int k = 1; k < kThreads / 32; ++k) r = fmin(r, red[k]);
+  if (kThreads <= 32) return red[0];
+  // every warp reduces the partials with shuffles (no serial smem loop)
+  const int lane = threadIdx.x & 31;
+  double r = lane < kThreads / 32 ? red[lane] : INFINITY;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) r = fmin(r, __shfl_xor_sync(0xffffffffu, r, off));
   return r;
 }
 
@@ -498,11 +516,11 @@ __global__ void __launch_bounds__(kThreads, 1) band_filter_kernel(BandFit bf, Ba
         const double D = bf.dev * fabs(u - uM) * (1.0 + 0x1p-40);
         const double E = slack_base(bf, fabs(u), uM) + 0x1p-20 * H + 1e-300;
         const double pad = D + E;
-        const int top = upper_idx(K, n, __double2float_ru(z + H + pad));
-        const int bot = lower_idx(K, n, __double2float_rd(z - H - pad));
+        int top, bot;
+        lower_upper(K, n, __double2float_rd(z - H - pad), __double2float_ru(z + H + pad), &bot, &top);
         if (top - bot >= q) {
-          const int up_lo = lower_idx(K, n, __double2float_rd(z - pad));
-          const int dn_hi = upper_idx(K, n, __double2float_ru(z + pad));
+          int up_lo, dn_hi;
+          lower_upper(K, n, __double2float_rd(z - pad), __double2float_ru(z + pad), &up_lo, &dn_hi);
           keep = (top - up_lo >= q) || (dn_hi - bot >= q);
         }
       }
