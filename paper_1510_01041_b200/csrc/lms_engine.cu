@@ -901,64 +901,47 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     CUDA_TRY(cudaEventRecord(c->ev_chunk[7], c->stream));
   } else {
     CUDA_TRY(cudaEventRecord(c->ev_chunk[1], c->stream));
+    // ---- seeds, picked on the device (no round trip after the bounds): the
+    // bands with the narrowest q-windows at their centre slope (the bands an
+    // LMS line of that slope would come from); with coarse bounds a pool of
+    // the kSeedPool narrowest coarse windows gets exact bounds first and the
+    // kSeedBands narrowest exact windows among them seed
+    constexpr int kSeedPool = 64;
+    const int32_t* d_seed = c->blist.p;
+    if (coarse) {
+      lmsb::launch_band_top(c->bwq.p, 0, K, K, kSeedPool, c->blist.p, c->bflag.p, c->stream);
+      RC_TRY(exact_bounds(c->blist.p, kSeedPool));
+      lmsb::launch_band_top(c->bwq.p, 0, kSeedPool, K, kSeedBands, c->blist.p + kSeedPool,
+                            c->bflag.p, c->stream, c->blist.p);
+      d_seed = c->blist.p + kSeedPool;
+      st->launches += 2;
+    } else {
+      lmsb::launch_band_top(c->bwq.p, 0, K, K, kSeedBands, c->blist.p, c->bflag.p, c->stream);
+      st->launches += 1;
+    }
+    // the window-edge pairs (usually the optimum itself) and, as a safety net,
+    // up to 16 sampled vertices of each of the same bands, in one exact launch
+    CUDA_TRY(cudaMemsetAsync(sc + 2, 0, sizeof(unsigned long long), c->stream));
+    lmsb::launch_band_edge_seeds(bf, ba, d_seed, kSeedBands, c->ranks.p, c->item_fit.p, seed_cap,
+                                 sc + 2, c->stream);
+    lmsb::launch_band_seeds(bf, w, c->ranks.p, c->item_fit.p, 0, seed_cap, sc + 2, c->stream);
+    RC_TRY(exact_list(sc + 2, seed_cap, c->ranks.p, c->item_fit.p));
+    CUDA_TRY(cudaEventRecord(c->ev_chunk[7], c->stream));
+    // one readback: bounds, window widths, boundaries, the seed record, counts
     CUDA_TRY(cudaMemcpyAsync(p_wq, c->bwq.p, sizeof(double) * K, cudaMemcpyDeviceToHost,
                              c->stream));
     CUDA_TRY(cudaMemcpyAsync(p_lb, c->blb.p, sizeof(double) * K, cudaMemcpyDeviceToHost,
                              c->stream));
     CUDA_TRY(cudaMemcpyAsync(p_bnd, c->bbounds.p, sizeof(float) * (K - 1), cudaMemcpyDeviceToHost,
                              c->stream));
-    CUDA_TRY(cudaStreamSynchronize(c->stream));
-    lb.assign(p_lb, p_lb + K);
-    hbnd.assign(p_bnd, p_bnd + (K - 1));
-    wq.assign(p_wq, p_wq + K);
-
-    // ---- seeds: the samples of the bands with the narrowest q-windows at their
-    // centre slope (the bands an LMS line of that slope would come from)
-    // (coarse bounds: a pool of the kSeedPool narrowest coarse windows gets
-    // exact bounds, and the kSeedBands narrowest exact windows among them
-    // are picked on the device)
-    constexpr int kSeedPool = 64;
-    std::vector<int32_t> seed_bands;
-    {
-      std::vector<int32_t> byw(K);
-      for (int k = 0; k < K; ++k) byw[k] = k;
-      std::stable_sort(byw.begin(), byw.end(), [&](int32_t x, int32_t y) { return wq[x] < wq[y]; });
-      const int take = coarse ? kSeedPool : kSeedBands;
-      for (int e = 0; e < K && e < take; ++e)
-        if (std::isfinite(wq[byw[e]])) {
-          if (!coarse) flag[byw[e]] = 1;
-          seed_bands.push_back(byw[e]);
-        }
-    }
-    std::copy(seed_bands.begin(), seed_bands.end(), u_seed);
-    CUDA_TRY(cudaMemcpyAsync(c->blist.p, u_seed, sizeof(int32_t) * seed_bands.size(),
-                             cudaMemcpyHostToDevice, c->stream));
-    const int32_t* d_seed = c->blist.p;
-    int nseed = (int)seed_bands.size();
-    if (coarse) {
-      RC_TRY(exact_bounds(c->blist.p, nseed));
-      lmsb::launch_band_top(c->bwq.p, 0, nseed, K, kSeedBands, c->blist.p + kSeedPool, c->bflag.p,
-                            c->stream, c->blist.p);
-      d_seed = c->blist.p + kSeedPool;
-      nseed = kSeedBands;
-      st->launches += 1;
-    } else {
-      std::memcpy(u_flag1, flag.data(), K);
-      CUDA_TRY(cudaMemcpyAsync(c->bflag.p, u_flag1, K, cudaMemcpyHostToDevice, c->stream));
-    }
-    // the window-edge pairs (usually the optimum itself) and, as a safety net,
-    // up to 16 sampled vertices of each of the same bands, in one exact launch
-    CUDA_TRY(cudaMemsetAsync(sc + 2, 0, sizeof(unsigned long long), c->stream));
-    lmsb::launch_band_edge_seeds(bf, ba, d_seed, nseed, c->ranks.p, c->item_fit.p, seed_cap,
-                                 sc + 2, c->stream);
-    lmsb::launch_band_seeds(bf, w, c->ranks.p, c->item_fit.p, 0, seed_cap, sc + 2, c->stream);
-    RC_TRY(exact_list(sc + 2, seed_cap, c->ranks.p, c->item_fit.p));
-    CUDA_TRY(cudaEventRecord(c->ev_chunk[7], c->stream));
     CUDA_TRY(cudaMemcpyAsync(p_hb, c->best.p, sizeof(lms_candidate), cudaMemcpyDeviceToHost,
                              c->stream));
     CUDA_TRY(cudaMemcpyAsync(p_scnt, c->bscnt.p, sizeof(unsigned) * K, cudaMemcpyDeviceToHost,
                              c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
+    lb.assign(p_lb, p_lb + K);
+    hbnd.assign(p_bnd, p_bnd + (K - 1));
+    wq.assign(p_wq, p_wq + K);
     const lms_candidate hb = *p_hb;
     scnt.assign(p_scnt, p_scnt + K);
     H = hb.found ? hb.height : INFINITY;
