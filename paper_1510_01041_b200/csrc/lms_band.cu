@@ -916,6 +916,104 @@ __global__ void __launch_bounds__(kCountThreads) band_count_kernel(
   }
 }
 
+// Exact pass-0 screen of the count kernel's survivors (the first pass of
+// exact_vertex_t, lms_exact.cu, with the reference's fp64 arithmetic): lane
+// per vertex, the lines staged in shared memory once per CTA chunk and shared
+// by 32 vertices, instead of one CTA streaming the lines per vertex.  A
+// vertex survives when at least q lines x (anchors snapped to v0) satisfy
+// x >= v0 and fl(x - v0) <= bound, or x <= v0 and fl(v0 - x) <= bound, with
+// bound = the record's height (its next double below for vertices after the
+// record in (i, j) order) -- exactly the exact stage's own pruning test, so
+// only vertices the exact select would fully evaluate reach it.
+constexpr int kPreThreads = 512;
+constexpr int kPreWarps = kPreThreads / 32;
+constexpr int kPreLines = 8192;  // lines staged at once (128 KB of (a, b))
+
+__global__ void __launch_bounds__(kPreThreads) band_exact_prepass_kernel(
+    BandFit bf, const lms_candidate* __restrict__ best, const int64_t* __restrict__ in_ranks,
+    const unsigned long long* __restrict__ in_count, int64_t* __restrict__ out_ranks,
+    int32_t* __restrict__ out_fits, int32_t fit, unsigned long long* __restrict__ out_count) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* sl = reinterpret_cast<double2*>(smem_raw);
+  unsigned* cnt = reinterpret_cast<unsigned*>(sl + kPreLines);  // [2][32]
+  const int64_t total = (int64_t)*in_count;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n = (int)bf.n, q = (int)bf.q;
+  if ((int64_t)blockIdx.x * 32 >= total) return;
+  const lms_candidate rec = *best;
+  const int nst = min(n, kPreLines);
+  const int per = (nst + kPreWarps - 1) / kPreWarps;
+  const int k0 = warp * per, k1 = min(nst, k0 + per);
+  for (int64_t t0 = (int64_t)blockIdx.x * 32; t0 < total; t0 += (int64_t)gridDim.x * 32) {
+    const int64_t s = t0 + lane;
+    bool live = s < total;
+    int64_t rank = 0, i = 0, j = 0;
+    double u = 0.0, v0 = 0.0, bound = INFINITY;
+    if (live) {
+      rank = in_ranks[s];
+      decode_rank(bf.n, rank, &i, &j);
+      const double ai = bf.a[i], bi = bf.b[i];
+      const double da = __dsub_rn(ai, bf.a[j]);
+      u = __ddiv_rn(__dsub_rn(bi, bf.b[j]), da);
+      v0 = cut_value(u, ai, bi);
+      if (rec.found) {
+        const bool after = i > rec.i || (i == rec.i && j > rec.j);
+        bound = after ? nextafter(rec.height, -INFINITY) : rec.height;
+      }
+      live = da != 0.0 && bound >= 0.0;
+    }
+    if (tid < 64) cnt[tid] = 0u;
+    unsigned cu = 0, cd = 0;
+    for (int c0 = 0; c0 < n; c0 += nst) {
+      const int cn = min(nst, n - c0);
+      __syncthreads();
+      for (int k = tid; k < cn; k += kPreThreads) sl[k] = bf.ab[c0 + k];
+      __syncthreads();
+      const int e1 = min(k1, cn);
+#pragma unroll 4
+      for (int k = k0; k < e1; ++k) {
+        const double2 L = sl[k];
+        const double x = cut_value(u, L.x, L.y);
+        const double dx = __dsub_rn(x, v0), dv = __dsub_rn(v0, x);
+        cu += (x >= v0) & (dx <= bound);
+        cd += (x <= v0) & (dv <= bound);
+      }
+    }
+    atomicAdd(cnt + lane, cu);
+    atomicAdd(cnt + 32 + lane, cd);
+    __syncthreads();
+    if (warp == 0) {
+      bool keep = false;
+      if (live) {
+        int tu = (int)cnt[lane], td = (int)cnt[32 + lane];
+        // line j counted unsnapped; snapped it is v0 (counts in both windows;
+        // line i's cut is v0 already)
+        const double xj = cut_value(u, bf.a[j], bf.b[j]);
+        tu += 1 - (int)((xj >= v0) & (__dsub_rn(xj, v0) <= bound));
+        td += 1 - (int)((xj <= v0) & (__dsub_rn(v0, xj) <= bound));
+        keep = !isfinite(bound) || tu >= q || td >= q;
+#ifdef LMSB_PREPASS_TRACE
+        if (i == LMSB_PREPASS_TRACE_I && j == LMSB_PREPASS_TRACE_J)
+          printf("prepass (%lld,%lld) tu %d td %d q %d bound %.17g u %.17g v0 %.17g cnt %u %u\n",
+                 (long long)i, (long long)j, tu, td, q, bound, u, v0, cnt[lane], cnt[32 + lane]);
+#endif
+      }
+      const unsigned mask = __ballot_sync(0xffffffffu, keep);
+      if (mask) {
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(out_count, (unsigned long long)__popc(mask));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (keep) {
+          const unsigned slot = __popc(mask & ((1u << lane) - 1u));
+          out_ranks[base + slot] = rank;
+          out_fits[base + slot] = fit;
+        }
+      }
+    }
+    __syncthreads();  // warp 0 has read the counts before the next tile clears them
+  }
+}
+
 // Seeds from the narrowest q-window of each listed band: the lines whose
 // keys (recomputed exactly as the bound kernel formed them) lie among the
 // kEdge keys around either end of the window, paired within each end.
@@ -1740,6 +1838,16 @@ void launch_band_collect(const BandFit& bf, const BandWork& w, const BandRuns& r
     LMSB_COLLECT(8)
 #undef LMSB_COLLECT
   }
+}
+
+void launch_band_exact_prepass(const BandFit& bf, const BandCount& bc, int sms, cudaStream_t st) {
+  cudaMemsetAsync(bc.out_count, 0, sizeof(unsigned long long), st);
+  const size_t smem = (size_t)kPreLines * sizeof(double2) + 64 * sizeof(unsigned);
+  static bool done = false;
+  set_smem(band_exact_prepass_kernel, smem, &done);
+  band_exact_prepass_kernel<<<sms, kPreThreads, smem, st>>>(bf, bc.best, bc.in_ranks, bc.in_count,
+                                                            bc.out_ranks, bc.out_fits, bc.fit,
+                                                            bc.out_count);
 }
 
 void launch_band_count(const BandFit& bf, const BandCount& bc, int sms, cudaStream_t st) {

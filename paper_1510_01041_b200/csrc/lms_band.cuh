@@ -180,5 +180,9 @@ size_t band_direct_smem(int K, int nsub, int nadm);
 void launch_band_collect_direct(const BandFit& bf, const BandWork& w, const BandRuns& runs,
                                 const BandDirect& dg, int sms, cudaStream_t st);
 void launch_band_count(const BandFit& bf, const BandCount& bc, int sms, cudaStream_t st);
+// exact pass-0 screen (fp64, the reference's arithmetic) of bc.in_ranks[0 ..
+// *bc.in_count) against the record bc.best: the vertices the exact select
+// would not prune go to bc.out_*; lines from bf.ab
+void launch_band_exact_prepass(const BandFit& bf, const BandCount& bc, int sms, cudaStream_t st);
 
 }  // namespace lmsb

@@ -552,7 +552,7 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   RC_TRY(c->bbounds.need(K));
   RC_TRY(c->bscnt.need(K));
   RC_TRY(c->bflag.need(K + 1));
-  RC_TRY(c->bscal.need(6));  // [5]: running best height bits of the exact launches
+  RC_TRY(c->bscal.need(7));  // [5]: running best height bits of the exact launches, [6]: prepass
   RC_TRY(c->bstart.need(K + 1));
   RC_TRY(c->bend.need(K + 1));
   RC_TRY(c->blb.need(K));
@@ -1205,7 +1205,10 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   ba.out_ranks = c->ranks.p;
   ba.out_fits = c->item_fit.p;
   ba.out_count = sc + 3;
+  // [3] band survivors, [4] count survivors ([5] is the running best height;
+  // [6] the prepass output, cleared by its launcher)
   CUDA_TRY(cudaMemsetAsync(sc + 3, 0, 2 * sizeof(unsigned long long), c->stream));
+  CUDA_TRY(cudaMemsetAsync(sc + 6, 0, sizeof(unsigned long long), c->stream));
   if (m > 0) {
     // (small path: up to kMinChunks = 4 chunks per group beyond m / chunk)
     const int fgrid = (int)(((int64_t)m + ba.chunk - 1) / ba.chunk + 5 * (int64_t)ba.nlist);
@@ -1253,14 +1256,24 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     st->launches += 4;
     // the window-edge seeds put H at (or within a few ulps of) the optimum, so
     // the exact stage's pass 0 prunes every survivor that cannot tie it
-    RC_TRY(exact_list(sc + 4, scap, c->branks2.p, c->bfits2.p));
+    // exact pass-0 screen, lane per vertex with shared-memory lines; only the
+    // vertices the exact select would not prune go on to it
+    lmsb::BandCount bp = bc;
+    bp.in_ranks = c->branks2.p;
+    bp.in_count = sc + 4;
+    bp.out_ranks = c->ranks.p;
+    bp.out_fits = c->item_fit.p;
+    bp.out_count = sc + 6;
+    lmsb::launch_band_exact_prepass(bf, bp, c->sms, c->stream);
+    st->launches += 1;
+    RC_TRY(exact_list(sc + 6, scap, c->ranks.p, c->item_fit.p));
   }
   CUDA_TRY(cudaEventRecord(c->ev_chunk[4], c->stream));
   unsigned long long* cnts = reinterpret_cast<unsigned long long*>(c->pin);  // readbacks done
-  CUDA_TRY(cudaMemcpyAsync(cnts, sc + 3, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+  CUDA_TRY(cudaMemcpyAsync(cnts, sc + 3, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                            c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
-  st->survivors = (int64_t)cnts[1];
+  st->survivors = (int64_t)cnts[3];  // evaluated by the exact select (cnts[2]: running height)
   st->band_survivors = (int64_t)cnts[0];
   st->filtered_vertices = (int64_t)m;
   st->chunks = 1;
