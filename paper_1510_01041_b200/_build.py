@@ -51,7 +51,10 @@ def build(verbose: bool = False, extra: list[str] | None = None, out: str | None
         with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 1)) as pool:
             list(pool.map(compile_one, SOURCES))
         tmp = out + ".tmp"
-        subprocess.run([nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-cudart", "static"], check=True)
+        # --no-undefined: a symbol missing from the objects fails the link here
+        # instead of the load on the GPU box
+        subprocess.run([nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-cudart", "static",
+                        "-Xlinker", "--no-undefined"], check=True)
         os.replace(tmp, out)
     finally:
         for o in objs:

@@ -1730,29 +1730,39 @@ void launch_band_filter_big(const BandFit& bf, const BandArgs& ba, const float* 
   band_filter_big_kernel<<<grid, kBigThreads, smem, st>>>(bf, ba, store);
 }
 
-__global__ void __launch_bounds__(1024) band_top_kernel(const double* __restrict__ wq, int k0,
-                                                       int k1, const int32_t* __restrict__ ids,
-                                                       int K, int T, int32_t* __restrict__ list,
-                                                       uint8_t* __restrict__ flag) {
+// T rounds of a block-wide (wq, index) argmin; every thread holds its share
+// of the candidates (at most 16) in registers and marks the ones taken.
+constexpr int kTopThreads = 1024;
+constexpr int kTopItems = 16;  // candidates per thread: K <= 16,384
+
+__global__ void __launch_bounds__(kTopThreads) band_top_kernel(const double* __restrict__ wq, int k0,
+                                                              int k1, const int32_t* __restrict__ ids,
+                                                              int K, int T, int32_t* __restrict__ list,
+                                                              uint8_t* __restrict__ flag) {
   __shared__ double rv[32];
   __shared__ int rk[32];
-  __shared__ int chosen[64];
-  for (int k = threadIdx.x; k < K; k += blockDim.x) flag[k] = 0;
+  __shared__ int pick_s;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double cv[kTopItems];
+  int ck[kTopItems];
+#pragma unroll
+  for (int e = 0; e < kTopItems; ++e) {
+    const int x0 = k0 + e * kTopThreads + tid;
+    const int k = x0 < k1 ? (ids ? ids[x0] : x0) : -1;
+    ck[e] = k;
+    cv[e] = k >= 0 ? wq[k] : INFINITY;
+  }
+  for (int k = tid; k < K; k += kTopThreads) flag[k] = 0;
   __syncthreads();
   for (int t = 0; t < T; ++t) {
     double v = INFINITY;
     int bk = INT_MAX;
-    for (int x0 = k0 + (int)threadIdx.x; x0 < k1; x0 += blockDim.x) {
-      const int k = ids ? ids[x0] : x0;
-      if (k < 0) continue;
-      bool taken = false;
-      for (int e = 0; e < t; ++e) taken |= chosen[e] == k;
-      const double x = wq[k];
-      if (!taken && x < v) {
-        v = x;
-        bk = k;
+#pragma unroll
+    for (int e = 0; e < kTopItems; ++e)
+      if (ck[e] >= 0 && (cv[e] < v || (cv[e] == v && ck[e] < bk))) {
+        v = cv[e];
+        bk = ck[e];
       }
-    }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
       const double ov = __shfl_xor_sync(0xffffffffu, v, off);
@@ -1762,23 +1772,35 @@ __global__ void __launch_bounds__(1024) band_top_kernel(const double* __restrict
         bk = ok;
       }
     }
-    if ((threadIdx.x & 31) == 0) {
-      rv[threadIdx.x >> 5] = v;
-      rk[threadIdx.x >> 5] = bk;
+    if (lane == 0) {
+      rv[warp] = v;
+      rk[warp] = bk;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
-        if (rv[w] < v || (rv[w] == v && rk[w] < bk)) {
-          v = rv[w];
-          bk = rk[w];
+    if (warp == 0) {
+      v = rv[lane];
+      bk = rk[lane];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, v, off);
+        const int ok = __shfl_xor_sync(0xffffffffu, bk, off);
+        if (ov < v || (ov == v && ok < bk)) {
+          v = ov;
+          bk = ok;
         }
-      const int pick = v < INFINITY ? bk : -1;
-      chosen[t] = pick;
-      list[t] = pick;
-      if (pick >= 0) flag[pick] = 1;
+      }
+      if (lane == 0) {
+        const int pick = v < INFINITY ? bk : -1;
+        pick_s = pick;
+        list[t] = pick;
+        if (pick >= 0) flag[pick] = 1;
+      }
     }
     __syncthreads();
+    const int pick = pick_s;
+#pragma unroll
+    for (int e = 0; e < kTopItems; ++e)
+      if (ck[e] == pick) ck[e] = -1;  // taken
   }
 }
 
@@ -1797,7 +1819,7 @@ void launch_band_interleave(const double* a, const double* b, int64_t n, double2
 
 void launch_band_top(const double* wq, int k0, int k1, int K, int T, int32_t* list, uint8_t* flag,
                      cudaStream_t st, const int32_t* ids) {
-  band_top_kernel<<<1, 1024, 0, st>>>(wq, k0, k1, ids, K, T < 64 ? T : 64, list, flag);
+  band_top_kernel<<<1, kTopThreads, 0, st>>>(wq, k0, k1, ids, K, T < 64 ? T : 64, list, flag);
 }
 
 void launch_band_edge_seeds(const BandFit& bf, const BandArgs& ba, const int32_t* bands, int nb,
