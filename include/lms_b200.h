@@ -159,6 +159,12 @@ int lms_hough_vote_points(const double* x, const double* y, int64_t npts, const 
 int lms_hough_support(const double* cos_p, const double* sin_p, const int64_t* rbin_p,
                       int64_t npeaks, double rho_max, double delta_rho, int64_t n_rho, int device,
                       int64_t* offsets, int64_t* out, int64_t capacity);
+/* lms_hough_support with the ids written as int32 (half the download; the
+ * ids are narrowed on the device).  LMS_ERR_INVALID when an id of the last
+ * vote could exceed INT32_MAX (more than 2^31 pixels or points). */
+int lms_hough_support_i32(const double* cos_p, const double* sin_p, const int64_t* rbin_p,
+                          int64_t npeaks, double rho_max, double delta_rho, int64_t n_rho,
+                          int device, int64_t* offsets, int32_t* out, int64_t capacity);
 
 /* Anchored window at each explicit intersection (i[k], j[k], u[k]).  When v
  * is non-NULL the anchors are snapped to v[k] (bracelet_at); when NULL to

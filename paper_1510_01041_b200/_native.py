@@ -139,6 +139,9 @@ SIGNATURES = {
                                              ctypes.c_int, _I]),
     "lms_hough_support": (ctypes.c_int, [_D, _D, _I, ctypes.c_int64, ctypes.c_double, ctypes.c_double,
                                          ctypes.c_int64, ctypes.c_int, _I, _I, ctypes.c_int64]),
+    "lms_hough_support_i32": (ctypes.c_int, [_D, _D, _I, ctypes.c_int64, ctypes.c_double, ctypes.c_double,
+                                             ctypes.c_int64, ctypes.c_int, _I,
+                                             ctypes.POINTER(ctypes.c_int32), ctypes.c_int64]),
     "lms_eval_vertices_f64": (ctypes.c_int, [_D, _D, ctypes.c_int64, ctypes.c_int64, _I, _I, _D, _D,
                                              ctypes.c_int64, ctypes.c_int, _C]),
     "lms_min_over_vertices_f64": (ctypes.c_int, [_D, _D, ctypes.c_int64, ctypes.c_int64, _I, _I, _D,
@@ -319,18 +322,27 @@ def hough_vote_points(x, y, cos_t, sin_t, rho_max: float, delta_rho: float, n_rh
 
 
 def hough_support(cos_p, sin_p, rbin_p, rho_max: float, delta_rho: float, n_rho: int,
-                  capacity: int, device: int = 0):
-    """lms_hough_support on the last vote's points -> (offsets[P+1], ids)."""
+                  capacity: int, device: int = 0, narrow: bool = False):
+    """lms_hough_support on the last vote's points -> (offsets[P+1], ids);
+    narrow=True: int32 ids through lms_hough_support_i32 (half the download)."""
     lib = _lib_ready()
     cos_p, sin_p, rbin_p = _f64(cos_p), _f64(sin_p), _i64(rbin_p)
     npk = cos_p.size
     offsets = np.zeros(npk + 1, dtype=np.int64)
-    out = np.empty(max(int(capacity), 1), dtype=np.int64)
-    rc = lib.lms_hough_support(_dp(cos_p), _dp(sin_p), _ip(rbin_p), npk, float(rho_max),
-                               float(delta_rho), int(n_rho), int(device), _ip(offsets), _ip(out),
-                               int(capacity))
+    if narrow:
+        out = np.empty(max(int(capacity), 1), dtype=np.int32)
+        rc = lib.lms_hough_support_i32(_dp(cos_p), _dp(sin_p), _ip(rbin_p), npk, float(rho_max),
+                                       float(delta_rho), int(n_rho), int(device), _ip(offsets),
+                                       out.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                       int(capacity))
+    else:
+        out = np.empty(max(int(capacity), 1), dtype=np.int64)
+        rc = lib.lms_hough_support(_dp(cos_p), _dp(sin_p), _ip(rbin_p), npk, float(rho_max),
+                                   float(delta_rho), int(n_rho), int(device), _ip(offsets), _ip(out),
+                                   int(capacity))
     if rc == LMS_ERR_INVALID and offsets[-1] > capacity:
-        return hough_support(cos_p, sin_p, rbin_p, rho_max, delta_rho, n_rho, int(offsets[-1]), device)
+        return hough_support(cos_p, sin_p, rbin_p, rho_max, delta_rho, n_rho, int(offsets[-1]),
+                             device, narrow)
     check(rc)
     return offsets, out[: offsets[-1]]
 

@@ -196,6 +196,7 @@ struct lms_ctx {
   DevBuf<unsigned long long> acc, masks;
   DevBuf<double> tcos, tsin;
   DevBuf<int64_t> rbin, scounts, soffsets, sout;
+  DevBuf<int32_t> sout32;
   // slope bands (lms_band.cu)
   int band_mode = 1;  // LMSB_BAND: 0 count-filter path only, 1 auto (large fits), 2 always
   int64_t band_vertices = 196608; // target vertices per band (LMSB_BAND_VERTICES)
@@ -249,6 +250,7 @@ struct lms_ctx {
   uint64_t gen = 0;            // bumped whenever the bound lines change
   int hough_mode = 0;  // 0 none, 1 image pixels, 2 explicit points
   int64_t hough_npts = 0, hough_width = 1;
+  int64_t hough_maxid = 0;  // bound of the support ids of the last vote
   lms_stats stats{};
   std::mutex mu;
 };
@@ -1860,6 +1862,7 @@ int ctx_vote_image(lms_ctx* c, const uint8_t* img, int64_t height, int64_t width
   c->hough_mode = 1;
   c->hough_npts = npts;
   c->hough_width = std::max<int64_t>(width, 1);
+  c->hough_maxid = npix;  // pixel indices < width * height
   *npoints = npts;
   return ctx_vote(c, cos_t, sin_t, n_theta, rho_max, drho, n_rho, acc_out);
 }
@@ -1879,12 +1882,13 @@ int ctx_vote_points(lms_ctx* c, const double* x, const double* y, int64_t npts,
   c->hough_mode = 2;
   c->hough_npts = npts;
   c->hough_width = 1;
+  c->hough_maxid = npts;
   return ctx_vote(c, cos_t, sin_t, n_theta, rho_max, drho, n_rho, acc_out);
 }
 
 int ctx_support(lms_ctx* c, const double* cos_p, const double* sin_p, const int64_t* rbin_p,
                 int64_t npeaks, double rho_max, double drho, int64_t n_rho, int64_t* offsets,
-                int64_t* out, int64_t capacity) {
+                int64_t* out, int64_t capacity, int32_t* out32 = nullptr) {
   if (npeaks < 0 || !offsets || (npeaks > 0 && (!cos_p || !sin_p || !rbin_p)))
     return set_error(LMS_ERR_INVALID, "bad peaks");
   if (c->hough_mode == 0) return set_error(LMS_ERR_INVALID, "no points: call a vote first");
@@ -1940,6 +1944,13 @@ int ctx_support(lms_ctx* c, const double* cos_p, const double* sin_p, const int6
     if (out && total + group_total <= capacity && group_total > 0)
       CUDA_TRY(cudaMemcpyAsync(out + total, c->sout.p, sizeof(int64_t) * group_total,
                                cudaMemcpyDeviceToHost, c->stream));
+    if (out32 && total + group_total <= capacity && group_total > 0) {
+      // half the download: indices narrowed on the device
+      RC_TRY(c->sout32.need(group_total));
+      lmsb::launch_narrow_i32(c->sout.p, c->sout32.p, group_total, c->stream);
+      CUDA_TRY(cudaMemcpyAsync(out32 + total, c->sout32.p, sizeof(int32_t) * group_total,
+                               cudaMemcpyDeviceToHost, c->stream));
+    }
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     total += group_total;
   }
@@ -2104,6 +2115,18 @@ int lms_hough_support(const double* cos_p, const double* sin_p, const int64_t* r
   std::lock_guard<std::mutex> lk(c->mu);
   return ctx_support(c, cos_p, sin_p, rbin_p, npeaks, rho_max, delta_rho, n_rho, offsets, out,
                      capacity);
+}
+
+int lms_hough_support_i32(const double* cos_p, const double* sin_p, const int64_t* rbin_p,
+                          int64_t npeaks, double rho_max, double delta_rho, int64_t n_rho,
+                          int device, int64_t* offsets, int32_t* out, int64_t capacity) {
+  lms_ctx* c = nullptr;
+  RC_TRY(shared_ctx(device, &c));
+  std::lock_guard<std::mutex> lk(c->mu);
+  if (std::max(c->hough_npts, c->hough_maxid) > INT32_MAX)
+    return set_error(LMS_ERR_INVALID, "support ids exceed int32: use lms_hough_support");
+  return ctx_support(c, cos_p, sin_p, rbin_p, npeaks, rho_max, delta_rho, n_rho, offsets, nullptr,
+                     capacity, out);
 }
 
 int lms_eval_vertices_f64(const double* a, const double* b, int64_t n, int64_t q, const int64_t* i,

@@ -27,6 +27,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <algorithm>
 #include <cstdint>
 
 #include "lms_hough.cuh"
@@ -338,6 +339,18 @@ size_t extract_temp_bytes(int64_t npix) {
   LitPixel pred{nullptr, 0};
   cub::DeviceSelect::If(nullptr, bytes, it, (int64_t*)nullptr, (int64_t*)nullptr, npix, pred);
   return bytes;
+}
+
+__global__ void narrow_i32_kernel(const int64_t* __restrict__ in, int32_t* __restrict__ out,
+                                  int64_t m) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m;
+       k += (int64_t)gridDim.x * blockDim.x)
+    out[k] = (int32_t)in[k];
+}
+
+void launch_narrow_i32(const int64_t* in, int32_t* out, int64_t m, cudaStream_t st) {
+  if (m <= 0) return;
+  narrow_i32_kernel<<<(int)std::min<int64_t>((m + 255) / 256, 4096), 256, 0, st>>>(in, out, m);
 }
 
 }  // namespace lmsb

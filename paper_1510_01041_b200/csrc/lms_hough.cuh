@@ -31,4 +31,7 @@ int hough_support(const int64_t* d_pix, const double* d_x, const double* d_y, in
                   size_t temp_bytes, int64_t* d_out, int64_t out_cap, cudaStream_t stream);
 size_t support_scan_temp_bytes(int64_t m);
 
+// out[k] = (int32) in[k], k < m (support ids narrowed for the download)
+void launch_narrow_i32(const int64_t* in, int32_t* out, int64_t m, cudaStream_t st);
+
 }  // namespace lmsb

@@ -63,7 +63,8 @@ class SupportPoints(Sequence):
         coordinates are formed on first use."""
         sp = cls.__new__(cls)
         sp._xy = None
-        sp._ids = np.asarray(ids, dtype=np.int64)
+        ids = np.asarray(ids)
+        sp._ids = ids if ids.dtype in (np.int32, np.int64) else ids.astype(np.int64)
         sp._width = int(width)
         return sp
 
@@ -235,10 +236,12 @@ def detect_lines(image: np.ndarray, params: HoughParams, method: str = METHOD_LM
     if not peaks:
         return []
     trig = [params.support_trig(p.theta_bin) for p in peaks]
+    # int32 pixel ids (half the download) whenever the image has < 2^31 pixels
     offsets, ids = _native.hough_support([t[0] for t in trig], [t[1] for t in trig],
                                          [p.rho_bin for p in peaks], params.rho_max,
                                          params.delta_rho, params.n_rho,
-                                         capacity=sum(p.votes for p in peaks))
+                                         capacity=sum(p.votes for p in peaks),
+                                         narrow=img.size < 2**31)
     width = img.shape[1]
     supports = [SupportPoints.from_pixels(ids[offsets[k]: offsets[k + 1]], width)
                 for k in range(len(peaks))]
