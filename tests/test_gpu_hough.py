@@ -91,6 +91,13 @@ def test_config5_scale_vote_and_support_vs_oracle():
         ords = hough_oracle.support(x, y, k.theta_bin, k.rho_bin, p.delta_rho, p.delta_theta, p.rho_max)
         assert np.array_equal(ids[offsets[q]:offsets[q + 1]], lit[ords])
     assert all(offsets[q + 1] - offsets[q] == k.votes for q, k in enumerate(peaks))
+    # the int32 download (lms_hough_support_i32, used by detect_lines) carries
+    # the same ids, including through the grow-and-retry path
+    off32, ids32 = _native.hough_support([t[0] for t in trig], [t[1] for t in trig],
+                                         [k.rho_bin for k in peaks], p.rho_max, p.delta_rho,
+                                         p.n_rho, capacity=10, narrow=True)
+    assert ids32.dtype == np.int32
+    assert np.array_equal(off32, offsets) and np.array_equal(ids32.astype(np.int64), ids)
 
 
 def test_detect_lines_deterministic_and_batched_equals_single():

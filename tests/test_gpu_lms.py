@@ -694,3 +694,25 @@ def test_device_contacts_match_host_tail():
         want = fit_from_record(xx, yy, q, rec)
         assert got == want
     assert len(lms.solve_lms(cases[3]).contact_indices) == 500
+
+
+@pytest.mark.parametrize("n", [4096, 16384])
+def test_coarse_bounds_on_small_n_and_shards_match(n):
+    """The sort-free coarse bounds (LMSB_BAND_COARSE=1, the large-n default)
+    forced on the shared-memory band path, single and sharded over 4: the
+    same record as the default path."""
+    from paper_1510_01041_b200 import distributed
+
+    pts = workloads.contaminated_line_points(n, 6)
+    a, b = pts[:, 0].copy(), pts[:, 1].copy()
+    q = n // 2 + 1
+    total = n * (n - 1) // 2
+    ref = _native.Context()
+    ref.upload(a, b)
+    want = record_from_native(ref.solve(q, 0, total))
+    ctx = _ctx_with({"LMSB_BAND_COARSE": "1"})
+    ctx.upload(a, b)
+    assert record_from_native(ctx.solve(q, 0, total)) == want
+    assert ctx.stats()["bands_refined"] > 0
+    _, _, got = _sharded_sequential(ctx, q, 4)
+    assert got == want
