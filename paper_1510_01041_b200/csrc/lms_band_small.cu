@@ -45,6 +45,9 @@ namespace lmsb {
 
 namespace {
 
+#ifndef LMSB_SMALL_AB
+#define LMSB_SMALL_AB 1
+#endif
 #ifndef LMSB_SMALL_BAND_VERTS
 #define LMSB_SMALL_BAND_VERTS 512
 #endif
@@ -63,9 +66,15 @@ constexpr int kSampleItems = kSamples / kThreads;
 constexpr int kSeedsPerBand = 16;
 constexpr int kSeedBands = 2;
 constexpr int kEdge = 5;  // keys kept around each end of a band's narrowest q-window
-constexpr int kSlots = 16;    // admitted bands whose keys are resident at once
+#ifndef LMSB_SMALL_SLOTS
+#define LMSB_SMALL_SLOTS 16
+#endif
+constexpr int kSlots = LMSB_SMALL_SLOTS;  // admitted bands whose keys are resident at once
 constexpr int kSegRun = 16;   // ranks per lane per warp segment
-constexpr int kSweepStep = 4; // vertices per lane per sweep step
+#ifndef LMSB_SMALL_STEP
+#define LMSB_SMALL_STEP 4
+#endif
+constexpr int kSweepStep = LMSB_SMALL_STEP; // vertices per lane per sweep step
 constexpr int kQueue = 32 * (kSweepStep + 1);  // per-warp queues: < 32 waiting + a step
 static_assert(kSegRun % kSweepStep == 0, "whole sweep steps per segment");
 constexpr int kMaxRuns = 8;   // slope runs tested before a band lookup
@@ -76,7 +85,9 @@ struct SmallShared {
   using SampleSort = cub::BlockRadixSort<float, kThreads, kSampleItems, int>;
   alignas(16) double a[kNP];
   alignas(16) double b[kNP];
+#if LMSB_SMALL_AB
   double2 ab[kNP];            // (a_k, b_k) interleaved for the sweeps
+#endif
   float4 l2[kNP / 2];         // (A_k, A_k+1, -B_k, -B_k+1) for the packed counts
   float rlo[kMaxRuns], rhi[kMaxRuns];  // slope runs of the current sweep (widened)
   int nruns;
@@ -282,7 +293,9 @@ __global__ void __launch_bounds__(kThreads, LMSB_SMALL_MINB) small_fit_kernel(Sm
       sh.a[k] = ak;
       sh.b[k] = bk;
     }
+#if LMSB_SMALL_AB
     sh.ab[k] = make_double2(ak, bk);
+#endif
     alo = fmin(alo, ak);
     ahi = fmax(ahi, ak);
     am = fmax(am, fabs(ak));
@@ -727,7 +740,13 @@ __global__ void __launch_bounds__(kThreads, LMSB_SMALL_MINB) small_fit_kernel(Sm
 #pragma unroll
         for (int t = 0; t < kSweepStep; ++t) {
           // j runs past n only beyond the triangle's end
+#if LMSB_SMALL_AB
           const double2 li = sh.ab[vi[t]], lj = sh.ab[min(vj[t], n - 1)];
+#else
+          const int jj = min(vj[t], n - 1);
+          const double2 li = make_double2(sh.a[vi[t]], sh.b[vi[t]]);
+          const double2 lj = make_double2(sh.a[jj], sh.b[jj]);
+#endif
           const double da = __dsub_rn(li.x, lj.x);
           const double num = __dsub_rn(li.y, lj.y);
           const float da32 = (float)da, num32 = (float)num;
