@@ -1473,17 +1473,14 @@ __global__ void __launch_bounds__(kBigThreads, 1) band_filter_big_kernel(BandFit
 }
 
 template <typename Kern>
-void set_smem(Kern kern, size_t smem, bool* done) {
-  if (!*done) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    *done = true;
-  }
+void set_smem(Kern kern, size_t smem, DeviceOnce* done) {
+  set_max_smem(kern, smem, *done);
 }
 
 template <int kThreads, int kItems>
 void launch_band_t(const BandFit& bf, const BandArgs& ba, int mode, int grid, cudaStream_t st) {
   constexpr size_t smem = sizeof(BandShared<kThreads, kItems>);
-  static bool c0 = false, c1 = false;
+  static DeviceOnce c0, c1;
   if (mode == 0) {
     set_smem(band_bound_kernel<kThreads, kItems>, smem, &c0);
     band_bound_kernel<kThreads, kItems><<<grid, kThreads, smem, st>>>(bf, ba);
@@ -1725,7 +1722,7 @@ void launch_band_filter_big(const BandFit& bf, const BandArgs& ba, const float* 
   band_chunks_kernel<<<1, 32, 0, st>>>(ba.list, ba.nlist, ba.start, ba.end, ba.chunk, false,
                                        ba.chunk_prefix);
   const size_t smem = kSliceRow * sizeof(unsigned);
-  static bool done = false;
+  static DeviceOnce done;
   set_smem(band_filter_big_kernel, smem, &done);
   band_filter_big_kernel<<<grid, kBigThreads, smem, st>>>(bf, ba, store);
 }
@@ -1807,7 +1804,7 @@ __global__ void __launch_bounds__(kTopThreads) band_top_kernel(const double* __r
 void launch_band_coarse(const BandFit& bf, const BandArgs& ba, int grid, cudaStream_t st) {
   if (grid <= 0) return;
   constexpr size_t smem = (kCoarseBins + 1) * sizeof(unsigned);
-  static bool done = false;
+  static DeviceOnce done;
   set_smem(band_coarse_kernel, smem, &done);
   band_coarse_kernel<<<grid, kCoarseThreads, smem, st>>>(bf, ba);
 }
@@ -1843,7 +1840,7 @@ void launch_band_collect(const BandFit& bf, const BandWork& w, const BandRuns& r
   switch (runs.count) {
 #define LMSB_COLLECT(R)                                                                       \
   case R: {                                                                                   \
-    static bool done = false;                                                                 \
+    static DeviceOnce done;                                                                 \
     set_smem(band_collect_kernel<R>, band_collect_smem(kBandMaxK), &done);                    \
     band_collect_kernel<R><<<sms * 4, kCollectThreads, band_collect_smem(w.K), st>>>(         \
         bf, w.bounds, w.K, w.flag, runs, w.ckeys, w.cvals, cap, w.ncollect);                  \
@@ -1865,7 +1862,7 @@ void launch_band_collect(const BandFit& bf, const BandWork& w, const BandRuns& r
 void launch_band_exact_prepass(const BandFit& bf, const BandCount& bc, int sms, cudaStream_t st) {
   cudaMemsetAsync(bc.out_count, 0, sizeof(unsigned long long), st);
   const size_t smem = (size_t)kPreLines * sizeof(double2) + 64 * sizeof(unsigned);
-  static bool done = false;
+  static DeviceOnce done;
   set_smem(band_exact_prepass_kernel, smem, &done);
   band_exact_prepass_kernel<<<sms, kPreThreads, smem, st>>>(bf, bc.best, bc.in_ranks, bc.in_count,
                                                             bc.out_ranks, bc.out_fits, bc.fit,
@@ -1877,7 +1874,7 @@ void launch_band_count(const BandFit& bf, const BandCount& bc, int sms, cudaStre
   cudaMemsetAsync(bc.out_count, 0, sizeof(unsigned long long), st);
   const size_t smem = (size_t)std::min<int64_t>(bf.n + (bf.n & 1), kBandMaxN) * sizeof(float2) +
                       64 * sizeof(unsigned);
-  static bool done = false;
+  static DeviceOnce done;
   set_smem(band_count_kernel, (size_t)kBandMaxN * sizeof(float2) + 64 * sizeof(unsigned), &done);
   band_count_kernel<<<sms, kCountThreads, smem, st>>>(bf, bc.lines, bc.best, bc.in_ranks,
                                                       bc.in_count, bc.out_ranks, bc.out_fits,

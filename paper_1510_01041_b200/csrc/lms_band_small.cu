@@ -825,12 +825,8 @@ __global__ void __launch_bounds__(kThreads, LMSB_SMALL_MINB) small_fit_kernel(Sm
 template <int kItems>
 void launch_small_t(const SmallArgs& args, int grid, cudaStream_t st) {
   constexpr size_t smem = sizeof(SmallShared<kItems>);
-  static bool done = false;
-  if (!done) {
-    cudaFuncSetAttribute(small_fit_kernel<kItems>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    done = true;
-  }
+  static DeviceOnce done;
+  set_max_smem(small_fit_kernel<kItems>, smem, done);
   small_fit_kernel<kItems><<<grid, kThreads, smem, st>>>(args);
 }
 

@@ -8,6 +8,9 @@
 // uses FMA, and it carries an explicit error margin.
 #pragma once
 
+#include <cuda_runtime.h>
+
+#include <atomic>
 #include <cstdint>
 
 #include "../../include/lms_b200.h"
@@ -103,6 +106,23 @@ __device__ __forceinline__ lms_candidate warp_min_cand(lms_candidate c) {
     if (cand_less(o, c)) c = o;
   }
   return c;
+}
+
+// cudaFuncSetAttribute applies to the current device: remember it per device
+// (bit d of the mask), so a process driving several GPUs (the `par` backend)
+// sets every kernel's shared-memory limit on each of them.
+struct DeviceOnce {
+  std::atomic<unsigned long long> mask{0};
+};
+
+template <typename Kern>
+inline void set_max_smem(Kern kern, size_t smem, DeviceOnce& once) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (once.mask.load(std::memory_order_relaxed) & bit) return;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  once.mask.fetch_or(bit);
 }
 
 // ---------------------------------------------------------------- bulk copy

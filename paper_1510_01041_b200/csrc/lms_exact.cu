@@ -529,15 +529,13 @@ void launch_exact(const ExactArgs& args, int grid, cudaStream_t stream, int64_t 
   if (args.cached && max_n <= kExactCacheN && max_n > kWarpExactMaxN) {
     using SM = SelectSharedT<kCachedThreads / kWarp>;
     const size_t smem = ((sizeof(SM) + 15) & ~size_t(15)) + sizeof(unsigned long long) * max_n;
-    static bool done = false;
-    if (!done) {
-      cudaFuncSetAttribute(exact_cached_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)(((sizeof(SM) + 15) & ~size_t(15)) +
-                                 sizeof(unsigned long long) * kExactCacheN));
-      done = true;
-    }
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    static DeviceOnce done;
+    set_max_smem(exact_cached_kernel,
+                 ((sizeof(SM) + 15) & ~size_t(15)) + sizeof(unsigned long long) * kExactCacheN,
+                 done);
+    int sms = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     exact_cached_kernel<<<sms, kCachedThreads, smem, stream>>>(args);
     if (args.cached_end <= 0) return;
     // the rest of a long list (beyond cached_end) streams
