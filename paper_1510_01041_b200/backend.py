@@ -143,8 +143,13 @@ class ParallelBackend:
     def minimum_bracelet(self, a: np.ndarray, b: np.ndarray, q: int, *,
                          materialize: bool = False) -> CandidateRecord | None:
         devices = max(1, min(self.workers, _native.device_count()))
+        # LMSB_PAR_SHARDS: shard count of the sharded band search (tests run
+        # several shards on one GPU); by default one per visible device
+        shards = int(os.environ.get("LMSB_PAR_SHARDS", devices))
         plan = BatchPlan.create(a, devices)
         parts = plan.partitions()
+        if shards > 1 and not materialize:
+            return _sharded_search(a, b, q, shards, devices)
         if len(parts) <= 1:
             return solve_range(a, b, q, *parts[0], 0, materialize) if parts else None
         with ThreadPoolExecutor(max_workers=len(parts)) as pool:
@@ -155,6 +160,45 @@ class ParallelBackend:
         for rec in results:
             best = merge(best, rec)
         return best
+
+
+_SHARD_CTX: dict = {}
+
+
+def _shard_context(shard: int, device: int):
+    key = (shard, device)
+    if key not in _SHARD_CTX:
+        _SHARD_CTX[key] = _native.Context(device)
+    return _SHARD_CTX[key]
+
+
+def _sharded_search(a: np.ndarray, b: np.ndarray, q: int, shards: int,
+                    devices: int) -> CandidateRecord | None:
+    """The sharded band search (distributed.solve_sharded) over the visible
+    GPUs of this process, one thread and context per shard: each shard bounds
+    its slice of the slope bands, the slices and seeds are joined on the host,
+    each shard searches its BatchPlan partition against the full table, and
+    the records are merged (backend.py:182-187).  Same record as one solve."""
+    from . import distributed
+
+    ctxs = [_shard_context(r, r % devices) for r in range(shards)]
+    with ThreadPoolExecutor(max_workers=shards) as pool:
+        list(pool.map(lambda c: c.upload(a, b), ctxs))
+        plans = list(pool.map(lambda r: ctxs[r].shard_plan(q, shards, r), range(shards)))
+        nbands = plans[0][0]
+        table = (distributed.interleave_band_table([p[1] for p in plans], nbands) if nbands
+                 else plans[0][1])
+        seed = None
+        for p in plans:
+            seed = merge(seed, record_from_native(p[2]))
+        seed_c = _native.Candidate.of(seed)
+        recs = list(pool.map(lambda r: record_from_native(ctxs[r].shard_search(q, shards, r, table,
+                                                                                 seed_c)),
+                             range(shards)))
+    best: CandidateRecord | None = None
+    for rec in recs:
+        best = merge(best, rec)
+    return best
 
 
 _BACKENDS = {"seq": SequentialBackend, "par": ParallelBackend}

@@ -716,3 +716,22 @@ def test_coarse_bounds_on_small_n_and_shards_match(n):
     assert ctx.stats()["bands_refined"] > 0
     _, _, got = _sharded_sequential(ctx, q, 4)
     assert got == want
+
+
+@pytest.mark.parametrize("n,shards", [(16384, 3), (20000, 2)])
+def test_par_backend_sharded_search_matches_seq(n, shards):
+    """The `par` backend's in-process sharded band search (one thread and
+    context per shard; LMSB_PAR_SHARDS puts several shards on this one GPU)
+    returns the seq backend's fit."""
+    pts = workloads.contaminated_line_points(n, 2)
+    want = lms.solve_lms(pts)
+    old = os.environ.get("LMSB_PAR_SHARDS")
+    os.environ["LMSB_PAR_SHARDS"] = str(shards)
+    try:
+        got = lms.solve_lms(pts, backend="par", workers=shards)
+    finally:
+        if old is None:
+            os.environ.pop("LMSB_PAR_SHARDS", None)
+        else:
+            os.environ["LMSB_PAR_SHARDS"] = old
+    assert got == want
