@@ -609,7 +609,7 @@ __device__ __forceinline__ void advance_pair(int n, int step, int& i, int& j) {
 #endif
 template <int kR>
 __global__ void __launch_bounds__(kCollectThreads, LMSB_COLLECT_MINB) band_collect_kernel(
-    BandFit bf, const float* __restrict__ bounds, int K, const uint8_t* __restrict__ flag,
+    BandFit bf, const float* __restrict__ bounds, int K, const int16_t* __restrict__ slot,
     BandRuns runs, uint32_t* __restrict__ out_keys, uint32_t* __restrict__ out_vals, int64_t cap,
     unsigned long long* __restrict__ count) {
   float rlo[kR], rhi[kR];
@@ -622,10 +622,10 @@ __global__ void __launch_bounds__(kCollectThreads, LMSB_COLLECT_MINB) band_colle
   constexpr int kWarps = kCollectThreads / 32;
   uint32_t* queue = reinterpret_cast<uint32_t*>(smem_raw);  // [kWarps][kCollectQueue]
   float* bnd = reinterpret_cast<float*>(queue + kWarps * kCollectQueue);
-  uint8_t* fl = reinterpret_cast<uint8_t*>(bnd + K);
-  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+  int16_t* sl16 = reinterpret_cast<int16_t*>(bnd + K);
+  for (int k = threadIdx.x; k <= K; k += blockDim.x) {
     if (k < K - 1) bnd[k] = bounds[k];
-    fl[k] = flag[k];
+    sl16[k] = slot[k];
   }
   __syncthreads();
   const int lane = threadIdx.x & 31;
@@ -650,7 +650,8 @@ __global__ void __launch_bounds__(kCollectThreads, LMSB_COLLECT_MINB) band_colle
       if (cls == 1) {
         const float bk = band_key(u);
         const int band = band_of(bnd, K - 1, bk);
-        take = fl[band] != 0;
+        const int sb = sl16[band];
+        take = sb >= 0;
         // members of a band ordered by slope: kSlopeBits of fixed-point position
         // between the band's boundaries (monotone in u; 0 in the outer bands)
         uint32_t t = 0;
@@ -659,10 +660,11 @@ __global__ void __launch_bounds__(kCollectThreads, LMSB_COLLECT_MINB) band_colle
           const float f = w > 0.f ? (bk - lo) / w * (float)(1 << kSlopeBits) : 0.f;
           t = (uint32_t)fminf(fmaxf(f, 0.f), (float)((1 << kSlopeBits) - 1));
         }
-        key = ((uint32_t)band << kSlopeBits) | t;
+        // grouped by collection slot (few bits: fewer radix passes), then slope
+        key = ((uint32_t)max(sb, 0) << kSlopeBits) | t;
       } else if (cls == 2) {
         take = true;
-        key = (uint32_t)K << kSlopeBits;
+        key = (uint32_t)sl16[K] << kSlopeBits;
       }
     }
     const unsigned mask = __ballot_sync(0xffffffffu, take);
@@ -1513,7 +1515,7 @@ size_t band_group_temp_bytes(int64_t m) {
 
 size_t band_collect_smem(int K) {
   return (size_t)(kCollectThreads / 32) * kCollectQueue * sizeof(uint32_t) +
-         (size_t)K * (sizeof(float) + sizeof(uint8_t)) + 16;
+         (size_t)K * sizeof(float) + (size_t)(K + 1) * sizeof(int16_t) + 16;
 }
 
 int launch_band_sample(const BandFit& bf, const BandWork& w, int sms, cudaStream_t st) {
@@ -1843,7 +1845,7 @@ void launch_band_collect(const BandFit& bf, const BandWork& w, const BandRuns& r
     static DeviceOnce done;                                                                 \
     set_smem(band_collect_kernel<R>, band_collect_smem(kBandMaxK), &done);                    \
     band_collect_kernel<R><<<sms * 4, kCollectThreads, band_collect_smem(w.K), st>>>(         \
-        bf, w.bounds, w.K, w.flag, runs, w.ckeys, w.cvals, cap, w.ncollect);                  \
+        bf, w.bounds, w.K, w.slot, runs, w.ckeys, w.cvals, cap, w.ncollect);                  \
     break;                                                                                    \
   }
     LMSB_COLLECT(1)
@@ -1917,12 +1919,13 @@ void launch_band_collect_direct(const BandFit& bf, const BandWork& w, const Band
 }
 
 int launch_band_group(const BandWork& w, int64_t m, cudaStream_t st) {
-  cudaMemsetAsync(w.start, 0, sizeof(int64_t) * (w.K + 1), st);
-  cudaMemsetAsync(w.end, 0, sizeof(int64_t) * (w.K + 1), st);
+  cudaMemsetAsync(w.start, 0, sizeof(int64_t) * w.nslot, st);
+  cudaMemsetAsync(w.end, 0, sizeof(int64_t) * w.nslot, st);
   if (m <= 0) return 0;
   size_t bytes = w.temp_bytes;
   if (cub::DeviceRadixSort::SortPairs(w.temp, bytes, w.ckeys, w.ckeys_alt, w.cvals, w.members,
-                                      (int)m, 0, kSlopeBits + bits_for(w.K), st) != cudaSuccess)
+                                      (int)m, 0, kSlopeBits + bits_for(w.nslot - 1), st) !=
+      cudaSuccess)
     return -1;
   band_runs_kernel<<<(int)std::min<int64_t>((m + 255) / 256, 4096), 256, 0, st>>>(
       w.ckeys_alt, m, w.start, w.end);

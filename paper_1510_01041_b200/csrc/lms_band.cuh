@@ -40,7 +40,10 @@ struct BandWork {
   unsigned long long* nvalid;
   float* bounds;          // K - 1
   unsigned* sample_counts;// K
-  uint8_t* flag;          // K: band selected (seeds / collection)
+  uint8_t* flag;          // K: band selected (seeds)
+  const int16_t* slot;    // K + 1: grouping slot of every collected band (-1: not
+                          // collected; entry K: the beyond-range vertices)
+  int nslot;              // slots (collected bands + 1)
   uint32_t* ckeys;        // collected (band, packed i<<16|j), capacity cap
   uint32_t* cvals;
   uint32_t* ckeys_alt;    // grouped copies

@@ -220,6 +220,8 @@ struct lms_ctx {
   DevBuf<int64_t> bslice_seg, bslice_prefix;
   DevBuf<double> bslice_u;
   DevBuf<int32_t> bslice_ids;  // a shard plan's interleaved bands
+  DevBuf<int16_t> bslot;       // grouping slot of every band
+  DevBuf<int32_t> bident;      // 0 .. nslot - 1
   DevBuf<unsigned> bslice_ptab;
   int64_t big_slice = 65536;     // n > 16,384: members per filter slice (LMSB_BIG_SLICE)
   // sort-free band bounds first, exact ones where they cannot dismiss a band
@@ -370,6 +372,8 @@ void ctx_release(lms_ctx* c) {
   c->bslice_prefix.release();
   c->bslice_u.release();
   c->bslice_ids.release();
+  c->bslot.release();
+  c->bident.release();
   c->bslice_ptab.release();
   c->bab.release();
   c->bbig_seg.release();
@@ -719,7 +723,9 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   // small readbacks through pinned staging (truly asynchronous copies)
   const size_t pin_rb = ((size_t)K * (2 * sizeof(double) + sizeof(float) + sizeof(unsigned)) +
                         sizeof(lms_candidate) + 64 + 255) & ~(size_t)255;
-  const size_t pin_up = (size_t)(K + 1) * (2 + 2 * sizeof(int32_t)) + 1024;
+  // flags x2, seed bands, collected bands, grouping slots, slot identity
+  const size_t pin_up = (size_t)(K + 1) * (2 + 2 * sizeof(int32_t) + sizeof(int16_t) +
+                                          sizeof(int32_t)) + 1024;
   // a search's band table goes up through pinned staging as well
   const size_t pin_tab = (sh && sh->mode == 2) ? (size_t)K * (2 * sizeof(double) +
                                                               2 * lmsb::kEdge * sizeof(float)) : 0;
@@ -985,11 +991,30 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   for (int32_t k : list) flag[k] = 1;
   list.push_back(K);  // vertices beyond the key range
   int64_t cap = std::min<int64_t>(span, (int64_t)(2.0 * est * (double)span / (double)S) + 65536);
-  std::memcpy(u_flag2, flag.data(), K);
   std::copy(list.begin(), list.end(), u_list);
-  CUDA_TRY(cudaMemcpyAsync(c->bflag.p, u_flag2, K, cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(cudaMemcpyAsync(c->blist.p, u_list, sizeof(int32_t) * list.size(),
                            cudaMemcpyHostToDevice, c->stream));
+  // grouping slot of every band (its index in `list`, -1 when not collected;
+  // the beyond-range pseudo band last): the grouping sort keys on the slot
+  const int nslot = (int)list.size();
+  {
+    int16_t* u_slot = reinterpret_cast<int16_t*>(u_list + (K + 1));
+    int32_t* u_ident =
+        reinterpret_cast<int32_t*>(((uintptr_t)(u_slot + (K + 1)) + 15) & ~(uintptr_t)15);
+    for (int k = 0; k <= K; ++k) u_slot[k] = -1;
+    for (int e = 0; e < nslot; ++e) {
+      u_slot[list[e]] = (int16_t)e;
+      u_ident[e] = e;
+    }
+    RC_TRY(c->bslot.need(K + 1));
+    RC_TRY(c->bident.need(K + 1));
+    CUDA_TRY(cudaMemcpyAsync(c->bslot.p, u_slot, sizeof(int16_t) * (K + 1), cudaMemcpyHostToDevice,
+                             c->stream));
+    CUDA_TRY(cudaMemcpyAsync(c->bident.p, u_ident, sizeof(int32_t) * nslot,
+                             cudaMemcpyHostToDevice, c->stream));
+    w.slot = c->bslot.p;
+    w.nslot = nslot;
+  }
   // slope runs of the flagged bands for the collect pre-test, merged across the
   // smallest gaps down to kMaxRuns
   std::vector<std::pair<int, int>> rr;
@@ -1199,8 +1224,9 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   RC_TRY(c->bchunks.need((int64_t)std::max<size_t>(list.size(), (size_t)ngroups) + 1));
   ba.members = c->bmem.p;
   if (!direct) {
-    ba.list = c->blist.p;
-    ba.nlist = (int)list.size();
+    ba.list = c->bident.p;       // groups are the slots 0 .. nslot - 1
+    ba.group_band = c->blist.p;  // slot -> band
+    ba.nlist = nslot;
   }
   ba.chunk = c->band_chunk;
   ba.chunk_prefix = c->bchunks.p;
