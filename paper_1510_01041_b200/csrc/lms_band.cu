@@ -540,20 +540,33 @@ __global__ void __launch_bounds__(kThreads, 1) band_filter_kernel(BandFit bf, Ba
 }
 
 // chunk_prefix[e] = first chunk of listed band e (single block; nlist small)
+// one warp: exclusive prefix of the listed groups' chunk counts, 32 groups
+// per step (independent loads, shuffle scan, running carry)
 __global__ void band_chunks_kernel(const int32_t* __restrict__ list, int nlist,
                                    const int64_t* __restrict__ start,
                                    const int64_t* __restrict__ end, int64_t chunk, bool adaptive,
                                    int64_t* __restrict__ prefix) {
-  if (threadIdx.x == 0) {
-    int64_t acc = 0;
-    for (int e = 0; e < nlist; ++e) {
-      prefix[e] = acc;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x >= 32) return;
+  int64_t carry = 0;
+  for (int e0 = 0; e0 < nlist; e0 += 32) {
+    const int e = e0 + lane;
+    int64_t c = 0;
+    if (e < nlist) {
       const int64_t sz = end[list[e]] - start[list[e]];
       const int64_t cs = chunk_size(sz, chunk, adaptive);
-      acc += (sz + cs - 1) / cs;
+      c = (sz + cs - 1) / cs;
     }
-    prefix[nlist] = acc;
+    int64_t incl = c;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int64_t o = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += o;
+    }
+    if (e < nlist) prefix[e] = carry + incl - c;
+    carry += __shfl_sync(0xffffffffu, incl, 31);
   }
+  if (lane == 0) prefix[nlist] = carry;
 }
 
 // seeds: the sampled vertices of the flagged (lowest-bound) bands; also the
