@@ -1587,16 +1587,27 @@ __global__ void band_slice_prefix_kernel(const int32_t* __restrict__ list, int n
                                          const int64_t* __restrict__ start,
                                          const int64_t* __restrict__ end, int64_t chunk,
                                          int64_t slice, int64_t* __restrict__ prefix) {
-  if (threadIdx.x == 0) {
-    int64_t acc = 0;
-    for (int e = 0; e < nlist; ++e) {
-      prefix[e] = acc;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x >= 32) return;
+  int64_t carry = 0;
+  for (int e0 = 0; e0 < nlist; e0 += 32) {
+    const int e = e0 + lane;
+    int64_t c = 0;
+    if (e < nlist) {
       const int64_t sz = end[list[e]] - start[list[e]];
       const int64_t sb = group_slice(sz, chunk, slice);
-      acc += (sz + sb - 1) / sb;
+      c = (sz + sb - 1) / sb;
     }
-    prefix[nlist] = acc;
+    int64_t incl = c;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int64_t o = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += o;
+    }
+    if (e < nlist) prefix[e] = carry + incl - c;
+    carry += __shfl_sync(0xffffffffu, incl, 31);
   }
+  if (lane == 0) prefix[nlist] = carry;
 }
 
 // exact slope of member pair p, or NaN when it is not a banded vertex
