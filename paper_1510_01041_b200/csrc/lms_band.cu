@@ -189,26 +189,6 @@ struct BandShared {
   int kstar;
 };
 
-__device__ __forceinline__ int lower_idx(const float* __restrict__ k, int n, float x) {
-  int lo = 0, hi = n;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (k[mid] < x) lo = mid + 1;
-    else hi = mid;
-  }
-  return lo;
-}
-
-__device__ __forceinline__ int upper_idx(const float* __restrict__ k, int n, float x) {
-  int lo = 0, hi = n;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (k[mid] <= x) lo = mid + 1;
-    else hi = mid;
-  }
-  return lo;
-}
-
 // Two branch-free binary searches in lockstep (independent loads in flight):
 // *lo = first index with k >= xl, *up = first index with k > xu (n >= 1).
 __device__ __forceinline__ void lower_upper(const float* __restrict__ k, int n, float xl, float xu,

@@ -723,18 +723,14 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   // small readbacks through pinned staging (truly asynchronous copies)
   const size_t pin_rb = ((size_t)K * (2 * sizeof(double) + sizeof(float) + sizeof(unsigned)) +
                         sizeof(lms_candidate) + 64 + 255) & ~(size_t)255;
-  // flags x2, seed bands, collected bands, grouping slots, slot identity
-  const size_t pin_up = (size_t)(K + 1) * (2 + 2 * sizeof(int32_t) + sizeof(int16_t) +
-                                          sizeof(int32_t)) + 1024;
+  // upload staging: collected bands (or a shard's slice), grouping slots, slot identity
+  const size_t pin_up = (size_t)(K + 1) * (2 * sizeof(int32_t) + sizeof(int16_t)) + 1024;
   // a search's band table goes up through pinned staging as well
   const size_t pin_tab = (sh && sh->mode == 2) ? (size_t)K * (2 * sizeof(double) +
                                                               2 * lmsb::kEdge * sizeof(float)) : 0;
   RC_TRY(ensure_pinned(c, pin_rb + pin_up + pin_tab));
-  // upload staging after the readbacks: flags x2, seed bands, collected bands
-  uint8_t* u_flag1 = c->pin + pin_rb;
-  uint8_t* u_flag2 = u_flag1 + (K + 1);
-  int32_t* u_seed = reinterpret_cast<int32_t*>(((uintptr_t)(u_flag2 + (K + 1)) + 15) & ~(uintptr_t)15);
-  int32_t* u_list = u_seed + 64;
+  // upload staging after the readbacks
+  int32_t* u_list = reinterpret_cast<int32_t*>(((uintptr_t)(c->pin + pin_rb) + 15) & ~(uintptr_t)15);
   double* p_lb = reinterpret_cast<double*>(c->pin);
   double* p_wq = p_lb + K;
   lms_candidate* p_hb = reinterpret_cast<lms_candidate*>(p_wq + K);
