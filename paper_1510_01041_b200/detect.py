@@ -29,7 +29,7 @@ from .hough import (
     needs_axis_swap,
     polar_to_frame_fit,
 )
-from .solver import LmsFit, solve_lms, solve_lms_batch
+from .solver import _solve_concat, LmsFit, solve_lms, solve_lms_batch
 
 METHOD_SHT = "sht"
 METHOD_OLS = "ols"
@@ -250,11 +250,25 @@ def detect_lines(image: np.ndarray, params: HoughParams, method: str = METHOD_LM
     lms_fits: list[LmsFit] = []
     if method == METHOD_LMS:
         get_backend(backend, workers)  # same name / worker validation as solve_lms
-        designs = []
-        for sup, sw in zip(supports, swapped):
-            t, z = _design_xy(*_thinned_xy(sup, support_cap), sw)
-            designs.append(np.column_stack([t, z]))
-        lms_fits = solve_lms_batch(designs, q)
+        if support_cap is not None and support_cap < 3:
+            raise InvalidInputError(f"support cap must be at least 3, got {support_cap}")
+        # every peak's thinned design in one pair of arrays: the subsample
+        # picks (detect.py:118-131) gathered from the pixel ids, decoded once
+        picks = []
+        for sup in supports:
+            m = sup._ids.size
+            picks.append(sup._ids if support_cap is None or m <= support_cap
+                         else sup._ids[_subsample_index(m, support_cap)])
+        counts = np.array([p.size for p in picks], dtype=np.int64)
+        offsets = np.zeros(len(picks) + 1, dtype=np.int64)
+        offsets[1:] = np.cumsum(counts)
+        row, col = np.divmod(np.concatenate(picks), width)
+        col = col.astype(float)
+        row = row.astype(float)
+        swap = np.repeat(np.array(swapped, dtype=bool), counts)
+        T = np.where(swap, row, col)  # design frame: (y, x) when axis-swapped
+        Z = np.where(swap, col, row)
+        lms_fits = _solve_concat(T, Z, offsets, q)
 
     out: list[LineDetection] = []
     for k, (peak, sup, sw) in enumerate(zip(peaks, supports, swapped)):

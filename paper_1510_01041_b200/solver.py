@@ -153,13 +153,70 @@ def solve_lms_batch(point_sets, q=None) -> list[LmsFit]:
         return []
     offsets = np.zeros(len(sets) + 1, dtype=np.int64)
     offsets[1:] = np.cumsum([x.size for x in xs])
-    X = np.concatenate(xs)
-    Y = np.concatenate(ys)
-    recs = _native.batched(X, Y, offsets, np.asarray(qv, dtype=np.int64))
+    return _solve_concat(np.concatenate(xs), np.concatenate(ys), offsets,
+                         np.asarray(qv, dtype=np.int64), checked=True)
+
+
+def _solve_concat(X: np.ndarray, Y: np.ndarray, offsets: np.ndarray, q, *,
+                  checked: bool = False) -> list[LmsFit]:
+    """Batched solve of the sets X[offsets[k]:offsets[k+1]] (fp64, finite)
+    with the solve_lms tail vectorised over all sets: the checks of
+    validated() in set order unless already `checked`, one batched device
+    call, then the contact sets of fit_from_record computed for every set at
+    once with the same elementwise arithmetic (solver.py:122-140)."""
+    from . import _native
+    from .backend import record_from_native
+
+    F = offsets.size - 1
+    counts = np.diff(offsets)
+    if q is None or isinstance(q, (int, np.integer)):
+        qv = counts // 2 + 1 if q is None else np.full(F, int(q), dtype=np.int64)
+    else:
+        qv = np.asarray(q, dtype=np.int64)
+    if not checked:
+        if counts.size and counts.min() < 3:
+            k = int(np.flatnonzero(counts < 3)[0])
+            if counts[k] == 0:
+                raise InvalidInputError("point set must be nonempty")
+            raise DegenerateInputError(f"LMS needs at least 3 points, got {int(counts[k])}")
+        lo = np.minimum.reduceat(X, offsets[:-1])
+        hi = np.maximum.reduceat(X, offsets[:-1])
+        bad_x = ~(lo < hi)
+        bad_q = (qv < 2) | (qv > counts)
+        if bad_x.any() or bad_q.any():
+            k = int(np.flatnonzero(bad_x | bad_q)[0])
+            if bad_x[k]:
+                raise DegenerateInputError(
+                    "all points share one x-coordinate; no non-vertical line fits")
+            raise InvalidInputError(f"coverage must satisfy 2 <= q <= {int(counts[k])}, got {int(qv[k])}")
+    cands = _native.batched(X, Y, offsets, qv)
+    recs = [record_from_native(c) for c in cands]
+    if any(r is None for r in recs):
+        raise DegenerateInputError("no candidate slab found")
+    u = np.array([r.u for r in recs])
+    vl = np.array([r.v_low for r in recs])
+    vh = np.array([r.v_high for r in recs])
+    gi = offsets[:-1] + np.array([r.i for r in recs], dtype=np.int64)
+    gj = offsets[:-1] + np.array([r.j for r in recs], dtype=np.int64)
+    cut = X * np.repeat(u, counts) - Y
+    anchor = X[gi] * u - Y[gi]
+    cut[gi] = anchor
+    cut[gj] = anchor
+    tol = GEOM_EPS * np.maximum(1.0, np.maximum.reduceat(np.abs(cut), offsets[:-1]))
+    tt = np.repeat(tol, counts)
+    touching = (np.abs(cut - np.repeat(vl, counts)) <= tt) | (np.abs(cut - np.repeat(vh, counts)) <= tt)
+    idx = np.flatnonzero(touching)
+    owner = np.searchsorted(offsets, idx, side="right") - 1
+    local = idx - offsets[owner]
+    bounds = np.searchsorted(owner, np.arange(F + 1))
     fits = []
-    for k, c in enumerate(recs):
-        rec = record_from_native(c)
-        if rec is None:
-            raise DegenerateInputError("no candidate slab found")
-        fits.append(fit_from_record(xs[k], ys[k], qv[k], rec))
+    for k, rec in enumerate(recs):
+        half = (rec.v_high - rec.v_low) * 0.5
+        fits.append(LmsFit(
+            line=LineEq(slope=rec.u, intercept=-(rec.v_low + rec.v_high) * 0.5),
+            lms_value=half * half,
+            slab_height=rec.v_high - rec.v_low,
+            coverage=int(qv[k]),
+            contact_indices=tuple(local[bounds[k]:bounds[k + 1]].tolist()),
+        ))
     return fits
