@@ -33,7 +33,7 @@ def build(verbose: bool = False, extra: list[str] | None = None, out: str | None
     out = out or LIB_PATH
     os.makedirs(os.path.dirname(out), exist_ok=True)
     objs = []
-    common = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+    common = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fopenmp",
               "-I", os.path.join(ROOT, "include"), "--expt-relaxed-constexpr"]
     if verbose:
         common += ["-Xptxas", "-v"]
@@ -53,7 +53,7 @@ def build(verbose: bool = False, extra: list[str] | None = None, out: str | None
         tmp = out + ".tmp"
         # --no-undefined: a symbol missing from the objects fails the link here
         # instead of the load on the GPU box
-        subprocess.run([nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-cudart", "static",
+        subprocess.run([nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-cudart", "static", "-lgomp",
                         "-Xlinker", "--no-undefined"], check=True)
         os.replace(tmp, out)
     finally:

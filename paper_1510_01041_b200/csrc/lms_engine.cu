@@ -186,6 +186,8 @@ struct lms_ctx {
   DevBuf<double> uu, vv;
   lms_candidate* h_best = nullptr;  // pinned
   unsigned char* pin = nullptr;      // pinned staging of the band stage's small readbacks
+  unsigned char* stage = nullptr;    // 2 x 4 MB pinned chunks for large transfers
+  cudaEvent_t ev_stage[2] = {};
   size_t cap_pin = 0;
   int64_t cap_h_best = 0;
   // Hough: the points of the last vote (image pixels or explicit x/y)
@@ -299,6 +301,10 @@ void ctx_release(lms_ctx* c) {
   for (auto& e : c->user_ev)
     if (e) cudaEventDestroy(e);
   for (auto e : c->ev_chunk) cudaEventDestroy(e);
+  for (auto& e : c->ev_stage)
+    if (e) cudaEventDestroy(e);
+  if (c->stage) cudaFreeHost(c->stage);
+  c->stage = nullptr;
   if (c->ev_begin) cudaEventDestroy(c->ev_begin);
   if (c->ev_end) cudaEventDestroy(c->ev_end);
   c->a_own.release();
@@ -442,6 +448,84 @@ int ctx_upload(lms_ctx* c, const double* a, const double* b, int64_t n) {
   c->b = c->b_own.p;
   c->nlines = n;
   cache_line_stats(c);
+  return LMS_OK;
+}
+
+// Host memcpy split over threads (the large pageable <-> pinned copies of
+// the Hough image and supports).
+void par_memcpy(void* dst, const void* src, size_t n) {
+  if (n < ((size_t)1 << 20)) {
+    std::memcpy(dst, src, n);
+    return;
+  }
+  constexpr int kThreadsCopy = 8;
+  const size_t part = ((n + kThreadsCopy - 1) / kThreadsCopy + 63) & ~(size_t)63;
+#pragma omp parallel for num_threads(kThreadsCopy) schedule(static)
+  for (int t = 0; t < kThreadsCopy; ++t) {
+    const size_t o = (size_t)t * part;
+    if (o < n) std::memcpy(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o,
+                           std::min(part, n - o));
+  }
+}
+
+constexpr size_t kStageChunk = (size_t)4 << 20;
+
+int ensure_stage(lms_ctx* c) {
+  if (c->stage) return LMS_OK;
+  CUDA_TRY(cudaMallocHost(&c->stage, 2 * kStageChunk));
+  for (auto& e : c->ev_stage) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  return LMS_OK;
+}
+
+// H2D of a large pageable buffer: threaded copies into two pinned chunks,
+// each DMA overlapping the next chunk's copy (stream-ordered; returns once
+// the last chunk is queued).
+int upload_staged(lms_ctx* c, void* d_dst, const void* h_src, size_t bytes) {
+  if (bytes < 2 * kStageChunk) {
+    CUDA_TRY(cudaMemcpyAsync(d_dst, h_src, bytes, cudaMemcpyHostToDevice, c->stream));
+    return LMS_OK;
+  }
+  RC_TRY(ensure_stage(c));
+  bool used[2] = {false, false};
+  int slot = 0;
+  for (size_t off = 0; off < bytes; off += kStageChunk, slot ^= 1) {
+    const size_t len = std::min(kStageChunk, bytes - off);
+    unsigned char* buf = c->stage + slot * kStageChunk;
+    if (used[slot]) CUDA_TRY(cudaEventSynchronize(c->ev_stage[slot]));
+    par_memcpy(buf, static_cast<const char*>(h_src) + off, len);
+    CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(d_dst) + off, buf, len, cudaMemcpyHostToDevice,
+                             c->stream));
+    CUDA_TRY(cudaEventRecord(c->ev_stage[slot], c->stream));
+    used[slot] = true;
+  }
+  return LMS_OK;
+}
+
+// D2H into a large pageable buffer: chunk k + 1's DMA overlaps chunk k's
+// threaded copy out of pinned memory.  Synchronous.
+int download_staged(lms_ctx* c, void* h_dst, const void* d_src, size_t bytes) {
+  if (bytes < 2 * kStageChunk) {
+    CUDA_TRY(cudaMemcpyAsync(h_dst, d_src, bytes, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return LMS_OK;
+  }
+  RC_TRY(ensure_stage(c));
+  const size_t nchunks = (bytes + kStageChunk - 1) / kStageChunk;
+  auto issue = [&](size_t k) -> int {
+    const size_t off = k * kStageChunk, len = std::min(kStageChunk, bytes - off);
+    unsigned char* buf = c->stage + (k & 1) * kStageChunk;
+    CUDA_TRY(cudaMemcpyAsync(buf, static_cast<const char*>(d_src) + off, len,
+                             cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaEventRecord(c->ev_stage[k & 1], c->stream));
+    return LMS_OK;
+  };
+  RC_TRY(issue(0));
+  for (size_t k = 0; k < nchunks; ++k) {
+    if (k + 1 < nchunks) RC_TRY(issue(k + 1));
+    CUDA_TRY(cudaEventSynchronize(c->ev_stage[k & 1]));
+    const size_t off = k * kStageChunk, len = std::min(kStageChunk, bytes - off);
+    par_memcpy(static_cast<char*>(h_dst) + off, c->stage + (k & 1) * kStageChunk, len);
+  }
   return LMS_OK;
 }
 
@@ -1872,7 +1956,7 @@ int ctx_vote_image(lms_ctx* c, const uint8_t* img, int64_t height, int64_t width
   RC_TRY(c->ext_tmp.need((int64_t)lmsb::extract_temp_bytes(std::max<int64_t>(npix, 1))));
   int64_t npts = 0;
   if (npix > 0) {
-    CUDA_TRY(cudaMemcpyAsync(c->img.p, img, npix, cudaMemcpyHostToDevice, c->stream));
+    RC_TRY(upload_staged(c, c->img.p, img, (size_t)npix));
     size_t tb = (size_t)c->ext_tmp.cap;
     if (lmsb::hough_extract(c->img.p, npix, threshold, c->pix.p, c->pcount.p, c->ext_tmp.p, &tb,
                             c->stream) != 0)
@@ -1964,14 +2048,12 @@ int ctx_support(lms_ctx* c, const double* cos_p, const double* sin_p, const int6
     }
     for (int q = 0; q < np; ++q) offsets[g0 + q + 1] = total + goff[(int64_t)(q + 1) * nb];
     if (out && total + group_total <= capacity && group_total > 0)
-      CUDA_TRY(cudaMemcpyAsync(out + total, c->sout.p, sizeof(int64_t) * group_total,
-                               cudaMemcpyDeviceToHost, c->stream));
+      RC_TRY(download_staged(c, out + total, c->sout.p, sizeof(int64_t) * group_total));
     if (out32 && total + group_total <= capacity && group_total > 0) {
       // half the download: indices narrowed on the device
       RC_TRY(c->sout32.need(group_total));
       lmsb::launch_narrow_i32(c->sout.p, c->sout32.p, group_total, c->stream);
-      CUDA_TRY(cudaMemcpyAsync(out32 + total, c->sout32.p, sizeof(int32_t) * group_total,
-                               cudaMemcpyDeviceToHost, c->stream));
+      RC_TRY(download_staged(c, out32 + total, c->sout32.p, sizeof(int32_t) * group_total));
     }
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     total += group_total;
