@@ -143,14 +143,34 @@ def solve_lms_batch(point_sets, q=None) -> list[LmsFit]:
         qs = list(q)
         if len(qs) != len(sets):
             raise InvalidInputError(f"got {len(qs)} coverages for {len(sets)} point sets")
+    if not sets:
+        return []
+    if all(isinstance(p, np.ndarray) and p.ndim == 2 and p.shape[1] == 2 and p.shape[0] > 0
+           for p in sets):
+        # fast path: (n, 2) arrays, validated all at once (same checks, same
+        # order of the first failure)
+        counts = np.array([p.shape[0] for p in sets], dtype=np.int64)
+        offsets = np.zeros(len(sets) + 1, dtype=np.int64)
+        offsets[1:] = np.cumsum(counts)
+        P = np.concatenate([np.asarray(p, dtype=float) for p in sets])
+        fin = np.isfinite(P).all(axis=1)
+        if not fin.all():
+            bad = np.flatnonzero(~fin)[0]
+            k = int(np.searchsorted(offsets, bad, side="right") - 1)
+            # the sets before k are valid; report k's error as validated() would
+            for j in range(k):
+                validated(sets[j], qs[j])
+            validated(sets[k], qs[k])
+        qv = np.array([default_coverage(int(c)) if qq is None else int(qq)
+                       for c, qq in zip(counts, qs)], dtype=np.int64)
+        return _solve_concat(np.ascontiguousarray(P[:, 0]), np.ascontiguousarray(P[:, 1]), offsets,
+                             qv)
     xs, ys, qv = [], [], []
     for pts, qq in zip(sets, qs):
         x, y, qq = validated(pts, qq)
         xs.append(x)
         ys.append(y)
         qv.append(qq)
-    if not sets:
-        return []
     offsets = np.zeros(len(sets) + 1, dtype=np.int64)
     offsets[1:] = np.cumsum([x.size for x in xs])
     return _solve_concat(np.concatenate(xs), np.concatenate(ys), offsets,
@@ -174,17 +194,19 @@ def _solve_concat(X: np.ndarray, Y: np.ndarray, offsets: np.ndarray, q, *,
     else:
         qv = np.asarray(q, dtype=np.int64)
     if not checked:
-        if counts.size and counts.min() < 3:
-            k = int(np.flatnonzero(counts < 3)[0])
+        # validated()'s checks per set, the first failing set reported
+        small = counts < 3
+        starts = np.minimum(offsets[:-1], max(X.size - 1, 0))
+        lo = np.minimum.reduceat(X, starts) if X.size else np.zeros(F)
+        hi = np.maximum.reduceat(X, starts) if X.size else np.zeros(F)
+        bad_x = ~small & ~(lo < hi)
+        bad_q = ~small & ~bad_x & ((qv < 2) | (qv > counts))
+        if small.any() or bad_x.any() or bad_q.any():
+            k = int(np.flatnonzero(small | bad_x | bad_q)[0])
             if counts[k] == 0:
                 raise InvalidInputError("point set must be nonempty")
-            raise DegenerateInputError(f"LMS needs at least 3 points, got {int(counts[k])}")
-        lo = np.minimum.reduceat(X, offsets[:-1])
-        hi = np.maximum.reduceat(X, offsets[:-1])
-        bad_x = ~(lo < hi)
-        bad_q = (qv < 2) | (qv > counts)
-        if bad_x.any() or bad_q.any():
-            k = int(np.flatnonzero(bad_x | bad_q)[0])
+            if small[k]:
+                raise DegenerateInputError(f"LMS needs at least 3 points, got {int(counts[k])}")
             if bad_x[k]:
                 raise DegenerateInputError(
                     "all points share one x-coordinate; no non-vertical line fits")

@@ -122,3 +122,35 @@ def test_workload_generators_match_golden_inputs(golden):
     for s in (0, 1):
         assert np.array_equal(workloads.config1_points(s), by_name[f"config1_s{s}"].points)
     assert np.array_equal(workloads.contaminated_line_points(2000, 0), by_name["config2_gen_n2000_s0"].points)
+
+
+def test_batch_validation_fast_path_matches_per_set_order():
+    """solve_lms_batch's vectorised validation raises what the per-set
+    validated() loop raises first (before any device work)."""
+    import numpy as np
+
+    from paper_1510_01041_b200 import solver
+
+    good = np.array([[1.0, 2.0], [2.0, 3.0], [3.0, 5.0], [4.0, 1.0]])
+    cases = [
+        [np.zeros((5, 2)), np.array([[1.0, 2.0], [2.0, 3.0]])],
+        [good, np.array([[1.0, 2.0], [2.0, 3.0]])],
+        [good, np.array([[1.0, 2.0], [np.nan, 1.0], [3.0, 4.0]])],
+        [good, np.array([[1.0, 2.0], [1.0, 1.0], [1.0, 4.0]]), np.zeros((2, 2))],
+    ]
+    for sets in cases:
+        for q in (None, 3, 7):
+            want = None
+            for p in sets:
+                try:
+                    solver.validated(p, q)
+                except ValueError as e:
+                    want = e
+                    break
+            assert want is not None
+            try:
+                solver.solve_lms_batch(sets, q)
+            except ValueError as got:
+                assert (type(got), str(got)) == (type(want), str(want)), (sets, q)
+            else:
+                raise AssertionError("no error raised")
