@@ -688,7 +688,9 @@ __global__ void __launch_bounds__(kCollectThreads, LMSB_COLLECT_MINB) band_colle
     // unless num32 is subnormal (passes below) or u32 underflows (absolute
     // error < 1.2e-38, inside the runs' 1e-37 absolute widening).
     const float u32 = num32 * rcp_approx_ftz(da32);
-    bool cand = !(fabsf(u32) <= FLT_MAX) | ((fabsf(num32) < 1e-30f) & (num != 0.0));
+    // (|num32| < 1e-30 includes num == 0 exactly: horizontal pairs go to the
+    // exact band lookup, which is correct and rare outside integer data)
+    bool cand = !(fabsf(u32) <= FLT_MAX) | (fabsf(num32) < 1e-30f);
 #pragma unroll
     for (int k = 0; k < kR; ++k) cand |= (u32 >= rlo[k]) & (u32 <= rhi[k]);
     return cand & (da != 0.0);
