@@ -126,6 +126,11 @@ int lms_min_bracelet_materialized_f64(const double* a, const double* b, int64_t 
  * minimum over all of the fit's pair ranks.  offsets[0] == 0. */
 int lms_batched_f64(const double* x, const double* y, const int64_t* offsets, const int64_t* q,
                     int64_t nfits, int device, lms_candidate* out);
+/* lms_batched_f64 plus the solve_lms tail on the device: contact_flags[k]
+ * (one per point, offsets[nfits] of them) is 1 when point k touches its
+ * fit's slab edges within GEOM_EPS max(1, max |cut|) (solver.py:122-140). */
+int lms_batched_fit_f64(const double* x, const double* y, const int64_t* offsets, const int64_t* q,
+                        int64_t nfits, int device, lms_candidate* out, uint8_t* contact_flags);
 
 /* oracle_lms (solver.py:143-196), the reference's independent primal brute
  * force: per pair slope, sorted intercepts, narrowest q-window (first

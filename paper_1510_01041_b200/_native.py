@@ -130,6 +130,8 @@ SIGNATURES = {
     "lms_solve_fit_f64": (ctypes.c_int, [_D, _D, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, _C, _I,
                                          ctypes.c_int64, _I]),
     "lms_batched_f64": (ctypes.c_int, [_D, _D, _I, _I, ctypes.c_int64, ctypes.c_int, _C]),
+    "lms_batched_fit_f64": (ctypes.c_int, [_D, _D, _I, _I, ctypes.c_int64, ctypes.c_int, _C,
+                                           ctypes.POINTER(ctypes.c_uint8)]),
     "lms_primal_brute_f64": (ctypes.c_int, [_D, _D, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, _C]),
     "lms_hough_vote_u8": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
                                          _D, _D, ctypes.c_int64, ctypes.c_double, ctypes.c_double,
@@ -271,6 +273,19 @@ def min_bracelet_materialized(a, b, q: int, rank_begin: int, rank_end: int,
     check(lib.lms_min_bracelet_materialized_f64(_dp(a), _dp(b), a.size, int(q), int(rank_begin),
                                                 int(rank_end), int(device), ctypes.byref(out)))
     return out
+
+
+def batched_fit(x, y, offsets, q, device: int = 0):
+    """lms_batched_fit_f64: the records and one contact flag per point."""
+    lib = _lib_ready()
+    x, y = _f64(x), _f64(y)
+    offsets, q = _i64(offsets), _i64(q)
+    nfits = offsets.size - 1
+    out = (Candidate * max(nfits, 1))()
+    flags = np.zeros(max(int(offsets[-1]), 1), dtype=np.uint8)
+    check(lib.lms_batched_fit_f64(_dp(x), _dp(y), _ip(offsets), _ip(q), nfits, int(device), out,
+                                  flags.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8))))
+    return out, flags[: int(offsets[-1])]
 
 
 def batched(x, y, offsets, q, device: int = 0) -> list:

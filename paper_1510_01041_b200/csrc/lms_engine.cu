@@ -223,6 +223,8 @@ struct lms_ctx {
   DevBuf<double> bslice_u;
   DevBuf<int32_t> bslice_ids;  // a shard plan's interleaved bands
   DevBuf<int16_t> bslot;       // grouping slot of every band
+  DevBuf<int64_t> boffs;       // batched contacts: fit offsets
+  DevBuf<uint8_t> bcflags;     // batched contacts: one flag per point
   DevBuf<int32_t> bident;      // 0 .. nslot - 1
   DevBuf<unsigned> bslice_ptab;
   int64_t big_slice = 65536;     // n > 16,384: members per filter slice (LMSB_BIG_SLICE)
@@ -379,6 +381,8 @@ void ctx_release(lms_ctx* c) {
   c->bslice_u.release();
   c->bslice_ids.release();
   c->bslot.release();
+  c->boffs.release();
+  c->bcflags.release();
   c->bident.release();
   c->bslice_ptab.release();
   c->bab.release();
@@ -2177,6 +2181,30 @@ int lms_batched_f64(const double* x, const double* y, const int64_t* offsets, co
   std::lock_guard<std::mutex> lk(c->mu);
   RC_TRY(ctx_upload(c, x, y, offsets[nfits]));
   return ctx_solve_batch(c, offsets, q, nfits, out);
+}
+
+int lms_batched_fit_f64(const double* x, const double* y, const int64_t* offsets, const int64_t* q,
+                        int64_t nfits, int device, lms_candidate* out, uint8_t* contact_flags) {
+  if (!offsets || nfits < 0 || (nfits > 0 && (!out || !x || !y || !q || !contact_flags)))
+    return set_error(LMS_ERR_INVALID, "null argument");
+  if (nfits == 0) return LMS_OK;
+  if (offsets[0] != 0) return set_error(LMS_ERR_INVALID, "offsets[0] must be 0");
+  lms_ctx* c = nullptr;
+  RC_TRY(shared_ctx(device, &c));
+  std::lock_guard<std::mutex> lk(c->mu);
+  const int64_t N = offsets[nfits];
+  RC_TRY(ctx_upload(c, x, y, N));
+  RC_TRY(ctx_solve_batch(c, offsets, q, nfits, out));
+  // the fits' records are in c->best (fit-local anchors)
+  RC_TRY(c->boffs.need(nfits + 1));
+  RC_TRY(c->bcflags.need(std::max<int64_t>(N, 1)));
+  CUDA_TRY(cudaMemcpyAsync(c->boffs.p, offsets, sizeof(int64_t) * (nfits + 1),
+                           cudaMemcpyHostToDevice, c->stream));
+  lmsb::launch_contacts_batch(c->a, c->b, c->boffs.p, c->best.p, nfits, c->bcflags.p, c->sms,
+                              c->stream);
+  CUDA_TRY(cudaGetLastError());
+  RC_TRY(download_staged(c, contact_flags, c->bcflags.p, (size_t)N));
+  return LMS_OK;
 }
 
 int lms_primal_brute_f64(const double* x, const double* y, int64_t n, int64_t q, int device,

@@ -623,6 +623,55 @@ __global__ void contacts_collect_kernel(const double* __restrict__ a, const doub
 }
 }  // namespace
 
+// Batched contact sets: one CTA per fit (grid-stride over fits), the fit's
+// max |cut| by a block reduction, then a flag per point (fit-local anchors
+// snapped as in contact_cut).
+__global__ void __launch_bounds__(256) contacts_batch_kernel(const double* __restrict__ a,
+                                                             const double* __restrict__ b,
+                                                             const int64_t* __restrict__ offs,
+                                                             const lms_candidate* __restrict__ recs,
+                                                             int64_t nfits,
+                                                             uint8_t* __restrict__ flags) {
+  __shared__ unsigned long long red[8];
+  for (int64_t f = blockIdx.x; f < nfits; f += gridDim.x) {
+    const int64_t o = offs[f], n = offs[f + 1] - o;
+    const lms_candidate r = recs[f];
+    if (!r.found) {
+      for (int64_t k = threadIdx.x; k < n; k += blockDim.x) flags[o + k] = 0;
+      continue;
+    }
+    unsigned long long m = 0;
+    for (int64_t k = threadIdx.x; k < n; k += blockDim.x) {
+      const unsigned long long v =
+          (unsigned long long)__double_as_longlong(fabs(contact_cut(a + o, b + o, k, r.i, r.j, r.u)));
+      m = v > m ? v : m;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const unsigned long long x = __shfl_xor_sync(0xffffffffu, m, off);
+      m = x > m ? x : m;
+    }
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    m = red[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = red[w] > m ? red[w] : m;
+    const double tol = 1e-9 * fmax(1.0, __longlong_as_double((long long)m));
+    for (int64_t k = threadIdx.x; k < n; k += blockDim.x) {
+      const double x = contact_cut(a + o, b + o, k, r.i, r.j, r.u);
+      flags[o + k] = (fabs(__dsub_rn(x, r.v_low)) <= tol || fabs(__dsub_rn(x, r.v_high)) <= tol);
+    }
+    __syncthreads();  // red reused by the next fit
+  }
+}
+
+void launch_contacts_batch(const double* a, const double* b, const int64_t* offs,
+                           const lms_candidate* recs, int64_t nfits, uint8_t* flags, int sms,
+                           cudaStream_t st) {
+  if (nfits <= 0) return;
+  const int grid = (int)std::min<int64_t>(nfits, (int64_t)sms * 8);
+  contacts_batch_kernel<<<grid, 256, 0, st>>>(a, b, offs, recs, nfits, flags);
+}
+
 void launch_contacts(const double* a, const double* b, int64_t n, const lms_candidate& rec,
                      unsigned long long* scratch, int64_t* out, int64_t cap, int sms,
                      cudaStream_t st) {

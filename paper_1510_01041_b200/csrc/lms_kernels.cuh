@@ -90,6 +90,12 @@ void launch_contacts(const double* a, const double* b, int64_t n, const lms_cand
                      unsigned long long* scratch, int64_t* out, int64_t cap, int sms,
                      cudaStream_t st);
 
+// Contact flags of every point of a batch (offs: F + 1 device offsets, recs:
+// the fits' records on the device, fit-local i / j).
+void launch_contacts_batch(const double* a, const double* b, const int64_t* offs,
+                           const lms_candidate* recs, int64_t nfits, uint8_t* flags, int sms,
+                           cudaStream_t st);
+
 // Seeds: stratified vertex samples per fit; seed_prefix[f] = first seed of fit f.
 void launch_gen_seeds(const FitDesc* fits, const int64_t* seed_prefix, int64_t nfits,
                       int64_t* ranks, int32_t* fit_of, cudaStream_t stream);

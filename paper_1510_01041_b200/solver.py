@@ -211,23 +211,13 @@ def _solve_concat(X: np.ndarray, Y: np.ndarray, offsets: np.ndarray, q, *,
                 raise DegenerateInputError(
                     "all points share one x-coordinate; no non-vertical line fits")
             raise InvalidInputError(f"coverage must satisfy 2 <= q <= {int(counts[k])}, got {int(qv[k])}")
-    cands = _native.batched(X, Y, offsets, qv)
-    recs = [record_from_native(c) for c in cands]
+    # the records and, computed on the device with fit_from_record's
+    # arithmetic, one contact flag per point
+    cands, flags = _native.batched_fit(X, Y, offsets, qv)
+    recs = [record_from_native(cands[k]) for k in range(F)]
     if any(r is None for r in recs):
         raise DegenerateInputError("no candidate slab found")
-    u = np.array([r.u for r in recs])
-    vl = np.array([r.v_low for r in recs])
-    vh = np.array([r.v_high for r in recs])
-    gi = offsets[:-1] + np.array([r.i for r in recs], dtype=np.int64)
-    gj = offsets[:-1] + np.array([r.j for r in recs], dtype=np.int64)
-    cut = X * np.repeat(u, counts) - Y
-    anchor = X[gi] * u - Y[gi]
-    cut[gi] = anchor
-    cut[gj] = anchor
-    tol = GEOM_EPS * np.maximum(1.0, np.maximum.reduceat(np.abs(cut), offsets[:-1]))
-    tt = np.repeat(tol, counts)
-    touching = (np.abs(cut - np.repeat(vl, counts)) <= tt) | (np.abs(cut - np.repeat(vh, counts)) <= tt)
-    idx = np.flatnonzero(touching)
+    idx = np.flatnonzero(flags)
     owner = np.searchsorted(offsets, idx, side="right") - 1
     local = idx - offsets[owner]
     bounds = np.searchsorted(owner, np.arange(F + 1))

@@ -735,3 +735,22 @@ def test_par_backend_sharded_search_matches_seq(n, shards):
         else:
             os.environ["LMSB_PAR_SHARDS"] = old
     assert got == want
+
+
+def test_batched_device_contacts_match_host_tail():
+    """solve_lms_batch's contact sets, flagged on the device
+    (lms_batched_fit_f64), equal fit_from_record's numpy tail for every set:
+    noisy, exact (hundreds of contacts), duplicated and pixel-grid sets."""
+    from paper_1510_01041_b200.solver import fit_from_record, validated
+
+    rng = np.random.default_rng(12)
+    sets = [workloads.bench_points(512, seed=s) for s in range(5)]
+    sets.append(workloads.config1_points(1, n=300))
+    x = rng.integers(0, 60, 400).astype(float)
+    sets.append(np.column_stack([x, 2 * x + 3]))
+    sets.append(np.column_stack([rng.integers(0, 64, 256), rng.integers(0, 64, 256)]).astype(float))
+    got = lms.solve_lms_batch(sets)
+    for pts, g in zip(sets, got):
+        xx, yy, q = validated(pts, None)
+        rec = lms.get_backend("seq").minimum_bracelet(xx, yy, q)
+        assert g == fit_from_record(xx, yy, q, rec)
