@@ -152,19 +152,19 @@ def solve_lms_batch(point_sets, q=None) -> list[LmsFit]:
         counts = np.array([p.shape[0] for p in sets], dtype=np.int64)
         offsets = np.zeros(len(sets) + 1, dtype=np.int64)
         offsets[1:] = np.cumsum(counts)
-        P = np.concatenate([np.asarray(p, dtype=float) for p in sets])
-        fin = np.isfinite(P).all(axis=1)
-        if not fin.all():
-            bad = np.flatnonzero(~fin)[0]
-            k = int(np.searchsorted(offsets, bad, side="right") - 1)
-            # the sets before k are valid; report k's error as validated() would
-            for j in range(k):
-                validated(sets[j], qs[j])
-            validated(sets[k], qs[k])
-        qv = np.array([default_coverage(int(c)) if qq is None else int(qq)
-                       for c, qq in zip(counts, qs)], dtype=np.int64)
-        return _solve_concat(np.ascontiguousarray(P[:, 0]), np.ascontiguousarray(P[:, 1]), offsets,
-                             qv)
+        X = np.concatenate([p[:, 0] for p in sets]).astype(float, copy=False)
+        Y = np.concatenate([p[:, 1] for p in sets]).astype(float, copy=False)
+        if not (np.isfinite(X).all() and np.isfinite(Y).all()):
+            for pts, qq in zip(sets, qs):  # raises the first set's error, as the loop below
+                validated(pts, qq)
+        if q is None:
+            qv = counts // 2 + 1
+        elif isinstance(q, (int, np.integer)):
+            qv = np.full(len(sets), int(q), dtype=np.int64)
+        else:
+            qv = np.array([default_coverage(int(c)) if qq is None else int(qq)
+                           for c, qq in zip(counts, qs)], dtype=np.int64)
+        return _solve_concat(X, Y, offsets, qv)
     xs, ys, qv = [], [], []
     for pts, qq in zip(sets, qs):
         x, y, qq = validated(pts, qq)
