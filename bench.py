@@ -243,8 +243,16 @@ def other_configs(device: int, reps: int = 3) -> dict:
     qs = np.full(F, m // 2 + 1, dtype=np.int64)
     ctx.upload(X, Y)
     ms = timed(lambda: ctx.solve_batch(offs, qs))
+    lms.solve_lms_batch(sets)  # warm-up of the public batch path
+    walls4 = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        lms.solve_lms_batch(sets)  # host arrays in, LmsFit objects (with contact sets) out
+        walls4.append(time.perf_counter() - t0)
     res["config4"] = {"workload": "8192 fits x n=512 (bench_points), q=257", "ms_per_batch": ms,
-                      "evals_per_s": F * m * (m * (m - 1) // 2) / (ms / 1e3)}
+                      "evals_per_s": F * m * (m * (m - 1) // 2) / (ms / 1e3),
+                      "e2e_ms": 1e3 * statistics.median(walls4),
+                      "e2e_path": "solve_lms_batch(list of (512, 2) arrays) -> list[LmsFit]"}
     # config 5: detect_lines end to end (host image in, LineDetections out)
     img = workloads.line_image(4096, 4096, 64, 0.30, seed=0)
     params = lms.HoughParams.for_image(4096, 4096, 20.0, 20.0)
