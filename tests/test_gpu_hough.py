@@ -109,3 +109,30 @@ def test_detect_lines_deterministic_and_batched_equals_single():
     for d in a:
         fit = lms.refine_lms(d.support, None, d.axis_swapped, support_cap=256)
         assert (fit.line.slope, fit.line.intercept, fit.lms_value) == (d.slope, d.intercept, d.lms_value)
+
+
+def test_config5_staged_transfers_integrity():
+    """The 4096^2 image upload and the multi-MB support downloads go through
+    the pinned double-buffered staging (chunks of 4 MB): vote totals, lit
+    count, per-peak support sizes, scan order, lit pixels, and the int32 and
+    int64 downloads agreeing."""
+    img = workloads.line_image(4096, 4096, 64, 0.30, seed=0)
+    p = lms.HoughParams.for_image(4096, 4096, 20.0, 20.0)
+    c, s = p.vote_trig()
+    bins, npts = _native.hough_vote_image(img, 128, c, s, p.rho_max, p.delta_rho, p.n_rho)
+    flat = img.ravel()
+    assert npts == int((flat >= 128).sum())
+    assert int(bins.sum()) == npts * len(c)
+    peaks = lms.find_peaks(lms.HoughAccumulator(bins=bins, params=p), 64, 2)
+    trig = [p.support_trig(k.theta_bin) for k in peaks]
+    args = ([t[0] for t in trig], [t[1] for t in trig], [k.rho_bin for k in peaks], p.rho_max,
+            p.delta_rho, p.n_rho)
+    cap = sum(k.votes for k in peaks)
+    off64, ids64 = _native.hough_support(*args, capacity=cap)
+    off32, ids32 = _native.hough_support(*args, capacity=cap, narrow=True)
+    assert ids64.nbytes > 8 * (1 << 20)  # large enough for the staged path
+    assert np.array_equal(off32, off64) and np.array_equal(ids32.astype(np.int64), ids64)
+    assert all(off64[q + 1] - off64[q] == k.votes for q, k in enumerate(peaks))
+    for q in range(len(peaks)):
+        seg = ids64[off64[q]:off64[q + 1]]
+        assert np.all(np.diff(seg) > 0) and np.all(flat[seg] >= 128)
