@@ -426,16 +426,21 @@ void line_stats(const lms_ctx* c, int64_t off, int64_t n, double* alo, double* a
 
 void cache_line_stats(lms_ctx* c) {
   ++c->gen;
-  c->s_alo = INFINITY;
-  c->s_ahi = -INFINITY;
-  c->s_am = 0.0;
-  c->s_bm = 0.0;
-  for (int64_t k = 0; k < c->nlines; ++k) {
-    c->s_alo = std::min(c->s_alo, c->h_a[k]);
-    c->s_ahi = std::max(c->s_ahi, c->h_a[k]);
-    c->s_am = std::max(c->s_am, std::fabs(c->h_a[k]));
-    c->s_bm = std::max(c->s_bm, std::fabs(c->h_b[k]));
+  double alo = INFINITY, ahi = -INFINITY, am = 0.0, bm = 0.0;
+  const double* a = c->h_a.data();
+  const double* b = c->h_b.data();
+  const int64_t n = c->nlines;
+#pragma omp simd reduction(min : alo) reduction(max : ahi, am, bm)
+  for (int64_t k = 0; k < n; ++k) {
+    alo = a[k] < alo ? a[k] : alo;
+    ahi = a[k] > ahi ? a[k] : ahi;
+    am = std::fabs(a[k]) > am ? std::fabs(a[k]) : am;
+    bm = std::fabs(b[k]) > bm ? std::fabs(b[k]) : bm;
   }
+  c->s_alo = alo;
+  c->s_ahi = ahi;
+  c->s_am = am;
+  c->s_bm = bm;
 }
 
 int ctx_upload(lms_ctx* c, const double* a, const double* b, int64_t n) {
