@@ -2142,14 +2142,24 @@ int lms_solve_fit_f64(const double* a, const double* b, int64_t n, int64_t q, in
   RC_TRY(c->counters.need(2));
   lmsb::launch_contacts(c->a, c->b, n, *out, c->counters.p, c->ii.p, n, c->sms, c->stream);
   CUDA_TRY(cudaGetLastError());
-  unsigned long long cnt = 0;
-  CUDA_TRY(cudaMemcpyAsync(&cnt, c->counters.p + 1, sizeof(cnt), cudaMemcpyDeviceToHost,
+  // one round trip for the usual few contacts: the count and the first
+  // kPrefetch indices come back together
+  constexpr int64_t kPrefetch = 1024;
+  RC_TRY(ensure_pinned(c, (kPrefetch + 1) * sizeof(int64_t)));
+  unsigned long long* p_cnt = reinterpret_cast<unsigned long long*>(c->pin);
+  int64_t* p_idx = reinterpret_cast<int64_t*>(c->pin) + 1;
+  const int64_t pre = std::min<int64_t>(kPrefetch, n);
+  CUDA_TRY(cudaMemcpyAsync(p_cnt, c->counters.p + 1, sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(p_idx, c->ii.p, sizeof(int64_t) * pre, cudaMemcpyDeviceToHost,
                            c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
+  const unsigned long long cnt = *p_cnt;
   const int64_t m = std::min<int64_t>((int64_t)cnt, cap);
   if (m > 0) {
     std::vector<int64_t> h((size_t)cnt);
-    CUDA_TRY(cudaMemcpy(h.data(), c->ii.p, sizeof(int64_t) * cnt, cudaMemcpyDeviceToHost));
+    if ((int64_t)cnt <= pre) std::copy(p_idx, p_idx + cnt, h.begin());
+    else CUDA_TRY(cudaMemcpy(h.data(), c->ii.p, sizeof(int64_t) * cnt, cudaMemcpyDeviceToHost));
     std::sort(h.begin(), h.end());
     std::copy(h.begin(), h.begin() + m, contacts);
   }
