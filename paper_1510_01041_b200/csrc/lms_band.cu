@@ -1867,6 +1867,137 @@ void launch_band_collect(const BandFit& bf, const BandWork& w, const BandRuns& r
   }
 }
 
+// Split form of the pass-0 screen for few survivors: (tile of 32 vertices,
+// slice of the lines) work items over the whole GPU, partial window counts
+// added into per-vertex global counters; a second kernel applies the test
+// and clears the counters for the next use.
+__global__ void __launch_bounds__(kPreThreads) band_prepass_count_kernel(
+    BandFit bf, const lms_candidate* __restrict__ best, const int64_t* __restrict__ in_ranks,
+    const unsigned long long* __restrict__ in_count, unsigned* __restrict__ gcnt) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* sl = reinterpret_cast<double2*>(smem_raw);
+  unsigned* cnt = reinterpret_cast<unsigned*>(sl + kPreLines);  // [2][32]
+  const int64_t total = (int64_t)*in_count;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n = (int)bf.n;
+  const int64_t ntiles = (total + 31) / 32;
+  if (ntiles == 0) return;
+  const lms_candidate rec = *best;
+  const int64_t want = ((int64_t)gridDim.x + ntiles - 1) / ntiles;
+  const int nsplit = (int)max((int64_t)1, min(want, (int64_t)((n + 1023) / 1024)));
+  const int64_t nwork = ntiles * nsplit;
+  for (int64_t wk = blockIdx.x; wk < nwork; wk += gridDim.x) {
+    const int64_t tile = wk / nsplit;
+    const int sp = (int)(wk % nsplit);
+    const int L0 = (int)((int64_t)n * sp / nsplit), L1 = (int)((int64_t)n * (sp + 1) / nsplit);
+    const int64_t s = tile * 32 + lane;
+    bool live = s < total;
+    double u = 0.0, v0 = 0.0, bound = INFINITY;
+    if (live) {
+      int64_t i, j;
+      decode_rank(bf.n, in_ranks[s], &i, &j);
+      const double ai = bf.a[i], bi = bf.b[i];
+      const double da = __dsub_rn(ai, bf.a[j]);
+      u = __ddiv_rn(__dsub_rn(bi, bf.b[j]), da);
+      v0 = cut_value(u, ai, bi);
+      if (rec.found) {
+        const bool after = i > rec.i || (i == rec.i && j > rec.j);
+        bound = after ? nextafter(rec.height, -INFINITY) : rec.height;
+      }
+    }
+    if (tid < 64) cnt[tid] = 0u;
+    unsigned cu = 0, cd = 0;
+    for (int c0 = L0; c0 < L1; c0 += kPreLines) {
+      const int cn = min(kPreLines, L1 - c0);
+      __syncthreads();
+      for (int k = tid; k < cn; k += kPreThreads) sl[k] = bf.ab[c0 + k];
+      __syncthreads();
+      const int per = (cn + kPreWarps - 1) / kPreWarps;
+      const int k0 = warp * per, k1 = min(cn, k0 + per);
+#pragma unroll 4
+      for (int k = k0; k < k1; ++k) {
+        const double2 L = sl[k];
+        const double x = cut_value(u, L.x, L.y);
+        const double dx = __dsub_rn(x, v0), dv = __dsub_rn(v0, x);
+        cu += (x >= v0) & (dx <= bound);
+        cd += (x <= v0) & (dv <= bound);
+      }
+    }
+    atomicAdd(cnt + lane, cu);
+    atomicAdd(cnt + 32 + lane, cd);
+    __syncthreads();
+    if (warp == 0 && live) {
+      atomicAdd(gcnt + 2 * s, cnt[lane]);
+      atomicAdd(gcnt + 2 * s + 1, cnt[32 + lane]);
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void band_prepass_select_kernel(BandFit bf, const lms_candidate* __restrict__ best,
+                                           const int64_t* __restrict__ in_ranks,
+                                           const unsigned long long* __restrict__ in_count,
+                                           unsigned* __restrict__ gcnt,
+                                           int64_t* __restrict__ out_ranks,
+                                           int32_t* __restrict__ out_fits, int32_t fit,
+                                           unsigned long long* __restrict__ out_count) {
+  const int64_t total = (int64_t)*in_count;
+  const int lane = threadIdx.x & 31;
+  const lms_candidate rec = *best;
+  const int q = (int)bf.q;
+  for (int64_t s0 = (int64_t)blockIdx.x * blockDim.x; s0 < total; s0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = s0 + threadIdx.x;
+    bool keep = false;
+    int64_t rank = 0;
+    if (s < total) {
+      int64_t i, j;
+      rank = in_ranks[s];
+      decode_rank(bf.n, rank, &i, &j);
+      const double ai = bf.a[i], bi = bf.b[i];
+      const double da = __dsub_rn(ai, bf.a[j]);
+      const double u = __ddiv_rn(__dsub_rn(bi, bf.b[j]), da);
+      const double v0 = cut_value(u, ai, bi);
+      double bound = INFINITY;
+      if (rec.found) {
+        const bool after = i > rec.i || (i == rec.i && j > rec.j);
+        bound = after ? nextafter(rec.height, -INFINITY) : rec.height;
+      }
+      int tu = (int)gcnt[2 * s], td = (int)gcnt[2 * s + 1];
+      gcnt[2 * s] = 0u;  // cleared for the next use
+      gcnt[2 * s + 1] = 0u;
+      const double xj = cut_value(u, bf.a[j], bf.b[j]);
+      tu += 1 - (int)((xj >= v0) & (__dsub_rn(xj, v0) <= bound));
+      td += 1 - (int)((xj <= v0) & (__dsub_rn(v0, xj) <= bound));
+      keep = da != 0.0 && bound >= 0.0 && (!isfinite(bound) || tu >= q || td >= q);
+    }
+    const unsigned mask = __ballot_sync(0xffffffffu, keep);
+    if (mask) {
+      unsigned long long base = 0;
+      const int leader = __ffs(mask) - 1;
+      if (lane == leader) base = atomicAdd(out_count, (unsigned long long)__popc(mask));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (keep) {
+        const unsigned slot = __popc(mask & ((1u << lane) - 1u));
+        out_ranks[base + slot] = rank;
+        out_fits[base + slot] = fit;
+      }
+    }
+  }
+}
+
+void launch_band_prepass_split(const BandFit& bf, const BandCount& bc, unsigned* gcnt, int sms,
+                               cudaStream_t st) {
+  cudaMemsetAsync(bc.out_count, 0, sizeof(unsigned long long), st);
+  const size_t smem = (size_t)kPreLines * sizeof(double2) + 64 * sizeof(unsigned);
+  static DeviceOnce done;
+  set_smem(band_prepass_count_kernel, smem, &done);
+  band_prepass_count_kernel<<<sms, kPreThreads, smem, st>>>(bf, bc.best, bc.in_ranks, bc.in_count,
+                                                            gcnt);
+  band_prepass_select_kernel<<<sms * 2, 256, 0, st>>>(bf, bc.best, bc.in_ranks, bc.in_count, gcnt,
+                                                      bc.out_ranks, bc.out_fits, bc.fit,
+                                                      bc.out_count);
+}
+
 void launch_band_exact_prepass(const BandFit& bf, const BandCount& bc, int sms, cudaStream_t st) {
   cudaMemsetAsync(bc.out_count, 0, sizeof(unsigned long long), st);
   const size_t smem = (size_t)kPreLines * sizeof(double2) + 64 * sizeof(unsigned);

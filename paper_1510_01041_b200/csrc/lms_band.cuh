@@ -187,5 +187,10 @@ void launch_band_count(const BandFit& bf, const BandCount& bc, int sms, cudaStre
 // *bc.in_count) against the record bc.best: the vertices the exact select
 // would not prune go to bc.out_*; lines from bf.ab
 void launch_band_exact_prepass(const BandFit& bf, const BandCount& bc, int sms, cudaStream_t st);
+// the same screen with the lines split over several CTAs per 32-vertex tile
+// (few survivors: the whole GPU busy); gcnt: 2 counters per survivor, zero
+// on entry and left zero
+void launch_band_prepass_split(const BandFit& bf, const BandCount& bc, unsigned* gcnt, int sms,
+                               cudaStream_t st);
 
 }  // namespace lmsb

@@ -215,6 +215,7 @@ struct lms_ctx {
   DevBuf<float> bedge;
   DevBuf<int32_t> blist;
   DevBuf<int64_t> branks2;
+  DevBuf<unsigned> pcnt;  // split prepass counters (2 per survivor), kept zero
   DevBuf<int32_t> bfits2;
   DevBuf<int64_t> bchunks;
   DevBuf<float> bbig_keys, bbig_store;
@@ -232,6 +233,7 @@ struct lms_ctx {
   // (LMSB_BAND_COARSE: 0 never, 1 always, 2 large n only -- for n <= 16,384
   // one shared-memory sort per band is cheaper than binning plus a refine)
   int band_coarse = 2;
+  int prepass_split = 1;         // pass-0 screen with lines split over CTAs (LMSB_PREPASS_SPLIT)
   int seed_bands = 8;            // bands whose window-edge pairs seed H (LMSB_SEED_BANDS)
   DevBuf<int64_t> bbig_seg;
   DevBuf<int32_t> small_list, dg_i32;
@@ -283,6 +285,7 @@ int ctx_init(lms_ctx* c, int device) {
   if (const char* bs = getenv("LMSB_BIG_SLICE"); bs && atoll(bs) >= 1) c->big_slice = atoll(bs);
   if (const char* sb = getenv("LMSB_SEED_BANDS"); sb && atoi(sb) >= 1)
     c->seed_bands = std::min(48, atoi(sb));
+  if (const char* ps = getenv("LMSB_PREPASS_SPLIT")) c->prepass_split = atoi(ps) != 0;
   if (const char* bc0 = getenv("LMSB_BAND_COARSE")) c->band_coarse = std::max(0, std::min(2, atoi(bc0)));
   const char* sm = getenv("LMSB_SMALL");
   c->small_mode = sm ? std::max(0, std::min(2, atoi(sm))) : 1;
@@ -370,6 +373,7 @@ void ctx_release(lms_ctx* c) {
   c->bedge.release();
   c->blist.release();
   c->branks2.release();
+  c->pcnt.release();
   c->bfits2.release();
   c->bchunks.release();
   c->bbig_keys.release();
@@ -1381,8 +1385,17 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     bp.out_ranks = c->ranks.p;
     bp.out_fits = c->item_fit.p;
     bp.out_count = sc + 6;
-    lmsb::launch_band_exact_prepass(bf, bp, c->sms, c->stream);
-    st->launches += 1;
+    if (c->prepass_split) {
+      if (c->pcnt.cap < 2 * scap) {
+        RC_TRY(c->pcnt.need(2 * scap));
+        CUDA_TRY(cudaMemsetAsync(c->pcnt.p, 0, (size_t)c->pcnt.cap * sizeof(unsigned), c->stream));
+      }
+      lmsb::launch_band_prepass_split(bf, bp, c->pcnt.p, c->sms, c->stream);
+      st->launches += 2;
+    } else {
+      lmsb::launch_band_exact_prepass(bf, bp, c->sms, c->stream);
+      st->launches += 1;
+    }
     RC_TRY(exact_list(sc + 6, scap, c->ranks.p, c->item_fit.p));
   }
   CUDA_TRY(cudaEventRecord(c->ev_chunk[4], c->stream));
