@@ -754,3 +754,27 @@ def test_batched_device_contacts_match_host_tail():
         xx, yy, q = validated(pts, None)
         rec = lms.get_backend("seq").minimum_bracelet(xx, yy, q)
         assert g == fit_from_record(xx, yy, q, rec)
+
+
+@pytest.mark.parametrize("n,seed,qf", [(2000, 11, 0.5), (16384, 3, 0.5), (6000, 5, 0.25),
+                                       (3000, 9, 0.0)])
+def test_split_prepass_matches_single_cta_prepass(n, seed, qf):
+    """The split pass-0 screen (LMSB_PREPASS_SPLIT=1, default: line slices over
+    several CTAs, partial counts in global counters that it leaves zero) and
+    the one-CTA-per-tile screen give the same record, on repeated solves
+    through the same context (the counters must be clean each time) and on
+    q = 2 (huge tied survivor lists)."""
+    pts = workloads.contaminated_line_points(n, seed)
+    a, b = pts[:, 0].copy(), pts[:, 1].copy()
+    q = max(2, int(n * qf) + 1)
+    total = n * (n - 1) // 2
+    one = _ctx_with({"LMSB_PREPASS_SPLIT": "0", "LMSB_BAND": "2"})
+    split = _ctx_with({"LMSB_PREPASS_SPLIT": "1", "LMSB_BAND": "2"})
+    one.upload(a, b)
+    split.upload(a, b)
+    want = record_from_native(one.solve(q, 0, total))
+    for _ in range(3):
+        assert record_from_native(split.solve(q, 0, total)) == want
+    half = total // 2
+    assert record_from_native(split.solve(q, half, total)) == record_from_native(
+        one.solve(q, half, total))
