@@ -87,6 +87,14 @@ int grow(T** ptr, int64_t* cap, int64_t need) {
   return LMS_OK;
 }
 
+// Large-n band size (vertices per band = mult * n): fewer, wider bands pay
+// once n > ~36 k (config 3, n = 65,536: 8 -> 18.6 ms, 16 -> 17.9, 32 ->
+// 16.5; n = 40,000: 8 -> 7.35, 16 -> 6.98; n = 20,000-32,768: 8 best).
+int64_t big_band_mult(int64_t knob, int64_t n) {
+  if (knob > 0) return knob;
+  return n >= 57344 ? 32 : n > 36864 ? 16 : 8;
+}
+
 template <typename T>
 struct DevBuf {
   T* p = nullptr;
@@ -203,7 +211,8 @@ struct lms_ctx {
   int band_mode = 1;  // LMSB_BAND: 0 count-filter path only, 1 auto (large fits), 2 always
   int64_t band_vertices = 196608; // target vertices per band (LMSB_BAND_VERTICES)
   int64_t band_chunk = 12288;    // collected members per filter CTA (LMSB_BAND_CHUNK)
-  int64_t big_mult = 8;          // n > 16,384: vertices per band >= big_mult * n (LMSB_BIG_MULT)
+  int64_t big_mult = 0;          // n > 16,384: vertices per band >= big_mult * n (LMSB_BIG_MULT;
+                                 // 0: by n, see big_band_mult)
   DevBuf<float> bsample, bbounds;
   DevBuf<unsigned> bscnt;
   DevBuf<uint8_t> bflag;
@@ -628,7 +637,8 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   // large n: bands of >= 32 n vertices (their keys are sorted in global memory)
   const bool big = h.n > lmsb::kBandMaxN;
   const bool coarse = c->band_coarse == 1 || (c->band_coarse == 2 && big);
-  const int64_t bv = big ? std::max<int64_t>(c->band_vertices, c->big_mult * h.n) : c->band_vertices;
+  const int64_t bv =
+      big ? std::max<int64_t>(c->band_vertices, big_band_mult(c->big_mult, h.n) * h.n) : c->band_vertices;
   const int K = (int)std::max<int64_t>(3, std::min<int64_t>(lmsb::kBandMaxK, (pspan + bv - 1) / bv));
   const int64_t S =
       std::min<int64_t>(pspan, std::min<int64_t>(1 << 20, std::max<int64_t>(64 * K, 1 << 16)));
