@@ -91,6 +91,14 @@ int grow(T** ptr, int64_t* cap, int64_t need) {
 // Large-n band size (vertices per band = mult * n): fewer, wider bands pay
 // once n > ~36 k (config 3, n = 65,536: 8 -> 18.6 ms, 16 -> 17.9, 32 ->
 // 16.5; n = 40,000: 8 -> 7.35, 16 -> 6.98; n = 20,000-32,768: 8 best).
+// Vertices per band: smaller bands for small fits, where the per-band sort
+// is cheap and the tighter bounds prune more (n = 2,048-3,000: 196,608 ->
+// 65,536 is 5-9 % faster; n = 4,096: 98,304 is 11 % faster).
+int64_t band_size(int64_t knob, int64_t n) {
+  if (knob > 0) return knob;
+  return n <= 3072 ? 65536 : n <= 5120 ? 98304 : 196608;
+}
+
 int64_t big_band_mult(int64_t knob, int64_t n) {
   if (knob > 0) return knob;
   return n >= 57344 ? 32 : n > 36864 ? 16 : 8;
@@ -210,7 +218,8 @@ struct lms_ctx {
   DevBuf<int32_t> sout32;
   // slope bands (lms_band.cu)
   int band_mode = 1;  // LMSB_BAND: 0 count-filter path only, 1 auto (large fits), 2 always
-  int64_t band_vertices = 196608; // target vertices per band (LMSB_BAND_VERTICES)
+  int64_t band_vertices = 0;      // target vertices per band (LMSB_BAND_VERTICES; 0: by n,
+                                  // see band_size)
   int64_t band_chunk = 12288;    // collected members per filter CTA (LMSB_BAND_CHUNK)
   int64_t big_mult = 0;          // n > 16,384: vertices per band >= big_mult * n (LMSB_BIG_MULT;
                                  // 0: by n, see big_band_mult)
@@ -638,8 +647,8 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   // large n: bands of >= 32 n vertices (their keys are sorted in global memory)
   const bool big = h.n > lmsb::kBandMaxN;
   const bool coarse = c->band_coarse == 1 || (c->band_coarse == 2 && big);
-  const int64_t bv =
-      big ? std::max<int64_t>(c->band_vertices, big_band_mult(c->big_mult, h.n) * h.n) : c->band_vertices;
+  const int64_t bv0 = band_size(c->band_vertices, h.n);
+  const int64_t bv = big ? std::max<int64_t>(bv0, big_band_mult(c->big_mult, h.n) * h.n) : bv0;
   const int K = (int)std::max<int64_t>(3, std::min<int64_t>(lmsb::kBandMaxK, (pspan + bv - 1) / bv));
   const int64_t S =
       std::min<int64_t>(pspan, std::min<int64_t>(1 << 20, std::max<int64_t>(64 * K, 1 << 16)));
