@@ -93,10 +93,11 @@ int grow(T** ptr, int64_t* cap, int64_t need) {
 // 16.5; n = 40,000: 8 -> 7.35, 16 -> 6.98; n = 20,000-32,768: 8 best).
 // Vertices per band: smaller bands for small fits, where the per-band sort
 // is cheap and the tighter bounds prune more (n = 2,048-3,000: 196,608 ->
-// 65,536 is 5-9 % faster; n = 4,096: 98,304 is 11 % faster).
+// 65,536 is 5-9 % faster; n = 4,096: 98,304 is 11 % faster; n = 8,192:
+// 131,072 is 3-7 % faster).
 int64_t band_size(int64_t knob, int64_t n) {
   if (knob > 0) return knob;
-  return n <= 3072 ? 65536 : n <= 5120 ? 98304 : 196608;
+  return n <= 3072 ? 65536 : n <= 5120 ? 98304 : n <= 12288 ? 131072 : 196608;
 }
 
 int64_t big_band_mult(int64_t knob, int64_t n) {
