@@ -11,8 +11,9 @@ reference; the tests only read this committed file.
 Cases (each cites the reference test it mirrors):
   * known answers: COLLINEAR4 / majority / SQUARE (test_solver.py:18-74),
     duplicates (:212-216), vertical majority (:241-245)
-  * criterion-1 generic + degenerate sets (test_acceptance.py:50-90)
-  * criterion-2 breakdown sets (test_acceptance.py:95-121)
+  * criterion-1 generic + degenerate sets, the reference's full sets: 1,000
+    generic (n in 4..64 x 200 seeds) + 100 degenerate (test_acceptance.py:50-90)
+  * criterion-2 breakdown sets, all 100 seeds (test_acceptance.py:95-121)
   * criterion-8 determinism sets with collapsed x (test_acceptance.py:248-266)
   * normal(0, s) sets of test_solver.py / test_backend.py
   * dyadic exact fits (test_solver.py:162-175)
@@ -120,20 +121,21 @@ def main():
     cases.append(case("kat_cli_bench", [[0, -2], [1, -1.5], [2, -1], [3, -0.5], [0.5, 7], [2.5, -9]], None))
 
     # --- criterion 1: generic and degenerate sets ---
+    # the reference's full sets: 5 sizes x 200 seeds generic, 100 degenerate
     for n in (4, 8, 16, 32, 64):
-        for seed in range(12):
+        for seed in range(200):
             rng = np.random.default_rng([11, n, seed])
             pts = random_points(rng, n)
             q = int(rng.integers(3, n + 1))
             cases.append(case(f"crit1_n{n}_s{seed}", pts, q))
-    for seed in range(40):
+    for seed in range(100):
         rng = np.random.default_rng([12, seed])
         pts = random_points(rng, 16, collapse_x=True)
         q = int(rng.integers(2, 17))
         cases.append(case(f"crit1_degenerate_s{seed}", pts, q))
 
     # --- criterion 2: breakdown with outliers at 1e6 ---
-    for seed in range(20):
+    for seed in range(100):
         rng = np.random.default_rng([22, seed])
         n = 15
         q = n // 2 + 1
