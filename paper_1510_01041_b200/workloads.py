@@ -13,6 +13,8 @@ GPU box.
 
 from __future__ import annotations
 
+import math
+
 import numpy as np
 
 
@@ -63,9 +65,8 @@ def line_image(width: int = 4096, height: int = 4096, lines: int = 64, salt: flo
     (normal angle in [20, 160) degrees, passing within width/4 of the
     centre, pixels kept with probability ``sampling``) plus salt noise.
 
-    Stands in for the reference's gen_synthetic + np.maximum composition
-    (synth.py:132-191, test_detect.py:246-257); the exact raster differs, the
-    workload shape (4096^2 pixels, ~5.1 M lit points at 30% salt) does not.
+    A quick generic generator for tests; the BASELINE config-5 input is
+    ``config5_image`` (the reference's own ``gen_synthetic`` recipe).
     """
     rng = np.random.Generator(np.random.PCG64(np.random.SeedSequence([seed, 0])))
     img = np.zeros((height, width), dtype=np.uint8)
@@ -85,4 +86,49 @@ def line_image(width: int = 4096, height: int = 4096, lines: int = 64, salt: flo
         img[ys[keep], xs[keep]] = 255
     noise = np.random.Generator(np.random.PCG64(np.random.SeedSequence([seed, 1])))
     img[noise.random((height, width)) < salt] = 255
+    return img
+
+
+def config5_specs(seed: int = 0, width: int = 4096, height: int = 4096, lines: int = 64,
+                  sampling: float = 0.5):
+    """The ``lines`` SyntheticSpecs of the config-5 image: normal
+    angle θ ~ U[20°, 160°), the line passing at a signed distance ~ U[−W/4, W/4)
+    from the frame centre, each rendered by ``gen_synthetic(SyntheticSpec(W, H,
+    slope, intercept, sampling_prob=0.5, noise_prob=0, seed=1000·seed + k))``.
+    The (θ, offset) draws come from ``PCG64(SeedSequence([seed, 2]))``."""
+    from .synth import SyntheticSpec
+
+    rng = np.random.Generator(np.random.PCG64(np.random.SeedSequence([seed, 2])))
+    cx, cy = (width - 1) / 2.0, (height - 1) / 2.0
+    specs = []
+    for k in range(lines):
+        th = math.radians(float(rng.uniform(20.0, 160.0)))
+        off = float(rng.uniform(-width / 4.0, width / 4.0))
+        rho = cx * math.cos(th) + cy * math.sin(th) + off
+        slope = -math.cos(th) / math.sin(th)
+        intercept = rho / math.sin(th)
+        specs.append(SyntheticSpec(width=width, height=height, slope=slope, intercept=intercept,
+                                   sampling_prob=sampling, noise_prob=0.0, seed=1000 * seed + k))
+    return specs
+
+
+def config5_image(seed: int = 0, width: int = 4096, height: int = 4096, lines: int = 64,
+                  salt: float = 0.30, render=None) -> np.ndarray:
+    """BASELINE config 5: the ``config5_specs`` lines combined with
+    ``np.maximum`` (as test_detect.py:246-257 combines images), then salt
+    ``PCG64(SeedSequence([seed, 1])).random((H, W)) < salt`` set to 255.
+
+    ``render(spec) -> uint8 image`` defaults to this package's
+    ``synth.render``; the golden script passes the reference's
+    ``gen_synthetic`` to pin the two against each other."""
+    from . import synth
+
+    if render is None:
+        render = lambda sp: synth.render(sp)[0]  # noqa: E731
+    img = np.zeros((height, width), dtype=np.uint8)
+    for sp in config5_specs(seed, width, height, lines):
+        np.maximum(img, render(sp), out=img)
+    if salt > 0.0:
+        noise = np.random.Generator(np.random.PCG64(np.random.SeedSequence([seed, 1])))
+        img[noise.random((height, width)) < salt] = 255
     return img
