@@ -173,7 +173,9 @@ int lms_hough_support_i32(const double* cos_p, const double* sin_p, const int64_
 
 /* Anchored window at each explicit intersection (i[k], j[k], u[k]).  When v
  * is non-NULL the anchors are snapped to v[k] (bracelet_at); when NULL to
- * a[i]*u - b[i] (_evaluate_pairs).  out: m records. */
+ * a[i]*u - b[i] (_evaluate_pairs).  With v non-NULL an index of -1 snaps no
+ * line (the caller has already placed its anchor lines at v).  out: m
+ * records. */
 int lms_eval_vertices_f64(const double* a, const double* b, int64_t n, int64_t q,
                           const int64_t* i, const int64_t* j, const double* u, const double* v,
                           int64_t m, int device, lms_candidate* out);

@@ -113,6 +113,21 @@ def unpack_band_table(table):
 _lib = None
 _lock = threading.Lock()
 
+# The Hough entry points keep the points of the last vote on the device and
+# lms_hough_support reads them, so a vote and the support gather that follows
+# it must not interleave with another thread's vote on the same device: every
+# Hough call holds the device's re-entrant lock, and callers that chain a
+# vote and a gather (detect_lines, supporting_points) hold it across both.
+_hough_locks: dict = {}
+
+
+def hough_lock(device: int = 0) -> threading.RLock:
+    with _lock:
+        lk = _hough_locks.get(int(device))
+        if lk is None:
+            lk = _hough_locks[int(device)] = threading.RLock()
+        return lk
+
 _D = ctypes.POINTER(ctypes.c_double)
 _I = ctypes.POINTER(ctypes.c_int64)
 _C = ctypes.POINTER(Candidate)
@@ -308,7 +323,7 @@ def primal_brute(x, y, q: int, device: int = 0) -> Candidate:
     return out
 
 
-def hough_vote_image(img, threshold: int, cos_t, sin_t, rho_max: float, delta_rho: float,
+def _hough_vote_image_locked(img, threshold: int, cos_t, sin_t, rho_max: float, delta_rho: float,
                      n_rho: int, device: int = 0):
     """lms_hough_vote_u8 -> (acc int64[n_rho, n_theta], number of lit pixels)."""
     lib = _lib_ready()
@@ -324,7 +339,7 @@ def hough_vote_image(img, threshold: int, cos_t, sin_t, rho_max: float, delta_rh
     return acc, npts.value
 
 
-def hough_vote_points(x, y, cos_t, sin_t, rho_max: float, delta_rho: float, n_rho: int,
+def _hough_vote_points_locked(x, y, cos_t, sin_t, rho_max: float, delta_rho: float, n_rho: int,
                       device: int = 0) -> np.ndarray:
     """lms_hough_vote_points -> acc int64[n_rho, n_theta]."""
     lib = _lib_ready()
@@ -336,7 +351,7 @@ def hough_vote_points(x, y, cos_t, sin_t, rho_max: float, delta_rho: float, n_rh
     return acc
 
 
-def hough_support(cos_p, sin_p, rbin_p, rho_max: float, delta_rho: float, n_rho: int,
+def _hough_support_locked(cos_p, sin_p, rbin_p, rho_max: float, delta_rho: float, n_rho: int,
                   capacity: int, device: int = 0, narrow: bool = False):
     """lms_hough_support on the last vote's points -> (offsets[P+1], ids);
     narrow=True: int32 ids through lms_hough_support_i32 (half the download)."""
@@ -356,10 +371,32 @@ def hough_support(cos_p, sin_p, rbin_p, rho_max: float, delta_rho: float, n_rho:
                                    float(delta_rho), int(n_rho), int(device), _ip(offsets), _ip(out),
                                    int(capacity))
     if rc == LMS_ERR_INVALID and offsets[-1] > capacity:
-        return hough_support(cos_p, sin_p, rbin_p, rho_max, delta_rho, n_rho, int(offsets[-1]),
-                             device, narrow)
+        return _hough_support_locked(cos_p, sin_p, rbin_p, rho_max, delta_rho, n_rho,
+                                     int(offsets[-1]), device, narrow)
     check(rc)
     return offsets, out[: offsets[-1]]
+
+
+def hough_vote_image(img, threshold: int, cos_t, sin_t, rho_max: float, delta_rho: float,
+                     n_rho: int, device: int = 0):
+    """lms_hough_vote_u8 -> (acc int64[n_rho, n_theta], number of lit pixels)."""
+    with hough_lock(device):
+        return _hough_vote_image_locked(img, threshold, cos_t, sin_t, rho_max, delta_rho, n_rho, device)
+
+
+def hough_vote_points(x, y, cos_t, sin_t, rho_max: float, delta_rho: float, n_rho: int,
+                      device: int = 0) -> np.ndarray:
+    """lms_hough_vote_points -> acc int64[n_rho, n_theta]."""
+    with hough_lock(device):
+        return _hough_vote_points_locked(x, y, cos_t, sin_t, rho_max, delta_rho, n_rho, device)
+
+
+def hough_support(cos_p, sin_p, rbin_p, rho_max: float, delta_rho: float, n_rho: int,
+                  capacity: int, device: int = 0, narrow: bool = False):
+    """lms_hough_support on the last vote's points -> (offsets[P+1], ids)."""
+    with hough_lock(device):
+        return _hough_support_locked(cos_p, sin_p, rbin_p, rho_max, delta_rho, n_rho, capacity,
+                                     device, narrow)
 
 
 def eval_vertices(a, b, q: int, i, j, u, v=None, device: int = 0):

@@ -26,6 +26,7 @@ from __future__ import annotations
 
 import math
 import os
+import threading
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
 from typing import Iterable, Iterator, Sequence
@@ -145,7 +146,7 @@ class ParallelBackend:
         devices = max(1, min(self.workers, _native.device_count()))
         # LMSB_PAR_SHARDS: shard count of the sharded band search (tests run
         # several shards on one GPU); by default one per visible device
-        shards = int(os.environ.get("LMSB_PAR_SHARDS", devices))
+        shards = _env_shards(devices)
         plan = BatchPlan.create(a, devices)
         parts = plan.partitions()
         if shards > 1 and not materialize:
@@ -162,14 +163,31 @@ class ParallelBackend:
         return best
 
 
+def _env_shards(devices: int) -> int:
+    raw = os.environ.get("LMSB_PAR_SHARDS")
+    if raw is None:
+        return devices
+    try:
+        shards = int(raw)
+    except ValueError:
+        raise InvalidInputError(f"LMSB_PAR_SHARDS must be an integer, got {raw!r}") from None
+    if shards < 1:
+        raise InvalidInputError(f"LMSB_PAR_SHARDS must be positive, got {shards}")
+    return shards
+
+
 _SHARD_CTX: dict = {}
+# The shard contexts are process-global and a sharded search binds its lines
+# to them across three calls (upload, plan, search): one search at a time.
+_SHARD_LOCK = threading.Lock()
 
 
 def _shard_context(shard: int, device: int):
     key = (shard, device)
-    if key not in _SHARD_CTX:
-        _SHARD_CTX[key] = _native.Context(device)
-    return _SHARD_CTX[key]
+    ctx = _SHARD_CTX.get(key)
+    if ctx is None:
+        ctx = _SHARD_CTX[key] = _native.Context(device)
+    return ctx
 
 
 def _sharded_search(a: np.ndarray, b: np.ndarray, q: int, shards: int,
@@ -179,6 +197,13 @@ def _sharded_search(a: np.ndarray, b: np.ndarray, q: int, shards: int,
     its slice of the slope bands, the slices and seeds are joined on the host,
     each shard searches its BatchPlan partition against the full table, and
     the records are merged (backend.py:182-187).  Same record as one solve."""
+    from . import distributed
+
+    with _SHARD_LOCK:
+        return _sharded_search_locked(a, b, q, shards, devices)
+
+
+def _sharded_search_locked(a, b, q, shards, devices):
     from . import distributed
 
     ctxs = [_shard_context(r, r % devices) for r in range(shards)]

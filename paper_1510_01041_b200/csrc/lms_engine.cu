@@ -88,9 +88,6 @@ int grow(T** ptr, int64_t* cap, int64_t need) {
   return LMS_OK;
 }
 
-// Large-n band size (vertices per band = mult * n): fewer, wider bands pay
-// once n > ~36 k (config 3, n = 65,536: 8 -> 18.6 ms, 16 -> 17.9, 32 ->
-// 16.5; n = 40,000: 8 -> 7.35, 16 -> 6.98; n = 20,000-32,768: 8 best).
 // Vertices per band: smaller bands for small fits, where the per-band sort
 // is cheap and the tighter bounds prune more (n = 2,048-3,000: 196,608 ->
 // 65,536 is 5-9 % faster; n = 4,096: 98,304 is 11 % faster; n = 8,192:
@@ -100,6 +97,9 @@ int64_t band_size(int64_t knob, int64_t n) {
   return n <= 3072 ? 65536 : n <= 5120 ? 98304 : n <= 12288 ? 131072 : 196608;
 }
 
+// Large-n band size (vertices per band = mult * n): fewer, wider bands pay
+// once n > ~36 k (config 3, n = 65,536: 8 -> 18.6 ms, 16 -> 17.9, 32 ->
+// 16.5; n = 40,000: 8 -> 7.35, 16 -> 6.98; n = 20,000-32,768: 8 best).
 int64_t big_band_mult(int64_t knob, int64_t n) {
   if (knob > 0) return knob;
   return n >= 57344 ? 32 : n > 36864 ? 16 : 8;
@@ -1862,7 +1862,9 @@ int ctx_eval_explicit(lms_ctx* c, int64_t q, const int64_t* i, const int64_t* j,
   const int64_t n = c->nlines;
   RC_TRY(check_fit(c, 0, n, q));
   for (int64_t s = 0; s < m; ++s) {
-    if (i[s] < 0 || i[s] >= n || j[s] < 0 || j[s] >= n)
+    // with explicit anchor ordinates (v) an index of -1 snaps no line
+    const int64_t lo = (v && !reduce) ? -1 : 0;
+    if (i[s] < lo || i[s] >= n || j[s] < lo || j[s] >= n)
       return set_error(LMS_ERR_INVALID, "vertex %lld has a line index out of range", (long long)s);
     if (reduce && i[s] >= j[s])
       return set_error(LMS_ERR_INVALID, "vertex %lld must have i < j", (long long)s);

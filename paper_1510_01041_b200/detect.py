@@ -228,20 +228,23 @@ def detect_lines(image: np.ndarray, params: HoughParams, method: str = METHOD_LM
         raise InvalidInputError(f"unknown method {method!r}; expected one of {METHODS}")
     img, thr = lit_mask_u8(image, threshold)
     c, s = params.vote_trig()
-    bins, npoints = _native.hough_vote_image(img, thr, c, s, params.rho_max, params.delta_rho,
-                                             params.n_rho)
-    if npoints == 0:
-        return []
-    peaks = find_peaks(HoughAccumulator(bins=bins, params=params), max_peaks, min_votes)
-    if not peaks:
-        return []
-    trig = [params.support_trig(p.theta_bin) for p in peaks]
-    # int32 pixel ids (half the download) whenever the image has < 2^31 pixels
-    offsets, ids = _native.hough_support([t[0] for t in trig], [t[1] for t in trig],
-                                         [p.rho_bin for p in peaks], params.rho_max,
-                                         params.delta_rho, params.n_rho,
-                                         capacity=sum(p.votes for p in peaks),
-                                         narrow=img.size < 2**31)
+    # the support gather reads the points the vote leaves on the device: one
+    # lock across both, so another thread's vote cannot land in between
+    with _native.hough_lock(0):
+        bins, npoints = _native.hough_vote_image(img, thr, c, s, params.rho_max, params.delta_rho,
+                                                 params.n_rho)
+        if npoints == 0:
+            return []
+        peaks = find_peaks(HoughAccumulator(bins=bins, params=params), max_peaks, min_votes)
+        if not peaks:
+            return []
+        trig = [params.support_trig(p.theta_bin) for p in peaks]
+        # int32 pixel ids (half the download) whenever the image has < 2^31 pixels
+        offsets, ids = _native.hough_support([t[0] for t in trig], [t[1] for t in trig],
+                                             [p.rho_bin for p in peaks], params.rho_max,
+                                             params.delta_rho, params.n_rho,
+                                             capacity=sum(p.votes for p in peaks),
+                                             narrow=img.size < 2**31)
     width = img.shape[1]
     supports = [SupportPoints.from_pixels(ids[offsets[k]: offsets[k + 1]], width)
                 for k in range(len(peaks))]

@@ -20,6 +20,7 @@ The combine is expressed over ``torch.distributed`` so the same code runs on
 
 from __future__ import annotations
 
+import threading
 from typing import Callable
 
 import numpy as np
@@ -94,8 +95,9 @@ def solve_distributed(a: np.ndarray, b: np.ndarray, q: int, *, group=None,
         if device is None and dist.get_backend(group) == "nccl":
             device = torch.device("cuda", dev)  # NCCL collectives take device tensors
         ctx = _context(dev)
-        ctx.upload(a, b)
-        return solve_sharded(ctx, q, group=group, device=device)
+        with _solve_lock:  # upload, plan and search bind the lines to one shared context
+            ctx.upload(a, b)
+            return solve_sharded(ctx, q, group=group, device=device)
     n = int(np.asarray(a).size)
     total = n * (n - 1) // 2
     r0, r1 = partition(total, dist.get_world_size(group), dist.get_rank(group))
@@ -104,15 +106,18 @@ def solve_distributed(a: np.ndarray, b: np.ndarray, q: int, *, group=None,
 
 
 _contexts: dict = {}
+_contexts_lock = threading.Lock()
+_solve_lock = threading.Lock()
 
 
 def _context(device: int):
     """This process's engine context on `device` (created on first use)."""
-    if device not in _contexts:
-        from . import _native
+    with _contexts_lock:
+        if device not in _contexts:
+            from . import _native
 
-        _contexts[device] = _native.Context(device)
-    return _contexts[device]
+            _contexts[device] = _native.Context(device)
+        return _contexts[device]
 
 
 def band_slice(nbands: int, world: int, rank: int) -> range:

@@ -58,6 +58,24 @@ def test_golden_bracelets(golden):
                 assert (br.v_low, br.v_high, br.height) == (want["v_low"], want["v_high"], want["height"])
 
 
+def test_bracelet_duplicate_and_absent_anchor_ids():
+    """bracelet_at snaps every line whose source index is i or j and does not
+    raise for absent anchors (geometry.py:199-203), as the reference does
+    (tests/golden/make_golden_bracelet_edges.py)."""
+    import json
+    import os
+
+    rows = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "bracelet_edges_golden.json")))
+    for r in rows:
+        lines = [lms.DualLine(a=a, b=b, source_index=s) for a, b, s in zip(r["a"], r["b"], r["src"])]
+        ip = lms.DualIntersection(u=float.fromhex(r["u"]), v=float.fromhex(r["v"]), i=r["i"], j=r["j"])
+        br = lms.bracelet_at(ip, lines, r["q"])
+        if r["bracelet"] is None:
+            assert br is None
+        else:
+            assert (br.v_low, br.v_high, br.height) == tuple(float.fromhex(h) for h in r["bracelet"])
+
+
 def test_phase2_matches_oracle_and_bracelets(golden):
     _, brs = golden
     for g in brs:

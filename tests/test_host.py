@@ -154,3 +154,28 @@ def test_batch_validation_fast_path_matches_per_set_order():
                 assert (type(got), str(got)) == (type(want), str(want)), (sets, q)
             else:
                 raise AssertionError("no error raised")
+
+
+def test_lit_mask_non_finite_threshold_follows_numpy():
+    """hough.py:102: img >= threshold; a NaN / inf threshold must not reach int()."""
+    from paper_1510_01041_b200.hough import lit_mask_u8
+
+    img = np.array([[0, 127, 128, 255]], dtype=np.uint8)
+    for thr, want in ((math.nan, [0, 0, 0, 0]), (math.inf, [0, 0, 0, 0]), (-math.inf, [1, 1, 1, 1])):
+        m, t = lit_mask_u8(img, thr)
+        assert list((m >= t).ravel().astype(int)) == want
+    m, t = lit_mask_u8(img, 128)
+    assert t == 128 and m is not None
+
+
+def test_par_shards_env_validated(monkeypatch):
+    from paper_1510_01041_b200.backend import _env_shards
+
+    monkeypatch.delenv("LMSB_PAR_SHARDS", raising=False)
+    assert _env_shards(3) == 3
+    monkeypatch.setenv("LMSB_PAR_SHARDS", "2")
+    assert _env_shards(3) == 2
+    for bad in ("x", "0", "-1", "1.5"):
+        monkeypatch.setenv("LMSB_PAR_SHARDS", bad)
+        with pytest.raises(lms.InvalidInputError):
+            _env_shards(1)
