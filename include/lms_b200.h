@@ -88,6 +88,7 @@ typedef struct lms_stats {
   int64_t small_fits;       /* fits of the batch solved by the fused per-fit band kernel */
   int64_t direct_groups;    /* sub-band regions of the direct grouping (0: radix-sort path) */
   int64_t bands_refined;    /* bands whose coarse bound admitted H and got the exact bound */
+  int64_t sweep_runs;       /* slope runs of the sweep collect (0: the pre-test pass ran) */
 } lms_stats;
 
 /* Library identity and device discovery. */

@@ -81,6 +81,7 @@ class Stats(ctypes.Structure):
         ("small_fits", ctypes.c_int64),
         ("direct_groups", ctypes.c_int64),
         ("bands_refined", ctypes.c_int64),
+        ("sweep_runs", ctypes.c_int64),
     ]
 
     def as_dict(self) -> dict:

@@ -59,6 +59,7 @@
 #include <cstdint>
 
 #include "lms_band.cuh"
+#include "lms_band_dev.cuh"
 #include "lms_common.cuh"
 
 namespace lmsb {
@@ -80,17 +81,6 @@ constexpr unsigned kSeedPerBand = 16;  // sampled vertices per seed band (safety
 #endif
 constexpr int kRun = LMSB_COLLECT_RUN;  // ranks per lane per warp segment (lane-interleaved)
 static_assert(kRun % kCollectStep == 0, "whole collect steps per segment");
-
-#ifndef LMSB_SLOPE_BITS
-#define LMSB_SLOPE_BITS 17
-#endif
-constexpr int kSlopeBits = LMSB_SLOPE_BITS;  // within-band slope order bits of a collected key
-
-__device__ __forceinline__ float band_key(double u) {
-  // monotone non-decreasing map of the slope to fp32 (clamped, so ordered)
-  const float f = (float)u;
-  return fminf(fmaxf(f, -FLT_MAX), FLT_MAX);
-}
 
 __device__ __forceinline__ float rcp_approx_ftz(float x) {
   float r;
@@ -119,32 +109,8 @@ __host__ __device__ __forceinline__ int64_t chunk_size(int64_t cnt, int64_t chun
   return nc >= want ? chunk : (cnt + want - 1) / want;
 }
 
-// slope and class of vertex (i, j) exactly as _scan_rank_range forms it
-// (backend.py:200-205): 0 never a window (a_i == a_j or non-finite u),
-// 1 banded, 2 beyond the fp32 key range (always passed to the exact stage)
-__device__ __forceinline__ int classify(const BandFit& bf, double ai, double bi, double aj,
-                                        double bj, double* pu) {
-  const double da = __dsub_rn(ai, aj);
-  if (da == 0.0) return 0;
-  const double u = __ddiv_rn(__dsub_rn(bi, bj), da);
-  if (!isfinite(u)) return 0;
-  *pu = u;
-  return fabs(u) * bf.amax < 1e30 ? 1 : 2;
-}
-
 __device__ __forceinline__ int64_t sample_rank(const BandFit& bf, int64_t S, int64_t s) {
   return bf.P0 + ((2 * s + 1) * bf.pspan) / (2 * S);
-}
-
-// number of boundaries <= key, i.e. the band index
-__device__ __forceinline__ int band_of(const float* __restrict__ bnd, int nb, float key) {
-  int lo = 0, hi = nb;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (bnd[mid] <= key) lo = mid + 1;
-    else hi = mid;
-  }
-  return lo;
 }
 
 __global__ void band_sample_kernel(BandFit bf, int64_t S, float* __restrict__ keys,

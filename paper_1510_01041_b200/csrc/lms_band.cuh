@@ -193,4 +193,47 @@ void launch_band_exact_prepass(const BandFit& bf, const BandCount& bc, int sms, 
 void launch_band_prepass_split(const BandFit& bf, const BandCount& bc, unsigned* gcnt, int sms,
                                cudaStream_t st);
 
+// ---- output-sensitive collect (lms_sweep.cu): the vertices of each admitted
+// slope run as the inversions between the lines' orders at its two ends
+struct SweepEnd {
+  double s;    // kind 0: abscissa of the sort
+  double fin;  // kinds 1/2: the run's finite end (ties of equal slopes)
+  int kind;    // 0 finite, 1 -inf, 2 +inf, 3 sort by slope a
+  int pad;
+};
+struct SweepSort {  // ping-pong (k1, k2, idx) buffers, nseg * n each
+  uint64_t* k1[2];
+  uint64_t* k2[2];
+  uint32_t* idx[2];
+  int cur;  // buffer holding the sorted segments
+};
+struct SweepArgs {
+  const float* bounds;   // K - 1 band boundaries
+  int K;
+  const int16_t* slot;   // K + 1 grouping slots (-1: not collected)
+  int nruns;
+  const int32_t* run_k0;  // per run: first and last band
+  const int32_t* run_k1;
+  const int32_t* P;       // nruns * n
+  const int32_t* bmin;    // nruns * ceil(n / 32)
+  const int32_t* suf;
+  const uint32_t* idx;    // sorted segments (run r: 2r at s0', 2r + 1 at s1')
+  const uint64_t* k1a;    // the slope-sorted segment (near-parallel pass), or null
+  const uint32_t* idxa;
+  double tau;             // pairs with 0 < |a_i - a_j| <= tau: near-parallel pass
+  uint32_t* out_keys;
+  uint32_t* out_vals;
+  int64_t cap;
+  unsigned long long* count;
+};
+size_t sweep_chunk_smem();
+// sort nseg segments of the n lines by their end keys; returns launches
+int launch_sweep_sort(const double2* ab, int n, const SweepEnd* ends, int nseg, SweepSort& ss,
+                      int sms, cudaStream_t st);
+// P, block minima and suffix minima of every run (pos: nruns * n scratch)
+void launch_sweep_prepare(int n, int nruns, const SweepSort& ss, int32_t* pos, int32_t* P,
+                          int32_t* bmin, int32_t* suf, int sms, cudaStream_t st);
+// enumerate and classify; members appended to out_keys / out_vals (count may exceed cap)
+void launch_sweep_emit(const BandFit& bf, const SweepArgs& sa, int sms, cudaStream_t st);
+
 }  // namespace lmsb

@@ -97,6 +97,9 @@ int64_t band_size(int64_t knob, int64_t n) {
   return n <= 3072 ? 65536 : n <= 5120 ? 98304 : n <= 12288 ? 131072 : 196608;
 }
 
+// Most slope runs of the sweep collect (two sorts of the n lines each).
+constexpr int kSweepMaxRuns = 16;
+
 // Large-n band size (vertices per band = mult * n): fewer, wider bands pay
 // once n > ~36 k (config 3, n = 65,536: 8 -> 18.6 ms, 16 -> 17.9, 32 ->
 // 16.5; n = 40,000: 8 -> 7.35, 16 -> 6.98; n = 20,000-32,768: 8 best).
@@ -265,6 +268,11 @@ struct lms_ctx {
   // slower on config 2 (sub-bands are wider than slope-sorted chunks), kept
   // for A/B runs
   int band_direct = 0;
+  int band_sweep = 1;  // LMSB_SWEEP: output-sensitive collect (lms_sweep.cu); 0 = pre-test pass
+  DevBuf<uint64_t> sw_k1, sw_k2;
+  DevBuf<uint32_t> sw_idx;
+  DevBuf<int32_t> sw_pos, sw_P, sw_bmin, sw_suf, sw_rk;
+  DevBuf<lmsb::SweepEnd> sw_ends;
   DevBuf<unsigned long long> small_cnt;
   int small_mode = 1;  // LMSB_SMALL: 0 off, 1 batches, 2 also single fits
   DevBuf<float2> blines32;
@@ -300,6 +308,7 @@ int ctx_init(lms_ctx* c, int device) {
   if (bv && atoll(bv) >= 256) c->band_vertices = atoll(bv);
   const char* bd = getenv("LMSB_BAND_DIRECT");
   c->band_direct = (bd && std::strcmp(bd, "1") == 0) ? 1 : 0;
+  if (const char* sw = getenv("LMSB_SWEEP")) c->band_sweep = atoi(sw) != 0;
   const char* bmul = getenv("LMSB_BIG_MULT");
   if (bmul && atoll(bmul) >= 1) c->big_mult = atoll(bmul);
   if (const char* bs = getenv("LMSB_BIG_SLICE"); bs && atoll(bs) >= 1) c->big_slice = atoll(bs);
@@ -846,7 +855,12 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   // a search's band table goes up through pinned staging as well
   const size_t pin_tab = (sh && sh->mode == 2) ? (size_t)K * (2 * sizeof(double) +
                                                               2 * lmsb::kEdge * sizeof(float)) : 0;
-  RC_TRY(ensure_pinned(c, pin_rb + pin_up + pin_tab));
+  // sweep collect: run ends and band ranges (lms_sweep.cu)
+  const size_t pin_sw = (size_t)kSweepMaxRuns * (2 * sizeof(lmsb::SweepEnd) + 2 * sizeof(int32_t)) +
+                        sizeof(lmsb::SweepEnd) + 64;
+  RC_TRY(ensure_pinned(c, pin_rb + pin_up + pin_tab + pin_sw));
+  unsigned char* u_sweep = reinterpret_cast<unsigned char*>(
+      ((uintptr_t)(c->pin + pin_rb + pin_up + pin_tab) + 15) & ~(uintptr_t)15);
   // upload staging after the readbacks
   int32_t* u_list = reinterpret_cast<int32_t*>(((uintptr_t)(c->pin + pin_rb) + 15) & ~(uintptr_t)15);
   double* p_lb = reinterpret_cast<double*>(c->pin);
@@ -1293,16 +1307,127 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     }
   }
   if (!direct) {
+  // output-sensitive collect: the vertices of each admitted slope run as the
+  // inversions between the lines' orders at its ends (lms_sweep.cu).  Needs
+  // every inner boundary inside the fp32-key range, so that vertices beyond
+  // it (class 2) can only lie in the two outer bands.
+  bool sweep = c->band_sweep && !rr.empty() && h.n >= 3 && h.n <= lmsb::kBandMaxBigN;
+  for (int k = 0; sweep && k < K - 1; ++k)
+    sweep = std::isfinite(hbnd[k]) && std::fabs((double)hbnd[k]) * bf.amax < 1e29;
+  lmsb::SweepArgs sa{};
+  if (sweep) {
+    // runs of flagged bands (outer bands always: class-2 vertices), merged
+    // across the smallest gaps down to kSweepMaxRuns
+    std::vector<std::pair<int, int>> sr;
+    for (int k = 0; k < K; ++k) {
+      if (!(flag[k] || k == 0 || k == K - 1)) continue;
+      if (!sr.empty() && sr.back().second == k - 1) sr.back().second = k;
+      else sr.push_back({k, k});
+    }
+    while ((int)sr.size() > kSweepMaxRuns) {
+      size_t best = 0;
+      for (size_t e = 1; e + 1 < sr.size(); ++e)
+        if (sr[e + 1].first - sr[e].second < sr[best + 1].first - sr[best].second) best = e;
+      sr[best].second = sr[best + 1].second;
+      sr.erase(sr.begin() + best + 1);
+    }
+    const int nr = (int)sr.size();
+    const int nseg = 2 * nr + 1;
+    lmsb::SweepEnd* ends = reinterpret_cast<lmsb::SweepEnd*>(u_sweep);
+    int32_t* rk = reinterpret_cast<int32_t*>(ends + nseg);
+    double tau = 0.0;
+    for (int e = 0; e < nr; ++e) {
+      const int k0 = sr[e].first, k1 = sr[e].second;
+      double lo = -INFINITY, hi = INFINITY;
+      if (k0 > 0) {
+        lo = (double)std::nextafter(hbnd[k0 - 1], -INFINITY);
+        lo -= 0x1p-18 * std::fabs(lo) + 1e-37;
+      }
+      if (k1 < K - 1) {
+        hi = (double)hbnd[k1];
+        hi += 0x1p-18 * std::fabs(hi) + 1e-37;
+      }
+      double m;
+      if (std::isfinite(lo) && std::isfinite(hi))
+        m = 0x1p-20 * std::max(std::fabs(lo), std::fabs(hi)) + 0x1p-14 * (hi - lo) + 1e-30;
+      else
+        m = 0x1p-20 * (std::isfinite(lo) ? std::fabs(lo) : std::isfinite(hi) ? std::fabs(hi) : 0.0) +
+            1e-30;
+      const double s0 = lo - m, s1 = hi + m;
+      double smax = 0.0;
+      if (std::isfinite(s0)) smax = std::fabs(s0);
+      if (std::isfinite(s1)) smax = std::max(smax, std::fabs(s1));
+      const double err = 0x1p-52 * (bf.amax * smax + bf.bmax) + 1e-300;
+      if (std::isfinite(s0) || std::isfinite(s1)) tau = std::max(tau, 4.0 * err / m);
+      const double fin = std::isfinite(s0) ? s0 : std::isfinite(s1) ? s1 : 0.0;
+      ends[2 * e] = lmsb::SweepEnd{std::isfinite(s0) ? s0 : 0.0, fin, std::isfinite(s0) ? 0 : 1, 0};
+      ends[2 * e + 1] = lmsb::SweepEnd{std::isfinite(s1) ? s1 : 0.0, fin, std::isfinite(s1) ? 0 : 2, 0};
+      rk[e] = k0;
+      rk[nr + e] = k1;
+    }
+    ends[2 * nr] = lmsb::SweepEnd{0.0, 0.0, 3, 0};
+    const int64_t nn = h.n;
+    const int64_t nbk = (nn + 31) / 32;
+    RC_TRY(c->sw_k1.need(2 * nseg * nn));
+    RC_TRY(c->sw_k2.need(2 * nseg * nn));
+    RC_TRY(c->sw_idx.need(2 * nseg * nn));
+    RC_TRY(c->sw_pos.need(nr * nn));
+    RC_TRY(c->sw_P.need(nr * nn));
+    RC_TRY(c->sw_bmin.need(nr * nbk));
+    RC_TRY(c->sw_suf.need(nr * nbk));
+    RC_TRY(c->sw_rk.need(2 * nr));
+    RC_TRY(c->sw_ends.need(nseg));
+    CUDA_TRY(cudaMemcpyAsync(c->sw_ends.p, ends, sizeof(lmsb::SweepEnd) * nseg,
+                             cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(c->sw_rk.p, rk, sizeof(int32_t) * 2 * nr, cudaMemcpyHostToDevice,
+                             c->stream));
+    lmsb::SweepSort ss{};
+    for (int b = 0; b < 2; ++b) {
+      ss.k1[b] = c->sw_k1.p + b * nseg * nn;
+      ss.k2[b] = c->sw_k2.p + b * nseg * nn;
+      ss.idx[b] = c->sw_idx.p + b * nseg * nn;
+    }
+    CUDA_TRY(cudaEventRecord(c->ev_chunk[5], c->stream));
+    st->launches += lmsb::launch_sweep_sort(bf.ab, (int)nn, c->sw_ends.p, nseg, ss, c->sms,
+                                            c->stream);
+    lmsb::launch_sweep_prepare((int)nn, nr, ss, c->sw_pos.p, c->sw_P.p, c->sw_bmin.p, c->sw_suf.p,
+                               c->sms, c->stream);
+    CUDA_TRY(cudaGetLastError());
+    st->launches += 3;
+    sa.bounds = c->bbounds.p;
+    sa.K = K;
+    sa.slot = w.slot;
+    sa.nruns = nr;
+    sa.run_k0 = c->sw_rk.p;
+    sa.run_k1 = c->sw_rk.p + nr;
+    sa.P = c->sw_P.p;
+    sa.bmin = c->sw_bmin.p;
+    sa.suf = c->sw_suf.p;
+    sa.idx = ss.idx[ss.cur];
+    sa.k1a = ss.k1[ss.cur] + (int64_t)(2 * nr) * nn;
+    sa.idxa = ss.idx[ss.cur] + (int64_t)(2 * nr) * nn;
+    sa.tau = tau;
+    sa.count = w.ncollect;
+    st->sweep_runs = nr;
+  }
   for (int attempt = 0; attempt < 2; ++attempt) {
     RC_TRY(c->bck.need(cap));
     RC_TRY(c->bcv.need(cap));
     w.ckeys = c->bck.p;
     w.cvals = c->bcv.p;
-    CUDA_TRY(cudaEventRecord(c->ev_chunk[5], c->stream));
-    lmsb::launch_band_collect(bf, w, runs, cap, c->sms, c->stream);
+    if (sweep) {
+      sa.out_keys = w.ckeys;
+      sa.out_vals = w.cvals;
+      sa.cap = cap;
+      lmsb::launch_sweep_emit(bf, sa, c->sms, c->stream);
+      st->launches += 2;
+    } else {
+      CUDA_TRY(cudaEventRecord(c->ev_chunk[5], c->stream));
+      lmsb::launch_band_collect(bf, w, runs, cap, c->sms, c->stream);
+      st->launches += 1;
+    }
     CUDA_TRY(cudaEventRecord(c->ev_chunk[6], c->stream));
     CUDA_TRY(cudaGetLastError());
-    st->launches += 1;
     unsigned long long* p_m = reinterpret_cast<unsigned long long*>(c->pin);
     CUDA_TRY(cudaMemcpyAsync(p_m, sc + 1, sizeof(m), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));

@@ -1,0 +1,472 @@
+// lms_sweep.cu -- output-sensitive collect of the band stage.
+//
+// The band stage must hand the filter every vertex (i, j) whose slope
+// u = (b_i - b_j) / (a_i - a_j) (formed as _scan_rank_range does,
+// backend.py:200-205) falls in a band whose lower bound admits H.  The
+// admitted bands form a few slope runs [s0, s1].  Testing every one of the
+// n(n-1)/2 vertices against the runs is O(n^2); this file enumerates the
+// vertices of each run directly, in O(n log n + K) for K vertices in the run:
+//
+//   Two dual lines v = a u - b cross inside (s0', s1') exactly when their
+//   order by value at s0' differs from their order at s1'.  Sort the lines
+//   by value at both ends; with P[t] = position at s1' of the line at
+//   position t at s0', the crossings are the inversions t < t', P[t'] < P[t].
+//   A warp per t walks t' with per-32 block minima of P (skipping blocks
+//   without a smaller value) and a suffix minimum (stopping when no smaller
+//   value is left), so the work is proportional to the inversions found.
+//
+// Exactness (superset contract, as the pre-test it replaces): the runs are
+// the admitted bands' fp32 extents widened by 2^-18 relative + 1e-37
+// (lms_engine.cu); the sort ends s0' = lo - m and s1' = hi + m add a margin m
+// so every vertex whose fp64 slope lies in the run has its real crossing u*
+// at least m inside (s0', s1').  Keys are fma(a, s, -b) (one rounding,
+// error <= 2^-53 |a s - b|), so two keys' errors sum to at most
+// e = 2^-52 (amax |s| + bmax) + 1e-300; a crossing pair's true values differ
+// at each end by |a_i - a_j| m, so for |a_i - a_j| > tau = 4 e / m the sorted
+// orders are right at both ends and the pair is an inversion.  Pairs with
+// 0 < |a_i - a_j| <= tau (nearly parallel lines) are skipped by the inversion
+// pass and enumerated by a separate pass over the lines sorted by a.  An
+// infinite end (the outer bands) sorts by slope exactly (a descending at
+// -inf, ascending at +inf; equal slopes by their value at the finite end).
+// Every enumerated pair is then classified with the reference's fp64 slope
+// and kept only if its band is an admitted band of this run (or, beyond the
+// fp32 key range, if the run is the outer one on that side), so each member
+// is emitted once and the output is exactly the pre-test collect's member
+// set: same (slot, slope position) keys, same packed i<<16|j values.
+
+#include <cuda_runtime.h>
+
+#include <cfloat>
+#include <climits>
+#include <cmath>
+#include <cstdint>
+
+#include "lms_band.cuh"
+#include "lms_band_dev.cuh"
+#include "lms_common.cuh"
+
+namespace lmsb {
+
+namespace {
+
+constexpr int kChunk = 4096;        // items per CTA-local bitonic sort
+constexpr int kChunkThreads = 1024;
+constexpr int kMergeItems = 8;      // outputs per thread of a merge round
+constexpr int kMergeThreads = 256;
+constexpr int kEnumThreads = 256;
+constexpr int kEnumWarps = kEnumThreads / 32;
+constexpr int kEnumQueue = 64;
+
+__device__ __forceinline__ int64_t i64min(int64_t x, int64_t y) { return x < y ? x : y; }
+__device__ __forceinline__ int64_t i64max(int64_t x, int64_t y) { return x > y ? x : y; }
+
+__device__ __forceinline__ bool item_less(uint64_t ak1, uint64_t ak2, uint64_t bk1, uint64_t bk2) {
+  return ak1 < bk1 || (ak1 == bk1 && ak2 < bk2);
+}
+
+// Sort keys of every (segment, line): kind 0 finite end s, 1 at -inf, 2 at +inf
+// (ties by the value at the finite end `fin`), 3 by slope a (near-parallel pass).
+__global__ void sweep_keys_kernel(const double2* __restrict__ ab, int n, const SweepEnd* __restrict__ ends,
+                                  int nseg, uint64_t* __restrict__ k1, uint64_t* __restrict__ k2,
+                                  uint32_t* __restrict__ idx) {
+  const int64_t total = (int64_t)nseg * n;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int s = (int)(g / n);
+    const int k = (int)(g - (int64_t)s * n);
+    const SweepEnd e = ends[s];
+    const double2 l = ab[k];
+    uint64_t p, q;
+    if (e.kind == 0) {
+      p = key_of(fma(l.x, e.s, -l.y));
+      q = (uint64_t)k;
+    } else if (e.kind == 3) {
+      p = key_of(l.x);
+      q = (uint64_t)k;
+    } else {
+      p = key_of(e.kind == 1 ? -l.x : l.x);
+      q = (key_of(fma(l.x, e.fin, -l.y)) & ~(uint64_t)0xFFFF) | (uint64_t)k;
+    }
+    k1[g] = p;
+    k2[g] = q;
+    idx[g] = (uint32_t)k;
+  }
+}
+
+// One CTA sorts one chunk of kChunk items of one segment in shared memory
+// (bitonic network; keys are unique, so the order is deterministic).
+__global__ void __launch_bounds__(kChunkThreads, 1) sweep_chunk_sort_kernel(
+    int n, int chunks_per_seg, uint64_t* __restrict__ k1, uint64_t* __restrict__ k2,
+    uint32_t* __restrict__ idx) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint64_t* s1 = reinterpret_cast<uint64_t*>(smem_raw);
+  uint64_t* s2 = s1 + kChunk;
+  uint32_t* si = reinterpret_cast<uint32_t*>(s2 + kChunk);
+  const int seg = blockIdx.x / chunks_per_seg;
+  const int c = blockIdx.x - seg * chunks_per_seg;
+  const int64_t base = (int64_t)seg * n + (int64_t)c * kChunk;
+  const int cnt = min(kChunk, n - c * kChunk);
+  for (int t = threadIdx.x; t < kChunk; t += kChunkThreads) {
+    if (t < cnt) {
+      s1[t] = k1[base + t];
+      s2[t] = k2[base + t];
+      si[t] = idx[base + t];
+    } else {
+      s1[t] = ~0ull;
+      s2[t] = ~0ull;
+      si[t] = 0xFFFFFFFFu;
+    }
+  }
+  __syncthreads();
+  for (int k = 2; k <= kChunk; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int t = threadIdx.x; t < kChunk / 2; t += kChunkThreads) {
+        const int lo = 2 * t - (t & (j - 1));
+        const int hi = lo + j;
+        const bool up = (lo & k) == 0;
+        const uint64_t a1 = s1[lo], a2 = s2[lo], b1 = s1[hi], b2 = s2[hi];
+        if (item_less(b1, b2, a1, a2) == up) {
+          s1[lo] = b1;
+          s2[lo] = b2;
+          s1[hi] = a1;
+          s2[hi] = a2;
+          const uint32_t x = si[lo];
+          si[lo] = si[hi];
+          si[hi] = x;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int t = threadIdx.x; t < cnt; t += kChunkThreads) {
+    k1[base + t] = s1[t];
+    k2[base + t] = s2[t];
+    idx[base + t] = si[t];
+  }
+}
+
+// One merge round: sorted runs of width w (per segment) pairwise into runs
+// of 2w; merge path per thread (kMergeItems outputs).
+__global__ void __launch_bounds__(kMergeThreads) sweep_merge_kernel(
+    int n, int64_t w, int blocks_per_seg, const uint64_t* __restrict__ x1,
+    const uint64_t* __restrict__ x2, const uint32_t* __restrict__ xi, uint64_t* __restrict__ y1,
+    uint64_t* __restrict__ y2, uint32_t* __restrict__ yi) {
+  const int seg = blockIdx.x / blocks_per_seg;
+  const int64_t d0 =
+      ((int64_t)(blockIdx.x - seg * blocks_per_seg) * kMergeThreads + threadIdx.x) * kMergeItems;
+  if (d0 >= n) return;
+  const int64_t sb = (int64_t)seg * n;
+  const int64_t pbase = (d0 / (2 * w)) * (2 * w);
+  const int64_t la = i64min(w, n - pbase);
+  const int64_t lb = i64max(0, i64min(w, n - pbase - w));
+  const int64_t a0 = sb + pbase, b0 = a0 + la;
+  const int64_t dd = d0 - pbase;
+  int64_t lo = i64max(0, dd - lb), hi = i64min(dd, la);
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    const int64_t jb = dd - mid - 1;
+    // take A[mid] before B[jb]?  (keys are unique)
+    if (item_less(x1[b0 + jb], x2[b0 + jb], x1[a0 + mid], x2[a0 + mid])) hi = mid;
+    else lo = mid + 1;
+  }
+  int64_t ia = lo, ib = dd - lo;
+  const int64_t end = i64min(d0 + kMergeItems, pbase + la + lb);
+  for (int64_t d = d0; d < end; ++d) {
+    bool takeA;
+    if (ia >= la) takeA = false;
+    else if (ib >= lb) takeA = true;
+    else takeA = !item_less(x1[b0 + ib], x2[b0 + ib], x1[a0 + ia], x2[a0 + ia]);
+    const int64_t src = takeA ? a0 + ia : b0 + ib;
+    y1[sb + d] = x1[src];
+    y2[sb + d] = x2[src];
+    yi[sb + d] = xi[src];
+    if (takeA) ++ia;
+    else ++ib;
+  }
+}
+
+// pos[run][line] = position of the line in the run's s1' order
+__global__ void sweep_pos_kernel(int n, int nruns, const uint32_t* __restrict__ idx,
+                                 int32_t* __restrict__ pos) {
+  const int64_t total = (int64_t)nruns * n;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(g / n);
+    const int p = (int)(g - (int64_t)r * n);
+    pos[(int64_t)r * n + idx[(int64_t)(2 * r + 1) * n + p]] = p;
+  }
+}
+
+// P[run][t] = s1' position of the line at s0' position t, and per 32-block minima
+__global__ void sweep_p_kernel(int n, int nruns, const uint32_t* __restrict__ idx,
+                               const int32_t* __restrict__ pos, int32_t* __restrict__ P,
+                               int32_t* __restrict__ bmin) {
+  const int nb = (n + 31) / 32;
+  const int64_t total = (int64_t)nruns * nb * 32;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(g / ((int64_t)nb * 32));
+    const int t = (int)(g - (int64_t)r * nb * 32);
+    int v = INT_MAX;
+    if (t < n) {
+      v = pos[(int64_t)r * n + idx[(int64_t)(2 * r) * n + t]];
+      P[(int64_t)r * n + t] = v;
+    }
+    int m = v;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, off));
+    if ((threadIdx.x & 31) == 0) bmin[(int64_t)r * nb + (t >> 5)] = m;
+  }
+}
+
+// suffix minima of the block minima, one CTA per run
+__global__ void __launch_bounds__(1024) sweep_suffix_kernel(int n, const int32_t* __restrict__ bmin,
+                                                            int32_t* __restrict__ suf) {
+  __shared__ int32_t part[1024];
+  const int nb = (n + 31) / 32;
+  const int r = blockIdx.x;
+  const int per = (nb + 1023) / 1024;
+  const int b0 = threadIdx.x * per;
+  const int b1 = min(nb, b0 + per);
+  const int32_t* bm = bmin + (int64_t)r * nb;
+  int32_t* sf = suf + (int64_t)r * nb;
+  int m = INT_MAX;
+  for (int b = b1 - 1; b >= b0; --b) m = min(m, bm[b]);
+  part[threadIdx.x] = m;
+  __syncthreads();
+  // inclusive suffix minimum over the thread totals (Hillis-Steele)
+  for (int off = 1; off < 1024; off <<= 1) {
+    const int v = threadIdx.x + off < 1024 ? part[threadIdx.x + off] : INT_MAX;
+    __syncthreads();
+    part[threadIdx.x] = min(part[threadIdx.x], v);
+    __syncthreads();
+  }
+  m = threadIdx.x + 1 < 1024 ? part[threadIdx.x + 1] : INT_MAX;
+  for (int b = b1 - 1; b >= b0; --b) {
+    m = min(m, bm[b]);
+    sf[b] = m;
+  }
+}
+
+// Band of slope key bk if it lies in bands [k0, k1] of the K bands, else -1.
+__device__ __forceinline__ int band_in_run(const float* __restrict__ bnd, int K, int k0, int k1,
+                                           float bk) {
+  if (k0 > 0 && !(__ldg(bnd + k0 - 1) <= bk)) return -1;
+  if (k1 < K - 1 && !(bk < __ldg(bnd + k1))) return -1;
+  int lo = k0, hi = k1;  // band = number of boundaries <= bk, in [k0, k1]
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;  // boundary mid separates bands mid and mid + 1
+    if (__ldg(bnd + mid) <= bk) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// (slot, slope position) key of a member of band `band` (lms_band.cu collect)
+__device__ __forceinline__ uint32_t member_key(const float* __restrict__ bnd, int K, int band,
+                                               float bk, int sb) {
+  uint32_t t = 0;
+  if (band > 0 && band < K - 1) {
+    const float lo = __ldg(bnd + band - 1), w = __ldg(bnd + band) - lo;
+    const float f = w > 0.f ? (bk - lo) / w * (float)(1 << kSlopeBits) : 0.f;
+    t = (uint32_t)fminf(fmaxf(f, 0.f), (float)((1 << kSlopeBits) - 1));
+  }
+  return ((uint32_t)max(sb, 0) << kSlopeBits) | t;
+}
+
+// Classify enumerated pair (k, l) and decide whether run (k0, k1) emits it
+// (k0 < 0: the near-parallel pass, which owns every admitted band).
+__device__ __forceinline__ bool sweep_take(const BandFit& bf, const SweepArgs& sa, int k0, int k1,
+                                           bool parallel_pass, int k, int l, uint32_t* key,
+                                           uint32_t* val) {
+  const int i = min(k, l), j = max(k, l);
+  if (i == j) return false;
+  const int64_t r = row_offset(bf.n, i) + (j - i - 1);
+  if (r < bf.R0 || r >= bf.R0 + bf.span) return false;
+  const double2 li = bf.ab[i], lj = bf.ab[j];
+  const double da = fabs(__dsub_rn(li.x, lj.x));
+  if (!parallel_pass && da <= sa.tau) return false;  // the near-parallel pass owns it
+  double u = 0.0;
+  const int cls = classify(bf, li.x, li.y, lj.x, lj.y, &u);
+  *val = ((uint32_t)i << 16) | (uint32_t)j;
+  if (cls == 1) {
+    const float bk = band_key(u);
+    const int band = parallel_pass ? band_of(sa.bounds, sa.K - 1, bk)
+                                   : band_in_run(sa.bounds, sa.K, k0, k1, bk);
+    if (band < 0) return false;
+    const int sb = __ldg(sa.slot + band);
+    if (sb < 0) return false;
+    *key = member_key(sa.bounds, sa.K, band, bk, sb);
+    return true;
+  }
+  if (cls == 2) {
+    const bool own = parallel_pass || (u < 0.0 ? k0 == 0 : k1 == sa.K - 1);
+    if (!own) return false;
+    *key = (uint32_t)__ldg(sa.slot + sa.K) << kSlopeBits;
+    return true;
+  }
+  return false;
+}
+
+__global__ void __launch_bounds__(kEnumThreads) sweep_enum_kernel(BandFit bf, SweepArgs sa) {
+  __shared__ uint32_t queue[kEnumWarps][kEnumQueue];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  uint32_t* q = queue[wib];
+  int qn = 0;
+  const int n = (int)bf.n;
+  const int nb = (n + 31) / 32;
+  const int64_t nitems = (int64_t)sa.nruns * n;
+  const int64_t gw0 = (int64_t)blockIdx.x * kEnumWarps + wib;
+  const int64_t nw = (int64_t)gridDim.x * kEnumWarps;
+  int cur_run = -1, k0 = 0, k1 = 0;
+
+  auto drain = [&](int cnt) {
+    uint32_t key = 0, val = 0;
+    bool take = false;
+    if (lane < cnt) {
+      const uint32_t e = q[lane];
+      take = sweep_take(bf, sa, k0, k1, false, (int)(e >> 16), (int)(e & 0xFFFF), &key, &val);
+    }
+    const unsigned mask = __ballot_sync(0xffffffffu, take);
+    if (mask) {
+      const int leader = __ffs(mask) - 1;
+      unsigned long long b0 = 0;
+      if (lane == leader) b0 = atomicAdd(sa.count, (unsigned long long)__popc(mask));
+      b0 = __shfl_sync(0xffffffffu, b0, leader);
+      if (take) {
+        const unsigned long long pos = b0 + __popc(mask & ((1u << lane) - 1u));
+        if ((int64_t)pos < sa.cap) {
+          sa.out_keys[pos] = key;
+          sa.out_vals[pos] = val;
+        }
+      }
+    }
+  };
+  auto flush = [&]() {
+    __syncwarp();
+    while (qn >= 32) {
+      drain(32);
+      __syncwarp();
+      if (lane < qn - 32) q[lane] = q[32 + lane];
+      __syncwarp();
+      qn -= 32;
+    }
+  };
+
+  // items ordered run-major: a warp's consecutive items share the run
+  for (int64_t it = gw0; it < nitems; it += nw) {
+    const int r = (int)(it / n);
+    const int t = (int)(it - (int64_t)r * n);
+    if (r != cur_run) {
+      if (qn > 0) {  // the queue holds pairs of the previous run
+        __syncwarp();
+        drain(qn);
+        qn = 0;
+        __syncwarp();
+      }
+      cur_run = r;
+      k0 = sa.run_k0[r];
+      k1 = sa.run_k1[r];
+    }
+    const int32_t* P = sa.P + (int64_t)r * n;
+    const int32_t* bm = sa.bmin + (int64_t)r * nb;
+    const int32_t* sf = sa.suf + (int64_t)r * nb;
+    const uint32_t* line0 = sa.idx + (int64_t)(2 * r) * n;
+    const int p = P[t];
+    const uint32_t me = line0[t] << 16;
+    int b = (t + 1) >> 5;
+    while (b < nb && sf[b] < p) {
+      const int bb = b + lane;
+      const bool hit = bb < nb && bm[bb] < p;
+      unsigned hits = __ballot_sync(0xffffffffu, hit);
+      while (hits) {
+        const int h = __ffs(hits) - 1;
+        hits &= hits - 1;
+        const int tp = ((b + h) << 5) + lane;
+        const bool c = tp > t && tp < n && P[tp] < p;
+        const unsigned m = __ballot_sync(0xffffffffu, c);
+        if (c) q[qn + __popc(m & ((1u << lane) - 1u))] = me | line0[tp];
+        qn += __popc(m);
+        if (qn >= 32) flush();
+      }
+      b += 32;
+    }
+  }
+  __syncwarp();
+  if (qn > 0) drain(qn);
+}
+
+// Nearly parallel pairs (0 < |a_i - a_j| <= tau): lines sorted by a, each
+// against the following lines with a larger slope within tau.
+__global__ void sweep_parallel_kernel(BandFit bf, SweepArgs sa) {
+  const int n = (int)bf.n;
+  const uint64_t* ka = sa.k1a;
+  const uint32_t* ia = sa.idxa;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    const int k = (int)ia[t];
+    const double ak = bf.ab[k].x;
+    // first position with a strictly larger slope
+    int lo = t + 1, hi = n;
+    const uint64_t kk = ka[t];
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (ka[mid] <= kk) lo = mid + 1;
+      else hi = mid;
+    }
+    for (int tp = lo; tp < n; ++tp) {
+      const int l = (int)ia[tp];
+      if (__dsub_rn(bf.ab[l].x, ak) > sa.tau) break;
+      uint32_t key, val;
+      if (sweep_take(bf, sa, -1, -1, true, k, l, &key, &val)) {
+        const unsigned long long pos = atomicAdd(sa.count, 1ull);
+        if ((int64_t)pos < sa.cap) {
+          sa.out_keys[pos] = key;
+          sa.out_vals[pos] = val;
+        }
+      }
+    }
+  }
+}
+
+}  // namespace
+
+size_t sweep_chunk_smem() { return (size_t)kChunk * (2 * sizeof(uint64_t) + sizeof(uint32_t)); }
+
+int launch_sweep_sort(const double2* ab, int n, const SweepEnd* ends, int nseg, SweepSort& ss,
+                      int sms, cudaStream_t st) {
+  if (n <= 0 || nseg <= 0) return 0;
+  sweep_keys_kernel<<<sms * 4, 256, 0, st>>>(ab, n, ends, nseg, ss.k1[0], ss.k2[0], ss.idx[0]);
+  static DeviceOnce done;
+  set_max_smem(sweep_chunk_sort_kernel, sweep_chunk_smem(), done);
+  const int cps = (n + kChunk - 1) / kChunk;
+  sweep_chunk_sort_kernel<<<nseg * cps, kChunkThreads, sweep_chunk_smem(), st>>>(
+      n, cps, ss.k1[0], ss.k2[0], ss.idx[0]);
+  int cur = 0;
+  const int bps = (n + kMergeThreads * kMergeItems - 1) / (kMergeThreads * kMergeItems);
+  for (int64_t w = kChunk; w < n; w *= 2) {
+    sweep_merge_kernel<<<nseg * bps, kMergeThreads, 0, st>>>(n, w, bps, ss.k1[cur], ss.k2[cur],
+                                                              ss.idx[cur], ss.k1[cur ^ 1],
+                                                              ss.k2[cur ^ 1], ss.idx[cur ^ 1]);
+    cur ^= 1;
+  }
+  ss.cur = cur;
+  return 2 + (cur != 0 ? 1 : 0);
+}
+
+void launch_sweep_prepare(int n, int nruns, const SweepSort& ss, int32_t* pos, int32_t* P,
+                          int32_t* bmin, int32_t* suf, int sms, cudaStream_t st) {
+  if (nruns <= 0) return;
+  sweep_pos_kernel<<<sms * 4, 256, 0, st>>>(n, nruns, ss.idx[ss.cur], pos);
+  sweep_p_kernel<<<sms * 4, 256, 0, st>>>(n, nruns, ss.idx[ss.cur], pos, P, bmin);
+  sweep_suffix_kernel<<<nruns, 1024, 0, st>>>(n, bmin, suf);
+}
+
+void launch_sweep_emit(const BandFit& bf, const SweepArgs& sa, int sms, cudaStream_t st) {
+  cudaMemsetAsync(sa.count, 0, sizeof(unsigned long long), st);
+  if (sa.nruns > 0) sweep_enum_kernel<<<sms * 8, kEnumThreads, 0, st>>>(bf, sa);
+  if (sa.tau > 0.0 && sa.k1a)
+    sweep_parallel_kernel<<<(int)((bf.n + 255) / 256), 256, 0, st>>>(bf, sa);
+}
+
+}  // namespace lmsb
