@@ -225,6 +225,7 @@ struct SweepArgs {
   uint32_t* out_vals;
   int64_t cap;
   unsigned long long* count;
+  int smem_tables;        // (launcher) boundaries and slots staged in shared memory
 };
 size_t sweep_chunk_smem();
 // sort nseg segments of the n lines by their end keys; returns launches

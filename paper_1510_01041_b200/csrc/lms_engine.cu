@@ -99,6 +99,9 @@ int64_t band_size(int64_t knob, int64_t n) {
 
 // Most slope runs of the sweep collect (two sorts of the n lines each).
 constexpr int kSweepMaxRuns = 16;
+// Auto mode: sweep collect from this many lines (measured: n = 8,000 pre-test
+// 0.11 ms vs sweep 0.21 ms; n = 16,384 0.36 vs 0.31; n = 65,536 5.4 vs 1.6).
+constexpr int64_t kSweepMinN = 12288;
 
 // Large-n band size (vertices per band = mult * n): fewer, wider bands pay
 // once n > ~36 k (config 3, n = 65,536: 8 -> 18.6 ms, 16 -> 17.9, 32 ->
@@ -268,7 +271,10 @@ struct lms_ctx {
   // slower on config 2 (sub-bands are wider than slope-sorted chunks), kept
   // for A/B runs
   int band_direct = 0;
-  int band_sweep = 1;  // LMSB_SWEEP: output-sensitive collect (lms_sweep.cu); 0 = pre-test pass
+  // LMSB_SWEEP: output-sensitive collect (lms_sweep.cu): 0 never (the
+  // pre-test pass over every vertex), 1 always, 2 auto (n >= kSweepMinN, where
+  // its fixed sort cost is below the pre-test pass's O(n^2))
+  int band_sweep = 2;
   DevBuf<uint64_t> sw_k1, sw_k2;
   DevBuf<uint32_t> sw_idx;
   DevBuf<int32_t> sw_pos, sw_P, sw_bmin, sw_suf, sw_rk;
@@ -308,7 +314,7 @@ int ctx_init(lms_ctx* c, int device) {
   if (bv && atoll(bv) >= 256) c->band_vertices = atoll(bv);
   const char* bd = getenv("LMSB_BAND_DIRECT");
   c->band_direct = (bd && std::strcmp(bd, "1") == 0) ? 1 : 0;
-  if (const char* sw = getenv("LMSB_SWEEP")) c->band_sweep = atoi(sw) != 0;
+  if (const char* sw = getenv("LMSB_SWEEP")) c->band_sweep = std::max(0, std::min(2, atoi(sw)));
   const char* bmul = getenv("LMSB_BIG_MULT");
   if (bmul && atoll(bmul) >= 1) c->big_mult = atoll(bmul);
   if (const char* bs = getenv("LMSB_BIG_SLICE"); bs && atoll(bs) >= 1) c->big_slice = atoll(bs);
@@ -1311,7 +1317,8 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   // inversions between the lines' orders at its ends (lms_sweep.cu).  Needs
   // every inner boundary inside the fp32-key range, so that vertices beyond
   // it (class 2) can only lie in the two outer bands.
-  bool sweep = c->band_sweep && !rr.empty() && h.n >= 3 && h.n <= lmsb::kBandMaxBigN;
+  bool sweep = (c->band_sweep == 1 || (c->band_sweep == 2 && h.n >= kSweepMinN)) && !rr.empty() &&
+               h.n >= 3 && h.n <= lmsb::kBandMaxBigN;
   for (int k = 0; sweep && k < K - 1; ++k)
     sweep = std::isfinite(hbnd[k]) && std::fabs((double)hbnd[k]) * bf.amax < 1e29;
   lmsb::SweepArgs sa{};

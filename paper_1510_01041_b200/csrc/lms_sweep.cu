@@ -56,6 +56,9 @@ constexpr int kMergeThreads = 256;
 constexpr int kEnumThreads = 256;
 constexpr int kEnumWarps = kEnumThreads / 32;
 constexpr int kEnumQueue = 64;
+constexpr int kOutBuf = 128;
+constexpr int kOutFlush = kOutBuf - 32;
+constexpr int kHitBatch = 4;
 
 __device__ __forceinline__ int64_t i64min(int64_t x, int64_t y) { return x < y ? x : y; }
 __device__ __forceinline__ int64_t i64max(int64_t x, int64_t y) { return x > y ? x : y; }
@@ -249,25 +252,23 @@ __global__ void __launch_bounds__(1024) sweep_suffix_kernel(int n, const int32_t
 }
 
 // Band of slope key bk if it lies in bands [k0, k1] of the K bands, else -1.
-__device__ __forceinline__ int band_in_run(const float* __restrict__ bnd, int K, int k0, int k1,
-                                           float bk) {
-  if (k0 > 0 && !(__ldg(bnd + k0 - 1) <= bk)) return -1;
-  if (k1 < K - 1 && !(bk < __ldg(bnd + k1))) return -1;
+__device__ __forceinline__ int band_in_run(const float* bnd, int K, int k0, int k1, float bk) {
+  if (k0 > 0 && !(bnd[k0 - 1] <= bk)) return -1;
+  if (k1 < K - 1 && !(bk < bnd[k1])) return -1;
   int lo = k0, hi = k1;  // band = number of boundaries <= bk, in [k0, k1]
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;  // boundary mid separates bands mid and mid + 1
-    if (__ldg(bnd + mid) <= bk) lo = mid + 1;
+    if (bnd[mid] <= bk) lo = mid + 1;
     else hi = mid;
   }
   return lo;
 }
 
 // (slot, slope position) key of a member of band `band` (lms_band.cu collect)
-__device__ __forceinline__ uint32_t member_key(const float* __restrict__ bnd, int K, int band,
-                                               float bk, int sb) {
+__device__ __forceinline__ uint32_t member_key(const float* bnd, int K, int band, float bk, int sb) {
   uint32_t t = 0;
   if (band > 0 && band < K - 1) {
-    const float lo = __ldg(bnd + band - 1), w = __ldg(bnd + band) - lo;
+    const float lo = bnd[band - 1], w = bnd[band] - lo;
     const float f = w > 0.f ? (bk - lo) / w * (float)(1 << kSlopeBits) : 0.f;
     t = (uint32_t)fminf(fmaxf(f, 0.f), (float)((1 << kSlopeBits) - 1));
   }
@@ -276,9 +277,9 @@ __device__ __forceinline__ uint32_t member_key(const float* __restrict__ bnd, in
 
 // Classify enumerated pair (k, l) and decide whether run (k0, k1) emits it
 // (k0 < 0: the near-parallel pass, which owns every admitted band).
-__device__ __forceinline__ bool sweep_take(const BandFit& bf, const SweepArgs& sa, int k0, int k1,
-                                           bool parallel_pass, int k, int l, uint32_t* key,
-                                           uint32_t* val) {
+__device__ __forceinline__ bool sweep_take(const BandFit& bf, const SweepArgs& sa, const float* bnd,
+                                           const int16_t* slot, int k0, int k1, bool parallel_pass,
+                                           int k, int l, uint32_t* key, uint32_t* val) {
   const int i = min(k, l), j = max(k, l);
   if (i == j) return false;
   const int64_t r = row_offset(bf.n, i) + (j - i - 1);
@@ -291,29 +292,47 @@ __device__ __forceinline__ bool sweep_take(const BandFit& bf, const SweepArgs& s
   *val = ((uint32_t)i << 16) | (uint32_t)j;
   if (cls == 1) {
     const float bk = band_key(u);
-    const int band = parallel_pass ? band_of(sa.bounds, sa.K - 1, bk)
-                                   : band_in_run(sa.bounds, sa.K, k0, k1, bk);
+    const int band = parallel_pass ? band_of(bnd, sa.K - 1, bk) : band_in_run(bnd, sa.K, k0, k1, bk);
     if (band < 0) return false;
-    const int sb = __ldg(sa.slot + band);
+    const int sb = slot[band];
     if (sb < 0) return false;
-    *key = member_key(sa.bounds, sa.K, band, bk, sb);
+    *key = member_key(bnd, sa.K, band, bk, sb);
     return true;
   }
   if (cls == 2) {
     const bool own = parallel_pass || (u < 0.0 ? k0 == 0 : k1 == sa.K - 1);
     if (!own) return false;
-    *key = (uint32_t)__ldg(sa.slot + sa.K) << kSlopeBits;
+    *key = (uint32_t)slot[sa.K] << kSlopeBits;
     return true;
   }
   return false;
 }
 
-__global__ void __launch_bounds__(kEnumThreads) sweep_enum_kernel(BandFit bf, SweepArgs sa) {
+__global__ void __launch_bounds__(kEnumThreads, 4) sweep_enum_kernel(BandFit bf, SweepArgs sa) {
   __shared__ uint32_t queue[kEnumWarps][kEnumQueue];
+  __shared__ uint32_t okey[kEnumWarps][kOutBuf];
+  __shared__ uint32_t oval[kEnumWarps][kOutBuf];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   uint32_t* q = queue[wib];
-  int qn = 0;
+  uint32_t* ok = okey[wib];
+  uint32_t* ov = oval[wib];
+  int qn = 0, on = 0;
+  // band boundaries and grouping slots in shared memory when they fit
+  extern __shared__ __align__(16) unsigned char sw_dyn[];
+  const float* bnd = sa.bounds;
+  const int16_t* slot = sa.slot;
+  if (sa.smem_tables) {
+    float* sb = reinterpret_cast<float*>(sw_dyn);
+    int16_t* ss = reinterpret_cast<int16_t*>(sb + sa.K);
+    for (int e = threadIdx.x; e <= sa.K; e += blockDim.x) {
+      if (e < sa.K - 1) sb[e] = sa.bounds[e];
+      ss[e] = sa.slot[e];
+    }
+    __syncthreads();
+    bnd = sb;
+    slot = ss;
+  }
   const int n = (int)bf.n;
   const int nb = (n + 31) / 32;
   const int64_t nitems = (int64_t)sa.nruns * n;
@@ -321,27 +340,39 @@ __global__ void __launch_bounds__(kEnumThreads) sweep_enum_kernel(BandFit bf, Sw
   const int64_t nw = (int64_t)gridDim.x * kEnumWarps;
   int cur_run = -1, k0 = 0, k1 = 0;
 
+  // members are buffered per warp and appended with one atomic per ~kOutFlush
+  auto flush_out = [&]() {
+    if (on == 0) return;
+    unsigned long long b0 = 0;
+    if (lane == 0) b0 = atomicAdd(sa.count, (unsigned long long)on);
+    b0 = __shfl_sync(0xffffffffu, b0, 0);
+    for (int e = lane; e < on; e += 32) {
+      const unsigned long long pos = b0 + e;
+      if ((int64_t)pos < sa.cap) {
+        sa.out_keys[pos] = ok[e];
+        sa.out_vals[pos] = ov[e];
+      }
+    }
+    __syncwarp();
+    on = 0;
+  };
   auto drain = [&](int cnt) {
     uint32_t key = 0, val = 0;
     bool take = false;
     if (lane < cnt) {
       const uint32_t e = q[lane];
-      take = sweep_take(bf, sa, k0, k1, false, (int)(e >> 16), (int)(e & 0xFFFF), &key, &val);
+      take = sweep_take(bf, sa, bnd, slot, k0, k1, false, (int)(e >> 16), (int)(e & 0xFFFF), &key,
+                        &val);
     }
     const unsigned mask = __ballot_sync(0xffffffffu, take);
-    if (mask) {
-      const int leader = __ffs(mask) - 1;
-      unsigned long long b0 = 0;
-      if (lane == leader) b0 = atomicAdd(sa.count, (unsigned long long)__popc(mask));
-      b0 = __shfl_sync(0xffffffffu, b0, leader);
-      if (take) {
-        const unsigned long long pos = b0 + __popc(mask & ((1u << lane) - 1u));
-        if ((int64_t)pos < sa.cap) {
-          sa.out_keys[pos] = key;
-          sa.out_vals[pos] = val;
-        }
-      }
+    if (take) {
+      const int at = on + __popc(mask & ((1u << lane) - 1u));
+      ok[at] = key;
+      ov[at] = val;
     }
+    on += __popc(mask);
+    __syncwarp();
+    if (on >= kOutFlush) flush_out();
   };
   auto flush = [&]() {
     __syncwarp();
@@ -381,20 +412,38 @@ __global__ void __launch_bounds__(kEnumThreads) sweep_enum_kernel(BandFit bf, Sw
       const bool hit = bb < nb && bm[bb] < p;
       unsigned hits = __ballot_sync(0xffffffffu, hit);
       while (hits) {
-        const int h = __ffs(hits) - 1;
-        hits &= hits - 1;
-        const int tp = ((b + h) << 5) + lane;
-        const bool c = tp > t && tp < n && P[tp] < p;
-        const unsigned m = __ballot_sync(0xffffffffu, c);
-        if (c) q[qn + __popc(m & ((1u << lane) - 1u))] = me | line0[tp];
-        qn += __popc(m);
-        if (qn >= 32) flush();
+        // up to kHitBatch hit blocks at a time: all their loads in flight at once
+        int tp[kHitBatch];
+        int32_t pv[kHitBatch];
+        uint32_t lv[kHitBatch];
+#pragma unroll
+        for (int e = 0; e < kHitBatch; ++e) {
+          tp[e] = -1;
+          if (hits) {
+            const int h = __ffs(hits) - 1;
+            hits &= hits - 1;
+            tp[e] = ((b + h) << 5) + lane;
+          }
+          const int tq = min(max(tp[e], 0), n - 1);
+          pv[e] = P[tq];
+          lv[e] = line0[tq];
+        }
+#pragma unroll
+        for (int e = 0; e < kHitBatch; ++e) {
+          if (tp[e] < 0 && e > 0) break;  // (warp-uniform: the same hits on every lane)
+          const bool c = tp[e] > t && tp[e] < n && pv[e] < p;
+          const unsigned m = __ballot_sync(0xffffffffu, c);
+          if (c) q[qn + __popc(m & ((1u << lane) - 1u))] = me | lv[e];
+          qn += __popc(m);
+          if (qn >= 32) flush();
+        }
       }
       b += 32;
     }
   }
   __syncwarp();
   if (qn > 0) drain(qn);
+  flush_out();
 }
 
 // Nearly parallel pairs (0 < |a_i - a_j| <= tau): lines sorted by a, each
@@ -418,7 +467,7 @@ __global__ void sweep_parallel_kernel(BandFit bf, SweepArgs sa) {
       const int l = (int)ia[tp];
       if (__dsub_rn(bf.ab[l].x, ak) > sa.tau) break;
       uint32_t key, val;
-      if (sweep_take(bf, sa, -1, -1, true, k, l, &key, &val)) {
+      if (sweep_take(bf, sa, sa.bounds, sa.slot, -1, -1, true, k, l, &key, &val)) {
         const unsigned long long pos = atomicAdd(sa.count, 1ull);
         if ((int64_t)pos < sa.cap) {
           sa.out_keys[pos] = key;
@@ -464,7 +513,12 @@ void launch_sweep_prepare(int n, int nruns, const SweepSort& ss, int32_t* pos, i
 
 void launch_sweep_emit(const BandFit& bf, const SweepArgs& sa, int sms, cudaStream_t st) {
   cudaMemsetAsync(sa.count, 0, sizeof(unsigned long long), st);
-  if (sa.nruns > 0) sweep_enum_kernel<<<sms * 8, kEnumThreads, 0, st>>>(bf, sa);
+  if (sa.nruns > 0) {
+    const size_t tab = (size_t)sa.K * sizeof(float) + (size_t)(sa.K + 1) * sizeof(int16_t) + 16;
+    SweepArgs a2 = sa;
+    a2.smem_tables = tab <= 24 * 1024;
+    sweep_enum_kernel<<<sms * 8, kEnumThreads, a2.smem_tables ? tab : 0, st>>>(bf, a2);
+  }
   if (sa.tau > 0.0 && sa.k1a)
     sweep_parallel_kernel<<<(int)((bf.n + 255) / 256), 256, 0, st>>>(bf, sa);
 }

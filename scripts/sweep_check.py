@@ -12,7 +12,7 @@ from paper_1510_01041_b200 import _native, workloads  # noqa: E402
 
 
 def ctx_with(sweep):
-    os.environ["LMSB_SWEEP"] = str(sweep)
+    os.environ["LMSB_SWEEP"] = str(sweep)  # 0 never, 1 always
     c = _native.Context(0)
     os.environ.pop("LMSB_SWEEP", None)
     return c
