@@ -136,3 +136,49 @@ def test_config5_staged_transfers_integrity():
     for q in range(len(peaks)):
         seg = ids64[off64[q]:off64[q + 1]]
         assert np.all(np.diff(seg) > 0) and np.all(flat[seg] >= 128)
+
+
+def _config5_golden():
+    import gzip
+    import json
+    import os
+
+    path = os.path.join(os.path.dirname(__file__), "golden", "config5_golden.json.gz")
+    with gzip.open(path, "rt") as fh:
+        return json.load(fh)
+
+
+def test_config5_full_size_matches_reference_golden():
+    """BASELINE config 5 at full size: the 4096^2 image of 64 gen_synthetic lines
+    + 30 % salt (workloads.config5_image, the reference's own generator
+    recipe), detect_lines(..., "lms", 64) with support caps 256 and 512
+    against the reference's own run (tests/golden/make_golden_config5.py):
+    accumulator, peaks, every LineDetection field, and each peak's full
+    support (length and sha256 of its (x, y) pairs in order)."""
+    import hashlib
+
+    doc = _config5_golden()
+    img = workloads.config5_image(0)
+    assert hashlib.sha256(img.tobytes()).hexdigest() == doc["image_sha256"]
+    p = lms.HoughParams.for_image(4096, 4096, 20.0, 20.0)
+    assert [p.delta_rho.hex(), p.delta_theta.hex(), p.rho_max.hex()] == doc["params"]
+    c, s = p.vote_trig()
+    bins, npts = _native.hough_vote_image(img, 128, c, s, p.rho_max, p.delta_rho, p.n_rho)
+    assert npts == doc["lit"]
+    want = np.zeros_like(bins)
+    for r, t, v in doc["bins"]:
+        want[r, t] = v
+    assert np.array_equal(bins, want)
+    peaks = lms.find_peaks(lms.HoughAccumulator(bins=bins, params=p), 64, 2)
+    assert [[k.rho_bin, k.theta_bin, k.votes, k.rho.hex(), k.theta.hex()] for k in peaks] == doc["peaks"]
+    for cap in (256, 512):
+        dets = lms.detect_lines(img, p, "lms", 64, support_cap=cap)
+        gold = doc["detect"][str(cap)]
+        assert len(dets) == len(gold)
+        for d, g in zip(dets, gold):
+            assert (d.rho, d.theta, d.slope, d.intercept, d.lms_value) == \
+                tuple(f(g[k]) for k in ("rho", "theta", "slope", "intercept", "lms_value")), cap
+            assert d.axis_swapped == g["axis_swapped"] and d.method == g["method"]
+            assert len(d.support) == g["support_len"]
+            xy = np.array([(q.x, q.y) for q in d.support], dtype=np.int32)
+            assert hashlib.sha256(xy.tobytes()).hexdigest() == g["support_sha256"]

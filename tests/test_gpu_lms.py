@@ -541,6 +541,78 @@ def test_config2_full_fit_matches_unpruned_materialized_flow():
     assert full == band
 
 
+def test_config3_full_fit_matches_unpruned_materialized_flow():
+    """BASELINE config 3 at full size (n = 65,536): the pruned large-n band
+    search returns exactly the record of the unpruned K1/K2 flow over all
+    2,147,450,880 vertices (the reference's arithmetic on every vertex, no
+    filter; minutes on one B200)."""
+    n = 65536
+    pts = workloads.contaminated_line_points(n, 0)
+    q = n // 2 + 1
+    total = n * (n - 1) // 2
+    ctx = _native.Context()
+    ctx.upload(pts[:, 0].copy(), pts[:, 1].copy())
+    band = record_from_native(ctx.solve(q, 0, total))
+    assert ctx.stats()["bands"] > 0
+    full = record_from_native(ctx.solve_materialized(q, 0, total))
+    assert full == band
+
+
+def _ctx_env(**env):
+    import os
+
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update({k: str(v) for k, v in env.items()})
+    try:
+        return _native.Context()
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+@pytest.mark.parametrize("case", ["config2", "grid", "outliers", "dupx", "near_parallel", "shards"])
+def test_sweep_collect_matches_pretest_collect(case):
+    """The output-sensitive sweep collect (lms_sweep.cu) hands the filter the
+    same member set as the pre-test pass over every vertex: identical
+    records and collected counts, on inputs with duplicate x, integer grids,
+    1e6 outliers, nearly parallel lines, and per-shard rank ranges."""
+    rng = np.random.default_rng(7)
+    if case == "config2":
+        pts = workloads.contaminated_line_points(16384, 0)
+    elif case == "grid":
+        pts = rng.integers(0, 300, (5000, 2)).astype(float)
+    elif case == "outliers":
+        pts = workloads.contaminated_line_points(4000, 2)
+        pts[:200, 1] += 1e6
+    elif case == "dupx":
+        x = rng.uniform(0, 1, 4096)
+        x[::7] = x[0]
+        pts = np.column_stack([x, 3 * x + rng.normal(0, 0.01, 4096)])
+    elif case == "near_parallel":
+        x = 1.0 + np.arange(3000) * 1e-12
+        pts = np.column_stack([x, rng.normal(0, 1, 3000)])
+    else:
+        pts = workloads.contaminated_line_points(6000, 4)
+    n = len(pts)
+    q = n // 2 + 1
+    total = n * (n - 1) // 2
+    ranges = [(0, total)] if case != "shards" else [(0, total // 3), (total // 3, total - 5), (total - 5, total)]
+    c0, c1 = _ctx_env(LMSB_SWEEP=0, LMSB_BAND=2), _ctx_env(LMSB_SWEEP=1, LMSB_BAND=2)
+    for c in (c0, c1):
+        c.upload(pts[:, 0].copy(), pts[:, 1].copy())
+    for r0, r1 in ranges:
+        a = record_from_native(c0.solve(q, r0, r1))
+        sa = c0.stats()
+        b = record_from_native(c1.solve(q, r0, r1))
+        sb = c1.stats()
+        assert a == b, (case, r0, r1)
+        if sa["bands"] > 0 and sb["sweep_runs"] > 0:
+            assert sa["filtered_vertices"] == sb["filtered_vertices"], (case, r0, r1)
+
+
 @pytest.mark.parametrize("scale", [(1e-8, 1e8), (1e12, 1.0), (1.0, 1e-12), (3e5, 3e5)])
 def test_band_and_filter_paths_vs_unpruned_at_extreme_scales(scale):
     """The fp32 pre-tests of both pruned searches carry magnitude-scaled
@@ -557,7 +629,8 @@ def test_band_and_filter_paths_vs_unpruned_at_extreme_scales(scale):
     ref = _native.Context()
     ref.upload(x, y)
     want = record_from_native(ref.solve_materialized(q, 0, total))
-    for env in ({"LMSB_BAND": "2"}, {"LMSB_BAND": "0"}):
+    for env in ({"LMSB_BAND": "2", "LMSB_SWEEP": "0"}, {"LMSB_BAND": "2", "LMSB_SWEEP": "1"},
+                {"LMSB_BAND": "0"}):
         ctx = _ctx_with(env)
         ctx.upload(x, y)
         got = record_from_native(ctx.solve(q, 0, total))
