@@ -251,6 +251,42 @@ int lms_probe_fp64_rate(int device, double* dfma_per_second);
  * roofline denominator of the default FP32/FP16 count filter. */
 int lms_probe_fp32_rate(int device, double* fma_lanes_per_second);
 
+/* ---- multi-GPU exact LMS: the vertex space of one fit
+ * shared over several GPUs, one NCCL collective exchange of 56-byte records
+ * before the search (the best seed) and one after it (the results).
+ *
+ * Sharded band search with band ownership: every shard bounds and seeds its
+ * own interleaved slice of the slope bands, the seed records are
+ * all-gathered, and each shard searches the vertices of its own bands that
+ * the best seed cannot dismiss; the lexicographic (height, i, j) minimum of
+ * the shards' records is the one-GPU record (backend.py:182-187).  Fits too
+ * small for the band stage split the pair ranks into contiguous partitions
+ * instead (BatchPlan.partitions, backend.py:84-92). */
+
+/* In one process: shard r runs on devices[r] (one host thread per shard).
+ * Distinct devices exchange through NCCL (ncclCommInitAll, ncclAllGather on
+ * device buffers); shards sharing a device exchange through host memory.
+ * Replaces ParallelBackend.minimum_bracelet's thread fan-out and merge
+ * (backend.py:264-289). */
+int lms_min_bracelet_multi(const double* a, const double* b, int64_t n, int64_t q,
+                           int32_t nshards, const int32_t* devices, lms_candidate* out);
+/* 1 when libnccl.so.2 could be loaded (its version in *version), else 0. */
+int lms_nccl_available(int* version);
+/* One process per GPU (torchrun): rank 0 makes the 128-byte NCCL unique id,
+ * the caller broadcasts it, every rank binds a communicator to its context,
+ * then lms_ctx_solve_distributed runs plan -> all-gather of seed records ->
+ * own-band search -> all-gather of records -> minimum, same record on
+ * every rank. */
+int lms_nccl_unique_id(uint8_t* id);
+int lms_ctx_comm_init(lms_ctx* c, int32_t nranks, int32_t rank, const uint8_t* id);
+int lms_ctx_solve_distributed(lms_ctx* c, int64_t q, lms_candidate* out);
+/* The own-band search of one shard after lms_ctx_shard_plan(c, q, nshards,
+ * shard, ...) on the same context, with the best seed over all shards
+ * (seed may be NULL).  Not banded (the plan reported no bands): the shard's
+ * pair-rank partition. */
+int lms_ctx_shard_search_owned(lms_ctx* c, int64_t q, int32_t nshards, int32_t shard,
+                               const lms_candidate* seed, lms_candidate* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -17,7 +17,7 @@ CSRC = os.path.join(PKG_DIR, "csrc")
 LIB_DIR = os.path.join(PKG_DIR, "_lib")
 LIB_PATH = os.path.join(LIB_DIR, "liblmsb200.so")
 
-SOURCES = ["lms_engine.cu", "lms_band.cu", "lms_sweep.cu", "lms_band_small.cu", "lms_exact.cu", "lms_filter32m.cu", "lms_order.cu", "lms_plan.cu",
+SOURCES = ["lms_engine.cu", "lms_band.cu", "lms_sweep.cu", "lms_nccl.cu", "lms_band_small.cu", "lms_exact.cu", "lms_filter32m.cu", "lms_order.cu", "lms_plan.cu",
            "lms_hough.cu", "lms_primal.cu", "lms_probe.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -53,7 +53,7 @@ def build(verbose: bool = False, extra: list[str] | None = None, out: str | None
         tmp = out + ".tmp"
         # --no-undefined: a symbol missing from the objects fails the link here
         # instead of the load on the GPU box
-        subprocess.run([nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-cudart", "static", "-lgomp",
+        subprocess.run([nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-cudart", "static", "-lgomp", "-ldl",
                         "-Xlinker", "--no-undefined"], check=True)
         os.replace(tmp, out)
     finally:

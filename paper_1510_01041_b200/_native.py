@@ -185,6 +185,15 @@ SIGNATURES = {
     "lms_ctx_event_elapsed_ms": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                                 ctypes.POINTER(ctypes.c_float)]),
     "lms_ctx_synchronize": (ctypes.c_int, [ctypes.c_void_p]),
+    "lms_min_bracelet_multi": (ctypes.c_int, [_D, _D, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32,
+                                              ctypes.POINTER(ctypes.c_int32), _C]),
+    "lms_nccl_available": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int)]),
+    "lms_nccl_unique_id": (ctypes.c_int, [ctypes.POINTER(ctypes.c_uint8)]),
+    "lms_ctx_comm_init": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32,
+                                         ctypes.POINTER(ctypes.c_uint8)]),
+    "lms_ctx_solve_distributed": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, _C]),
+    "lms_ctx_shard_search_owned": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
+                                                  ctypes.c_int32, _C, _C]),
     "lms_probe_fp64_rate": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_double)]),
     "lms_probe_fp32_rate": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_double)]),
 }
@@ -259,6 +268,33 @@ def min_bracelet(a, b, q: int, rank_begin: int, rank_end: int, device: int = 0) 
     check(lib.lms_min_bracelet_f64(_dp(a), _dp(b), a.size, int(q), int(rank_begin), int(rank_end),
                                    int(device), ctypes.byref(out)))
     return out
+
+
+def min_bracelet_multi(a, b, q: int, devices) -> Candidate:
+    """lms_min_bracelet_multi: one fit sharded over len(devices) shards, shard r
+    on GPU devices[r] (NCCL between distinct GPUs, host exchange otherwise)."""
+    lib = _lib_ready()
+    a = _f64(a)
+    b = _f64(b)
+    dv = np.ascontiguousarray(devices, dtype=np.int32)
+    out = Candidate()
+    check(lib.lms_min_bracelet_multi(_dp(a), _dp(b), a.size, int(q), dv.size,
+                                     dv.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), ctypes.byref(out)))
+    return out
+
+
+def nccl_available() -> tuple[bool, int]:
+    """(libnccl.so.2 loadable, its version code)."""
+    v = ctypes.c_int(0)
+    ok = load_library().lms_nccl_available(ctypes.byref(v))
+    return bool(ok), v.value
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh 128-byte NCCL unique id (rank 0 of a torchrun job makes it)."""
+    buf = (ctypes.c_uint8 * 128)()
+    check(load_library().lms_nccl_unique_id(buf))
+    return bytes(buf)
 
 
 def solve_fit(a, b, q: int, device: int = 0):
@@ -507,6 +543,30 @@ class Context:
             self._h, int(q), int(nshards), int(shard), len(lb), lb.ctypes.data_as(_D),
             wq.ctypes.data_as(_D), edge.ctypes.data_as(ctypes.POINTER(ctypes.c_float)),
             ctypes.byref(seed) if seed is not None else None, ctypes.byref(out)))
+        return out
+
+    def shard_search_owned(self, q: int, nshards: int, shard: int, seed=None) -> Candidate:
+        """Own-band search of this shard after its shard_plan on this context,
+        with the best seed over all shards (lms_ctx_shard_search_owned)."""
+        out = Candidate()
+        check(self._lib.lms_ctx_shard_search_owned(self._h, int(q), int(nshards), int(shard),
+                                                   ctypes.byref(seed) if seed is not None else None,
+                                                   ctypes.byref(out)))
+        return out
+
+    def comm_init(self, nranks: int, rank: int, unique_id: bytes):
+        """Bind an NCCL communicator (rank of nranks) to this context."""
+        if len(unique_id) != 128:
+            raise ValueError("an NCCL unique id has 128 bytes")
+        buf = (ctypes.c_uint8 * 128).from_buffer_copy(unique_id)
+        check(self._lib.lms_ctx_comm_init(self._h, int(nranks), int(rank), buf))
+
+    def solve_distributed(self, q: int) -> Candidate:
+        """The sharded band search of the bound lines over the communicator:
+        plan, all-gather of seed records, own-band search, all-gather of the
+        records; the same record on every rank."""
+        out = Candidate()
+        check(self._lib.lms_ctx_solve_distributed(self._h, int(q), ctypes.byref(out)))
         return out
 
     def solve_materialized(self, q: int, rank_begin: int, rank_end: int) -> Candidate:

@@ -26,7 +26,6 @@ from __future__ import annotations
 
 import math
 import os
-import threading
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
 from typing import Iterable, Iterator, Sequence
@@ -176,54 +175,15 @@ def _env_shards(devices: int) -> int:
     return shards
 
 
-_SHARD_CTX: dict = {}
-# The shard contexts are process-global and a sharded search binds its lines
-# to them across three calls (upload, plan, search): one search at a time.
-_SHARD_LOCK = threading.Lock()
-
-
-def _shard_context(shard: int, device: int):
-    key = (shard, device)
-    ctx = _SHARD_CTX.get(key)
-    if ctx is None:
-        ctx = _SHARD_CTX[key] = _native.Context(device)
-    return ctx
-
-
 def _sharded_search(a: np.ndarray, b: np.ndarray, q: int, shards: int,
                     devices: int) -> CandidateRecord | None:
-    """The sharded band search (distributed.solve_sharded) over the visible
-    GPUs of this process, one thread and context per shard: each shard bounds
-    its slice of the slope bands, the slices and seeds are joined on the host,
-    each shard searches its BatchPlan partition against the full table, and
-    the records are merged (backend.py:182-187).  Same record as one solve."""
-    from . import distributed
-
-    with _SHARD_LOCK:
-        return _sharded_search_locked(a, b, q, shards, devices)
-
-
-def _sharded_search_locked(a, b, q, shards, devices):
-    from . import distributed
-
-    ctxs = [_shard_context(r, r % devices) for r in range(shards)]
-    with ThreadPoolExecutor(max_workers=shards) as pool:
-        list(pool.map(lambda c: c.upload(a, b), ctxs))
-        plans = list(pool.map(lambda r: ctxs[r].shard_plan(q, shards, r), range(shards)))
-        nbands = plans[0][0]
-        table = (distributed.interleave_band_table([p[1] for p in plans], nbands) if nbands
-                 else plans[0][1])
-        seed = None
-        for p in plans:
-            seed = merge(seed, record_from_native(p[2]))
-        seed_c = _native.Candidate.of(seed)
-        recs = list(pool.map(lambda r: record_from_native(ctxs[r].shard_search(q, shards, r, table,
-                                                                                 seed_c)),
-                             range(shards)))
-    best: CandidateRecord | None = None
-    for rec in recs:
-        best = merge(best, rec)
-    return best
+    """The sharded band search over the visible GPUs of this process
+    (lms_min_bracelet_multi): shard r on GPU r % devices, one host thread per
+    shard inside the library, NCCL between distinct GPUs; each shard bounds
+    and seeds its own slice of the slope bands, the seed records are
+    all-gathered, each shard searches its own bands, and the records are
+    all-gathered and merged (backend.py:182-187).  Same record as one solve."""
+    return record_from_native(_native.min_bracelet_multi(a, b, q, [r % devices for r in range(shards)]))
 
 
 _BACKENDS = {"seq": SequentialBackend, "par": ParallelBackend}

@@ -23,7 +23,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <condition_variable>
 #include <mutex>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -32,6 +34,7 @@
 #include "lms_common.cuh"
 #include "lms_hough.cuh"
 #include "lms_kernels.cuh"
+#include "lms_nccl.cuh"
 #include "lms_plan.cuh"
 #include "lms_primal.cuh"
 
@@ -134,7 +137,7 @@ struct HostFit {
 // takes every band's bound from the caller (search) and searches its own
 // rank range.
 struct ShardSpec {
-  int mode = 0;          // 1 plan, 2 search
+  int mode = 0;          // 1 plan, 2 search (rank range), 3 search (own bands)
   int64_t P0 = 0, P1 = 0;
   int nshards = 1, shard = 0;
   int64_t K = 0, k0 = 0, k1 = 0;  // plan: set by band_solve (k0 = k1 = bands in the slice)
@@ -158,6 +161,8 @@ struct ShardPlanState {
   int64_t n = 0, q = 0, K = 0, S = 0, P0 = 0, pspan = 0;
   std::vector<float> h_bnd;
   std::vector<unsigned> h_scnt;
+  std::vector<double> h_lb;  // the plan's bounds of its own slice (+inf elsewhere)
+  int nshards = 0, shard = -1;
 };
 
 // contiguous share `s` of `total` items over `parts` (ceil split, as
@@ -294,6 +299,16 @@ struct lms_ctx {
   int64_t hough_npts = 0, hough_width = 1;
   int64_t hough_maxid = 0;  // bound of the support ids of the last vote
   lms_stats stats{};
+  // multi-GPU: this context's NCCL communicator (lms_ctx_comm_init) and the
+  // device buffers of its two record exchanges
+  // the last shard plan run on this context (gen of its lines, shard, bands)
+  uint64_t plan_gen = ~0ull;
+  int plan_nshards = 0, plan_shard = -1;
+  int64_t plan_K = 0;
+  ncclComm_t comm = nullptr;
+  bool comm_owned = false;
+  int comm_ranks = 0, comm_rank = -1;
+  DevBuf<lms_candidate> xsend, xrecv;
   std::mutex mu;
 };
 
@@ -434,6 +449,19 @@ void ctx_release(lms_ctx* c) {
   c->dg_slot.release();
   c->small_cnt.release();
   c->blines32.release();
+  c->sw_k1.release();
+  c->sw_k2.release();
+  c->sw_idx.release();
+  c->sw_pos.release();
+  c->sw_P.release();
+  c->sw_bmin.release();
+  c->sw_suf.release();
+  c->sw_rk.release();
+  c->sw_ends.release();
+  c->xsend.release();
+  c->xrecv.release();
+  if (c->comm && c->comm_owned && lmsb::nccl().ok) lmsb::nccl().CommDestroy(c->comm);
+  c->comm = nullptr;
   if (c->h_best) cudaFreeHost(c->h_best);
   if (c->pin) cudaFreeHost(c->pin);
   if (c->stream) cudaStreamDestroy(c->stream);
@@ -685,6 +713,7 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
                        (long long)sh->K_in, K);
     k0 = k1 = 0;
   }
+  if (sh && sh->mode == 3) k0 = k1 = 0;  // own bands' bounds come from this context's plan
   const int kSeedBands = c->seed_bands;
   const int64_t seed_cap = S;
   RC_TRY(c->bsample.need(2 * S));
@@ -787,8 +816,13 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   // a shard search reuses its context's plan (samples, boundaries, counts)
   // when the same fit was planned on it last
   ShardPlanState& sp = c->splan;
-  const bool reuse = sh && sh->mode == 2 && sp.valid && sp.gen == c->gen && sp.n == h.n &&
-                     sp.q == h.q && sp.K == K && sp.S == S && sp.P0 == P0 && sp.pspan == pspan;
+  const bool reuse = sh && (sh->mode == 2 || sh->mode == 3) && sp.valid && sp.gen == c->gen &&
+                     sp.n == h.n && sp.q == h.q && sp.K == K && sp.S == S && sp.P0 == P0 &&
+                     sp.pspan == pspan;
+  if (sh && sh->mode == 3 &&
+      !(reuse && sp.nshards == sh->nshards && sp.shard == sh->shard))
+    return set_error(LMS_ERR_INVALID,
+                     "own-band shard search needs the shard's plan on this context first");
   if (!reuse) {
     sp.valid = false;
     if (lmsb::launch_band_sample(bf, w, c->sms, c->stream) != 0)
@@ -924,7 +958,7 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
       CUDA_TRY(cudaMemsetAsync(sc + 2, 0, sizeof(unsigned long long), c->stream));
       lmsb::launch_band_seeds(bf, w, c->ranks.p, c->item_fit.p, 0, 0, sc + 2, c->stream);
     }
-    if (nsl > sh->cap)
+    if (sh->lb_out && nsl > sh->cap)
       return set_error(LMS_ERR_INVALID, "shard plan: %d bands exceed the capacity %lld", nsl,
                        (long long)sh->cap);
     if (coarse && nsl > 0) {
@@ -961,7 +995,7 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     CUDA_TRY(cudaMemcpyAsync(h_edge.data(), c->bedge.p, sizeof(float) * h_edge.size(),
                              cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
-    for (int t = 0; t < nsl; ++t) {
+    for (int t = 0; t < nsl && sh->lb_out; ++t) {
       const int32_t k = slice_ids[t];
       sh->lb_out[t] = p_lb[k];
       sh->wq_out[t] = p_wq[k];
@@ -974,6 +1008,10 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     sh->k1 = nsl;
     sp.h_bnd.assign(p_bnd, p_bnd + (K - 1));
     sp.h_scnt.assign(p_scnt, p_scnt + K);
+    sp.h_lb.assign(K, INFINITY);
+    for (int32_t k : slice_ids) sp.h_lb[k] = p_lb[k];
+    sp.nshards = sh->nshards;
+    sp.shard = sh->shard;
     sp.valid = true;
     sp.gen = c->gen;
     sp.n = h.n;
@@ -994,7 +1032,28 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   std::vector<unsigned> scnt;
   double H = INFINITY;
   std::vector<uint8_t> flag(K + 1, 0);
-  if (sh && sh->mode == 2) {
+  if (sh && sh->mode == 3) {
+    // ---- own-band search: this shard's bands (shard, shard + nshards, ...)
+    // with the bounds its own plan computed, every other band dismissed, the
+    // global seed record (exchanged) installed; the whole pair space searched
+    if (sh->seed_in.found) {
+      lms_candidate* p_seed = p_hb;
+      *p_seed = sh->seed_in;
+      p_seed->reserved = 0;
+      CUDA_TRY(cudaMemcpyAsync(c->recs.p, p_seed, sizeof(lms_candidate), cudaMemcpyHostToDevice,
+                               c->stream));
+      lmsb::launch_reduce(c->recs.p, nullptr, 1, 1, c->fits.p, c->keys.p, c->best.p, 1,
+                          c->stream);
+      st->launches += 2;
+      H = sh->seed_in.height;
+    }
+    hbnd = sp.h_bnd;
+    scnt = sp.h_scnt;
+    lb = sp.h_lb;
+    wq.assign(K, INFINITY);
+    CUDA_TRY(cudaEventRecord(c->ev_chunk[1], c->stream));
+    CUDA_TRY(cudaEventRecord(c->ev_chunk[7], c->stream));
+  } else if (sh && sh->mode == 2) {
     // ---- search: every band's bound and the global seed record from the
     // caller (the exchanged plan); boundaries and counts from this context's
     // plan, or recomputed
@@ -1088,7 +1147,7 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     scnt.assign(p_scnt, p_scnt + K);
     H = hb.found ? hb.height : INFINITY;
   }
-  if (coarse && !(sh && sh->mode == 2)) {  // (a shard's plan refined its own slice)
+  if (coarse && !(sh && (sh->mode == 2 || sh->mode == 3))) {  // (a shard's plan refined its own slice)
     // the bands the coarse bounds cannot dismiss get their exact bound
     std::vector<int32_t> cand;
     for (int k = 0; k < K; ++k)
@@ -1171,7 +1230,7 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     runs.lo[0] = INFINITY;
     runs.hi[0] = -INFINITY;
   }
-  for (int e = 0; e < runs.count; ++e) {
+  for (int e = 0; e < (int)rr.size(); ++e) {  // (no run: the empty run set above)
     const int k0 = rr[e].first, k1 = rr[e].second;
     const double lo = k0 == 0 ? -INFINITY : (double)std::nextafter(hbnd[k0 - 1], -INFINITY);
     const double hi = k1 == K - 1 ? INFINITY : (double)hbnd[k1];
@@ -1317,8 +1376,13 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   // inversions between the lines' orders at its ends (lms_sweep.cu).  Needs
   // every inner boundary inside the fp32-key range, so that vertices beyond
   // it (class 2) can only lie in the two outer bands.
-  bool sweep = (c->band_sweep == 1 || (c->band_sweep == 2 && h.n >= kSweepMinN)) && !rr.empty() &&
+  // an own-band search covers the whole pair space for few bands: always swept
+  const bool own_bands = sh && sh->mode == 3;
+  bool sweep = (c->band_sweep == 1 || (c->band_sweep == 2 && (h.n >= kSweepMinN || own_bands))) &&
                h.n >= 3 && h.n <= lmsb::kBandMaxBigN;
+  // (an own-band search with no admitted band still owns the outer bands'
+  // class-2 vertices; otherwise a search needs a run)
+  if (rr.empty() && !own_bands) sweep = false;
   for (int k = 0; sweep && k < K - 1; ++k)
     sweep = std::isfinite(hbnd[k]) && std::fabs((double)hbnd[k]) * bf.amax < 1e29;
   lmsb::SweepArgs sa{};
@@ -1327,7 +1391,8 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     // across the smallest gaps down to kSweepMaxRuns
     std::vector<std::pair<int, int>> sr;
     for (int k = 0; k < K; ++k) {
-      if (!(flag[k] || k == 0 || k == K - 1)) continue;
+      const bool outer = (k == 0 || k == K - 1) && (!own_bands || k % sh->nshards == sh->shard);
+      if (!(flag[k] || outer)) continue;
       if (!sr.empty() && sr.back().second == k - 1) sr.back().second = k;
       else sr.push_back({k, k});
     }
@@ -2267,6 +2332,190 @@ int shared_ctx(int device, lms_ctx** out) {
   return LMS_OK;
 }
 
+// ---------------------------------------------------------------- multi-GPU
+// Sharded band search with band ownership: every shard samples the whole
+// pair space (the same slope bands everywhere), bounds and seeds its own
+// interleaved slice of the bands (shard, shard + nshards, ...), the seed
+// records are exchanged (one all-gather of 56-byte records), and each shard
+// searches the vertices of its own bands that the best seed cannot dismiss,
+// over the whole pair space; a second all-gather of the records and the
+// lexicographic (height, i, j) minimum (backend.py:182-187) finish the fit.
+// Every vertex lies in exactly one band and the global seed is a real
+// vertex, so the minimum is the one-GPU record for any shard count.  Fits
+// too small for the band stage (the plan reports no bands) split the pair
+// ranks instead (BatchPlan.partitions, backend.py:84-92).
+
+// plan of shard `shard` (no band-table output); *nbands = 0: not banded
+int owned_plan(lms_ctx* c, int64_t q, int nshards, int shard, lms_candidate* seed,
+               int64_t* nbands) {
+  const int64_t n = c->nlines;
+  RC_TRY(check_fit(c, 0, n, q));
+  const int64_t total = n * (n - 1) / 2;
+  ShardSpec sp;
+  sp.mode = 1;
+  sp.P0 = 0;
+  sp.P1 = total;
+  sp.nshards = nshards;
+  sp.shard = shard;
+  c->shard = &sp;
+  lms_candidate dummy;
+  std::vector<HostFit> hf{{0, n, q, 0, total}};
+  const int rc = ctx_solve_fits(c, hf, &dummy);
+  c->shard = nullptr;
+  if (rc != LMS_OK) return rc;
+  *seed = sp.seed_out;
+  *nbands = sp.K;
+  c->plan_gen = c->gen;
+  c->plan_nshards = nshards;
+  c->plan_shard = shard;
+  c->plan_K = sp.K;
+  return LMS_OK;
+}
+
+// search of shard `shard` after its plan: own bands (banded) or its pair-rank
+// partition (not banded), with the exchanged best seed installed
+int owned_search(lms_ctx* c, int64_t q, int nshards, int shard, int64_t nbands,
+                 const lms_candidate& seed, lms_candidate* out) {
+  const int64_t n = c->nlines;
+  RC_TRY(check_fit(c, 0, n, q));
+  const int64_t total = n * (n - 1) / 2;
+  std::memset(out, 0, sizeof(*out));
+  if (nbands <= 0) {
+    int64_t r0, r1;
+    share_of(total, nshards, shard, &r0, &r1);
+    if (r1 <= r0) return LMS_OK;
+    std::vector<HostFit> hf{{0, n, q, r0, r1}};
+    return ctx_solve_fits(c, hf, out);
+  }
+  ShardSpec sp;
+  sp.mode = 3;
+  sp.P0 = 0;
+  sp.P1 = total;
+  sp.nshards = nshards;
+  sp.shard = shard;
+  sp.seed_in = seed;
+  c->shard = &sp;
+  std::vector<HostFit> hf{{0, n, q, 0, total}};
+  const int rc = ctx_solve_fits(c, hf, out);
+  c->shard = nullptr;
+  return rc;
+}
+
+lms_candidate cand_min(const lms_candidate* recs, int m) {
+  lms_candidate best{};
+  for (int r = 0; r < m; ++r)
+    if (lmsb::cand_less(recs[r], best)) best = recs[r];
+  return best;
+}
+
+#define NCCL_TRY(expr)                                                                     \
+  do {                                                                                     \
+    const ncclResult_t nr_ = (expr);                                                       \
+    if (nr_ != ncclSuccess)                                                                \
+      return set_error(LMS_ERR_CUDA, "%s: %s", #expr, lmsb::nccl().GetErrorString(nr_)); \
+  } while (0)
+
+// All-gather of one record per rank over the context's NCCL communicator, on
+// device buffers (the context's stream); all[0 .. comm_ranks) on the host.
+int nccl_gather_records(lms_ctx* c, const lms_candidate& mine, lms_candidate* all) {
+  const int R = c->comm_ranks;
+  RC_TRY(c->xsend.need(1));
+  RC_TRY(c->xrecv.need(R));
+  RC_TRY(ensure_pinned(c, sizeof(lms_candidate) * (R + 1)));
+  lms_candidate* pin = reinterpret_cast<lms_candidate*>(c->pin);
+  pin[0] = mine;
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaMemcpyAsync(c->xsend.p, pin, sizeof(lms_candidate), cudaMemcpyHostToDevice,
+                           c->stream));
+  NCCL_TRY(lmsb::nccl().AllGather(c->xsend.p, c->xrecv.p, sizeof(lms_candidate), ncclUint8,
+                                  c->comm, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(pin + 1, c->xrecv.p, sizeof(lms_candidate) * R, cudaMemcpyDeviceToHost,
+                           c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  std::memcpy(all, pin + 1, sizeof(lms_candidate) * R);
+  return LMS_OK;
+}
+
+// In-process exchange between the shard threads of one lms_min_bracelet_multi
+// call: a host barrier (shards that share a GPU cannot form an NCCL clique).
+struct HostExchange {
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0, phase = 0, parties = 0;
+  std::vector<lms_candidate> slots;
+  bool failed = false;
+  // publish `mine` at `rank`, wait for everyone, copy all records out
+  bool gather(int rank, const lms_candidate& mine, lms_candidate* all, bool ok) {
+    std::unique_lock<std::mutex> lk(mu);
+    slots[rank] = mine;
+    failed |= !ok;
+    const int ph = phase;
+    if (++arrived == parties) {
+      arrived = 0;
+      ++phase;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return phase != ph; });
+    }
+    std::copy(slots.begin(), slots.end(), all);
+    return !failed;
+  }
+};
+
+struct MultiCtx {
+  std::vector<int> devices;
+  std::vector<lms_ctx*> ctxs;
+  bool nccl = false;
+};
+std::mutex g_multi_mu;
+MultiCtx g_multi;
+
+void multi_release() {
+  for (lms_ctx* c : g_multi.ctxs) {
+    ctx_release(c);
+    delete c;
+  }
+  g_multi.ctxs.clear();
+  g_multi.devices.clear();
+  g_multi.nccl = false;
+}
+
+// contexts (and, with NCCL, a communicator clique) for this shard-to-device map
+int multi_setup(const int32_t* devices, int nshards, bool use_nccl) {
+  std::vector<int> dv(devices, devices + nshards);
+  if (g_multi.devices == dv && g_multi.nccl == use_nccl && (int)g_multi.ctxs.size() == nshards)
+    return LMS_OK;
+  multi_release();
+  for (int r = 0; r < nshards; ++r) {
+    lms_ctx* c = new lms_ctx();
+    const int rc = ctx_init(c, dv[r]);
+    if (rc) {
+      ctx_release(c);
+      delete c;
+      multi_release();
+      return rc;
+    }
+    g_multi.ctxs.push_back(c);
+  }
+  if (use_nccl) {
+    std::vector<ncclComm_t> comms(nshards);
+    const ncclResult_t nr = lmsb::nccl().CommInitAll(comms.data(), nshards, dv.data());
+    if (nr != ncclSuccess) {
+      multi_release();
+      return set_error(LMS_ERR_CUDA, "ncclCommInitAll: %s", lmsb::nccl().GetErrorString(nr));
+    }
+    for (int r = 0; r < nshards; ++r) {
+      g_multi.ctxs[r]->comm = comms[r];
+      g_multi.ctxs[r]->comm_owned = true;
+      g_multi.ctxs[r]->comm_ranks = nshards;
+      g_multi.ctxs[r]->comm_rank = r;
+    }
+  }
+  g_multi.devices = dv;
+  g_multi.nccl = use_nccl;
+  return LMS_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -2550,6 +2799,10 @@ int lms_ctx_shard_plan(lms_ctx* c, int64_t q, int32_t nshards, int32_t shard, in
   *nbands = sp.K;
   *nslice = sp.k0;
   *seed = sp.seed_out;
+  c->plan_gen = c->gen;
+  c->plan_nshards = nshards;
+  c->plan_shard = shard;
+  c->plan_K = sp.K;
   return LMS_OK;
 }
 
@@ -2585,6 +2838,148 @@ int lms_ctx_shard_search(lms_ctx* c, int64_t q, int32_t nshards, int32_t shard, 
   const int rc = ctx_solve_fits(c, hf, out);
   c->shard = nullptr;
   return rc;
+}
+
+int lms_ctx_shard_search_owned(lms_ctx* c, int64_t q, int32_t nshards, int32_t shard,
+                               const lms_candidate* seed, lms_candidate* out) {
+  if (!c || !out) return set_error(LMS_ERR_INVALID, "null argument");
+  if (nshards < 1 || shard < 0 || shard >= nshards)
+    return set_error(LMS_ERR_INVALID, "bad shard %d of %d", shard, nshards);
+  std::lock_guard<std::mutex> lk(c->mu);
+  std::memset(out, 0, sizeof(*out));
+  if (!c->a) return set_error(LMS_ERR_INVALID, "no lines bound to the context");
+  if (!(c->plan_gen == c->gen && c->plan_nshards == nshards && c->plan_shard == shard))
+    return set_error(LMS_ERR_INVALID,
+                     "own-band search of shard %d/%d needs that shard's plan on this context first",
+                     shard, nshards);
+  lms_candidate none{};
+  return owned_search(c, q, nshards, shard, c->plan_K, seed ? *seed : none, out);
+}
+
+int lms_nccl_available(int* version) {
+  const lmsb::NcclApi& api = lmsb::nccl();
+  if (version) {
+    *version = 0;
+    if (api.ok) api.GetVersion(version);
+  }
+  return api.ok ? 1 : 0;
+}
+
+int lms_nccl_unique_id(uint8_t* id) {
+  if (!id) return set_error(LMS_ERR_INVALID, "null argument");
+  if (!lmsb::nccl().ok) return set_error(LMS_ERR_INVALID, "NCCL (libnccl.so.2) not available");
+  ncclUniqueId u;
+  NCCL_TRY(lmsb::nccl().GetUniqueId(&u));
+  std::memcpy(id, u.internal, NCCL_UNIQUE_ID_BYTES);
+  return LMS_OK;
+}
+
+int lms_ctx_comm_init(lms_ctx* c, int32_t nranks, int32_t rank, const uint8_t* id) {
+  if (!c || !id) return set_error(LMS_ERR_INVALID, "null argument");
+  if (nranks < 1 || rank < 0 || rank >= nranks)
+    return set_error(LMS_ERR_INVALID, "bad rank %d of %d", rank, nranks);
+  if (!lmsb::nccl().ok) return set_error(LMS_ERR_INVALID, "NCCL (libnccl.so.2) not available");
+  std::lock_guard<std::mutex> lk(c->mu);
+  if (c->comm && c->comm_owned) lmsb::nccl().CommDestroy(c->comm);
+  c->comm = nullptr;
+  ncclUniqueId u;
+  std::memcpy(u.internal, id, NCCL_UNIQUE_ID_BYTES);
+  CUDA_TRY(cudaSetDevice(c->device));
+  ncclComm_t comm;
+  NCCL_TRY(lmsb::nccl().CommInitRank(&comm, nranks, u, rank));
+  c->comm = comm;
+  c->comm_owned = true;
+  c->comm_ranks = nranks;
+  c->comm_rank = rank;
+  return LMS_OK;
+}
+
+int lms_ctx_solve_distributed(lms_ctx* c, int64_t q, lms_candidate* out) {
+  if (!c || !out) return set_error(LMS_ERR_INVALID, "null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  std::memset(out, 0, sizeof(*out));
+  if (!c->comm) return set_error(LMS_ERR_INVALID, "no communicator (lms_ctx_comm_init first)");
+  if (!c->a) return set_error(LMS_ERR_INVALID, "no lines bound to the context");
+  const int R = c->comm_ranks, r = c->comm_rank;
+  lms_candidate seed{}, mine{};
+  int64_t nb = 0;
+  RC_TRY(owned_plan(c, q, R, r, &seed, &nb));
+  std::vector<lms_candidate> all(R);
+  RC_TRY(nccl_gather_records(c, seed, all.data()));
+  RC_TRY(owned_search(c, q, R, r, nb, cand_min(all.data(), R), &mine));
+  RC_TRY(nccl_gather_records(c, mine, all.data()));
+  *out = cand_min(all.data(), R);
+  return LMS_OK;
+}
+
+int lms_min_bracelet_multi(const double* a, const double* b, int64_t n, int64_t q,
+                           int32_t nshards, const int32_t* devices, lms_candidate* out) {
+  if (!a || !b || !out || !devices) return set_error(LMS_ERR_INVALID, "null argument");
+  if (nshards < 1 || nshards > 64) return set_error(LMS_ERR_INVALID, "bad shard count %d", nshards);
+  std::memset(out, 0, sizeof(*out));
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+    return set_error(LMS_ERR_NODEVICE, "no CUDA device available");
+  std::vector<int> dv(devices, devices + nshards);
+  bool distinct = true;
+  for (int r = 0; r < nshards; ++r) {
+    if (dv[r] < 0 || dv[r] >= count)
+      return set_error(LMS_ERR_NODEVICE, "device %d out of range (%d devices)", dv[r], count);
+    for (int t = 0; t < r; ++t) distinct &= dv[t] != dv[r];
+  }
+  // NCCL between distinct GPUs (LMSB_NCCL=0 disables, =1 also for one shard);
+  // shards sharing a GPU exchange through host memory
+  const char* env = getenv("LMSB_NCCL");
+  const int nccl_knob = env ? atoi(env) : 2;
+  const bool use_nccl = lmsb::nccl().ok && distinct && nccl_knob != 0 &&
+                        (nshards > 1 || nccl_knob == 1);
+  std::lock_guard<std::mutex> lk(g_multi_mu);
+  RC_TRY(multi_setup(devices, nshards, use_nccl));
+  HostExchange hx;
+  hx.parties = nshards;
+  hx.slots.assign(nshards, lms_candidate{});
+  std::vector<int> rcs(nshards, LMS_OK);
+  std::vector<std::string> errs(nshards);
+  std::vector<lms_candidate> result(nshards);
+  auto shard_main = [&](int r) {
+    lms_ctx* c = g_multi.ctxs[r];
+    std::lock_guard<std::mutex> ck(c->mu);
+    std::vector<lms_candidate> all(nshards);
+    lms_candidate seed{}, mine{};
+    int64_t nb = 0;
+    int rc = ctx_upload(c, a, b, n);
+    if (rc == LMS_OK) rc = owned_plan(c, q, nshards, r, &seed, &nb);
+    if (use_nccl) {
+      // (a failed rank still joins both collectives with an empty record)
+      int rc2 = nccl_gather_records(c, seed, all.data());
+      if (rc == LMS_OK) rc = rc2;
+      if (rc == LMS_OK) rc = owned_search(c, q, nshards, r, nb, cand_min(all.data(), nshards), &mine);
+      rc2 = nccl_gather_records(c, rc == LMS_OK ? mine : lms_candidate{}, all.data());
+      if (rc == LMS_OK) rc = rc2;
+    } else {
+      bool ok = hx.gather(r, seed, all.data(), rc == LMS_OK);
+      if (rc == LMS_OK && ok) rc = owned_search(c, q, nshards, r, nb, cand_min(all.data(), nshards), &mine);
+      ok = hx.gather(r, mine, all.data(), rc == LMS_OK && ok);
+      if (rc == LMS_OK && !ok) rc = LMS_ERR_CUDA;
+    }
+    if (rc != LMS_OK) errs[r] = lms_last_error();
+    rcs[r] = rc;
+    result[r] = cand_min(all.data(), nshards);
+  };
+  if (nshards == 1) {
+    shard_main(0);
+  } else {
+    std::vector<std::thread> th;
+    for (int r = 0; r < nshards; ++r) th.emplace_back(shard_main, r);
+    for (auto& t : th) t.join();
+  }
+  for (int r = 0; r < nshards; ++r)
+    if (rcs[r] != LMS_OK) {
+      const bool own = !errs[r].empty() && errs[r] != "ok";
+      return set_error(rcs[r], "shard %d: %s", r, own ? errs[r].c_str() : "peer failure");
+    }
+  *out = result[0];
+  return LMS_OK;
 }
 
 int lms_ctx_solve_batch(lms_ctx* c, const int64_t* offsets, const int64_t* q, int64_t nfits,

@@ -1,21 +1,21 @@
-"""Multi-GPU exact LMS: one process per GPU, rank-space partitions, one collective.
+"""Multi-GPU exact LMS: one process per GPU, one fit's vertices shared out.
 
-The vertex index space (row-major pair ranks, backend.py:111-122) is split
-into contiguous partitions exactly as ``BatchPlan.partitions`` does
-(backend.py:84-92).  Each process solves its partition on its own GPU; the
-per-rank best records are combined with a single ``all_gather`` (NCCL over
-NVLink on the GPU box) and every rank takes the same lexicographic
-(height, i, j) minimum (backend.py:182-187), so the result is bit-identical
-for any world size.
+``solve_sharded`` is the sharded band search with band ownership (SURVEY
+section 8e; the C ABI's lms_ctx_solve_distributed): every rank samples the
+whole pair space (the same slope bands everywhere), bounds and seeds its own
+interleaved slice of the bands, the 56-byte seed records are all-gathered,
+each rank searches the vertices of its own bands that the best seed cannot
+dismiss, and the records are all-gathered and merged with the lexicographic
+(height, i, j) minimum (backend.py:182-187) -- the one-GPU record for any
+world size.  With the ``nccl`` backend both collectives run inside the
+library (ncclAllGather on device buffers over NVLink, the communicator
+bootstrapped from a unique id that rank 0 broadcasts); with ``gloo`` (CPU
+tests, functional runs on one GPU) the same flow runs over
+``torch.distributed`` on host records.
 
-``solve_sharded`` is the band-search form of the same split: the slope-band
-table (one lower bound, window and edge keys per band) is computed in slices,
-one per rank, and exchanged with one more ``all_gather`` before each rank
-searches its partition, so the per-band work is divided as well instead of
-being repeated on every rank.
-
-The combine is expressed over ``torch.distributed`` so the same code runs on
-``nccl`` (GPU tensors) and ``gloo`` (CPU tensors, used by the CPU tests).
+``solve_distributed(..., solve_range=f)`` keeps the plain contiguous-partition
+form (``BatchPlan.partitions``, backend.py:84-92) for CPU tests: each rank
+solves its rank range and one all-gather of records combines them.
 """
 
 from __future__ import annotations
@@ -121,13 +121,14 @@ def _context(device: int):
 
 
 def band_slice(nbands: int, world: int, rank: int) -> range:
-    """Bands a rank bounds in a sharded plan: rank, rank + world, ... (interleaved)."""
+    """Bands a rank owns in a sharded search: rank, rank + world, ... (interleaved)."""
     return range(rank, nbands, world)
 
 
 def interleave_band_table(slices: list, nbands: int) -> np.ndarray:
-    """Full (nbands, cols) table from the ranks' slices (band k = row k // world of
-    rank k % world's slice)."""
+    """Full (nbands, cols) band table from the ranks' interleaved slices (band
+    k = row k // world of rank k % world's slice), the input of the
+    rank-range shard search (lms_ctx_shard_search)."""
     world = len(slices)
     cols = slices[0].shape[1] if slices and slices[0].ndim == 2 else 0
     full = np.empty((nbands, cols), dtype=np.float64)
@@ -136,53 +137,49 @@ def interleave_band_table(slices: list, nbands: int) -> np.ndarray:
     return full
 
 
-def exchange_band_table(table: np.ndarray, nbands: int, seed: CandidateRecord | None = None,
-                        group=None, device=None) -> tuple[np.ndarray, CandidateRecord | None]:
-    """All-gather every rank's band-table slice and plan seed in one collective.
+_comms: dict = {}
 
-    Returns the full (nbands, cols) table and the minimum of the seeds.  Each
-    rank sends one header row (its packed seed record, RECORD_FIELDS wide)
-    followed by its slice (bands rank, rank + world, ...; band_slice), padded
-    to ceil(nbands / world) rows.
-    """
-    import torch
+
+def _native_comm(ctx, group) -> bool:
+    """Bind an NCCL communicator over ``group`` to ``ctx`` inside the library
+    (rank 0 makes the unique id, one broadcast); False when the library
+    cannot load NCCL."""
     import torch.distributed as dist
 
-    world = dist.get_world_size(group)
-    cols = table.shape[1]
-    assert cols == RECORD_FIELDS, "band table rows and records share one row width"
-    per = max(1, -(-nbands // world))
-    mine = torch.zeros((1 + per, cols), dtype=torch.float64)
-    mine[0] = torch.from_numpy(pack(seed))
-    if len(table):
-        mine[1: 1 + len(table)] = torch.from_numpy(np.ascontiguousarray(table))
-    if device is not None:
-        mine = mine.to(device)
-    out = torch.empty((world, 1 + per, cols), dtype=torch.float64, device=mine.device)
-    dist.all_gather_into_tensor(out.view(world * (1 + per), cols), mine, group=group)
-    out = out.cpu().numpy()
-    full = interleave_band_table([out[r, 1:] for r in range(world)], nbands)
-    return full, combine(out[:, 0])
+    from . import _native
+
+    key = (id(ctx), id(group) if group is not None else 0)
+    if key in _comms:
+        return True
+    ok, _ = _native.nccl_available()
+    flags = [ok]
+    dist.broadcast_object_list(flags, src=0, group=group)  # every rank takes the same road
+    if not flags[0]:
+        return False
+    obj = [_native.nccl_unique_id() if dist.get_rank(group) == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    ctx.comm_init(dist.get_world_size(group), dist.get_rank(group), obj[0])
+    _comms[key] = True
+    return True
 
 
 def solve_sharded(ctx, q: int, *, group=None, device=None) -> CandidateRecord | None:
     """Sharded band search of the lines bound to ``ctx`` (this rank's GPU).
 
-    plan (this rank's band slice and seed) -> one all_gather of the band table
-    and seeds -> search of this rank's partition against the full table ->
-    all_gather of the records -> lexicographic minimum.  Same record as one
-    ``ctx.solve`` over the whole pair space.
+    plan (this rank's own bands and seed) -> all-gather of the seed records ->
+    search of this rank's own bands (or, for fits too small for bands, its
+    pair-rank partition) -> all-gather of the records -> lexicographic
+    minimum.  Same record as one ``ctx.solve`` over the whole pair space.
     """
     import torch.distributed as dist
 
     from ._native import Candidate
 
+    if dist.get_backend(group) == "nccl" and _native_comm(ctx, group):
+        return record_from_native(ctx.solve_distributed(q))
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    nbands, table, seed = ctx.shard_plan(q, world, rank)
-    full, best_seed = table[:0], None
-    if nbands:
-        full, best_seed = exchange_band_table(table, nbands, record_from_native(seed), group=group,
-                                              device=device)
-    rec = record_from_native(ctx.shard_search(q, world, rank, full, Candidate.of(best_seed)))
+    _, _, seed = ctx.shard_plan(q, world, rank)
+    seeds = all_gather_records(record_from_native(seed), group=group, device=device)
+    rec = record_from_native(ctx.shard_search_owned(q, world, rank, Candidate.of(combine(seeds))))
     return combine(all_gather_records(rec, group=group, device=device))

@@ -1,16 +1,23 @@
-"""Dev helper: simulate the N-GPU strong-scaling split on one GPU.
+"""Simulate the N-GPU strong-scaling split of one fit on one GPU.
 
 For every world size R, run each rank's share on the same device and report
 the max over ranks of its device time (what bench.py reports at N=R, minus
-the collectives): `range` = the plain partitioned solve (ctx.solve over the
-rank's partition), `sharded` = the sharded band search (plan slice +
-search of the partition against the exchanged table; the exchange itself is
-a host concatenation here).
+the two 56-byte-per-rank record all-gathers): `range` = the plain
+partitioned solve (ctx.solve over the rank's pair-rank partition),
+`owned` = the sharded band search with band ownership (plan of the rank's
+own band slice + search of its own bands from the best seed over all ranks;
+lms_ctx_solve_distributed's flow, the exchanges done on the host here).
+
+usage: python scripts/sim_scaling.py N [reps]
 """
-import sys, json
-sys.path.insert(0, '.')
+import json
+import sys
+
 import numpy as np
-from paper_1510_01041_b200 import _native, workloads, distributed
+
+sys.path.insert(0, ".")
+from paper_1510_01041_b200 import _native, distributed, workloads  # noqa: E402
+from paper_1510_01041_b200.backend import record_from_native  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
@@ -32,34 +39,30 @@ def timed(fn):
     return best, out
 
 
-ref = None
+one_ms, one = timed(lambda: ctx.solve(q, 0, total))
+ref = record_from_native(one)
 for R in (1, 2, 4, 8):
-    per_range, per_shard, recs = [], [], []
-    plans = []
+    per_range, plans = [], []
     for r in range(R):
         r0, r1 = distributed.partition(total, R, r)
-        ms, rec = timed(lambda: ctx.solve(q, r0, r1))
+        ms, _ = timed(lambda: ctx.solve(q, r0, r1))
         per_range.append(ms)
-        ms_p, plan = timed(lambda: ctx.shard_plan(q, R, r))
-        plans.append((ms_p, plan))
-    K = plans[0][1][0]
-    table = distributed.interleave_band_table([p[1][1] for p in plans], K)
-    from paper_1510_01041_b200.backend import record_from_native
+        plans.append(timed(lambda: ctx.shard_plan(q, R, r)))
     seed = distributed.combine(np.stack([distributed.pack(record_from_native(p[1][2])) for p in plans]))
-    seed = _native.Candidate.of(seed)
-    detail = []
+    seed_c = _native.Candidate.of(seed)
+    detail, recs = [], []
     for r in range(R):
-        ms_s, rec = timed(lambda: ctx.shard_search(q, R, r, table, seed))
+        ctx.shard_plan(q, R, r)  # the search reuses this rank's plan on the context
+        ms_s, rec = timed(lambda: ctx.shard_search_owned(q, R, r, seed_c))
         st = ctx.stats()
-        recs.append(distributed.pack(__import__("paper_1510_01041_b200").backend.record_from_native(rec)))
-        per_shard.append(plans[r][0] + ms_s)
+        recs.append(distributed.pack(record_from_native(rec)))
         detail.append({"rank": r, "plan_ms": round(plans[r][0], 3), "search_ms": round(ms_s, 3),
                        "searched": st["bands_searched"], "collected": st["filtered_vertices"],
                        "band_surv": st["band_survivors"], "surv": st["survivors"],
-                       "bound": round(st["ms_bound"], 3), "part": round(st["ms_partition"], 3),
-                       "filter": round(st["ms_band_filter"], 3)})
+                       "collect_ms": round(st["ms_collect"], 3),
+                       "filter_ms": round(st["ms_band_filter"], 3)})
     comb = distributed.combine(np.stack(recs))
-    ref = ref or comb
-    print(json.dumps({"n": n, "R": R, "bands": K, "range_max_ms": round(max(per_range), 3),
-                      "sharded_max_ms": round(max(per_shard), 3), "same_record": comb == ref,
-                      "ranks": detail}), flush=True)
+    print(json.dumps({"n": n, "R": R, "one_gpu_ms": round(one_ms, 3), "bands": plans[0][1][0],
+                      "range_max_ms": round(max(per_range), 3),
+                      "owned_max_ms": round(max(d["plan_ms"] + d["search_ms"] for d in detail), 3),
+                      "same_record": comb == ref, "ranks": detail}), flush=True)

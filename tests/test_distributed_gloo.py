@@ -80,35 +80,66 @@ def test_pack_roundtrip_and_combine_order():
     assert distributed.combine(rows) == r2  # equal height: smaller (i, j) wins
 
 
-def _table_worker(rank, world, port, nbands, out_path):
+class _OracleShardCtx:
+    """CPU stand-in for one rank's engine context in the sharded search: the
+    plan's seed is the oracle minimum over a few vertices of the rank's own
+    share, the own-band search the oracle minimum over the whole share merged
+    with the exchanged seed (as the device installs it)."""
+
+    def __init__(self, a, b):
+        self.a, self.b = a, b
+
+    def _rec(self, q, r0, r1):
+        from paper_1510_01041_b200._native import Candidate
+        from paper_1510_01041_b200.backend import CandidateRecord
+
+        rec = oracle.min_bracelet(self.a, self.b, q, r0, r1, threads=1)
+        return Candidate.of(None if rec is None else
+                            CandidateRecord(rec.height, rec.i, rec.j, rec.u, rec.v_low, rec.v_high))
+
+    def shard_plan(self, q, world, rank):
+        n = self.a.size
+        r0, r1 = distributed.partition(n * (n - 1) // 2, world, rank)
+        self.share = (r0, r1)
+        return 3 * world, None, self._rec(q, r0, min(r1, r0 + 7))
+
+    def shard_search_owned(self, q, world, rank, seed):
+        from paper_1510_01041_b200._native import Candidate
+        from paper_1510_01041_b200.backend import merge, record_from_native
+
+        own = record_from_native(self._rec(q, *self.share))
+        return Candidate.of(merge(record_from_native(seed), own))
+
+
+def _owned_worker(rank, world, port, a, b, q, out_path):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from paper_1510_01041_b200.backend import CandidateRecord
-
-        full = np.arange(nbands * 7, dtype=np.float64).reshape(nbands, 7) * 0.5 - 3.0
-        mine = full[list(distributed.band_slice(nbands, world, rank))]
-        seed = None if rank == 0 else CandidateRecord(2.0, 10 - rank, 20, 0.5, -1.0, 1.0)
-        got, best = distributed.exchange_band_table(mine, nbands, seed)
-        np.save(f"{out_path}.{rank}.npy", got)
-        np.save(f"{out_path}.{rank}.seed.npy", distributed.pack(best))
+        rec = distributed.solve_sharded(_OracleShardCtx(a, b), q)
+        np.save(f"{out_path}.{rank}.npy", distributed.pack(rec))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,nbands", [(2, 1024), (3, 1024), (3, 2), (2, 5)])
-def test_gloo_band_table_exchange(tmp_path, world, nbands):
-    """The sharded plan's all_gather reassembles every rank's band slice into
-    the full table in band order, including short and empty last slices."""
-    out = str(tmp_path / "tab")
-    mp.start_processes(_table_worker, args=(world, _free_port(), nbands, out), nprocs=world,
+@pytest.mark.parametrize("world,n,seed", [(2, 40, 0), (3, 33, 1), (2, 25, 2)])
+def test_gloo_sharded_search_flow(tmp_path, world, n, seed):
+    """The sharded search's host flow over gloo: plan seeds all-gathered and
+    merged, each rank's own search started from the best seed, records
+    all-gathered and merged -- every rank ends with the single-process
+    record (duplicate x and exact ties included)."""
+    rng = np.random.default_rng(seed)
+    pts = rng.integers(0, 12, (n, 2)).astype(float)
+    a, b = pts[:, 0].copy(), pts[:, 1].copy()
+    q = n // 2 + 1
+    out = str(tmp_path / "own")
+    mp.start_processes(_owned_worker, args=(world, _free_port(), a, b, q, out), nprocs=world,
                        start_method="spawn")
-    full = np.arange(nbands * 7, dtype=np.float64).reshape(nbands, 7) * 0.5 - 3.0
+    want = oracle.min_bracelet(a, b, q, threads=1)
     for r in range(world):
-        assert np.array_equal(np.load(f"{out}.{r}.npy"), full)
-        best = distributed.unpack(np.load(f"{out}.{r}.seed.npy"))
-        assert (best.i, best.j) == (10 - (world - 1), 20)  # equal heights: smallest (i, j)
+        got = distributed.unpack(np.load(f"{out}.{r}.npy"))
+        assert (got.height, got.i, got.j, got.u, got.v_low, got.v_high) == \
+            (want.height, want.i, want.j, want.u, want.v_low, want.v_high)
 
 
 def test_band_table_pack_roundtrip():

@@ -739,6 +739,75 @@ def test_sharded_band_search_matches_single_solve(n, seed):
         assert record_from_native(ctx.shard_search(q, 4, 1, table, seed)) == warm[1]
 
 
+@pytest.mark.parametrize("n,seed", [(16384, 0), (4096, 3), (20000, 1), (1000, 2), (65536, 0)])
+def test_owned_band_search_matches_single_solve(n, seed):
+    """Band-ownership sharded search (each shard bounds, seeds and searches
+    its own interleaved bands over the whole pair space; seeds and records
+    exchanged) gives the single-GPU record for 1-8 shards, through the
+    context API (plan + shard_search_owned) and through
+    lms_min_bracelet_multi with every shard on this GPU (host exchange).
+    n = 1,000 is below the band threshold: contiguous rank partitions."""
+    from paper_1510_01041_b200 import distributed
+
+    pts = workloads.contaminated_line_points(n, seed)
+    a, b = pts[:, 0].copy(), pts[:, 1].copy()
+    q = n // 2 + 1
+    total = n * (n - 1) // 2
+    ctx = _native.Context()
+    ctx.upload(a, b)
+    want = record_from_native(ctx.solve(q, 0, total))
+    worlds = (1, 2, 3, 8) if n < 65536 else (1, 4)
+    for world in worlds:
+        plans = [ctx.shard_plan(q, world, r) for r in range(world)]
+        seed_c = _native.Candidate.of(distributed.combine(
+            np.stack([distributed.pack(record_from_native(p[2])) for p in plans])))
+        recs = []
+        for r in range(world):
+            ctx.shard_plan(q, world, r)
+            recs.append(distributed.pack(record_from_native(ctx.shard_search_owned(q, world, r, seed_c))))
+        assert distributed.combine(np.stack(recs)) == want, (n, world)
+        got = record_from_native(_native.min_bracelet_multi(a, b, q, [0] * world))
+        assert got == want, (n, world)
+
+
+def test_owned_search_needs_its_plan():
+    pts = workloads.contaminated_line_points(4096, 1)
+    ctx = _native.Context()
+    ctx.upload(pts[:, 0].copy(), pts[:, 1].copy())
+    ctx.shard_plan(2049, 4, 1)
+    with pytest.raises(lms.InvalidInputError):
+        ctx.shard_search_owned(2049, 4, 2)  # the context holds shard 1's plan
+
+
+def test_nccl_paths_one_rank():
+    """The NCCL code paths with the one GPU this box has: a one-rank clique
+    through lms_min_bracelet_multi (LMSB_NCCL=1) and a one-rank
+    communicator bound to a context (lms_ctx_comm_init +
+    lms_ctx_solve_distributed), both on device buffers; same record as the
+    single solve."""
+    ok, ver = _native.nccl_available()
+    assert ok and ver >= 22000, ver
+    n = 16384
+    pts = workloads.contaminated_line_points(n, 0)
+    a, b = pts[:, 0].copy(), pts[:, 1].copy()
+    q = n // 2 + 1
+    ctx = _native.Context()
+    ctx.upload(a, b)
+    want = record_from_native(ctx.solve(q, 0, n * (n - 1) // 2))
+    old = os.environ.get("LMSB_NCCL")
+    os.environ["LMSB_NCCL"] = "1"
+    try:
+        assert record_from_native(_native.min_bracelet_multi(a, b, q, [0])) == want
+    finally:
+        if old is None:
+            os.environ.pop("LMSB_NCCL", None)
+        else:
+            os.environ["LMSB_NCCL"] = old
+    ctx.comm_init(1, 0, _native.nccl_unique_id())
+    assert record_from_native(ctx.solve_distributed(q)) == want
+    assert record_from_native(ctx.solve_distributed(q)) == want  # communicator reused
+
+
 def test_sharded_band_search_degenerate_q_and_ties():
     """q = n (whole-set windows) and a duplicated-x, many-ties input under
     4 shards: same record as the single solve."""
