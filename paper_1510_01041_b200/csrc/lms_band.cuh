@@ -226,6 +226,7 @@ struct SweepArgs {
   int64_t cap;
   unsigned long long* count;
   int smem_tables;        // (launcher) boundaries and slots staged in shared memory
+  unsigned long long* dbg;  // optional: per run, pairs enumerated (LMSB_SWEEP_DEBUG)
 };
 size_t sweep_chunk_smem();
 // sort nseg segments of the n lines by their end keys; returns launches

@@ -284,6 +284,7 @@ struct lms_ctx {
   DevBuf<uint32_t> sw_idx;
   DevBuf<int32_t> sw_pos, sw_P, sw_bmin, sw_suf, sw_rk;
   DevBuf<lmsb::SweepEnd> sw_ends;
+  DevBuf<unsigned long long> sw_dbg;
   DevBuf<unsigned long long> small_cnt;
   int small_mode = 1;  // LMSB_SMALL: 0 off, 1 batches, 2 also single fits
   DevBuf<float2> blines32;
@@ -458,6 +459,7 @@ void ctx_release(lms_ctx* c) {
   c->sw_suf.release();
   c->sw_rk.release();
   c->sw_ends.release();
+  c->sw_dbg.release();
   c->xsend.release();
   c->xrecv.release();
   if (c->comm && c->comm_owned && lmsb::nccl().ok) lmsb::nccl().CommDestroy(c->comm);
@@ -1419,12 +1421,15 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
         hi = (double)hbnd[k1];
         hi += 0x1p-18 * std::fabs(hi) + 1e-37;
       }
+      // clearance of the sort ends: relative to the run's magnitude and width
+      // (not more: a wide sparse run next to a dense slope region must not
+      // reach into it)
       double m;
       if (std::isfinite(lo) && std::isfinite(hi))
-        m = 0x1p-20 * std::max(std::fabs(lo), std::fabs(hi)) + 0x1p-14 * (hi - lo) + 1e-30;
+        m = 0x1p-20 * (std::max(std::fabs(lo), std::fabs(hi)) + (hi - lo)) + 1e-300;
       else
         m = 0x1p-20 * (std::isfinite(lo) ? std::fabs(lo) : std::isfinite(hi) ? std::fabs(hi) : 0.0) +
-            1e-30;
+            1e-300;
       const double s0 = lo - m, s1 = hi + m;
       double smax = 0.0;
       if (std::isfinite(s0)) smax = std::fabs(s0);
@@ -1481,6 +1486,15 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     sa.tau = tau;
     sa.count = w.ncollect;
     st->sweep_runs = nr;
+    if (getenv("LMSB_SWEEP_DEBUG")) {
+      RC_TRY(c->sw_dbg.need(nr + 1));
+      CUDA_TRY(cudaMemsetAsync(c->sw_dbg.p, 0, sizeof(unsigned long long) * (nr + 1), c->stream));
+      sa.dbg = c->sw_dbg.p;
+      for (int e = 0; e < nr; ++e)
+        fprintf(stderr, "sweep run %d: bands [%d, %d] s0 %.17g s1 %.17g kinds %d/%d\n", e, rk[e],
+                rk[nr + e], ends[2 * e].s, ends[2 * e + 1].s, ends[2 * e].kind, ends[2 * e + 1].kind);
+      fprintf(stderr, "sweep tau %.6g\n", tau);
+    }
   }
   for (int attempt = 0; attempt < 2; ++attempt) {
     RC_TRY(c->bck.need(cap));
@@ -1500,6 +1514,13 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     }
     CUDA_TRY(cudaEventRecord(c->ev_chunk[6], c->stream));
     CUDA_TRY(cudaGetLastError());
+    if (sweep && sa.dbg) {
+      std::vector<unsigned long long> d(sa.nruns);
+      CUDA_TRY(cudaMemcpyAsync(d.data(), sa.dbg, sizeof(unsigned long long) * sa.nruns,
+                               cudaMemcpyDeviceToHost, c->stream));
+      CUDA_TRY(cudaStreamSynchronize(c->stream));
+      for (int e = 0; e < sa.nruns; ++e) fprintf(stderr, "sweep run %d: %llu pairs\n", e, d[e]);
+    }
     unsigned long long* p_m = reinterpret_cast<unsigned long long*>(c->pin);
     CUDA_TRY(cudaMemcpyAsync(p_m, sc + 1, sizeof(m), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));

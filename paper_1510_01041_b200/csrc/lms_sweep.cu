@@ -433,6 +433,7 @@ __global__ void __launch_bounds__(kEnumThreads, 4) sweep_enum_kernel(BandFit bf,
           if (tp[e] < 0 && e > 0) break;  // (warp-uniform: the same hits on every lane)
           const bool c = tp[e] > t && tp[e] < n && pv[e] < p;
           const unsigned m = __ballot_sync(0xffffffffu, c);
+          if (sa.dbg && lane == 0) atomicAdd(sa.dbg + r, (unsigned long long)__popc(m));
           if (c) q[qn + __popc(m & ((1u << lane) - 1u))] = me | lv[e];
           qn += __popc(m);
           if (qn >= 32) flush();
