@@ -197,13 +197,12 @@ void launch_band_prepass_split(const BandFit& bf, const BandCount& bc, unsigned*
 // slope run as the inversions between the lines' orders at its two ends
 struct SweepEnd {
   double s;    // kind 0: abscissa of the sort
-  double fin;  // kinds 1/2: the run's finite end (ties of equal slopes)
+  double fin;  // (unused: equal slopes at an infinite end tie-break by line id)
   int kind;    // 0 finite, 1 -inf, 2 +inf, 3 sort by slope a
   int pad;
 };
-struct SweepSort {  // ping-pong (k1, k2, idx) buffers, nseg * n each
+struct SweepSort {  // ping-pong (key, line id) buffers, nseg * n each
   uint64_t* k1[2];
-  uint64_t* k2[2];
   uint32_t* idx[2];
   int cur;  // buffer holding the sorted segments
 };

@@ -280,7 +280,7 @@ struct lms_ctx {
   // pre-test pass over every vertex), 1 always, 2 auto (n >= kSweepMinN, where
   // its fixed sort cost is below the pre-test pass's O(n^2))
   int band_sweep = 2;
-  DevBuf<uint64_t> sw_k1, sw_k2;
+  DevBuf<uint64_t> sw_k1;
   DevBuf<uint32_t> sw_idx;
   DevBuf<int32_t> sw_pos, sw_P, sw_bmin, sw_suf, sw_rk;
   DevBuf<lmsb::SweepEnd> sw_ends;
@@ -451,7 +451,6 @@ void ctx_release(lms_ctx* c) {
   c->small_cnt.release();
   c->blines32.release();
   c->sw_k1.release();
-  c->sw_k2.release();
   c->sw_idx.release();
   c->sw_pos.release();
   c->sw_P.release();
@@ -1446,7 +1445,6 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     const int64_t nn = h.n;
     const int64_t nbk = (nn + 31) / 32;
     RC_TRY(c->sw_k1.need(2 * nseg * nn));
-    RC_TRY(c->sw_k2.need(2 * nseg * nn));
     RC_TRY(c->sw_idx.need(2 * nseg * nn));
     RC_TRY(c->sw_pos.need(nr * nn));
     RC_TRY(c->sw_P.need(nr * nn));
@@ -1461,7 +1459,6 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     lmsb::SweepSort ss{};
     for (int b = 0; b < 2; ++b) {
       ss.k1[b] = c->sw_k1.p + b * nseg * nn;
-      ss.k2[b] = c->sw_k2.p + b * nseg * nn;
       ss.idx[b] = c->sw_idx.p + b * nseg * nn;
     }
     CUDA_TRY(cudaEventRecord(c->ev_chunk[5], c->stream));

@@ -49,9 +49,9 @@ namespace lmsb {
 
 namespace {
 
-constexpr int kChunk = 4096;        // items per CTA-local bitonic sort
-constexpr int kChunkThreads = 1024;
-constexpr int kMergeItems = 8;      // outputs per thread of a merge round
+constexpr int kChunk = 2048;        // items per CTA-local bitonic sort (shared memory)
+constexpr int kChunkThreads = 512;
+constexpr int kMergeItems = 8;      // outputs per thread of a global merge round
 constexpr int kMergeThreads = 256;
 constexpr int kEnumThreads = 256;
 constexpr int kEnumWarps = kEnumThreads / 32;
@@ -63,15 +63,16 @@ constexpr int kHitBatch = 4;
 __device__ __forceinline__ int64_t i64min(int64_t x, int64_t y) { return x < y ? x : y; }
 __device__ __forceinline__ int64_t i64max(int64_t x, int64_t y) { return x > y ? x : y; }
 
-__device__ __forceinline__ bool item_less(uint64_t ak1, uint64_t ak2, uint64_t bk1, uint64_t bk2) {
-  return ak1 < bk1 || (ak1 == bk1 && ak2 < bk2);
+// items are (key, line id): keys unique with the id as the tie-break
+__device__ __forceinline__ bool item_less(uint64_t ak, uint32_t ai, uint64_t bk, uint32_t bi) {
+  return ak < bk || (ak == bk && ai < bi);
 }
 
-// Sort keys of every (segment, line): kind 0 finite end s, 1 at -inf, 2 at +inf
-// (ties by the value at the finite end `fin`), 3 by slope a (near-parallel pass).
+// Sort keys of every (segment, line): kind 0 finite end s (fma(a, s, -b)),
+// 1 at -inf (a descending), 2 at +inf (a ascending), 3 by slope a (the
+// near-parallel pass); equal keys in line order.
 __global__ void sweep_keys_kernel(const double2* __restrict__ ab, int n, const SweepEnd* __restrict__ ends,
-                                  int nseg, uint64_t* __restrict__ k1, uint64_t* __restrict__ k2,
-                                  uint32_t* __restrict__ idx) {
+                                  int nseg, uint64_t* __restrict__ k1, uint32_t* __restrict__ idx) {
   const int64_t total = (int64_t)nseg * n;
   for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total;
        g += (int64_t)gridDim.x * blockDim.x) {
@@ -79,81 +80,59 @@ __global__ void sweep_keys_kernel(const double2* __restrict__ ab, int n, const S
     const int k = (int)(g - (int64_t)s * n);
     const SweepEnd e = ends[s];
     const double2 l = ab[k];
-    uint64_t p, q;
-    if (e.kind == 0) {
-      p = key_of(fma(l.x, e.s, -l.y));
-      q = (uint64_t)k;
-    } else if (e.kind == 3) {
-      p = key_of(l.x);
-      q = (uint64_t)k;
-    } else {
-      p = key_of(e.kind == 1 ? -l.x : l.x);
-      q = (key_of(fma(l.x, e.fin, -l.y)) & ~(uint64_t)0xFFFF) | (uint64_t)k;
-    }
+    uint64_t p;
+    if (e.kind == 0) p = key_of(fma(l.x, e.s, -l.y));
+    else if (e.kind == 1) p = key_of(-l.x);
+    else p = key_of(l.x);
     k1[g] = p;
-    k2[g] = q;
     idx[g] = (uint32_t)k;
   }
 }
 
 // One CTA sorts one chunk of kChunk items of one segment in shared memory
-// (bitonic network; keys are unique, so the order is deterministic).
-__global__ void __launch_bounds__(kChunkThreads, 1) sweep_chunk_sort_kernel(
-    int n, int chunks_per_seg, uint64_t* __restrict__ k1, uint64_t* __restrict__ k2,
-    uint32_t* __restrict__ idx) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  uint64_t* s1 = reinterpret_cast<uint64_t*>(smem_raw);
-  uint64_t* s2 = s1 + kChunk;
-  uint32_t* si = reinterpret_cast<uint32_t*>(s2 + kChunk);
+// (bitonic network over (key, line id); unique keys, deterministic order).
+__global__ void __launch_bounds__(kChunkThreads) sweep_chunk_sort_kernel(
+    int n, int chunks_per_seg, uint64_t* __restrict__ k1, uint32_t* __restrict__ idx) {
+  __shared__ uint64_t sk[kChunk];
+  __shared__ uint32_t si[kChunk];
   const int seg = blockIdx.x / chunks_per_seg;
   const int c = blockIdx.x - seg * chunks_per_seg;
   const int64_t base = (int64_t)seg * n + (int64_t)c * kChunk;
   const int cnt = min(kChunk, n - c * kChunk);
   for (int t = threadIdx.x; t < kChunk; t += kChunkThreads) {
-    if (t < cnt) {
-      s1[t] = k1[base + t];
-      s2[t] = k2[base + t];
-      si[t] = idx[base + t];
-    } else {
-      s1[t] = ~0ull;
-      s2[t] = ~0ull;
-      si[t] = 0xFFFFFFFFu;
-    }
+    sk[t] = t < cnt ? k1[base + t] : ~0ull;
+    si[t] = t < cnt ? idx[base + t] : 0xFFFFFFFFu;
   }
   __syncthreads();
   for (int k = 2; k <= kChunk; k <<= 1) {
     for (int j = k >> 1; j > 0; j >>= 1) {
+#pragma unroll
       for (int t = threadIdx.x; t < kChunk / 2; t += kChunkThreads) {
         const int lo = 2 * t - (t & (j - 1));
         const int hi = lo + j;
-        const bool up = (lo & k) == 0;
-        const uint64_t a1 = s1[lo], a2 = s2[lo], b1 = s1[hi], b2 = s2[hi];
-        if (item_less(b1, b2, a1, a2) == up) {
-          s1[lo] = b1;
-          s2[lo] = b2;
-          s1[hi] = a1;
-          s2[hi] = a2;
-          const uint32_t x = si[lo];
-          si[lo] = si[hi];
-          si[hi] = x;
+        const uint64_t a = sk[lo], b = sk[hi];
+        const uint32_t ia = si[lo], ib = si[hi];
+        if (item_less(b, ib, a, ia) == ((lo & k) == 0)) {
+          sk[lo] = b;
+          sk[hi] = a;
+          si[lo] = ib;
+          si[hi] = ia;
         }
       }
       __syncthreads();
     }
   }
   for (int t = threadIdx.x; t < cnt; t += kChunkThreads) {
-    k1[base + t] = s1[t];
-    k2[base + t] = s2[t];
+    k1[base + t] = sk[t];
     idx[base + t] = si[t];
   }
 }
 
-// One merge round: sorted runs of width w (per segment) pairwise into runs
-// of 2w; merge path per thread (kMergeItems outputs).
+// One global merge round: sorted runs of width w (per segment) pairwise into
+// runs of 2w; merge path per thread (kMergeItems outputs).
 __global__ void __launch_bounds__(kMergeThreads) sweep_merge_kernel(
     int n, int64_t w, int blocks_per_seg, const uint64_t* __restrict__ x1,
-    const uint64_t* __restrict__ x2, const uint32_t* __restrict__ xi, uint64_t* __restrict__ y1,
-    uint64_t* __restrict__ y2, uint32_t* __restrict__ yi) {
+    const uint32_t* __restrict__ xi, uint64_t* __restrict__ y1, uint32_t* __restrict__ yi) {
   const int seg = blockIdx.x / blocks_per_seg;
   const int64_t d0 =
       ((int64_t)(blockIdx.x - seg * blocks_per_seg) * kMergeThreads + threadIdx.x) * kMergeItems;
@@ -168,8 +147,7 @@ __global__ void __launch_bounds__(kMergeThreads) sweep_merge_kernel(
   while (lo < hi) {
     const int64_t mid = (lo + hi) >> 1;
     const int64_t jb = dd - mid - 1;
-    // take A[mid] before B[jb]?  (keys are unique)
-    if (item_less(x1[b0 + jb], x2[b0 + jb], x1[a0 + mid], x2[a0 + mid])) hi = mid;
+    if (item_less(x1[b0 + jb], xi[b0 + jb], x1[a0 + mid], xi[a0 + mid])) hi = mid;
     else lo = mid + 1;
   }
   int64_t ia = lo, ib = dd - lo;
@@ -178,10 +156,9 @@ __global__ void __launch_bounds__(kMergeThreads) sweep_merge_kernel(
     bool takeA;
     if (ia >= la) takeA = false;
     else if (ib >= lb) takeA = true;
-    else takeA = !item_less(x1[b0 + ib], x2[b0 + ib], x1[a0 + ia], x2[a0 + ia]);
+    else takeA = !item_less(x1[b0 + ib], xi[b0 + ib], x1[a0 + ia], xi[a0 + ia]);
     const int64_t src = takeA ? a0 + ia : b0 + ib;
     y1[sb + d] = x1[src];
-    y2[sb + d] = x2[src];
     yi[sb + d] = xi[src];
     if (takeA) ++ia;
     else ++ib;
@@ -481,27 +458,24 @@ __global__ void sweep_parallel_kernel(BandFit bf, SweepArgs sa) {
 
 }  // namespace
 
-size_t sweep_chunk_smem() { return (size_t)kChunk * (2 * sizeof(uint64_t) + sizeof(uint32_t)); }
+size_t sweep_chunk_smem() { return 0; }  // static shared memory
 
 int launch_sweep_sort(const double2* ab, int n, const SweepEnd* ends, int nseg, SweepSort& ss,
                       int sms, cudaStream_t st) {
   if (n <= 0 || nseg <= 0) return 0;
-  sweep_keys_kernel<<<sms * 4, 256, 0, st>>>(ab, n, ends, nseg, ss.k1[0], ss.k2[0], ss.idx[0]);
-  static DeviceOnce done;
-  set_max_smem(sweep_chunk_sort_kernel, sweep_chunk_smem(), done);
+  sweep_keys_kernel<<<sms * 4, 256, 0, st>>>(ab, n, ends, nseg, ss.k1[0], ss.idx[0]);
   const int cps = (n + kChunk - 1) / kChunk;
-  sweep_chunk_sort_kernel<<<nseg * cps, kChunkThreads, sweep_chunk_smem(), st>>>(
-      n, cps, ss.k1[0], ss.k2[0], ss.idx[0]);
-  int cur = 0;
+  sweep_chunk_sort_kernel<<<nseg * cps, kChunkThreads, 0, st>>>(n, cps, ss.k1[0], ss.idx[0]);
+  int cur = 0, launches = 2;
   const int bps = (n + kMergeThreads * kMergeItems - 1) / (kMergeThreads * kMergeItems);
   for (int64_t w = kChunk; w < n; w *= 2) {
-    sweep_merge_kernel<<<nseg * bps, kMergeThreads, 0, st>>>(n, w, bps, ss.k1[cur], ss.k2[cur],
-                                                              ss.idx[cur], ss.k1[cur ^ 1],
-                                                              ss.k2[cur ^ 1], ss.idx[cur ^ 1]);
+    sweep_merge_kernel<<<nseg * bps, kMergeThreads, 0, st>>>(n, w, bps, ss.k1[cur], ss.idx[cur],
+                                                              ss.k1[cur ^ 1], ss.idx[cur ^ 1]);
     cur ^= 1;
+    ++launches;
   }
   ss.cur = cur;
-  return 2 + (cur != 0 ? 1 : 0);
+  return launches;
 }
 
 void launch_sweep_prepare(int n, int nruns, const SweepSort& ss, int32_t* pos, int32_t* P,
