@@ -541,6 +541,41 @@ def test_config2_full_fit_matches_unpruned_materialized_flow():
     assert full == band
 
 
+def test_config2_full_fit_matches_reference_golden():
+    """BASELINE config 2 (n = 16,384, 49 % outliers) against the reference's
+    own run: lmsline.solve_lms(pts, backend="par", workers=8) took 70 min on
+    8 cores (tests/golden/make_golden_config2.py).  Record, fit and contact
+    set bit-equal, through seq, par (4 shards on this GPU) and the raw
+    record API."""
+    import hashlib
+    import json
+
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "config2_golden.json")))
+    n = gold["n"]
+    pts = workloads.contaminated_line_points(n, 0)
+    assert hashlib.sha256(pts.tobytes()).hexdigest() == gold["points_sha256"]
+    r = gold["record"]
+    want_rec = lms.CandidateRecord(height=float.fromhex(r["height"]), i=r["i"], j=r["j"],
+                                   u=float.fromhex(r["u"]), v_low=float.fromhex(r["v_low"]),
+                                   v_high=float.fromhex(r["v_high"]))
+    f = gold["fit"]
+    want_fit = {"slope": float.fromhex(f["slope"]), "intercept": float.fromhex(f["intercept"]),
+                "lms_value": float.fromhex(f["lms_value"]), "slab_height": float.fromhex(f["slab_height"]),
+                "coverage": f["coverage"], "contact_indices": tuple(f["contact_indices"])}
+    rec = lms.get_backend("seq").minimum_bracelet(pts[:, 0].copy(), pts[:, 1].copy(), gold["q"])
+    assert rec == want_rec
+    assert fit_matches(lms.solve_lms(pts), want_fit)
+    old = os.environ.get("LMSB_PAR_SHARDS")
+    os.environ["LMSB_PAR_SHARDS"] = "4"
+    try:
+        assert fit_matches(lms.solve_lms(pts, backend="par", workers=4), want_fit)
+    finally:
+        if old is None:
+            os.environ.pop("LMSB_PAR_SHARDS", None)
+        else:
+            os.environ["LMSB_PAR_SHARDS"] = old
+
+
 def test_config3_full_fit_matches_unpruned_materialized_flow():
     """BASELINE config 3 at full size (n = 65,536): the pruned large-n band
     search returns exactly the record of the unpruned K1/K2 flow over all
