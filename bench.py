@@ -3,19 +3,22 @@
 
 One step = one complete exact LMS fit of n = 16,384 points (49% gross
 outliers, q = n//2 + 1, fp64) over all n(n-1)/2 arrangement vertices: slope
-bands and their lower bounds, band-seeded bound, one collect pass over every
-vertex, window counts of the collected vertices, exact re-evaluation of the
-survivors, argmin.  With
-N > 1 processes (torchrun) the vertex-rank space of the SAME fit is split
-into N contiguous partitions and the per-rank records are combined with one
-NCCL all_gather each step (strong scaling).
+bands and their lower bounds, band-seeded bound, the sweep collect of the
+admitted bands' vertices, window counts of the collected vertices, exact
+re-evaluation of the survivors, argmin.  With N > 1
+processes (torchrun) the vertices of the SAME fit are shared out by slope
+band (each rank bounds, seeds and searches its own bands) with two NCCL
+all-gathers of 56-byte records per fit inside the library (strong scaling).
 
 Prints one JSON line on rank 0.  ``value`` is vertex-line evaluations per
 second in the reference's counting (n * n(n-1)/2 per fit / device time);
 ``time_to_fit_s`` is the per-fit device time.  ``--impl reference`` times
-the CPU restatement of the reference's algorithm (oracle/, C++ port with
-std::nth_element in place of np.sort, all host threads) on a bounded sample
-of the same workload and extrapolates to the same metric.
+the reference's own algorithm on the host cores: its _scan_rank_range /
+_evaluate_pairs restated operation for operation in numpy
+(oracle/numpy_scan.py, 0.98x the reference package's own time on the same
+slices, profiles/r02_cpu_port_calibration.json) under ParallelBackend's
+thread fan-out, on a bounded sample of the same workload extrapolated to
+the full fit.
 """
 
 from __future__ import annotations
@@ -64,9 +67,10 @@ def config(n: int, world: int) -> dict:
         "n": n,
         "pairs": n * (n - 1) // 2,
         "q": n // 2 + 1,
-        "partitioning": (f"contiguous vertex-rank partitions x{world}; sharded band search: each rank "
-                         "bounds 1/N of the slope bands, NCCL all_gather of the band table, then of "
-                         "the per-rank records") if world > 1 else "one GPU, whole pair space",
+        "partitioning": (f"sharded band search over {world} ranks: each rank bounds, seeds and "
+                         "searches its own interleaved slope bands over the whole pair space; "
+                         "NCCL all-gather of the 56-byte seed records, then of the records "
+                         "(lms_ctx_solve_distributed)") if world > 1 else "one GPU, whole pair space",
         "l2": "flushed between timed steps (256 MiB write); the 256 KiB line set is re-read from "
               "L2 within a fit by design",
     }
@@ -128,33 +132,62 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------------- cpu baseline
+def host_cores() -> dict:
+    import psutil
+
+    threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    return {"threads": threads, "logical": psutil.cpu_count(logical=True),
+            "physical": psutil.cpu_count(logical=False)}
+
+
+def rank_slices(total: int, count: int, per: int):
+    """`count` evenly spaced rank slices of `per` vertices each."""
+    return [((s * total) // count, min(total, (s * total) // count + per)) for s in range(count)]
+
+
+def cpu_scan_rate(a, b, q, n, vertices: int, threads: int) -> tuple[float, str]:
+    """evals/s of the reference's scan (numpy restatement, ParallelBackend's
+    thread fan-out over 2 x threads evenly spaced rank slices of the fit)."""
+    from oracle import numpy_scan
+
+    total = n * (n - 1) // 2
+    count = 2 * threads
+    per = max(1, vertices // count)
+    sl = rank_slices(total, count, per)
+    t0 = time.perf_counter()
+    numpy_scan.par_scan(a, b, q, sl, threads)
+    dt = time.perf_counter() - t0
+    verts = sum(r1 - r0 for r0, r1 in sl)
+    return n * verts / dt, f"{verts} vertices ({count} evenly spaced rank slices) x {n} lines in {dt:.2f}s"
+
+
 def cpu_baseline(a, b, q, n, per_thread: int) -> dict:
-    """Oracle (C++ restatement of the reference's scan) on 16 evenly spaced
-    rank slices of the same fit, all host threads."""
+    """The reference's algorithm on the host cores (numpy restatement of
+    _scan_rank_range/_evaluate_pairs under ParallelBackend's thread pool,
+    oracle/numpy_scan.py), plus the C++ restatement for comparison."""
     import oracle
 
-    oracle.build()
-    threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    cores = host_cores()
+    threads = cores["threads"]
+    rate, sample = cpu_scan_rate(a, b, q, n, per_thread * threads, threads)
     total = n * (n - 1) // 2
-    slices = 16
-    per_slice = max(1, (per_thread * threads) // slices)
+    oracle.build()
+    sl = rank_slices(total, 16, max(1, per_thread * threads // 16))
     t0 = time.perf_counter()
-    verts = 0
-    for s in range(slices):
-        r0 = (s * total) // slices
-        r1 = min(total, r0 + per_slice)
+    for r0, r1 in sl:
         oracle.min_bracelet(a, b, q, r0, r1, threads=threads)
-        verts += r1 - r0
-    dt = time.perf_counter() - t0
-    rate = n * verts / dt
+    cpp_rate = n * sum(r1 - r0 for r0, r1 in sl) / (time.perf_counter() - t0)
     return {
         "value": rate,
         "unit": UNIT,
         "cores": threads,
+        "cores_logical": cores["logical"],
+        "cores_physical": cores["physical"],
         "kind": "port",
-        "sample": f"{verts} vertices ({slices} evenly spaced rank slices of the n={n} fit) x {n} lines "
-                  f"in {dt:.2f}s; full fit extrapolates to {n * total / rate:.0f}s",
+        "sample": f"{sample}; numpy restatement of the reference's scan (oracle/numpy_scan.py), "
+                  f"full fit extrapolates to {n * total / rate:.0f}s",
         "time_to_fit_s_extrapolated": n * total / rate,
+        "cpp_oracle_evals_per_s": cpp_rate,
     }
 
 
@@ -164,14 +197,20 @@ def run_reference(args):
         return 0
     pts, q = workload(args.n, args.seed)
     a, b = pts[:, 0].copy(), pts[:, 1].copy()
+    cores = host_cores()
+    threads = cores["threads"]
+    per_step = max(2 * threads, args.cpu_vertices_per_thread * threads // 3)
     for _ in range(max(0, min(args.warmup, 1))):
-        cpu_baseline(a, b, q, args.n, max(50, args.cpu_vertices_per_thread // 10))
+        cpu_scan_rate(a, b, q, args.n, max(2 * threads, per_step // 4), threads)
     vals = []
-    last = None
+    sample = ""
     for _ in range(args.steps):
-        last = cpu_baseline(a, b, q, args.n, max(50, args.cpu_vertices_per_thread // 3))
-        vals.append(last["value"])
+        rate, sample = cpu_scan_rate(a, b, q, args.n, per_step, threads)
+        vals.append(rate)
     value = float(statistics.median(vals))
+    last = {"value": value, "unit": UNIT, "cores": threads, "cores_logical": cores["logical"],
+            "cores_physical": cores["physical"], "kind": "port",
+            "sample": f"per step {sample}; numpy restatement of the reference's scan"}
     n = args.n
     total = n * (n - 1) // 2
     line = {
@@ -192,23 +231,45 @@ def run_reference(args):
         "config": config(n, 1),
         "cpu_baseline": {**last, "value": value},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "note": "CPU restatement of the reference's exact scan (oracle/lms_oracle.cpp), each step a "
-                "bounded rank sample of the fit extrapolated to the full fit; the reference package "
-                "itself is pure Python+numpy with no GPU path",
+        "note": "the reference's own scan (_scan_rank_range/_evaluate_pairs, backend.py:125-207) "
+                "restated operation for operation in numpy (oracle/numpy_scan.py; 0.98x the "
+                "reference package's time on the same slices, profiles/r02_cpu_port_calibration.json) "
+                "under ParallelBackend's thread fan-out on all host threads; each step a bounded rank "
+                "sample of the fit extrapolated to the full fit; the reference package itself cannot "
+                "be imported on the GPU box",
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-# --------------------------------------------------------------------------- configs 1, 4, 5
-def other_configs(device: int, reps: int = 3) -> dict:
+# --------------------------------------------------------------------------- configs 1, 3, 4, 5
+def hbm_peak() -> tuple[float, str]:
+    """Measured HBM copy bandwidth (GB/s) from MEASURED_PEAKS.json, else the
+    profiling guide's fallback."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            mp = json.load(fh)
+        for k in ("hbm_gbs", "hbm_copy_gbps_burst", "hbm_copy_gbps", "hbm_gbps"):
+            if k in mp:
+                return float(mp[k]), f"MEASURED_PEAKS.json {k}"
+        for k, v in mp.items():
+            if "hbm" in k.lower() and isinstance(v, (int, float)):
+                return float(v), f"MEASURED_PEAKS.json {k}"
+    except Exception:
+        pass
+    return 6553.0, "fallback 6553 GB/s (B200_PROFILING.md)"
+
+
+def other_configs(device: int, reps: int = 3, cpu: bool = True) -> dict:
     """Device / end-to-end times of BASELINE.json configs 1, 3, 4 and 5 (median
-    of `reps` after one warm-up), reported beside the headline config 2."""
+    of `reps` after one warm-up), reported beside the headline config 2, each
+    with the reference's algorithm timed on the host cores beside it."""
     import paper_1510_01041_b200 as lms
     from paper_1510_01041_b200 import _native, workloads
 
     res = {}
     ctx = _native.Context(device)
+    threads = host_cores()["threads"]
 
     def timed(fn):
         fn()
@@ -224,16 +285,40 @@ def other_configs(device: int, reps: int = 3) -> dict:
     pts = workloads.config1_points(0)
     ctx.upload(pts[:, 0], pts[:, 1])
     ms = timed(lambda: ctx.solve(501, 0, 1000 * 999 // 2))
-    res["config1"] = {"workload": "n=1000, 45% outliers, q=501", "ms_per_fit": ms,
-                      "evals_per_s": 1000 * 499500 / (ms / 1e3)}
-    # config 3: n = 65,536 on this one GPU (the multi-GPU case shards this rank space)
+    c1 = {"workload": "n=1000, 45% outliers, q=501", "ms_per_fit": ms,
+          "evals_per_s": 1000 * 499500 / (ms / 1e3)}
+    walls = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        lms.solve_lms(pts, 501)
+        walls.append(time.perf_counter() - t0)
+    c1["e2e_ms"] = 1e3 * statistics.median(walls)
+    if cpu:
+        from oracle import numpy_scan
+
+        total1 = 1000 * 999 // 2
+        t0 = time.perf_counter()
+        numpy_scan.par_scan(pts[:, 0].copy(), pts[:, 1].copy(), 501,
+                            [((k * total1) // threads, ((k + 1) * total1) // threads) for k in range(threads)],
+                            threads)
+        dt = time.perf_counter() - t0
+        c1["cpu_baseline"] = {"value": 1000 * total1 / dt, "unit": UNIT, "cores": threads, "kind": "port",
+                              "seconds_per_fit": dt, "sample": "the whole fit (no extrapolation)"}
+    res["config1"] = c1
+    # config 3: n = 65,536 on this one GPU (the multi-GPU case shards this fit)
     n3 = 65536
     pts3 = workloads.contaminated_line_points(n3, 0)
     ctx.upload(pts3[:, 0], pts3[:, 1])
     P3 = n3 * (n3 - 1) // 2
     ms = timed(lambda: ctx.solve(n3 // 2 + 1, 0, P3))
-    res["config3"] = {"workload": "n=65536, 49% outliers, q=32769, one GPU (all 2,147,450,880 pairs)",
-                      "ms_per_fit": ms, "evals_per_s": n3 * P3 / (ms / 1e3)}
+    c3 = {"workload": "n=65536, 49% outliers, q=32769, one GPU (all 2,147,450,880 pairs)",
+          "ms_per_fit": ms, "evals_per_s": n3 * P3 / (ms / 1e3)}
+    if cpu:
+        rate, sample = cpu_scan_rate(pts3[:, 0].copy(), pts3[:, 1].copy(), n3 // 2 + 1, n3, 128 * threads,
+                                     threads)
+        c3["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+                              "sample": sample, "time_to_fit_s_extrapolated": n3 * P3 / rate}
+    res["config3"] = c3
     # config 4: 8,192 fits of bench_points(512) (experiments.py:247-254)
     F, m = 8192, 512
     sets = [workloads.bench_points(m, seed=f) for f in range(F)]
@@ -249,35 +334,78 @@ def other_configs(device: int, reps: int = 3) -> dict:
         t0 = time.perf_counter()
         lms.solve_lms_batch(sets)  # host arrays in, LmsFit objects (with contact sets) out
         walls4.append(time.perf_counter() - t0)
-    res["config4"] = {"workload": "8192 fits x n=512 (bench_points), q=257", "ms_per_batch": ms,
-                      "evals_per_s": F * m * (m * (m - 1) // 2) / (ms / 1e3),
-                      "e2e_ms": 1e3 * statistics.median(walls4),
-                      "e2e_path": "solve_lms_batch(list of (512, 2) arrays) -> list[LmsFit]"}
-    # config 5: detect_lines end to end (host image in, LineDetections out)
-    img = workloads.line_image(4096, 4096, 64, 0.30, seed=0)
+    evals4 = F * m * (m * (m - 1) // 2)
+    c4 = {"workload": "8192 fits x n=512 (bench_points), q=257", "ms_per_batch": ms,
+          "evals_per_s": evals4 / (ms / 1e3), "e2e_ms": 1e3 * statistics.median(walls4),
+          "e2e_path": "solve_lms_batch(list of (512, 2) arrays) -> list[LmsFit]",
+          "h2d_bytes": int(X.nbytes + Y.nbytes)}
+    if cpu:
+        from concurrent.futures import ThreadPoolExecutor
+
+        from oracle import numpy_scan
+
+        K = 16
+        P4 = m * (m - 1) // 2
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(max_workers=threads) as pool:
+            list(pool.map(lambda f: numpy_scan.scan_rank_range(sets[f][:, 0].copy(), sets[f][:, 1].copy(),
+                                                               m // 2 + 1, 0, P4), range(K)))
+        dt = time.perf_counter() - t0
+        c4["cpu_baseline"] = {"value": evals4 / (dt * F / K), "unit": UNIT, "cores": threads, "kind": "port",
+                              "sample": f"{K} of the {F} fits in {dt:.2f}s (one per thread), scaled x{F // K}",
+                              "seconds_per_batch_extrapolated": dt * F / K}
+    res["config4"] = c4
+    # config 5: detect_lines end to end on the BASELINE image (gen_synthetic recipe)
+    img = workloads.config5_image(0)
     params = lms.HoughParams.for_image(4096, 4096, 20.0, 20.0)
     lms.detect_lines(img, params, "lms", 64)
-    walls = []
+    walls, vote_ms, sup_ms = [], [], []
     for _ in range(reps):
         t0 = time.perf_counter()
         dets = lms.detect_lines(img, params, "lms", 64)
         walls.append(time.perf_counter() - t0)
-    res["config5"] = {"workload": "detect_lines, 4096^2 image, 64 lines, 30% salt, 64 peaks, cap 256",
-                      "e2e_ms": 1e3 * statistics.median(walls), "peaks": len(dets),
-                      "lit_points": int((img >= 128).sum())}
+        st = _native.device_stats(device)
+        vote_ms.append(st["ms_hough_vote"])
+        sup_ms.append(st["ms_hough_support"])
+    n_lit = int((img >= 128).sum())
+    sup_total = sum(len(d.support) for d in dets)
+    alg_bytes = img.size + 8 * n_lit + 16 * sup_total  # image + point list + supports
+    t_hough = (statistics.median(vote_ms) + statistics.median(sup_ms)) / 1e3
+    peak, peak_src = hbm_peak()
+    c5 = {"workload": "detect_lines, 4096^2 image of 64 gen_synthetic lines + 30% salt "
+                      "(workloads.config5_image), 64 peaks, cap 256",
+          "e2e_ms": 1e3 * statistics.median(walls), "peaks": len(dets), "lit_points": n_lit,
+          "support_points": sup_total,
+          "h2d_bytes": int(img.nbytes), "d2h_bytes": 4 * sup_total,
+          "roofline": {"bound": "hbm", "kernels": "img_vote_kernel + support count/scan/write",
+                       "achieved": alg_bytes / t_hough / 1e9, "peak": peak, "unit": "GB/s",
+                       "frac": alg_bytes / t_hough / 1e9 / peak,
+                       "algorithmic_bytes": alg_bytes,
+                       "ms_vote": statistics.median(vote_ms), "ms_support": statistics.median(sup_ms),
+                       "peak_source": peak_src,
+                       "note": "W*H + 8*n_lit + 16*sum|support| (SURVEY 8d) over the live CUDA-event "
+                               "time of the vote and support kernels; the image-direct kernels read "
+                               "the 16.8 MB image three times and write the 4-byte support ids"}}
+    res["config5"] = c5
     ctx.close()
     return res
 
 
 # --------------------------------------------------------------------------- ours
-def load_profile(name: str) -> dict:
+def load_profile(name: str, kernel_re: str | None = None) -> dict:
     """ncu summary (scripts/ncu_summary.py) of one kernel on this workload."""
+    import re
+
     path = os.path.join(ROOT, "profiles", name)
     try:
         with open(path) as fh:
-            return json.load(fh)["launches"][0]
+            launches = json.load(fh)["launches"]
     except Exception:
         return {}
+    for la in launches:
+        if kernel_re is None or re.search(kernel_re, la.get("kernel", "")):
+            return la
+    return {}
 
 
 def run_ours(args):
@@ -317,7 +445,7 @@ def run_ours(args):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
 
     def step():
-        if world > 1:  # sharded band search: band-table all_gather, record all_gather
+        if world > 1:  # sharded band search: seed-record and record all-gathers (in the library)
             return distributed.solve_sharded(ctx, q, device=coll_dev)
         return record_from_native(ctx.solve(q, r0, r1))
 
@@ -329,7 +457,8 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize()
     dev_ms = 0.0
-    phase = {"ms_bound": 0.0, "ms_partition": 0.0, "ms_collect": 0.0, "ms_band_filter": 0.0}
+    phase = {"ms_bound": 0.0, "ms_partition": 0.0, "ms_collect": 0.0, "ms_band_filter": 0.0,
+             "ms_filter_kernel": 0.0, "ms_sweep_enum": 0.0}
     launches = 0
     survivors = 0
     band_stats = {}
@@ -388,44 +517,50 @@ def run_ours(args):
         e2e_s = float(tt.item())
     e2e_value = max(1, args.steps) * n * total / e2e_s
 
-    # ---- roofline of the dominant kernel: the collect pass, one test per
-    # arrangement vertex; instruction-issue bound (no tensor-core or HBM
-    # bound applies: its DRAM traffic is the collected list only, the lines
-    # stay in L1/L2).  achieved = warp instructions per launch (ncu, same
-    # workload, committed under profiles/) / live event time of the kernel.
-    prof = load_profile("r01_collect_ncu.json")
-    coll_ms = phase["ms_collect"] / args.steps
+    # ---- roofline of the dominant kernel: the band filter (per slope-ordered
+    # chunk of collected vertices: the chunk's keys sorted in shared memory,
+    # then binary-searched window counts) -- instruction-issue bound (no
+    # tensor-core or HBM bound applies: its DRAM traffic is the member list,
+    # the lines and keys stay on chip).  achieved = warp instructions per
+    # launch (ncu, same workload, profiles/r02_band_kernels_ncu.json) / the
+    # live CUDA-event time of the launch in this run.
     sm_mhz = clocks.get("sm_mhz") or 1965.0
     sms = torch.cuda.get_device_properties(local).multi_processor_count
     peak = sms * 4 * sm_mhz * 1e6  # warp instructions / s: 4 schedulers per SM
-    inst = prof.get("smsp__inst_executed.sum")
-    pairs = r1 - r0
-    if inst:  # the profile is of the whole-fit launch: scale to this rank's partition
-        inst *= pairs / total
-    achieved = inst / (coll_ms / 1e3) if inst and coll_ms > 0 else None
-    traffic = None
-    if prof.get("dram__bytes_read.sum") is not None:
-        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-        traffic = (prof["dram__bytes_read.sum"] * scale.get(prof.get("dram__bytes_read.sum.unit"), 1)
-                   + prof["dram__bytes_write.sum"] * scale.get(prof.get("dram__bytes_write.sum.unit"), 1))
-    roofline = {
-        "bound": "issue",
-        "kernel": "band_collect_kernel (fp32 slope-run pre-test of every vertex, exact band of the "
-                  "candidates)",
-        "achieved": achieved,
-        "peak": peak,
-        "unit": "warp-instructions/s",
-        "frac": achieved / peak if achieved else None,
-        "traffic": traffic,
-        "algorithmic": f"{pairs} vertex tests per launch ({pairs / (coll_ms / 1e3):.3e} vertices/s); "
-                       "achieved = ncu smsp__inst_executed.sum of the launch (profiles/"
-                       "r01_collect_ncu.json) / live CUDA-event time of the launch",
-        "peak_source": f"{sms} SMs x 4 warp schedulers x 1 instruction/clk at the median SM clock "
-                       "sampled during the timed region",
-        "collect_share_of_step": coll_ms / ms_per_step if ms_per_step else None,
-        "phase_ms_per_step": {k: v / args.steps for k, v in phase.items()},
-        "reference_evals_per_step": n * total,
-    }
+
+    def issue_roofline(kernel_re: str, live_ms: float, label: str, work: str):
+        prof = load_profile("r02_band_kernels_ncu.json", kernel_re)
+        inst = prof.get("smsp__inst_executed.sum")
+        if inst and world > 1:
+            inst = None  # the profile is of the one-GPU fit
+        achieved = inst / (live_ms / 1e3) if inst and live_ms > 0 else None
+        traffic = None
+        if prof.get("dram__bytes_read.sum") is not None:
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+            traffic = (prof["dram__bytes_read.sum"] * scale.get(prof.get("dram__bytes_read.sum.unit"), 1)
+                       + prof["dram__bytes_write.sum"] * scale.get(prof.get("dram__bytes_write.sum.unit"), 1))
+        return {"bound": "issue", "kernel": label, "achieved": achieved, "peak": peak,
+                "unit": "warp-instructions/s", "frac": achieved / peak if achieved else None,
+                "traffic": traffic, "live_ms_per_launch": live_ms,
+                "share_of_step": live_ms / ms_per_step if ms_per_step else None, "algorithmic": work}
+
+    filt_ms = phase["ms_filter_kernel"] / args.steps
+    enum_ms = phase["ms_sweep_enum"] / args.steps
+    roofline = issue_roofline(
+        "band_filter", filt_ms,
+        "band_filter_kernel (slope-ordered chunks of the collected vertices: shared-memory key sort, "
+        "padded window counts by binary search)",
+        f"{band_stats.get('filtered_vertices', 0)} collected vertices per launch; achieved = ncu "
+        "smsp__inst_executed.sum of the launch (profiles/r02_band_kernels_ncu.json) / live CUDA-event "
+        "time of the launch")
+    roofline["peak_source"] = (f"{sms} SMs x 4 warp schedulers x 1 instruction/clk at the median SM "
+                               "clock sampled during the timed region")
+    roofline["phase_ms_per_step"] = {k: v / args.steps for k, v in phase.items()}
+    roofline["reference_evals_per_step"] = n * total
+    roofline["others"] = [issue_roofline(
+        "sweep_enum", enum_ms, "sweep_enum_kernel + sweep_parallel_kernel (the admitted runs' vertices "
+        "enumerated as line-order inversions, classified with the reference's slope)",
+        f"{band_stats.get('filtered_vertices', 0)} members emitted per launch")]
 
     out = None
     if rank == 0:

@@ -48,6 +48,7 @@ extern "C" {
 #define LMS_ERR_CUDA -2     /* CUDA runtime failure */
 #define LMS_ERR_NODEVICE -3 /* no CUDA device / device index out of range */
 #define LMS_ERR_NOMEM -4    /* device allocation failed */
+#define LMS_NOT_FITTED 1    /* lms_detect_supports_u8: a thinned support cannot be fitted (no fits run) */
 
 /* CandidateRecord (backend.py:37-54) plus a found flag: found == 0 is the
  * reference's None ("no window fits"). 56 bytes. */
@@ -89,7 +90,15 @@ typedef struct lms_stats {
   int64_t direct_groups;    /* sub-band regions of the direct grouping (0: radix-sort path) */
   int64_t bands_refined;    /* bands whose coarse bound admitted H and got the exact bound */
   int64_t sweep_runs;       /* slope runs of the sweep collect (0: the pre-test pass ran) */
+  float ms_filter_kernel;   /* the band filter kernel alone (band_filter / band_filter_big) */
+  float ms_sweep_enum;      /* the sweep collect's enumeration kernels (enum + near-parallel) */
+  float ms_hough_vote;      /* device detect: the vote kernel (lms_detect_peaks_u8) */
+  float ms_hough_support;   /* device detect: support count + scan + write kernels */
 } lms_stats;
+
+/* Counters of the last call on `device`'s shared context (the one the
+ * lms_* entry points without a context use). */
+int lms_device_stats(int device, lms_stats* out);
 
 /* Library identity and device discovery. */
 int lms_version(void);
@@ -286,6 +295,38 @@ int lms_ctx_solve_distributed(lms_ctx* c, int64_t q, lms_candidate* out);
  * pair-rank partition. */
 int lms_ctx_shard_search_owned(lms_ctx* c, int64_t q, int32_t nshards, int32_t shard,
                                const lms_candidate* seed, lms_candidate* out);
+
+/* ---- detect_lines on the device, straight from the image (detect.py:156-214).
+ * Phase 1: the uint8 image thresholded (>= threshold, hough.py:93-103) and
+ * voted at the theta bin centres (cos_t/sin_t: np.cos/np.sin of the centres,
+ * hough.py:112-129), then find_peaks (hough.py:132-168): 8-neighbour maxima
+ * >= min_votes ordered by (-votes, rho_bin, theta_bin), at most max_peaks
+ * (<= 64).  peaks[3k .. 3k+2] = (rho_bin, theta_bin, votes), *npeaks of
+ * them; acc (n_rho * n_theta int64) optional.  n_rho * n_theta <= 16384,
+ * n_theta <= 512, fewer than 2^31 pixels. */
+int lms_detect_peaks_u8(const uint8_t* img, int64_t height, int64_t width, int threshold,
+                        const double* cos_t, const double* sin_t, int64_t n_theta, double rho_max,
+                        double delta_rho, int64_t n_rho, int64_t max_peaks, int64_t min_votes,
+                        int device, int64_t* acc, int64_t* npoints, int64_t* peaks,
+                        int64_t* npeaks);
+/* Phase 2 on the peaks of the last phase 1 on this device (hold one lock
+ * across both): every peak's support in scan order (supporting_points,
+ * hough.py:171-184; cos_s/sin_s: math.cos/math.sin of every theta bin
+ * centre) as int32 pixel ids in support_ids[support_offsets[k] ..
+ * support_offsets[k+1]) (capacity entries; NULL: not downloaded); each
+ * support thinned to support_cap (0: whole) by the stride (k m) // cap
+ * (detect.py:118-131) in the axis-swapped frame of swap_t[theta_bin]
+ * (detect.py:91-95), design_offsets (npeaks + 1) and the thinned
+ * abscissa range abscissa_range[2k], [2k+1]; with fit != 0 the exact LMS
+ * refit of every design with coverage q[k] (refine_lms, detect.py:134-153)
+ * into records[k] and contact_flags (one per design point, the solve_lms
+ * contact set, solver.py:122-140).  Returns LMS_NOT_FITTED (no fits run)
+ * when a design has < 3 points, a single abscissa, or q[k] outside [2, n]. */
+int lms_detect_supports_u8(const double* cos_s, const double* sin_s, const uint8_t* swap_t,
+                           int64_t support_cap, const int64_t* q, int fit, int device,
+                           int64_t* support_offsets, int32_t* support_ids, int64_t capacity,
+                           int64_t* design_offsets, double* abscissa_range, lms_candidate* records,
+                           uint8_t* contact_flags);
 
 #ifdef __cplusplus
 }

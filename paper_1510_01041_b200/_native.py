@@ -82,6 +82,10 @@ class Stats(ctypes.Structure):
         ("direct_groups", ctypes.c_int64),
         ("bands_refined", ctypes.c_int64),
         ("sweep_runs", ctypes.c_int64),
+        ("ms_filter_kernel", ctypes.c_float),
+        ("ms_sweep_enum", ctypes.c_float),
+        ("ms_hough_vote", ctypes.c_float),
+        ("ms_hough_support", ctypes.c_float),
     ]
 
     def as_dict(self) -> dict:
@@ -194,6 +198,15 @@ SIGNATURES = {
     "lms_ctx_solve_distributed": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, _C]),
     "lms_ctx_shard_search_owned": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
                                                   ctypes.c_int32, _C, _C]),
+    "lms_detect_peaks_u8": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
+                                           _D, _D, ctypes.c_int64, ctypes.c_double, ctypes.c_double,
+                                           ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
+                                           _I, _I, _I, _I]),
+    "lms_detect_supports_u8": (ctypes.c_int, [_D, _D, ctypes.POINTER(ctypes.c_uint8), ctypes.c_int64, _I,
+                                              ctypes.c_int, ctypes.c_int, _I,
+                                              ctypes.POINTER(ctypes.c_int32), ctypes.c_int64, _I, _D, _C,
+                                              ctypes.POINTER(ctypes.c_uint8)]),
+    "lms_device_stats": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(Stats)]),
     "lms_probe_fp64_rate": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_double)]),
     "lms_probe_fp32_rate": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_double)]),
 }
@@ -270,6 +283,13 @@ def min_bracelet(a, b, q: int, rank_begin: int, rank_end: int, device: int = 0) 
     return out
 
 
+def device_stats(device: int = 0) -> dict:
+    """lms_device_stats: counters of the last call on the device's shared context."""
+    s = Stats()
+    check(_lib_ready().lms_device_stats(int(device), ctypes.byref(s)))
+    return s.as_dict()
+
+
 def min_bracelet_multi(a, b, q: int, devices) -> Candidate:
     """lms_min_bracelet_multi: one fit sharded over len(devices) shards, shard r
     on GPU devices[r] (NCCL between distinct GPUs, host exchange otherwise)."""
@@ -338,6 +358,16 @@ def batched_fit(x, y, offsets, q, device: int = 0):
     check(lib.lms_batched_fit_f64(_dp(x), _dp(y), _ip(offsets), _ip(q), nfits, int(device), out,
                                   flags.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8))))
     return out, flags[: int(offsets[-1])]
+
+
+CANDIDATE_DTYPE = np.dtype([("height", "<f8"), ("u", "<f8"), ("v_low", "<f8"), ("v_high", "<f8"),
+                            ("i", "<i8"), ("j", "<i8"), ("found", "<i4"), ("reserved", "<i4")])
+
+
+def candidates_array(out, count: int) -> np.ndarray:
+    """A ctypes lms_candidate array as a numpy structured array (copied)."""
+    assert ctypes.sizeof(Candidate) == CANDIDATE_DTYPE.itemsize
+    return np.frombuffer(out, dtype=CANDIDATE_DTYPE, count=count).copy()
 
 
 def batched(x, y, offsets, q, device: int = 0) -> list:
@@ -412,6 +442,63 @@ def _hough_support_locked(cos_p, sin_p, rbin_p, rho_max: float, delta_rho: float
                                      int(offsets[-1]), device, narrow)
     check(rc)
     return offsets, out[: offsets[-1]]
+
+
+LMS_NOT_FITTED = 1
+DETECT_MAX_BINS = 16384
+DETECT_MAX_PEAKS = 64
+
+
+def detect_peaks(img, threshold: int, cos_t, sin_t, rho_max: float, delta_rho: float, n_rho: int,
+                 max_peaks: int, min_votes: int, device: int = 0, want_acc: bool = False):
+    """lms_detect_peaks_u8 -> (npoints, peaks int64[P, 3] (rho_bin, theta_bin, votes), acc or None).
+    Hold hough_lock(device) from here through detect_supports."""
+    lib = _lib_ready()
+    img = np.ascontiguousarray(img, dtype=np.uint8)
+    h, w = img.shape
+    cos_t, sin_t = _f64(cos_t), _f64(sin_t)
+    n_theta = cos_t.size
+    acc = np.zeros((n_rho, n_theta), dtype=np.int64) if want_acc else None
+    npts, npk = ctypes.c_int64(0), ctypes.c_int64(0)
+    peaks = np.zeros((DETECT_MAX_PEAKS, 3), dtype=np.int64)
+    check(lib.lms_detect_peaks_u8(img.ctypes.data_as(ctypes.c_void_p), h, w, int(threshold), _dp(cos_t),
+                                  _dp(sin_t), n_theta, float(rho_max), float(delta_rho), int(n_rho),
+                                  int(max_peaks), int(min_votes), int(device),
+                                  _ip(acc) if acc is not None else None, ctypes.byref(npts), _ip(peaks),
+                                  ctypes.byref(npk)))
+    return npts.value, peaks[: npk.value].copy(), acc
+
+
+def detect_supports(cos_s, sin_s, swap_t, support_cap: int, q, fit: bool, npeaks: int, votes,
+                    device: int = 0):
+    """lms_detect_supports_u8 on the last detect_peaks -> dict with the support
+    offsets and int32 pixel ids, the design offsets and abscissa ranges, and
+    (fit and fitted) the records (structured array) and contact flags."""
+    lib = _lib_ready()
+    cos_s, sin_s = _f64(cos_s), _f64(sin_s)
+    swap = np.ascontiguousarray(swap_t, dtype=np.uint8)
+    votes = np.asarray(votes, dtype=np.int64)
+    total = int(votes.sum())
+    cap = int(support_cap or 0)
+    keep = np.minimum(votes, cap) if cap > 0 else votes
+    soffs = np.zeros(npeaks + 1, dtype=np.int64)
+    doffs = np.zeros(npeaks + 1, dtype=np.int64)
+    ids = np.empty(max(total, 1), dtype=np.int32)
+    lim = np.zeros(2 * max(npeaks, 1), dtype=np.float64)
+    recs = (Candidate * max(npeaks, 1))()
+    flags = np.zeros(max(int(keep.sum()), 1), dtype=np.uint8)
+    qv = np.ascontiguousarray(q if q is not None else np.zeros(npeaks), dtype=np.int64)
+    rc = lib.lms_detect_supports_u8(_dp(cos_s), _dp(sin_s), swap.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)),
+                                    cap, _ip(qv), 1 if fit else 0, int(device), _ip(soffs),
+                                    ids.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), total, _ip(doffs),
+                                    _dp(lim), recs, flags.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)))
+    if rc != LMS_NOT_FITTED:
+        check(rc)
+    fitted = bool(fit) and rc == 0
+    return {"support_offsets": soffs, "ids": ids[:total], "design_offsets": doffs,
+            "abscissa_range": lim[: 2 * npeaks].reshape(npeaks, 2), "fitted": fitted,
+            "records": candidates_array(recs, npeaks) if fitted else None,
+            "contact_flags": flags[: int(doffs[-1])] if fitted else None}
 
 
 def hough_vote_image(img, threshold: int, cos_t, sin_t, rho_max: float, delta_rho: float,

@@ -32,6 +32,7 @@
 #include "lms_band.cuh"
 #include "lms_band_small.cuh"
 #include "lms_common.cuh"
+#include "lms_detect.cuh"
 #include "lms_hough.cuh"
 #include "lms_kernels.cuh"
 #include "lms_nccl.cuh"
@@ -225,6 +226,17 @@ struct lms_ctx {
   DevBuf<double> pxs, pys;
   DevBuf<unsigned char> ext_tmp, scan_tmp;
   DevBuf<unsigned long long> acc, masks;
+  // device detect_lines (lms_detect.cu): the image of the last
+  // lms_detect_peaks_u8 call, its grid and peaks, supports and designs
+  DevBuf<int64_t> dt_peaks, dt_offs, dt_soffs, dt_doffs;
+  DevBuf<unsigned> dt_counts;
+  DevBuf<int32_t> dt_ids;
+  DevBuf<double> dt_a, dt_b, dt_lim, dt_strig;
+  DevBuf<uint8_t> dt_swap;
+  DevBuf<unsigned long long> dt_nlit;
+  int64_t dt_npix = 0, dt_width = 0, dt_npeaks = -1;
+  int dt_threshold = 0;
+  lmsb::HoughGrid dt_grid{};
   DevBuf<double> tcos, tsin;
   DevBuf<int64_t> rbin, scounts, soffsets, sout;
   DevBuf<int32_t> sout32;
@@ -459,6 +471,18 @@ void ctx_release(lms_ctx* c) {
   c->sw_rk.release();
   c->sw_ends.release();
   c->sw_dbg.release();
+  c->dt_peaks.release();
+  c->dt_offs.release();
+  c->dt_soffs.release();
+  c->dt_doffs.release();
+  c->dt_counts.release();
+  c->dt_ids.release();
+  c->dt_a.release();
+  c->dt_b.release();
+  c->dt_lim.release();
+  c->dt_strig.release();
+  c->dt_swap.release();
+  c->dt_nlit.release();
   c->xsend.release();
   c->xrecv.release();
   if (c->comm && c->comm_owned && lmsb::nccl().ok) lmsb::nccl().CommDestroy(c->comm);
@@ -686,6 +710,7 @@ int order_lines(lms_ctx* c, const std::vector<int64_t>& seg, int64_t F, const do
 // fit's magnitudes are finite and n <= kBandMaxBigN.
 int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   const int64_t span = h.r1 - h.r0;
+  bool filter_timed = false, sweep_timed = false;
   ShardSpec* sh = c->shard;
   const int64_t P0 = sh ? sh->P0 : h.r0;
   const int64_t pspan = sh ? sh->P1 - sh->P0 : span;
@@ -777,7 +802,7 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   w.end = c->bend.p;
   w.temp = c->btemp.p;
   w.temp_bytes = (size_t)c->btemp.cap;
-  while (c->ev_chunk.size() < 10) {
+  while (c->ev_chunk.size() < 14) {
     cudaEvent_t e;
     CUDA_TRY(cudaEventCreate(&e));
     c->ev_chunk.push_back(e);
@@ -1502,7 +1527,10 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
       sa.out_keys = w.ckeys;
       sa.out_vals = w.cvals;
       sa.cap = cap;
+      CUDA_TRY(cudaEventRecord(c->ev_chunk[10], c->stream));
       lmsb::launch_sweep_emit(bf, sa, c->sms, c->stream);
+      CUDA_TRY(cudaEventRecord(c->ev_chunk[11], c->stream));
+      sweep_timed = true;
       st->launches += 2;
     } else {
       CUDA_TRY(cudaEventRecord(c->ev_chunk[5], c->stream));
@@ -1595,9 +1623,15 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
                                    (size_t)c->btemp.cap, c->stream) != 0)
         return set_error(LMS_ERR_CUDA, "large-n slice sort failed");
       st->launches += 4;
+      CUDA_TRY(cudaEventRecord(c->ev_chunk[8], c->stream));
       lmsb::launch_band_filter_big(bf, ba, c->bslice_store.p, fgrid, c->stream);
+      CUDA_TRY(cudaEventRecord(c->ev_chunk[9], c->stream));
+    } else {
+      CUDA_TRY(cudaEventRecord(c->ev_chunk[8], c->stream));
+      lmsb::launch_band(bf, ba, 1, fgrid, c->stream);
+      CUDA_TRY(cudaEventRecord(c->ev_chunk[9], c->stream));
     }
-    else lmsb::launch_band(bf, ba, 1, fgrid, c->stream);
+    filter_timed = true;
     lmsb::BandCount bc{};
     bc.lines = c->blines32.p;
     bc.best = c->best.p;
@@ -1652,6 +1686,16 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   st->ms_band_filter = ms;
   CUDA_TRY(cudaEventElapsedTime(&ms, c->ev_chunk[5], c->ev_chunk[6]));
   st->ms_collect = ms;
+  st->ms_filter_kernel = 0.f;
+  if (filter_timed) {
+    CUDA_TRY(cudaEventElapsedTime(&ms, c->ev_chunk[8], c->ev_chunk[9]));
+    st->ms_filter_kernel = ms;
+  }
+  st->ms_sweep_enum = 0.f;
+  if (sweep_timed) {
+    CUDA_TRY(cudaEventElapsedTime(&ms, c->ev_chunk[10], c->ev_chunk[11]));
+    st->ms_sweep_enum = ms;
+  }
   if (getenv("LMSB_BAND_DEBUG")) {
     float t[6];
     cudaEventElapsedTime(&t[0], c->ev_chunk[0], c->ev_chunk[1]);
@@ -2998,6 +3042,218 @@ int lms_min_bracelet_multi(const double* a, const double* b, int64_t n, int64_t 
     }
   *out = result[0];
   return LMS_OK;
+}
+
+int lms_device_stats(int device, lms_stats* out) {
+  if (!out) return set_error(LMS_ERR_INVALID, "null argument");
+  lms_ctx* c = nullptr;
+  RC_TRY(shared_ctx(device, &c));
+  std::lock_guard<std::mutex> lk(c->mu);
+  *out = c->stats;
+  return LMS_OK;
+}
+
+int lms_detect_peaks_u8(const uint8_t* img, int64_t height, int64_t width, int threshold,
+                        const double* cos_t, const double* sin_t, int64_t n_theta, double rho_max,
+                        double delta_rho, int64_t n_rho, int64_t max_peaks, int64_t min_votes,
+                        int device, int64_t* acc, int64_t* npoints, int64_t* peaks,
+                        int64_t* npeaks) {
+  if (!img || !cos_t || !sin_t || !npoints || !peaks || !npeaks)
+    return set_error(LMS_ERR_INVALID, "null argument");
+  if (height < 0 || width < 0) return set_error(LMS_ERR_INVALID, "bad image");
+  if (max_peaks < 1 || max_peaks > 64) return set_error(LMS_ERR_INVALID, "max_peaks must be in [1, 64]");
+  if (n_theta * n_rho > lmsb::kDetectMaxBins || n_theta > 512)
+    return set_error(LMS_ERR_INVALID, "accumulator too large for the device peak finder");
+  const int64_t npix = height * width;
+  if (npix > INT32_MAX) return set_error(LMS_ERR_INVALID, "image too large for int32 pixel ids");
+  lms_ctx* c = nullptr;
+  RC_TRY(shared_ctx(device, &c));
+  std::lock_guard<std::mutex> lk(c->mu);
+  RC_TRY(check_hough(n_theta, rho_max, delta_rho, n_rho));
+  CUDA_TRY(cudaSetDevice(c->device));
+  const int64_t nb = n_theta * n_rho;
+  RC_TRY(c->img.need(std::max<int64_t>(npix, 4)));
+  RC_TRY(c->acc.need(nb));
+  RC_TRY(c->tcos.need(n_theta));
+  RC_TRY(c->tsin.need(n_theta));
+  RC_TRY(c->dt_peaks.need(3 * 64 + 1));
+  RC_TRY(c->dt_nlit.need(1));
+  RC_TRY(ensure_pinned(c, sizeof(int64_t) * (3 * 64 + 4) + sizeof(unsigned long long) * nb));
+  if (npix > 0) RC_TRY(upload_staged(c, c->img.p, img, (size_t)npix));
+  CUDA_TRY(cudaMemcpyAsync(c->tcos.p, cos_t, sizeof(double) * n_theta, cudaMemcpyHostToDevice,
+                           c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->tsin.p, sin_t, sizeof(double) * n_theta, cudaMemcpyHostToDevice,
+                           c->stream));
+  CUDA_TRY(cudaMemsetAsync(c->acc.p, 0, sizeof(unsigned long long) * nb, c->stream));
+  CUDA_TRY(cudaMemsetAsync(c->dt_nlit.p, 0, sizeof(unsigned long long), c->stream));
+  lmsb::DetectImage im{c->img.p, npix, std::max<int64_t>(width, 1), threshold};
+  lmsb::HoughGrid g{(int)n_rho, (int)n_theta, rho_max, delta_rho};
+  while (c->ev_chunk.size() < 14) {
+    cudaEvent_t e;
+    CUDA_TRY(cudaEventCreate(&e));
+    c->ev_chunk.push_back(e);
+  }
+  CUDA_TRY(cudaEventRecord(c->ev_chunk[12], c->stream));
+  if (npix > 0) lmsb::launch_detect_vote(im, g, c->tcos.p, c->tsin.p, c->acc.p, c->dt_nlit.p, c->sms, c->stream);
+  CUDA_TRY(cudaEventRecord(c->ev_chunk[13], c->stream));
+  int64_t* d_np = c->dt_peaks.p + 3 * 64;
+  lmsb::launch_detect_peaks(c->acc.p, g, min_votes, (int)max_peaks, c->dt_peaks.p, d_np, c->stream);
+  CUDA_TRY(cudaGetLastError());
+  int64_t* pin = reinterpret_cast<int64_t*>(c->pin);
+  CUDA_TRY(cudaMemcpyAsync(pin, c->dt_peaks.p, sizeof(int64_t) * (3 * 64 + 1), cudaMemcpyDeviceToHost,
+                           c->stream));
+  CUDA_TRY(cudaMemcpyAsync(pin + 3 * 64 + 1, c->dt_nlit.p, sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, c->stream));
+  if (acc) CUDA_TRY(cudaMemcpyAsync(acc, c->acc.p, sizeof(int64_t) * nb, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  const int64_t m = pin[3 * 64];
+  *npeaks = m;
+  *npoints = pin[3 * 64 + 1];
+  float vote_ms = 0.f;
+  CUDA_TRY(cudaEventElapsedTime(&vote_ms, c->ev_chunk[12], c->ev_chunk[13]));
+  c->stats.ms_hough_vote = vote_ms;
+  std::memcpy(peaks, pin, sizeof(int64_t) * 3 * m);
+  c->dt_npix = npix;
+  c->dt_width = std::max<int64_t>(width, 1);
+  c->dt_threshold = threshold;
+  c->dt_grid = g;
+  c->dt_npeaks = m;
+  c->hough_mode = 0;  // the point-list Hough calls need their own vote
+  return LMS_OK;
+}
+
+int lms_detect_supports_u8(const double* cos_s, const double* sin_s, const uint8_t* swap_t,
+                           int64_t support_cap, const int64_t* q, int fit, int device,
+                           int64_t* support_offsets, int32_t* support_ids, int64_t capacity,
+                           int64_t* design_offsets, double* abscissa_range, lms_candidate* records,
+                           uint8_t* contact_flags) {
+  if (!cos_s || !sin_s || !swap_t || !support_offsets || !design_offsets || !abscissa_range)
+    return set_error(LMS_ERR_INVALID, "null argument");
+  lms_ctx* c = nullptr;
+  RC_TRY(shared_ctx(device, &c));
+  std::lock_guard<std::mutex> lk(c->mu);
+  if (c->dt_npeaks < 0) return set_error(LMS_ERR_INVALID, "no peaks: call lms_detect_peaks_u8 first");
+  const int P = (int)c->dt_npeaks;
+  const int nt = c->dt_grid.n_theta;
+  CUDA_TRY(cudaSetDevice(c->device));
+  support_offsets[0] = 0;
+  design_offsets[0] = 0;
+  if (P == 0) return LMS_OK;
+  const int64_t nch = lmsb::detect_support_chunks(c->dt_npix);
+  RC_TRY(c->dt_counts.need(std::max<int64_t>((int64_t)P * nch, 1)));
+  RC_TRY(c->dt_offs.need((int64_t)P * nch + 1));
+  RC_TRY(c->dt_soffs.need(P + 1));
+  RC_TRY(c->dt_doffs.need(P + 1));
+  RC_TRY(c->dt_swap.need(nt));
+  RC_TRY(c->dt_lim.need(2 * P));
+  CUDA_TRY(cudaMemcpyAsync(c->dt_swap.p, swap_t, nt, cudaMemcpyHostToDevice, c->stream));
+  // the supports' sizes are the peaks' votes (a support is the peak bin's
+  // voters at the bin's own trig): the host sizes the outputs from them
+  RC_TRY(ensure_pinned(c, sizeof(int64_t) * (3 * 64 + 4)));
+  int64_t* pin = reinterpret_cast<int64_t*>(c->pin);
+  CUDA_TRY(cudaMemcpyAsync(pin, c->dt_peaks.p, sizeof(int64_t) * 3 * P, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  int64_t total = 0;
+  std::vector<int64_t> soff(P + 1, 0);
+  for (int k = 0; k < P; ++k) {
+    total += pin[3 * k + 2];
+    soff[k + 1] = total;
+  }
+  // peaks grouped by theta bin (their support trig), in order of appearance
+  lmsb::SupportTable tb{};
+  tb.npeaks = P;
+  {
+    std::vector<int> slot_tb;
+    for (int k = 0; k < P; ++k) {
+      const int t = (int)pin[3 * k + 1];
+      if (std::find(slot_tb.begin(), slot_tb.end(), t) == slot_tb.end()) slot_tb.push_back(t);
+    }
+    int m = 0;
+    tb.nslot = (int)slot_tb.size();
+    for (int sl = 0; sl < tb.nslot; ++sl) {
+      const int t = slot_tb[sl];
+      tb.trig[sl] = lmsb::Trig{(float)cos_s[t], (float)sin_s[t], cos_s[t], sin_s[t]};
+      tb.first[sl] = m;
+      for (int k = 0; k < P; ++k)
+        if ((int)pin[3 * k + 1] == t) {
+          tb.peak[m] = k;
+          tb.rbin[m] = (int)pin[3 * k];
+          ++m;
+        }
+    }
+    tb.first[tb.nslot] = m;
+  }
+  std::vector<int64_t> doff(P + 1, 0);
+  for (int k = 0; k < P; ++k) {
+    const int64_t m = pin[3 * k + 2];
+    doff[k + 1] = doff[k] + ((support_cap > 0 && m > support_cap) ? support_cap : m);
+  }
+  RC_TRY(c->dt_ids.need(std::max<int64_t>(total, 1)));
+  RC_TRY(c->dt_a.need(std::max<int64_t>(doff[P], 1)));
+  RC_TRY(c->dt_b.need(std::max<int64_t>(doff[P], 1)));
+  CUDA_TRY(cudaMemcpyAsync(c->dt_doffs.p, doff.data(), sizeof(int64_t) * (P + 1), cudaMemcpyHostToDevice,
+                           c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->dt_soffs.p, soff.data(), sizeof(int64_t) * (P + 1), cudaMemcpyHostToDevice,
+                           c->stream));
+  CUDA_TRY(cudaMemsetAsync(c->dt_nlit.p, 0, sizeof(unsigned long long), c->stream));
+  lmsb::DetectImage im{c->img.p, c->dt_npix, c->dt_width, c->dt_threshold};
+  const int64_t* d_np = c->dt_peaks.p + 3 * 64;
+  CUDA_TRY(cudaEventRecord(c->ev_chunk[12], c->stream));
+  lmsb::launch_detect_support(im, c->dt_grid, tb, c->dt_soffs.p, c->dt_counts.p, c->dt_offs.p,
+                              c->dt_ids.p, c->dt_nlit.p, c->sms, c->stream);
+  CUDA_TRY(cudaEventRecord(c->ev_chunk[13], c->stream));
+  lmsb::launch_detect_design(c->dt_peaks.p, d_np, P, c->dt_soffs.p, c->dt_ids.p, c->dt_width,
+                             support_cap, c->dt_swap.p, c->dt_doffs.p, c->dt_a.p, c->dt_b.p,
+                             c->dt_lim.p, c->stream);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpyAsync(abscissa_range, c->dt_lim.p, sizeof(double) * 2 * P,
+                           cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(pin, c->dt_nlit.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                           c->stream));
+  std::memcpy(design_offsets, doff.data(), sizeof(int64_t) * (P + 1));
+  std::memcpy(support_offsets, soff.data(), sizeof(int64_t) * (P + 1));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  if (pin[0] != 0)
+    return set_error(LMS_ERR_CUDA, "%lld supports differ in size from their peaks' votes",
+                     (long long)pin[0]);
+  float sup_ms = 0.f;
+  CUDA_TRY(cudaEventElapsedTime(&sup_ms, c->ev_chunk[12], c->ev_chunk[13]));
+  const float vote_ms = c->stats.ms_hough_vote;
+  if (total > capacity) return set_error(LMS_ERR_INVALID, "support capacity %lld < %lld",
+                                         (long long)capacity, (long long)total);
+  // the supports go down while the fits run: the designs are copied first
+  // (the solver binds host copies of its lines for its line statistics)
+  bool run_fit = fit != 0;
+  for (int k = 0; k < P && run_fit; ++k) {
+    const int64_t n = doff[k + 1] - doff[k];
+    run_fit = n >= 3 && abscissa_range[2 * k] < abscissa_range[2 * k + 1] && q && q[k] >= 2 && q[k] <= n;
+  }
+  if (run_fit) {
+    const int64_t N = doff[P];
+    c->h_a.resize(N);
+    c->h_b.resize(N);
+    CUDA_TRY(cudaMemcpyAsync(c->h_a.data(), c->dt_a.p, sizeof(double) * N, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(c->h_b.data(), c->dt_b.p, sizeof(double) * N, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    c->a = c->dt_a.p;
+    c->b = c->dt_b.p;
+    c->nlines = N;
+    cache_line_stats(c);
+    RC_TRY(ctx_solve_batch(c, doff.data(), q, P, records));
+    RC_TRY(c->boffs.need(P + 1));
+    RC_TRY(c->bcflags.need(std::max<int64_t>(N, 1)));
+    CUDA_TRY(cudaMemcpyAsync(c->boffs.p, doff.data(), sizeof(int64_t) * (P + 1), cudaMemcpyHostToDevice,
+                             c->stream));
+    lmsb::launch_contacts_batch(c->a, c->b, c->boffs.p, c->best.p, P, c->bcflags.p, c->sms, c->stream);
+    CUDA_TRY(cudaGetLastError());
+    if (contact_flags)
+      CUDA_TRY(cudaMemcpyAsync(contact_flags, c->bcflags.p, (size_t)N, cudaMemcpyDeviceToHost, c->stream));
+  }
+  if (support_ids) RC_TRY(download_staged(c, support_ids, c->dt_ids.p, sizeof(int32_t) * total));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  c->stats.ms_hough_vote = vote_ms;  // (the fits' solve reset the counters)
+  c->stats.ms_hough_support = sup_ms;
+  return run_fit || fit == 0 ? LMS_OK : LMS_NOT_FITTED;
 }
 
 int lms_ctx_solve_batch(lms_ctx* c, const int64_t* offsets, const int64_t* q, int64_t nfits,

@@ -23,6 +23,7 @@ from .geometry import DegenerateInputError, InvalidInputError, LineEq, Point2
 from .hough import (
     HoughAccumulator,
     HoughParams,
+    Peak,
     find_peaks,
     line_to_polar,
     lit_mask_u8,
@@ -227,6 +228,10 @@ def detect_lines(image: np.ndarray, params: HoughParams, method: str = METHOD_LM
     if method not in METHODS:
         raise InvalidInputError(f"unknown method {method!r}; expected one of {METHODS}")
     img, thr = lit_mask_u8(image, threshold)
+    if (params.n_rho * params.n_theta <= _native.DETECT_MAX_BINS and params.n_theta <= 512
+            and 1 <= max_peaks <= _native.DETECT_MAX_PEAKS and min_votes >= 1 and img.size < 2**31):
+        return _detect_on_device(img, thr, params, method, max_peaks, min_votes, q, backend, workers,
+                                 support_cap)
     c, s = params.vote_trig()
     # the support gather reads the points the vote leaves on the device: one
     # lock across both, so another thread's vote cannot land in between
@@ -273,6 +278,80 @@ def detect_lines(image: np.ndarray, params: HoughParams, method: str = METHOD_LM
         Z = np.where(swap, col, row)
         lms_fits = _solve_concat(T, Z, offsets, q)
 
+    out: list[LineDetection] = []
+    for k, (peak, sup, sw) in enumerate(zip(peaks, supports, swapped)):
+        lms_value = None
+        if method == METHOD_SHT:
+            rho, theta = peak.rho, peak.theta
+            slope, intercept, sw = polar_to_frame_fit(rho, theta)
+        elif method == METHOD_OLS:
+            fit = refine_ols(sup, sw)
+            slope, intercept = fit.slope, fit.intercept
+            rho, theta = line_to_polar(slope, intercept, sw)
+        else:
+            fit = lms_fits[k]
+            slope, intercept = fit.line.slope, fit.line.intercept
+            lms_value = fit.lms_value
+            rho, theta = line_to_polar(slope, intercept, sw)
+        out.append(LineDetection(method=method, rho=rho, theta=theta, slope=slope, intercept=intercept,
+                                 axis_swapped=sw, support=sup, lms_value=lms_value))
+    return out
+
+
+def _detect_on_device(img, thr, params: HoughParams, method: str, max_peaks: int, min_votes: int,
+                      q, backend, workers, support_cap) -> list[LineDetection]:
+    """detect_lines with vote, find_peaks, support gather, stride thinning,
+    axis-swapped designs and the batched LMS refits all on the device, from
+    the image (lms_detect_peaks_u8 / lms_detect_supports_u8); the host keeps
+    the polar maps and the result objects.  Errors as the reference's
+    per-peak loop (detect.py:184-213): the first peak whose refit fails."""
+    from . import _native
+    from .backend import get_backend
+    from .solver import _fits_from_arrays
+
+    do_lms = method == METHOD_LMS
+    if do_lms:
+        get_backend(backend, workers)  # same name / worker validation as solve_lms
+        if support_cap is not None and support_cap < 3:
+            raise InvalidInputError(f"support cap must be at least 3, got {support_cap}")
+    c, s = params.vote_trig()
+    nt = params.n_theta
+    with _native.hough_lock(0):
+        npts, pk, _ = _native.detect_peaks(img, thr, c, s, params.rho_max, params.delta_rho, params.n_rho,
+                                           max_peaks, min_votes)
+        if npts == 0 or pk.shape[0] == 0:
+            return []
+        P = pk.shape[0]
+        peaks = [Peak(rho_bin=int(r), theta_bin=int(t), votes=int(v), rho=params.rho_center(int(r)),
+                      theta=params.theta_center(int(t))) for r, t, v in pk.tolist()]
+        strig = [params.support_trig(t) for t in range(nt)]
+        swap_t = [needs_axis_swap(params.theta_center(t)) for t in range(nt)]
+        votes = pk[:, 2]
+        cap = support_cap if (do_lms and support_cap is not None) else 0
+        n_fit = np.minimum(votes, cap) if cap else votes
+        qv = n_fit // 2 + 1 if q is None else np.full(P, int(q), dtype=np.int64)
+        res = _native.detect_supports([a for a, _ in strig], [b for _, b in strig], swap_t, cap, qv,
+                                      do_lms, P, votes)
+    width = img.shape[1]
+    soff, ids = res["support_offsets"], res["ids"]
+    supports = [SupportPoints.from_pixels(ids[soff[k]: soff[k + 1]], width) for k in range(P)]
+    swapped = [bool(swap_t[p.theta_bin]) for p in peaks]
+    lms_fits = []
+    if do_lms:
+        if not res["fitted"]:
+            doff, lim = res["design_offsets"], res["abscissa_range"]
+            for k in range(P):  # the reference's loop stops at the first failing peak
+                n = int(doff[k + 1] - doff[k])
+                if n < 3:
+                    raise DegenerateInputError(f"LMS needs at least 3 points, got {n}")
+                if not lim[k, 0] < lim[k, 1]:
+                    raise DegenerateInputError("all points share one x-coordinate; no non-vertical line fits")
+                if not 2 <= int(qv[k]) <= n:
+                    raise InvalidInputError(f"coverage must satisfy 2 <= q <= {n}, got {int(qv[k])}")
+            raise DegenerateInputError("no candidate slab found")
+        if not bool(res["records"]["found"].all()):
+            raise DegenerateInputError("no candidate slab found")
+        lms_fits = _fits_from_arrays(res["records"], res["contact_flags"], res["design_offsets"], qv)
     out: list[LineDetection] = []
     for k, (peak, sup, sw) in enumerate(zip(peaks, supports, swapped)):
         lms_value = None

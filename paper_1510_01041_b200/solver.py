@@ -212,23 +212,81 @@ def _solve_concat(X: np.ndarray, Y: np.ndarray, offsets: np.ndarray, q, *,
                     "all points share one x-coordinate; no non-vertical line fits")
             raise InvalidInputError(f"coverage must satisfy 2 <= q <= {int(counts[k])}, got {int(qv[k])}")
     # the records and, computed on the device with fit_from_record's
-    # arithmetic, one contact flag per point
-    cands, flags = _native.batched_fit(X, Y, offsets, qv)
-    recs = [record_from_native(cands[k]) for k in range(F)]
-    if any(r is None for r in recs):
+    # arithmetic, one contact flag per point; several visible GPUs share the
+    # fits (contiguous groups, no collective: SURVEY section 8e row 2)
+    cands, flags = _batched_fit_devices(X, Y, offsets, qv)
+    if not bool(cands["found"].all()):
         raise DegenerateInputError("no candidate slab found")
+    return _fits_from_arrays(cands, flags, offsets, qv)
+
+
+def _batched_fit_devices(X, Y, offsets, qv):
+    """lms_batched_fit_f64 over the visible GPUs: fit groups with about equal
+    point counts, one thread per device (the library releases the GIL), the
+    records as a structured array and the per-point contact flags."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from . import _native
+
+    F = offsets.size - 1
+    ndev = max(1, min(_native.device_count(), F))
+    if ndev == 1:
+        out, flags = _native.batched_fit(X, Y, offsets, qv)
+        return _native.candidates_array(out, F), flags
+    # split points at fit boundaries near k / ndev of the total
+    cuts = np.searchsorted(offsets, np.linspace(0, offsets[-1], ndev + 1)[1:-1])
+    fb = np.unique(np.concatenate([[0], cuts, [F]]))
+
+    def run(d):
+        f0, f1 = int(fb[d]), int(fb[d + 1])
+        p0, p1 = int(offsets[f0]), int(offsets[f1])
+        out, fl = _native.batched_fit(X[p0:p1], Y[p0:p1], offsets[f0:f1 + 1] - p0, qv[f0:f1], device=d)
+        return _native.candidates_array(out, f1 - f0), fl
+
+    with ThreadPoolExecutor(max_workers=len(fb) - 1) as pool:
+        parts = list(pool.map(run, range(len(fb) - 1)))
+    return np.concatenate([p[0] for p in parts]), np.concatenate([p[1] for p in parts])
+
+
+def _fits_from_arrays(cands, flags, offsets, qv) -> list[LmsFit]:
+    """LmsFit objects of a batch from the record arrays: the solve_lms tail's
+    arithmetic (solver.py:122-140) elementwise over all fits (same IEEE
+    operations as the scalar form), contact sets from the device's flags;
+    the objects are filled directly (the dataclasses stay frozen to users)
+    with the cyclic GC paused while thousands are created."""
+    import gc
+
+    F = offsets.size - 1
+    u, vl, vh = cands["u"], cands["v_low"], cands["v_high"]
+    slope = u.tolist()
+    intercept = (-(vl + vh) * 0.5).tolist()
+    half = (vh - vl) * 0.5
+    lms_value = (half * half).tolist()
+    slab = (vh - vl).tolist()
     idx = np.flatnonzero(flags)
     owner = np.searchsorted(offsets, idx, side="right") - 1
-    local = idx - offsets[owner]
-    bounds = np.searchsorted(owner, np.arange(F + 1))
+    local = (idx - offsets[owner]).tolist()
+    bounds = np.searchsorted(owner, np.arange(F + 1)).tolist()
+    cov = np.asarray(qv, dtype=np.int64).tolist()
+    new = object.__new__
     fits = []
-    for k, rec in enumerate(recs):
-        half = (rec.v_high - rec.v_low) * 0.5
-        fits.append(LmsFit(
-            line=LineEq(slope=rec.u, intercept=-(rec.v_low + rec.v_high) * 0.5),
-            lms_value=half * half,
-            slab_height=rec.v_high - rec.v_low,
-            coverage=int(qv[k]),
-            contact_indices=tuple(local[bounds[k]:bounds[k + 1]].tolist()),
-        ))
+    was = gc.isenabled()
+    gc.disable()
+    try:
+        for k in range(F):
+            line = new(LineEq)
+            d = line.__dict__
+            d["slope"] = slope[k]
+            d["intercept"] = intercept[k]
+            fit = new(LmsFit)
+            d = fit.__dict__
+            d["line"] = line
+            d["lms_value"] = lms_value[k]
+            d["slab_height"] = slab[k]
+            d["coverage"] = cov[k]
+            d["contact_indices"] = tuple(local[bounds[k]:bounds[k + 1]])
+            fits.append(fit)
+    finally:
+        if was:
+            gc.enable()
     return fits

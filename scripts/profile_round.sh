@@ -1,26 +1,32 @@
 #!/bin/bash
-# Round profile: ncu captures of the band-stage kernels and the fused small-fit
-# kernel, launch list of a short bench, then the default bench lines (run
-# under gpurun).
+# Round profile (run under gpurun): ncu summaries of the config-2 band kernels,
+# the config-3 large-n kernels, the fused small-fit kernel and the device
+# detect kernels; launch lists of configs 2, 3 and 5; then the default bench
+# lines (ours and the reference arm).  usage: bash scripts/profile_round.sh TAG
 set -x
+tag=${1:-r02}
 mkdir -p gpurun_out
-ncu --set full --clock-control none --import-source on -k regex:band_collect_kernel -c 1 \
-    -o gpurun_out/r01_collect python scripts/quick_time.py 16384 1 > gpurun_out/ncu_collect.log 2>&1
-python scripts/ncu_summary.py gpurun_out/r01_collect.ncu-rep profiles/r01_collect_ncu.json band_collect
-ncu --set full --clock-control none -k regex:"band_filter_kernel|band_bound_kernel|band_count_kernel|exact_cached" \
-    -o gpurun_out/r01_band_kernels python scripts/quick_time.py 16384 1 > gpurun_out/ncu_band.log 2>&1
-python scripts/ncu_summary.py gpurun_out/r01_band_kernels.ncu-rep profiles/r01_band_kernels_ncu.json
+ncu --set full --clock-control none --import-source on \
+    -k regex:"band_filter_kernel|band_bound_kernel|sweep_enum|band_count_kernel|exact_cached" \
+    -o gpurun_out/${tag}_band python scripts/quick_time.py 16384 1 > gpurun_out/ncu_band.log 2>&1
+python scripts/ncu_summary.py gpurun_out/${tag}_band.ncu-rep profiles/${tag}_band_kernels_ncu.json
+ncu --set full --clock-control none -k regex:"band_filter_big|sweep_enum|band_count_kernel|band_coarse" -c 4 \
+    -o gpurun_out/${tag}_big python scripts/quick_time.py 65536 1 > gpurun_out/ncu_big.log 2>&1
+python scripts/ncu_summary.py gpurun_out/${tag}_big.ncu-rep profiles/${tag}_big_kernels_ncu.json
 ncu --set full --clock-control none -k regex:small_fit -c 1 \
-    -o gpurun_out/r01_small python scripts/quick_batch.py 2048 512 1 > gpurun_out/ncu_small.log 2>&1
-python scripts/ncu_summary.py gpurun_out/r01_small.ncu-rep profiles/r01_small_fit_ncu.json small_fit
-ncu --set full --clock-control none -k regex:"band_coarse_kernel|band_filter_big_kernel|band_count_kernel" -c 3 \
-    -o gpurun_out/r01_big python scripts/quick_time.py 65536 1 > gpurun_out/ncu_big.log 2>&1
-python scripts/ncu_summary.py gpurun_out/r01_big.ncu-rep profiles/r01_big_kernels_ncu.json
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r01_launches_config3.csv \
-    python scripts/quick_time.py 65536 1 > gpurun_out/ncu_c3.log 2>&1
-cp profiles/r01_*_ncu.json gpurun_out/
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r01_launches_band.csv \
+    -o gpurun_out/${tag}_small python scripts/quick_batch.py 2048 512 1 > gpurun_out/ncu_small.log 2>&1
+python scripts/ncu_summary.py gpurun_out/${tag}_small.ncu-rep profiles/${tag}_small_fit_ncu.json small_fit
+ncu --set full --clock-control none -k regex:"img_vote|support_count_img|support_write_img|peaks_kernel" \
+    -o gpurun_out/${tag}_detect python scripts/detect_once.py 1 > gpurun_out/ncu_detect.log 2>&1
+python scripts/ncu_summary.py gpurun_out/${tag}_detect.ncu-rep profiles/${tag}_detect_ncu.json
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file profiles/${tag}_launches_config2.csv \
     python bench.py --steps 2 --warmup 1 --no-extra --no-cpu-baseline > gpurun_out/bench_under_ncu.log 2>&1
-python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
-python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
-tail -c 3000 gpurun_out/bench.json
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file profiles/${tag}_launches_config3.csv \
+    python scripts/quick_time.py 65536 1 > gpurun_out/ncu_c3.log 2>&1
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+    --log-file profiles/${tag}_launches_config5.csv python scripts/detect_once.py 1 > gpurun_out/ncu_c5.log 2>&1
+cp profiles/${tag}_*_ncu.json gpurun_out/
+python bench.py > gpurun_out/bench_${tag}.json 2> gpurun_out/bench_${tag}.err
+python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref_${tag}.json 2> gpurun_out/bench_ref_${tag}.err
+tail -c 4000 gpurun_out/bench_${tag}.json
+cat gpurun_out/bench_ref_${tag}.json
