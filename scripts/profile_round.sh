@@ -19,12 +19,12 @@ python scripts/ncu_summary.py gpurun_out/${tag}_small.ncu-rep profiles/${tag}_sm
 ncu --set full --clock-control none -k regex:"img_vote|support_count_img|support_write_img|peaks_kernel" \
     -o gpurun_out/${tag}_detect python scripts/detect_once.py 1 > gpurun_out/ncu_detect.log 2>&1
 python scripts/ncu_summary.py gpurun_out/${tag}_detect.ncu-rep profiles/${tag}_detect_ncu.json
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file profiles/${tag}_launches_config2.csv \
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${tag}_launches_config2.csv \
     python bench.py --steps 2 --warmup 1 --no-extra --no-cpu-baseline > gpurun_out/bench_under_ncu.log 2>&1
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file profiles/${tag}_launches_config3.csv \
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${tag}_launches_config3.csv \
     python scripts/quick_time.py 65536 1 > gpurun_out/ncu_c3.log 2>&1
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
-    --log-file profiles/${tag}_launches_config5.csv python scripts/detect_once.py 1 > gpurun_out/ncu_c5.log 2>&1
+    --log-file gpurun_out/${tag}_launches_config5.csv python scripts/detect_once.py 1 > gpurun_out/ncu_c5.log 2>&1
 cp profiles/${tag}_*_ncu.json gpurun_out/
 python bench.py > gpurun_out/bench_${tag}.json 2> gpurun_out/bench_${tag}.err
 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref_${tag}.json 2> gpurun_out/bench_ref_${tag}.err
