@@ -231,7 +231,8 @@ struct lms_ctx {
   DevBuf<int64_t> dt_peaks, dt_offs, dt_soffs, dt_doffs;
   DevBuf<unsigned> dt_counts;
   DevBuf<int32_t> dt_ids;
-  DevBuf<double> dt_a, dt_b, dt_lim, dt_strig;
+  DevBuf<double> dt_a, dt_b, dt_lim, dt_strig, dt_wedge;
+  DevBuf<uint32_t> dt_bits;
   DevBuf<uint8_t> dt_swap;
   DevBuf<unsigned long long> dt_nlit;
   int64_t dt_npix = 0, dt_width = 0, dt_npeaks = -1;
@@ -481,6 +482,8 @@ void ctx_release(lms_ctx* c) {
   c->dt_b.release();
   c->dt_lim.release();
   c->dt_strig.release();
+  c->dt_wedge.release();
+  c->dt_bits.release();
   c->dt_swap.release();
   c->dt_nlit.release();
   c->xsend.release();
@@ -3066,6 +3069,8 @@ int lms_detect_peaks_u8(const uint8_t* img, int64_t height, int64_t width, int t
     return set_error(LMS_ERR_INVALID, "accumulator too large for the device peak finder");
   const int64_t npix = height * width;
   if (npix > INT32_MAX) return set_error(LMS_ERR_INVALID, "image too large for int32 pixel ids");
+  if (width > lmsb::kDetectMaxWidth || n_rho > 4095)
+    return set_error(LMS_ERR_INVALID, "image too wide or rho range too fine for the device vote");
   lms_ctx* c = nullptr;
   RC_TRY(shared_ctx(device, &c));
   std::lock_guard<std::mutex> lk(c->mu);
@@ -3094,7 +3099,11 @@ int lms_detect_peaks_u8(const uint8_t* img, int64_t height, int64_t width, int t
     c->ev_chunk.push_back(e);
   }
   CUDA_TRY(cudaEventRecord(c->ev_chunk[12], c->stream));
-  if (npix > 0) lmsb::launch_detect_vote(im, g, c->tcos.p, c->tsin.p, c->acc.p, c->dt_nlit.p, c->sms, c->stream);
+  RC_TRY(c->dt_wedge.need(n_rho));
+  RC_TRY(c->dt_bits.need(std::max<int64_t>(1, height * ((width + 31) / 32))));
+  if (npix > 0)
+    lmsb::launch_detect_vote(im, g, c->tcos.p, c->tsin.p, c->dt_wedge.p, c->dt_bits.p, c->acc.p,
+                             c->dt_nlit.p, c->sms, c->stream);
   CUDA_TRY(cudaEventRecord(c->ev_chunk[13], c->stream));
   int64_t* d_np = c->dt_peaks.p + 3 * 64;
   lmsb::launch_detect_peaks(c->acc.p, g, min_votes, (int)max_peaks, c->dt_peaks.p, d_np, c->stream);
@@ -3139,7 +3148,7 @@ int lms_detect_supports_u8(const double* cos_s, const double* sin_s, const uint8
   support_offsets[0] = 0;
   design_offsets[0] = 0;
   if (P == 0) return LMS_OK;
-  const int64_t nch = lmsb::detect_support_chunks(c->dt_npix);
+  const int64_t nch = lmsb::detect_support_rows(c->dt_npix, c->dt_width);
   RC_TRY(c->dt_counts.need(std::max<int64_t>((int64_t)P * nch, 1)));
   RC_TRY(c->dt_offs.need((int64_t)P * nch + 1));
   RC_TRY(c->dt_soffs.need(P + 1));
@@ -3199,8 +3208,9 @@ int lms_detect_supports_u8(const double* cos_s, const double* sin_s, const uint8
   lmsb::DetectImage im{c->img.p, c->dt_npix, c->dt_width, c->dt_threshold};
   const int64_t* d_np = c->dt_peaks.p + 3 * 64;
   CUDA_TRY(cudaEventRecord(c->ev_chunk[12], c->stream));
-  lmsb::launch_detect_support(im, c->dt_grid, tb, c->dt_soffs.p, c->dt_counts.p, c->dt_offs.p,
-                              c->dt_ids.p, c->dt_nlit.p, c->sms, c->stream);
+  lmsb::launch_detect_support(im, c->dt_grid, tb, c->dt_wedge.p, c->dt_bits.p, c->dt_soffs.p,
+                              c->dt_counts.p, c->dt_offs.p, c->dt_ids.p, c->dt_nlit.p, c->sms,
+                              c->stream);
   CUDA_TRY(cudaEventRecord(c->ev_chunk[13], c->stream));
   lmsb::launch_detect_design(c->dt_peaks.p, d_np, P, c->dt_soffs.p, c->dt_ids.p, c->dt_width,
                              support_cap, c->dt_swap.p, c->dt_doffs.p, c->dt_a.p, c->dt_b.p,

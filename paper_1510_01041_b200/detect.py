@@ -229,6 +229,7 @@ def detect_lines(image: np.ndarray, params: HoughParams, method: str = METHOD_LM
         raise InvalidInputError(f"unknown method {method!r}; expected one of {METHODS}")
     img, thr = lit_mask_u8(image, threshold)
     if (params.n_rho * params.n_theta <= _native.DETECT_MAX_BINS and params.n_theta <= 512
+            and params.n_rho <= 4095 and img.shape[1] <= 4096 * 32
             and 1 <= max_peaks <= _native.DETECT_MAX_PEAKS and min_votes >= 1 and img.size < 2**31):
         return _detect_on_device(img, thr, params, method, max_peaks, min_votes, q, backend, workers,
                                  support_cap)
