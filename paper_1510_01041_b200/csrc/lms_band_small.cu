@@ -79,10 +79,12 @@ constexpr int kQueue = 32 * (kSweepStep + 1);  // per-warp queues: < 32 waiting 
 static_assert(kSegRun % kSweepStep == 0, "whole sweep steps per segment");
 constexpr int kMaxRuns = 8;   // slope runs tested before a band lookup
 
-template <int kItems>
+template <int kItems, int kT = kThreads>
 struct SmallShared {
   static constexpr int kNP = 32 * kItems;  // padded lines (one warp sorts a band)
-  using SampleSort = cub::BlockRadixSort<float, kThreads, kSampleItems, int>;
+  static constexpr int kWarps = kT / 32;
+  static constexpr int kSampleItems = kSamples / kT;
+  using SampleSort = cub::BlockRadixSort<float, kT, kSampleItems, int>;
   alignas(16) double a[kNP];
   alignas(16) double b[kNP];
 #if LMSB_SMALL_AB
@@ -186,8 +188,9 @@ __device__ __forceinline__ void advance_pair(int n, int step, int& i, int& j) {
   }
 }
 
-template <int kItems>
-__device__ __forceinline__ double block_min(double v, SmallShared<kItems>& sh, int slot) {
+template <int kItems, int kT>
+__device__ __forceinline__ double block_min(double v, SmallShared<kItems, kT>& sh, int slot) {
+  constexpr int kWarps = kT / 32;
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, off));
   __syncthreads();
@@ -241,8 +244,8 @@ __device__ __forceinline__ void warp_bitonic_sort(float (&x)[kItems]) {
 }
 
 // keys of band `band` at its centre uM, sorted by the calling warp into dst
-template <int kItems>
-__device__ __forceinline__ void band_keys_warp(const SmallShared<kItems>& sh, int n, double c,
+template <int kItems, int kT>
+__device__ __forceinline__ void band_keys_warp(const SmallShared<kItems, kT>& sh, int n, double c,
                                                double uM, float* dst) {
   const int lane = threadIdx.x & 31;
   float x[kItems];
@@ -257,9 +260,12 @@ __device__ __forceinline__ void band_keys_warp(const SmallShared<kItems>& sh, in
   __syncwarp();
 }
 
-template <int kItems>
-__global__ void __launch_bounds__(kThreads, LMSB_SMALL_MINB) small_fit_kernel(SmallArgs args) {
-  using SH = SmallShared<kItems>;
+template <int kItems, int kT>
+__global__ void __launch_bounds__(kT, kT == kThreads ? LMSB_SMALL_MINB : 1) small_fit_kernel(SmallArgs args) {
+  using SH = SmallShared<kItems, kT>;
+  constexpr int kThreads = kT;  // this instance's CTA size (the file-scope default is 256)
+  constexpr int kWarps = kT / 32;
+  constexpr int kSampleItems = kSamples / kT;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SH& sh = *reinterpret_cast<SH*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -822,21 +828,30 @@ __global__ void __launch_bounds__(kThreads, LMSB_SMALL_MINB) small_fit_kernel(Sm
   }
 }
 
-template <int kItems>
+template <int kItems, int kT>
 void launch_small_t(const SmallArgs& args, int grid, cudaStream_t st) {
-  constexpr size_t smem = sizeof(SmallShared<kItems>);
+  constexpr size_t smem = sizeof(SmallShared<kItems, kT>);
   static DeviceOnce done;
-  set_max_smem(small_fit_kernel<kItems>, smem, done);
-  small_fit_kernel<kItems><<<grid, kThreads, smem, st>>>(args);
+  set_max_smem(small_fit_kernel<kItems, kT>, smem, done);
+  small_fit_kernel<kItems, kT><<<grid, kT, smem, st>>>(args);
 }
 
 }  // namespace
 
-void launch_small_fits(const SmallArgs& args, int64_t count, int64_t max_n, cudaStream_t st) {
+void launch_small_fits(const SmallArgs& args, int64_t count, int64_t max_n, int sms, cudaStream_t st) {
   if (count <= 0) return;
-  if (max_n <= 256) launch_small_t<8>(args, (int)count, st);
-  else if (max_n <= 512) launch_small_t<16>(args, (int)count, st);
-  else launch_small_t<32>(args, (int)count, st);
+  // fewer fits than SMs (the 64 peaks of a detect_lines call): one CTA per
+  // fit is the latency, so 512 threads a fit; otherwise 256 (2 CTAs/SM)
+  const bool wide = count <= sms;
+  if (max_n <= 256) {
+    if (wide) launch_small_t<8, 512>(args, (int)count, st);
+    else launch_small_t<8, 256>(args, (int)count, st);
+  } else if (max_n <= 512) {
+    if (wide) launch_small_t<16, 512>(args, (int)count, st);
+    else launch_small_t<16, 256>(args, (int)count, st);
+  } else {
+    launch_small_t<32, 256>(args, (int)count, st);
+  }
 }
 
 }  // namespace lmsb

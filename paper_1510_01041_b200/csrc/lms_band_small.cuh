@@ -23,6 +23,6 @@ struct SmallArgs {
   int timing;                    // also accumulate per-stage clock64 cycles (LMSB_SMALL_DEBUG)
 };
 
-void launch_small_fits(const SmallArgs& args, int64_t count, int64_t max_n, cudaStream_t st);
+void launch_small_fits(const SmallArgs& args, int64_t count, int64_t max_n, int sms, cudaStream_t st);
 
 }  // namespace lmsb

@@ -1873,7 +1873,7 @@ int ctx_solve_fits(lms_ctx* c, const std::vector<HostFit>& hf, lms_candidate* ou
     CUDA_TRY(cudaMemsetAsync(c->small_cnt.p, 0, 12 * sizeof(unsigned long long), c->stream));
     sa.counters = c->small_cnt.p;
     sa.timing = getenv("LMSB_SMALL_DEBUG") != nullptr;
-    lmsb::launch_small_fits(sa, (int64_t)small_list.size(), small_maxn, c->stream);
+    lmsb::launch_small_fits(sa, (int64_t)small_list.size(), small_maxn, c->sms, c->stream);
     CUDA_TRY(cudaGetLastError());
     st.launches += 1;
     st.small_fits = (int64_t)small_list.size();
