@@ -142,6 +142,25 @@ int lms_batched_f64(const double* x, const double* y, const int64_t* offsets, co
 int lms_batched_fit_f64(const double* x, const double* y, const int64_t* offsets, const int64_t* q,
                         int64_t nfits, int device, lms_candidate* out, uint8_t* contact_flags);
 
+/* solve_lms over a list of point sets (solve_lms_batch; the reference's
+ * per-peak refits, detect.py:184-213): set f is sets[f], counts[f] rows of
+ * (x, y) fp64, row-major, coverage q[f].  The sets go up through pinned
+ * staging filled by host threads (no concatenated host copy), are checked on
+ * the device as solve_lms checks them (solver.py:67-80) -- status[f] = 0 ok,
+ * 1 non-finite, 2 fewer than 3 points, 3 one distinct x, 4 q outside
+ * [2, n]; any non-zero: LMS_NOT_FITTED, nothing solved -- then solved in one
+ * batch; out[f] the record, each set's contact indices (solver.py:122-140)
+ * ascending in contacts[contact_offsets[f] .. contact_offsets[f+1]),
+ * *ncontacts in total (only written when <= contact_capacity). */
+int lms_batched_fit_sets_f64(const double* const* sets, const int64_t* counts, const int64_t* q,
+                             int64_t nfits, int device, int32_t* status, lms_candidate* out,
+                             int64_t* contact_offsets, int32_t* contacts, int64_t contact_capacity,
+                             int64_t* ncontacts);
+/* Python-binding helper: data pointers and row counts of `count` numpy
+ * arrays given by object address (id()), each checked to be a C-contiguous
+ * (n, 2) array of 8-byte elements (the caller checks the dtype). */
+int lms_ndarray_rows_f64(const uintptr_t* objs, int64_t count, const double** data, int64_t* rows);
+
 /* oracle_lms (solver.py:143-196), the reference's independent primal brute
  * force: per pair slope, sorted intercepts, narrowest q-window (first
  * minimal); lexicographic (span, i, j) minimum.  out->height = span,

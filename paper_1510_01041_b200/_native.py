@@ -207,6 +207,10 @@ SIGNATURES = {
                                               ctypes.POINTER(ctypes.c_int32), ctypes.c_int64, _I, _D, _C,
                                               ctypes.POINTER(ctypes.c_uint8)]),
     "lms_device_stats": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(Stats)]),
+    "lms_batched_fit_sets_f64": (ctypes.c_int, [ctypes.c_void_p, _I, _I, ctypes.c_int64, ctypes.c_int,
+                                                ctypes.POINTER(ctypes.c_int32), _C, _I,
+                                                ctypes.POINTER(ctypes.c_int32), ctypes.c_int64, _I]),
+    "lms_ndarray_rows_f64": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, _I]),
     "lms_probe_fp64_rate": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_double)]),
     "lms_probe_fp32_rate": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_double)]),
 }
@@ -368,6 +372,33 @@ def candidates_array(out, count: int) -> np.ndarray:
     """A ctypes lms_candidate array as a numpy structured array (copied)."""
     assert ctypes.sizeof(Candidate) == CANDIDATE_DTYPE.itemsize
     return np.frombuffer(out, dtype=CANDIDATE_DTYPE, count=count).copy()
+
+
+def batched_fit_sets(sets, q, device: int = 0):
+    """lms_batched_fit_sets_f64 over a list of C-contiguous (n, 2) float64
+    arrays -> (status int32[F], records structured[F] or None, contact
+    offsets int64[F + 1], contacts int32).  status all zero: fitted."""
+    lib = _lib_ready()
+    F = len(sets)
+    objs = np.fromiter(map(id, sets), dtype=np.uintp, count=F)
+    ptrs = np.empty(F, dtype=np.uintp)
+    rows = np.empty(F, dtype=np.int64)
+    check(lib.lms_ndarray_rows_f64(objs.ctypes.data, F, ptrs.ctypes.data, _ip(rows)))
+    qv = np.ascontiguousarray(q, dtype=np.int64)
+    status = np.zeros(F, dtype=np.int32)
+    out = (Candidate * max(F, 1))()
+    coff = np.zeros(F + 1, dtype=np.int64)
+    total = int(rows.sum())
+    contacts = np.empty(max(total, 1), dtype=np.int32)
+    ncon = ctypes.c_int64(0)
+    rc = lib.lms_batched_fit_sets_f64(ptrs.ctypes.data, _ip(rows), _ip(qv), F, int(device),
+                                      status.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), out, _ip(coff),
+                                      contacts.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), total,
+                                      ctypes.byref(ncon))
+    if rc == LMS_NOT_FITTED:
+        return status, None, coff, contacts[:0]
+    check(rc)
+    return status, candidates_array(out, F), coff, contacts[: ncon.value]
 
 
 def batched(x, y, offsets, q, device: int = 0) -> list:

@@ -37,6 +37,7 @@
 #include "lms_kernels.cuh"
 #include "lms_nccl.cuh"
 #include "lms_plan.cuh"
+#include "lms_sets.cuh"
 #include "lms_primal.cuh"
 
 #define LMS_VERSION 2
@@ -190,6 +191,13 @@ struct lms_ctx {
   const double* b = nullptr;
   int64_t nlines = 0;
   std::vector<double> h_a, h_b;  // host copy: per-fit max |a|, max |b| for the filter margins
+  // or, for lines that stay on the device (lms_batched_fit_sets_f64), the
+  // per-fit statistics computed there: fit offsets and (alo, ahi, am, bm)
+  std::vector<int64_t> ext_off;
+  std::vector<double> ext_st;
+  DevBuf<double> set_xy, set_stats;
+  DevBuf<int64_t> set_cnt, set_coff;
+  DevBuf<int32_t> set_contacts;
   double s_alo = 0, s_ahi = 0, s_am = 0, s_bm = 0;  // range / magnitudes of all bound lines
   // fits
   DevBuf<lmsb::FitDesc> fits;
@@ -486,6 +494,11 @@ void ctx_release(lms_ctx* c) {
   c->dt_bits.release();
   c->dt_swap.release();
   c->dt_nlit.release();
+  c->set_xy.release();
+  c->set_stats.release();
+  c->set_cnt.release();
+  c->set_coff.release();
+  c->set_contacts.release();
   c->xsend.release();
   c->xrecv.release();
   if (c->comm && c->comm_owned && lmsb::nccl().ok) lmsb::nccl().CommDestroy(c->comm);
@@ -499,6 +512,17 @@ void ctx_release(lms_ctx* c) {
 // at upload).
 void line_stats(const lms_ctx* c, int64_t off, int64_t n, double* alo, double* ahi, double* am,
                 double* bm) {
+  if (!c->ext_off.empty()) {
+    const auto it = std::lower_bound(c->ext_off.begin(), c->ext_off.end(), off);
+    if (it != c->ext_off.end() && *it == off) {
+      const size_t k = (size_t)(it - c->ext_off.begin());
+      *alo = c->ext_st[4 * k];
+      *ahi = c->ext_st[4 * k + 1];
+      *am = c->ext_st[4 * k + 2];
+      *bm = c->ext_st[4 * k + 3];
+      return;
+    }
+  }
   if (off == 0 && n == c->nlines) {
     *alo = c->s_alo;
     *ahi = c->s_ahi;
@@ -548,6 +572,7 @@ int ctx_upload(lms_ctx* c, const double* a, const double* b, int64_t n) {
   CUDA_TRY(cudaMemcpyAsync(c->b_own.p, b, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
   c->h_a.assign(a, a + n);
   c->h_b.assign(b, b + n);
+  c->ext_off.clear();
   c->a = c->a_own.p;
   c->b = c->b_own.p;
   c->nlines = n;
@@ -2811,6 +2836,7 @@ int lms_ctx_bind_dev(lms_ctx* c, const double* d_a, const double* d_b, int64_t n
   if (!c || !d_a || !d_b || n < 1) return set_error(LMS_ERR_INVALID, "bad arguments");
   std::lock_guard<std::mutex> lk(c->mu);
   CUDA_TRY(cudaSetDevice(c->device));
+  c->ext_off.clear();
   c->h_a.resize(n);
   c->h_b.resize(n);
   CUDA_TRY(cudaMemcpy(c->h_a.data(), d_a, sizeof(double) * n, cudaMemcpyDeviceToHost));
@@ -3240,6 +3266,7 @@ int lms_detect_supports_u8(const double* cos_s, const double* sin_s, const uint8
   }
   if (run_fit) {
     const int64_t N = doff[P];
+    c->ext_off.clear();
     c->h_a.resize(N);
     c->h_b.resize(N);
     CUDA_TRY(cudaMemcpyAsync(c->h_a.data(), c->dt_a.p, sizeof(double) * N, cudaMemcpyDeviceToHost, c->stream));
@@ -3264,6 +3291,172 @@ int lms_detect_supports_u8(const double* cos_s, const double* sin_s, const uint8
   c->stats.ms_hough_vote = vote_ms;  // (the fits' solve reset the counters)
   c->stats.ms_hough_support = sup_ms;
   return run_fit || fit == 0 ? LMS_OK : LMS_NOT_FITTED;
+}
+
+// H2D of many host pieces concatenated: each 4 MB pinned chunk is filled by
+// host threads from the pieces it overlaps (the concatenation and the copy
+// into pinned memory are one pass), its DMA overlapping the next chunk.
+int upload_gather(lms_ctx* c, void* d_dst, const unsigned char* const* src, const int64_t* bytes,
+                  int64_t count) {
+  std::vector<int64_t> start(count + 1, 0);
+  for (int64_t k = 0; k < count; ++k) start[k + 1] = start[k] + bytes[k];
+  const int64_t total = start[count];
+  if (total == 0) return LMS_OK;
+  RC_TRY(ensure_stage(c));
+  bool used[2] = {false, false};
+  int slot = 0;
+  int64_t first = 0;  // first piece overlapping the chunk
+  for (int64_t off = 0; off < total; off += (int64_t)kStageChunk, slot ^= 1) {
+    const int64_t len = std::min<int64_t>((int64_t)kStageChunk, total - off);
+    unsigned char* buf = c->stage + slot * kStageChunk;
+    if (used[slot]) CUDA_TRY(cudaEventSynchronize(c->ev_stage[slot]));
+    while (start[first + 1] <= off) ++first;
+    int64_t last = first;
+    while (last + 1 < count && start[last + 1] < off + len) ++last;
+#pragma omp parallel for num_threads(8) schedule(static)
+    for (int64_t k = first; k <= last; ++k) {
+      const int64_t s0 = std::max(start[k], off), s1 = std::min(start[k + 1], off + len);
+      if (s1 > s0) std::memcpy(buf + (s0 - off), src[k] + (s0 - start[k]), (size_t)(s1 - s0));
+    }
+    CUDA_TRY(cudaMemcpyAsync(static_cast<unsigned char*>(d_dst) + off, buf, (size_t)len,
+                             cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(cudaEventRecord(c->ev_stage[slot], c->stream));
+    used[slot] = true;
+  }
+  return LMS_OK;
+}
+
+int lms_ndarray_rows_f64(const uintptr_t* objs, int64_t count, const double** data, int64_t* rows) {
+  // numpy's PyArrayObject_fields (numpy/ndarraytypes.h): after PyObject_HEAD
+  // (refcount, type: 16 bytes) come char* data, int nd, npy_intp* dimensions,
+  // npy_intp* strides -- a stable part of numpy's C ABI
+  if (count < 0 || (count > 0 && (!objs || !data || !rows))) return set_error(LMS_ERR_INVALID, "null argument");
+  for (int64_t k = 0; k < count; ++k) {
+    const unsigned char* o = reinterpret_cast<const unsigned char*>(objs[k]);
+    const char* d = *reinterpret_cast<const char* const*>(o + 16);
+    const int nd = *reinterpret_cast<const int*>(o + 24);
+    const int64_t* dims = *reinterpret_cast<const int64_t* const*>(o + 32);
+    const int64_t* strides = *reinterpret_cast<const int64_t* const*>(o + 40);
+    if (nd != 2 || dims[1] != 2 || (dims[0] > 0 && strides[1] != 8) || (dims[0] > 1 && strides[0] != 16))
+      return set_error(LMS_ERR_INVALID, "set %lld is not a C-contiguous (n, 2) float64 array", (long long)k);
+    data[k] = reinterpret_cast<const double*>(d);
+    rows[k] = dims[0];
+  }
+  return LMS_OK;
+}
+
+int lms_batched_fit_sets_f64(const double* const* sets, const int64_t* counts, const int64_t* q,
+                             int64_t nfits, int device, int32_t* status, lms_candidate* out,
+                             int64_t* contact_offsets, int32_t* contacts, int64_t contact_capacity,
+                             int64_t* ncontacts) {
+  if (nfits < 0 || (nfits > 0 && (!sets || !counts || !q || !status || !out || !contact_offsets ||
+                                  !ncontacts)))
+    return set_error(LMS_ERR_INVALID, "null argument");
+  if (nfits == 0) {
+    if (contact_offsets) contact_offsets[0] = 0;
+    if (ncontacts) *ncontacts = 0;
+    return LMS_OK;
+  }
+  lms_ctx* c = nullptr;
+  RC_TRY(shared_ctx(device, &c));
+  std::lock_guard<std::mutex> lk(c->mu);
+  CUDA_TRY(cudaSetDevice(c->device));
+  std::vector<int64_t> offs(nfits + 1, 0), bytes(nfits);
+  for (int64_t f = 0; f < nfits; ++f) {
+    if (counts[f] < 0 || (counts[f] > 0 && !sets[f])) return set_error(LMS_ERR_INVALID, "bad set %lld", (long long)f);
+    offs[f + 1] = offs[f] + counts[f];
+    bytes[f] = 16 * counts[f];
+  }
+  const int64_t N = offs[nfits];
+  RC_TRY(c->set_xy.need(2 * std::max<int64_t>(N, 1)));
+  RC_TRY(c->a_own.need(std::max<int64_t>(N, 1)));
+  RC_TRY(c->b_own.need(std::max<int64_t>(N, 1)));
+  RC_TRY(c->boffs.need(nfits + 1));
+  RC_TRY(c->set_stats.need(3 * nfits));
+  RC_TRY(upload_gather(c, c->set_xy.p, reinterpret_cast<const unsigned char* const*>(sets), bytes.data(),
+                       nfits));
+  CUDA_TRY(cudaMemcpyAsync(c->boffs.p, offs.data(), sizeof(int64_t) * (nfits + 1),
+                           cudaMemcpyHostToDevice, c->stream));
+  lmsb::launch_split_xy(c->set_xy.p, N, c->a_own.p, c->b_own.p, c->sms, c->stream);
+  lmsb::launch_set_stats(c->a_own.p, c->b_own.p, c->boffs.p, nfits, c->set_stats.p, c->sms, c->stream);
+  CUDA_TRY(cudaGetLastError());
+  std::vector<double> stv(3 * nfits);
+  CUDA_TRY(cudaMemcpyAsync(stv.data(), c->set_stats.p, sizeof(double) * 3 * nfits, cudaMemcpyDeviceToHost,
+                           c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  // solve_lms's checks per set (solver.py:67-80): 1 non-finite, 2 fewer than
+  // 3 points, 3 one distinct x, 4 q outside [2, n]; the caller raises the
+  // first failing set's error
+  bool all_ok = true;
+  for (int64_t f = 0; f < nfits; ++f) {
+    const int64_t n = counts[f];
+    int32_t st = 0;
+    if (n > 0 && stv[3 * f] == 0.0) st = 1;
+    else if (n < 3) st = 2;
+    else if (!(stv[3 * f + 1] < stv[3 * f + 2])) st = 3;
+    else if (q[f] < 2 || q[f] > n) st = 4;
+    status[f] = st;
+    all_ok &= st == 0;
+  }
+  if (!all_ok) return LMS_NOT_FITTED;
+  // bind the device lines; the solver's per-fit magnitudes come from a
+  // second small reduction instead of a host copy of the lines
+  c->a = c->a_own.p;
+  c->b = c->b_own.p;
+  c->nlines = N;
+  c->h_a.clear();
+  c->h_b.clear();
+  ++c->gen;
+  {
+    // per-set max |a| = max(|min x|, |max x|); max |b| from y's range: the
+    // stats kernel again with the arrays swapped (x's stats are on the host)
+    lmsb::launch_set_stats(c->b_own.p, c->a_own.p, c->boffs.p, nfits, c->set_stats.p, c->sms, c->stream);
+    std::vector<double> sty(3 * nfits);
+    CUDA_TRY(cudaMemcpyAsync(sty.data(), c->set_stats.p, sizeof(double) * 3 * nfits, cudaMemcpyDeviceToHost,
+                             c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    c->ext_off.assign(offs.begin(), offs.end() - 1);
+    c->ext_st.resize(4 * nfits);
+    double alo = INFINITY, ahi = -INFINITY, am = 0.0, bm = 0.0;
+    for (int64_t f = 0; f < nfits; ++f) {
+      const double lo = stv[3 * f + 1], hi = stv[3 * f + 2];
+      const double bmx = std::max(std::fabs(sty[3 * f + 1]), std::fabs(sty[3 * f + 2]));
+      c->ext_st[4 * f] = lo;
+      c->ext_st[4 * f + 1] = hi;
+      c->ext_st[4 * f + 2] = std::max(std::fabs(lo), std::fabs(hi));
+      c->ext_st[4 * f + 3] = bmx;
+      alo = std::min(alo, lo);
+      ahi = std::max(ahi, hi);
+      am = std::max(am, c->ext_st[4 * f + 2]);
+      bm = std::max(bm, bmx);
+    }
+    c->s_alo = alo;
+    c->s_ahi = ahi;
+    c->s_am = am;
+    c->s_bm = bm;
+  }
+  RC_TRY(ctx_solve_batch(c, offs.data(), q, nfits, out));
+  RC_TRY(c->bcflags.need(std::max<int64_t>(N, 1)));
+  RC_TRY(c->set_cnt.need(nfits));
+  RC_TRY(c->set_coff.need(nfits + 1));
+  RC_TRY(c->set_contacts.need(std::max<int64_t>(N, 1)));
+  CUDA_TRY(cudaMemcpyAsync(c->boffs.p, offs.data(), sizeof(int64_t) * (nfits + 1),
+                           cudaMemcpyHostToDevice, c->stream));
+  lmsb::launch_contacts_batch(c->a, c->b, c->boffs.p, c->best.p, nfits, c->bcflags.p, c->sms, c->stream);
+  lmsb::launch_contact_compact(c->bcflags.p, c->boffs.p, nfits, c->set_cnt.p, c->set_coff.p,
+                               c->set_contacts.p, c->sms, c->stream);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpyAsync(contact_offsets, c->set_coff.p, sizeof(int64_t) * (nfits + 1),
+                           cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  const int64_t total = contact_offsets[nfits];
+  *ncontacts = total;
+  if (total > contact_capacity) return LMS_OK;  // the caller asks again with room (records kept)
+  if (total > 0 && contacts)
+    CUDA_TRY(cudaMemcpyAsync(contacts, c->set_contacts.p, sizeof(int32_t) * total, cudaMemcpyDeviceToHost,
+                             c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return LMS_OK;
 }
 
 int lms_ctx_solve_batch(lms_ctx* c, const int64_t* offsets, const int64_t* q, int64_t nfits,

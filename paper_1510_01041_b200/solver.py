@@ -145,6 +145,11 @@ def solve_lms_batch(point_sets, q=None) -> list[LmsFit]:
             raise InvalidInputError(f"got {len(qs)} coverages for {len(sets)} point sets")
     if not sets:
         return []
+    if all(type(p) is np.ndarray and p.dtype == np.float64 and p.ndim == 2 and p.shape[1] == 2
+           and p.flags.c_contiguous for p in sets):
+        # the sets stay where they are: the library gathers them into pinned
+        # staging and checks them on the device
+        return _solve_sets(sets, qs, q)
     if all(isinstance(p, np.ndarray) and p.ndim == 2 and p.shape[1] == 2 and p.shape[0] > 0
            for p in sets):
         # fast path: (n, 2) arrays, validated all at once (same checks, same
@@ -220,6 +225,58 @@ def _solve_concat(X: np.ndarray, Y: np.ndarray, offsets: np.ndarray, q, *,
     return _fits_from_arrays(cands, flags, offsets, qv)
 
 
+def _solve_sets(sets, qs, q) -> list[LmsFit]:
+    """solve_lms_batch over C-contiguous (n, 2) float64 arrays through
+    lms_batched_fit_sets_f64 (split over the visible GPUs by contiguous
+    groups of sets); errors as the per-set loop raises them."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from . import _native
+
+    F = len(sets)
+    counts = np.fromiter((p.shape[0] for p in sets), dtype=np.int64, count=F)
+    if q is None:
+        qv = counts // 2 + 1
+    elif isinstance(q, (int, np.integer)):
+        qv = np.full(F, int(q), dtype=np.int64)
+    else:
+        qv = np.array([default_coverage(int(c)) if qq is None else int(qq) for c, qq in zip(counts, qs)],
+                      dtype=np.int64)
+    visible = _native.device_count()
+    if visible == 0:
+        # no GPU: the same errors, checked on the host, before the library
+        # reports that it cannot run
+        for p, qq in zip(sets, qs):
+            validated(p, qq)
+    ndev = max(1, min(visible, F))
+    bounds = np.linspace(0, F, ndev + 1).astype(int)
+
+    def run(d):
+        f0, f1 = int(bounds[d]), int(bounds[d + 1])
+        return _native.batched_fit_sets(sets[f0:f1], qv[f0:f1], device=d)
+
+    if ndev == 1:
+        parts = [run(0)]
+    else:
+        with ThreadPoolExecutor(max_workers=ndev) as pool:
+            parts = list(pool.map(run, range(ndev)))
+    status = np.concatenate([p[0] for p in parts])
+    bad = np.flatnonzero(status)
+    if bad.size:
+        k = int(bad[0])
+        validated(sets[k], qs[k])  # raises the per-set loop's error for the first failing set
+        raise DegenerateInputError("no candidate slab found")
+    cands = np.concatenate([p[1] for p in parts])
+    if not bool(cands["found"].all()):
+        raise DegenerateInputError("no candidate slab found")
+    coff = [parts[0][2]]
+    for p in parts[1:]:
+        coff.append(p[2][1:] + coff[-1][-1])
+    coff = np.concatenate(coff)
+    contacts = np.concatenate([p[3] for p in parts])
+    return _fits_from_contacts(cands, coff, contacts, qv)
+
+
 def _batched_fit_devices(X, Y, offsets, qv):
     """lms_batched_fit_f64 over the visible GPUs: fit groups with about equal
     point counts, one thread per device (the library releases the GIL), the
@@ -246,6 +303,45 @@ def _batched_fit_devices(X, Y, offsets, qv):
     with ThreadPoolExecutor(max_workers=len(fb) - 1) as pool:
         parts = list(pool.map(run, range(len(fb) - 1)))
     return np.concatenate([p[0] for p in parts]), np.concatenate([p[1] for p in parts])
+
+
+def _fits_from_contacts(cands, coff, contacts, qv) -> list[LmsFit]:
+    """_fits_from_arrays with the contact sets already compacted (set-local
+    ascending indices, contacts[coff[k] .. coff[k+1]))."""
+    import gc
+
+    F = coff.size - 1
+    u, vl, vh = cands["u"], cands["v_low"], cands["v_high"]
+    slope = u.tolist()
+    intercept = (-(vl + vh) * 0.5).tolist()
+    half = (vh - vl) * 0.5
+    lms_value = (half * half).tolist()
+    slab = (vh - vl).tolist()
+    local = contacts.tolist()
+    bounds = coff.tolist()
+    cov = np.asarray(qv, dtype=np.int64).tolist()
+    new = object.__new__
+    fits = []
+    was = gc.isenabled()
+    gc.disable()
+    try:
+        for k in range(F):
+            line = new(LineEq)
+            d = line.__dict__
+            d["slope"] = slope[k]
+            d["intercept"] = intercept[k]
+            fit = new(LmsFit)
+            d = fit.__dict__
+            d["line"] = line
+            d["lms_value"] = lms_value[k]
+            d["slab_height"] = slab[k]
+            d["coverage"] = cov[k]
+            d["contact_indices"] = tuple(local[bounds[k]:bounds[k + 1]])
+            fits.append(fit)
+    finally:
+        if was:
+            gc.enable()
+    return fits
 
 
 def _fits_from_arrays(cands, flags, offsets, qv) -> list[LmsFit]:

@@ -973,3 +973,44 @@ def test_split_prepass_matches_single_cta_prepass(n, seed, qf):
     half = total // 2
     assert record_from_native(split.solve(q, half, total)) == record_from_native(
         one.solve(q, half, total))
+
+
+def test_batch_sets_device_validation_matches_per_set_order():
+    """solve_lms_batch over (n, 2) float64 arrays checks the sets on the
+    device (lms_batched_fit_sets_f64): the error raised is the one the
+    per-set validated() loop raises first."""
+    from paper_1510_01041_b200 import solver
+
+    good = np.array([[1.0, 2.0], [2.0, 3.0], [3.0, 5.0], [4.0, 1.0]])
+    cases = [
+        [np.zeros((5, 2)), np.array([[1.0, 2.0], [2.0, 3.0]])],
+        [good, np.array([[1.0, 2.0], [2.0, 3.0]])],
+        [good, np.array([[1.0, 2.0], [np.nan, 1.0], [3.0, 4.0]])],
+        [good, np.array([[1.0, 2.0], [1.0, 1.0], [1.0, 4.0]]), np.zeros((2, 2))],
+        [good, np.array([[1.0, np.inf], [2.0, 1.0], [3.0, 4.0]])],
+        [good, np.zeros((0, 2))],
+    ]
+    for sets in cases:
+        for q in (None, 3, 7):
+            want = None
+            for p in sets:
+                try:
+                    solver.validated(p, q)
+                except ValueError as e:
+                    want = e
+                    break
+            assert want is not None
+            with pytest.raises(ValueError) as ei:
+                solver.solve_lms_batch(sets, q)
+            assert (type(ei.value), str(ei.value)) == (type(want), str(want)), (sets, q)
+
+
+def test_batch_sets_path_equals_single_fits():
+    """The sets path (staged gather upload, device checks, device contact
+    compaction) gives solve_lms's fit for every set, mixed sizes included."""
+    rng = np.random.default_rng(3)
+    sets = [workloads.bench_points(int(n), seed=k) for k, n in enumerate(rng.integers(3, 700, 40))]
+    sets.append(np.ascontiguousarray(rng.integers(0, 9, (300, 2)).astype(float)))
+    fits = lms.solve_lms_batch(sets)
+    for p, f in zip(sets, fits):
+        assert f == lms.solve_lms(p)
