@@ -1175,16 +1175,6 @@ __global__ void __launch_bounds__(kCollectThreads) band_collect_direct_kernel(
   if (qn > 0) drain(qn);
 }
 
-__global__ void band_runs_kernel(const uint32_t* __restrict__ keys, int64_t m,
-                                 int64_t* __restrict__ start, int64_t* __restrict__ end) {
-  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < m;
-       p += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t k = keys[p] >> kSlopeBits;
-    if (p == 0 || (keys[p - 1] >> kSlopeBits) != k) start[k] = p;
-    if (p == m - 1 || (keys[p + 1] >> kSlopeBits) != k) end[k] = p + 1;
-  }
-}
-
 // ------------------------------------------------------------------ n > kBandMaxN
 // The n keys of a band no longer fit shared memory.  Bounds: the keys of a
 // batch of bands are written to global memory, sorted by a CUB segmented
@@ -1453,11 +1443,7 @@ void launch_band_t(const BandFit& bf, const BandArgs& ba, int mode, int grid, cu
   }
 }
 
-int bits_for(int64_t v) {
-  int b = 1;
-  while (b < 32 && ((int64_t)1 << b) <= v) ++b;
-  return b;
-}
+
 
 }  // namespace
 
@@ -1467,11 +1453,31 @@ size_t band_sample_temp_bytes(int64_t S) {
   return bytes;
 }
 
+// grouping buckets: (slot, top slope bits), at most kGroupBuckets
+constexpr int kGroupBuckets = 1 << 14;  // scatter CTA: 12 bytes of shared memory per bucket
+constexpr int kGroupTile = 4096;  // collected vertices per CTA of the bucket passes
+
 size_t band_group_temp_bytes(int64_t m) {
   size_t bytes = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
                                   (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)m);
-  return bytes;
+  return std::max(bytes, (size_t)3 * (kGroupBuckets + 1) * sizeof(int64_t));
+}
+
+int bits_for(int64_t v) {
+  int b = 1;
+  while (b < 32 && ((int64_t)1 << b) <= v) ++b;
+  return b;
+}
+
+__global__ void band_runs_kernel(const uint32_t* __restrict__ keys, int64_t m,
+                                 int64_t* __restrict__ start, int64_t* __restrict__ end) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < m;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t k = keys[p] >> kSlopeBits;
+    if (p == 0 || (keys[p - 1] >> kSlopeBits) != k) start[k] = p;
+    if (p == m - 1 || (keys[p + 1] >> kSlopeBits) != k) end[k] = p + 1;
+  }
 }
 
 size_t band_collect_smem(int K) {
@@ -2021,17 +2027,118 @@ void launch_band_collect_direct(const BandFit& bf, const BandWork& w, const Band
   }
 }
 
-int launch_band_group(const BandWork& w, int64_t m, cudaStream_t st) {
+// Grouping of the collected vertices by (slot, top slope bits): one bucket
+// (counting) sort instead of a full radix sort of the keys -- the filter only
+// needs every group contiguous and its chunks slope-local (each chunk takes
+// its own slope extent from its members), not the order inside a bucket.
+// Pass 1: per-CTA shared-memory histograms added into global counts; one CTA
+// scans them (and writes each slot's [start, end)); pass 2: per-CTA
+// histograms again, one global reservation per (CTA, bucket), members
+// scattered to their reserved ranges.
+__global__ void __launch_bounds__(1024) group_hist_kernel(const uint32_t* __restrict__ keys, int64_t m,
+                                                          int shift, int nb,
+                                                          unsigned long long* __restrict__ counts) {
+  extern __shared__ unsigned int gh[];
+  for (int e = threadIdx.x; e < nb; e += blockDim.x) gh[e] = 0u;
+  __syncthreads();
+  for (int64_t p = (int64_t)blockIdx.x * kGroupTile + threadIdx.x;
+       p < m && p < (int64_t)(blockIdx.x + 1) * kGroupTile; p += blockDim.x)
+    atomicAdd(&gh[keys[p] >> shift], 1u);
+  __syncthreads();
+  for (int e = threadIdx.x; e < nb; e += blockDim.x)
+    if (gh[e]) atomicAdd(&counts[e], (unsigned long long)gh[e]);
+}
+
+__global__ void __launch_bounds__(1024) group_scan_kernel(const unsigned long long* __restrict__ counts,
+                                                          int nb, int per_slot, int nslot,
+                                                          unsigned long long* __restrict__ cursor,
+                                                          int64_t* __restrict__ start,
+                                                          int64_t* __restrict__ end) {
+  __shared__ int64_t part[1024];
+  const int per = (nb + 1023) / 1024;
+  const int b0 = threadIdx.x * per, b1 = b0 + per < nb ? b0 + per : nb;
+  int64_t sum = 0;
+  for (int b = b0; b < b1; ++b) sum += (int64_t)counts[b];
+  part[threadIdx.x] = sum;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {
+    const int64_t v = threadIdx.x >= off ? part[threadIdx.x - off] : 0;
+    __syncthreads();
+    part[threadIdx.x] += v;
+    __syncthreads();
+  }
+  int64_t run = threadIdx.x ? part[threadIdx.x - 1] : 0;
+  for (int b = b0; b < b1; ++b) {
+    cursor[b] = (unsigned long long)run;
+    if (b % per_slot == 0) start[b / per_slot] = run;
+    run += (int64_t)counts[b];
+    if ((b + 1) % per_slot == 0) end[b / per_slot] = run;
+  }
+  (void)nslot;
+}
+
+__global__ void __launch_bounds__(1024) group_scatter_kernel(const uint32_t* __restrict__ keys,
+                                                             const uint32_t* __restrict__ vals, int64_t m,
+                                                             int shift, int nb,
+                                                             unsigned long long* __restrict__ cursor,
+                                                             uint32_t* __restrict__ out) {
+  extern __shared__ unsigned int gh[];  // [nb] counts, then [nb] bases (64-bit)
+  unsigned long long* base = reinterpret_cast<unsigned long long*>(gh + ((nb + 1) & ~1));
+  for (int e = threadIdx.x; e < nb; e += blockDim.x) gh[e] = 0u;
+  __syncthreads();
+  const int64_t t0 = (int64_t)blockIdx.x * kGroupTile;
+  const int64_t t1 = t0 + kGroupTile < m ? t0 + kGroupTile : m;
+  for (int64_t p = t0 + threadIdx.x; p < t1; p += blockDim.x) atomicAdd(&gh[keys[p] >> shift], 1u);
+  __syncthreads();
+  for (int e = threadIdx.x; e < nb; e += blockDim.x) {
+    base[e] = gh[e] ? atomicAdd(&cursor[e], (unsigned long long)gh[e]) : 0ull;
+    gh[e] = 0u;
+  }
+  __syncthreads();
+  for (int64_t p = t0 + threadIdx.x; p < t1; p += blockDim.x) {
+    const int b = (int)(keys[p] >> shift);
+    out[base[b] + atomicAdd(&gh[b], 1u)] = vals[p];
+  }
+}
+
+int launch_band_group(const BandWork& w, int64_t m, bool full_order, cudaStream_t st) {
   cudaMemsetAsync(w.start, 0, sizeof(int64_t) * w.nslot, st);
   cudaMemsetAsync(w.end, 0, sizeof(int64_t) * w.nslot, st);
   if (m <= 0) return 0;
-  size_t bytes = w.temp_bytes;
-  if (cub::DeviceRadixSort::SortPairs(w.temp, bytes, w.ckeys, w.ckeys_alt, w.cvals, w.members,
-                                      (int)m, 0, kSlopeBits + bits_for(w.nslot - 1), st) !=
-      cudaSuccess)
-    return -1;
-  band_runs_kernel<<<(int)std::min<int64_t>((m + 255) / 256, 4096), 256, 0, st>>>(
-      w.ckeys_alt, m, w.start, w.end);
+  if (full_order) {
+    // n <= kBandMaxN: the filter's chunks are cut from the members in full
+    // slope order (17 bits within the band) -- inside a band the members
+    // crowd near the optimum slope, where coarser buckets would give chunks
+    // 10x wider extents (12x the survivors measured)
+    size_t bytes = w.temp_bytes;
+    if (cub::DeviceRadixSort::SortPairs(w.temp, bytes, w.ckeys, w.ckeys_alt, w.cvals, w.members,
+                                        (int)m, 0, kSlopeBits + bits_for(w.nslot - 1), st) !=
+        cudaSuccess)
+      return -1;
+    band_runs_kernel<<<(int)std::min<int64_t>((m + 255) / 256, 4096), 256, 0, st>>>(
+        w.ckeys_alt, m, w.start, w.end);
+    return 0;
+  }
+  // slope bits kept per slot: as many as fit kGroupBuckets buckets (<= 8)
+  int sb = 8;
+  while (sb > 0 && ((int64_t)w.nslot << sb) > kGroupBuckets) --sb;
+  const int shift = kSlopeBits - sb;
+  const int per_slot = 1 << sb;
+  const int nb = w.nslot * per_slot;
+  if ((size_t)3 * (nb + 1) * sizeof(int64_t) > w.temp_bytes) return -1;
+  unsigned long long* counts = reinterpret_cast<unsigned long long*>(w.temp);
+  unsigned long long* cursor = counts + (nb + 1);
+  cudaMemsetAsync(counts, 0, sizeof(unsigned long long) * nb, st);
+  const int tiles = (int)((m + kGroupTile - 1) / kGroupTile);
+  static DeviceOnce d1, d2;
+  const size_t smem1 = (size_t)nb * sizeof(unsigned);
+  const size_t smem2 = (size_t)((nb + 1) & ~1) * sizeof(unsigned) + (size_t)nb * sizeof(unsigned long long);
+  if (smem2 > 200 * 1024) return -1;
+  set_max_smem(group_hist_kernel, 200 * 1024, d1);
+  set_max_smem(group_scatter_kernel, 200 * 1024, d2);
+  group_hist_kernel<<<tiles, 1024, smem1, st>>>(w.ckeys, m, shift, nb, counts);
+  group_scan_kernel<<<1, 1024, 0, st>>>(counts, nb, per_slot, w.nslot, cursor, w.start, w.end);
+  group_scatter_kernel<<<tiles, 1024, smem2, st>>>(w.ckeys, w.cvals, m, shift, nb, cursor, w.members);
   return 0;
 }
 

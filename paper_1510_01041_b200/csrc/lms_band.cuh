@@ -178,7 +178,9 @@ void launch_band_seeds(const BandFit& bf, const BandWork& w, int64_t* ranks, int
                        int32_t fit, int64_t cap, unsigned long long* count, cudaStream_t st);
 void launch_band_collect(const BandFit& bf, const BandWork& w, const BandRuns& runs, int64_t cap,
                          int sms, cudaStream_t st);
-int launch_band_group(const BandWork& w, int64_t m, cudaStream_t st);
+// group the collected vertices by slot: full_order sorts by (slot, slope
+// position) (radix sort), else buckets of (slot, top 8 slope bits)
+int launch_band_group(const BandWork& w, int64_t m, bool full_order, cudaStream_t st);
 size_t band_direct_smem(int K, int nsub, int nadm);
 void launch_band_collect_direct(const BandFit& bf, const BandWork& w, const BandRuns& runs,
                                 const BandDirect& dg, int sms, cudaStream_t st);

@@ -1589,7 +1589,7 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   w.members = c->bmem.p;
   w.temp = c->btemp.p;
   w.temp_bytes = (size_t)c->btemp.cap;
-  if (lmsb::launch_band_group(w, (int64_t)m, c->stream) != 0)
+  if (lmsb::launch_band_group(w, (int64_t)m, !big, c->stream) != 0)
     return set_error(LMS_ERR_CUDA, "band grouping sort failed");
   CUDA_TRY(cudaGetLastError());
   st->launches += 3;
