@@ -228,6 +228,9 @@ struct SweepArgs {
   unsigned long long* count;
   int smem_tables;        // (launcher) boundaries and slots staged in shared memory
   unsigned long long* dbg;  // optional: per run, pairs enumerated (LMSB_SWEEP_DEBUG)
+  unsigned long long* raw;  // enumerated (run << 32 | pair) entries, raw_cap of them
+  int64_t raw_cap;
+  unsigned long long* raw_count;
 };
 size_t sweep_chunk_smem();
 // sort nseg segments of the n lines by their end keys; returns launches

@@ -305,7 +305,7 @@ struct lms_ctx {
   DevBuf<uint32_t> sw_idx;
   DevBuf<int32_t> sw_pos, sw_P, sw_bmin, sw_suf, sw_rk;
   DevBuf<lmsb::SweepEnd> sw_ends;
-  DevBuf<unsigned long long> sw_dbg;
+  DevBuf<unsigned long long> sw_dbg, sw_raw, sw_rawcnt;
   DevBuf<unsigned long long> small_cnt;
   int small_mode = 1;  // LMSB_SMALL: 0 off, 1 batches, 2 also single fits
   DevBuf<float2> blines32;
@@ -480,6 +480,8 @@ void ctx_release(lms_ctx* c) {
   c->sw_rk.release();
   c->sw_ends.release();
   c->sw_dbg.release();
+  c->sw_raw.release();
+  c->sw_rawcnt.release();
   c->dt_peaks.release();
   c->dt_offs.release();
   c->dt_soffs.release();
@@ -1555,6 +1557,11 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
       sa.out_keys = w.ckeys;
       sa.out_vals = w.cvals;
       sa.cap = cap;
+      RC_TRY(c->sw_raw.need(cap));
+      RC_TRY(c->sw_rawcnt.need(1));
+      sa.raw = c->sw_raw.p;
+      sa.raw_cap = cap;
+      sa.raw_count = c->sw_rawcnt.p;
       CUDA_TRY(cudaEventRecord(c->ev_chunk[10], c->stream));
       lmsb::launch_sweep_emit(bf, sa, c->sms, c->stream);
       CUDA_TRY(cudaEventRecord(c->ev_chunk[11], c->stream));

@@ -56,8 +56,9 @@ constexpr int kMergeThreads = 256;
 constexpr int kEnumThreads = 256;
 constexpr int kEnumWarps = kEnumThreads / 32;
 constexpr int kEnumQueue = 64;
-constexpr int kOutBuf = 128;
+constexpr int kOutBuf = 512;  // per-warp raw-pair buffer (one global atomic per ~480 pairs)
 constexpr int kOutFlush = kOutBuf - 32;
+constexpr int kClsBuf = 4096;  // per-CTA member buffer of the classification
 constexpr int kHitBatch = 4;
 
 __device__ __forceinline__ int64_t i64min(int64_t x, int64_t y) { return x < y ? x : y; }
@@ -321,33 +322,23 @@ __global__ void __launch_bounds__(kEnumThreads, 4) sweep_enum_kernel(BandFit bf,
   auto flush_out = [&]() {
     if (on == 0) return;
     unsigned long long b0 = 0;
-    if (lane == 0) b0 = atomicAdd(sa.count, (unsigned long long)on);
+    if (lane == 0) b0 = atomicAdd(sa.raw_count, (unsigned long long)on);
     b0 = __shfl_sync(0xffffffffu, b0, 0);
     for (int e = lane; e < on; e += 32) {
       const unsigned long long pos = b0 + e;
-      if ((int64_t)pos < sa.cap) {
-        sa.out_keys[pos] = ok[e];
-        sa.out_vals[pos] = ov[e];
-      }
+      if ((int64_t)pos < sa.raw_cap) sa.raw[pos] = ((unsigned long long)ov[e] << 32) | ok[e];
     }
     __syncwarp();
     on = 0;
   };
+  // the enumerated pairs go out raw (run, pair) -- classified by
+  // sweep_classify_kernel, a thread per pair with all its loads in flight
   auto drain = [&](int cnt) {
-    uint32_t key = 0, val = 0;
-    bool take = false;
     if (lane < cnt) {
-      const uint32_t e = q[lane];
-      take = sweep_take(bf, sa, bnd, slot, k0, k1, false, (int)(e >> 16), (int)(e & 0xFFFF), &key,
-                        &val);
+      ok[on + lane] = q[lane];
+      ov[on + lane] = (uint32_t)cur_run;
     }
-    const unsigned mask = __ballot_sync(0xffffffffu, take);
-    if (take) {
-      const int at = on + __popc(mask & ((1u << lane) - 1u));
-      ok[at] = key;
-      ov[at] = val;
-    }
-    on += __popc(mask);
+    on += cnt;
     __syncwarp();
     if (on >= kOutFlush) flush_out();
   };
@@ -424,6 +415,77 @@ __global__ void __launch_bounds__(kEnumThreads, 4) sweep_enum_kernel(BandFit bf,
   flush_out();
 }
 
+// Classification of the enumerated pairs: the reference's slope, the band,
+// ownership by the pair's run (sweep_take); members appended per warp.
+__global__ void __launch_bounds__(256) sweep_classify_kernel(BandFit bf, SweepArgs sa) {
+  extern __shared__ __align__(16) unsigned char cl_dyn[];
+  const float* bnd = sa.bounds;
+  const int16_t* slot = sa.slot;
+  if (sa.smem_tables) {
+    float* sb = reinterpret_cast<float*>(cl_dyn);
+    int16_t* ss = reinterpret_cast<int16_t*>(sb + sa.K);
+    for (int e = threadIdx.x; e <= sa.K; e += blockDim.x) {
+      if (e < sa.K - 1) sb[e] = sa.bounds[e];
+      ss[e] = sa.slot[e];
+    }
+    __syncthreads();
+    bnd = sb;
+    slot = ss;
+  }
+  // members staged per CTA, appended with one global atomic per flush
+  __shared__ uint32_t bkey[kClsBuf], bval[kClsBuf];
+  __shared__ unsigned bn;
+  __shared__ unsigned long long bbase;
+  if (threadIdx.x == 0) bn = 0;
+  __syncthreads();
+  auto flush = [&]() {
+    __syncthreads();
+    const unsigned m = bn;
+    if (threadIdx.x == 0 && m) bbase = atomicAdd(sa.count, (unsigned long long)m);
+    __syncthreads();
+    for (unsigned e = threadIdx.x; e < m; e += blockDim.x) {
+      const unsigned long long pos = bbase + e;
+      if ((int64_t)pos < sa.cap) {
+        sa.out_keys[pos] = bkey[e];
+        sa.out_vals[pos] = bval[e];
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) bn = 0;
+    __syncthreads();
+  };
+  int64_t cnt = (int64_t)*sa.raw_count;
+  if (cnt > sa.raw_cap) cnt = sa.raw_cap;
+  const int64_t step = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t p0 = (int64_t)blockIdx.x * blockDim.x; p0 < cnt; p0 += step) {
+    const int64_t p = p0 + threadIdx.x;
+    uint32_t key = 0, val = 0;
+    bool take = false;
+    if (p < cnt) {
+      const unsigned long long e = sa.raw[p];
+      const int r = (int)(e >> 32);
+      const uint32_t pr = (uint32_t)e;
+      take = sweep_take(bf, sa, bnd, slot, sa.run_k0[r], sa.run_k1[r], false, (int)(pr >> 16),
+                        (int)(pr & 0xFFFF), &key, &val);
+    }
+    if (take) {
+      const unsigned at = atomicAdd(&bn, 1u);
+      bkey[at] = key;
+      bval[at] = val;
+    }
+    __syncthreads();
+    if (bn > kClsBuf - 256) flush();  // (uniform: bn read after the barrier)
+  }
+  flush();
+}
+
+// a raw-buffer overflow makes the member count exceed its capacity (the
+// caller grows both and enumerates again)
+__global__ void sweep_overflow_kernel(SweepArgs sa) {
+  const unsigned long long raw = *sa.raw_count;
+  if ((int64_t)raw > sa.raw_cap && *sa.count < raw) *sa.count = raw;
+}
+
 // Nearly parallel pairs (0 < |a_i - a_j| <= tau): lines sorted by a, each
 // against the following lines with a larger slope within tau.
 __global__ void sweep_parallel_kernel(BandFit bf, SweepArgs sa) {
@@ -488,11 +550,16 @@ void launch_sweep_prepare(int n, int nruns, const SweepSort& ss, int32_t* pos, i
 
 void launch_sweep_emit(const BandFit& bf, const SweepArgs& sa, int sms, cudaStream_t st) {
   cudaMemsetAsync(sa.count, 0, sizeof(unsigned long long), st);
+  cudaMemsetAsync(sa.raw_count, 0, sizeof(unsigned long long), st);
   if (sa.nruns > 0) {
     const size_t tab = (size_t)sa.K * sizeof(float) + (size_t)(sa.K + 1) * sizeof(int16_t) + 16;
     SweepArgs a2 = sa;
     a2.smem_tables = tab <= 24 * 1024;
-    sweep_enum_kernel<<<sms * 8, kEnumThreads, a2.smem_tables ? tab : 0, st>>>(bf, a2);
+    SweepArgs ae = a2;
+    ae.smem_tables = 0;  // the enumeration does not classify
+    sweep_enum_kernel<<<sms * 8, kEnumThreads, 0, st>>>(bf, ae);
+    sweep_classify_kernel<<<sms * 4, 256, a2.smem_tables ? tab : 0, st>>>(bf, a2);
+    sweep_overflow_kernel<<<1, 1, 0, st>>>(a2);
   }
   if (sa.tau > 0.0 && sa.k1a)
     sweep_parallel_kernel<<<(int)((bf.n + 255) / 256), 256, 0, st>>>(bf, sa);
