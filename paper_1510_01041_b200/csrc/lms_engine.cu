@@ -3001,11 +3001,32 @@ int lms_ctx_solve_distributed(lms_ctx* c, int64_t q, lms_candidate* out) {
   const int R = c->comm_ranks, r = c->comm_rank;
   lms_candidate seed{}, mine{};
   int64_t nb = 0;
-  RC_TRY(owned_plan(c, q, R, r, &seed, &nb));
+  // every rank joins both collectives whatever happens locally (a failed
+  // rank sends a record with reserved = -1, so no peer waits forever and
+  // every rank reports the failure)
+  int rc = owned_plan(c, q, R, r, &seed, &nb);
+  std::string err = rc != LMS_OK ? std::string(lms_last_error()) : std::string();
   std::vector<lms_candidate> all(R);
+  if (rc != LMS_OK) {
+    seed = lms_candidate{};
+    seed.reserved = -1;
+  }
   RC_TRY(nccl_gather_records(c, seed, all.data()));
-  RC_TRY(owned_search(c, q, R, r, nb, cand_min(all.data(), R), &mine));
+  bool peer_failed = false;
+  for (int k = 0; k < R; ++k) peer_failed |= all[k].reserved == -1;
+  if (rc == LMS_OK && !peer_failed) {
+    rc = owned_search(c, q, R, r, nb, cand_min(all.data(), R), &mine);
+    if (rc != LMS_OK) err = lms_last_error();
+  }
+  if (rc != LMS_OK || peer_failed) {
+    mine = lms_candidate{};
+    mine.reserved = -1;
+  }
   RC_TRY(nccl_gather_records(c, mine, all.data()));
+  for (int k = 0; k < R; ++k) peer_failed |= all[k].reserved == -1;
+  if (rc != LMS_OK) return set_error(rc, "%s", err.c_str());
+  if (peer_failed) return set_error(LMS_ERR_CUDA, "a peer rank of the sharded search failed");
+  for (auto& x : all) x.reserved = 0;
   *out = cand_min(all.data(), R);
   return LMS_OK;
 }
