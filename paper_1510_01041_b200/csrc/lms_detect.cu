@@ -148,7 +148,8 @@ __global__ void __launch_bounds__(kVoteThreads) img_vote_kernel(DetectImage im, 
   double* wedge = reinterpret_cast<double*>(hist + ((nbins + 1) & ~1));  // after the histogram
   for (int b = threadIdx.x; b < g.n_rho; b += blockDim.x) wedge[b] = wedge_g[b];
   for (int t = threadIdx.x; t < g.n_theta; t += blockDim.x)
-    trig[t] = Trig{(float)cos_t[t], (float)sin_t[t], cos_t[t], sin_t[t]};
+    trig[t] = Trig{(float)cos_t[t], (float)sin_t[t], cos_t[t], sin_t[t],
+                   cos_t[t] != 0.0 ? 1.0 / cos_t[t] : 0.0};
   for (int e = threadIdx.x; e < nbins; e += blockDim.x) hist[e] = 0u;
   const float rho_max32 = (float)g.rho_max;
   const float inv_drho32 = (float)(1.0 / g.drho);
@@ -211,8 +212,9 @@ __global__ void __launch_bounds__(kVoteThreads) img_vote_kernel(DetectImage im, 
       const int dir = b1 >= b0 ? 1 : -1;
       const int T = (b1 - b0) * dir;  // bin changes along the row
       const double ys = __dmul_rn((double)y, tr.s);
+      const int Wi = (int)W;
       // w(x) = fl(fl(fl(x c) + fl(y s)) + rho_max): bin(x) >= b  <=>  w(x) >= wedge[b]
-      auto wof = [&](int64_t x) { return __dadd_rn(__dadd_rn(__dmul_rn((double)x, tr.c), ys), g.rho_max); };
+      auto wof = [&](int x) { return __dadd_rn(__dadd_rn(__dmul_rn((double)x, tr.c), ys), g.rho_max); };
       int64_t carry = 0;  // start of the segment of bin b0 + dir * k0 (k0 = first k of this round)
       for (int k0 = 0; k0 <= T; k0 += 32) {
         const int k = k0 + lane;  // this lane: the segment of bin b0 + dir * k, [x_k, x_{k+1})
@@ -222,32 +224,34 @@ __global__ void __launch_bounds__(kVoteThreads) img_vote_kernel(DetectImage im, 
           const int target = b0 + dir * (k + 1);
           // up: bin >= target <=> w >= wedge[target]; down: bin <= target <=> w < wedge[target + 1]
           const double wt = dir > 0 ? wedge[target] : wedge[target + 1];
-          auto beyond = [&](int64_t x) { return dir > 0 ? wof(x) >= wt : wof(x) < wt; };
-          const double edge = -g.rho_max + (dir > 0 ? target : target + 1) * g.drho;
-          const double xp = (edge - ys) / tr.c;
-          int64_t lo = 1, hi = W - 1;  // beyond(W - 1) holds, beyond(0) does not
-          bool found = false;
-          if (xp == xp && fabs(xp) < 4.0e18) {
-            const int64_t xg = (int64_t)fmin(fmax(ceil(xp), 1.0), (double)(W - 1));
-            for (int d = 0; d <= 2 && !found; ++d) {
-              const int64_t cand[2] = {xg - d, xg + d};
-              for (int c2 = 0; c2 < (d ? 2 : 1) && !found; ++c2) {
-                const int64_t xc = cand[c2];
-                if (xc >= 1 && xc <= W - 1 && beyond(xc) && !beyond(xc - 1)) {
-                  xe = xc;
-                  found = true;
-                }
-              }
+          auto beyond = [&](int x) { return dir > 0 ? wof(x) >= wt : wof(x) < wt; };
+          // predicted crossing (real arithmetic), then the exact test walks to
+          // it: beyond(W - 1) holds, beyond(0) does not
+          const double xp = (wt - g.rho_max - ys) * tr.ic;
+          int x = (xp == xp && fabs(xp) < 1.0e9) ? (int)fmin(fmax(ceil(xp), 1.0), (double)(Wi - 1))
+                                                 : Wi / 2;
+          int steps = 0;
+          if (beyond(x)) {
+            while (x > 1 && steps < 4 && beyond(x - 1)) {
+              --x;
+              ++steps;
+            }
+          } else {
+            while (steps < 4 && !beyond(x)) {
+              ++x;
+              ++steps;
             }
           }
-          if (!found) {
+          if (steps == 4) {  // prediction off: bisection over the row
+            int lo = 1, hi = Wi - 1;
             while (lo < hi) {
-              const int64_t mid = (lo + hi) >> 1;
+              const int mid = (lo + hi) >> 1;
               if (beyond(mid)) hi = mid;
               else lo = mid + 1;
             }
-            xe = lo;
+            x = lo;
           }
+          xe = x;
         }
         int64_t xs = __shfl_up_sync(0xffffffffu, xe, 1);
         if (lane == 0) xs = carry;
@@ -373,7 +377,7 @@ __device__ __forceinline__ void member_segment(const StripArgs& sa, int slot, in
   const bool top = rb + 1 >= sa.g.n_rho;
   const double wlo = sa.wedge[rb];                      // bin >= rb  <=>  w >= wlo (rb >= 1)
   const double whi = top ? INFINITY : sa.wedge[rb + 1];  // bin >= rb + 1  <=>  w >= whi
-  const double inv_c = 1.0 / tr.c;
+  const double inv_c = tr.ic;
   if (tr.c >= 0.0) {  // bins non-decreasing in x
     *xa = rb == 0 ? 0 : first_true(sa.W, (wlo - sa.g.rho_max - ys) * inv_c, [&](int64_t x) { return w_at(x) >= wlo; });
     *xb = top ? sa.W : first_true(sa.W, (whi - sa.g.rho_max - ys) * inv_c, [&](int64_t x) { return w_at(x) >= whi; });

@@ -42,6 +42,7 @@ int64_t detect_support_rows(int64_t npix, int64_t width);
 struct Trig {
   float c32, s32;
   double c, s;
+  double ic;  // 1 / c (0 when c == 0): predictions only, never a decision
 };
 // The peaks grouped by their support trig (one slot per distinct theta bin;
 // slot s holds peak[first[s] .. first[s + 1]) with their rho bins), built on

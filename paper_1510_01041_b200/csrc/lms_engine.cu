@@ -3235,7 +3235,8 @@ int lms_detect_supports_u8(const double* cos_s, const double* sin_s, const uint8
     tb.nslot = (int)slot_tb.size();
     for (int sl = 0; sl < tb.nslot; ++sl) {
       const int t = slot_tb[sl];
-      tb.trig[sl] = lmsb::Trig{(float)cos_s[t], (float)sin_s[t], cos_s[t], sin_s[t]};
+      tb.trig[sl] = lmsb::Trig{(float)cos_s[t], (float)sin_s[t], cos_s[t], sin_s[t],
+                               cos_s[t] != 0.0 ? 1.0 / cos_s[t] : 0.0};
       tb.first[sl] = m;
       for (int k = 0; k < P; ++k)
         if ((int)pin[3 * k + 1] == t) {
