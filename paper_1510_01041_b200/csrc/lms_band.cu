@@ -262,6 +262,10 @@ __global__ void __launch_bounds__(kThreads, 1) band_bound_kernel(BandFit bf, Ban
   const double dmax = bf.dev * fmax(uR - uM, uM - uL) * (1.0 + 0x1p-40);
   band_keys<kThreads, kItems>(bf, uM, sh);
   const int n = (int)bf.n, q = (int)bf.q;
+  if (ba.bkeys) {  // kept for the filter (row padded to a multiple of 4 keys)
+    float* row = ba.bkeys + (int64_t)band * ba.bkeys_ld;
+    for (int k = threadIdx.x; k < ba.bkeys_ld; k += kThreads) row[k] = k < n ? sh.keys[k] : INFINITY;
+  }
   double w = INFINITY;
   for (int k = threadIdx.x; k + q - 1 < n; k += kThreads)
     w = fmin(w, (double)sh.keys[k + q - 1] - (double)sh.keys[k]);
@@ -396,20 +400,30 @@ __global__ void __launch_bounds__(kThreads, 1) band_filter_kernel(BandFit bf, Ba
   SH& sh = *reinterpret_cast<SH*>(band_smem);
   const int tid = threadIdx.x;
   const int lane = tid & 31;
-  // chunk -> (listed band, chunk index)
+  // chunk -> (band, member range): the explicit chunk table, or (listed
+  // group, chunk index) from the groups' chunk prefix
   const int64_t cidx = blockIdx.x;
-  if (cidx >= ba.chunk_prefix[ba.nlist]) return;
-  int lo = 0, hi = ba.nlist - 1;  // largest e with chunk_prefix[e] <= cidx
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (ba.chunk_prefix[mid] <= cidx) lo = mid;
-    else hi = mid - 1;
+  int band;
+  int64_t m0, m1;
+  if (ba.ctab) {
+    if (cidx >= (int64_t)*ba.nctab) return;
+    band = ba.cband[cidx];
+    m0 = ba.ctab[2 * cidx];
+    m1 = ba.ctab[2 * cidx + 1];
+  } else {
+    if (cidx >= ba.chunk_prefix[ba.nlist]) return;
+    int lo = 0, hi = ba.nlist - 1;  // largest e with chunk_prefix[e] <= cidx
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (ba.chunk_prefix[mid] <= cidx) lo = mid;
+      else hi = mid - 1;
+    }
+    const int grp = ba.list[lo];
+    band = ba.group_band ? ba.group_band[grp] : grp;
+    const int64_t cs = chunk_size(ba.end[grp] - ba.start[grp], ba.chunk, !ba.chunk_fixed);
+    m0 = ba.start[grp] + (cidx - ba.chunk_prefix[lo]) * cs;
+    m1 = min(ba.end[grp], m0 + cs);
   }
-  const int grp = ba.list[lo];
-  const int band = ba.group_band ? ba.group_band[grp] : grp;
-  const int64_t cs = chunk_size(ba.end[grp] - ba.start[grp], ba.chunk, true);
-  const int64_t m0 = ba.start[grp] + (cidx - ba.chunk_prefix[lo]) * cs;
-  const int64_t m1 = min(ba.end[grp], m0 + cs);
   if (m1 <= m0) return;
   double H = INFINITY;
   {
@@ -419,7 +433,23 @@ __global__ void __launch_bounds__(kThreads, 1) band_filter_kernel(BandFit bf, Ba
   bool all = band >= ba.K;  // the beyond-range pseudo band: every member survives
   if (!all && ba.lb[band] > H * (1.0 + 0x1p-19)) return;  // H tightened since collection
   double uL = 0.0, uR = 0.0;
-  if (!all) {
+  const float* K = sh.keys;
+  const int n = (int)bf.n, q = (int)bf.q;
+  double uM = 0.0;
+  // inner band with stored keys: its sorted keys at the band centre (the
+  // padding D = dev |u - uM| is valid for any uM; the chunk's own centre
+  // measured no fewer survivors), no sort and no chunk bound here
+  bool stored = false;
+  if (!all && ba.bkeys && boundary_extent(ba.bounds, ba.K, band, &uL, &uR) &&
+      keys_in_range(bf, uL, uR) && bf.dev * (uR - uL) <= ba.bkeys_tau * H) {
+    stored = true;
+    uM = 0.5 * uL + 0.5 * uR;
+    const float4* src = reinterpret_cast<const float4*>(ba.bkeys + (int64_t)band * ba.bkeys_ld);
+    float4* dst = reinterpret_cast<float4*>(sh.keys);
+    for (int k = tid; k < (int)(ba.bkeys_ld >> 2); k += kThreads) dst[k] = __ldg(src + k);
+    __syncthreads();
+  }
+  if (!all && !stored) {
     double l = INFINITY, h = -INFINITY;
     for (int64_t s = m0 + tid; s < m1; s += kThreads) {
       const uint32_t p = ba.members[s];
@@ -432,10 +462,8 @@ __global__ void __launch_bounds__(kThreads, 1) band_filter_kernel(BandFit bf, Ba
     uR = -block_min<kThreads>(-h, sh.red[1]);
     all = !(isfinite(uL) && isfinite(uR)) || !keys_in_range(bf, uL, uR);
   }
-  const double uM = 0.5 * uL + 0.5 * uR;
-  const float* K = sh.keys;
-  const int n = (int)bf.n, q = (int)bf.q;
-  if (!all) {
+  if (!all && !stored) {
+    uM = 0.5 * uL + 0.5 * uR;
     band_keys<kThreads, kItems>(bf, uM, sh);
     // the chunk's own lower bound (as band_bound_kernel, with its narrower extent)
     double w = INFINITY;
@@ -1498,8 +1526,9 @@ int launch_band_sample(const BandFit& bf, const BandWork& w, int sms, cudaStream
 
 void launch_band(const BandFit& bf, const BandArgs& ba, int mode, int grid, cudaStream_t st) {
   if (grid <= 0) return;
-  if (mode == 1)
-    band_chunks_kernel<<<1, 32, 0, st>>>(ba.list, ba.nlist, ba.start, ba.end, ba.chunk, true,
+  if (mode == 1 && !ba.ctab)
+    band_chunks_kernel<<<1, 32, 0, st>>>(ba.list, ba.nlist, ba.start, ba.end, ba.chunk,
+                                         !ba.chunk_fixed,
                                          ba.chunk_prefix);
   if (bf.n <= 1024) launch_band_t<256, 4>(bf, ba, mode, grid, st);
   else if (bf.n <= 4096) launch_band_t<512, 8>(bf, ba, mode, grid, st);
@@ -2140,6 +2169,207 @@ int launch_band_group(const BandWork& w, int64_t m, bool full_order, cudaStream_
   group_scan_kernel<<<1, 1024, 0, st>>>(counts, nb, per_slot, w.nslot, cursor, w.start, w.end);
   group_scatter_kernel<<<tiles, 1024, smem2, st>>>(w.ckeys, w.cvals, m, shift, nb, cursor, w.members);
   return 0;
+}
+
+// ---- sub-band grouping: counting sort of the collected members by group
+// key, the member count read on the device (no host round trip for it).
+// Pass 1 (sub_hist_kernel): per-CTA shared-memory histograms over a
+// grid-stride range, added into the global counts once per CTA; one CTA
+// scans them into group ranges and cursors (and clears the counts); pass 2
+// (sub_scatter_kernel): per tile a shared-memory histogram, one global
+// reservation per (tile, group), members scattered into the reservations.
+constexpr int kSubTile = 4096;
+
+__device__ __forceinline__ int64_t sub_count(const unsigned long long* m, int64_t cap) {
+  const int64_t v = (int64_t)*m;
+  return v < cap ? v : cap;
+}
+
+__global__ void __launch_bounds__(1024) sub_hist_kernel(const uint32_t* __restrict__ keys,
+                                                        const unsigned long long* __restrict__ dm,
+                                                        int64_t cap, int nb,
+                                                        unsigned long long* __restrict__ counts) {
+  extern __shared__ unsigned int sh_hist[];
+  for (int e = threadIdx.x; e < nb; e += blockDim.x) sh_hist[e] = 0u;
+  __syncthreads();
+  const int64_t m = sub_count(dm, cap);
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < m;
+       p += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&sh_hist[min(keys[p], (uint32_t)(nb - 1))], 1u);
+  __syncthreads();
+  for (int e = threadIdx.x; e < nb; e += blockDim.x)
+    if (sh_hist[e]) atomicAdd(&counts[e], (unsigned long long)sh_hist[e]);
+}
+
+__global__ void __launch_bounds__(1024) sub_scan_kernel(unsigned long long* __restrict__ counts,
+                                                        int nb,
+                                                        unsigned long long* __restrict__ cursor,
+                                                        int64_t* __restrict__ start,
+                                                        int64_t* __restrict__ end) {
+  __shared__ unsigned long long part[1024];
+  const int per = (nb + 1023) / 1024;
+  const int b0 = min((int)threadIdx.x * per, nb), b1 = min(b0 + per, nb);
+  unsigned long long sum = 0;
+  for (int b = b0; b < b1; ++b) sum += counts[b];
+  part[threadIdx.x] = sum;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {
+    const unsigned long long v = threadIdx.x >= off ? part[threadIdx.x - off] : 0ull;
+    __syncthreads();
+    part[threadIdx.x] += v;
+    __syncthreads();
+  }
+  unsigned long long run = threadIdx.x ? part[threadIdx.x - 1] : 0ull;
+  for (int b = b0; b < b1; ++b) {
+    cursor[b] = run;
+    start[b] = (int64_t)run;
+    run += counts[b];
+    end[b] = (int64_t)run;
+    counts[b] = 0ull;  // left zero for the next grouping
+  }
+}
+
+__global__ void __launch_bounds__(1024) sub_scatter_kernel(const uint32_t* __restrict__ keys,
+                                                           const uint32_t* __restrict__ vals,
+                                                           const unsigned long long* __restrict__ dm,
+                                                           int64_t cap, int nb,
+                                                           unsigned long long* __restrict__ cursor,
+                                                           uint32_t* __restrict__ out) {
+  extern __shared__ unsigned int sh_hist[];  // [nb] counts, then [nb] bases (64-bit)
+  unsigned long long* base = reinterpret_cast<unsigned long long*>(sh_hist + ((nb + 1) & ~1));
+  const int64_t m = sub_count(dm, cap);
+  constexpr int kPer = kSubTile / 1024;
+  for (int64_t t0 = (int64_t)blockIdx.x * kSubTile; t0 < m; t0 += (int64_t)gridDim.x * kSubTile) {
+    const int64_t t1 = t0 + kSubTile < m ? t0 + kSubTile : m;
+    for (int e = threadIdx.x; e < nb; e += blockDim.x) sh_hist[e] = 0u;
+    __syncthreads();
+    uint32_t k[kPer], v[kPer];
+#pragma unroll
+    for (int r = 0; r < kPer; ++r) {
+      const int64_t p = t0 + r * 1024 + threadIdx.x;
+      k[r] = 0u;
+      v[r] = 0u;
+      if (p < t1) {
+        k[r] = min(keys[p], (uint32_t)(nb - 1));
+        v[r] = vals[p];
+        atomicAdd(&sh_hist[k[r]], 1u);
+      }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < nb; e += blockDim.x) {
+      base[e] = sh_hist[e] ? atomicAdd(&cursor[e], (unsigned long long)sh_hist[e]) : 0ull;
+      sh_hist[e] = 0u;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kPer; ++r) {
+      const int64_t p = t0 + r * 1024 + threadIdx.x;
+      if (p < t1) out[base[k[r]] + atomicAdd(&sh_hist[k[r]], 1u)] = v[r];
+    }
+    __syncthreads();
+  }
+}
+
+void launch_band_subbounds(const BandWork& w, const int32_t* list, const int32_t* sb_first,
+                           int nadm, float* sub, cudaStream_t st) {
+  band_subbounds_kernel<<<std::max(nadm, 1), 128, 0, st>>>(w.sample_sorted, w.nvalid, w.bounds,
+                                                           w.K, list, sb_first, nadm, sub);
+}
+
+int launch_band_group_sub(const uint32_t* keys, const uint32_t* vals,
+                          const unsigned long long* m, int64_t cap, int ngroups,
+                          unsigned long long* counts, unsigned long long* cursor, int64_t* start,
+                          int64_t* end, uint32_t* members, cudaStream_t st) {
+  if (ngroups <= 0 || ngroups > kSubMaxGroups) return -1;
+  static DeviceOnce d1, d2;
+  const size_t smem1 = (size_t)ngroups * sizeof(unsigned);
+  const size_t smem2 = (size_t)((ngroups + 1) & ~1) * sizeof(unsigned) +
+                       (size_t)ngroups * sizeof(unsigned long long);
+  set_max_smem(sub_hist_kernel, 200 * 1024, d1);
+  set_max_smem(sub_scatter_kernel, 200 * 1024, d2);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t tiles = (std::max<int64_t>(cap, 1) + kSubTile - 1) / kSubTile;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)sms * 2));
+  sub_hist_kernel<<<grid, 1024, smem1, st>>>(keys, m, cap, ngroups, counts);
+  sub_scan_kernel<<<1, 1024, 0, st>>>(counts, ngroups, cursor, start, end);
+  sub_scatter_kernel<<<grid, 1024, smem2, st>>>(keys, vals, m, cap, ngroups, cursor, members);
+  return 0;
+}
+
+
+// Filter chunks of a slot's consecutive groups [g0, g1): greedy packing into
+// chunks of <= chunk members (a group larger than chunk alone, split
+// evenly).  One warp per slot: the group sizes are loaded 32 at a time and
+// lane 0 walks them from registers (shuffles); run twice, counting first,
+// then writing at the reserved position.
+template <typename Emit>
+__device__ __forceinline__ void pack_groups_warp(int g0, int g1, const int64_t* __restrict__ gstart,
+                                                 const int64_t* __restrict__ gend, int64_t chunk,
+                                                 Emit emit) {
+  const int lane = threadIdx.x & 31;
+  int64_t c0 = 0, cur = 0;
+  for (int b = g0; b < g1; b += 32) {
+    const int g = b + lane;
+    int64_t s0 = 0, cnt = 0;
+    if (g < g1) {
+      s0 = gstart[g];
+      cnt = gend[g] - s0;
+    }
+    const int nb = min(32, g1 - b);
+    for (int t = 0; t < nb; ++t) {
+      const int64_t ts = __shfl_sync(0xffffffffu, s0, t);
+      const int64_t tc = __shfl_sync(0xffffffffu, cnt, t);
+      if (lane != 0 || tc <= 0) continue;
+      if (cur > 0 && cur + tc > chunk) {  // close the open chunk before this group
+        emit(c0, c0 + cur);
+        cur = 0;
+      }
+      if (tc > chunk) {
+        const int64_t pieces = (tc + chunk - 1) / chunk, cs = (tc + pieces - 1) / pieces;
+        for (int64_t p = ts; p < ts + tc; p += cs) emit(p, min(p + cs, ts + tc));
+        continue;
+      }
+      if (cur == 0) c0 = ts;
+      cur += tc;
+    }
+  }
+  if (lane == 0 && cur > 0) emit(c0, c0 + cur);
+}
+
+__global__ void band_pack_chunks_kernel(const int32_t* __restrict__ sbf, int nslot,
+                                        const int64_t* __restrict__ gstart,
+                                        const int64_t* __restrict__ gend,
+                                        const int32_t* __restrict__ gband, int64_t chunk,
+                                        int64_t* __restrict__ ctab, int32_t* __restrict__ cband,
+                                        unsigned long long* __restrict__ nct) {
+  const int e = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (e >= nslot) return;
+  const int g0 = sbf[e], g1 = sbf[e + 1];
+  if (g1 <= g0) return;
+  const int band = gband[g0];
+  unsigned long long nc = 0;
+  pack_groups_warp(g0, g1, gstart, gend, chunk, [&](int64_t, int64_t) { ++nc; });
+  unsigned long long at = 0;
+  if ((threadIdx.x & 31) == 0 && nc) at = atomicAdd(nct, nc);
+  if (__shfl_sync(0xffffffffu, nc, 0) == 0) return;
+  pack_groups_warp(g0, g1, gstart, gend, chunk, [&](int64_t a, int64_t b) {
+    ctab[2 * at] = a;
+    ctab[2 * at + 1] = b;
+    cband[at] = band;
+    ++at;
+  });
+}
+
+void launch_band_pack_chunks(const int32_t* sb_first, int nslot, const int64_t* gstart,
+                             const int64_t* gend, const int32_t* gband, int64_t chunk,
+                             int64_t* ctab, int32_t* cband, unsigned long long* nctab,
+                             cudaStream_t st) {
+  cudaMemsetAsync(nctab, 0, sizeof(unsigned long long), st);
+  if (nslot <= 0) return;
+  band_pack_chunks_kernel<<<(nslot + 3) / 4, 128, 0, st>>>(sb_first, nslot, gstart, gend, gband,
+                                                            chunk, ctab, cband, nctab);
 }
 
 }  // namespace lmsb

@@ -94,6 +94,19 @@ struct BandArgs {
   const int32_t* group_band;  // optional: band of every group
   int nlist;
   int64_t chunk;              // filter: members per CTA
+  // sorted keys of every inner band at its centre slope, row b at
+  // bkeys + b * bkeys_ld: written by the bound kernel when non-null, read by
+  // the filter (no per-chunk sort) when non-null
+  float* bkeys;
+  int64_t bkeys_ld;
+  double bkeys_tau;  // filter: stored keys for bands with dev * (width) <= bkeys_tau * H
+  int chunk_fixed;            // filter: 1 = groups are cut into `chunk`-member pieces only;
+                              // 0 = adaptive (>= kMinChunks per group)
+  // optional explicit chunk table (sub-band grouping, launch_band_pack_chunks):
+  // chunk c = members [ctab[2c], ctab[2c + 1]) of band cband[c], *nctab chunks
+  const int64_t* ctab;
+  const int32_t* cband;
+  const unsigned long long* nctab;
   int64_t* chunk_prefix;      // nlist + 1 scratch: first chunk of every listed band
   double* lb;                 // per band lower bound of any vertex height (-inf: unknown)
   double* wq;                 // per band narrowest q-window of the keys at the band centre
@@ -181,6 +194,27 @@ void launch_band_collect(const BandFit& bf, const BandWork& w, const BandRuns& r
 // group the collected vertices by slot: full_order sorts by (slot, slope
 // position) (radix sort), else buckets of (slot, top 8 slope bits)
 int launch_band_group(const BandWork& w, int64_t m, bool full_order, cudaStream_t st);
+constexpr int kSubMaxGroups = 1 << 14;  // groups of launch_band_group_sub
+// Sub-band grouping (the default for the sweep collect at n <= kBandMaxN):
+// inner sub-band boundaries of every admitted band from its sorted samples
+// (band_subbounds_kernel), then a counting sort of the collected members by
+// their group key (SweepArgs::sub_first): members of a group are contiguous,
+// unordered inside it.  m: the device member count (clamped to cap); counts,
+// cursor: ngroups scratch each; start / end: ngroups group ranges.
+void launch_band_subbounds(const BandWork& w, const int32_t* list, const int32_t* sb_first,
+                           int nadm, float* sub, cudaStream_t st);
+int launch_band_group_sub(const uint32_t* keys, const uint32_t* vals,
+                          const unsigned long long* m, int64_t cap, int ngroups,
+                          unsigned long long* counts, unsigned long long* cursor, int64_t* start,
+                          int64_t* end, uint32_t* members, cudaStream_t st);
+// filter chunks of the sub-band groups: per admitted slot e (groups
+// sb_first[e] .. sb_first[e + 1] - 1, contiguous in slope and in memory)
+// consecutive groups packed greedily into chunks of <= chunk members, a
+// larger group split evenly; ctab / cband / nctab as BandArgs
+void launch_band_pack_chunks(const int32_t* sb_first, int nslot, const int64_t* gstart,
+                             const int64_t* gend, const int32_t* gband, int64_t chunk,
+                             int64_t* ctab, int32_t* cband, unsigned long long* nctab,
+                             cudaStream_t st);
 size_t band_direct_smem(int K, int nsub, int nadm);
 void launch_band_collect_direct(const BandFit& bf, const BandWork& w, const BandRuns& runs,
                                 const BandDirect& dg, int sms, cudaStream_t st);
@@ -231,6 +265,13 @@ struct SweepArgs {
   unsigned long long* raw;  // enumerated (run << 32 | pair) entries, raw_cap of them
   int64_t raw_cap;
   unsigned long long* raw_count;
+  // optional sub-band grouping (launch_band_group_sub): the key of a member of
+  // slot e is its sub-band group sub_first[e] + (number of the slot's inner
+  // sub-band boundaries sub[sub_first[e] - e ...] <= fl32(u)); the
+  // beyond-range pseudo slot gets group sub_first[nslot - 1].  null: the
+  // (slot, slope position) key.
+  const int32_t* sub_first;
+  const float* sub;
 };
 size_t sweep_chunk_smem();
 // sort nseg segments of the n lines by their end keys; returns launches

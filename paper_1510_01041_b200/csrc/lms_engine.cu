@@ -25,6 +25,7 @@
 #include <cstring>
 #include <condition_variable>
 #include <mutex>
+#include <string>
 #include <thread>
 #include <string>
 #include <vector>
@@ -184,6 +185,12 @@ struct lms_ctx {
   cudaEvent_t user_ev[kNumEvents] = {};
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
   std::vector<cudaEvent_t> ev_chunk;
+  // LMSB_TRACE=1: an event after every stage of a band solve, the stage
+  // times printed to stderr (one JSON line per solve)
+  bool trace = false;
+  std::vector<cudaEvent_t> tr_ev;
+  std::vector<const char*> tr_lab;
+  int tr_n = 0;
   bool line_order = true;  // far-first streaming order (LMSB_ORDER=0 disables, for A/B runs)
   // lines (concatenated over fits)
   DevBuf<double> a_own, b_own;
@@ -297,6 +304,20 @@ struct lms_ctx {
   // slower on config 2 (sub-bands are wider than slope-sorted chunks), kept
   // for A/B runs
   int band_direct = 0;
+  // LMSB_GROUP_MODE: grouping of the swept members for n <= kBandMaxN:
+  // 3 (default) = hybrid: a band narrow enough that its centre keys serve
+  // every member (dev * width <= bkeys_tau * H: the filter reads the keys the
+  // bound kernel stored, no sort) is one group; a wide band is cut into
+  // sub-bands at every `sub_samples`-th sorted sample; the groups are
+  // counting-sorted on the device and packed into filter chunks;
+  // 1 = a radix sort by (slot, 17-bit slope position), keys sorted per chunk
+  int group_mode = 3;
+  int sub_samples = 1;     // LMSB_SUB_SAMPLES
+  int filter_keys = 1;     // LMSB_FILTER_KEYS: store the bands' sorted keys (group_mode 3)
+  double bkeys_tau = 0.1;  // LMSB_BKEYS_TAU
+  DevBuf<float> bkeys;
+  DevBuf<int64_t> bctab;
+  DevBuf<int32_t> bcband;
   // LMSB_SWEEP: output-sensitive collect (lms_sweep.cu): 0 never (the
   // pre-test pass over every vertex), 1 always, 2 auto (n >= kSweepMinN, where
   // its fixed sort cost is below the pre-test pass's O(n^2))
@@ -352,6 +373,11 @@ int ctx_init(lms_ctx* c, int device) {
   const char* bd = getenv("LMSB_BAND_DIRECT");
   c->band_direct = (bd && std::strcmp(bd, "1") == 0) ? 1 : 0;
   if (const char* sw = getenv("LMSB_SWEEP")) c->band_sweep = std::max(0, std::min(2, atoi(sw)));
+  if (const char* fk = getenv("LMSB_FILTER_KEYS")) c->filter_keys = atoi(fk) != 0 ? 1 : 0;
+  if (const char* bt = getenv("LMSB_BKEYS_TAU")) c->bkeys_tau = atof(bt);
+  if (const char* gm = getenv("LMSB_GROUP_MODE")) c->group_mode = atoi(gm) == 1 ? 1 : 3;
+  if (const char* ss = getenv("LMSB_SUB_SAMPLES"); ss && atoi(ss) >= 1)
+    c->sub_samples = std::min(64, atoi(ss));
   const char* bmul = getenv("LMSB_BIG_MULT");
   if (bmul && atoll(bmul) >= 1) c->big_mult = atoll(bmul);
   if (const char* bs = getenv("LMSB_BIG_SLICE"); bs && atoll(bs) >= 1) c->big_slice = atoll(bs);
@@ -363,6 +389,7 @@ int ctx_init(lms_ctx* c, int device) {
   c->small_mode = sm ? std::max(0, std::min(2, atoi(sm))) : 1;
   const char* bc = getenv("LMSB_BAND_CHUNK");
   if (bc && atoll(bc) >= 32) c->band_chunk = atoll(bc);
+  if (const char* tr = getenv("LMSB_TRACE")) c->trace = atoi(tr) != 0;
   CUDA_TRY(cudaSetDevice(device));
   CUDA_TRY(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device));
   CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
@@ -468,6 +495,9 @@ void ctx_release(lms_ctx* c) {
   c->dg_i64.release();
   c->dg_cursor.release();
   c->dg_sub.release();
+  c->bctab.release();
+  c->bkeys.release();
+  c->bcband.release();
   c->dg_slot.release();
   c->small_cnt.release();
   c->blines32.release();
@@ -680,6 +710,41 @@ int ensure_host_best(lms_ctx* c, int64_t nfits) {
   return LMS_OK;
 }
 
+void trace_mark(lms_ctx* c, const char* label) {
+  if (!c->trace) return;
+  if (c->tr_n >= (int)c->tr_ev.size()) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+    c->tr_ev.push_back(e);
+    c->tr_lab.push_back(nullptr);
+  }
+  c->tr_lab[c->tr_n] = label;
+  cudaEventRecord(c->tr_ev[c->tr_n++], c->stream);
+}
+
+void trace_dump(lms_ctx* c) {
+  if (!c->trace || c->tr_n < 2) {
+    c->tr_n = 0;
+    return;
+  }
+  cudaEventSynchronize(c->tr_ev[c->tr_n - 1]);
+  std::string out = "{\"trace_us\": [";
+  for (int e = 1; e < c->tr_n; ++e) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->tr_ev[e - 1], c->tr_ev[e]);
+    char buf[160];
+    snprintf(buf, sizeof(buf), "%s[\"%s\", %.1f]", e > 1 ? ", " : "", c->tr_lab[e], ms * 1e3f);
+    out += buf;
+  }
+  float tot = 0.f;
+  cudaEventElapsedTime(&tot, c->tr_ev[0], c->tr_ev[c->tr_n - 1]);
+  char buf[64];
+  snprintf(buf, sizeof(buf), "], \"total_us\": %.1f}", tot * 1e3f);
+  out += buf;
+  fprintf(stderr, "%s\n", out.c_str());
+  c->tr_n = 0;
+}
+
 int persistent_grid(const lms_ctx* c, int64_t count) {
   int64_t g = (int64_t)c->sms * 8;
   if (count >= 0) g = std::min<int64_t>(g, std::max<int64_t>(count, 1));
@@ -776,7 +841,8 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   RC_TRY(c->bbounds.need(K));
   RC_TRY(c->bscnt.need(K));
   RC_TRY(c->bflag.need(K + 1));
-  RC_TRY(c->bscal.need(7));  // [5]: running best height bits of the exact launches, [6]: prepass
+  RC_TRY(c->bscal.need(8));  // [5]: running best height bits of the exact launches, [6]: prepass,
+                             // [7]: filter chunks of the sub-band grouping
   RC_TRY(c->bstart.need(K + 1));
   RC_TRY(c->bend.need(K + 1));
   RC_TRY(c->blb.need(K));
@@ -802,6 +868,7 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   bf.dev = std::max(ahi - bf.c, bf.c - alo) * (1.0 + 0x1p-40) + 1e-300;
   bf.amax = am;
   bf.bmax = bmx;
+  trace_mark(c, "begin");
   // interleaved copy of the fit's lines for the collect pass (kept while the
   // bound lines and the fit's offset are unchanged)
   RC_TRY(c->bab.need(h.n));
@@ -813,6 +880,7 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     c->ab_n = h.n;
     c->ab_ptr = c->bab.p;
   }
+  trace_mark(c, "interleave");
   bf.ab = c->bab.p;
 
   // [0] valid samples [1] collected [2] seeds [3] band survivors [4] count survivors
@@ -885,6 +953,7 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
       return set_error(LMS_ERR_CUDA, "band sample sort failed");
     st->launches += 4;
   }
+  trace_mark(c, "sample");
   lmsb::BandArgs ba{};
   ba.K = K;
   ba.band0 = (int)k0;
@@ -897,6 +966,16 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   ba.edge = c->bedge.p;
   ba.best = c->best.p;
   ba.fit = 0;
+  // stored band keys: bounds computed here (or by this context's own plan
+  // for an own-band search), not taken from a caller
+  const bool use_bkeys = !big && c->filter_keys && c->group_mode == 3 &&
+                         (!sh || sh->mode == 1 || sh->mode == 3);
+  if (use_bkeys) {
+    ba.bkeys_ld = (h.n + 3) & ~(int64_t)3;
+    RC_TRY(c->bkeys.need((int64_t)K * ba.bkeys_ld));
+    ba.bkeys = c->bkeys.p;
+    ba.bkeys_tau = c->bkeys_tau;
+  }
   lmsb::BandBig bg{};
   if (big) {
     constexpr int kBatch = 256;
@@ -924,6 +1003,7 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     lmsb::launch_band_coarse(bf, ba, (int)(k1 - k0), c->stream);
     st->launches += 1;
   }
+  trace_mark(c, "bound");
   // exact (sorted-key) bounds, window widths and edge keys of `nb` listed bands
   // (device list; entries < 0 are skipped)
   auto exact_bounds = [&](const int32_t* d_ids, int nb) -> int {
@@ -954,7 +1034,11 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   // sweep collect: run ends and band ranges (lms_sweep.cu)
   const size_t pin_sw = (size_t)kSweepMaxRuns * (2 * sizeof(lmsb::SweepEnd) + 2 * sizeof(int32_t)) +
                         sizeof(lmsb::SweepEnd) + 64;
-  RC_TRY(ensure_pinned(c, pin_rb + pin_up + pin_tab + pin_sw));
+  // sub-band grouping: group firsts and bands
+  const size_t pin_sub = (size_t)(K + 3 + lmsb::kSubMaxGroups) * sizeof(int32_t) + 64;
+  RC_TRY(ensure_pinned(c, pin_rb + pin_up + pin_tab + pin_sw + pin_sub));
+  int32_t* u_sub = reinterpret_cast<int32_t*>(
+      ((uintptr_t)(c->pin + pin_rb + pin_up + pin_tab + pin_sw) + 15) & ~(uintptr_t)15);
   unsigned char* u_sweep = reinterpret_cast<unsigned char*>(
       ((uintptr_t)(c->pin + pin_rb + pin_up + pin_tab) + 15) & ~(uintptr_t)15);
   // upload staging after the readbacks
@@ -1176,6 +1260,7 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
       lmsb::launch_band_top(c->bwq.p, 0, K, K, kSeedBands, c->blist.p, c->bflag.p, c->stream);
       st->launches += 1;
     }
+    trace_mark(c, "top");
     // the window-edge pairs (usually the optimum itself) and, as a safety net,
     // up to 16 sampled vertices of each of the same bands, in one exact launch
     CUDA_TRY(cudaMemsetAsync(sc + 2, 0, sizeof(unsigned long long), c->stream));
@@ -1184,6 +1269,7 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     lmsb::launch_band_seeds(bf, w, c->ranks.p, c->item_fit.p, 0, seed_cap, sc + 2, c->stream);
     RC_TRY(exact_list(sc + 2, seed_cap, c->ranks.p, c->item_fit.p));
     CUDA_TRY(cudaEventRecord(c->ev_chunk[7], c->stream));
+    trace_mark(c, "seeds");
     // one readback: bounds, window widths, boundaries, the seed record, counts
     CUDA_TRY(cudaMemcpyAsync(p_wq, c->bwq.p, sizeof(double) * K, cudaMemcpyDeviceToHost,
                              c->stream));
@@ -1202,6 +1288,7 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     const lms_candidate hb = *p_hb;
     scnt.assign(p_scnt, p_scnt + K);
     H = hb.found ? hb.height : INFINITY;
+    trace_mark(c, "readback1");
   }
   if (coarse && !(sh && (sh->mode == 2 || sh->mode == 3))) {  // (a shard's plan refined its own slice)
     // the bands the coarse bounds cannot dismiss get their exact bound
@@ -1236,6 +1323,16 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     est += (double)scnt[k] + 2.0;
   }
   st->bands_searched = (int64_t)list.size();
+  if (getenv("LMSB_DEBUG_BANDS")) {
+    for (int32_t k : list) {
+      double uL = -INFINITY, uR = INFINITY;
+      if (k > 0 && k < K) uL = (double)std::nextafter(hbnd[k - 1], -INFINITY);
+      if (k < K - 1) uR = (double)hbnd[k];
+      fprintf(stderr, "band %d lb %.4g wq %.4g uL %.6g uR %.6g devw/H %.4g scnt %u\n", k,
+              k < K ? lb[k] : 0.0, k < K ? wq[k] : 0.0, uL, uR, bf.dev * (uR - uL) / H,
+              k < K ? scnt[k] : 0u);
+    }
+  }
   std::fill(flag.begin(), flag.end(), 0);
   for (int32_t k : list) flag[k] = 1;
   list.push_back(K);  // vertices beyond the key range
@@ -1305,8 +1402,10 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
       runs.hi[e] = f;
     }
   }
+  trace_mark(c, "plan_upload");
   CUDA_TRY(cudaEventRecord(c->ev_chunk[2], c->stream));
   unsigned long long m = 0;
+  int64_t nchunk_max = 0;  // > 0: filter chunks from the sub-band grouping's table
   // direct grouping into sub-band regions (falls back to the sorting path on a
   // region overflow)
   bool direct = false;
@@ -1519,8 +1618,10 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     CUDA_TRY(cudaEventRecord(c->ev_chunk[5], c->stream));
     st->launches += lmsb::launch_sweep_sort(bf.ab, (int)nn, c->sw_ends.p, nseg, ss, c->sms,
                                             c->stream);
+    trace_mark(c, "sweep_sort");
     lmsb::launch_sweep_prepare((int)nn, nr, ss, c->sw_pos.p, c->sw_P.p, c->sw_bmin.p, c->sw_suf.p,
                                c->sms, c->stream);
+    trace_mark(c, "sweep_prep");
     CUDA_TRY(cudaGetLastError());
     st->launches += 3;
     sa.bounds = c->bbounds.p;
@@ -1548,6 +1649,54 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
       fprintf(stderr, "sweep tau %.6g\n", tau);
     }
   }
+  // sub-band groups of the admitted bands (boundaries at every sub_samples-th
+  // sorted sample of the band, computed on the device): the collected keys
+  // are group ids, counting-sorted after the collect and packed into chunks
+  bool subgrp = false;
+  int ngroups_sub = 0, nadm_sub = 0;
+  int32_t* d_sbf = nullptr;
+  int32_t* d_gband = nullptr;
+  if (sweep && use_bkeys) {
+    nadm_sub = nslot - 1;  // the last slot is the beyond-range pseudo band
+    int32_t* sbf = u_sub;  // nadm + 2
+    int32_t* gb = u_sub + (nadm_sub + 2);
+    sbf[0] = 0;
+    int G = 0;
+    bool fits = true;
+    for (int e = 0; e < nadm_sub && fits; ++e) {
+      const int32_t k = list[e];
+      // narrow inner band: one group (its stored keys serve every member);
+      // wide (or outer) band: sub-bands at the samples
+      bool narrow = false;
+      if (k > 0 && k < K - 1) {
+        const double uL = (double)std::nextafter(hbnd[k - 1], -INFINITY), uR = (double)hbnd[k];
+        narrow = std::isfinite(uL) && std::isfinite(uR) && bf.dev * (uR - uL) <= c->bkeys_tau * H;
+      }
+      const int Se =
+          narrow ? 1 : std::max(1, std::min(1024, (int)(scnt[k] / (unsigned)c->sub_samples)));
+      if (G + Se + 1 > lmsb::kSubMaxGroups) fits = false;
+      for (int t = 0; t < Se && fits; ++t) gb[G + t] = k;
+      G += Se;
+      sbf[e + 1] = G;
+    }
+    if (fits) {
+      sbf[nadm_sub + 1] = G + 1;
+      gb[G] = K;
+      ngroups_sub = G + 1;
+      RC_TRY(c->dg_i32.need((int64_t)(nadm_sub + 2) + ngroups_sub));
+      RC_TRY(c->dg_sub.need(std::max(G - nadm_sub, 1)));
+      d_sbf = c->dg_i32.p;
+      d_gband = d_sbf + (nadm_sub + 2);
+      CUDA_TRY(cudaMemcpyAsync(d_sbf, u_sub, sizeof(int32_t) * ((nadm_sub + 2) + ngroups_sub),
+                               cudaMemcpyHostToDevice, c->stream));
+      lmsb::launch_band_subbounds(w, c->blist.p, d_sbf, nadm_sub, c->dg_sub.p, c->stream);
+      sa.sub_first = d_sbf;
+      sa.sub = c->dg_sub.p;
+      subgrp = true;
+      st->launches += 1;
+      trace_mark(c, "subbounds");
+    }
+  }
   for (int attempt = 0; attempt < 2; ++attempt) {
     RC_TRY(c->bck.need(cap));
     RC_TRY(c->bcv.need(cap));
@@ -1564,6 +1713,7 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
       sa.raw_count = c->sw_rawcnt.p;
       CUDA_TRY(cudaEventRecord(c->ev_chunk[10], c->stream));
       lmsb::launch_sweep_emit(bf, sa, c->sms, c->stream);
+      trace_mark(c, "sweep_emit");
       CUDA_TRY(cudaEventRecord(c->ev_chunk[11], c->stream));
       sweep_timed = true;
       st->launches += 2;
@@ -1585,9 +1735,36 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     CUDA_TRY(cudaMemcpyAsync(p_m, sc + 1, sizeof(m), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     m = *p_m;
+    trace_mark(c, "readback2");
     if ((int64_t)m <= cap) break;
     cap = (int64_t)m;  // estimate too small: collect again with the exact size
   }
+  if (subgrp) {
+    // counting sort by group, then the groups packed into filter chunks
+    nchunk_max = 2 * (((int64_t)m + c->band_chunk - 1) / c->band_chunk) + ngroups_sub + nslot + 1;
+    RC_TRY(c->bmem.need(std::max<int64_t>((int64_t)m, 1)));
+    RC_TRY(c->dg_cursor.need(2 * (int64_t)ngroups_sub));
+    RC_TRY(c->bstart.need(std::max<int64_t>(ngroups_sub, K + 1)));
+    RC_TRY(c->bend.need(std::max<int64_t>(ngroups_sub, K + 1)));
+    RC_TRY(c->bctab.need(2 * nchunk_max));
+    RC_TRY(c->bcband.need(nchunk_max));
+    w.start = c->bstart.p;
+    w.end = c->bend.p;
+    ba.start = c->bstart.p;
+    ba.end = c->bend.p;
+    CUDA_TRY(cudaMemsetAsync(c->dg_cursor.p, 0, sizeof(unsigned long long) * ngroups_sub,
+                             c->stream));
+    if (lmsb::launch_band_group_sub(w.ckeys, w.cvals, sc + 1, (int64_t)m, ngroups_sub,
+                                    c->dg_cursor.p, c->dg_cursor.p + ngroups_sub, c->bstart.p,
+                                    c->bend.p, c->bmem.p, c->stream) != 0)
+      return set_error(LMS_ERR_CUDA, "sub-band grouping failed");
+    trace_mark(c, "group");
+    lmsb::launch_band_pack_chunks(d_sbf, nadm_sub + 1, c->bstart.p, c->bend.p, d_gband,
+                                  c->band_chunk, c->bctab.p, c->bcband.p, sc + 7, c->stream);
+    trace_mark(c, "pack");
+    CUDA_TRY(cudaGetLastError());
+    st->launches += 4;
+  } else {
   RC_TRY(c->bcka.need((int64_t)m));
   RC_TRY(c->bmem.need((int64_t)m));
   RC_TRY(c->btemp.need((int64_t)std::max(lmsb::band_sample_temp_bytes(S),
@@ -1598,8 +1775,10 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   w.temp_bytes = (size_t)c->btemp.cap;
   if (lmsb::launch_band_group(w, (int64_t)m, !big, c->stream) != 0)
     return set_error(LMS_ERR_CUDA, "band grouping sort failed");
+  trace_mark(c, "group");
   CUDA_TRY(cudaGetLastError());
   st->launches += 3;
+  }
   }
   CUDA_TRY(cudaEventRecord(c->ev_chunk[3], c->stream));
 
@@ -1620,6 +1799,11 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     ba.group_band = c->blist.p;  // slot -> band
     ba.nlist = nslot;
   }
+  if (nchunk_max > 0) {  // sub-band grouping: the packed chunk table
+    ba.ctab = c->bctab.p;
+    ba.cband = c->bcband.p;
+    ba.nctab = sc + 7;
+  }
   ba.chunk = c->band_chunk;
   ba.chunk_prefix = c->bchunks.p;
   ba.out_ranks = c->ranks.p;
@@ -1631,7 +1815,9 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   CUDA_TRY(cudaMemsetAsync(sc + 6, 0, sizeof(unsigned long long), c->stream));
   if (m > 0) {
     // (small path: up to kMinChunks = 4 chunks per group beyond m / chunk)
-    const int fgrid = (int)(((int64_t)m + ba.chunk - 1) / ba.chunk + 5 * (int64_t)ba.nlist);
+    const int fgrid = nchunk_max > 0
+                          ? (int)nchunk_max
+                          : (int)(((int64_t)m + ba.chunk - 1) / ba.chunk + 5 * (int64_t)ba.nlist);
     if (big) {
       // sorted keys per slice of `big_slice` members at the slice's own
       // centre slope (padding D shrinks with the slice's slope range)
@@ -1664,6 +1850,7 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     } else {
       CUDA_TRY(cudaEventRecord(c->ev_chunk[8], c->stream));
       lmsb::launch_band(bf, ba, 1, fgrid, c->stream);
+      trace_mark(c, "filter");
       CUDA_TRY(cudaEventRecord(c->ev_chunk[9], c->stream));
     }
     filter_timed = true;
@@ -1678,6 +1865,7 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     bc.out_count = sc + 4;
     bc.make_lines = true;
     lmsb::launch_band_count(bf, bc, c->sms, c->stream);
+    trace_mark(c, "count");
     CUDA_TRY(cudaGetLastError());
     st->launches += 4;
     // the window-edge seeds put H at (or within a few ulps of) the optimum, so
@@ -1701,14 +1889,18 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
       lmsb::launch_band_exact_prepass(bf, bp, c->sms, c->stream);
       st->launches += 1;
     }
+    trace_mark(c, "prepass");
     RC_TRY(exact_list(sc + 6, scap, c->ranks.p, c->item_fit.p));
+    trace_mark(c, "exact");
   }
   CUDA_TRY(cudaEventRecord(c->ev_chunk[4], c->stream));
   unsigned long long* cnts = reinterpret_cast<unsigned long long*>(c->pin);  // readbacks done
   CUDA_TRY(cudaMemcpyAsync(cnts, sc + 3, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                            c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
-  st->survivors = (int64_t)cnts[3];  // evaluated by the exact select (cnts[2]: running height)
+  st->survivors = (int64_t)cnts[3];
+  trace_mark(c, "readback3");
+  trace_dump(c);  // evaluated by the exact select (cnts[2]: running height)
   st->band_survivors = (int64_t)cnts[0];
   st->filtered_vertices = (int64_t)m;
   st->chunks = 1;

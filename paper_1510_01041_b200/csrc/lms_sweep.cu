@@ -253,6 +253,21 @@ __device__ __forceinline__ uint32_t member_key(const float* bnd, int K, int band
   return ((uint32_t)max(sb, 0) << kSlopeBits) | t;
 }
 
+// sub-band group of a member of slot sb (SweepArgs::sub_first): the slot's
+// first group plus the number of its inner sub-band boundaries <= bk (the
+// same convention as band_of)
+__device__ __forceinline__ uint32_t sub_group(const SweepArgs& sa, int sb, float bk) {
+  const int g0 = __ldg(sa.sub_first + sb);
+  const float* s = sa.sub + (g0 - sb);
+  int lo = 0, hi = __ldg(sa.sub_first + sb + 1) - g0 - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(s + mid) <= bk) lo = mid + 1;
+    else hi = mid;
+  }
+  return (uint32_t)(g0 + lo);
+}
+
 // Classify enumerated pair (k, l) and decide whether run (k0, k1) emits it
 // (k0 < 0: the near-parallel pass, which owns every admitted band).
 __device__ __forceinline__ bool sweep_take(const BandFit& bf, const SweepArgs& sa, const float* bnd,
@@ -274,13 +289,13 @@ __device__ __forceinline__ bool sweep_take(const BandFit& bf, const SweepArgs& s
     if (band < 0) return false;
     const int sb = slot[band];
     if (sb < 0) return false;
-    *key = member_key(bnd, sa.K, band, bk, sb);
+    *key = sa.sub_first ? sub_group(sa, sb, bk) : member_key(bnd, sa.K, band, bk, sb);
     return true;
   }
   if (cls == 2) {
     const bool own = parallel_pass || (u < 0.0 ? k0 == 0 : k1 == sa.K - 1);
     if (!own) return false;
-    *key = (uint32_t)slot[sa.K] << kSlopeBits;
+    *key = sa.sub_first ? (uint32_t)sa.sub_first[slot[sa.K]] : (uint32_t)slot[sa.K] << kSlopeBits;
     return true;
   }
   return false;

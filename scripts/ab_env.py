@@ -26,11 +26,15 @@ for v in variants:
     ctxs.append(c)
 times = [[] for _ in variants]
 recs = [None] * len(variants)
+stats = [None] * len(variants)
 for r in range(reps):
     for k, c in enumerate(ctxs):
         rec = c.solve(q, 0, total)
         recs[k] = (rec.i, rec.j, rec.height)
-        times[k].append(c.stats()["ms_total"])
+        st = c.stats()
+        times[k].append(st["ms_total"])
+        stats[k] = {x: st[x] for x in ("band_survivors", "survivors", "ms_bound", "ms_partition",
+                                        "ms_band_filter", "ms_filter_kernel", "launches") if x in st}
 for k, v in enumerate(variants):
     print(json.dumps({"n": n, "env": v or "default", "ms": round(float(np.median(times[k][3:])), 4),
-                      "same": recs[k] == recs[0]}))
+                      "same": recs[k] == recs[0], **stats[k]}))
