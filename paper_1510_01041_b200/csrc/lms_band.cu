@@ -1286,6 +1286,19 @@ __host__ __device__ __forceinline__ int64_t group_slice(int64_t cnt, int64_t chu
   return s < chunk ? chunk : (s > smax ? smax : s);
 }
 
+// slice size of listed group grp: a narrow band (BandArgs::narrow: its
+// centre keys serve every member, dev * width <= tau * H) is one slice --
+// one key sort for the whole band; otherwise group_slice
+__device__ __forceinline__ int64_t slice_of(const BandArgs& ba, int grp) {
+  const int64_t cnt = ba.end[grp] - ba.start[grp];
+  const int band = ba.group_band ? ba.group_band[grp] : grp;
+  if (ba.narrow && band < ba.K && ba.narrow[band]) {
+    const int64_t s = (cnt + ba.chunk - 1) / ba.chunk * ba.chunk;
+    return s < ba.chunk ? ba.chunk : s;
+  }
+  return group_slice(cnt, ba.chunk, ba.slice);
+}
+
 // per-slice bin table of the large-n filter: kSliceBins linear bins between
 // the slice's extreme keys, P[0 .. kSliceBins] first key index of each bin
 // (rows padded to a 16-byte multiple for the bulk copy)
@@ -1330,8 +1343,7 @@ __global__ void __launch_bounds__(kBigThreads, 1) band_filter_big_kernel(BandFit
   int64_t sl = 0;
   double uM = 0.0;
   if (!all) {
-    sl = ba.slice_prefix[lo] +
-         (m0 - ba.start[grp]) / group_slice(ba.end[grp] - ba.start[grp], ba.chunk, ba.slice);
+    sl = ba.slice_prefix[lo] + (m0 - ba.start[grp]) / slice_of(ba, grp);
     uM = ba.slice_u[sl];
   }
   if (!all) {
@@ -1566,19 +1578,19 @@ int launch_band_bound_big(const BandFit& bf, const BandArgs& ba, const BandBig& 
   return 0;
 }
 
-__global__ void band_slice_prefix_kernel(const int32_t* __restrict__ list, int nlist,
-                                         const int64_t* __restrict__ start,
-                                         const int64_t* __restrict__ end, int64_t chunk,
-                                         int64_t slice, int64_t* __restrict__ prefix) {
+__global__ void band_slice_prefix_kernel(BandArgs ba) {
   const int lane = threadIdx.x & 31;
   if (threadIdx.x >= 32) return;
+  const int nlist = ba.nlist;
+  int64_t* prefix = ba.slice_prefix;
   int64_t carry = 0;
   for (int e0 = 0; e0 < nlist; e0 += 32) {
     const int e = e0 + lane;
     int64_t c = 0;
     if (e < nlist) {
-      const int64_t sz = end[list[e]] - start[list[e]];
-      const int64_t sb = group_slice(sz, chunk, slice);
+      const int grp = ba.list[e];
+      const int64_t sz = ba.end[grp] - ba.start[grp];
+      const int64_t sb = slice_of(ba, grp);
       c = (sz + sb - 1) / sb;
     }
     int64_t incl = c;
@@ -1618,7 +1630,7 @@ __global__ void band_slice_keys_kernel(BandFit bf, BandArgs ba, int64_t nslices_
       }
       const int grp = ba.list[lo];
       const int band = ba.group_band ? ba.group_band[grp] : grp;
-      const int64_t sb = group_slice(ba.end[grp] - ba.start[grp], ba.chunk, ba.slice);
+      const int64_t sb = slice_of(ba, grp);
       const int64_t m0 = ba.start[grp] + (s - ba.slice_prefix[lo]) * sb;
       const int64_t m1 = min(ba.end[grp], m0 + sb);
       double uL, uR;
@@ -1708,8 +1720,7 @@ int launch_band_slices(const BandFit& bf, const BandArgs& ba, int64_t nslices_ma
                        float* store, int64_t* seg_begin, int64_t* seg_end, void* temp,
                        size_t temp_bytes, cudaStream_t st) {
   if (nslices_max <= 0) return 0;
-  band_slice_prefix_kernel<<<1, 32, 0, st>>>(ba.list, ba.nlist, ba.start, ba.end, ba.chunk,
-                                             ba.slice, ba.slice_prefix);
+  band_slice_prefix_kernel<<<1, 32, 0, st>>>(ba);
   dim3 grid((unsigned)std::min<int64_t>((bf.n + 255) / 256, 64),
             (unsigned)std::min<int64_t>(nslices_max, 65535));
   band_slice_keys_kernel<<<grid, 256, 0, st>>>(bf, ba, nslices_max, keys, seg_begin, seg_end);
@@ -2342,13 +2353,16 @@ __global__ void band_pack_chunks_kernel(const int32_t* __restrict__ sbf, int nsl
                                         const int64_t* __restrict__ gstart,
                                         const int64_t* __restrict__ gend,
                                         const int32_t* __restrict__ gband, int64_t chunk,
-                                        int64_t* __restrict__ ctab, int32_t* __restrict__ cband,
+                                        int64_t chunk_one, int64_t* __restrict__ ctab,
+                                        int32_t* __restrict__ cband,
                                         unsigned long long* __restrict__ nct) {
   const int e = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   if (e >= nslot) return;
   const int g0 = sbf[e], g1 = sbf[e + 1];
   if (g1 <= g0) return;
   const int band = gband[g0];
+  // a one-group slot (a narrow band read with its stored keys): chunk_one
+  if (g1 - g0 == 1) chunk = chunk_one;
   unsigned long long nc = 0;
   pack_groups_warp(g0, g1, gstart, gend, chunk, [&](int64_t, int64_t) { ++nc; });
   unsigned long long at = 0;
@@ -2364,12 +2378,13 @@ __global__ void band_pack_chunks_kernel(const int32_t* __restrict__ sbf, int nsl
 
 void launch_band_pack_chunks(const int32_t* sb_first, int nslot, const int64_t* gstart,
                              const int64_t* gend, const int32_t* gband, int64_t chunk,
-                             int64_t* ctab, int32_t* cband, unsigned long long* nctab,
-                             cudaStream_t st) {
+                             int64_t chunk_one, int64_t* ctab, int32_t* cband,
+                             unsigned long long* nctab, cudaStream_t st) {
   cudaMemsetAsync(nctab, 0, sizeof(unsigned long long), st);
   if (nslot <= 0) return;
   band_pack_chunks_kernel<<<(nslot + 3) / 4, 128, 0, st>>>(sb_first, nslot, gstart, gend, gband,
-                                                            chunk, ctab, cband, nctab);
+                                                            chunk, chunk_one, ctab, cband,
+                                                            nctab);
 }
 
 }  // namespace lmsb

@@ -120,6 +120,7 @@ struct BandArgs {
   double* slice_kmin;         // per slice: smallest key and bin width of its bin table
   double* slice_res;
   unsigned* slice_ptab;       // per slice: bin table (band_slice_table_kernel)
+  const uint8_t* narrow;      // optional, per band: 1 = one slice for the whole band
   const lms_candidate* best;  // the fit's current best record (H)
   int64_t* out_ranks;
   int32_t* out_fits;
@@ -210,11 +211,12 @@ int launch_band_group_sub(const uint32_t* keys, const uint32_t* vals,
 // filter chunks of the sub-band groups: per admitted slot e (groups
 // sb_first[e] .. sb_first[e + 1] - 1, contiguous in slope and in memory)
 // consecutive groups packed greedily into chunks of <= chunk members, a
-// larger group split evenly; ctab / cband / nctab as BandArgs
+// larger group split evenly (chunk_one members for a one-group slot); ctab /
+// cband / nctab as BandArgs
 void launch_band_pack_chunks(const int32_t* sb_first, int nslot, const int64_t* gstart,
                              const int64_t* gend, const int32_t* gband, int64_t chunk,
-                             int64_t* ctab, int32_t* cband, unsigned long long* nctab,
-                             cudaStream_t st);
+                             int64_t chunk_one, int64_t* ctab, int32_t* cband,
+                             unsigned long long* nctab, cudaStream_t st);
 size_t band_direct_smem(int K, int nsub, int nadm);
 void launch_band_collect_direct(const BandFit& bf, const BandWork& w, const BandRuns& runs,
                                 const BandDirect& dg, int sms, cudaStream_t st);

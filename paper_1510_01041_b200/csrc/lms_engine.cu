@@ -315,7 +315,14 @@ struct lms_ctx {
   int sub_samples = 1;     // LMSB_SUB_SAMPLES
   int filter_keys = 1;     // LMSB_FILTER_KEYS: store the bands' sorted keys (group_mode 3)
   double bkeys_tau = 0.1;  // LMSB_BKEYS_TAU
+  int64_t wide_chunk = 4096;    // LMSB_WIDE_CHUNK: members per filter chunk of a wide band
+  int64_t narrow_chunk = 8192;  // LMSB_NARROW_CHUNK: ... of a narrow band (stored keys)
   DevBuf<float> bkeys;
+  DevBuf<uint8_t> bnarrow;
+  // LMSB_BIG_NARROW=1: n > kBandMaxN cuts a narrow band into one filter slice
+  // (one key sort instead of >= 8); measured no faster at config 3 (more
+  // survivors offset the saved sorts), so off by default
+  int big_narrow = 0;
   DevBuf<int64_t> bctab;
   DevBuf<int32_t> bcband;
   // LMSB_SWEEP: output-sensitive collect (lms_sweep.cu): 0 never (the
@@ -375,6 +382,10 @@ int ctx_init(lms_ctx* c, int device) {
   if (const char* sw = getenv("LMSB_SWEEP")) c->band_sweep = std::max(0, std::min(2, atoi(sw)));
   if (const char* fk = getenv("LMSB_FILTER_KEYS")) c->filter_keys = atoi(fk) != 0 ? 1 : 0;
   if (const char* bt = getenv("LMSB_BKEYS_TAU")) c->bkeys_tau = atof(bt);
+  if (const char* bn = getenv("LMSB_BIG_NARROW")) c->big_narrow = atoi(bn) != 0;
+  if (const char* wc = getenv("LMSB_WIDE_CHUNK"); wc && atoll(wc) >= 256) c->wide_chunk = atoll(wc);
+  if (const char* nc = getenv("LMSB_NARROW_CHUNK"); nc && atoll(nc) >= 256)
+    c->narrow_chunk = atoll(nc);
   if (const char* gm = getenv("LMSB_GROUP_MODE")) c->group_mode = atoi(gm) == 1 ? 1 : 3;
   if (const char* ss = getenv("LMSB_SUB_SAMPLES"); ss && atoi(ss) >= 1)
     c->sub_samples = std::min(64, atoi(ss));
@@ -497,6 +508,7 @@ void ctx_release(lms_ctx* c) {
   c->dg_sub.release();
   c->bctab.release();
   c->bkeys.release();
+  c->bnarrow.release();
   c->bcband.release();
   c->dg_slot.release();
   c->small_cnt.release();
@@ -1741,7 +1753,8 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   }
   if (subgrp) {
     // counting sort by group, then the groups packed into filter chunks
-    nchunk_max = 2 * (((int64_t)m + c->band_chunk - 1) / c->band_chunk) + ngroups_sub + nslot + 1;
+    const int64_t cmin = std::max<int64_t>(1, std::min(c->wide_chunk, c->narrow_chunk));
+    nchunk_max = 2 * (((int64_t)m + cmin - 1) / cmin) + ngroups_sub + nslot + 1;
     RC_TRY(c->bmem.need(std::max<int64_t>((int64_t)m, 1)));
     RC_TRY(c->dg_cursor.need(2 * (int64_t)ngroups_sub));
     RC_TRY(c->bstart.need(std::max<int64_t>(ngroups_sub, K + 1)));
@@ -1760,7 +1773,8 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
       return set_error(LMS_ERR_CUDA, "sub-band grouping failed");
     trace_mark(c, "group");
     lmsb::launch_band_pack_chunks(d_sbf, nadm_sub + 1, c->bstart.p, c->bend.p, d_gband,
-                                  c->band_chunk, c->bctab.p, c->bcband.p, sc + 7, c->stream);
+                                  c->wide_chunk, c->narrow_chunk, c->bctab.p, c->bcband.p, sc + 7,
+                                  c->stream);
     trace_mark(c, "pack");
     CUDA_TRY(cudaGetLastError());
     st->launches += 4;
@@ -1833,6 +1847,19 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
       RC_TRY(c->btemp.need((int64_t)std::max<size_t>((size_t)c->btemp.cap,
                                                      lmsb::band_slice_sort_temp_bytes(nsl, h.n))));
       ba.slice = SB;
+      if (c->big_narrow) {  // narrow bands: one slice (one key sort) per band
+        RC_TRY(c->bnarrow.need(K + 1));
+        uint8_t* u_nar = reinterpret_cast<uint8_t*>(u_sub);  // (sub-band staging unused here)
+        for (int k = 0; k <= K; ++k) u_nar[k] = 0;
+        for (int e = 0; e + 1 < nslot; ++e) {
+          const int32_t k = list[e];
+          if (k <= 0 || k >= K - 1) continue;
+          const double uL = (double)std::nextafter(hbnd[k - 1], -INFINITY), uR = (double)hbnd[k];
+          u_nar[k] = std::isfinite(uL) && std::isfinite(uR) && bf.dev * (uR - uL) <= c->bkeys_tau * H;
+        }
+        CUDA_TRY(cudaMemcpyAsync(c->bnarrow.p, u_nar, K + 1, cudaMemcpyHostToDevice, c->stream));
+        ba.narrow = c->bnarrow.p;
+      }
       ba.slice_prefix = c->bslice_prefix.p;
       ba.slice_u = c->bslice_u.p;
       ba.slice_wq = c->bslice_u.p + nsl;
@@ -1843,9 +1870,11 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
                                    c->bslice_seg.p, c->bslice_seg.p + nsl, c->btemp.p,
                                    (size_t)c->btemp.cap, c->stream) != 0)
         return set_error(LMS_ERR_CUDA, "large-n slice sort failed");
+      trace_mark(c, "slices");
       st->launches += 4;
       CUDA_TRY(cudaEventRecord(c->ev_chunk[8], c->stream));
       lmsb::launch_band_filter_big(bf, ba, c->bslice_store.p, fgrid, c->stream);
+      trace_mark(c, "filter_big");
       CUDA_TRY(cudaEventRecord(c->ev_chunk[9], c->stream));
     } else {
       CUDA_TRY(cudaEventRecord(c->ev_chunk[8], c->stream));
