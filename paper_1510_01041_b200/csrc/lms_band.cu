@@ -2349,6 +2349,11 @@ __device__ __forceinline__ void pack_groups_warp(int g0, int g1, const int64_t* 
   if (lane == 0 && cur > 0) emit(c0, c0 + cur);
 }
 
+#ifndef LMSB_PACK_FIXED
+#define LMSB_PACK_FIXED 1
+#endif
+constexpr bool kPackFixed = LMSB_PACK_FIXED != 0;
+
 __global__ void band_pack_chunks_kernel(const int32_t* __restrict__ sbf, int nslot,
                                         const int64_t* __restrict__ gstart,
                                         const int64_t* __restrict__ gend,
@@ -2363,6 +2368,23 @@ __global__ void band_pack_chunks_kernel(const int32_t* __restrict__ sbf, int nsl
   const int band = gband[g0];
   // a one-group slot (a narrow band read with its stored keys): chunk_one
   if (g1 - g0 == 1) chunk = chunk_one;
+  if (kPackFixed) {
+    // fixed-size chunks over the slot's member range (its groups are slope
+    // ordered, so a chunk spans at most a few adjacent groups)
+    const int lane = threadIdx.x & 31;
+    const int64_t s0 = gstart[g0], s1 = gend[g1 - 1];
+    const int64_t ncs = s1 > s0 ? (s1 - s0 + chunk - 1) / chunk : 0;
+    if (ncs == 0) return;
+    unsigned long long at = 0;
+    if (lane == 0) at = atomicAdd(nct, (unsigned long long)ncs);
+    at = __shfl_sync(0xffffffffu, at, 0);
+    for (int64_t c = lane; c < ncs; c += 32) {
+      ctab[2 * (at + c)] = s0 + c * chunk;
+      ctab[2 * (at + c) + 1] = min(s1, s0 + (c + 1) * chunk);
+      cband[at + c] = band;
+    }
+    return;
+  }
   unsigned long long nc = 0;
   pack_groups_warp(g0, g1, gstart, gend, chunk, [&](int64_t, int64_t) { ++nc; });
   unsigned long long at = 0;

@@ -315,7 +315,7 @@ struct lms_ctx {
   int sub_samples = 1;     // LMSB_SUB_SAMPLES
   int filter_keys = 1;     // LMSB_FILTER_KEYS: store the bands' sorted keys (group_mode 3)
   double bkeys_tau = 0.1;  // LMSB_BKEYS_TAU
-  int64_t wide_chunk = 4096;    // LMSB_WIDE_CHUNK: members per filter chunk of a wide band
+  int64_t wide_chunk = 3072;    // LMSB_WIDE_CHUNK: members per filter chunk of a wide band
   int64_t narrow_chunk = 8192;  // LMSB_NARROW_CHUNK: ... of a narrow band (stored keys)
   DevBuf<float> bkeys;
   DevBuf<uint8_t> bnarrow;
