@@ -315,6 +315,8 @@ struct lms_ctx {
   int sub_samples = 1;     // LMSB_SUB_SAMPLES
   int filter_keys = 1;     // LMSB_FILTER_KEYS: store the bands' sorted keys (group_mode 3)
   double bkeys_tau = 0.1;  // LMSB_BKEYS_TAU
+  int64_t collect_floor = 0;    // smallest member capacity (grown after a deferred overflow)
+  bool cap_test = false;        // LMSB_CAP_TEST=1: first collect capacity 4,096 (overflow path)
   int64_t wide_chunk = 3072;    // LMSB_WIDE_CHUNK: members per filter chunk of a wide band
   int64_t narrow_chunk = 8192;  // LMSB_NARROW_CHUNK: ... of a narrow band (stored keys)
   DevBuf<float> bkeys;
@@ -383,6 +385,7 @@ int ctx_init(lms_ctx* c, int device) {
   if (const char* fk = getenv("LMSB_FILTER_KEYS")) c->filter_keys = atoi(fk) != 0 ? 1 : 0;
   if (const char* bt = getenv("LMSB_BKEYS_TAU")) c->bkeys_tau = atof(bt);
   if (const char* bn = getenv("LMSB_BIG_NARROW")) c->big_narrow = atoi(bn) != 0;
+  if (const char* ct = getenv("LMSB_CAP_TEST")) c->cap_test = atoi(ct) != 0;
   if (const char* wc = getenv("LMSB_WIDE_CHUNK"); wc && atoll(wc) >= 256) c->wide_chunk = atoll(wc);
   if (const char* nc = getenv("LMSB_NARROW_CHUNK"); nc && atoll(nc) >= 256)
     c->narrow_chunk = atoll(nc);
@@ -1349,6 +1352,8 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   for (int32_t k : list) flag[k] = 1;
   list.push_back(K);  // vertices beyond the key range
   int64_t cap = std::min<int64_t>(span, (int64_t)(2.0 * est * (double)span / (double)S) + 65536);
+  cap = std::max(cap, std::min<int64_t>(span, c->collect_floor));
+  if (c->cap_test && c->collect_floor == 0) cap = std::min<int64_t>(cap, 4096);  // (tests)
   std::copy(list.begin(), list.end(), u_list);
   CUDA_TRY(cudaMemcpyAsync(c->blist.p, u_list, sizeof(int32_t) * list.size(),
                            cudaMemcpyHostToDevice, c->stream));
@@ -1743,6 +1748,13 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
       CUDA_TRY(cudaStreamSynchronize(c->stream));
       for (int e = 0; e < sa.nruns; ++e) fprintf(stderr, "sweep run %d: %llu pairs\n", e, d[e]);
     }
+    if (subgrp) {
+      // the member count stays on the device (the grouping reads it there);
+      // buffers are sized for `cap` and an overflow is caught by the final
+      // readback (the fit is then solved again with the exact capacity)
+      m = (unsigned long long)cap;
+      break;
+    }
     unsigned long long* p_m = reinterpret_cast<unsigned long long*>(c->pin);
     CUDA_TRY(cudaMemcpyAsync(p_m, sc + 1, sizeof(m), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
@@ -1924,9 +1936,20 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   }
   CUDA_TRY(cudaEventRecord(c->ev_chunk[4], c->stream));
   unsigned long long* cnts = reinterpret_cast<unsigned long long*>(c->pin);  // readbacks done
-  CUDA_TRY(cudaMemcpyAsync(cnts, sc + 3, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+  CUDA_TRY(cudaMemcpyAsync(cnts, sc + 1, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                            c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
+  const unsigned long long m_dev = cnts[0];
+  cnts += 2;  // [0] band survivors .. [3] exact-stage inputs, as before
+  if (m_dev > m && !direct) {
+    // deferred member count above the capacity: members were dropped, so
+    // solve again with room for all of them (the record found so far stays
+    // installed; it is a real vertex)
+    c->collect_floor = (int64_t)m_dev;
+    trace_dump(c);
+    return band_solve(c, h, st);
+  }
+  m = m_dev;
   st->survivors = (int64_t)cnts[3];
   trace_mark(c, "readback3");
   trace_dump(c);  // evaluated by the exact select (cnts[2]: running height)

@@ -1,1 +1,3 @@
-python scripts/ab_env.py 16384 10 '' 'LMSB_WIDE_CHUNK=2048' 'LMSB_WIDE_CHUNK=3072' 'LMSB_WIDE_CHUNK=6144' 'LMSB_NARROW_CHUNK=12288' 'LMSB_NARROW_CHUNK=6144' 2>/dev/null
+python scripts/ab_env.py 16384 10 '' 2>/dev/null
+LMSB_TRACE=1 python scripts/trace_fit.py 16384 3 2>&1 | tail -2
+timeout 900 python -m pytest tests/test_gpu_lms.py -m gpu -x -q -k "hybrid or deferred or golden or sweep or sharded or owned" 2>&1 | tail -3

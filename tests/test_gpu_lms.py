@@ -1014,3 +1014,73 @@ def test_batch_sets_path_equals_single_fits():
     fits = lms.solve_lms_batch(sets)
     for p, f in zip(sets, fits):
         assert f == lms.solve_lms(p)
+
+
+@pytest.mark.parametrize("case", ["config2", "grid", "outliers", "dupx", "near_parallel", "shards",
+                                  "wide_q"])
+def test_hybrid_grouping_matches_radix_grouping(case):
+    """The hybrid grouping of the swept members (narrow bands: one group read
+    with the keys the bound kernel stored; wide bands: sample sub-bands,
+    device counting sort, fixed-size chunks) against the radix-sorted
+    (slot, slope position) grouping with per-chunk key sorts: identical
+    records and member counts, sweep forced on so n < 12,288 runs it too."""
+    rng = np.random.default_rng(11)
+    if case == "config2":
+        pts = workloads.contaminated_line_points(16384, 0)
+    elif case == "grid":
+        pts = rng.integers(0, 300, (5000, 2)).astype(float)
+    elif case == "outliers":
+        pts = workloads.contaminated_line_points(4000, 2)
+        pts[:200, 1] += 1e6
+    elif case == "dupx":
+        x = rng.uniform(0, 1, 4096)
+        x[::7] = x[0]
+        pts = np.column_stack([x, 3 * x + rng.normal(0, 0.01, 4096)])
+    elif case == "near_parallel":
+        x = 1.0 + np.arange(3000) * 1e-12
+        pts = np.column_stack([x, rng.normal(0, 1, 3000)])
+    elif case == "wide_q":
+        pts = workloads.contaminated_line_points(7000, 9)
+    else:
+        pts = workloads.contaminated_line_points(6000, 4)
+    n = len(pts)
+    q = n // 2 + 1 if case != "wide_q" else (3 * n) // 4
+    total = n * (n - 1) // 2
+    ranges = [(0, total)] if case != "shards" else [(0, total // 3), (total // 3, total - 5), (total - 5, total)]
+    c0 = _ctx_env(LMSB_SWEEP=1, LMSB_BAND=2, LMSB_GROUP_MODE=1)
+    c1 = _ctx_env(LMSB_SWEEP=1, LMSB_BAND=2, LMSB_GROUP_MODE=3)
+    for c in (c0, c1):
+        c.upload(pts[:, 0].copy(), pts[:, 1].copy())
+    for r0, r1 in ranges:
+        a = record_from_native(c0.solve(q, r0, r1))
+        sa = c0.stats()
+        b = record_from_native(c1.solve(q, r0, r1))
+        sb = c1.stats()
+        assert a == b, (case, r0, r1)
+        assert sa["filtered_vertices"] == sb["filtered_vertices"], (case, r0, r1)
+        want = oracle_rec(pts[:, 0].copy(), pts[:, 1].copy(), q, r0, r1) if n <= 5000 else None
+        if want is not None:
+            assert record_matches(b, want), (case, r0, r1)
+
+
+def test_deferred_member_count_overflow_resolves():
+    """The hybrid grouping never reads the member count back mid-fit; a
+    collect capacity that is too small (forced: 4,096 members) is caught by
+    the final readback and the fit solved again with room for every member:
+    the config-2 record stays the reference's, the member count the full one."""
+    import json
+
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "config2_golden.json")))
+    pts = workloads.contaminated_line_points(gold["n"], 0)
+    q = gold["q"]
+    total = gold["n"] * (gold["n"] - 1) // 2
+    ref = _ctx_env(LMSB_GROUP_MODE=3)
+    tiny = _ctx_env(LMSB_GROUP_MODE=3, LMSB_CAP_TEST=1)
+    for c in (ref, tiny):
+        c.upload(pts[:, 0].copy(), pts[:, 1].copy())
+    a = record_from_native(ref.solve(q, 0, total))
+    b = record_from_native(tiny.solve(q, 0, total))
+    assert a == b
+    assert (b.i, b.j, b.height) == (gold["record"]["i"], gold["record"]["j"],
+                                    float.fromhex(gold["record"]["height"]))
+    assert tiny.stats()["filtered_vertices"] == ref.stats()["filtered_vertices"] > 4096
