@@ -59,6 +59,7 @@ constexpr int kEnumQueue = 64;
 constexpr int kOutBuf = 512;  // per-warp raw-pair buffer (one global atomic per ~480 pairs)
 constexpr int kOutFlush = kOutBuf - 32;
 constexpr int kClsBuf = 4096;  // per-CTA member buffer of the classification
+constexpr int kClsUnroll = 4;  // pairs per thread per step of the classification
 constexpr int kHitBatch = 4;
 
 __device__ __forceinline__ int64_t i64min(int64_t x, int64_t y) { return x < y ? x : y; }
@@ -471,25 +472,44 @@ __global__ void __launch_bounds__(256) sweep_classify_kernel(BandFit bf, SweepAr
   };
   int64_t cnt = (int64_t)*sa.raw_count;
   if (cnt > sa.raw_cap) cnt = sa.raw_cap;
-  const int64_t step = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t p0 = (int64_t)blockIdx.x * blockDim.x; p0 < cnt; p0 += step) {
-    const int64_t p = p0 + threadIdx.x;
-    uint32_t key = 0, val = 0;
-    bool take = false;
-    if (p < cnt) {
-      const unsigned long long e = sa.raw[p];
-      const int r = (int)(e >> 32);
-      const uint32_t pr = (uint32_t)e;
-      take = sweep_take(bf, sa, bnd, slot, sa.run_k0[r], sa.run_k1[r], false, (int)(pr >> 16),
-                        (int)(pr & 0xFFFF), &key, &val);
+  // kClsUnroll pairs per thread per step (their loads and divisions
+  // interleaved), appended to the CTA buffer with one shared atomic per warp
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const int64_t step = (int64_t)gridDim.x * blockDim.x * kClsUnroll;
+  for (int64_t p0 = (int64_t)blockIdx.x * blockDim.x * kClsUnroll; p0 < cnt; p0 += step) {
+    uint32_t key[kClsUnroll], val[kClsUnroll];
+    bool take[kClsUnroll];
+    unsigned long long e[kClsUnroll];
+#pragma unroll
+    for (int u = 0; u < kClsUnroll; ++u) {
+      const int64_t p = p0 + (int64_t)u * blockDim.x + threadIdx.x;
+      e[u] = p < cnt ? sa.raw[p] : ~0ull;
     }
-    if (take) {
-      const unsigned at = atomicAdd(&bn, 1u);
-      bkey[at] = key;
-      bval[at] = val;
+#pragma unroll
+    for (int u = 0; u < kClsUnroll; ++u) {
+      take[u] = false;
+      key[u] = val[u] = 0;
+      if (e[u] != ~0ull) {
+        const int r = (int)(e[u] >> 32);
+        const uint32_t pr = (uint32_t)e[u];
+        take[u] = sweep_take(bf, sa, bnd, slot, sa.run_k0[r], sa.run_k1[r], false, (int)(pr >> 16),
+                             (int)(pr & 0xFFFF), &key[u], &val[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kClsUnroll; ++u) {
+      const unsigned m = __ballot_sync(0xffffffffu, take[u]);
+      unsigned at = 0;
+      if (lane == 0 && m) at = atomicAdd(&bn, (unsigned)__popc(m));
+      at = __shfl_sync(0xffffffffu, at, 0) + __popc(m & lt);
+      if (take[u]) {
+        bkey[at] = key[u];
+        bval[at] = val[u];
+      }
     }
     __syncthreads();
-    if (bn > kClsBuf - 256) flush();  // (uniform: bn read after the barrier)
+    if (bn > kClsBuf - kClsUnroll * 256) flush();  // (uniform: bn read after the barrier)
   }
   flush();
 }

@@ -1,3 +1,2 @@
 python scripts/ab_env.py 16384 10 '' 2>/dev/null
 LMSB_TRACE=1 python scripts/trace_fit.py 16384 3 2>&1 | tail -2
-timeout 900 python -m pytest tests/test_gpu_lms.py -m gpu -x -q -k "hybrid or deferred or golden or sweep or sharded or owned" 2>&1 | tail -3
