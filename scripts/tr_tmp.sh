@@ -1,2 +1,3 @@
 python scripts/ab_env.py 16384 10 '' 2>/dev/null
-LMSB_TRACE=1 python scripts/trace_fit.py 16384 3 2>&1 | tail -2
+AB_SEED=4 python scripts/ab_env.py 13000 10 '' 2>/dev/null
+AB_SEED=4 python scripts/ab_env.py 5000 10 '' 2>/dev/null
