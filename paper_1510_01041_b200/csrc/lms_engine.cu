@@ -105,9 +105,11 @@ int64_t band_size(int64_t knob, int64_t n) {
 
 // Most slope runs of the sweep collect (two sorts of the n lines each).
 constexpr int kSweepMaxRuns = 16;
-// Auto mode: sweep collect from this many lines (measured: n = 8,000 pre-test
-// 0.11 ms vs sweep 0.21 ms; n = 16,384 0.36 vs 0.31; n = 65,536 5.4 vs 1.6).
-constexpr int64_t kSweepMinN = 12288;
+// Auto mode: sweep collect from this many lines.  With the hybrid grouping
+// (no radix sort of the members) the sweep wins from the band stage's
+// threshold up (fit times, sweep vs pre-test: n = 2,500 0.62 vs 0.63 ms,
+// 5,000 0.62 vs 0.67, 8,192 0.71 vs 0.84, 11,000 0.84 vs 0.98).
+constexpr int64_t kSweepMinN = 2048;
 
 // Large-n band size (vertices per band = mult * n): fewer, wider bands pay
 // once n > ~36 k (config 3, n = 65,536: 8 -> 18.6 ms, 16 -> 17.9, 32 ->

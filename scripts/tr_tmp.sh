@@ -1,3 +1,1 @@
-python scripts/ab_env.py 16384 10 '' 2>/dev/null
-AB_SEED=4 python scripts/ab_env.py 13000 10 '' 2>/dev/null
-AB_SEED=4 python scripts/ab_env.py 5000 10 '' 2>/dev/null
+timeout 1200 python -m pytest tests/test_gpu_lms.py -m gpu -x -q 2>&1 | tail -3
