@@ -76,7 +76,7 @@ typedef struct lms_stats {
   float ms_total;           /* device time of the whole solve (CUDA events) */
   float ms_filter;          /* device time inside the filter kernels */
   float ms_exact;           /* device time inside seed + exact-select + reduce */
-  float reserved;
+  float ms_bound_kernel;    /* the per-band bound kernel alone (band_bound_kernel) */
   /* slope-band stage (lms_band.cu); zero when the count filter ran instead */
   int64_t bands;            /* slope bands the fit's vertices were grouped into */
   int64_t bands_searched;   /* bands whose lower bound admitted the bound H */

@@ -69,7 +69,7 @@ class Stats(ctypes.Structure):
         ("ms_total", ctypes.c_float),
         ("ms_filter", ctypes.c_float),
         ("ms_exact", ctypes.c_float),
-        ("reserved", ctypes.c_float),
+        ("ms_bound_kernel", ctypes.c_float),
         ("bands", ctypes.c_int64),
         ("bands_searched", ctypes.c_int64),
         ("ms_partition", ctypes.c_float),

@@ -822,7 +822,7 @@ int order_lines(lms_ctx* c, const std::vector<int64_t>& seg, int64_t F, const do
 // fit's magnitudes are finite and n <= kBandMaxBigN.
 int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   const int64_t span = h.r1 - h.r0;
-  bool filter_timed = false, sweep_timed = false;
+  bool filter_timed = false, sweep_timed = false, bound_timed = false;
   ShardSpec* sh = c->shard;
   const int64_t P0 = sh ? sh->P0 : h.r0;
   const int64_t pspan = sh ? sh->P1 - sh->P0 : span;
@@ -1013,7 +1013,10 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
       st->launches += 4 * ((k1 - k0 + kBatch - 1) / kBatch);
     }
   } else if (k1 > k0 && !coarse) {
+    CUDA_TRY(cudaEventRecord(c->ev_chunk[12], c->stream));
     lmsb::launch_band(bf, ba, 0, (int)(k1 - k0), c->stream);
+    CUDA_TRY(cudaEventRecord(c->ev_chunk[13], c->stream));
+    bound_timed = true;
     st->launches += 1;
   }
   if (k1 > k0 && coarse) {  // sort-free bounds; exact ones only where needed
@@ -1971,6 +1974,11 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   if (filter_timed) {
     CUDA_TRY(cudaEventElapsedTime(&ms, c->ev_chunk[8], c->ev_chunk[9]));
     st->ms_filter_kernel = ms;
+  }
+  st->ms_bound_kernel = 0.f;
+  if (bound_timed) {
+    CUDA_TRY(cudaEventElapsedTime(&ms, c->ev_chunk[12], c->ev_chunk[13]));
+    st->ms_bound_kernel = ms;
   }
   st->ms_sweep_enum = 0.f;
   if (sweep_timed) {

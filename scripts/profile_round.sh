@@ -7,7 +7,7 @@ set -x
 tag=${1:-r02}
 mkdir -p gpurun_out
 ncu --set full --clock-control none --import-source on \
-    -k regex:"band_filter_kernel|band_bound_kernel|sweep_enum|band_count_kernel|exact_cached" \
+    -k regex:"band_filter_kernel|band_bound_kernel|sweep_enum|sweep_classify|band_count_kernel|exact_cached|sub_scatter|band_prepass_count" \
     -o gpurun_out/${tag}_band python scripts/quick_time.py 16384 1 > gpurun_out/ncu_band.log 2>&1
 python scripts/ncu_summary.py gpurun_out/${tag}_band.ncu-rep profiles/${tag}_band_kernels_ncu.json
 ncu --set full --clock-control none -k regex:"band_filter_big|sweep_enum|band_count_kernel|band_coarse" -c 4 \
