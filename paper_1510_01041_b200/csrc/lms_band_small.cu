@@ -77,7 +77,8 @@ constexpr int kSegRun = 16;   // ranks per lane per warp segment
 constexpr int kSweepStep = LMSB_SMALL_STEP; // vertices per lane per sweep step
 constexpr int kQueue = 32 * (kSweepStep + 1);  // per-warp queues: < 32 waiting + a step
 static_assert(kSegRun % kSweepStep == 0, "whole sweep steps per segment");
-constexpr int kMaxRuns = 8;   // slope runs tested before a band lookup
+constexpr int kMaxRuns = 8;   // slope runs tested before a band lookup (a 3-step search)
+static_assert(kMaxRuns == 8, "the sweep's run search takes 3 steps");
 
 template <int kItems, int kT = kThreads>
 struct SmallShared {
@@ -643,9 +644,9 @@ __global__ void __launch_bounds__(kT, kT == kThreads ? LMSB_SMALL_MINB : 1) smal
         k = k1 + 1;
       }
       sh.nruns = nr;
+      for (int w = nr; w < kMaxRuns; ++w) sh.rlo[w] = INFINITY;  // (the run search below)
     }
     __syncthreads();
-    const int nruns = sh.nruns;
     const float amf = (float)am;
     // band lookup and padded window counts of queued in-run vertices, lane per
     // vertex; vertices of keyless bands go straight to the fp32 counts
@@ -763,9 +764,13 @@ __global__ void __launch_bounds__(kT, kT == kThreads ? LMSB_SMALL_MINB : 1) smal
           const bool live = (da != 0.0) & (e0 + t < valid);
           const bool beyond = huge | !(fabsf(u32) * amf < 1e29f) |
                               ((fabsf(num32) < 1e-30f) & (num != 0.0));
-          bool inrun = false;  // runs from shared memory (broadcast reads)
-#pragma unroll 1
-          for (int w = 0; w < nruns; ++w) inrun |= (u32 >= sh.rlo[w]) & (u32 <= sh.rhi[w]);
+          // the last run starting at or below u32 (runs ascend, unused
+          // entries start at +inf), then its end: 3 steps instead of a test
+          // per run
+          int w = (sh.rlo[4] <= u32) ? 4 : 0;
+          w += (sh.rlo[w + 2] <= u32) ? 2 : 0;
+          w += (sh.rlo[w + 1] <= u32) ? 1 : 0;
+          const bool inrun = (sh.rlo[w] <= u32) & (u32 <= sh.rhi[w]);
           cand[t] = live & beyond & first;  // beyond the fp32 tests (first sweep only)
           inr[t] = live & !beyond & inrun;  // band lookup deferred to search()
         }
