@@ -394,23 +394,36 @@ __global__ void __launch_bounds__(kCoarseThreads, 1) band_coarse_kernel(BandFit 
 // band, so a chunk spans a narrow slope range and gets its own centre uM,
 // sorted keys, padding D and lower bound)
 template <int kThreads, int kItems>
+__device__ __forceinline__ void filter_chunk(const BandFit& bf, const BandArgs& ba,
+                                             BandShared<kThreads, kItems>& sh, int band, int64_t m0,
+                                             int64_t m1);
+
+template <int kThreads, int kItems>
 __global__ void __launch_bounds__(kThreads, 1) band_filter_kernel(BandFit bf, BandArgs ba) {
   using SH = BandShared<kThreads, kItems>;
   extern __shared__ __align__(16) unsigned char band_smem[];
   SH& sh = *reinterpret_cast<SH*>(band_smem);
-  const int tid = threadIdx.x;
-  const int lane = tid & 31;
-  // chunk -> (band, member range): the explicit chunk table, or (listed
-  // group, chunk index) from the groups' chunk prefix
+  // chunk -> (band, member range): the explicit chunk table (persistent CTAs
+  // taking chunks from a ticket counter: the table's length is known only on
+  // the device), or (listed group, chunk index) from the groups' chunk prefix
+  if (ba.ctab) {
+    __shared__ int64_t s_ticket;
+    const int64_t nct = (int64_t)*ba.nctab;
+    for (;;) {
+      __syncthreads();
+      if (threadIdx.x == 0)
+        s_ticket = ba.ticket ? (int64_t)atomicAdd(ba.ticket, 1ull) : (int64_t)blockIdx.x;
+      __syncthreads();
+      const int64_t c = s_ticket;
+      if (c >= nct) return;
+      filter_chunk<kThreads, kItems>(bf, ba, sh, ba.cband[c], ba.ctab[2 * c], ba.ctab[2 * c + 1]);
+      if (!ba.ticket) return;
+    }
+  }
   const int64_t cidx = blockIdx.x;
   int band;
   int64_t m0, m1;
-  if (ba.ctab) {
-    if (cidx >= (int64_t)*ba.nctab) return;
-    band = ba.cband[cidx];
-    m0 = ba.ctab[2 * cidx];
-    m1 = ba.ctab[2 * cidx + 1];
-  } else {
+  {
     if (cidx >= ba.chunk_prefix[ba.nlist]) return;
     int lo = 0, hi = ba.nlist - 1;  // largest e with chunk_prefix[e] <= cidx
     while (lo < hi) {
@@ -424,6 +437,16 @@ __global__ void __launch_bounds__(kThreads, 1) band_filter_kernel(BandFit bf, Ba
     m0 = ba.start[grp] + (cidx - ba.chunk_prefix[lo]) * cs;
     m1 = min(ba.end[grp], m0 + cs);
   }
+  filter_chunk<kThreads, kItems>(bf, ba, sh, band, m0, m1);
+}
+
+// window counts of members [m0, m1) of `band` (band_filter_kernel)
+template <int kThreads, int kItems>
+__device__ __forceinline__ void filter_chunk(const BandFit& bf, const BandArgs& ba,
+                                             BandShared<kThreads, kItems>& sh, int band, int64_t m0,
+                                             int64_t m1) {
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
   if (m1 <= m0) return;
   double H = INFINITY;
   {
@@ -1069,7 +1092,8 @@ __global__ void band_subbounds_kernel(const float* __restrict__ sorted,
                                       const float* __restrict__ bounds, int K,
                                       const int32_t* __restrict__ list,
                                       const int32_t* __restrict__ sb_first, int nadm,
-                                      float* __restrict__ sub) {
+                                      float* __restrict__ sub, const int* __restrict__ dnadm) {
+  if (dnadm) nadm = *dnadm;
   const int e = blockIdx.x;
   if (e >= nadm) return;
   const int k = list[e];
@@ -2046,7 +2070,7 @@ void launch_band_collect_direct(const BandFit& bf, const BandWork& w, const Band
                                 const BandDirect& dg, int sms, cudaStream_t st) {
   band_subbounds_kernel<<<std::max(dg.nadm, 1), 128, 0, st>>>(w.sample_sorted, w.nvalid, w.bounds,
                                                               w.K, dg.list, dg.sb_first, dg.nadm,
-                                                              dg.sub);
+                                                              dg.sub, nullptr);
   const size_t smem = band_direct_smem(w.K, dg.nsub, dg.nadm);
   switch (runs.count) {
 #define LMSB_DIRECT(R)                                                                        \
@@ -2202,7 +2226,9 @@ __device__ __forceinline__ int64_t sub_count(const unsigned long long* m, int64_
 __global__ void __launch_bounds__(1024) sub_hist_kernel(const uint32_t* __restrict__ keys,
                                                         const unsigned long long* __restrict__ dm,
                                                         int64_t cap, int nb,
-                                                        unsigned long long* __restrict__ counts) {
+                                                        unsigned long long* __restrict__ counts,
+                                                        const int* __restrict__ dnb) {
+  if (dnb) nb = *dnb;
   extern __shared__ unsigned int sh_hist[];
   for (int e = threadIdx.x; e < nb; e += blockDim.x) sh_hist[e] = 0u;
   __syncthreads();
@@ -2219,7 +2245,9 @@ __global__ void __launch_bounds__(1024) sub_scan_kernel(unsigned long long* __re
                                                         int nb,
                                                         unsigned long long* __restrict__ cursor,
                                                         int64_t* __restrict__ start,
-                                                        int64_t* __restrict__ end) {
+                                                        int64_t* __restrict__ end,
+                                                        const int* __restrict__ dnb) {
+  if (dnb) nb = *dnb;
   __shared__ unsigned long long part[1024];
   const int per = (nb + 1023) / 1024;
   const int b0 = min((int)threadIdx.x * per, nb), b1 = min(b0 + per, nb);
@@ -2248,9 +2276,12 @@ __global__ void __launch_bounds__(1024) sub_scatter_kernel(const uint32_t* __res
                                                            const unsigned long long* __restrict__ dm,
                                                            int64_t cap, int nb,
                                                            unsigned long long* __restrict__ cursor,
-                                                           uint32_t* __restrict__ out) {
+                                                           uint32_t* __restrict__ out,
+                                                           const int* __restrict__ dnb) {
   extern __shared__ unsigned int sh_hist[];  // [nb] counts, then [nb] bases (64-bit)
+  // (the base array sits after the launch-time maximum of nb)
   unsigned long long* base = reinterpret_cast<unsigned long long*>(sh_hist + ((nb + 1) & ~1));
+  if (dnb) nb = *dnb;
   const int64_t m = sub_count(dm, cap);
   constexpr int kPer = kSubTile / 1024;
   for (int64_t t0 = (int64_t)blockIdx.x * kSubTile; t0 < m; t0 += (int64_t)gridDim.x * kSubTile) {
@@ -2285,15 +2316,15 @@ __global__ void __launch_bounds__(1024) sub_scatter_kernel(const uint32_t* __res
 }
 
 void launch_band_subbounds(const BandWork& w, const int32_t* list, const int32_t* sb_first,
-                           int nadm, float* sub, cudaStream_t st) {
+                           int nadm, float* sub, cudaStream_t st, const int* dnadm) {
   band_subbounds_kernel<<<std::max(nadm, 1), 128, 0, st>>>(w.sample_sorted, w.nvalid, w.bounds,
-                                                           w.K, list, sb_first, nadm, sub);
+                                                           w.K, list, sb_first, nadm, sub, dnadm);
 }
 
 int launch_band_group_sub(const uint32_t* keys, const uint32_t* vals,
                           const unsigned long long* m, int64_t cap, int ngroups,
                           unsigned long long* counts, unsigned long long* cursor, int64_t* start,
-                          int64_t* end, uint32_t* members, cudaStream_t st) {
+                          int64_t* end, uint32_t* members, cudaStream_t st, const int* dngroups) {
   if (ngroups <= 0 || ngroups > kSubMaxGroups) return -1;
   static DeviceOnce d1, d2;
   const size_t smem1 = (size_t)ngroups * sizeof(unsigned);
@@ -2306,9 +2337,10 @@ int launch_band_group_sub(const uint32_t* keys, const uint32_t* vals,
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t tiles = (std::max<int64_t>(cap, 1) + kSubTile - 1) / kSubTile;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)sms * 2));
-  sub_hist_kernel<<<grid, 1024, smem1, st>>>(keys, m, cap, ngroups, counts);
-  sub_scan_kernel<<<1, 1024, 0, st>>>(counts, ngroups, cursor, start, end);
-  sub_scatter_kernel<<<grid, 1024, smem2, st>>>(keys, vals, m, cap, ngroups, cursor, members);
+  sub_hist_kernel<<<grid, 1024, smem1, st>>>(keys, m, cap, ngroups, counts, dngroups);
+  sub_scan_kernel<<<1, 1024, 0, st>>>(counts, ngroups, cursor, start, end, dngroups);
+  sub_scatter_kernel<<<grid, 1024, smem2, st>>>(keys, vals, m, cap, ngroups, cursor, members,
+                                                dngroups);
   return 0;
 }
 
@@ -2363,11 +2395,15 @@ __global__ void band_pack_chunks_kernel(const int32_t* __restrict__ sbf, int nsl
                                         const int32_t* __restrict__ gband, int64_t chunk,
                                         int64_t chunk_one, int64_t* __restrict__ ctab,
                                         int32_t* __restrict__ cband,
-                                        unsigned long long* __restrict__ nct) {
+                                        unsigned long long* __restrict__ nct,
+                                        const int* __restrict__ dnslot, int which) {
+  if (dnslot) nslot = *dnslot;
   const int e = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   if (e >= nslot) return;
   const int g0 = sbf[e], g1 = sbf[e + 1];
   if (g1 <= g0) return;
+  // which: 1 the multi-group (wide) slots, 2 the one-group slots
+  if ((which == 1) != (g1 - g0 > 1)) return;
   const int band = gband[g0];
   // a one-group slot (a narrow band read with its stored keys): chunk_one
   if (g1 - g0 == 1) chunk = chunk_one;
@@ -2404,12 +2440,270 @@ __global__ void band_pack_chunks_kernel(const int32_t* __restrict__ sbf, int nsl
 void launch_band_pack_chunks(const int32_t* sb_first, int nslot, const int64_t* gstart,
                              const int64_t* gend, const int32_t* gband, int64_t chunk,
                              int64_t chunk_one, int64_t* ctab, int32_t* cband,
-                             unsigned long long* nctab, cudaStream_t st) {
+                             unsigned long long* nctab, cudaStream_t st, const int* dnslot) {
   cudaMemsetAsync(nctab, 0, sizeof(unsigned long long), st);
   if (nslot <= 0) return;
-  band_pack_chunks_kernel<<<(nslot + 3) / 4, 128, 0, st>>>(sb_first, nslot, gstart, gend, gband,
-                                                            chunk, chunk_one, ctab, cband,
-                                                            nctab);
+  // wide bands' chunks (each sorts its keys: the heavy ones) first in the
+  // table, so the filter's persistent CTAs do not end on them
+  for (int which = 1; which <= 2; ++which)
+    band_pack_chunks_kernel<<<(nslot + 3) / 4, 128, 0, st>>>(sb_first, nslot, gstart, gend, gband,
+                                                              chunk, chunk_one, ctab, cband,
+                                                              nctab, dnslot, which);
+}
+
+// ---- device-side plan of a band search (DevPlan, lms_band.cuh): the host
+// planning of band_solve after the seeds, on one CTA, so the search needs no
+// readback.  Same decisions as the host: admitted bands lb <= H (1 + 2^-19);
+// sweep runs of the admitted and outer bands merged across the smallest gaps
+// (ties: the earliest first) down to kPlanMaxRuns; run ends with the
+// clearance and near-parallel threshold of band_solve; narrow bands one
+// group, wide bands one sub-band per sorted sample.  Slots follow the band
+// index (the host orders them by lb; only the member layout differs).
+constexpr int kPlanThreads = 1024;
+constexpr int kPlanPer = kPlanMaxK / kPlanThreads;  // bands per thread
+
+// exclusive block scan of one int per thread; *total the sum
+__device__ __forceinline__ int plan_scan(int v, int* wtot, int* total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  __syncthreads();
+  if (lane == 31) wtot[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    const int t = wtot[lane];
+    int ti = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, ti, o);
+      if (lane >= o) ti += y;
+    }
+    wtot[lane] = ti - t;
+    if (lane == 31) wtot[32] = ti;
+  }
+  __syncthreads();
+  *total = wtot[32];
+  return wtot[w] + incl - v;
+}
+
+__global__ void __launch_bounds__(kPlanThreads) band_plan_kernel(
+    BandFit bf, const float* __restrict__ bnd, const unsigned* __restrict__ scnt,
+    const double* __restrict__ lb, const lms_candidate* __restrict__ best, int K, int sub_samples,
+    double bkeys_tau, DevPlan dp) {
+  __shared__ int wtot[33];
+  __shared__ int rk0[kPlanMaxK / 2 + 2], rk1[kPlanMaxK / 2 + 2];
+  __shared__ int fk0[kPlanMaxRuns], fk1[kPlanMaxRuns];
+  __shared__ unsigned char act[kPlanMaxK];
+  __shared__ int s_bail;
+  __shared__ double s_tau;
+  __shared__ unsigned long long s_est;
+  const int tid = threadIdx.x;
+  const lms_candidate rec = *best;
+  const double H = rec.found ? rec.height : INFINITY;
+  const double thr = H * (1.0 + 0x1p-19);
+  if (tid == 0) {
+    s_bail = K > kPlanMaxK ? 1 : 0;
+    s_tau = 0.0;
+    s_est = 0ull;
+  }
+  __syncthreads();
+  if (s_bail) {
+    if (tid == 0) dp.hdr->bail = 1;
+    return;
+  }
+  const int kb = tid * kPlanPer, ke = min(K, kb + kPlanPer);
+  // (a) admitted bands -> slots; the sample estimate; sweep eligibility
+  bool adm[kPlanPer];
+  int cnt = 0;
+  unsigned long long est = 0;
+  bool bad = false;
+#pragma unroll
+  for (int t = 0; t < kPlanPer; ++t) {
+    const int k = kb + t;
+    adm[t] = k < ke && lb[k] <= thr;
+    cnt += adm[t];
+    if (adm[t]) est += (unsigned long long)scnt[k] + 2ull;
+    if (k < ke && k < K - 1) bad |= !(isfinite(bnd[k]) && fabs((double)bnd[k]) * bf.amax < 1e29);
+  }
+  if (bad) atomicOr(&s_bail, 1);
+  if (est) atomicAdd(&s_est, est);
+  int nadm = 0;
+  int base = plan_scan(cnt, wtot, &nadm);
+#pragma unroll
+  for (int t = 0; t < kPlanPer; ++t) {
+    const int k = kb + t;
+    if (k >= ke) break;
+    if (adm[t]) {
+      dp.slot[k] = (int16_t)base;
+      dp.list[base] = k;
+      ++base;
+    } else {
+      dp.slot[k] = -1;
+    }
+    act[k] = adm[t] || k == 0 || k == K - 1;
+  }
+  for (int e = tid; e <= nadm; e += kPlanThreads) dp.ident[e] = e;
+  if (tid == 0) {
+    dp.slot[K] = (int16_t)nadm;
+    dp.list[nadm] = K;
+  }
+  __syncthreads();
+  // (b) maximal runs of active bands (the j-th start pairs with the j-th end)
+  int ns = 0;
+#pragma unroll
+  for (int t = 0; t < kPlanPer; ++t) {
+    const int k = kb + t;
+    if (k < ke && act[k] && (k == 0 || !act[k - 1])) ++ns;
+  }
+  int R0 = 0;
+  int rb = plan_scan(ns, wtot, &R0);
+#pragma unroll
+  for (int t = 0; t < kPlanPer; ++t) {
+    const int k = kb + t;
+    if (k >= ke || !act[k]) continue;
+    if (k == 0 || !act[k - 1]) rk0[rb++] = k;  // rb: runs started at or before k
+    if (k == K - 1 || !act[k + 1]) rk1[rb - 1] = k;
+  }
+  __syncthreads();
+  // (c) merge across the smallest gaps down to kPlanMaxRuns: gap j (between
+  // runs j and j + 1) is kept when fewer than kPlanMaxRuns - 1 gaps rank
+  // above it in (width desc, index desc) -- the host's greedy merging of
+  // the smallest, earliest gap first
+  int nr = R0;
+  if (R0 > kPlanMaxRuns) {
+    for (int j0 = 0; j0 < R0 - 1; j0 += kPlanThreads) {
+      const int j = j0 + tid;
+      bool keep = false;
+      if (j < R0 - 1) {
+        const int gj = rk0[j + 1] - rk1[j];
+        int above = 0;
+        for (int i = 0; i < R0 - 1 && above < kPlanMaxRuns - 1; ++i) {
+          const int gi = rk0[i + 1] - rk1[i];
+          above += (gi > gj) || (gi == gj && i > j);
+        }
+        keep = above < kPlanMaxRuns - 1;
+      }
+      if (j < R0 - 1) act[j] = keep;  // (act is free after (b): the kept gaps)
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int r = 0;
+      fk0[0] = rk0[0];
+      for (int j = 0; j < R0 - 1; ++j)
+        if (act[j]) {
+          fk1[r++] = rk1[j];
+          fk0[r] = rk0[j + 1];
+        }
+      fk1[r] = rk1[R0 - 1];
+      nr = r + 1;
+      wtot[0] = nr;
+    }
+    __syncthreads();
+    nr = wtot[0];
+  } else if (tid < R0) {
+    fk0[tid] = rk0[tid];
+    fk1[tid] = rk1[tid];
+  }
+  __syncthreads();
+  if (nr == 0 || nadm == 0) atomicOr(&s_bail, 1);
+  // (d) run ends, as band_solve: the bands' fp32 extents widened 2^-18, sort
+  // ends a clearance m outside, tau = 4 e / m
+  if (tid < nr) {
+    const int k0 = fk0[tid], k1 = fk1[tid];
+    double lo = -INFINITY, hi = INFINITY;
+    if (k0 > 0) {
+      lo = (double)nextafterf(bnd[k0 - 1], -INFINITY);
+      lo -= 0x1p-18 * fabs(lo) + 1e-37;
+    }
+    if (k1 < K - 1) {
+      hi = (double)bnd[k1];
+      hi += 0x1p-18 * fabs(hi) + 1e-37;
+    }
+    double m;
+    if (isfinite(lo) && isfinite(hi))
+      m = 0x1p-20 * (fmax(fabs(lo), fabs(hi)) + (hi - lo)) + 1e-300;
+    else
+      m = 0x1p-20 * (isfinite(lo) ? fabs(lo) : isfinite(hi) ? fabs(hi) : 0.0) + 1e-300;
+    const double s0 = lo - m, s1 = hi + m;
+    double smax = 0.0;
+    if (isfinite(s0)) smax = fabs(s0);
+    if (isfinite(s1)) smax = fmax(smax, fabs(s1));
+    const double err = 0x1p-52 * (bf.amax * smax + bf.bmax) + 1e-300;
+    if (isfinite(s0) || isfinite(s1)) {
+      const double tr = 4.0 * err / m;  // tau >= 0: integer-ordered atomicMax on the bits
+      atomicMax(reinterpret_cast<unsigned long long*>(&s_tau),
+                (unsigned long long)__double_as_longlong(tr));
+    }
+    const double fin = isfinite(s0) ? s0 : isfinite(s1) ? s1 : 0.0;
+    dp.ends[2 * tid] = SweepEnd{isfinite(s0) ? s0 : 0.0, fin, isfinite(s0) ? 0 : 1, 0};
+    dp.ends[2 * tid + 1] = SweepEnd{isfinite(s1) ? s1 : 0.0, fin, isfinite(s1) ? 0 : 2, 0};
+    dp.rk[tid] = k0;
+    dp.rk[kPlanMaxRuns + tid] = k1;
+  }
+  if (tid == 0) dp.ends[2 * kPlanMaxRuns] = SweepEnd{0.0, 0.0, 3, 0};
+  // (e) sub-band groups: a narrow band one group, a wide one a group per
+  // sub_samples sorted samples (<= 1,024); all bands one group each when
+  // that would exceed kSubMaxGroups
+  int se[kPlanPer];
+  int scnt_local = 0;
+#pragma unroll
+  for (int t = 0; t < kPlanPer; ++t) {
+    const int e = kb + t;
+    se[t] = 0;
+    if (e >= nadm) continue;
+    const int k = dp.list[e];
+    bool narrow = false;
+    if (k > 0 && k < K - 1) {
+      const double uL = (double)nextafterf(bnd[k - 1], -INFINITY), uR = (double)bnd[k];
+      narrow = isfinite(uL) && isfinite(uR) && bf.dev * (uR - uL) <= bkeys_tau * H;
+    }
+    se[t] = narrow ? 1 : max(1, min(1024, (int)(scnt[k] / (unsigned)sub_samples)));
+    scnt_local += se[t];
+  }
+  int G = 0;
+  int gb = plan_scan(scnt_local, wtot, &G);
+  const bool flat = G + 1 > kSubMaxGroups;
+  if (flat) {
+    G = nadm;
+    gb = min(kb, nadm);
+  }
+#pragma unroll
+  for (int t = 0; t < kPlanPer; ++t) {
+    const int e = kb + t;
+    if (e >= nadm) continue;
+    const int k = dp.list[e];
+    const int s_e = flat ? 1 : se[t];
+    dp.sbf[e] = gb;
+    for (int g = 0; g < s_e; ++g) dp.gband[gb + g] = k;
+    gb += s_e;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    dp.sbf[nadm] = G;
+    dp.sbf[nadm + 1] = G + 1;
+    dp.gband[G] = K;
+    DevPlanHdr h{};
+    h.nadm = nadm;
+    h.nslot = nadm + 1;
+    h.nr = nr;
+    h.ngroups = G + 1;
+    h.bail = s_bail;
+    h.H = H;
+    h.tau = s_tau;
+    h.est = s_est;
+    *dp.hdr = h;
+  }
+}
+
+void launch_band_plan(const BandFit& bf, const BandWork& w, const double* lb,
+                      const lms_candidate* best, int K, int sub_samples, double bkeys_tau,
+                      const DevPlan& dp, cudaStream_t st) {
+  band_plan_kernel<<<1, kPlanThreads, 0, st>>>(bf, w.bounds, w.sample_counts, lb, best, K,
+                                               sub_samples, bkeys_tau, dp);
 }
 
 }  // namespace lmsb

@@ -107,6 +107,7 @@ struct BandArgs {
   const int64_t* ctab;
   const int32_t* cband;
   const unsigned long long* nctab;
+  unsigned long long* ticket;  // optional: chunk tickets of persistent filter CTAs (zeroed)
   int64_t* chunk_prefix;      // nlist + 1 scratch: first chunk of every listed band
   double* lb;                 // per band lower bound of any vertex height (-inf: unknown)
   double* wq;                 // per band narrowest q-window of the keys at the band centre
@@ -196,6 +197,8 @@ void launch_band_collect(const BandFit& bf, const BandWork& w, const BandRuns& r
 // position) (radix sort), else buckets of (slot, top 8 slope bits)
 int launch_band_group(const BandWork& w, int64_t m, bool full_order, cudaStream_t st);
 constexpr int kSubMaxGroups = 1 << 14;  // groups of launch_band_group_sub
+
+
 // Sub-band grouping (the default for the sweep collect at n <= kBandMaxN):
 // inner sub-band boundaries of every admitted band from its sorted samples
 // (band_subbounds_kernel), then a counting sort of the collected members by
@@ -203,11 +206,12 @@ constexpr int kSubMaxGroups = 1 << 14;  // groups of launch_band_group_sub
 // unordered inside it.  m: the device member count (clamped to cap); counts,
 // cursor: ngroups scratch each; start / end: ngroups group ranges.
 void launch_band_subbounds(const BandWork& w, const int32_t* list, const int32_t* sb_first,
-                           int nadm, float* sub, cudaStream_t st);
+                           int nadm, float* sub, cudaStream_t st, const int* dnadm = nullptr);
 int launch_band_group_sub(const uint32_t* keys, const uint32_t* vals,
                           const unsigned long long* m, int64_t cap, int ngroups,
                           unsigned long long* counts, unsigned long long* cursor, int64_t* start,
-                          int64_t* end, uint32_t* members, cudaStream_t st);
+                          int64_t* end, uint32_t* members, cudaStream_t st,
+                          const int* dngroups = nullptr);
 // filter chunks of the sub-band groups: per admitted slot e (groups
 // sb_first[e] .. sb_first[e + 1] - 1, contiguous in slope and in memory)
 // consecutive groups packed greedily into chunks of <= chunk members, a
@@ -216,7 +220,8 @@ int launch_band_group_sub(const uint32_t* keys, const uint32_t* vals,
 void launch_band_pack_chunks(const int32_t* sb_first, int nslot, const int64_t* gstart,
                              const int64_t* gend, const int32_t* gband, int64_t chunk,
                              int64_t chunk_one, int64_t* ctab, int32_t* cband,
-                             unsigned long long* nctab, cudaStream_t st);
+                             unsigned long long* nctab, cudaStream_t st,
+                             const int* dnslot = nullptr);
 size_t band_direct_smem(int K, int nsub, int nadm);
 void launch_band_collect_direct(const BandFit& bf, const BandWork& w, const BandRuns& runs,
                                 const BandDirect& dg, int sms, cudaStream_t st);
@@ -243,6 +248,11 @@ struct SweepSort {  // ping-pong (key, line id) buffers, nseg * n each
   uint64_t* k1[2];
   uint32_t* idx[2];
   int cur;  // buffer holding the sorted segments
+  // device-planned sweep (band_plan_kernel): the run count is read on the
+  // device; segments 2r, 2r + 1 for runs r < *dnr of nr_max, the slope
+  // segment at 2 * nr_max, the rest skipped (null: every segment is live)
+  const int32_t* dnr;
+  int nr_max;
 };
 struct SweepArgs {
   const float* bounds;   // K - 1 band boundaries
@@ -274,6 +284,10 @@ struct SweepArgs {
   // (slot, slope position) key.
   const int32_t* sub_first;
   const float* sub;
+  // device-planned sweep: run count and near-parallel threshold on the
+  // device (nruns / tau are then the maxima / unused)
+  const int32_t* dnr;
+  const double* dtau;
 };
 size_t sweep_chunk_smem();
 // sort nseg segments of the n lines by their end keys; returns launches
@@ -284,5 +298,37 @@ void launch_sweep_prepare(int n, int nruns, const SweepSort& ss, int32_t* pos, i
                           int32_t* bmin, int32_t* suf, int sms, cudaStream_t st);
 // enumerate and classify; members appended to out_keys / out_vals (count may exceed cap)
 void launch_sweep_emit(const BandFit& bf, const SweepArgs& sa, int sms, cudaStream_t st);
+
+// Device-side plan of a band search after the seeds (band_plan_kernel): the
+// admitted bands, grouping slots, sweep runs and ends, sub-band groups --
+// what band_solve's host planning computes from the readback, without the
+// round trip.  Counts live in DevPlanHdr; arrays in the pointers below.
+constexpr int kPlanMaxRuns = 16;  // = kSweepMaxRuns (lms_engine.cu)
+struct DevPlanHdr {
+  int nadm;      // admitted bands (the outer bands included when admitted)
+  int nslot;     // nadm + 1 (the beyond-range pseudo band last)
+  int nr;        // sweep runs (<= kPlanMaxRuns)
+  int ngroups;   // sub-band groups (nadm .. kSubMaxGroups)
+  int bail;      // 1: the plan cannot run on the device (the host plans instead)
+  int pad;
+  double H;      // the seed height the bands were admitted against
+  double tau;    // near-parallel threshold of the sweep
+  unsigned long long est;  // sampled members of the admitted bands (+2 each)
+};
+struct DevPlan {
+  DevPlanHdr* hdr;
+  int32_t* list;    // K + 1: slot -> band (pseudo band K last)
+  int16_t* slot;    // K + 1: band -> slot (-1)
+  int32_t* ident;   // K + 1: 0, 1, 2, ...
+  SweepEnd* ends;   // 2 * kPlanMaxRuns + 1 (slope segment last)
+  int32_t* rk;      // 2 * kPlanMaxRuns: run_k0 [0, 16), run_k1 [16, 32)
+  int32_t* sbf;     // K + 2: first group of every slot
+  int32_t* gband;   // kSubMaxGroups: band of every group
+};
+// one CTA; K <= kPlanMaxK
+constexpr int kPlanMaxK = 4096;
+void launch_band_plan(const BandFit& bf, const BandWork& w, const double* lb,
+                      const lms_candidate* best, int K, int sub_samples, double bkeys_tau,
+                      const DevPlan& dp, cudaStream_t st);
 
 }  // namespace lmsb

@@ -328,6 +328,7 @@ struct lms_ctx {
   // survivors offset the saved sorts), so off by default
   int big_narrow = 0;
   DevBuf<int64_t> bctab;
+  DevBuf<unsigned long long> bticket;
   DevBuf<int32_t> bcband;
   // LMSB_SWEEP: output-sensitive collect (lms_sweep.cu): 0 never (the
   // pre-test pass over every vertex), 1 always, 2 auto (n >= kSweepMinN, where
@@ -337,6 +338,17 @@ struct lms_ctx {
   DevBuf<uint32_t> sw_idx;
   DevBuf<int32_t> sw_pos, sw_P, sw_bmin, sw_suf, sw_rk;
   DevBuf<lmsb::SweepEnd> sw_ends;
+  // LMSB_DEVICE_PLAN (default 1): one-fit band searches plan their sweep and
+  // groups on the device (band_plan_kernel) once a host-planned fit of the
+  // same n has sized the member buffers (plan_cap); a plan the device cannot
+  // make, or a member overflow, re-solves with the host plan
+  int device_plan = 1;
+  int64_t plan_cap = 0, plan_cap_n = -1;
+  bool force_host_plan = false;
+  DevBuf<lmsb::DevPlanHdr> dp_hdr;
+  DevBuf<int32_t> dp_list, dp_ident, dp_rk, dp_sbf, dp_gband;
+  DevBuf<int16_t> dp_slot;
+  DevBuf<lmsb::SweepEnd> dp_ends;
   DevBuf<unsigned long long> sw_dbg, sw_raw, sw_rawcnt;
   DevBuf<unsigned long long> small_cnt;
   int small_mode = 1;  // LMSB_SMALL: 0 off, 1 batches, 2 also single fits
@@ -388,6 +400,7 @@ int ctx_init(lms_ctx* c, int device) {
   if (const char* bt = getenv("LMSB_BKEYS_TAU")) c->bkeys_tau = atof(bt);
   if (const char* bn = getenv("LMSB_BIG_NARROW")) c->big_narrow = atoi(bn) != 0;
   if (const char* ct = getenv("LMSB_CAP_TEST")) c->cap_test = atoi(ct) != 0;
+  if (const char* dpl = getenv("LMSB_DEVICE_PLAN")) c->device_plan = atoi(dpl) != 0;
   if (const char* wc = getenv("LMSB_WIDE_CHUNK"); wc && atoll(wc) >= 256) c->wide_chunk = atoll(wc);
   if (const char* nc = getenv("LMSB_NARROW_CHUNK"); nc && atoll(nc) >= 256)
     c->narrow_chunk = atoll(nc);
@@ -512,8 +525,17 @@ void ctx_release(lms_ctx* c) {
   c->dg_cursor.release();
   c->dg_sub.release();
   c->bctab.release();
+  c->bticket.release();
   c->bkeys.release();
   c->bnarrow.release();
+  c->dp_hdr.release();
+  c->dp_list.release();
+  c->dp_ident.release();
+  c->dp_rk.release();
+  c->dp_sbf.release();
+  c->dp_gband.release();
+  c->dp_slot.release();
+  c->dp_ends.release();
   c->bcband.release();
   c->dg_slot.release();
   c->small_cnt.release();
@@ -820,6 +842,142 @@ int order_lines(lms_ctx* c, const std::vector<int64_t>& seg, int64_t F, const do
 // the bands whose bound admits H, count their windows, and re-evaluate the
 // survivors exactly.  best[0] must be reset; the caller checked that the
 // fit's magnitudes are finite and n <= kBandMaxBigN.
+// The band search after the seeds with the plan made on the device
+// (band_plan_kernel): sweep collect over the planned runs (device run count,
+// kPlanMaxRuns segments reserved), sub-band grouping and chunking with
+// device counts.  Members are collected into c->plan_cap slots; *m = that
+// capacity (the real count is checked by the final readback).
+int devplan_search(lms_ctx* c, const HostFit& h, lms_stats* st, const lmsb::BandFit& bf,
+                   lmsb::BandArgs& ba, lmsb::BandWork& w, int K, int64_t S, unsigned long long* sc,
+                   unsigned long long* m, int64_t* nchunk_max) {
+  (void)S;
+  const int64_t n = h.n;
+  constexpr int R = lmsb::kPlanMaxRuns;
+  const int nseg = 2 * R + 1;
+  RC_TRY(c->dp_hdr.need(1));
+  RC_TRY(c->dp_list.need(K + 1));
+  RC_TRY(c->dp_ident.need(K + 1));
+  RC_TRY(c->dp_slot.need(K + 1));
+  RC_TRY(c->dp_rk.need(2 * R));
+  RC_TRY(c->dp_sbf.need(K + 2));
+  RC_TRY(c->dp_gband.need(lmsb::kSubMaxGroups));
+  RC_TRY(c->dp_ends.need(nseg));
+  lmsb::DevPlan dp{};
+  dp.hdr = c->dp_hdr.p;
+  dp.list = c->dp_list.p;
+  dp.slot = c->dp_slot.p;
+  dp.ident = c->dp_ident.p;
+  dp.ends = c->dp_ends.p;
+  dp.rk = c->dp_rk.p;
+  dp.sbf = c->dp_sbf.p;
+  dp.gband = c->dp_gband.p;
+  lmsb::launch_band_plan(bf, w, c->blb.p, c->best.p, K, c->sub_samples, c->bkeys_tau, dp,
+                         c->stream);
+  st->launches += 1;
+  trace_mark(c, "plan");
+  const int* d_nadm = &c->dp_hdr.p->nadm;
+  const int* d_nslot = &c->dp_hdr.p->nslot;
+  const int32_t* d_nr = &c->dp_hdr.p->nr;
+  const int* d_ng = &c->dp_hdr.p->ngroups;
+  const double* d_tau = &c->dp_hdr.p->tau;
+  // sweep sorts at the planned run ends
+  const int64_t nbk = (n + 31) / 32;
+  RC_TRY(c->sw_k1.need(2 * nseg * n));
+  RC_TRY(c->sw_idx.need(2 * nseg * n));
+  RC_TRY(c->sw_pos.need(R * n));
+  RC_TRY(c->sw_P.need(R * n));
+  RC_TRY(c->sw_bmin.need(R * nbk));
+  RC_TRY(c->sw_suf.need(R * nbk));
+  lmsb::SweepSort ss{};
+  for (int b = 0; b < 2; ++b) {
+    ss.k1[b] = c->sw_k1.p + b * nseg * n;
+    ss.idx[b] = c->sw_idx.p + b * nseg * n;
+  }
+  ss.dnr = d_nr;
+  ss.nr_max = R;
+  st->launches += lmsb::launch_sweep_sort(bf.ab, (int)n, c->dp_ends.p, nseg, ss, c->sms, c->stream);
+  trace_mark(c, "sweep_sort");
+  lmsb::launch_sweep_prepare((int)n, R, ss, c->sw_pos.p, c->sw_P.p, c->sw_bmin.p, c->sw_suf.p,
+                             c->sms, c->stream);
+  st->launches += 3;
+  trace_mark(c, "sweep_prep");
+  // sub-band boundaries of the admitted bands
+  RC_TRY(c->dg_sub.need(lmsb::kSubMaxGroups));
+  lmsb::launch_band_subbounds(w, c->dp_list.p, c->dp_sbf.p, K, c->dg_sub.p, c->stream, d_nadm);
+  st->launches += 1;
+  trace_mark(c, "subbounds");
+  // collect
+  const int64_t cap = c->plan_cap;
+  RC_TRY(c->bck.need(cap));
+  RC_TRY(c->bcv.need(cap));
+  RC_TRY(c->sw_raw.need(cap));
+  RC_TRY(c->sw_rawcnt.need(1));
+  w.ckeys = c->bck.p;
+  w.cvals = c->bcv.p;
+  lmsb::SweepArgs sa{};
+  sa.bounds = c->bbounds.p;
+  sa.K = K;
+  sa.slot = c->dp_slot.p;
+  sa.nruns = R;
+  sa.run_k0 = c->dp_rk.p;
+  sa.run_k1 = c->dp_rk.p + R;
+  sa.P = c->sw_P.p;
+  sa.bmin = c->sw_bmin.p;
+  sa.suf = c->sw_suf.p;
+  sa.idx = ss.idx[ss.cur];
+  sa.k1a = ss.k1[ss.cur] + (int64_t)(2 * R) * n;
+  sa.idxa = ss.idx[ss.cur] + (int64_t)(2 * R) * n;
+  sa.tau = 0.0;
+  sa.dtau = d_tau;
+  sa.dnr = d_nr;
+  sa.count = sc + 1;
+  sa.out_keys = w.ckeys;
+  sa.out_vals = w.cvals;
+  sa.cap = cap;
+  sa.raw = c->sw_raw.p;
+  sa.raw_cap = cap;
+  sa.raw_count = c->sw_rawcnt.p;
+  sa.sub_first = c->dp_sbf.p;
+  sa.sub = c->dg_sub.p;
+  CUDA_TRY(cudaEventRecord(c->ev_chunk[2], c->stream));
+  CUDA_TRY(cudaEventRecord(c->ev_chunk[5], c->stream));
+  CUDA_TRY(cudaEventRecord(c->ev_chunk[10], c->stream));
+  lmsb::launch_sweep_emit(bf, sa, c->sms, c->stream);
+  CUDA_TRY(cudaEventRecord(c->ev_chunk[11], c->stream));
+  CUDA_TRY(cudaEventRecord(c->ev_chunk[6], c->stream));
+  st->launches += 3;
+  trace_mark(c, "sweep_emit");
+  // grouping with device counts, then the chunk table
+  const int G = lmsb::kSubMaxGroups;
+  const int64_t cmin = std::max<int64_t>(1, std::min(c->wide_chunk, c->narrow_chunk));
+  *nchunk_max = 2 * ((cap + cmin - 1) / cmin) + G + K + 2;
+  RC_TRY(c->bmem.need(std::max<int64_t>(cap, 1)));
+  RC_TRY(c->dg_cursor.need(2 * (int64_t)G));
+  RC_TRY(c->bstart.need(std::max<int64_t>(G, K + 1)));
+  RC_TRY(c->bend.need(std::max<int64_t>(G, K + 1)));
+  RC_TRY(c->bctab.need(2 * *nchunk_max));
+  RC_TRY(c->bcband.need(*nchunk_max));
+  w.start = c->bstart.p;
+  w.end = c->bend.p;
+  ba.start = c->bstart.p;
+  ba.end = c->bend.p;
+  CUDA_TRY(cudaMemsetAsync(c->dg_cursor.p, 0, sizeof(unsigned long long) * G, c->stream));
+  if (lmsb::launch_band_group_sub(w.ckeys, w.cvals, sc + 1, cap, G, c->dg_cursor.p,
+                                  c->dg_cursor.p + G, c->bstart.p, c->bend.p, c->bmem.p, c->stream,
+                                  d_ng) != 0)
+    return set_error(LMS_ERR_CUDA, "sub-band grouping failed");
+  trace_mark(c, "group");
+  lmsb::launch_band_pack_chunks(c->dp_sbf.p, K + 1, c->bstart.p, c->bend.p, c->dp_gband.p,
+                                c->wide_chunk, c->narrow_chunk, c->bctab.p, c->bcband.p, sc + 7,
+                                c->stream, d_nslot);
+  CUDA_TRY(cudaGetLastError());
+  st->launches += 4;
+  trace_mark(c, "pack");
+  st->bands = K;
+  *m = (unsigned long long)cap;
+  return LMS_OK;
+}
+
 int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   const int64_t span = h.r1 - h.r0;
   bool filter_timed = false, sweep_timed = false, bound_timed = false;
@@ -1186,6 +1344,12 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     return LMS_OK;
   }
 
+  // device-side plan (no readback after the seeds): the one-fit default path
+  // once this context has a member capacity for n (a host-planned fit sets it)
+  const bool dplan = c->device_plan && !sh && !big && !coarse && use_bkeys && !c->band_direct &&
+                     (c->band_sweep == 1 || (c->band_sweep == 2 && h.n >= kSweepMinN)) &&
+                     K <= lmsb::kPlanMaxK && c->plan_cap_n == h.n && c->plan_cap > 0 &&
+                     !c->force_host_plan;
   std::vector<double>& lb = c->h_blb;
   std::vector<float> hbnd;
   std::vector<double> wq;
@@ -1290,6 +1454,7 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     RC_TRY(exact_list(sc + 2, seed_cap, c->ranks.p, c->item_fit.p));
     CUDA_TRY(cudaEventRecord(c->ev_chunk[7], c->stream));
     trace_mark(c, "seeds");
+    if (!dplan) {
     // one readback: bounds, window widths, boundaries, the seed record, counts
     CUDA_TRY(cudaMemcpyAsync(p_wq, c->bwq.p, sizeof(double) * K, cudaMemcpyDeviceToHost,
                              c->stream));
@@ -1309,7 +1474,19 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     scnt.assign(p_scnt, p_scnt + K);
     H = hb.found ? hb.height : INFINITY;
     trace_mark(c, "readback1");
+    }
   }
+  // (set by the host plan below, or by the device plan)
+  std::vector<int32_t> list;
+  int nslot = 0;
+  unsigned long long m = 0;
+  int64_t nchunk_max = 0;  // > 0: filter chunks from the sub-band grouping's table
+  bool direct = false;
+  int ngroups = 0;
+  if (dplan) {
+    RC_TRY(devplan_search(c, h, st, bf, ba, w, K, S, sc, &m, &nchunk_max));
+    sweep_timed = true;
+  } else {
   if (coarse && !(sh && (sh->mode == 2 || sh->mode == 3))) {  // (a shard's plan refined its own slice)
     // the bands the coarse bounds cannot dismiss get their exact bound
     std::vector<int32_t> cand;
@@ -1334,7 +1511,6 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   st->seed_height = H;
 
   // ---- collect the vertices of the bands whose bound admits H
-  std::vector<int32_t> list;
   double est = 0.0;
   for (int e = 0; e < K; ++e) {
     const int32_t k = order[e];
@@ -1359,12 +1535,17 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   int64_t cap = std::min<int64_t>(span, (int64_t)(2.0 * est * (double)span / (double)S) + 65536);
   cap = std::max(cap, std::min<int64_t>(span, c->collect_floor));
   if (c->cap_test && c->collect_floor == 0) cap = std::min<int64_t>(cap, 4096);  // (tests)
+  if (!sh && !big) {  // member capacity for later device-planned fits of this n
+    if (c->plan_cap_n != h.n) c->plan_cap = 0;
+    c->plan_cap = std::max(c->plan_cap, cap);
+    c->plan_cap_n = h.n;
+  }
   std::copy(list.begin(), list.end(), u_list);
   CUDA_TRY(cudaMemcpyAsync(c->blist.p, u_list, sizeof(int32_t) * list.size(),
                            cudaMemcpyHostToDevice, c->stream));
   // grouping slot of every band (its index in `list`, -1 when not collected;
   // the beyond-range pseudo band last): the grouping sort keys on the slot
-  const int nslot = (int)list.size();
+  nslot = (int)list.size();
   {
     int16_t* u_slot = reinterpret_cast<int16_t*>(u_list + (K + 1));
     int32_t* u_ident =
@@ -1426,12 +1607,8 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   }
   trace_mark(c, "plan_upload");
   CUDA_TRY(cudaEventRecord(c->ev_chunk[2], c->stream));
-  unsigned long long m = 0;
-  int64_t nchunk_max = 0;  // > 0: filter chunks from the sub-band grouping's table
   // direct grouping into sub-band regions (falls back to the sorting path on a
   // region overflow)
-  bool direct = false;
-  int ngroups = 0;
   std::vector<int64_t> gstart, gend;
   if (c->band_direct) {
     const int nadm = (int)list.size() - 1;  // the last entry is the beyond-range pseudo band
@@ -1811,6 +1988,7 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   st->launches += 3;
   }
   }
+  }
   CUDA_TRY(cudaEventRecord(c->ev_chunk[3], c->stream));
 
   // ---- window counts of the collected vertices; fp32 counts at each
@@ -1834,6 +2012,9 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     ba.ctab = c->bctab.p;
     ba.cband = c->bcband.p;
     ba.nctab = sc + 7;
+    RC_TRY(c->bticket.need(1));
+    CUDA_TRY(cudaMemsetAsync(c->bticket.p, 0, sizeof(unsigned long long), c->stream));
+    ba.ticket = c->bticket.p;
   }
   ba.chunk = c->band_chunk;
   ba.chunk_prefix = c->bchunks.p;
@@ -1846,8 +2027,9 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   CUDA_TRY(cudaMemsetAsync(sc + 6, 0, sizeof(unsigned long long), c->stream));
   if (m > 0) {
     // (small path: up to kMinChunks = 4 chunks per group beyond m / chunk)
+    // (the chunk table: persistent CTAs, one per SM, taking chunk tickets)
     const int fgrid = nchunk_max > 0
-                          ? (int)nchunk_max
+                          ? (int)std::min<int64_t>(nchunk_max, c->sms)
                           : (int)(((int64_t)m + ba.chunk - 1) / ba.chunk + 5 * (int64_t)ba.nlist);
     if (big) {
       // sorted keys per slice of `big_slice` members at the slice's own
@@ -1943,9 +2125,29 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   unsigned long long* cnts = reinterpret_cast<unsigned long long*>(c->pin);  // readbacks done
   CUDA_TRY(cudaMemcpyAsync(cnts, sc + 1, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                            c->stream));
+  lmsb::DevPlanHdr* ph = reinterpret_cast<lmsb::DevPlanHdr*>(c->pin + 128);
+  if (dplan)
+    CUDA_TRY(cudaMemcpyAsync(ph, c->dp_hdr.p, sizeof(lmsb::DevPlanHdr), cudaMemcpyDeviceToHost,
+                             c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   const unsigned long long m_dev = cnts[0];
   cnts += 2;  // [0] band survivors .. [3] exact-stage inputs, as before
+  if (dplan) {
+    const lmsb::DevPlanHdr hd = *ph;
+    if (hd.bail || m_dev > m) {
+      // the device could not plan this fit, or the members outgrew the
+      // capacity: solve again with the host plan (which also resizes)
+      if (m_dev > m) c->plan_cap = std::max<int64_t>(c->plan_cap, (int64_t)m_dev + m_dev / 4);
+      trace_dump(c);
+      c->force_host_plan = true;
+      const int rc = band_solve(c, h, st);
+      c->force_host_plan = false;
+      return rc;
+    }
+    st->bands_searched = hd.nadm;
+    st->seed_height = hd.H;
+    st->sweep_runs = hd.nr;
+  }
   if (m_dev > m && !direct) {
     // deferred member count above the capacity: members were dropped, so
     // solve again with room for all of them (the record found so far stays

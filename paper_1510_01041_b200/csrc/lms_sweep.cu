@@ -73,13 +73,20 @@ __device__ __forceinline__ bool item_less(uint64_t ak, uint32_t ai, uint64_t bk,
 // Sort keys of every (segment, line): kind 0 finite end s (fma(a, s, -b)),
 // 1 at -inf (a descending), 2 at +inf (a ascending), 3 by slope a (the
 // near-parallel pass); equal keys in line order.
+// a segment of a device-planned sweep that no run uses (SweepSort::dnr)
+__device__ __forceinline__ bool seg_dead(int seg, const int32_t* dnr, int nr_max) {
+  return dnr && seg < 2 * nr_max && seg >= 2 * *dnr;
+}
+
 __global__ void sweep_keys_kernel(const double2* __restrict__ ab, int n, const SweepEnd* __restrict__ ends,
-                                  int nseg, uint64_t* __restrict__ k1, uint32_t* __restrict__ idx) {
+                                  int nseg, uint64_t* __restrict__ k1, uint32_t* __restrict__ idx,
+                                  const int32_t* __restrict__ dnr, int nr_max) {
   const int64_t total = (int64_t)nseg * n;
   for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total;
        g += (int64_t)gridDim.x * blockDim.x) {
     const int s = (int)(g / n);
     const int k = (int)(g - (int64_t)s * n);
+    if (seg_dead(s, dnr, nr_max)) continue;
     const SweepEnd e = ends[s];
     const double2 l = ab[k];
     uint64_t p;
@@ -94,10 +101,12 @@ __global__ void sweep_keys_kernel(const double2* __restrict__ ab, int n, const S
 // One CTA sorts one chunk of kChunk items of one segment in shared memory
 // (bitonic network over (key, line id); unique keys, deterministic order).
 __global__ void __launch_bounds__(kChunkThreads) sweep_chunk_sort_kernel(
-    int n, int chunks_per_seg, uint64_t* __restrict__ k1, uint32_t* __restrict__ idx) {
+    int n, int chunks_per_seg, uint64_t* __restrict__ k1, uint32_t* __restrict__ idx,
+    const int32_t* __restrict__ dnr, int nr_max) {
   __shared__ uint64_t sk[kChunk];
   __shared__ uint32_t si[kChunk];
   const int seg = blockIdx.x / chunks_per_seg;
+  if (seg_dead(seg, dnr, nr_max)) return;
   const int c = blockIdx.x - seg * chunks_per_seg;
   const int64_t base = (int64_t)seg * n + (int64_t)c * kChunk;
   const int cnt = min(kChunk, n - c * kChunk);
@@ -134,8 +143,10 @@ __global__ void __launch_bounds__(kChunkThreads) sweep_chunk_sort_kernel(
 // runs of 2w; merge path per thread (kMergeItems outputs).
 __global__ void __launch_bounds__(kMergeThreads) sweep_merge_kernel(
     int n, int64_t w, int blocks_per_seg, const uint64_t* __restrict__ x1,
-    const uint32_t* __restrict__ xi, uint64_t* __restrict__ y1, uint32_t* __restrict__ yi) {
+    const uint32_t* __restrict__ xi, uint64_t* __restrict__ y1, uint32_t* __restrict__ yi,
+    const int32_t* __restrict__ dnr, int nr_max) {
   const int seg = blockIdx.x / blocks_per_seg;
+  if (seg_dead(seg, dnr, nr_max)) return;
   const int64_t d0 =
       ((int64_t)(blockIdx.x - seg * blocks_per_seg) * kMergeThreads + threadIdx.x) * kMergeItems;
   if (d0 >= n) return;
@@ -169,7 +180,8 @@ __global__ void __launch_bounds__(kMergeThreads) sweep_merge_kernel(
 
 // pos[run][line] = position of the line in the run's s1' order
 __global__ void sweep_pos_kernel(int n, int nruns, const uint32_t* __restrict__ idx,
-                                 int32_t* __restrict__ pos) {
+                                 int32_t* __restrict__ pos, const int32_t* __restrict__ dnr) {
+  if (dnr) nruns = *dnr;
   const int64_t total = (int64_t)nruns * n;
   for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total;
        g += (int64_t)gridDim.x * blockDim.x) {
@@ -182,7 +194,8 @@ __global__ void sweep_pos_kernel(int n, int nruns, const uint32_t* __restrict__ 
 // P[run][t] = s1' position of the line at s0' position t, and per 32-block minima
 __global__ void sweep_p_kernel(int n, int nruns, const uint32_t* __restrict__ idx,
                                const int32_t* __restrict__ pos, int32_t* __restrict__ P,
-                               int32_t* __restrict__ bmin) {
+                               int32_t* __restrict__ bmin, const int32_t* __restrict__ dnr) {
+  if (dnr) nruns = *dnr;
   const int nb = (n + 31) / 32;
   const int64_t total = (int64_t)nruns * nb * 32;
   for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total;
@@ -203,10 +216,12 @@ __global__ void sweep_p_kernel(int n, int nruns, const uint32_t* __restrict__ id
 
 // suffix minima of the block minima, one CTA per run
 __global__ void __launch_bounds__(1024) sweep_suffix_kernel(int n, const int32_t* __restrict__ bmin,
-                                                            int32_t* __restrict__ suf) {
+                                                            int32_t* __restrict__ suf,
+                                                            const int32_t* __restrict__ dnr) {
   __shared__ int32_t part[1024];
   const int nb = (n + 31) / 32;
   const int r = blockIdx.x;
+  if (dnr && r >= *dnr) return;
   const int per = (nb + 1023) / 1024;
   const int b0 = threadIdx.x * per;
   const int b1 = min(nb, b0 + per);
@@ -280,7 +295,8 @@ __device__ __forceinline__ bool sweep_take(const BandFit& bf, const SweepArgs& s
   if (r < bf.R0 || r >= bf.R0 + bf.span) return false;
   const double2 li = bf.ab[i], lj = bf.ab[j];
   const double da = fabs(__dsub_rn(li.x, lj.x));
-  if (!parallel_pass && da <= sa.tau) return false;  // the near-parallel pass owns it
+  if (!parallel_pass && da <= (sa.dtau ? __ldg(sa.dtau) : sa.tau))
+    return false;  // the near-parallel pass owns it
   double u = 0.0;
   const int cls = classify(bf, li.x, li.y, lj.x, lj.y, &u);
   *val = ((uint32_t)i << 16) | (uint32_t)j;
@@ -329,7 +345,7 @@ __global__ void __launch_bounds__(kEnumThreads, 4) sweep_enum_kernel(BandFit bf,
   }
   const int n = (int)bf.n;
   const int nb = (n + 31) / 32;
-  const int64_t nitems = (int64_t)sa.nruns * n;
+  const int64_t nitems = (int64_t)(sa.dnr ? *sa.dnr : sa.nruns) * n;
   const int64_t gw0 = (int64_t)blockIdx.x * kEnumWarps + wib;
   const int64_t nw = (int64_t)gridDim.x * kEnumWarps;
   int cur_run = -1, k0 = 0, k1 = 0;
@@ -524,6 +540,8 @@ __global__ void sweep_overflow_kernel(SweepArgs sa) {
 // Nearly parallel pairs (0 < |a_i - a_j| <= tau): lines sorted by a, each
 // against the following lines with a larger slope within tau.
 __global__ void sweep_parallel_kernel(BandFit bf, SweepArgs sa) {
+  const double tau = sa.dtau ? *sa.dtau : sa.tau;
+  if (!(tau > 0.0)) return;
   const int n = (int)bf.n;
   const uint64_t* ka = sa.k1a;
   const uint32_t* ia = sa.idxa;
@@ -540,7 +558,7 @@ __global__ void sweep_parallel_kernel(BandFit bf, SweepArgs sa) {
     }
     for (int tp = lo; tp < n; ++tp) {
       const int l = (int)ia[tp];
-      if (__dsub_rn(bf.ab[l].x, ak) > sa.tau) break;
+      if (__dsub_rn(bf.ab[l].x, ak) > tau) break;
       uint32_t key, val;
       if (sweep_take(bf, sa, sa.bounds, sa.slot, -1, -1, true, k, l, &key, &val)) {
         const unsigned long long pos = atomicAdd(sa.count, 1ull);
@@ -560,14 +578,17 @@ size_t sweep_chunk_smem() { return 0; }  // static shared memory
 int launch_sweep_sort(const double2* ab, int n, const SweepEnd* ends, int nseg, SweepSort& ss,
                       int sms, cudaStream_t st) {
   if (n <= 0 || nseg <= 0) return 0;
-  sweep_keys_kernel<<<sms * 4, 256, 0, st>>>(ab, n, ends, nseg, ss.k1[0], ss.idx[0]);
+  sweep_keys_kernel<<<sms * 4, 256, 0, st>>>(ab, n, ends, nseg, ss.k1[0], ss.idx[0], ss.dnr,
+                                             ss.nr_max);
   const int cps = (n + kChunk - 1) / kChunk;
-  sweep_chunk_sort_kernel<<<nseg * cps, kChunkThreads, 0, st>>>(n, cps, ss.k1[0], ss.idx[0]);
+  sweep_chunk_sort_kernel<<<nseg * cps, kChunkThreads, 0, st>>>(n, cps, ss.k1[0], ss.idx[0], ss.dnr,
+                                                                ss.nr_max);
   int cur = 0, launches = 2;
   const int bps = (n + kMergeThreads * kMergeItems - 1) / (kMergeThreads * kMergeItems);
   for (int64_t w = kChunk; w < n; w *= 2) {
     sweep_merge_kernel<<<nseg * bps, kMergeThreads, 0, st>>>(n, w, bps, ss.k1[cur], ss.idx[cur],
-                                                              ss.k1[cur ^ 1], ss.idx[cur ^ 1]);
+                                                              ss.k1[cur ^ 1], ss.idx[cur ^ 1],
+                                                              ss.dnr, ss.nr_max);
     cur ^= 1;
     ++launches;
   }
@@ -578,9 +599,9 @@ int launch_sweep_sort(const double2* ab, int n, const SweepEnd* ends, int nseg, 
 void launch_sweep_prepare(int n, int nruns, const SweepSort& ss, int32_t* pos, int32_t* P,
                           int32_t* bmin, int32_t* suf, int sms, cudaStream_t st) {
   if (nruns <= 0) return;
-  sweep_pos_kernel<<<sms * 4, 256, 0, st>>>(n, nruns, ss.idx[ss.cur], pos);
-  sweep_p_kernel<<<sms * 4, 256, 0, st>>>(n, nruns, ss.idx[ss.cur], pos, P, bmin);
-  sweep_suffix_kernel<<<nruns, 1024, 0, st>>>(n, bmin, suf);
+  sweep_pos_kernel<<<sms * 4, 256, 0, st>>>(n, nruns, ss.idx[ss.cur], pos, ss.dnr);
+  sweep_p_kernel<<<sms * 4, 256, 0, st>>>(n, nruns, ss.idx[ss.cur], pos, P, bmin, ss.dnr);
+  sweep_suffix_kernel<<<nruns, 1024, 0, st>>>(n, bmin, suf, ss.dnr);
 }
 
 void launch_sweep_emit(const BandFit& bf, const SweepArgs& sa, int sms, cudaStream_t st) {
@@ -596,7 +617,7 @@ void launch_sweep_emit(const BandFit& bf, const SweepArgs& sa, int sms, cudaStre
     sweep_classify_kernel<<<sms * 4, 256, a2.smem_tables ? tab : 0, st>>>(bf, a2);
     sweep_overflow_kernel<<<1, 1, 0, st>>>(a2);
   }
-  if (sa.tau > 0.0 && sa.k1a)
+  if ((sa.tau > 0.0 || sa.dtau) && sa.k1a)
     sweep_parallel_kernel<<<(int)((bf.n + 255) / 256), 256, 0, st>>>(bf, sa);
 }
 
