@@ -1036,11 +1036,35 @@ __global__ void __launch_bounds__(1024) band_edge_seed_kernel(BandFit bf, BandAr
                                                             int64_t* __restrict__ ranks,
                                                             int32_t* __restrict__ fits,
                                                             int64_t cap,
-                                                            unsigned long long* __restrict__ count) {
+                                                            unsigned long long* __restrict__ count,
+                                                            int T, uint8_t* __restrict__ flag) {
   constexpr int kGroup = 16;
   __shared__ int grp[2][kGroup];
   __shared__ int ng[2];
-  const int band = bands[blockIdx.x];
+  __shared__ int s_rank;
+  int band;
+  if (bands) {
+    band = bands[blockIdx.x];
+  } else {
+    // self-selecting (grid = K): a band seeds when fewer than T bands have a
+    // narrower window (ties: the lower index) -- band_top_kernel's choice
+    // without its launch
+    band = blockIdx.x;
+    const double wb = ba.wq[band];
+    if (!(wb < INFINITY)) return;
+    if (threadIdx.x == 0) s_rank = 0;
+    __syncthreads();
+    int c = 0;
+    for (int k = threadIdx.x; k < ba.K; k += blockDim.x) {
+      const double wk = ba.wq[k];
+      c += (wk < wb) || (wk == wb && k < band);
+    }
+    c = __reduce_add_sync(0xffffffffu, c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(&s_rank, c);
+    __syncthreads();
+    if (s_rank >= T) return;
+    if (threadIdx.x == 0 && flag) flag[band] = 1;
+  }
   double uL, uR;
   if (band < 0 || !boundary_extent(ba.bounds, ba.K, band, &uL, &uR) || !keys_in_range(bf, uL, uR))
     return;
@@ -1870,7 +1894,15 @@ void launch_band_edge_seeds(const BandFit& bf, const BandArgs& ba, const int32_t
                             int64_t* ranks, int32_t* fits, int64_t cap,
                             unsigned long long* count, cudaStream_t st) {
   if (nb > 0 && ba.edge)
-    band_edge_seed_kernel<<<nb, 1024, 0, st>>>(bf, ba, bands, ranks, fits, cap, count);
+    band_edge_seed_kernel<<<nb, 1024, 0, st>>>(bf, ba, bands, ranks, fits, cap, count, 0, nullptr);
+}
+
+void launch_band_edge_seeds_top(const BandFit& bf, const BandArgs& ba, int T, uint8_t* flag,
+                                int64_t* ranks, int32_t* fits, int64_t cap,
+                                unsigned long long* count, cudaStream_t st) {
+  cudaMemsetAsync(flag, 0, (size_t)ba.K, st);
+  if (ba.K > 0 && ba.edge)
+    band_edge_seed_kernel<<<ba.K, 1024, 0, st>>>(bf, ba, nullptr, ranks, fits, cap, count, T, flag);
 }
 
 void launch_band_seeds(const BandFit& bf, const BandWork& w, int64_t* ranks, int32_t* fits,

@@ -189,6 +189,11 @@ void launch_band_top(const double* wq, int k0, int k1, int K, int T, int32_t* li
 void launch_band_edge_seeds(const BandFit& bf, const BandArgs& ba, const int32_t* bands, int nb,
                             int64_t* ranks, int32_t* fits, int64_t cap,
                             unsigned long long* count, cudaStream_t st);
+// the same for the T bands with the narrowest windows, each CTA of a K grid
+// deciding whether its band is one of them (flag[] zeroed, then set for them)
+void launch_band_edge_seeds_top(const BandFit& bf, const BandArgs& ba, int T, uint8_t* flag,
+                                int64_t* ranks, int32_t* fits, int64_t cap,
+                                unsigned long long* count, cudaStream_t st);
 void launch_band_seeds(const BandFit& bf, const BandWork& w, int64_t* ranks, int32_t* fits,
                        int32_t fit, int64_t cap, unsigned long long* count, cudaStream_t st);
 void launch_band_collect(const BandFit& bf, const BandWork& w, const BandRuns& runs, int64_t cap,

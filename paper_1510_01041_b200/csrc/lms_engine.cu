@@ -1440,16 +1440,17 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
                             c->bflag.p, c->stream, c->blist.p);
       d_seed = c->blist.p + kSeedPool;
       st->launches += 2;
-    } else {
-      lmsb::launch_band_top(c->bwq.p, 0, K, K, kSeedBands, c->blist.p, c->bflag.p, c->stream);
-      st->launches += 1;
     }
     trace_mark(c, "top");
     // the window-edge pairs (usually the optimum itself) and, as a safety net,
     // up to 16 sampled vertices of each of the same bands, in one exact launch
     CUDA_TRY(cudaMemsetAsync(sc + 2, 0, sizeof(unsigned long long), c->stream));
-    lmsb::launch_band_edge_seeds(bf, ba, d_seed, kSeedBands, c->ranks.p, c->item_fit.p, seed_cap,
-                                 sc + 2, c->stream);
+    if (coarse)
+      lmsb::launch_band_edge_seeds(bf, ba, d_seed, kSeedBands, c->ranks.p, c->item_fit.p, seed_cap,
+                                   sc + 2, c->stream);
+    else  // the kSeedBands narrowest windows pick themselves (no top-k launch)
+      lmsb::launch_band_edge_seeds_top(bf, ba, kSeedBands, c->bflag.p, c->ranks.p, c->item_fit.p,
+                                       seed_cap, sc + 2, c->stream);
     lmsb::launch_band_seeds(bf, w, c->ranks.p, c->item_fit.p, 0, seed_cap, sc + 2, c->stream);
     RC_TRY(exact_list(sc + 2, seed_cap, c->ranks.p, c->item_fit.p));
     CUDA_TRY(cudaEventRecord(c->ev_chunk[7], c->stream));
