@@ -207,6 +207,29 @@ __device__ __forceinline__ bool keys_in_range(const BandFit& bf, double uL, doub
   return fmax(fabs(uL), fabs(uR)) * bf.dev + bf.bmax < 1e37;
 }
 
+// Slope bound of a band: at slope u the line values v_k = a_k u - b_k lie
+// within bmax of a_k u, so any window holding q of them is at least
+// |u| W_q(a) - 2 bmax wide, and a vertex's height is at least that window
+// (h_up, h_down each span q values at u; backend.py:153-159).  The
+// reference's roundings move it by <= 2^-48 (|u| amax + bmax); margins of
+// 2^-40 here.  Linear in |u|, so the band's smallest |u| bounds all of it
+// (fl32(u) in [b_{k-1}, b_k): |u| >= that end less 2^-20).  -inf when the
+// band reaches u = 0 or no W_q(a) bound is known.
+__device__ __forceinline__ double slope_lb(const BandFit& bf, const BandArgs& ba, int band) {
+  if (!ba.wqa) return -INFINITY;
+  const double wqa = *ba.wqa;
+  const double lo = band > 0 ? (double)ba.bounds[band - 1] : -INFINITY;
+  const double hi = band < ba.K - 1 ? (double)ba.bounds[band] : INFINITY;
+  double umin;
+  if (lo > 0.0) umin = lo;
+  else if (hi < 0.0) umin = -hi;
+  else return -INFINITY;
+  umin *= 1.0 - 0x1p-20;
+  const double slope = wqa * (1.0 - 0x1p-40) - 0x1p-40 * bf.amax;
+  if (!(slope > 0.0) || !isfinite(umin)) return -INFINITY;
+  return umin * slope * (1.0 - 0x1p-40) - 2.0 * bf.bmax * (1.0 + 0x1p-38) - 1e-300;
+}
+
 // sorted keys m_k = (a_k - c) uM - b_k of the band into sh.keys (the input
 // arrangement is irrelevant to a sort, so lines are loaded striped, i.e.
 // coalesced, and the result is written striped, i.e. bank-conflict free)
@@ -253,7 +276,7 @@ __global__ void __launch_bounds__(kThreads, 1) band_bound_kernel(BandFit bf, Ban
   double uL, uR;
   if (!boundary_extent(ba.bounds, ba.K, band, &uL, &uR) || !keys_in_range(bf, uL, uR)) {
     if (threadIdx.x == 0) {
-      ba.lb[band] = -INFINITY;  // outer / unbounded: always collected
+      ba.lb[band] = slope_lb(bf, ba, band);  // outer / unbounded: only the slope bound
       ba.wq[band] = INFINITY;
     }
     return;
@@ -280,7 +303,7 @@ __global__ void __launch_bounds__(kThreads, 1) band_bound_kernel(BandFit bf, Ban
   if (threadIdx.x == 0) {
     if (ba.edge && sh.kstar < n) write_edges(sh.keys, n, q, sh.kstar, ba.edge + (int64_t)band * 2 * kEdge);
     const double e = slack_base(bf, fmax(fabs(uL), fabs(uR)), uM) + 1e-300;
-    ba.lb[band] = (w - 2.0 * dmax - 2.0 * e) * (1.0 - 0x1p-40);
+    ba.lb[band] = fmax((w - 2.0 * dmax - 2.0 * e) * (1.0 - 0x1p-40), slope_lb(bf, ba, band));
     ba.wq[band] = w;
   }
 }
@@ -308,7 +331,7 @@ __global__ void __launch_bounds__(kCoarseThreads, 1) band_coarse_kernel(BandFit 
   double uL, uR;
   if (!boundary_extent(ba.bounds, ba.K, band, &uL, &uR) || !keys_in_range(bf, uL, uR)) {
     if (tid == 0) {
-      ba.lb[band] = -INFINITY;
+      ba.lb[band] = slope_lb(bf, ba, band);
       ba.wq[band] = INFINITY;
     }
     return;
@@ -384,7 +407,7 @@ __global__ void __launch_bounds__(kCoarseThreads, 1) band_coarse_kernel(BandFit 
   if (tid == 0) {
     const double w = fmax(best - 3.0, 0.0) * res;
     const double e = slack_base(bf, fmax(fabs(uL), fabs(uR)), uM) + 1e-300;
-    ba.lb[band] = (w - 2.0 * dmax - 2.0 * e) * (1.0 - 0x1p-40);
+    ba.lb[band] = fmax((w - 2.0 * dmax - 2.0 * e) * (1.0 - 0x1p-40), slope_lb(bf, ba, band));
     ba.wq[band] = est < INFINITY ? est * res : INFINITY;
   }
 }
@@ -1288,7 +1311,7 @@ __global__ void __launch_bounds__(1024) band_wq_kernel(BandFit bf, BandArgs ba, 
   double uL, uR;
   if (!boundary_extent(ba.bounds, ba.K, band, &uL, &uR) || !keys_in_range(bf, uL, uR)) {
     if (threadIdx.x == 0) {
-      ba.lb[band] = -INFINITY;
+      ba.lb[band] = slope_lb(bf, ba, band);
       ba.wq[band] = INFINITY;
     }
     return;
@@ -1314,7 +1337,7 @@ __global__ void __launch_bounds__(1024) band_wq_kernel(BandFit bf, BandArgs ba, 
     const double uM = 0.5 * uL + 0.5 * uR;
     const double dmax = bf.dev * fmax(uR - uM, uM - uL) * (1.0 + 0x1p-40);
     const double e = slack_base(bf, fmax(fabs(uL), fabs(uR)), uM) + 1e-300;
-    ba.lb[band] = (w - 2.0 * dmax - 2.0 * e) * (1.0 - 0x1p-40);
+    ba.lb[band] = fmax((w - 2.0 * dmax - 2.0 * e) * (1.0 - 0x1p-40), slope_lb(bf, ba, band));
     ba.wq[band] = w;
   }
   // keep the sorted keys of the band for the filter (admitted bands only use them)
@@ -2736,6 +2759,79 @@ void launch_band_plan(const BandFit& bf, const BandWork& w, const double* lb,
                       const DevPlan& dp, cudaStream_t st) {
   band_plan_kernel<<<1, kPlanThreads, 0, st>>>(bf, w.bounds, w.sample_counts, lb, best, K,
                                                sub_samples, bkeys_tau, dp);
+}
+
+// Lower bound of the narrowest window holding q of the slopes a_k: the a_k
+// binned linearly over [c - dev, c + dev] (which holds them all); a window
+// whose first slope falls in bin i ends in a bin >= j*(i), the first where
+// the counts from bin i reach q, so it is >= (j*(i) - i - 3) bin widths wide
+// (one bin, plus one either side for the binning's roundings).
+constexpr int kWqaBins = 8192;
+__global__ void __launch_bounds__(1024) line_wqa_kernel(BandFit bf, double* __restrict__ out) {
+  __shared__ unsigned P[kWqaBins + 1];
+  __shared__ unsigned wsum[32];
+  __shared__ double red[32];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int n = (int)bf.n, q = (int)bf.q;
+  const double lo = bf.c - bf.dev;
+  const double res = fmax(2.0 * bf.dev / kWqaBins, 1e-300) * (1.0 + 0x1p-30);
+  for (int b = tid; b <= kWqaBins; b += 1024) P[b] = 0;
+  __syncthreads();
+  for (int k = tid; k < n; k += 1024) {
+    const int b = (int)fmin(fmax(floor((__ldg(bf.a + k) - lo) / res), 0.0), kWqaBins - 1.0);
+    atomicAdd(P + b, 1u);
+  }
+  __syncthreads();
+  constexpr int kPer = kWqaBins / 1024;
+  unsigned mine[kPer], sum = 0;
+#pragma unroll
+  for (int e = 0; e < kPer; ++e) {
+    mine[e] = P[tid * kPer + e];
+    sum += mine[e];
+  }
+  unsigned incl = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) wsum[tid >> 5] = incl;
+  __syncthreads();
+  unsigned base = incl - sum;
+  for (int w = 0; w < (tid >> 5); ++w) base += wsum[w];
+  __syncthreads();
+#pragma unroll
+  for (int e = 0; e < kPer; ++e) {
+    P[tid * kPer + e] = base;  // keys in bins < tid * kPer + e
+    base += mine[e];
+  }
+  if (tid == 1023) P[kWqaBins] = base;
+  __syncthreads();
+  double best = INFINITY;
+  for (int b1 = tid; b1 < kWqaBins; b1 += 1024) {
+    const unsigned p1 = P[b1];
+    if (P[b1 + 1] == p1 || P[kWqaBins] - p1 < (unsigned)q) continue;
+    int a = b1, z = kWqaBins - 1;  // first b2 with P[b2 + 1] - p1 >= q
+    while (a < z) {
+      const int mid = (a + z) >> 1;
+      if (P[mid + 1] - p1 >= (unsigned)q) z = mid;
+      else a = mid + 1;
+    }
+    best = fmin(best, (double)(a - b1));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) best = fmin(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if (lane == 0) red[tid >> 5] = best;
+  __syncthreads();
+  if (tid == 0) {
+    double m = red[0];
+    for (int w = 1; w < 32; ++w) m = fmin(m, red[w]);
+    *out = isfinite(m) ? fmax(m - 3.0, 0.0) * res : 0.0;
+  }
+}
+
+void launch_line_wqa(const BandFit& bf, double* out, cudaStream_t st) {
+  line_wqa_kernel<<<1, 1024, 0, st>>>(bf, out);
 }
 
 }  // namespace lmsb

@@ -122,6 +122,10 @@ struct BandArgs {
   double* slice_res;
   unsigned* slice_ptab;       // per slice: bin table (band_slice_table_kernel)
   const uint8_t* narrow;      // optional, per band: 1 = one slice for the whole band
+  // optional: lower bound of the narrowest q-window of the lines' slopes a_k
+  // (line_wqa_kernel); every band bound is raised to the slope bound
+  // min |u| * W_q(a) - 2 bmax (slope_lb)
+  const double* wqa;
   const lms_candidate* best;  // the fit's current best record (H)
   int64_t* out_ranks;
   int32_t* out_fits;
@@ -172,6 +176,9 @@ size_t band_sample_temp_bytes(int64_t S);
 size_t band_group_temp_bytes(int64_t m);
 size_t band_collect_smem(int K);
 int launch_band_sample(const BandFit& bf, const BandWork& w, int sms, cudaStream_t st);
+// *out = a lower bound of the narrowest window of q of the lines' slopes a_k
+// (binned, one CTA)
+void launch_line_wqa(const BandFit& bf, double* out, cudaStream_t st);
 // mode 0: grid = bands [ba.band0, ba.band0 + grid) (their lower bounds); mode 1: grid >=
 // chunks of the listed bands
 void launch_band(const BandFit& bf, const BandArgs& ba, int mode, int grid, cudaStream_t st);

@@ -317,6 +317,11 @@ struct lms_ctx {
   int sub_samples = 1;     // LMSB_SUB_SAMPLES
   int filter_keys = 1;     // LMSB_FILTER_KEYS: store the bands' sorted keys (group_mode 3)
   double bkeys_tau = 0.1;  // LMSB_BKEYS_TAU
+  // LMSB_SLOPE_BOUND (default 1): band bounds raised to |u|min W_q(a) - 2 bmax
+  int slope_bound = 1;
+  DevBuf<double> bwqa;
+  uint64_t wqa_gen = ~0ull;
+  int64_t wqa_off = -1, wqa_n = -1, wqa_q = -1;
   int64_t collect_floor = 0;    // smallest member capacity (grown after a deferred overflow)
   bool cap_test = false;        // LMSB_CAP_TEST=1: first collect capacity 4,096 (overflow path)
   int64_t wide_chunk = 3072;    // LMSB_WIDE_CHUNK: members per filter chunk of a wide band
@@ -401,6 +406,7 @@ int ctx_init(lms_ctx* c, int device) {
   if (const char* bn = getenv("LMSB_BIG_NARROW")) c->big_narrow = atoi(bn) != 0;
   if (const char* ct = getenv("LMSB_CAP_TEST")) c->cap_test = atoi(ct) != 0;
   if (const char* dpl = getenv("LMSB_DEVICE_PLAN")) c->device_plan = atoi(dpl) != 0;
+  if (const char* sb = getenv("LMSB_SLOPE_BOUND")) c->slope_bound = atoi(sb) != 0;
   if (const char* wc = getenv("LMSB_WIDE_CHUNK"); wc && atoll(wc) >= 256) c->wide_chunk = atoll(wc);
   if (const char* nc = getenv("LMSB_NARROW_CHUNK"); nc && atoll(nc) >= 256)
     c->narrow_chunk = atoll(nc);
@@ -526,6 +532,7 @@ void ctx_release(lms_ctx* c) {
   c->dg_sub.release();
   c->bctab.release();
   c->bticket.release();
+  c->bwqa.release();
   c->bkeys.release();
   c->bnarrow.release();
   c->dp_hdr.release();
@@ -1057,6 +1064,18 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   }
   trace_mark(c, "interleave");
   bf.ab = c->bab.p;
+  // W_q of the slopes a_k (the slope bound of every band, slope_lb), kept
+  // while the lines, the fit and q are unchanged
+  RC_TRY(c->bwqa.need(1));
+  if (c->wqa_gen != c->gen || c->wqa_off != h.off || c->wqa_n != h.n || c->wqa_q != h.q ||
+      !c->slope_bound) {
+    lmsb::launch_line_wqa(bf, c->bwqa.p, c->stream);
+    st->launches += 1;
+    c->wqa_gen = c->gen;
+    c->wqa_off = h.off;
+    c->wqa_n = h.n;
+    c->wqa_q = h.q;
+  }
 
   // [0] valid samples [1] collected [2] seeds [3] band survivors [4] count survivors
   unsigned long long* sc = c->bscal.p;
@@ -1141,6 +1160,7 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   ba.edge = c->bedge.p;
   ba.best = c->best.p;
   ba.fit = 0;
+  ba.wqa = c->slope_bound ? c->bwqa.p : nullptr;
   // stored band keys: bounds computed here (or by this context's own plan
   // for an own-band search), not taken from a caller
   const bool use_bkeys = !big && c->filter_keys && c->group_mode == 3 &&

@@ -1125,3 +1125,45 @@ def test_device_plan_matches_host_plan(case):
         if k == "band_survivors":
             continue  # (chunk order differs: the running bound tightens at other points)
         assert sa[k] == sb[k], (case, k, sa[k], sb[k])
+
+
+@pytest.mark.parametrize("case", ["config2", "steep", "narrow_x", "dupx_majority", "huge_y", "small"])
+def test_slope_bound_matches_plain_bounds(case):
+    """Band bounds raised to the slope bound |u|min W_q(a) - 2 bmax (every
+    vertex at slope u is at least the narrowest q-window of the line values
+    there): identical records with and without it -- on config 2, a steep
+    line (large optimal |u|), x spread over a tiny range, a majority of
+    duplicate x (W_q(a) = 0: no bound), 1e12 outliers -- and against the
+    oracle at small n."""
+    rng = np.random.default_rng(33)
+    if case == "config2":
+        pts = workloads.contaminated_line_points(16384, 0)
+    elif case == "steep":
+        x = rng.uniform(0, 1, 6000)
+        y = 5000.0 * x + rng.normal(0, 1, 6000)
+        y[:2900] = rng.uniform(-1e4, 1e4, 2900)
+        pts = np.column_stack([x, y])
+    elif case == "narrow_x":
+        x = 1e3 + rng.uniform(0, 1e-6, 5000)
+        pts = np.column_stack([x, rng.normal(0, 1, 5000)])
+    elif case == "dupx_majority":
+        x = rng.uniform(0, 10, 5000)
+        x[:2600] = 3.0
+        pts = np.column_stack([x, x + rng.normal(0, 0.1, 5000)])
+    elif case == "huge_y":
+        pts = workloads.contaminated_line_points(5000, 5)
+        pts[:1000, 1] *= 1e8
+    else:
+        pts = workloads.contaminated_line_points(2600, 6)
+    n = len(pts)
+    q = n // 2 + 1
+    total = n * (n - 1) // 2
+    c0 = _ctx_env(LMSB_SLOPE_BOUND=0, LMSB_BAND=2)
+    c1 = _ctx_env(LMSB_SLOPE_BOUND=1, LMSB_BAND=2)
+    recs = []
+    for c in (c0, c1):
+        c.upload(pts[:, 0].copy(), pts[:, 1].copy())
+        recs.append(record_from_native(c.solve(q, 0, total)))
+    assert recs[0] == recs[1], case
+    if case == "small":
+        assert record_matches(recs[1], oracle_rec(pts[:, 0].copy(), pts[:, 1].copy(), q))
