@@ -115,6 +115,8 @@ struct SmallShared {
   };
   float bounds[kMaxBands - 1];
   double lb[kMaxBands], um[kMaxBands], wq[kMaxBands];
+  double slb[kMaxBands];  // slope bound of every band (keyless ones: dismissal test)
+  double wqa;             // lower bound of the narrowest q-window of the slopes a_k
   float edge[kMaxBands][2 * 5];  // keys around the ends of each band's narrowest q-window
   int egrp[2][16];               // edge-seed line groups
   int negrp[2];
@@ -387,6 +389,41 @@ __global__ void __launch_bounds__(kT, kT == kThreads ? LMSB_SMALL_MINB : 1) smal
     __syncthreads();
   }
 
+  // W_q of the slopes a_k (one warp sorts the centred slopes in fp32; each
+  // rounding moves a slope by <= 2^-24 dev): the slope bound |u| W_q(a) -
+  // 2 bmax of every band (lms_band.cu slope_lb)
+  if (warp == 0) {
+    float x[kItems];
+#pragma unroll
+    for (int e = 0; e < kItems; ++e) {
+      const int l = lane * kItems + e;
+      x[e] = l < n ? (float)__dsub_rn(sh.a[l], c) : INFINITY;
+    }
+    warp_bitonic_sort<kItems>(x);
+#pragma unroll
+    for (int e = 0; e < kItems; ++e) sh.wkeys[0][lane * kItems + e] = x[e];
+    __syncwarp();
+    double w = INFINITY;
+    for (int l = lane; l + q - 1 < n; l += 32)
+      w = fmin(w, (double)sh.wkeys[0][l + q - 1] - (double)sh.wkeys[0][l]);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) w = fmin(w, __shfl_xor_sync(0xffffffffu, w, off));
+    if (lane == 0) sh.wqa = isfinite(w) ? fmax(w - 0x1p-22 * dev, 0.0) : 0.0;
+  }
+  __syncthreads();
+  auto slope_bound = [&](int k) -> double {
+    const double lo = k > 0 ? (double)sh.bounds[k - 1] : -INFINITY;
+    const double hi = k < K - 1 ? (double)sh.bounds[k] : INFINITY;
+    double umin;
+    if (lo > 0.0) umin = lo;
+    else if (hi < 0.0) umin = -hi;
+    else return -INFINITY;
+    umin *= 1.0 - 0x1p-20;
+    const double slope = sh.wqa * (1.0 - 0x1p-40) - 0x1p-40 * am;
+    if (!(slope > 0.0) || !isfinite(umin) || huge) return -INFINITY;
+    return umin * slope * (1.0 - 0x1p-40) - 2.0 * bm * (1.0 + 0x1p-38) - 1e-300;
+  };
+
   long long t_mark = clock64();
   if (tid == 0) sh.cnt[4] = 0;
   // ---- per inner band (one warp each): sorted keys at the centre, lower bound
@@ -404,6 +441,7 @@ __global__ void __launch_bounds__(kT, kT == kThreads ? LMSB_SMALL_MINB : 1) smal
         sh.lb[k] = -INFINITY;  // no keys: members go straight to the fp32 counts
         sh.wq[k] = INFINITY;
         sh.um[k] = NAN;
+        sh.slb[k] = slope_bound(k);  // (unless the slope bound dismisses the band)
       }
       continue;
     }
@@ -431,7 +469,8 @@ __global__ void __launch_bounds__(kT, kT == kThreads ? LMSB_SMALL_MINB : 1) smal
     if (lane == 0) {
       const double dmax = dev * fmax(uR - uM, uM - uL) * (1.0 + 0x1p-40);
       const double e = 0x1p-20 * (fmax(fabs(uL), fabs(uR)) * am + bm + fabs(uM) * dev) + 1e-300;
-      sh.lb[k] = (w - 2.0 * dmax - 2.0 * e) * (1.0 - 0x1p-40);
+      sh.slb[k] = slope_bound(k);
+      sh.lb[k] = fmax((w - 2.0 * dmax - 2.0 * e) * (1.0 - 0x1p-40), sh.slb[k]);
       sh.wq[k] = w;
       sh.um[k] = uM;
     }
@@ -534,6 +573,8 @@ __global__ void __launch_bounds__(kT, kT == kThreads ? LMSB_SMALL_MINB : 1) smal
     int na = 0;
     for (int k = 0; k < K; ++k) {
       sh.band_slot[k] = -1;
+      // a keyless band the slope bound dismisses: neither keyless nor admitted
+      if (!(sh.lb[k] > -INFINITY) && sh.slb[k] > H * (1.0 + 0x1p-19)) sh.lb[k] = INFINITY;
       if (sh.lb[k] > -INFINITY && sh.lb[k] <= H * (1.0 + 0x1p-19)) sh.admitted[na++] = k;
     }
     sh.nadmitted = na;
