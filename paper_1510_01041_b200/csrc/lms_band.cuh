@@ -300,6 +300,10 @@ struct SweepArgs {
   // device (nruns / tau are then the maxima / unused)
   const int32_t* dnr;
   const double* dtau;
+  // deferred member count (no readback before the grouping): a raw-buffer
+  // overflow is flagged here instead of raising `count` past the members
+  // actually written (the grouping reads min(count, cap) of them)
+  unsigned long long* raw_overflow;
 };
 size_t sweep_chunk_smem();
 // sort nseg segments of the n lines by their end keys; returns launches

@@ -190,6 +190,7 @@ struct lms_ctx {
   // LMSB_TRACE=1: an event after every stage of a band solve, the stage
   // times printed to stderr (one JSON line per solve)
   bool trace = false;
+  bool sync_check = false;  // LMSB_SYNC_CHECK=1: synchronise after every traced stage
   std::vector<cudaEvent_t> tr_ev;
   std::vector<const char*> tr_lab;
   int tr_n = 0;
@@ -425,6 +426,7 @@ int ctx_init(lms_ctx* c, int device) {
   const char* bc = getenv("LMSB_BAND_CHUNK");
   if (bc && atoll(bc) >= 32) c->band_chunk = atoll(bc);
   if (const char* tr = getenv("LMSB_TRACE")) c->trace = atoi(tr) != 0;
+  if (const char* sc = getenv("LMSB_SYNC_CHECK")) c->sync_check = atoi(sc) != 0;
   CUDA_TRY(cudaSetDevice(device));
   CUDA_TRY(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device));
   CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
@@ -757,6 +759,10 @@ int ensure_host_best(lms_ctx* c, int64_t nfits) {
 }
 
 void trace_mark(lms_ctx* c, const char* label) {
+  if (c->sync_check) {  // (debugging) the first stage whose kernels fault
+    const cudaError_t e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) fprintf(stderr, "LMSB_SYNC_CHECK: stage %s: %s\n", label, cudaGetErrorString(e));
+  }
   if (!c->trace) return;
   if (c->tr_n >= (int)c->tr_ev.size()) {
     cudaEvent_t e;
@@ -944,6 +950,7 @@ int devplan_search(lms_ctx* c, const HostFit& h, lms_stats* st, const lmsb::Band
   sa.raw = c->sw_raw.p;
   sa.raw_cap = cap;
   sa.raw_count = c->sw_rawcnt.p;
+  sa.raw_overflow = sc + 8;
   sa.sub_first = c->dp_sbf.p;
   sa.sub = c->dg_sub.p;
   CUDA_TRY(cudaEventRecord(c->ev_chunk[2], c->stream));
@@ -1023,7 +1030,7 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   RC_TRY(c->bbounds.need(K));
   RC_TRY(c->bscnt.need(K));
   RC_TRY(c->bflag.need(K + 1));
-  RC_TRY(c->bscal.need(8));  // [5]: running best height bits of the exact launches, [6]: prepass,
+  RC_TRY(c->bscal.need(9));  // [5]: running best height bits of the exact launches, [6]: prepass,
                              // [7]: filter chunks of the sub-band grouping
   RC_TRY(c->bstart.need(K + 1));
   RC_TRY(c->bend.need(K + 1));
@@ -1080,6 +1087,7 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   // [0] valid samples [1] collected [2] seeds [3] band survivors [4] count survivors
   unsigned long long* sc = c->bscal.p;
   CUDA_TRY(cudaMemsetAsync(sc + 5, 0xFF, sizeof(unsigned long long), c->stream));  // no height yet
+  CUDA_TRY(cudaMemsetAsync(sc + 8, 0, sizeof(unsigned long long), c->stream));  // raw overflow
   lmsb::BandWork w{};
   w.S = S;
   w.K = K;
@@ -1931,6 +1939,7 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
       sa.raw = c->sw_raw.p;
       sa.raw_cap = cap;
       sa.raw_count = c->sw_rawcnt.p;
+      sa.raw_overflow = subgrp ? sc + 8 : nullptr;  // (deferred count: flagged, not counted)
       CUDA_TRY(cudaEventRecord(c->ev_chunk[10], c->stream));
       lmsb::launch_sweep_emit(bf, sa, c->sms, c->stream);
       trace_mark(c, "sweep_emit");
@@ -2144,14 +2153,16 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   }
   CUDA_TRY(cudaEventRecord(c->ev_chunk[4], c->stream));
   unsigned long long* cnts = reinterpret_cast<unsigned long long*>(c->pin);  // readbacks done
-  CUDA_TRY(cudaMemcpyAsync(cnts, sc + 1, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+  CUDA_TRY(cudaMemcpyAsync(cnts, sc + 1, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                            c->stream));
   lmsb::DevPlanHdr* ph = reinterpret_cast<lmsb::DevPlanHdr*>(c->pin + 128);
   if (dplan)
     CUDA_TRY(cudaMemcpyAsync(ph, c->dp_hdr.p, sizeof(lmsb::DevPlanHdr), cudaMemcpyDeviceToHost,
                              c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
-  const unsigned long long m_dev = cnts[0];
+  // members classified, or the raw enumeration count when the raw buffer
+  // overflowed (then not every member was seen)
+  const unsigned long long m_dev = std::max(cnts[0], cnts[7]);
   cnts += 2;  // [0] band survivors .. [3] exact-stage inputs, as before
   if (dplan) {
     const lmsb::DevPlanHdr hd = *ph;

@@ -534,7 +534,9 @@ __global__ void __launch_bounds__(256) sweep_classify_kernel(BandFit bf, SweepAr
 // caller grows both and enumerates again)
 __global__ void sweep_overflow_kernel(SweepArgs sa) {
   const unsigned long long raw = *sa.raw_count;
-  if ((int64_t)raw > sa.raw_cap && *sa.count < raw) *sa.count = raw;
+  if ((int64_t)raw <= sa.raw_cap) return;
+  if (sa.raw_overflow) *sa.raw_overflow = raw;
+  else if (*sa.count < raw) *sa.count = raw;
 }
 
 // Nearly parallel pairs (0 < |a_i - a_j| <= tau): lines sorted by a, each
