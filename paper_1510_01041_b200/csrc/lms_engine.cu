@@ -24,6 +24,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <condition_variable>
+#include <atomic>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -82,9 +83,14 @@ constexpr int64_t kBandMinSpan = 3 << 19;    // smaller fits: seeds + count filt
                                               // (measured crossover n ~ 1,800: 1.6 M pairs)
 constexpr int kNumEvents = 16;
 
+// bumped by every device allocation: a captured CUDA graph holds buffer
+// addresses, so it is valid only while the epoch it was captured at lasts
+std::atomic<uint64_t> g_buf_epoch{0};
+
 template <typename T>
 int grow(T** ptr, int64_t* cap, int64_t need) {
   if (need <= *cap) return LMS_OK;
+  g_buf_epoch.fetch_add(1);
   if (*ptr) cudaFree(*ptr);
   *ptr = nullptr;
   *cap = 0;
@@ -349,6 +355,14 @@ struct lms_ctx {
   // same n has sized the member buffers (plan_cap); a plan the device cannot
   // make, or a member overflow, re-solves with the host plan
   int device_plan = 1;
+  // LMSB_GRAPH (default 1): a device-planned search is captured into a CUDA
+  // graph on its second identical run (same shape, line statistics, buffer
+  // addresses) and replayed from then on -- one launch instead of ~45
+  int use_graph = 1;
+  cudaGraphExec_t gexec = nullptr;
+  unsigned char gkey[160] = {0}, gseen[160] = {0};
+  int64_t g_launches = 0;
+  bool capturing = false;  // a band search is being captured on `stream`
   int64_t plan_cap = 0, plan_cap_n = -1;
   bool force_host_plan = false;
   DevBuf<lmsb::DevPlanHdr> dp_hdr;
@@ -407,6 +421,7 @@ int ctx_init(lms_ctx* c, int device) {
   if (const char* bn = getenv("LMSB_BIG_NARROW")) c->big_narrow = atoi(bn) != 0;
   if (const char* ct = getenv("LMSB_CAP_TEST")) c->cap_test = atoi(ct) != 0;
   if (const char* dpl = getenv("LMSB_DEVICE_PLAN")) c->device_plan = atoi(dpl) != 0;
+  if (const char* gr = getenv("LMSB_GRAPH")) c->use_graph = atoi(gr) != 0;
   if (const char* sb = getenv("LMSB_SLOPE_BOUND")) c->slope_bound = atoi(sb) != 0;
   if (const char* wc = getenv("LMSB_WIDE_CHUNK"); wc && atoll(wc) >= 256) c->wide_chunk = atoll(wc);
   if (const char* nc = getenv("LMSB_NARROW_CHUNK"); nc && atoll(nc) >= 256)
@@ -537,6 +552,8 @@ void ctx_release(lms_ctx* c) {
   c->bwqa.release();
   c->bkeys.release();
   c->bnarrow.release();
+  if (c->gexec) cudaGraphExecDestroy(c->gexec);
+  c->gexec = nullptr;
   c->dp_hdr.release();
   c->dp_list.release();
   c->dp_ident.release();
@@ -758,6 +775,13 @@ int ensure_host_best(lms_ctx* c, int64_t nfits) {
   return LMS_OK;
 }
 
+// stage events: inside a CUDA-graph capture recorded as external event
+// nodes (their times stay readable after each replay)
+cudaError_t ev_rec(lms_ctx* c, cudaEvent_t e) {
+  return c->capturing ? cudaEventRecordWithFlags(e, c->stream, cudaEventRecordExternal)
+                      : cudaEventRecord(e, c->stream);
+}
+
 void trace_mark(lms_ctx* c, const char* label) {
   if (c->sync_check) {  // (debugging) the first stage whose kernels fault
     const cudaError_t e = cudaStreamSynchronize(c->stream);
@@ -953,12 +977,12 @@ int devplan_search(lms_ctx* c, const HostFit& h, lms_stats* st, const lmsb::Band
   sa.raw_overflow = sc + 8;
   sa.sub_first = c->dp_sbf.p;
   sa.sub = c->dg_sub.p;
-  CUDA_TRY(cudaEventRecord(c->ev_chunk[2], c->stream));
-  CUDA_TRY(cudaEventRecord(c->ev_chunk[5], c->stream));
-  CUDA_TRY(cudaEventRecord(c->ev_chunk[10], c->stream));
+  CUDA_TRY(ev_rec(c, c->ev_chunk[2]));
+  CUDA_TRY(ev_rec(c, c->ev_chunk[5]));
+  CUDA_TRY(ev_rec(c, c->ev_chunk[10]));
   lmsb::launch_sweep_emit(bf, sa, c->sms, c->stream);
-  CUDA_TRY(cudaEventRecord(c->ev_chunk[11], c->stream));
-  CUDA_TRY(cudaEventRecord(c->ev_chunk[6], c->stream));
+  CUDA_TRY(ev_rec(c, c->ev_chunk[11]));
+  CUDA_TRY(ev_rec(c, c->ev_chunk[6]));
   st->launches += 3;
   trace_mark(c, "sweep_emit");
   // grouping with device counts, then the chunk table
@@ -992,7 +1016,112 @@ int devplan_search(lms_ctx* c, const HostFit& h, lms_stats* st, const lmsb::Band
   return LMS_OK;
 }
 
+struct BandTail {
+  unsigned long long m;  // member capacity the search ran with (or the exact count)
+  bool direct, dplan, filter_timed, bound_timed, sweep_timed;
+};
+
+// The end of a band search: the one readback (counts, the device plan's
+// header), the overflow / bail re-solves, the stage times.
+int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st);
+
+int band_finish(lms_ctx* c, const HostFit& h, lms_stats* st, BandTail t) {
+  unsigned long long* sc = c->bscal.p;
+  unsigned long long m = t.m;
+  const bool direct = t.direct, dplan = t.dplan;
+  const bool filter_timed = t.filter_timed, bound_timed = t.bound_timed,
+             sweep_timed = t.sweep_timed;
+  unsigned long long* cnts = reinterpret_cast<unsigned long long*>(c->pin);  // readbacks done
+  CUDA_TRY(cudaMemcpyAsync(cnts, sc + 1, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                           c->stream));
+  lmsb::DevPlanHdr* ph = reinterpret_cast<lmsb::DevPlanHdr*>(c->pin + 128);
+  if (dplan)
+    CUDA_TRY(cudaMemcpyAsync(ph, c->dp_hdr.p, sizeof(lmsb::DevPlanHdr), cudaMemcpyDeviceToHost,
+                             c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  // members classified, or the raw enumeration count when the raw buffer
+  // overflowed (then not every member was seen)
+  const unsigned long long m_dev = std::max(cnts[0], cnts[7]);
+  cnts += 2;  // [0] band survivors .. [3] exact-stage inputs, as before
+  if (dplan) {
+    const lmsb::DevPlanHdr hd = *ph;
+    if (hd.bail || m_dev > m) {
+      // the device could not plan this fit, or the members outgrew the
+      // capacity: solve again with the host plan (which also resizes)
+      if (m_dev > m) c->plan_cap = std::max<int64_t>(c->plan_cap, (int64_t)m_dev + m_dev / 4);
+      trace_dump(c);
+      c->force_host_plan = true;
+      const int rc = band_solve(c, h, st);
+      c->force_host_plan = false;
+      return rc;
+    }
+    st->bands_searched = hd.nadm;
+    st->seed_height = hd.H;
+    st->sweep_runs = hd.nr;
+  }
+  if (m_dev > m && !direct) {
+    // deferred member count above the capacity: members were dropped, so
+    // solve again with room for all of them (the record found so far stays
+    // installed; it is a real vertex)
+    c->collect_floor = (int64_t)m_dev;
+    trace_dump(c);
+    return band_solve(c, h, st);
+  }
+  m = m_dev;
+  st->survivors = (int64_t)cnts[3];
+  trace_mark(c, "readback3");
+  trace_dump(c);  // evaluated by the exact select (cnts[2]: running height)
+  st->band_survivors = (int64_t)cnts[0];
+  st->filtered_vertices = (int64_t)m;
+  st->chunks = 1;
+  float ms = 0.f;
+  CUDA_TRY(cudaEventElapsedTime(&ms, c->ev_chunk[0], c->ev_chunk[1]));
+  st->ms_bound = ms;
+  CUDA_TRY(cudaEventElapsedTime(&ms, c->ev_chunk[2], c->ev_chunk[3]));
+  st->ms_partition = ms;
+  CUDA_TRY(cudaEventElapsedTime(&ms, c->ev_chunk[3], c->ev_chunk[4]));
+  st->ms_band_filter = ms;
+  CUDA_TRY(cudaEventElapsedTime(&ms, c->ev_chunk[5], c->ev_chunk[6]));
+  st->ms_collect = ms;
+  st->ms_filter_kernel = 0.f;
+  if (filter_timed) {
+    CUDA_TRY(cudaEventElapsedTime(&ms, c->ev_chunk[8], c->ev_chunk[9]));
+    st->ms_filter_kernel = ms;
+  }
+  st->ms_bound_kernel = 0.f;
+  if (bound_timed) {
+    CUDA_TRY(cudaEventElapsedTime(&ms, c->ev_chunk[12], c->ev_chunk[13]));
+    st->ms_bound_kernel = ms;
+  }
+  st->ms_sweep_enum = 0.f;
+  if (sweep_timed) {
+    CUDA_TRY(cudaEventElapsedTime(&ms, c->ev_chunk[10], c->ev_chunk[11]));
+    st->ms_sweep_enum = ms;
+  }
+  if (getenv("LMSB_BAND_DEBUG")) {
+    float t[6];
+    cudaEventElapsedTime(&t[0], c->ev_chunk[0], c->ev_chunk[1]);
+    cudaEventElapsedTime(&t[1], c->ev_chunk[1], c->ev_chunk[7]);
+    cudaEventElapsedTime(&t[2], c->ev_chunk[7], c->ev_chunk[2]);
+    cudaEventElapsedTime(&t[3], c->ev_chunk[2], c->ev_chunk[3]);
+    cudaEventElapsedTime(&t[4], c->ev_chunk[3], c->ev_chunk[4]);
+    cudaEventElapsedTime(&t[5], c->ev_begin, c->ev_chunk[0]);
+    fprintf(stderr,
+            "band: pre %.3f bound %.3f seeds %.3f gap %.3f collect+group %.3f filter+count+exact %.3f ms\n",
+            t[5], t[0], t[1], t[2], t[3], t[4]);
+  }
+  return LMS_OK;
+}
+
 int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
+  if (c->capturing) {  // a capture an error path left open: drop it, no graphs
+    cudaGraph_t g = nullptr;
+    cudaStreamEndCapture(c->stream, &g);
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();
+    c->capturing = false;
+    c->use_graph = 0;
+  }
   const int64_t span = h.r1 - h.r0;
   bool filter_timed = false, sweep_timed = false, bound_timed = false;
   ShardSpec* sh = c->shard;
@@ -1057,11 +1186,73 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   bf.dev = std::max(ahi - bf.c, bf.c - alo) * (1.0 + 0x1p-40) + 1e-300;
   bf.amax = am;
   bf.bmax = bmx;
+  // ---- CUDA graph: a device-planned search (no host step between its
+  // launches) is captured on the second fit with the same key -- shape, line
+  // statistics (the kernels' by-value arguments), member capacity, buffer
+  // epoch -- and replayed from then on; the replay recomputes everything from
+  // the lines in the context's buffers
+  const bool sweep_n = (c->band_sweep == 1 || (c->band_sweep == 2 && h.n >= kSweepMinN)) &&
+                       h.n <= lmsb::kBandMaxBigN;
+  const bool dplan_pre = c->device_plan && !sh && !big && !coarse && c->filter_keys &&
+                         c->group_mode == 3 && !c->band_direct && sweep_n &&
+                         K <= lmsb::kPlanMaxK && c->plan_cap_n == h.n && c->plan_cap > 0 &&
+                         !c->force_host_plan;
+  const bool graph_ok = c->use_graph && dplan_pre && !c->trace && !c->sync_check;
+  unsigned char gk[sizeof(c->gkey)];
+  std::memset(gk, 0, sizeof(gk));
+  const uint64_t epoch0 = g_buf_epoch.load();
+  {
+    struct GraphKey {
+      int64_t n, q, off, r0, span, P0, pspan, K, S, cap, wide, narrow, sub;
+      uint64_t epoch;
+      double c, dev, amax, bmax, tau;
+    } key;
+    std::memset(&key, 0, sizeof(key));
+    key.n = h.n;
+    key.q = h.q;
+    key.off = h.off;
+    key.r0 = h.r0;
+    key.span = span;
+    key.P0 = P0;
+    key.pspan = pspan;
+    key.K = K;
+    key.S = S;
+    key.cap = c->plan_cap;
+    key.wide = c->wide_chunk;
+    key.narrow = c->narrow_chunk;
+    key.sub = c->sub_samples;
+    key.epoch = epoch0;
+    key.c = bf.c;
+    key.dev = bf.dev;
+    key.amax = bf.amax;
+    key.bmax = bf.bmax;
+    key.tau = c->bkeys_tau;
+    static_assert(sizeof(key) <= sizeof(gk), "graph key size");
+    std::memcpy(gk, &key, sizeof(key));
+  }
+  if (graph_ok && c->gexec && std::memcmp(gk, c->gkey, sizeof(gk)) == 0) {
+    CUDA_TRY(cudaGraphLaunch(c->gexec, c->stream));
+    st->launches += c->g_launches;
+    st->bands = K;
+    return band_finish(c, h, st,
+                       BandTail{(unsigned long long)c->plan_cap, false, true, true, true, true});
+  }
+  bool capturing = false;
+  int64_t launches0 = st->launches;
+  if (graph_ok) {
+    if (std::memcmp(gk, c->gseen, sizeof(gk)) == 0) {
+      CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeRelaxed));
+      capturing = true;
+      c->capturing = true;
+    }
+    std::memcpy(c->gseen, gk, sizeof(gk));
+  }
   trace_mark(c, "begin");
   // interleaved copy of the fit's lines for the collect pass (kept while the
   // bound lines and the fit's offset are unchanged)
   RC_TRY(c->bab.need(h.n));
-  if (c->ab_gen != c->gen || c->ab_off != h.off || c->ab_n != h.n || c->ab_ptr != c->bab.p) {
+  if (capturing || c->ab_gen != c->gen || c->ab_off != h.off || c->ab_n != h.n ||
+      c->ab_ptr != c->bab.p) {
     lmsb::launch_band_interleave(bf.a, bf.b, h.n, c->bab.p, c->stream);
     st->launches += 1;
     c->ab_gen = c->gen;
@@ -1074,8 +1265,8 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   // W_q of the slopes a_k (the slope bound of every band, slope_lb), kept
   // while the lines, the fit and q are unchanged
   RC_TRY(c->bwqa.need(1));
-  if (c->wqa_gen != c->gen || c->wqa_off != h.off || c->wqa_n != h.n || c->wqa_q != h.q ||
-      !c->slope_bound) {
+  if (capturing || c->wqa_gen != c->gen || c->wqa_off != h.off || c->wqa_n != h.n ||
+      c->wqa_q != h.q || !c->slope_bound) {
     lmsb::launch_line_wqa(bf, c->bwqa.p, c->stream);
     st->launches += 1;
     c->wqa_gen = c->gen;
@@ -1138,7 +1329,7 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   };
 
   // ---- sample, boundaries, per-band lower bounds
-  CUDA_TRY(cudaEventRecord(c->ev_chunk[0], c->stream));
+  CUDA_TRY(ev_rec(c, c->ev_chunk[0]));
   // a shard search reuses its context's plan (samples, boundaries, counts)
   // when the same fit was planned on it last
   ShardPlanState& sp = c->splan;
@@ -1199,9 +1390,9 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
       st->launches += 4 * ((k1 - k0 + kBatch - 1) / kBatch);
     }
   } else if (k1 > k0 && !coarse) {
-    CUDA_TRY(cudaEventRecord(c->ev_chunk[12], c->stream));
+    CUDA_TRY(ev_rec(c, c->ev_chunk[12]));
     lmsb::launch_band(bf, ba, 0, (int)(k1 - k0), c->stream);
-    CUDA_TRY(cudaEventRecord(c->ev_chunk[13], c->stream));
+    CUDA_TRY(ev_rec(c, c->ev_chunk[13]));
     bound_timed = true;
     st->launches += 1;
   }
@@ -1368,7 +1559,7 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     sp.pspan = pspan;
     st->bands = K;
     st->seed_height = sh->seed_out.found ? sh->seed_out.height : INFINITY;
-    CUDA_TRY(cudaEventRecord(c->ev_chunk[1], c->stream));
+    CUDA_TRY(ev_rec(c, c->ev_chunk[1]));
     return LMS_OK;
   }
 
@@ -1403,8 +1594,8 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     scnt = sp.h_scnt;
     lb = sp.h_lb;
     wq.assign(K, INFINITY);
-    CUDA_TRY(cudaEventRecord(c->ev_chunk[1], c->stream));
-    CUDA_TRY(cudaEventRecord(c->ev_chunk[7], c->stream));
+    CUDA_TRY(ev_rec(c, c->ev_chunk[1]));
+    CUDA_TRY(ev_rec(c, c->ev_chunk[7]));
   } else if (sh && sh->mode == 2) {
     // ---- search: every band's bound and the global seed record from the
     // caller (the exchanged plan); boundaries and counts from this context's
@@ -1450,10 +1641,10 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     }
     lb.assign(sh->lb_in, sh->lb_in + K);
     wq.assign(sh->wq_in, sh->wq_in + K);
-    CUDA_TRY(cudaEventRecord(c->ev_chunk[1], c->stream));
-    CUDA_TRY(cudaEventRecord(c->ev_chunk[7], c->stream));
+    CUDA_TRY(ev_rec(c, c->ev_chunk[1]));
+    CUDA_TRY(ev_rec(c, c->ev_chunk[7]));
   } else {
-    CUDA_TRY(cudaEventRecord(c->ev_chunk[1], c->stream));
+    CUDA_TRY(ev_rec(c, c->ev_chunk[1]));
     // ---- seeds, picked on the device (no round trip after the bounds): the
     // bands with the narrowest q-windows at their centre slope (the bands an
     // LMS line of that slope would come from); with coarse bounds a pool of
@@ -1481,7 +1672,7 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
                                        seed_cap, sc + 2, c->stream);
     lmsb::launch_band_seeds(bf, w, c->ranks.p, c->item_fit.p, 0, seed_cap, sc + 2, c->stream);
     RC_TRY(exact_list(sc + 2, seed_cap, c->ranks.p, c->item_fit.p));
-    CUDA_TRY(cudaEventRecord(c->ev_chunk[7], c->stream));
+    CUDA_TRY(ev_rec(c, c->ev_chunk[7]));
     trace_mark(c, "seeds");
     if (!dplan) {
     // one readback: bounds, window widths, boundaries, the seed record, counts
@@ -1504,6 +1695,16 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     H = hb.found ? hb.height : INFINITY;
     trace_mark(c, "readback1");
     }
+  }
+  if (capturing && !dplan) {  // (cannot happen: the key's conditions are dplan's)
+    cudaGraph_t g = nullptr;
+    cudaStreamEndCapture(c->stream, &g);
+    c->capturing = false;
+    if (g) cudaGraphDestroy(g);
+    c->use_graph = 0;
+    c->ab_gen = ~0ull;
+    c->wqa_gen = ~0ull;
+    return band_solve(c, h, st);
   }
   // (set by the host plan below, or by the device plan)
   std::vector<int32_t> list;
@@ -1635,7 +1836,7 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     }
   }
   trace_mark(c, "plan_upload");
-  CUDA_TRY(cudaEventRecord(c->ev_chunk[2], c->stream));
+  CUDA_TRY(ev_rec(c, c->ev_chunk[2]));
   // direct grouping into sub-band regions (falls back to the sorting path on a
   // region overflow)
   std::vector<int64_t> gstart, gend;
@@ -1715,9 +1916,9 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
       dg.cap = d_cap;
       dg.rstart = d_rstart;
       dg.members = c->bmem.p;
-      CUDA_TRY(cudaEventRecord(c->ev_chunk[5], c->stream));
+      CUDA_TRY(ev_rec(c, c->ev_chunk[5]));
       lmsb::launch_band_collect_direct(bf, w, runs, dg, c->sms, c->stream);
-      CUDA_TRY(cudaEventRecord(c->ev_chunk[6], c->stream));
+      CUDA_TRY(ev_rec(c, c->ev_chunk[6]));
       CUDA_TRY(cudaGetLastError());
       st->launches += 2;
       std::vector<unsigned long long> cur(ngroups);
@@ -1843,7 +2044,7 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
       ss.k1[b] = c->sw_k1.p + b * nseg * nn;
       ss.idx[b] = c->sw_idx.p + b * nseg * nn;
     }
-    CUDA_TRY(cudaEventRecord(c->ev_chunk[5], c->stream));
+    CUDA_TRY(ev_rec(c, c->ev_chunk[5]));
     st->launches += lmsb::launch_sweep_sort(bf.ab, (int)nn, c->sw_ends.p, nseg, ss, c->sms,
                                             c->stream);
     trace_mark(c, "sweep_sort");
@@ -1940,18 +2141,18 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
       sa.raw_cap = cap;
       sa.raw_count = c->sw_rawcnt.p;
       sa.raw_overflow = subgrp ? sc + 8 : nullptr;  // (deferred count: flagged, not counted)
-      CUDA_TRY(cudaEventRecord(c->ev_chunk[10], c->stream));
+      CUDA_TRY(ev_rec(c, c->ev_chunk[10]));
       lmsb::launch_sweep_emit(bf, sa, c->sms, c->stream);
       trace_mark(c, "sweep_emit");
-      CUDA_TRY(cudaEventRecord(c->ev_chunk[11], c->stream));
+      CUDA_TRY(ev_rec(c, c->ev_chunk[11]));
       sweep_timed = true;
       st->launches += 2;
     } else {
-      CUDA_TRY(cudaEventRecord(c->ev_chunk[5], c->stream));
+      CUDA_TRY(ev_rec(c, c->ev_chunk[5]));
       lmsb::launch_band_collect(bf, w, runs, cap, c->sms, c->stream);
       st->launches += 1;
     }
-    CUDA_TRY(cudaEventRecord(c->ev_chunk[6], c->stream));
+    CUDA_TRY(ev_rec(c, c->ev_chunk[6]));
     CUDA_TRY(cudaGetLastError());
     if (sweep && sa.dbg) {
       std::vector<unsigned long long> d(sa.nruns);
@@ -2019,7 +2220,7 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   }
   }
   }
-  CUDA_TRY(cudaEventRecord(c->ev_chunk[3], c->stream));
+  CUDA_TRY(ev_rec(c, c->ev_chunk[3]));
 
   // ---- window counts of the collected vertices; fp32 counts at each
   // survivor's own slope; exact select of the most promising few (tightens H),
@@ -2101,15 +2302,15 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
         return set_error(LMS_ERR_CUDA, "large-n slice sort failed");
       trace_mark(c, "slices");
       st->launches += 4;
-      CUDA_TRY(cudaEventRecord(c->ev_chunk[8], c->stream));
+      CUDA_TRY(ev_rec(c, c->ev_chunk[8]));
       lmsb::launch_band_filter_big(bf, ba, c->bslice_store.p, fgrid, c->stream);
       trace_mark(c, "filter_big");
-      CUDA_TRY(cudaEventRecord(c->ev_chunk[9], c->stream));
+      CUDA_TRY(ev_rec(c, c->ev_chunk[9]));
     } else {
-      CUDA_TRY(cudaEventRecord(c->ev_chunk[8], c->stream));
+      CUDA_TRY(ev_rec(c, c->ev_chunk[8]));
       lmsb::launch_band(bf, ba, 1, fgrid, c->stream);
       trace_mark(c, "filter");
-      CUDA_TRY(cudaEventRecord(c->ev_chunk[9], c->stream));
+      CUDA_TRY(ev_rec(c, c->ev_chunk[9]));
     }
     filter_timed = true;
     lmsb::BandCount bc{};
@@ -2151,87 +2352,35 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     RC_TRY(exact_list(sc + 6, scap, c->ranks.p, c->item_fit.p));
     trace_mark(c, "exact");
   }
-  CUDA_TRY(cudaEventRecord(c->ev_chunk[4], c->stream));
-  unsigned long long* cnts = reinterpret_cast<unsigned long long*>(c->pin);  // readbacks done
-  CUDA_TRY(cudaMemcpyAsync(cnts, sc + 1, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                           c->stream));
-  lmsb::DevPlanHdr* ph = reinterpret_cast<lmsb::DevPlanHdr*>(c->pin + 128);
-  if (dplan)
-    CUDA_TRY(cudaMemcpyAsync(ph, c->dp_hdr.p, sizeof(lmsb::DevPlanHdr), cudaMemcpyDeviceToHost,
-                             c->stream));
-  CUDA_TRY(cudaStreamSynchronize(c->stream));
-  // members classified, or the raw enumeration count when the raw buffer
-  // overflowed (then not every member was seen)
-  const unsigned long long m_dev = std::max(cnts[0], cnts[7]);
-  cnts += 2;  // [0] band survivors .. [3] exact-stage inputs, as before
-  if (dplan) {
-    const lmsb::DevPlanHdr hd = *ph;
-    if (hd.bail || m_dev > m) {
-      // the device could not plan this fit, or the members outgrew the
-      // capacity: solve again with the host plan (which also resizes)
-      if (m_dev > m) c->plan_cap = std::max<int64_t>(c->plan_cap, (int64_t)m_dev + m_dev / 4);
-      trace_dump(c);
-      c->force_host_plan = true;
-      const int rc = band_solve(c, h, st);
-      c->force_host_plan = false;
-      return rc;
+  CUDA_TRY(ev_rec(c, c->ev_chunk[4]));
+  if (capturing) {
+    // the whole search captured: instantiate and run it (replayed by the
+    // next identical fit)
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(c->stream, &graph);
+    c->capturing = false;
+    cudaGraphExec_t ex = nullptr;
+    bool ok = ce == cudaSuccess && graph &&
+              cudaGraphInstantiate(&ex, graph, 0) == cudaSuccess &&
+              g_buf_epoch.load() == epoch0;
+    if (graph) cudaGraphDestroy(graph);
+    if (!ok) {
+      // nothing of the captured search ran: solve again with direct launches
+      // (and without the caches the capture marked as filled)
+      if (ex) cudaGraphExecDestroy(ex);
+      cudaGetLastError();
+      c->use_graph = 0;
+      c->ab_gen = ~0ull;
+      c->wqa_gen = ~0ull;
+      return band_solve(c, h, st);
     }
-    st->bands_searched = hd.nadm;
-    st->seed_height = hd.H;
-    st->sweep_runs = hd.nr;
+    if (c->gexec) cudaGraphExecDestroy(c->gexec);
+    c->gexec = ex;
+    std::memcpy(c->gkey, gk, sizeof(gk));
+    c->g_launches = st->launches - launches0;
+    CUDA_TRY(cudaGraphLaunch(c->gexec, c->stream));
   }
-  if (m_dev > m && !direct) {
-    // deferred member count above the capacity: members were dropped, so
-    // solve again with room for all of them (the record found so far stays
-    // installed; it is a real vertex)
-    c->collect_floor = (int64_t)m_dev;
-    trace_dump(c);
-    return band_solve(c, h, st);
-  }
-  m = m_dev;
-  st->survivors = (int64_t)cnts[3];
-  trace_mark(c, "readback3");
-  trace_dump(c);  // evaluated by the exact select (cnts[2]: running height)
-  st->band_survivors = (int64_t)cnts[0];
-  st->filtered_vertices = (int64_t)m;
-  st->chunks = 1;
-  float ms = 0.f;
-  CUDA_TRY(cudaEventElapsedTime(&ms, c->ev_chunk[0], c->ev_chunk[1]));
-  st->ms_bound = ms;
-  CUDA_TRY(cudaEventElapsedTime(&ms, c->ev_chunk[2], c->ev_chunk[3]));
-  st->ms_partition = ms;
-  CUDA_TRY(cudaEventElapsedTime(&ms, c->ev_chunk[3], c->ev_chunk[4]));
-  st->ms_band_filter = ms;
-  CUDA_TRY(cudaEventElapsedTime(&ms, c->ev_chunk[5], c->ev_chunk[6]));
-  st->ms_collect = ms;
-  st->ms_filter_kernel = 0.f;
-  if (filter_timed) {
-    CUDA_TRY(cudaEventElapsedTime(&ms, c->ev_chunk[8], c->ev_chunk[9]));
-    st->ms_filter_kernel = ms;
-  }
-  st->ms_bound_kernel = 0.f;
-  if (bound_timed) {
-    CUDA_TRY(cudaEventElapsedTime(&ms, c->ev_chunk[12], c->ev_chunk[13]));
-    st->ms_bound_kernel = ms;
-  }
-  st->ms_sweep_enum = 0.f;
-  if (sweep_timed) {
-    CUDA_TRY(cudaEventElapsedTime(&ms, c->ev_chunk[10], c->ev_chunk[11]));
-    st->ms_sweep_enum = ms;
-  }
-  if (getenv("LMSB_BAND_DEBUG")) {
-    float t[6];
-    cudaEventElapsedTime(&t[0], c->ev_chunk[0], c->ev_chunk[1]);
-    cudaEventElapsedTime(&t[1], c->ev_chunk[1], c->ev_chunk[7]);
-    cudaEventElapsedTime(&t[2], c->ev_chunk[7], c->ev_chunk[2]);
-    cudaEventElapsedTime(&t[3], c->ev_chunk[2], c->ev_chunk[3]);
-    cudaEventElapsedTime(&t[4], c->ev_chunk[3], c->ev_chunk[4]);
-    cudaEventElapsedTime(&t[5], c->ev_begin, c->ev_chunk[0]);
-    fprintf(stderr,
-            "band: pre %.3f bound %.3f seeds %.3f gap %.3f collect+group %.3f filter+count+exact %.3f ms\n",
-            t[5], t[0], t[1], t[2], t[3], t[4]);
-  }
-  return LMS_OK;
+  return band_finish(c, h, st, BandTail{m, direct, dplan, filter_timed, bound_timed, sweep_timed});
 }
 
 // Exact LMS search over a batch of fits; out[f] receives fit f's record.
