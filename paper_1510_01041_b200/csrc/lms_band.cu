@@ -2777,9 +2777,17 @@ __global__ void __launch_bounds__(1024) line_wqa_kernel(BandFit bf, double* __re
   const double res = fmax(2.0 * bf.dev / kWqaBins, 1e-300) * (1.0 + 0x1p-30);
   for (int b = tid; b <= kWqaBins; b += 1024) P[b] = 0;
   __syncthreads();
-  for (int k = tid; k < n; k += 1024) {
-    const int b = (int)fmin(fmax(floor((__ldg(bf.a + k) - lo) / res), 0.0), kWqaBins - 1.0);
-    atomicAdd(P + b, 1u);
+  for (int k0 = 0; k0 < n; k0 += 16 * 1024) {  // 16 independent loads in flight per thread
+    double av[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const int k = k0 + e * 1024 + tid;
+      av[e] = k < n ? __ldg(bf.a + k) : 0.0;
+    }
+#pragma unroll
+    for (int e = 0; e < 16; ++e)
+      if (k0 + e * 1024 + tid < n)
+        atomicAdd(P + (int)fmin(fmax(floor((av[e] - lo) / res), 0.0), kWqaBins - 1.0), 1u);
   }
   __syncthreads();
   constexpr int kPer = kWqaBins / 1024;
@@ -2807,17 +2815,29 @@ __global__ void __launch_bounds__(1024) line_wqa_kernel(BandFit bf, double* __re
   }
   if (tid == 1023) P[kWqaBins] = base;
   __syncthreads();
+  // each thread walks its kPer consecutive start bins: one binary search for
+  // the first end bin, then the end advances monotonically
   double best = INFINITY;
-  for (int b1 = tid; b1 < kWqaBins; b1 += 1024) {
-    const unsigned p1 = P[b1];
-    if (P[b1 + 1] == p1 || P[kWqaBins] - p1 < (unsigned)q) continue;
-    int a = b1, z = kWqaBins - 1;  // first b2 with P[b2 + 1] - p1 >= q
-    while (a < z) {
-      const int mid = (a + z) >> 1;
-      if (P[mid + 1] - p1 >= (unsigned)q) z = mid;
-      else a = mid + 1;
+  {
+    const int b0 = tid * kPer;
+    int z = -1;
+    for (int b1 = b0; b1 < b0 + kPer; ++b1) {
+      const unsigned p1 = P[b1];
+      if (P[kWqaBins] - p1 < (unsigned)q) break;  // (and for every later start)
+      if (z < 0) {  // first b2 with P[b2 + 1] - p1 >= q
+        int a = b1, hi = kWqaBins - 1;
+        while (a < hi) {
+          const int mid = (a + hi) >> 1;
+          if (P[mid + 1] - p1 >= (unsigned)q) hi = mid;
+          else a = mid + 1;
+        }
+        z = a;
+      } else {
+        if (z < b1) z = b1;
+        while (P[z + 1] - p1 < (unsigned)q) ++z;
+      }
+      if (P[b1 + 1] != p1) best = fmin(best, (double)(z - b1));
     }
-    best = fmin(best, (double)(a - b1));
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) best = fmin(best, __shfl_xor_sync(0xffffffffu, best, o));
