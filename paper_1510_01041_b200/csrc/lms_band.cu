@@ -964,7 +964,13 @@ __global__ void __launch_bounds__(kCountThreads) band_count_kernel(
 // only vertices the exact select would fully evaluate reach it.
 constexpr int kPreThreads = 512;
 constexpr int kPreWarps = kPreThreads / 32;
-constexpr int kPreLines = 8192;  // lines staged at once (128 KB of (a, b))
+#ifndef LMSB_PRE_LINES
+#define LMSB_PRE_LINES 4096
+#endif
+#ifndef LMSB_PRE_CTAS
+#define LMSB_PRE_CTAS 3
+#endif
+constexpr int kPreLines = LMSB_PRE_LINES;  // lines staged at once (16 B each)
 
 __global__ void __launch_bounds__(kPreThreads) band_exact_prepass_kernel(
     BandFit bf, const lms_candidate* __restrict__ best, const int64_t* __restrict__ in_ranks,
@@ -2085,7 +2091,7 @@ void launch_band_prepass_split(const BandFit& bf, const BandCount& bc, unsigned*
   const size_t smem = (size_t)kPreLines * sizeof(double2) + 64 * sizeof(unsigned);
   static DeviceOnce done;
   set_smem(band_prepass_count_kernel, smem, &done);
-  band_prepass_count_kernel<<<sms, kPreThreads, smem, st>>>(bf, bc.best, bc.in_ranks, bc.in_count,
+  band_prepass_count_kernel<<<sms * LMSB_PRE_CTAS, kPreThreads, smem, st>>>(bf, bc.best, bc.in_ranks, bc.in_count,
                                                             gcnt);
   band_prepass_select_kernel<<<sms * 2, 256, 0, st>>>(bf, bc.best, bc.in_ranks, bc.in_count, gcnt,
                                                       bc.out_ranks, bc.out_fits, bc.fit,

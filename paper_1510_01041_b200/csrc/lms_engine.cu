@@ -326,6 +326,11 @@ struct lms_ctx {
   double bkeys_tau = 0.1;  // LMSB_BKEYS_TAU
   // LMSB_SLOPE_BOUND (default 1): band bounds raised to |u|min W_q(a) - 2 bmax
   int slope_bound = 1;
+  // LMSB_COUNT (default 0): 1 runs the fp32 exact-slope window counts
+  // between the band filter and the exact pass-0 screen; with the slope bound
+  // they pass 93 % of the band survivors (config 2: 1,717 -> 1,605) and cost
+  // more than they save (config 2 0.869 vs 0.845 ms, config 3 0.27 ms)
+  int band_count = 0;
   DevBuf<double> bwqa;
   uint64_t wqa_gen = ~0ull;
   int64_t wqa_off = -1, wqa_n = -1, wqa_q = -1;
@@ -423,6 +428,7 @@ int ctx_init(lms_ctx* c, int device) {
   if (const char* dpl = getenv("LMSB_DEVICE_PLAN")) c->device_plan = atoi(dpl) != 0;
   if (const char* gr = getenv("LMSB_GRAPH")) c->use_graph = atoi(gr) != 0;
   if (const char* sb = getenv("LMSB_SLOPE_BOUND")) c->slope_bound = atoi(sb) != 0;
+  if (const char* bc = getenv("LMSB_COUNT")) c->band_count = atoi(bc) != 0;
   if (const char* wc = getenv("LMSB_WIDE_CHUNK"); wc && atoll(wc) >= 256) c->wide_chunk = atoll(wc);
   if (const char* nc = getenv("LMSB_NARROW_CHUNK"); nc && atoll(nc) >= 256)
     c->narrow_chunk = atoll(nc);
@@ -1069,6 +1075,9 @@ int band_finish(lms_ctx* c, const HostFit& h, lms_stats* st, BandTail t) {
   }
   m = m_dev;
   st->survivors = (int64_t)cnts[3];
+  if (getenv("LMSB_BAND_DEBUG"))
+    fprintf(stderr, "band: members %llu band survivors %llu count survivors %llu exact inputs %llu\n",
+            m_dev, cnts[0], cnts[1], cnts[3]);
   trace_mark(c, "readback3");
   trace_dump(c);  // evaluated by the exact select (cnts[2]: running height)
   st->band_survivors = (int64_t)cnts[0];
@@ -2323,19 +2332,24 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     bc.fit = 0;
     bc.out_count = sc + 4;
     bc.make_lines = true;
-    lmsb::launch_band_count(bf, bc, c->sms, c->stream);
-    trace_mark(c, "count");
-    CUDA_TRY(cudaGetLastError());
-    st->launches += 4;
+    const bool counted = c->band_count != 0;
+    if (counted) {
+      lmsb::launch_band_count(bf, bc, c->sms, c->stream);
+      trace_mark(c, "count");
+      CUDA_TRY(cudaGetLastError());
+      st->launches += 4;
+    }
     // the window-edge seeds put H at (or within a few ulps of) the optimum, so
     // the exact stage's pass 0 prunes every survivor that cannot tie it
     // exact pass-0 screen, lane per vertex with shared-memory lines; only the
     // vertices the exact select would not prune go on to it
     lmsb::BandCount bp = bc;
-    bp.in_ranks = c->branks2.p;
-    bp.in_count = sc + 4;
-    bp.out_ranks = c->ranks.p;
-    bp.out_fits = c->item_fit.p;
+    // (without the fp32 counts the screen reads the band survivors and
+    // writes into the count stage's buffers)
+    bp.in_ranks = counted ? c->branks2.p : c->ranks.p;
+    bp.in_count = counted ? sc + 4 : sc + 3;
+    bp.out_ranks = counted ? c->ranks.p : c->branks2.p;
+    bp.out_fits = counted ? c->item_fit.p : c->bfits2.p;
     bp.out_count = sc + 6;
     if (c->prepass_split) {
       if (c->pcnt.cap < 2 * scap) {
@@ -2349,7 +2363,7 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
       st->launches += 1;
     }
     trace_mark(c, "prepass");
-    RC_TRY(exact_list(sc + 6, scap, c->ranks.p, c->item_fit.p));
+    RC_TRY(exact_list(sc + 6, scap, bp.out_ranks, bp.out_fits));
     trace_mark(c, "exact");
   }
   CUDA_TRY(ev_rec(c, c->ev_chunk[4]));
