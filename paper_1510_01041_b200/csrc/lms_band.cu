@@ -2605,7 +2605,7 @@ __global__ void __launch_bounds__(kPlanThreads) band_plan_kernel(
     } else {
       dp.slot[k] = -1;
     }
-    act[k] = adm[t] || k == 0 || k == K - 1;
+    act[k] = adm[t];  // (the outer bands only when admitted: see (d))
   }
   for (int e = tid; e <= nadm; e += kPlanThreads) dp.ident[e] = e;
   if (tid == 0) {
@@ -2706,6 +2706,11 @@ __global__ void __launch_bounds__(kPlanThreads) band_plan_kernel(
     dp.rk[kPlanMaxRuns + tid] = k1;
   }
   if (tid == 0) dp.ends[2 * kPlanMaxRuns] = SweepEnd{0.0, 0.0, 3, 0};
+  // runs at the infinite ends are left out: the near-parallel pass owns
+  // every class-2 pair when 2 bmax amax / 1e30 <= tau (band_solve's rule);
+  // otherwise the host plans this fit (with the outer runs)
+  __syncthreads();
+  if (tid == 0 && !(2.0 * bf.bmax * bf.amax * (1.0 + 0x1p-20) <= 1e30 * s_tau)) s_bail = 1;
   // (e) sub-band groups: a narrow band one group, a wide one a group per
   // sub_samples sorted samples (<= 1,024); all bands one group each when
   // that would exceed kSubMaxGroups

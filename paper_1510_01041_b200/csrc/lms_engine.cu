@@ -335,6 +335,7 @@ struct lms_ctx {
   uint64_t wqa_gen = ~0ull;
   int64_t wqa_off = -1, wqa_n = -1, wqa_q = -1;
   int64_t collect_floor = 0;    // smallest member capacity (grown after a deferred overflow)
+  int64_t raw_floor = 0;        // smallest raw-enumeration capacity (grown after a raw overflow)
   bool cap_test = false;        // LMSB_CAP_TEST=1: first collect capacity 4,096 (overflow path)
   int64_t wide_chunk = 3072;    // LMSB_WIDE_CHUNK: members per filter chunk of a wide band
   int64_t narrow_chunk = 8192;  // LMSB_NARROW_CHUNK: ... of a narrow band (stored keys)
@@ -953,7 +954,8 @@ int devplan_search(lms_ctx* c, const HostFit& h, lms_stats* st, const lmsb::Band
   const int64_t cap = c->plan_cap;
   RC_TRY(c->bck.need(cap));
   RC_TRY(c->bcv.need(cap));
-  RC_TRY(c->sw_raw.need(cap));
+  const int64_t raw_cap = std::max(cap, c->raw_floor);
+  RC_TRY(c->sw_raw.need(raw_cap));
   RC_TRY(c->sw_rawcnt.need(1));
   w.ckeys = c->bck.p;
   w.cvals = c->bcv.p;
@@ -978,7 +980,7 @@ int devplan_search(lms_ctx* c, const HostFit& h, lms_stats* st, const lmsb::Band
   sa.out_vals = w.cvals;
   sa.cap = cap;
   sa.raw = c->sw_raw.p;
-  sa.raw_cap = cap;
+  sa.raw_cap = raw_cap;
   sa.raw_count = c->sw_rawcnt.p;
   sa.raw_overflow = sc + 8;
   sa.sub_first = c->dp_sbf.p;
@@ -1045,13 +1047,15 @@ int band_finish(lms_ctx* c, const HostFit& h, lms_stats* st, BandTail t) {
     CUDA_TRY(cudaMemcpyAsync(ph, c->dp_hdr.p, sizeof(lmsb::DevPlanHdr), cudaMemcpyDeviceToHost,
                              c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
-  // members classified, or the raw enumeration count when the raw buffer
-  // overflowed (then not every member was seen)
-  const unsigned long long m_dev = std::max(cnts[0], cnts[7]);
+  // members classified; a raw-enumeration overflow (cnts[7]: the raw count;
+  // then not every member was seen) grows the raw capacity to it
+  const unsigned long long m_dev = cnts[0];
+  const unsigned long long raw_over = cnts[7];
+  if (raw_over > 0) c->raw_floor = std::max<int64_t>(c->raw_floor, (int64_t)raw_over);
   cnts += 2;  // [0] band survivors .. [3] exact-stage inputs, as before
   if (dplan) {
     const lmsb::DevPlanHdr hd = *ph;
-    if (hd.bail || m_dev > m) {
+    if (hd.bail || m_dev > m || raw_over > 0) {
       // the device could not plan this fit, or the members outgrew the
       // capacity: solve again with the host plan (which also resizes)
       if (m_dev > m) c->plan_cap = std::max<int64_t>(c->plan_cap, (int64_t)m_dev + m_dev / 4);
@@ -1065,11 +1069,12 @@ int band_finish(lms_ctx* c, const HostFit& h, lms_stats* st, BandTail t) {
     st->seed_height = hd.H;
     st->sweep_runs = hd.nr;
   }
-  if (m_dev > m && !direct) {
-    // deferred member count above the capacity: members were dropped, so
-    // solve again with room for all of them (the record found so far stays
-    // installed; it is a real vertex)
-    c->collect_floor = (int64_t)m_dev;
+  if ((m_dev > m || raw_over > 0) && !direct) {
+    // deferred member count above the capacity (or raw entries dropped):
+    // members were lost, so solve again with room for all of them (the
+    // record found so far stays installed; it is a real vertex).  Both
+    // floors are exact counts, so this happens at most twice.
+    if (m_dev > m) c->collect_floor = std::max<int64_t>(c->collect_floor, (int64_t)m_dev);
     trace_dump(c);
     return band_solve(c, h, st);
   }
@@ -1980,11 +1985,22 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     sweep = std::isfinite(hbnd[k]) && std::fabs((double)hbnd[k]) * bf.amax < 1e29;
   lmsb::SweepArgs sa{};
   if (sweep) {
-    // runs of flagged bands (outer bands always: class-2 vertices), merged
-    // across the smallest gaps down to kSweepMaxRuns
+    // runs of flagged bands, merged across the smallest gaps down to
+    // kSweepMaxRuns.  The outer bands join for their class-2 vertices (|u|
+    // beyond the fp32 key range) unless the near-parallel pass already owns
+    // every such pair: |u| amax >= 1e30 needs |da| <= 2 bmax amax / 1e30,
+    // so when that is <= tau (and the outer bands' class-1 vertices are
+    // dismissed) a one-fit search sorts no lines at the infinite ends
     std::vector<std::pair<int, int>> sr;
+    int nr = 0, nseg = 0;
+    lmsb::SweepEnd* ends = reinterpret_cast<lmsb::SweepEnd*>(u_sweep);
+    int32_t* rk = nullptr;
+    double tau = 0.0;
+    for (int with_outer = sh ? 1 : 0; with_outer < 2; ++with_outer) {
+    sr.clear();
     for (int k = 0; k < K; ++k) {
-      const bool outer = (k == 0 || k == K - 1) && (!own_bands || k % sh->nshards == sh->shard);
+      const bool outer = with_outer && (k == 0 || k == K - 1) &&
+                         (!own_bands || k % sh->nshards == sh->shard);
       if (!(flag[k] || outer)) continue;
       if (!sr.empty() && sr.back().second == k - 1) sr.back().second = k;
       else sr.push_back({k, k});
@@ -1996,11 +2012,10 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
       sr[best].second = sr[best + 1].second;
       sr.erase(sr.begin() + best + 1);
     }
-    const int nr = (int)sr.size();
-    const int nseg = 2 * nr + 1;
-    lmsb::SweepEnd* ends = reinterpret_cast<lmsb::SweepEnd*>(u_sweep);
-    int32_t* rk = reinterpret_cast<int32_t*>(ends + nseg);
-    double tau = 0.0;
+    nr = (int)sr.size();
+    nseg = 2 * nr + 1;
+    rk = reinterpret_cast<int32_t*>(ends + nseg);
+    tau = 0.0;
     for (int e = 0; e < nr; ++e) {
       const int k0 = sr[e].first, k1 = sr[e].second;
       double lo = -INFINITY, hi = INFINITY;
@@ -2032,6 +2047,9 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
       ends[2 * e + 1] = lmsb::SweepEnd{std::isfinite(s1) ? s1 : 0.0, fin, std::isfinite(s1) ? 0 : 2, 0};
       rk[e] = k0;
       rk[nr + e] = k1;
+    }
+    if (with_outer) break;
+    if (nr > 0 && 2.0 * bf.bmax * bf.amax * (1.0 + 0x1p-20) <= 1e30 * tau) break;
     }
     ends[2 * nr] = lmsb::SweepEnd{0.0, 0.0, 3, 0};
     const int64_t nn = h.n;
@@ -2144,10 +2162,12 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
       sa.out_keys = w.ckeys;
       sa.out_vals = w.cvals;
       sa.cap = cap;
-      RC_TRY(c->sw_raw.need(cap));
+      // (raw entries: inversions, not members -- their own capacity)
+      const int64_t raw_cap = std::max(cap, c->raw_floor);
+      RC_TRY(c->sw_raw.need(raw_cap));
       RC_TRY(c->sw_rawcnt.need(1));
       sa.raw = c->sw_raw.p;
-      sa.raw_cap = cap;
+      sa.raw_cap = raw_cap;
       sa.raw_count = c->sw_rawcnt.p;
       sa.raw_overflow = subgrp ? sc + 8 : nullptr;  // (deferred count: flagged, not counted)
       CUDA_TRY(ev_rec(c, c->ev_chunk[10]));
