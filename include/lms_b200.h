@@ -278,6 +278,14 @@ int lms_probe_fp64_rate(int device, double* dfma_per_second);
 /* Measured FP32 FMA lane rate (FFMA2 packed chains, all SMs busy): the
  * roofline denominator of the default FP32/FP16 count filter. */
 int lms_probe_fp32_rate(int device, double* fma_lanes_per_second);
+/* Diagnostics: the band stage's cluster segmented sort (lms_segsort.cu) on
+ * host buffers: segment s = keys[seg_begin[s] .. seg_end[s]) sorted
+ * ascending into the same positions of out (positions outside every segment
+ * are left as in `keys`); segments of at most 65,536 keys.  Stands in for
+ * the np.sort of the reference's cut rows (backend.py:199-203) in parity
+ * tests of the sort itself. */
+int lms_debug_seg_sort(int device, const float* keys, float* out, int64_t total, int32_t nseg,
+                       const int64_t* seg_begin, const int64_t* seg_end);
 
 /* ---- multi-GPU exact LMS: the vertex space of one fit
  * shared over several GPUs, one NCCL collective exchange of 56-byte records

@@ -213,6 +213,8 @@ SIGNATURES = {
     "lms_ndarray_rows_f64": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, _I]),
     "lms_probe_fp64_rate": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_double)]),
     "lms_probe_fp32_rate": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_double)]),
+    "lms_debug_seg_sort": (ctypes.c_int, [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                          ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p]),
 }
 
 
@@ -593,6 +595,18 @@ def probe_fp32_rate(device: int = 0) -> float:
     r = ctypes.c_double(0.0)
     check(lib.lms_probe_fp32_rate(int(device), ctypes.byref(r)))
     return r.value
+
+
+def debug_seg_sort(keys: np.ndarray, seg_begin, seg_end, device: int = 0) -> np.ndarray:
+    """The band stage's cluster segmented sort on host arrays (diagnostic)."""
+    lib = _lib_ready()
+    k = np.ascontiguousarray(keys, dtype=np.float32)
+    out = np.empty_like(k)
+    sb = _i64(seg_begin)
+    se = _i64(seg_end)
+    check(lib.lms_debug_seg_sort(int(device), k.ctypes.data, out.ctypes.data, k.size, sb.size,
+                                 sb.ctypes.data, se.ctypes.data))
+    return out
 
 
 class Context:

@@ -57,6 +57,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "lms_band.cuh"
 #include "lms_band_dev.cuh"
@@ -1602,13 +1603,26 @@ size_t band_collect_smem(int K) {
          (size_t)K * sizeof(float) + (size_t)(K + 1) * sizeof(int16_t) + 16;
 }
 
+// Opt-in (LMSB_SEG_SORT=1): measured slower than the CUB sorts on every
+// path (config 2 0.802 -> 0.822 ms, n = 65,536 9.87 -> 11.4 ms; one 65,536-key
+// segment 63 us on one cluster: the merge rounds are shared-memory latency
+// bound at one 1,024-thread CTA per SM), so the CUB sorts stay the default.
+bool use_seg_sort(int64_t max_len) {
+  const char* e = getenv("LMSB_SEG_SORT");
+  return seg_sort_fits(max_len) && e && e[0] == '1';
+}
+
 int launch_band_sample(const BandFit& bf, const BandWork& w, int sms, cudaStream_t st) {
   cudaMemsetAsync(w.nvalid, 0, sizeof(unsigned long long), st);
   band_sample_kernel<<<sms * 4, 256, 0, st>>>(bf, w.S, w.sample, w.nvalid);
-  size_t bytes = w.temp_bytes;
-  if (cub::DeviceRadixSort::SortKeys(w.temp, bytes, w.sample, w.sample_sorted, (int)w.S, 0, 32,
-                                     st) != cudaSuccess)
-    return -1;
+  if (use_seg_sort(w.S)) {
+    if (launch_seg_sort(w.sample, w.sample_sorted, w.S, 1, nullptr, nullptr, st) != 0) return -1;
+  } else {
+    size_t bytes = w.temp_bytes;
+    if (cub::DeviceRadixSort::SortKeys(w.temp, bytes, w.sample, w.sample_sorted, (int)w.S, 0, 32,
+                                       st) != cudaSuccess)
+      return -1;
+  }
   band_bounds_kernel<<<(w.K + 255) / 256, 256, 0, st>>>(w.sample_sorted, w.nvalid, w.K, w.bounds);
   return 0;
 }
@@ -1648,11 +1662,15 @@ int launch_band_bound_big(const BandFit& bf, const BandArgs& ba, const BandBig& 
     const int nb = std::min(bg.batch, k1 - b0);
     dim3 grid((unsigned)std::min<int64_t>((n + 255) / 256, 64), (unsigned)std::min(nb, 65535));
     band_keys_global_kernel<<<grid, 256, 0, st>>>(bf, ba.bounds, ba.K, b0, ids, nb, bg.keys);
-    size_t bytes = bg.temp_bytes;
-    if (cub::DeviceSegmentedRadixSort::SortKeys(bg.temp, bytes, bg.keys, bg.keys_alt,
-                                                (int)(nb * n), nb, bg.seg, bg.seg + 1, 0, 32,
-                                                st) != cudaSuccess)
-      return -1;
+    if (use_seg_sort(n)) {
+      if (launch_seg_sort(bg.keys, bg.keys_alt, n, nb, nullptr, nullptr, st) != 0) return -1;
+    } else {
+      size_t bytes = bg.temp_bytes;
+      if (cub::DeviceSegmentedRadixSort::SortKeys(bg.temp, bytes, bg.keys, bg.keys_alt,
+                                                  (int)(nb * n), nb, bg.seg, bg.seg + 1, 0, 32,
+                                                  st) != cudaSuccess)
+        return -1;
+    }
     band_wq_kernel<<<nb, 1024, 0, st>>>(bf, ba, b0, ids, bg.keys_alt, bg.store);
   }
   return 0;
@@ -1804,11 +1822,16 @@ int launch_band_slices(const BandFit& bf, const BandArgs& ba, int64_t nslices_ma
   dim3 grid((unsigned)std::min<int64_t>((bf.n + 255) / 256, 64),
             (unsigned)std::min<int64_t>(nslices_max, 65535));
   band_slice_keys_kernel<<<grid, 256, 0, st>>>(bf, ba, nslices_max, keys, seg_begin, seg_end);
-  size_t bytes = temp_bytes;
-  if (cub::DeviceSegmentedRadixSort::SortKeys(temp, bytes, keys, store,
-                                              (int)(nslices_max * bf.n), (int)nslices_max,
-                                              seg_begin, seg_end, 0, 32, st) != cudaSuccess)
-    return -1;
+  if (use_seg_sort(bf.n)) {
+    if (launch_seg_sort(keys, store, bf.n, (int)nslices_max, seg_begin, seg_end, st) != 0)
+      return -1;
+  } else {
+    size_t bytes = temp_bytes;
+    if (cub::DeviceSegmentedRadixSort::SortKeys(temp, bytes, keys, store,
+                                                (int)(nslices_max * bf.n), (int)nslices_max,
+                                                seg_begin, seg_end, 0, 32, st) != cudaSuccess)
+      return -1;
+  }
   band_slice_wq_kernel<<<(int)std::min<int64_t>(nslices_max, 4096), 1024, 0, st>>>(
       bf, ba, nslices_max, store, seg_begin, seg_end);
   band_slice_table_kernel<<<(int)std::min<int64_t>(nslices_max, 4096), 1024, 0, st>>>(

@@ -173,6 +173,15 @@ void launch_band_filter_big(const BandFit& bf, const BandArgs& ba, const float* 
                             cudaStream_t st);
 
 size_t band_sample_temp_bytes(int64_t S);
+// Segmented ascending sort of fp32 keys, one 8-CTA cluster per segment
+// (lms_segsort.cu): segment s is in[seg_b[s] .. seg_e[s]) (or [s * stride,
+// (s + 1) * stride) without seg_b), written to the same positions of out.
+// seg_sort_fits(L): segments of L keys are supported (L <= 65,536).
+bool seg_sort_fits(int64_t max_len);
+int launch_seg_sort(const float* in, float* out, int64_t stride, int nseg, const int64_t* seg_b,
+                    const int64_t* seg_e, cudaStream_t st);
+// the cluster sort replaces the CUB device sorts when LMSB_SEG_SORT=1 (opt-in)
+bool use_seg_sort(int64_t max_len);
 size_t band_group_temp_bytes(int64_t m);
 size_t band_collect_smem(int K);
 int launch_band_sample(const BandFit& bf, const BandWork& w, int sms, cudaStream_t st);

@@ -1,0 +1,109 @@
+"""The band stage's cluster segmented sort (lms_segsort.cu) against numpy.
+
+The sort can replace the CUB device sorts of the slope samples and of the
+large-n band / slice keys (LMSB_SEG_SORT=1; measured slower, so opt-in); its output must be the ascending order of the
+unsigned ordered keys (the order a radix sort produces; -0.0 before +0.0),
+bit for bit.  The fits that run through it are covered by the golden and
+full-size parity tests; here the sort itself meets the cases a regular-
+sampling sort can get wrong: ties everywhere, runs shorter than the 8 CTAs
+of a cluster, already sorted / reversed input, infinities and signed zeros,
+segments with gaps and empty segments."""
+
+import os
+
+import numpy as np
+import pytest
+
+from paper_1510_01041_b200 import _native, workloads
+from paper_1510_01041_b200.backend import record_from_native
+
+pytestmark = pytest.mark.gpu
+
+
+def _radix_order(x: np.ndarray) -> np.ndarray:
+    u = x.view(np.uint32)
+    k = np.where(u >> 31, ~u, u | np.uint32(0x80000000))
+    return x[np.argsort(k, kind="stable")]
+
+
+def _check(keys, segs):
+    keys = np.asarray(keys, dtype=np.float32)
+    sb = np.array([s[0] for s in segs], dtype=np.int64)
+    se = np.array([s[1] for s in segs], dtype=np.int64)
+    got = _native.debug_seg_sort(keys, sb, se)
+    want = keys.copy()
+    for b, e in segs:
+        if e > b:
+            want[b:e] = _radix_order(keys[b:e])
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+@pytest.mark.parametrize("n", [1, 2, 7, 8, 9, 63, 100, 1000, 8191, 8192, 8193, 40000, 65535, 65536])
+def test_random_lengths(n):
+    rng = np.random.default_rng(n)
+    _check(rng.standard_normal(n).astype(np.float32) * 1e3, [(0, n)])
+
+
+@pytest.mark.parametrize("kind", ["equal", "two", "few", "sorted", "reversed", "special", "heavy"])
+def test_adversarial(kind):
+    n = 65536
+    rng = np.random.default_rng(7)
+    if kind == "equal":
+        x = np.full(n, 2.5, np.float32)
+    elif kind == "two":
+        x = np.where(rng.random(n) < 0.999, 1.0, -1.0).astype(np.float32)
+    elif kind == "few":
+        x = rng.integers(0, 5, n).astype(np.float32)
+    elif kind == "sorted":
+        x = np.sort(rng.standard_normal(n)).astype(np.float32)
+    elif kind == "reversed":
+        x = np.sort(rng.standard_normal(n))[::-1].astype(np.float32).copy()
+    elif kind == "special":
+        x = rng.standard_normal(n).astype(np.float32)
+        idx = rng.integers(0, n, 4000)
+        x[idx[:1000]] = np.inf
+        x[idx[1000:2000]] = -np.inf
+        x[idx[2000:3000]] = 0.0
+        x[idx[3000:]] = -0.0
+        x[:10] = np.float32(1e-45)
+    else:  # half the keys in one tight cluster (the inlier lines at the fit slope)
+        x = np.concatenate([rng.standard_normal(n // 2) * 1e-6 + 3.0,
+                            rng.standard_cauchy(n - n // 2) * 1e4]).astype(np.float32)
+        rng.shuffle(x)
+    _check(x, [(0, n)])
+
+
+def test_many_segments_with_gaps_and_empties():
+    rng = np.random.default_rng(3)
+    lens = [65536, 0, 17, 30000, 0, 8, 65536, 1, 12345, 0, 4096]
+    segs, pos = [], 5
+    for L in lens:
+        segs.append((pos, pos + L))
+        pos += L + int(rng.integers(0, 9))
+    keys = rng.standard_normal(pos + 3).astype(np.float32)
+    keys[segs[3][0]:segs[3][1]] = rng.integers(0, 3, lens[3])
+    _check(keys, segs)
+
+
+def test_big_band_fit_same_as_cub_sorts():
+    """A large-n band fit (n > 16,384: sample, per-band and per-slice sorts
+    all run through the cluster sort) gives the same record and the same
+    band count as with the CUB device sorts (the default; LMSB_SEG_SORT=1
+    selects the cluster sort).  (Survivor
+    counts depend on when the persistent filter CTAs see the falling best
+    height, so they are not compared.)"""
+    pts = workloads.contaminated_line_points(20000, 5)
+    a, b = pts[:, 0].copy(), pts[:, 1].copy()
+    n = a.size
+    out = []
+    for seg in ("1", "0"):
+        os.environ["LMSB_SEG_SORT"] = seg
+        try:
+            ctx = _native.Context(0)
+            ctx.upload(a, b)
+            rec = record_from_native(ctx.solve(n // 2 + 1, 0, n * (n - 1) // 2))
+            st = ctx.stats()
+        finally:
+            os.environ.pop("LMSB_SEG_SORT", None)
+        out.append(((rec.height, rec.i, rec.j, rec.u, rec.v_low, rec.v_high), st["bands"]))
+    assert out[0] == out[1]
