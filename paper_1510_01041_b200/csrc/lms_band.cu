@@ -68,7 +68,7 @@ namespace lmsb {
 namespace {
 
 #ifndef LMSB_RADIX_BITS
-#define LMSB_RADIX_BITS 4
+#define LMSB_RADIX_BITS 6  // 6 bits: config 2 0.811 -> 0.797 ms (4: 8 passes, 5 or 6: 6 or 7)
 #endif
 constexpr int kCollectThreads = 512;
 #ifndef LMSB_COLLECT_STEP
@@ -1603,19 +1603,28 @@ size_t band_collect_smem(int K) {
          (size_t)K * sizeof(float) + (size_t)(K + 1) * sizeof(int16_t) + 16;
 }
 
-// Opt-in (LMSB_SEG_SORT=1): measured slower than the CUB sorts on every
-// path (config 2 0.802 -> 0.822 ms, n = 65,536 9.87 -> 11.4 ms; one 65,536-key
-// segment 63 us on one cluster: the merge rounds are shared-memory latency
-// bound at one 1,024-thread CTA per SM), so the CUB sorts stay the default.
-bool use_seg_sort(int64_t max_len) {
+// The cluster sort (one 8-CTA cluster per segment, ~60 us for 65,536 keys,
+// ~16 clusters resident) against the CUB sorts (one CTA per segment over
+// several global passes: high latency, high throughput): the cluster sort
+// wins for a few segments (the exact bounds of a shard plan's pool and
+// refine lists), CUB for many (config 3's ~800 slices: 2.4 vs 3.1 ms) and
+// for the single sample sort (config 2: 0.80 vs 0.82 ms).
+// LMSB_SEG_SORT: 0 never, 1 always, 2 (default) segmented sorts of at most
+// LMSB_SEG_SORT_MAX (default 32) segments.
+bool use_seg_sort(int64_t max_len, int64_t nseg) {
   const char* e = getenv("LMSB_SEG_SORT");
-  return seg_sort_fits(max_len) && e && e[0] == '1';
+  const int mode = e ? atoi(e) : 2;
+  if (!seg_sort_fits(max_len) || mode == 0) return false;
+  if (mode == 1) return true;
+  const char* m = getenv("LMSB_SEG_SORT_MAX");
+  const int64_t cap = m ? atoll(m) : 32;
+  return nseg > 1 && nseg <= cap;
 }
 
 int launch_band_sample(const BandFit& bf, const BandWork& w, int sms, cudaStream_t st) {
   cudaMemsetAsync(w.nvalid, 0, sizeof(unsigned long long), st);
   band_sample_kernel<<<sms * 4, 256, 0, st>>>(bf, w.S, w.sample, w.nvalid);
-  if (use_seg_sort(w.S)) {
+  if (use_seg_sort(w.S, 1)) {
     if (launch_seg_sort(w.sample, w.sample_sorted, w.S, 1, nullptr, nullptr, st) != 0) return -1;
   } else {
     size_t bytes = w.temp_bytes;
@@ -1662,7 +1671,7 @@ int launch_band_bound_big(const BandFit& bf, const BandArgs& ba, const BandBig& 
     const int nb = std::min(bg.batch, k1 - b0);
     dim3 grid((unsigned)std::min<int64_t>((n + 255) / 256, 64), (unsigned)std::min(nb, 65535));
     band_keys_global_kernel<<<grid, 256, 0, st>>>(bf, ba.bounds, ba.K, b0, ids, nb, bg.keys);
-    if (use_seg_sort(n)) {
+    if (use_seg_sort(n, nb)) {
       if (launch_seg_sort(bg.keys, bg.keys_alt, n, nb, nullptr, nullptr, st) != 0) return -1;
     } else {
       size_t bytes = bg.temp_bytes;
@@ -1822,7 +1831,7 @@ int launch_band_slices(const BandFit& bf, const BandArgs& ba, int64_t nslices_ma
   dim3 grid((unsigned)std::min<int64_t>((bf.n + 255) / 256, 64),
             (unsigned)std::min<int64_t>(nslices_max, 65535));
   band_slice_keys_kernel<<<grid, 256, 0, st>>>(bf, ba, nslices_max, keys, seg_begin, seg_end);
-  if (use_seg_sort(bf.n)) {
+  if (use_seg_sort(bf.n, nslices_max)) {
     if (launch_seg_sort(keys, store, bf.n, (int)nslices_max, seg_begin, seg_end, st) != 0)
       return -1;
   } else {

@@ -180,8 +180,9 @@ size_t band_sample_temp_bytes(int64_t S);
 bool seg_sort_fits(int64_t max_len);
 int launch_seg_sort(const float* in, float* out, int64_t stride, int nseg, const int64_t* seg_b,
                     const int64_t* seg_e, cudaStream_t st);
-// the cluster sort replaces the CUB device sorts when LMSB_SEG_SORT=1 (opt-in)
-bool use_seg_sort(int64_t max_len);
+// the cluster sort or the CUB device sorts for `nseg` segments of at most
+// max_len keys (LMSB_SEG_SORT, lms_band.cu)
+bool use_seg_sort(int64_t max_len, int64_t nseg);
 size_t band_group_temp_bytes(int64_t m);
 size_t band_collect_smem(int K);
 int launch_band_sample(const BandFit& bf, const BandWork& w, int sms, cudaStream_t st);

@@ -303,6 +303,8 @@ struct lms_ctx {
   int band_coarse = 2;
   int prepass_split = 1;         // pass-0 screen with lines split over CTAs (LMSB_PREPASS_SPLIT)
   int seed_bands = 8;            // bands whose window-edge pairs seed H (LMSB_SEED_BANDS)
+  int plan_pool = 0;             // large-n shard plan: coarse-window pool given exact bounds
+                                 // (LMSB_PLAN_POOL; 0: 64 / shards, at least 4 T)
   DevBuf<int64_t> bbig_seg;
   DevBuf<int32_t> small_list, dg_i32;
   DevBuf<int64_t> dg_i64;
@@ -441,6 +443,8 @@ int ctx_init(lms_ctx* c, int device) {
   if (const char* bs = getenv("LMSB_BIG_SLICE"); bs && atoll(bs) >= 1) c->big_slice = atoll(bs);
   if (const char* sb = getenv("LMSB_SEED_BANDS"); sb && atoi(sb) >= 1)
     c->seed_bands = std::min(48, atoi(sb));
+  if (const char* pp = getenv("LMSB_PLAN_POOL"); pp && atoi(pp) >= 1)
+    c->plan_pool = std::min(64, atoi(pp));
   if (const char* ps = getenv("LMSB_PREPASS_SPLIT")) c->prepass_split = atoi(ps) != 0;
   if (const char* bc0 = getenv("LMSB_BAND_COARSE")) c->band_coarse = std::max(0, std::min(2, atoi(bc0)));
   const char* sm = getenv("LMSB_SMALL");
@@ -1474,6 +1478,7 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     } else {
       RC_TRY(exact_bounds(c->bslice_ids.p, nsl));
     }
+    trace_mark(c, "plan_bounds");
   }
 
   if (sh && sh->mode == 1) {
@@ -1488,13 +1493,18 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
       if (coarse) {
         // a pool of the narrowest coarse windows gets exact bounds (and edge
         // keys); the T narrowest exact windows among them seed
-        constexpr int kPool = 64;
+        // (the pools of all shards together cover the one-GPU pool: each
+        // shard's share of the narrowest windows shrinks as 1 / shards)
+        const int kPool = c->plan_pool > 0
+                              ? c->plan_pool
+                              : std::max(4 * T, (64 + sh->nshards - 1) / sh->nshards);
         lmsb::launch_band_top(c->bwq.p, 0, nsl, K, kPool, c->blist.p, c->bflag.p, c->stream, d_sl);
         RC_TRY(exact_bounds(c->blist.p, kPool));
         lmsb::launch_band_top(c->bwq.p, 0, kPool, K, T, c->blist.p + kPool, c->bflag.p, c->stream,
                               c->blist.p);
         d_seed = c->blist.p + kPool;
         st->launches += 2;
+        trace_mark(c, "plan_pool");
       } else {
         lmsb::launch_band_top(c->bwq.p, 0, nsl, K, T, c->blist.p, c->bflag.p, c->stream, d_sl);
       }
@@ -1504,6 +1514,7 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
       lmsb::launch_band_seeds(bf, w, c->ranks.p, c->item_fit.p, 0, seed_cap, sc + 2, c->stream);
       RC_TRY(exact_list(sc + 2, seed_cap, c->ranks.p, c->item_fit.p));
       st->launches += 3;
+      trace_mark(c, "plan_seeds");
     } else {  // no bands here: only the sample counts
       CUDA_TRY(cudaMemsetAsync(c->bflag.p, 0, K, c->stream));
       CUDA_TRY(cudaMemsetAsync(sc + 2, 0, sizeof(unsigned long long), c->stream));
@@ -1531,6 +1542,7 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
         RC_TRY(exact_bounds(c->blist.p, (int)cand.size()));
       }
       st->bands_refined = (int64_t)cand.size();
+      trace_mark(c, "plan_refine");
     }
     std::vector<float> h_edge((size_t)K * 2 * lmsb::kEdge);
     CUDA_TRY(cudaMemcpyAsync(p_lb, c->blb.p, sizeof(double) * K, cudaMemcpyDeviceToHost,
@@ -1553,6 +1565,7 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
       std::memcpy(sh->edge_out + (size_t)t * 2 * lmsb::kEdge,
                   h_edge.data() + (size_t)k * 2 * lmsb::kEdge, sizeof(float) * 2 * lmsb::kEdge);
     }
+    trace_mark(c, "plan_readback");
     sh->seed_out = nsl > 0 ? *p_hb : lms_candidate{};
     sh->K = K;
     sh->k0 = nsl;  // bands in the slice (shard, shard + nshards, ...)

@@ -1,4 +1,6 @@
-"""The band stage's cluster segmented sort (lms_segsort.cu) against numpy.
+"""The 8-CTA cluster kernels: the segmented sort (lms_segsort.cu) against
+numpy, and the cluster exact select (lms_exact.cu) against the streaming
+one-CTA-per-vertex select.
 
 The sort can replace the CUB device sorts of the slope samples and of the
 large-n band / slice keys (LMSB_SEG_SORT=1; measured slower, so opt-in); its output must be the ascending order of the
@@ -106,4 +108,24 @@ def test_big_band_fit_same_as_cub_sorts():
         finally:
             os.environ.pop("LMSB_SEG_SORT", None)
         out.append(((rec.height, rec.i, rec.j, rec.u, rec.v_low, rec.v_high), st["bands"]))
+    assert out[0] == out[1]
+
+
+@pytest.mark.parametrize("n,seed", [(20000, 1), (40000, 4), (65536, 0)])
+def test_exact_cluster_select_same_as_streaming(n, seed):
+    """Seeds and survivors of fits above 16,384 lines are evaluated by one
+    8-CTA cluster per vertex (LMSB_EXACT_CLUSTER, default on); the record
+    (and every field of it) equals the streaming select's."""
+    pts = workloads.contaminated_line_points(n, seed)
+    a, b = pts[:, 0].copy(), pts[:, 1].copy()
+    out = []
+    for flag in ("1", "0"):
+        os.environ["LMSB_EXACT_CLUSTER"] = flag
+        try:
+            ctx = _native.Context(0)
+            ctx.upload(a, b)
+            rec = record_from_native(ctx.solve(n // 2 + 1, 0, n * (n - 1) // 2))
+        finally:
+            os.environ.pop("LMSB_EXACT_CLUSTER", None)
+        out.append((rec.height, rec.i, rec.j, rec.u, rec.v_low, rec.v_high))
     assert out[0] == out[1]
