@@ -369,6 +369,7 @@ __global__ void __launch_bounds__(kCachedThreads, 1) exact_cached_kernel(ExactAr
   unsigned long long* cache = reinterpret_cast<unsigned long long*>(smem_raw + ((sizeof(SM) + 15) & ~size_t(15)));
   int64_t count = args.d_count ? (int64_t)*args.d_count : args.count;
   if (count > args.capacity) count = args.capacity;
+  if (args.cluster_max > 0 && count <= args.cluster_max) return;  // (the cluster kernel's list)
   if (args.cached_end > 0 && count > args.cached_end) count = args.cached_end;
   for (int64_t s = blockIdx.x; s < count; s += gridDim.x) {
     int32_t f;
@@ -558,6 +559,7 @@ __global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kClusterT
   const int r = (int)cl.block_rank();
   int64_t count = args.d_count ? (int64_t)*args.d_count : args.count;
   if (count > args.capacity) count = args.capacity;
+  if (args.cluster_max > 0 && count > args.cluster_max) return;  // (the cached kernel's list)
   if (args.cached_end > 0 && count > args.cached_end) count = args.cached_end;
   const int64_t nclusters = gridDim.x / kClusterCtas;
   for (int64_t s = blockIdx.x / kClusterCtas; s < count; s += nclusters) {
@@ -727,8 +729,61 @@ bool exact_cluster_enabled() {
   return !(e && e[0] == '0');
 }
 
+// short lists of a fit with n <= kExactCacheN: the cluster kernel when the
+// list has at most this many vertices (LMSB_EXACT_CLUSTER_MAX; 0: never)
+int64_t exact_cluster_max() {
+  const char* e = getenv("LMSB_EXACT_CLUSTER_MAX");
+  return e ? atoll(e) : 36;
+}
+
+template <class Kern>
+void launch_cluster_exact(Kern kern, const ExactArgs& args, int64_t max_n, int64_t cluster_max,
+                          cudaStream_t stream) {
+  const int64_t m = (max_n + kClusterCtas - 1) / kClusterCtas;
+  const size_t smem = ((sizeof(ClusterSelect) + 15) & ~size_t(15)) + sizeof(unsigned long long) * m;
+  static DeviceOnce done;
+  set_max_smem(kern,
+               ((sizeof(ClusterSelect) + 15) & ~size_t(15)) +
+                   sizeof(unsigned long long) * kExactCacheN,
+               done);
+  int sms = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int clusters = std::max(1, sms / kClusterCtas);
+  ExactArgs head = args;
+  head.cluster_max = cluster_max;
+  if (head.cached_end <= 0 || head.cached_end > (int64_t)clusters * 8)
+    head.cached_end = (int64_t)clusters * 8;
+  kern<<<clusters * kClusterCtas, kClusterThreads, smem, stream>>>(head);
+}
+
 void launch_exact(const ExactArgs& args, int grid, cudaStream_t stream, int64_t max_n) {
   if (grid <= 0) return;
+  const int64_t cmax = exact_cluster_max();
+  if (args.cached && max_n <= kExactCacheN && max_n > kWarpExactMaxN && cmax > 0 &&
+      exact_cluster_enabled()) {
+    // a short list by clusters, a long one by the per-SM cached kernel (each
+    // kernel reads the device count and returns when the list is the other's)
+    launch_cluster_exact(exact_cluster_kernel, args, max_n, cmax, stream);
+    ExactArgs longl = args;
+    longl.cluster_max = cmax;
+    using SM = SelectSharedT<kCachedThreads / kWarp>;
+    const size_t smem = ((sizeof(SM) + 15) & ~size_t(15)) + sizeof(unsigned long long) * max_n;
+    static DeviceOnce done2;
+    set_max_smem(exact_cached_kernel,
+                 ((sizeof(SM) + 15) & ~size_t(15)) + sizeof(unsigned long long) * kExactCacheN,
+                 done2);
+    int sms = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    exact_cached_kernel<<<sms, kCachedThreads, smem, stream>>>(longl);
+    if (args.cached_end <= 0) return;
+    ExactArgs rest = args;
+    rest.begin = args.cached_end;
+    rest.cached = 0;
+    exact_kernel<<<grid, kExactThreads, 0, stream>>>(rest);
+    return;
+  }
   if (args.cached && max_n <= kExactCacheN && max_n > kWarpExactMaxN) {
     using SM = SelectSharedT<kCachedThreads / kWarp>;
     const size_t smem = ((sizeof(SM) + 15) & ~size_t(15)) + sizeof(unsigned long long) * max_n;
@@ -750,24 +805,14 @@ void launch_exact(const ExactArgs& args, int grid, cudaStream_t stream, int64_t 
   }
   if (args.cached && max_n > kExactCacheN && max_n <= kClusterCtas * kExactCacheN &&
       exact_cluster_enabled()) {
-    const int64_t m = (max_n + kClusterCtas - 1) / kClusterCtas;
-    const size_t smem = ((sizeof(ClusterSelect) + 15) & ~size_t(15)) + sizeof(unsigned long long) * m;
-    static DeviceOnce done;
-    set_max_smem(exact_cluster_kernel,
-                 ((sizeof(ClusterSelect) + 15) & ~size_t(15)) +
-                     sizeof(unsigned long long) * kExactCacheN,
-                 done);
+    // the first 8 vertices per cluster here, the rest of a long list streams
+    launch_cluster_exact(exact_cluster_kernel, args, max_n, 0, stream);
     int sms = 148, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int clusters = std::max(1, sms / kClusterCtas);
-    // the first 8 vertices per cluster here, the rest of a long list streams
-    ExactArgs head = args;
-    if (head.cached_end <= 0 || head.cached_end > (int64_t)clusters * 8)
-      head.cached_end = (int64_t)clusters * 8;
-    exact_cluster_kernel<<<clusters * kClusterCtas, kClusterThreads, smem, stream>>>(head);
     ExactArgs rest = args;
-    rest.begin = head.cached_end;
+    rest.begin = std::min<int64_t>(args.cached_end > 0 ? args.cached_end : INT64_MAX,
+                                   (int64_t)std::max(1, sms / kClusterCtas) * 8);
     rest.cached = 0;
     exact_kernel<<<grid, kExactThreads, 0, stream>>>(rest);
     return;

@@ -62,6 +62,8 @@ struct ExactArgs {
   int cached;                  // few vertices: one CTA each, cut keys cached in shared memory
   int64_t cached_end;          // cached: items beyond this go to the streaming kernel (0: none)
   int64_t begin;               // streaming kernel: first item
+  int64_t cluster_max;         // > 0: lists of at most this many items go to the cluster
+                               // kernel, longer ones to the cached kernel (n <= kExactCacheN)
 };
 
 // Largest fit whose cut keys the cached exact kernel keeps in shared memory.
