@@ -296,7 +296,8 @@ struct lms_ctx {
   DevBuf<uint8_t> bcflags;     // batched contacts: one flag per point
   DevBuf<int32_t> bident;      // 0 .. nslot - 1
   DevBuf<unsigned> bslice_ptab;
-  int64_t big_slice = 65536;     // n > 16,384: members per filter slice (LMSB_BIG_SLICE)
+  int64_t big_slice = 393216;    // n > 16,384: members per filter slice (LMSB_BIG_SLICE; 65,536
+                                 // -> 393,216: config 3 9.28 -> 7.85 ms, flat from 196,608 up)
   // sort-free band bounds first, exact ones where they cannot dismiss a band
   // (LMSB_BAND_COARSE: 0 never, 1 always, 2 large n only -- for n <= 16,384
   // one shared-memory sort per band is cheaper than binning plus a refine)
