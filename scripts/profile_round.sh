@@ -7,10 +7,10 @@ set -x
 tag=${1:-r02}
 mkdir -p gpurun_out
 ncu --set full --clock-control none --import-source on \
-    -k regex:"band_filter_kernel|band_bound_kernel|sweep_enum|sweep_classify|band_count_kernel|exact_cached|sub_scatter|band_prepass_count" \
+    -k regex:"band_filter_kernel|band_bound_kernel|sweep_enum|sweep_classify|band_count_kernel|exact_cached|exact_cluster|sub_scatter|band_prepass_count" \
     -o gpurun_out/${tag}_band python scripts/quick_time.py 16384 1 > gpurun_out/ncu_band.log 2>&1
 python scripts/ncu_summary.py gpurun_out/${tag}_band.ncu-rep profiles/${tag}_band_kernels_ncu.json
-ncu --set full --clock-control none -k regex:"band_filter_big|sweep_enum|band_count_kernel|band_coarse" -c 4 \
+ncu --set full --clock-control none -k regex:"band_filter_big|sweep_enum|sweep_classify|band_prepass_count|band_coarse|exact_cluster|seg_sort" -c 8 \
     -o gpurun_out/${tag}_big python scripts/quick_time.py 65536 1 > gpurun_out/ncu_big.log 2>&1
 python scripts/ncu_summary.py gpurun_out/${tag}_big.ncu-rep profiles/${tag}_big_kernels_ncu.json
 ncu --set full --clock-control none -k regex:small_fit -c 1 \
@@ -30,3 +30,5 @@ python bench.py > gpurun_out/bench_${tag}.json 2> gpurun_out/bench_${tag}.err
 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref_${tag}.json 2> gpurun_out/bench_ref_${tag}.err
 tail -c 4000 gpurun_out/bench_${tag}.json
 cat gpurun_out/bench_ref_${tag}.json
+# the full reports stay on the box (gpurun copies back at most 64 MiB)
+rm -f gpurun_out/*.ncu-rep
