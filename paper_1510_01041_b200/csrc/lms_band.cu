@@ -282,6 +282,23 @@ __global__ void __launch_bounds__(kThreads, 1) band_bound_kernel(BandFit bf, Ban
     }
     return;
   }
+  if (ba.defer) {  // (uniform per CTA)
+    const double slb = slope_lb(bf, ba, band);
+    const bool deferred = slb > 0.0;
+    if (ba.defer == 1 && deferred) {
+      if (threadIdx.x == 0) {
+        ba.lb[band] = slb;
+        ba.wq[band] = INFINITY;
+      }
+      return;
+    }
+    if (ba.defer == 2) {
+      if (!deferred) return;
+      const lms_candidate best = *ba.best;
+      // a band whose slope bound exceeds the seeds' H keeps it: dismissed
+      if (best.found && slb > best.height * (1.0 + 0x1p-19)) return;
+    }
+  }
   const double uM = 0.5 * uL + 0.5 * uR;
   const double dmax = bf.dev * fmax(uR - uM, uM - uL) * (1.0 + 0x1p-40);
   band_keys<kThreads, kItems>(bf, uM, sh);

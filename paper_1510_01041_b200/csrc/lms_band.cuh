@@ -127,6 +127,11 @@ struct BandArgs {
   // min |u| * W_q(a) - 2 bmax (slope_lb)
   const double* wqa;
   const lms_candidate* best;  // the fit's current best record (H)
+  // bounds (mode 0) in two phases: 1 = bands whose slope bound is positive
+  // only get it (lb = slope bound, wq = inf: no seeds from them); 2 = after
+  // the seeds, exactly those bands, bounded fully unless the slope bound
+  // already exceeds H; 0 = one phase
+  int defer;
   int64_t* out_ranks;
   int32_t* out_fits;
   int32_t fit;

@@ -304,6 +304,8 @@ struct lms_ctx {
   int band_coarse = 2;
   int prepass_split = 1;         // pass-0 screen with lines split over CTAs (LMSB_PREPASS_SPLIT)
   int seed_bands = 8;            // bands whose window-edge pairs seed H (LMSB_SEED_BANDS)
+  int defer_bounds = 1;          // bands with a positive slope bound bounded after the seeds
+                                 // (LMSB_DEFER)
   int plan_pool = 0;             // large-n shard plan: coarse-window pool given exact bounds
                                  // (LMSB_PLAN_POOL; 0: 64 / shards, at least 4 T)
   DevBuf<int64_t> bbig_seg;
@@ -444,6 +446,7 @@ int ctx_init(lms_ctx* c, int device) {
   if (const char* bs = getenv("LMSB_BIG_SLICE"); bs && atoll(bs) >= 1) c->big_slice = atoll(bs);
   if (const char* sb = getenv("LMSB_SEED_BANDS"); sb && atoi(sb) >= 1)
     c->seed_bands = std::min(48, atoi(sb));
+  if (const char* df = getenv("LMSB_DEFER")) c->defer_bounds = atoi(df) != 0;
   if (const char* pp = getenv("LMSB_PLAN_POOL"); pp && atoi(pp) >= 1)
     c->plan_pool = std::min(64, atoi(pp));
   if (const char* ps = getenv("LMSB_PREPASS_SPLIT")) c->prepass_split = atoi(ps) != 0;
@@ -1143,6 +1146,7 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
   }
   const int64_t span = h.r1 - h.r0;
   bool filter_timed = false, sweep_timed = false, bound_timed = false;
+  bool defer_bounds = false;  // two-phase bounds (LMSB_DEFER)
   ShardSpec* sh = c->shard;
   const int64_t P0 = sh ? sh->P0 : h.r0;
   const int64_t pspan = sh ? sh->P1 - sh->P0 : span;
@@ -1410,7 +1414,12 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
     }
   } else if (k1 > k0 && !coarse) {
     CUDA_TRY(ev_rec(c, c->ev_chunk[12]));
-    lmsb::launch_band(bf, ba, 0, (int)(k1 - k0), c->stream);
+    // bands whose slope bound is positive are bounded after the seeds, and
+    // only while that bound does not already exceed H (LMSB_DEFER)
+    defer_bounds = c->defer_bounds && !sh && ba.wqa;
+    lmsb::BandArgs bd = ba;
+    bd.defer = defer_bounds ? 1 : 0;
+    lmsb::launch_band(bf, bd, 0, (int)(k1 - k0), c->stream);
     CUDA_TRY(ev_rec(c, c->ev_chunk[13]));
     bound_timed = true;
     st->launches += 1;
@@ -1700,6 +1709,12 @@ int band_solve(lms_ctx* c, const HostFit& h, lms_stats* st) {
                                        seed_cap, sc + 2, c->stream);
     lmsb::launch_band_seeds(bf, w, c->ranks.p, c->item_fit.p, 0, seed_cap, sc + 2, c->stream);
     RC_TRY(exact_list(sc + 2, seed_cap, c->ranks.p, c->item_fit.p));
+    if (defer_bounds) {
+      lmsb::BandArgs bd = ba;
+      bd.defer = 2;
+      lmsb::launch_band(bf, bd, 0, (int)(k1 - k0), c->stream);
+      st->launches += 1;
+    }
     CUDA_TRY(ev_rec(c, c->ev_chunk[7]));
     trace_mark(c, "seeds");
     if (!dplan) {
