@@ -303,7 +303,9 @@ struct lms_ctx {
   // one shared-memory sort per band is cheaper than binning plus a refine)
   int band_coarse = 2;
   int prepass_split = 1;         // pass-0 screen with lines split over CTAs (LMSB_PREPASS_SPLIT)
-  int seed_bands = 8;            // bands whose window-edge pairs seed H (LMSB_SEED_BANDS)
+  int seed_bands = 3;            // bands whose window-edge pairs seed H (LMSB_SEED_BANDS; 8 -> 3:
+                                 // config 2 0.762 -> 0.750 ms, n = 20,000 2.03 -> 1.98 ms, same
+                                 // survivors: the seeds fit one round of the cached exact kernel)
   int defer_bounds = 1;          // bands with a positive slope bound bounded after the seeds
                                  // (LMSB_DEFER)
   int plan_pool = 0;             // large-n shard plan: coarse-window pool given exact bounds
