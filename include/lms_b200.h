@@ -286,6 +286,9 @@ int lms_probe_fp32_rate(int device, double* fma_lanes_per_second);
  * tests of the sort itself. */
 int lms_debug_seg_sort(int device, const float* keys, float* out, int64_t total, int32_t nseg,
                        const int64_t* seg_begin, const int64_t* seg_end);
+/* Diagnostics: the band stage's slope-sample bucket sort (lms_samplesort.cu)
+ * on a host buffer: keys[0, n) ascending into out. */
+int lms_debug_sample_sort(int device, const float* keys, float* out, int64_t n);
 
 /* ---- multi-GPU exact LMS: the vertex space of one fit
  * shared over several GPUs, one NCCL collective exchange of 56-byte records

@@ -17,7 +17,7 @@ CSRC = os.path.join(PKG_DIR, "csrc")
 LIB_DIR = os.path.join(PKG_DIR, "_lib")
 LIB_PATH = os.path.join(LIB_DIR, "liblmsb200.so")
 
-SOURCES = ["lms_engine.cu", "lms_band.cu", "lms_sweep.cu", "lms_segsort.cu", "lms_nccl.cu", "lms_detect.cu", "lms_sets.cu", "lms_band_small.cu", "lms_exact.cu", "lms_filter32m.cu", "lms_order.cu", "lms_plan.cu",
+SOURCES = ["lms_engine.cu", "lms_band.cu", "lms_sweep.cu", "lms_segsort.cu", "lms_samplesort.cu", "lms_nccl.cu", "lms_detect.cu", "lms_sets.cu", "lms_band_small.cu", "lms_exact.cu", "lms_filter32m.cu", "lms_order.cu", "lms_plan.cu",
            "lms_hough.cu", "lms_primal.cu", "lms_probe.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

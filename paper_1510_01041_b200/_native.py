@@ -215,6 +215,7 @@ SIGNATURES = {
     "lms_probe_fp32_rate": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_double)]),
     "lms_debug_seg_sort": (ctypes.c_int, [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
                                           ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p]),
+    "lms_debug_sample_sort": (ctypes.c_int, [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64]),
 }
 
 
@@ -606,6 +607,15 @@ def debug_seg_sort(keys: np.ndarray, seg_begin, seg_end, device: int = 0) -> np.
     se = _i64(seg_end)
     check(lib.lms_debug_seg_sort(int(device), k.ctypes.data, out.ctypes.data, k.size, sb.size,
                                  sb.ctypes.data, se.ctypes.data))
+    return out
+
+
+def debug_sample_sort(keys: np.ndarray, device: int = 0) -> np.ndarray:
+    """The band stage's slope-sample bucket sort on a host array (diagnostic)."""
+    lib = _lib_ready()
+    k = np.ascontiguousarray(keys, dtype=np.float32)
+    out = np.empty_like(k)
+    check(lib.lms_debug_sample_sort(int(device), k.ctypes.data, out.ctypes.data, k.size))
     return out
 
 

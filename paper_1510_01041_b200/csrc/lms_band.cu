@@ -1585,7 +1585,13 @@ void launch_band_t(const BandFit& bf, const BandArgs& ba, int mode, int grid, cu
 size_t band_sample_temp_bytes(int64_t S) {
   size_t bytes = 0;
   cub::DeviceRadixSort::SortKeys(nullptr, bytes, (const float*)nullptr, (float*)nullptr, (int)S);
-  return bytes;
+  return std::max(bytes, sample_sort_scratch_bytes(S));
+}
+
+// the hand-written bucket sort of the sample (default) or CUB's (LMSB_SAMPLE_SORT=0)
+bool use_sample_sort() {
+  const char* e = getenv("LMSB_SAMPLE_SORT");
+  return !(e && e[0] == '0');
 }
 
 // grouping buckets: (slot, top slope bits), at most kGroupBuckets
@@ -1641,7 +1647,10 @@ bool use_seg_sort(int64_t max_len, int64_t nseg) {
 int launch_band_sample(const BandFit& bf, const BandWork& w, int sms, cudaStream_t st) {
   cudaMemsetAsync(w.nvalid, 0, sizeof(unsigned long long), st);
   band_sample_kernel<<<sms * 4, 256, 0, st>>>(bf, w.S, w.sample, w.nvalid);
-  if (use_seg_sort(w.S, 1)) {
+  if (use_sample_sort()) {
+    if (launch_sample_sort(w.sample, w.sample_sorted, w.S, w.temp, w.temp_bytes, st) != 0)
+      return -1;
+  } else if (use_seg_sort(w.S, 1)) {
     if (launch_seg_sort(w.sample, w.sample_sorted, w.S, 1, nullptr, nullptr, st) != 0) return -1;
   } else {
     size_t bytes = w.temp_bytes;

@@ -178,6 +178,12 @@ void launch_band_filter_big(const BandFit& bf, const BandArgs& ba, const float* 
                             cudaStream_t st);
 
 size_t band_sample_temp_bytes(int64_t S);
+// The slope-sample sort over the whole GPU (lms_samplesort.cu): keys[0, S)
+// ascending into out; scratch of sample_sort_scratch_bytes(S).  Used by
+// launch_band_sample unless LMSB_SAMPLE_SORT=0 (CUB's device radix sort).
+size_t sample_sort_scratch_bytes(int64_t S);
+int launch_sample_sort(const float* keys, float* out, int64_t S, void* scratch, size_t bytes,
+                       cudaStream_t st);
 // Segmented ascending sort of fp32 keys, one 8-CTA cluster per segment
 // (lms_segsort.cu): segment s is in[seg_b[s] .. seg_e[s]) (or [s * stride,
 // (s + 1) * stride) without seg_b), written to the same positions of out.

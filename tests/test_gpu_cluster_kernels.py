@@ -1,6 +1,7 @@
-"""The 8-CTA cluster kernels: the segmented sort (lms_segsort.cu) against
-numpy, and the cluster exact select (lms_exact.cu) against the streaming
-one-CTA-per-vertex select.
+"""The band stage's hand-written sorts and the cluster exact select: the
+8-CTA cluster segmented sort (lms_segsort.cu) and the whole-GPU slope-sample
+bucket sort (lms_samplesort.cu) against numpy, and the cluster exact select
+(lms_exact.cu) against the streaming one-CTA-per-vertex select.
 
 The sort can replace the CUB device sorts of the slope samples and of the
 large-n band / slice keys (LMSB_SEG_SORT=1; measured slower, so opt-in); its output must be the ascending order of the
@@ -129,3 +130,46 @@ def test_exact_cluster_select_same_as_streaming(n, seed):
             os.environ.pop("LMSB_EXACT_CLUSTER", None)
         out.append((rec.height, rec.i, rec.j, rec.u, rec.v_low, rec.v_high))
     assert out[0] == out[1]
+
+
+@pytest.mark.parametrize("n", [1, 2, 5, 1000, 1023, 1024, 1025, 65536, 100003, 1 << 20])
+def test_sample_sort_random(n):
+    rng = np.random.default_rng(n)
+    x = (rng.standard_cauchy(n) * 10).astype(np.float32)
+    got = _native.debug_sample_sort(x)
+    assert np.array_equal(got.view(np.uint32), _radix_order(x).view(np.uint32))
+
+
+@pytest.mark.parametrize("kind", ["equal", "infs", "few", "periodic", "sorted", "reversed", "special"])
+def test_sample_sort_adversarial(kind):
+    """Ties everywhere, invalid samples (+inf), and a periodic input whose
+    every 64th key (the splitter sample) differs from all the others: one
+    bucket then holds almost every key (the chunked merge fallback)."""
+    n = 65536
+    rng = np.random.default_rng(11)
+    if kind == "equal":
+        x = np.full(n, -3.25, np.float32)
+    elif kind == "infs":
+        x = rng.standard_normal(n).astype(np.float32)
+        x[rng.random(n) < 0.6] = np.inf
+    elif kind == "few":
+        x = rng.integers(-2, 3, n).astype(np.float32)
+    elif kind == "periodic":
+        x = np.full(n, 7.0, np.float32)
+        x[64::128] = rng.standard_normal(n // 128).astype(np.float32) * 100
+        x[:5000] = rng.standard_normal(5000).astype(np.float32)
+    elif kind == "sorted":
+        x = np.sort(rng.standard_normal(n)).astype(np.float32)
+    elif kind == "reversed":
+        x = np.sort(rng.standard_normal(n))[::-1].astype(np.float32).copy()
+    else:
+        x = rng.standard_normal(n).astype(np.float32)
+        x[::7] = 0.0
+        x[::11] = -0.0
+        x[::13] = -np.inf
+    got = _native.debug_sample_sort(x)
+    want = _radix_order(x)
+    if kind == "special":  # -0.0 / +0.0 order is free (no caller tells them apart)
+        assert np.array_equal(got, want)
+    else:
+        assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
