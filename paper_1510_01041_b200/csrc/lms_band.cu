@@ -1681,7 +1681,16 @@ size_t band_big_sort_temp_bytes(int nb, int64_t n) {
   cub::DeviceSegmentedRadixSort::SortKeys(nullptr, bytes, (const float*)nullptr, (float*)nullptr,
                                           (int)(nb * n), nb, (const int64_t*)nullptr,
                                           (const int64_t*)nullptr);
-  return bytes;
+  return std::max(bytes, seg_bucket_sort_scratch_bytes((int64_t)nb * n, nb, n));
+}
+
+// Opt-in (LMSB_SEG_BUCKET=1): the sample sort's bucket scheme per segment
+// measured slower than the cluster / CUB sorts on every large-n path (config
+// 3 7.65 -> 7.94 ms, n = 20,000 1.98 -> 2.45 ms: 256 buckets of ~78-256 keys
+// per segment leave its per-bucket CTAs mostly idle)
+bool use_seg_bucket() {
+  const char* e = getenv("LMSB_SEG_BUCKET");
+  return e && e[0] == '1';
 }
 
 __global__ void seg_offsets_kernel(int64_t* off, int nb, int64_t n) {
@@ -1697,7 +1706,11 @@ int launch_band_bound_big(const BandFit& bf, const BandArgs& ba, const BandBig& 
     const int nb = std::min(bg.batch, k1 - b0);
     dim3 grid((unsigned)std::min<int64_t>((n + 255) / 256, 64), (unsigned)std::min(nb, 65535));
     band_keys_global_kernel<<<grid, 256, 0, st>>>(bf, ba.bounds, ba.K, b0, ids, nb, bg.keys);
-    if (use_seg_sort(n, nb)) {
+    if (use_seg_bucket()) {
+      if (launch_seg_bucket_sort(bg.keys, bg.keys_alt, (int64_t)nb * n, nb, n, nullptr, nullptr,
+                                 bg.temp, bg.temp_bytes, st) != 0)
+        return -1;
+    } else if (use_seg_sort(n, nb)) {
       if (launch_seg_sort(bg.keys, bg.keys_alt, n, nb, nullptr, nullptr, st) != 0) return -1;
     } else {
       size_t bytes = bg.temp_bytes;
@@ -1846,7 +1859,8 @@ size_t band_slice_sort_temp_bytes(int64_t nslices_max, int64_t n) {
   cub::DeviceSegmentedRadixSort::SortKeys(nullptr, bytes, (const float*)nullptr, (float*)nullptr,
                                           (int)(nslices_max * n), (int)nslices_max,
                                           (const int64_t*)nullptr, (const int64_t*)nullptr);
-  return bytes;
+  return std::max(bytes,
+                  seg_bucket_sort_scratch_bytes(nslices_max * n, (int)nslices_max, n));
 }
 
 int launch_band_slices(const BandFit& bf, const BandArgs& ba, int64_t nslices_max, float* keys,
@@ -1857,7 +1871,11 @@ int launch_band_slices(const BandFit& bf, const BandArgs& ba, int64_t nslices_ma
   dim3 grid((unsigned)std::min<int64_t>((bf.n + 255) / 256, 64),
             (unsigned)std::min<int64_t>(nslices_max, 65535));
   band_slice_keys_kernel<<<grid, 256, 0, st>>>(bf, ba, nslices_max, keys, seg_begin, seg_end);
-  if (use_seg_sort(bf.n, nslices_max)) {
+  if (use_seg_bucket() && nslices_max <= 65535) {
+    if (launch_seg_bucket_sort(keys, store, nslices_max * bf.n, (int)nslices_max, bf.n, seg_begin,
+                               seg_end, temp, temp_bytes, st) != 0)
+      return -1;
+  } else if (use_seg_sort(bf.n, nslices_max)) {
     if (launch_seg_sort(keys, store, bf.n, (int)nslices_max, seg_begin, seg_end, st) != 0)
       return -1;
   } else {

@@ -182,6 +182,14 @@ size_t band_sample_temp_bytes(int64_t S);
 // ascending into out; scratch of sample_sort_scratch_bytes(S).  Used by
 // launch_band_sample unless LMSB_SAMPLE_SORT=0 (CUB's device radix sort).
 size_t sample_sort_scratch_bytes(int64_t S);
+// The same bucket sort per segment (segments keys[seg_b[y], seg_e[y]) or
+// [y * max_len, (y + 1) * max_len)), all segments in the same launches.
+size_t seg_bucket_sort_scratch_bytes(int64_t total, int nseg, int64_t max_len);
+int launch_seg_bucket_sort(const float* keys, float* out, int64_t total, int nseg,
+                           int64_t max_len, const int64_t* seg_b, const int64_t* seg_e,
+                           void* scratch, size_t bytes, cudaStream_t st);
+// the bucket sort for the large-n segmented sorts when LMSB_SEG_BUCKET=1 (opt-in)
+bool use_seg_bucket();
 int launch_sample_sort(const float* keys, float* out, int64_t S, void* scratch, size_t bytes,
                        cudaStream_t st);
 // Segmented ascending sort of fp32 keys, one 8-CTA cluster per segment

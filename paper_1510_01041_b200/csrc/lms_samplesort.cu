@@ -24,6 +24,7 @@
 // distinguishes).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include <cub/block/block_radix_sort.cuh>
@@ -52,16 +53,35 @@ __device__ __forceinline__ uint32_t ss_key(float f) {
 __device__ __forceinline__ float ss_float(uint32_t k) {
   return __uint_as_float(k ^ ((k >> 31) ? 0x80000000u : 0xFFFFFFFFu));
 }
-__device__ __forceinline__ unsigned long long ss_comp(const float* keys, int64_t s) {
-  return ((unsigned long long)ss_key(keys[s]) << 32) | (unsigned long long)(uint32_t)s;
+// segment y: keys[base, base + L) (seg_b / seg_e, or [y * stride, (y + 1) * stride))
+struct SsSeg {
+  const int64_t* seg_b;
+  const int64_t* seg_e;
+  int64_t stride;
+};
+__device__ __forceinline__ void ss_segment(const SsSeg& sg, int y, int64_t* base, int64_t* L) {
+  if (sg.seg_b) {
+    *base = sg.seg_b[y];
+    *L = sg.seg_e[y] - *base;
+  } else {
+    *base = (int64_t)y * sg.stride;
+    *L = sg.stride;
+  }
+}
+// (ordered key, position in the segment): distinct for equal keys
+__device__ __forceinline__ unsigned long long ss_comp(const float* keys, int64_t base, int64_t s) {
+  return ((unsigned long long)ss_key(keys[base + s]) << 32) | (unsigned long long)(uint32_t)s;
 }
 
-__global__ void __launch_bounds__(kSsR) ss_split_kernel(const float* __restrict__ keys, int64_t S,
+__global__ void __launch_bounds__(kSsR) ss_split_kernel(const float* __restrict__ keys, SsSeg sg,
                                                         unsigned long long* __restrict__ spl) {
   __shared__ unsigned long long v[kSsR];
+  int64_t base, S;
+  ss_segment(sg, blockIdx.x, &base, &S);
+  if (S <= 0) return;
   const int t = threadIdx.x;
   const int64_t pos = (t * S) / kSsR + (S / kSsR) / 2;
-  v[t] = ss_comp(keys, pos < S ? pos : S - 1);
+  v[t] = ss_comp(keys, base, pos < S ? pos : S - 1);
   for (int k = 2; k <= kSsR; k <<= 1) {
     for (int j = k >> 1; j > 0; j >>= 1) {
       __syncthreads();
@@ -76,51 +96,106 @@ __global__ void __launch_bounds__(kSsR) ss_split_kernel(const float* __restrict_
     }
   }
   __syncthreads();
-  if (t < kSsB - 1) spl[t] = v[(t + 1) * (kSsR / kSsB) - 1];
+  if (t < kSsB - 1) spl[(int64_t)blockIdx.x * kSsB + t] = v[(t + 1) * (kSsR / kSsB) - 1];
 }
 
-__global__ void __launch_bounds__(kSsT) ss_count_kernel(const float* __restrict__ keys, int64_t S,
+// grid (tiles, segments); hist[(y * G + g) * 256 + b]
+__global__ void __launch_bounds__(kSsT) ss_count_kernel(const float* __restrict__ keys, SsSeg sg,
+                                                        int G,
                                                         const unsigned long long* __restrict__ spl,
                                                         uint8_t* __restrict__ bkt,
                                                         unsigned* __restrict__ hist) {
   __shared__ unsigned long long sp[kSsB];
   __shared__ unsigned h[kSsB];
+  int64_t base, S;
+  ss_segment(sg, blockIdx.y, &base, &S);
+  const int64_t s0 = (int64_t)blockIdx.x * kSsTile;
+  if (S <= 0 || s0 >= S) return;
   const int t = threadIdx.x;
-  sp[t] = t < kSsB - 1 ? spl[t] : ~0ull;
+  sp[t] = t < kSsB - 1 ? spl[(int64_t)blockIdx.y * kSsB + t] : ~0ull;
   h[t] = 0;
   __syncthreads();
-  const int64_t s0 = (int64_t)blockIdx.x * kSsTile;
   const int64_t s1 = s0 + kSsTile < S ? s0 + kSsTile : S;
   for (int64_t s = s0 + t; s < s1; s += kSsT) {
-    const unsigned long long c = ss_comp(keys, s);
+    const unsigned long long c = ss_comp(keys, base, s);
     int lo = 0, hi = kSsB - 1;  // first splitter >= c (sp[255] = max)
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
       if (sp[mid] < c) lo = mid + 1;
       else hi = mid;
     }
-    bkt[s] = (uint8_t)lo;
+    bkt[base + s] = (uint8_t)lo;
     atomicAdd(&h[lo], 1u);
   }
   __syncthreads();
-  hist[(int64_t)blockIdx.x * kSsB + t] = h[t];
+  hist[((int64_t)blockIdx.y * G + blockIdx.x) * kSsB + t] = h[t];
 }
 
 // keys to their buckets; every CTA forms its own write offsets from the
 // tiles' histograms (bucket start + the bucket's keys in earlier tiles), CTA
 // 0 also publishes the bucket starts
-__global__ void __launch_bounds__(kSsT) ss_scatter_kernel(const float* __restrict__ keys, int64_t S,
-                                                          int G, const uint8_t* __restrict__ bkt,
+// one CTA per segment: bucket starts and every tile's write offsets (in
+// place of its histogram) -- many segments; one segment's tiles form their
+// own offsets in ss_scatter_kernel (fused: one launch less)
+__global__ void __launch_bounds__(kSsT) ss_scan_kernel(SsSeg sg, int G, unsigned* __restrict__ hist,
+                                                       unsigned* __restrict__ bstart) {
+  __shared__ unsigned wsum[kSsT / 32];
+  int64_t base, S;
+  ss_segment(sg, blockIdx.x, &base, &S);
+  if (S <= 0) return;
+  const int Gs = (int)((S + kSsTile - 1) / kSsTile);
+  unsigned* hs = hist + (int64_t)blockIdx.x * G * kSsB;
+  const int t = threadIdx.x;
+  unsigned tot = 0;
+  for (int g = 0; g < Gs; ++g) tot += hs[(int64_t)g * kSsB + t];
+  unsigned incl = tot;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned x = __shfl_up_sync(0xffffffffu, incl, o);
+    if ((t & 31) >= o) incl += x;
+  }
+  if ((t & 31) == 31) wsum[t >> 5] = incl;
+  __syncthreads();
+  unsigned b = incl - tot;
+  for (int w = 0; w < (t >> 5); ++w) b += wsum[w];
+  bstart[(int64_t)blockIdx.x * (kSsB + 1) + t] = b;
+  if (t == kSsB - 1) bstart[(int64_t)blockIdx.x * (kSsB + 1) + kSsB] = (unsigned)S;
+  for (int g = 0; g < Gs; ++g) {
+    const unsigned c = hs[(int64_t)g * kSsB + t];
+    hs[(int64_t)g * kSsB + t] = b;
+    b += c;
+  }
+}
+
+__global__ void __launch_bounds__(kSsT) ss_scatter_kernel(const float* __restrict__ keys, SsSeg sg,
+                                                          int G, bool fused,
+                                                          const uint8_t* __restrict__ bkt,
                                                           const unsigned* __restrict__ hist,
                                                           unsigned* __restrict__ bstart,
                                                           uint32_t* __restrict__ tmp) {
   __shared__ unsigned cur[kSsB];
   __shared__ unsigned wsum[kSsT / 32];
-  const int t = threadIdx.x;  // = bucket
+  int64_t base, S;
+  ss_segment(sg, blockIdx.y, &base, &S);
   const int g0 = blockIdx.x;
+  const int64_t s0 = (int64_t)g0 * kSsTile;
+  if (S <= 0 || s0 >= S) return;
+  const int Gs = (int)((S + kSsTile - 1) / kSsTile);  // this segment's tiles
+  const unsigned* hs = hist + (int64_t)blockIdx.y * G * kSsB;
+  const int t = threadIdx.x;  // = bucket
+  if (!fused) {  // offsets from ss_scan_kernel
+    cur[t] = hs[(int64_t)g0 * kSsB + t];
+    __syncthreads();
+    const int64_t s1 = s0 + kSsTile < S ? s0 + kSsTile : S;
+    for (int64_t s = s0 + t; s < s1; s += kSsT) {
+      const unsigned p = atomicAdd(&cur[bkt[base + s]], 1u);
+      tmp[base + p] = ss_key(keys[base + s]);
+    }
+    return;
+  }
   unsigned tot = 0, pre = 0;
-  for (int g = 0; g < G; ++g) {
-    const unsigned c = hist[(int64_t)g * kSsB + t];
+  for (int g = 0; g < Gs; ++g) {
+    const unsigned c = hs[(int64_t)g * kSsB + t];
     tot += c;
     pre += g < g0 ? c : 0u;
   }
@@ -132,19 +207,75 @@ __global__ void __launch_bounds__(kSsT) ss_scatter_kernel(const float* __restric
   }
   if ((t & 31) == 31) wsum[t >> 5] = incl;
   __syncthreads();
-  unsigned base = incl - tot;
-  for (int w = 0; w < (t >> 5); ++w) base += wsum[w];
+  unsigned b = incl - tot;
+  for (int w = 0; w < (t >> 5); ++w) b += wsum[w];
   if (g0 == 0) {
-    bstart[t] = base;
-    if (t == kSsB - 1) bstart[kSsB] = (unsigned)S;
+    bstart[(int64_t)blockIdx.y * (kSsB + 1) + t] = b;
+    if (t == kSsB - 1) bstart[(int64_t)blockIdx.y * (kSsB + 1) + kSsB] = (unsigned)S;
   }
-  cur[t] = base + pre;
+  cur[t] = b + pre;
   __syncthreads();
-  const int64_t s0 = (int64_t)g0 * kSsTile;
   const int64_t s1 = s0 + kSsTile < S ? s0 + kSsTile : S;
   for (int64_t s = s0 + t; s < s1; s += kSsT) {
-    const unsigned p = atomicAdd(&cur[bkt[s]], 1u);
-    tmp[p] = ss_key(keys[s]);
+    const unsigned p = atomicAdd(&cur[bkt[base + s]], 1u);
+    tmp[base + p] = ss_key(keys[base + s]);
+  }
+}
+
+// buckets of at most 512 keys (almost all): 2 keys per thread, few
+// registers, so many CTAs per SM; larger buckets are left to ss_bucket_kernel
+__global__ void __launch_bounds__(kSsT) ss_small_bucket_kernel(SsSeg sg,
+                                                               const uint32_t* __restrict__ tmp,
+                                                               const unsigned* __restrict__ bstart,
+                                                               float* __restrict__ out) {
+  __shared__ typename SmallSort::TempStorage sort;
+  __shared__ uint32_t red[2][kSsT / 32];
+  const int t = threadIdx.x;
+  int64_t base, S;
+  ss_segment(sg, blockIdx.y, &base, &S);
+  if (S <= 0) return;
+  const unsigned* bs = bstart + (int64_t)blockIdx.y * (kSsB + 1);
+  const int64_t b0 = base + bs[blockIdx.x], b1 = base + bs[blockIdx.x + 1];
+  const int64_t m = b1 - b0;
+  if (m <= 0 || m > kSsT * kSsSmallItems) return;
+  uint32_t k[kSsSmallItems];
+  uint32_t lo = 0xFFFFFFFFu, hi = 0u;
+#pragma unroll
+  for (int i = 0; i < kSsSmallItems; ++i) {
+    const int64_t e = (int64_t)i * kSsT + t;
+    k[i] = e < m ? tmp[b0 + e] : 0u;
+    if (e < m) {
+      lo = min(lo, k[i]);
+      hi = max(hi, k[i]);
+    }
+  }
+  lo = __reduce_min_sync(0xffffffffu, lo);
+  hi = __reduce_max_sync(0xffffffffu, hi);
+  if ((t & 31) == 0) {
+    red[0][t >> 5] = lo;
+    red[1][t >> 5] = hi;
+  }
+  __syncthreads();
+  lo = red[0][0];
+  hi = red[1][0];
+#pragma unroll
+  for (int w = 1; w < kSsT / 32; ++w) {
+    lo = min(lo, red[0][w]);
+    hi = max(hi, red[1][w]);
+  }
+  if (lo == hi) {
+    for (int64_t e = t; e < m; e += kSsT) out[b0 + e] = ss_float(lo);
+    return;
+  }
+  const int end_bit = 32 - __clz(lo ^ hi);
+#pragma unroll
+  for (int i = 0; i < kSsSmallItems; ++i)
+    if ((int64_t)i * kSsT + t >= m) k[i] = hi;  // padding = the largest key
+  SmallSort(sort).SortBlockedToStriped(k, 0, end_bit);
+#pragma unroll
+  for (int i = 0; i < kSsSmallItems; ++i) {
+    const int64_t e = (int64_t)i * kSsT + t;
+    if (e < m) out[b0 + e] = ss_float(k[i]);
   }
 }
 
@@ -177,7 +308,7 @@ __device__ void ss_merge_round(const uint32_t* __restrict__ src, uint32_t* __res
   }
 }
 
-__global__ void __launch_bounds__(kSsT) ss_bucket_kernel(uint32_t* __restrict__ tmp,
+__global__ void __launch_bounds__(kSsT) ss_bucket_kernel(SsSeg sg, int nseg, uint32_t* __restrict__ tmp,
                                                          uint32_t* __restrict__ tmp2,
                                                          const unsigned* __restrict__ bstart,
                                                          float* __restrict__ out) {
@@ -187,9 +318,17 @@ __global__ void __launch_bounds__(kSsT) ss_bucket_kernel(uint32_t* __restrict__ 
   } sort;
   __shared__ uint32_t red[2][kSsT / 32];
   const int t = threadIdx.x;
-  const int64_t b0 = bstart[blockIdx.x], b1 = bstart[blockIdx.x + 1];
+  // persistent over (segment, bucket): almost every bucket is small and
+  // belongs to ss_small_bucket_kernel
+  for (int64_t item = blockIdx.x; item < (int64_t)nseg * kSsB; item += gridDim.x) {
+  const int y = (int)(item / kSsB), bb = (int)(item % kSsB);
+  int64_t base, S;
+  ss_segment(sg, y, &base, &S);
+  if (S <= 0) continue;
+  const unsigned* bs = bstart + (int64_t)y * (kSsB + 1);
+  const int64_t b0 = base + bs[bb], b1 = base + bs[bb + 1];
   const int64_t m = b1 - b0;
-  if (m <= 0) return;
+  if (m <= kSsT * kSsSmallItems) continue;  // (ss_small_bucket_kernel's)
   if (m <= kSsCap) {
     uint32_t k[kSsItems];
     uint32_t lo = 0xFFFFFFFFu, hi = 0u;
@@ -220,7 +359,8 @@ __global__ void __launch_bounds__(kSsT) ss_bucket_kernel(uint32_t* __restrict__ 
     }
     if (lo == hi) {  // one value
       for (int64_t e = t; e < m; e += kSsT) out[b0 + e] = ss_float(lo);
-      return;
+      __syncthreads();  // (red is reused by the next bucket)
+      continue;
     }
     const int end_bit = 32 - __clz(lo ^ hi);
     // padding = the largest key: ties with it are equal values, so the first
@@ -228,25 +368,14 @@ __global__ void __launch_bounds__(kSsT) ss_bucket_kernel(uint32_t* __restrict__ 
 #pragma unroll
     for (int i = 0; i < kSsItems; ++i)
       if ((int64_t)i * kSsT + t >= m) k[i] = hi;
-    if (m <= kSsT * kSsSmallItems) {
-      uint32_t ks[kSsSmallItems];
-#pragma unroll
-      for (int i = 0; i < kSsSmallItems; ++i) ks[i] = k[i];
-      SmallSort(sort.small).SortBlockedToStriped(ks, 0, end_bit);
-#pragma unroll
-      for (int i = 0; i < kSsSmallItems; ++i) {
-        const int64_t e = (int64_t)i * kSsT + t;
-        if (e < m) out[b0 + e] = ss_float(ks[i]);
-      }
-      return;
-    }
     BucketSort(sort.big).SortBlockedToStriped(k, 0, end_bit);
 #pragma unroll
     for (int i = 0; i < kSsItems; ++i) {
       const int64_t e = (int64_t)i * kSsT + t;
       if (e < m) out[b0 + e] = ss_float(k[i]);
     }
-    return;
+    __syncthreads();
+    continue;
   }
   // oversize bucket: sorted 4,096-key chunks, then merge rounds (ping-pong)
   uint32_t* src = tmp + b0;
@@ -274,39 +403,60 @@ __global__ void __launch_bounds__(kSsT) ss_bucket_kernel(uint32_t* __restrict__ 
     dst = x;
   }
   for (int64_t e = t; e < m; e += kSsT) out[b0 + e] = ss_float(src[e]);
+  __syncthreads();
+  }
 }
 
 }  // namespace
 
-size_t sample_sort_scratch_bytes(int64_t S) {
-  const int64_t G = (S + kSsTile - 1) / kSsTile;
-  return (size_t)(kSsB * 8 + (kSsB + 1) * 4 + 16) + (size_t)G * kSsB * 4 + (size_t)S +
-         2 * (size_t)S * 4 + 256;
+// scratch of a segmented sort: per segment 255 splitters, 257 bucket starts
+// and max_len / 1,024 tile histograms; per key of keys[0, total) a bucket id
+// and two staging words
+size_t seg_bucket_sort_scratch_bytes(int64_t total, int nseg, int64_t max_len) {
+  const int64_t G = (max_len + kSsTile - 1) / kSsTile;
+  return (size_t)nseg * (kSsB * 8 + (kSsB + 1) * 4 + (size_t)G * kSsB * 4) + (size_t)total * 9 +
+         256;
 }
+
+int launch_seg_bucket_sort(const float* keys, float* out, int64_t total, int nseg,
+                           int64_t max_len, const int64_t* seg_b, const int64_t* seg_e,
+                           void* scratch, size_t bytes, cudaStream_t st) {
+  if (nseg <= 0 || max_len <= 0) return 0;
+  if (max_len > ((int64_t)1 << 31) - 1 || nseg > 65535 ||
+      bytes < seg_bucket_sort_scratch_bytes(total, nseg, max_len))
+    return -1;
+  const int G = (int)((max_len + kSsTile - 1) / kSsTile);
+  auto align = [](uintptr_t p) { return (p + 15) & ~(uintptr_t)15; };
+  uintptr_t p = align((uintptr_t)scratch);
+  auto* spl = reinterpret_cast<unsigned long long*>(p);
+  p = align(p + (size_t)nseg * kSsB * 8);
+  auto* bstart = reinterpret_cast<unsigned*>(p);
+  p = align(p + (size_t)nseg * (kSsB + 1) * 4);
+  auto* hist = reinterpret_cast<unsigned*>(p);
+  p = align(p + (size_t)nseg * G * kSsB * 4);
+  auto* tmp = reinterpret_cast<uint32_t*>(p);
+  p = align(p + (size_t)total * 4);
+  auto* tmp2 = reinterpret_cast<uint32_t*>(p);
+  p = align(p + (size_t)total * 4);
+  auto* bkt = reinterpret_cast<uint8_t*>(p);
+  SsSeg sg{seg_b, seg_e, seg_b ? 0 : max_len};
+  ss_split_kernel<<<nseg, kSsR, 0, st>>>(keys, sg, spl);
+  ss_count_kernel<<<dim3(G, nseg), kSsT, 0, st>>>(keys, sg, G, spl, bkt, hist);
+  const bool fused = nseg == 1;
+  if (!fused) ss_scan_kernel<<<nseg, kSsT, 0, st>>>(sg, G, hist, bstart);
+  ss_scatter_kernel<<<dim3(G, nseg), kSsT, 0, st>>>(keys, sg, G, fused, bkt, hist, bstart, tmp);
+  ss_small_bucket_kernel<<<dim3(kSsB, nseg), kSsT, 0, st>>>(sg, tmp, bstart, out);
+  ss_bucket_kernel<<<(unsigned)std::min<int64_t>((int64_t)nseg * kSsB, 296), kSsT, 0, st>>>(
+      sg, nseg, tmp, tmp2, bstart, out);
+  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+size_t sample_sort_scratch_bytes(int64_t S) { return seg_bucket_sort_scratch_bytes(S, 1, S); }
 
 int launch_sample_sort(const float* keys, float* out, int64_t S, void* scratch, size_t bytes,
                        cudaStream_t st) {
   if (S <= 0) return 0;
-  if (S > ((int64_t)1 << 31) - 1 || bytes < sample_sort_scratch_bytes(S)) return -1;
-  const int G = (int)((S + kSsTile - 1) / kSsTile);
-  auto align = [](uintptr_t p) { return (p + 15) & ~(uintptr_t)15; };
-  uintptr_t p = align((uintptr_t)scratch);
-  auto* spl = reinterpret_cast<unsigned long long*>(p);
-  p = align(p + kSsB * 8);
-  auto* bstart = reinterpret_cast<unsigned*>(p);
-  p = align(p + (kSsB + 1) * 4);
-  auto* hist = reinterpret_cast<unsigned*>(p);
-  p = align(p + (size_t)G * kSsB * 4);
-  auto* tmp = reinterpret_cast<uint32_t*>(p);
-  p = align(p + (size_t)S * 4);
-  auto* tmp2 = reinterpret_cast<uint32_t*>(p);
-  p = align(p + (size_t)S * 4);
-  auto* bkt = reinterpret_cast<uint8_t*>(p);
-  ss_split_kernel<<<1, kSsR, 0, st>>>(keys, S, spl);
-  ss_count_kernel<<<G, kSsT, 0, st>>>(keys, S, spl, bkt, hist);
-  ss_scatter_kernel<<<G, kSsT, 0, st>>>(keys, S, G, bkt, hist, bstart, tmp);
-  ss_bucket_kernel<<<kSsB, kSsT, 0, st>>>(tmp, tmp2, bstart, out);
-  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+  return launch_seg_bucket_sort(keys, out, S, 1, S, nullptr, nullptr, scratch, bytes, st);
 }
 
 }  // namespace lmsb

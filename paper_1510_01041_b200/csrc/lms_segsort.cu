@@ -28,6 +28,7 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "../../include/lms_b200.h"
@@ -366,6 +367,25 @@ int launch_seg_sort(const float* in, float* out, int64_t stride, int nseg, const
 
 }  // namespace lmsb
 
+namespace {
+// the cluster sort (default) or, with LMSB_SEG_BUCKET=1, the segmented bucket sort
+bool sort_segments(const float* d_in, float* d_out, int64_t total, int32_t nseg,
+                   const int64_t* h_b, const int64_t* h_e, const int64_t* d_seg) {
+  if (!lmsb::use_seg_bucket()) return lmsb::launch_seg_sort(d_in, d_out, 0, nseg, d_seg, d_seg + nseg, 0) == 0;
+  int64_t max_len = 0;
+  for (int32_t s = 0; s < nseg; ++s) max_len = std::max<int64_t>(max_len, h_e[s] - h_b[s]);
+  if (max_len <= 0) return true;
+  const size_t sb = lmsb::seg_bucket_sort_scratch_bytes(total, nseg, max_len);
+  void* scratch = nullptr;
+  if (cudaMalloc(&scratch, sb) != cudaSuccess) return false;
+  const bool ok = lmsb::launch_seg_bucket_sort(d_in, d_out, total, nseg, max_len, d_seg, d_seg + nseg,
+                                               scratch, sb, 0) == 0 &&
+                  cudaDeviceSynchronize() == cudaSuccess;
+  cudaFree(scratch);
+  return ok;
+}
+}  // namespace
+
 extern "C" int lms_debug_seg_sort(int device, const float* keys, float* out, int64_t total,
                                   int32_t nseg, const int64_t* seg_begin, const int64_t* seg_end) {
   if (!keys || !out || total < 0 || nseg < 0 || (nseg > 0 && (!seg_begin || !seg_end)))
@@ -394,7 +414,7 @@ extern "C" int lms_debug_seg_sort(int device, const float* keys, float* out, int
              cudaMemcpy(d_seg + nseg, seg_end, nseg * sizeof(int64_t), cudaMemcpyHostToDevice) !=
                  cudaSuccess) {
     rc = LMS_ERR_CUDA;
-  } else if (lmsb::launch_seg_sort(d_in, d_out, 0, nseg, d_seg, d_seg + nseg, 0) != 0 ||
+  } else if (!sort_segments(d_in, d_out, total, nseg, seg_begin, seg_end, d_seg) ||
              cudaDeviceSynchronize() != cudaSuccess ||
              cudaMemcpy(out, d_out, total * sizeof(float), cudaMemcpyDeviceToHost) !=
                  cudaSuccess) {

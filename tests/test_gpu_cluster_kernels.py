@@ -29,6 +29,19 @@ def _radix_order(x: np.ndarray) -> np.ndarray:
     return x[np.argsort(k, kind="stable")]
 
 
+@pytest.fixture(params=["1", "0"], ids=["bucket", "cluster"], autouse=True)
+def seg_impl(request):
+    """Every segmented-sort case runs through the segmented bucket sort
+    (LMSB_SEG_BUCKET=1) and the cluster sort (the default)."""
+    old = os.environ.get("LMSB_SEG_BUCKET")
+    os.environ["LMSB_SEG_BUCKET"] = request.param
+    yield request.param
+    if old is None:
+        os.environ.pop("LMSB_SEG_BUCKET", None)
+    else:
+        os.environ["LMSB_SEG_BUCKET"] = old
+
+
 def _check(keys, segs):
     keys = np.asarray(keys, dtype=np.float32)
     sb = np.array([s[0] for s in segs], dtype=np.int64)
