@@ -308,7 +308,8 @@ __device__ void ss_merge_round(const uint32_t* __restrict__ src, uint32_t* __res
   }
 }
 
-__global__ void __launch_bounds__(kSsT) ss_bucket_kernel(SsSeg sg, int nseg, uint32_t* __restrict__ tmp,
+__global__ void __launch_bounds__(kSsT) ss_bucket_kernel(SsSeg sg, int nseg, int64_t small_max,
+                                                         uint32_t* __restrict__ tmp,
                                                          uint32_t* __restrict__ tmp2,
                                                          const unsigned* __restrict__ bstart,
                                                          float* __restrict__ out) {
@@ -328,7 +329,8 @@ __global__ void __launch_bounds__(kSsT) ss_bucket_kernel(SsSeg sg, int nseg, uin
   const unsigned* bs = bstart + (int64_t)y * (kSsB + 1);
   const int64_t b0 = base + bs[bb], b1 = base + bs[bb + 1];
   const int64_t m = b1 - b0;
-  if (m <= kSsT * kSsSmallItems) continue;  // (ss_small_bucket_kernel's)
+  if (m <= small_max) continue;  // (ss_small_bucket_kernel's)
+  if (m <= 0) continue;
   if (m <= kSsCap) {
     uint32_t k[kSsItems];
     uint32_t lo = 0xFFFFFFFFu, hi = 0u;
@@ -368,6 +370,19 @@ __global__ void __launch_bounds__(kSsT) ss_bucket_kernel(SsSeg sg, int nseg, uin
 #pragma unroll
     for (int i = 0; i < kSsItems; ++i)
       if ((int64_t)i * kSsT + t >= m) k[i] = hi;
+    if (m <= kSsT * kSsSmallItems) {  // (a small bucket of the single-segment sort)
+      uint32_t ks[kSsSmallItems];
+#pragma unroll
+      for (int i = 0; i < kSsSmallItems; ++i) ks[i] = k[i];
+      SmallSort(sort.small).SortBlockedToStriped(ks, 0, end_bit);
+#pragma unroll
+      for (int i = 0; i < kSsSmallItems; ++i) {
+        const int64_t e = (int64_t)i * kSsT + t;
+        if (e < m) out[b0 + e] = ss_float(ks[i]);
+      }
+      __syncthreads();
+      continue;
+    }
     BucketSort(sort.big).SortBlockedToStriped(k, 0, end_bit);
 #pragma unroll
     for (int i = 0; i < kSsItems; ++i) {
@@ -445,9 +460,13 @@ int launch_seg_bucket_sort(const float* keys, float* out, int64_t total, int nse
   const bool fused = nseg == 1;
   if (!fused) ss_scan_kernel<<<nseg, kSsT, 0, st>>>(sg, G, hist, bstart);
   ss_scatter_kernel<<<dim3(G, nseg), kSsT, 0, st>>>(keys, sg, G, fused, bkt, hist, bstart, tmp);
-  ss_small_bucket_kernel<<<dim3(kSsB, nseg), kSsT, 0, st>>>(sg, tmp, bstart, out);
-  ss_bucket_kernel<<<(unsigned)std::min<int64_t>((int64_t)nseg * kSsB, 296), kSsT, 0, st>>>(
-      sg, nseg, tmp, tmp2, bstart, out);
+  if (nseg == 1) {  // one CTA per bucket, every size (the sample sort)
+    ss_bucket_kernel<<<kSsB, kSsT, 0, st>>>(sg, 1, 0, tmp, tmp2, bstart, out);
+  } else {  // small buckets by the light kernel, the rest by persistent CTAs
+    ss_small_bucket_kernel<<<dim3(kSsB, nseg), kSsT, 0, st>>>(sg, tmp, bstart, out);
+    ss_bucket_kernel<<<(unsigned)std::min<int64_t>((int64_t)nseg * kSsB, 296), kSsT, 0, st>>>(
+        sg, nseg, kSsT * kSsSmallItems, tmp, tmp2, bstart, out);
+  }
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
