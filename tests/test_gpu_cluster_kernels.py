@@ -186,3 +186,39 @@ def test_sample_sort_adversarial(kind):
         assert np.array_equal(got, want)
     else:
         assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+@pytest.mark.parametrize("case", ["grid", "collinear_majority", "dup_x", "huge_outliers"])
+def test_exact_cluster_select_adversarial(case):
+    """The cluster select on inputs full of ties (integer grids: many equal
+    cut values, exact-zero heights), a collinear majority (height 0), shared
+    x values (parallel duals) and 1e6 outliers, above the 16,384-line cache
+    limit: the same record as the streaming select."""
+    rng = np.random.default_rng(21)
+    n = 20000
+    if case == "grid":
+        pts = rng.integers(0, 300, (n, 2)).astype(float)
+    elif case == "collinear_majority":
+        x = rng.uniform(-50, 50, n)
+        y = 0.5 * x - 3.0
+        k = rng.random(n) < 0.45
+        y[k] = rng.uniform(-500, 500, k.sum())
+        pts = np.column_stack([x, y])
+    elif case == "dup_x":
+        x = np.round(rng.uniform(0, 40, n), 1)
+        pts = np.column_stack([x, -1.5 * x + rng.normal(0, 0.05, n)])
+    else:
+        pts = workloads.contaminated_line_points(n, 9)
+        pts[: n // 10, 1] += 1e6
+    a, b = pts[:, 0].copy(), pts[:, 1].copy()
+    out = []
+    for flag in ("1", "0"):
+        os.environ["LMSB_EXACT_CLUSTER"] = flag
+        try:
+            ctx = _native.Context(0)
+            ctx.upload(a, b)
+            rec = record_from_native(ctx.solve(n // 2 + 1, 0, n * (n - 1) // 2))
+        finally:
+            os.environ.pop("LMSB_EXACT_CLUSTER", None)
+        out.append((rec.height, rec.i, rec.j, rec.u, rec.v_low, rec.v_high))
+    assert out[0] == out[1]
