@@ -26,6 +26,7 @@
 #include <condition_variable>
 #include <atomic>
 #include <mutex>
+#include <new>
 #include <string>
 #include <thread>
 #include <string>
@@ -186,6 +187,25 @@ inline void share_of(int64_t total, int64_t parts, int64_t s, int64_t* lo, int64
 
 }  // namespace
 
+// Page-locked host memory for std::vector (cudaMallocHost / cudaFreeHost).
+template <class T>
+struct PinnedAlloc {
+  using value_type = T;
+  PinnedAlloc() = default;
+  template <class U>
+  PinnedAlloc(const PinnedAlloc<U>&) {}
+  T* allocate(size_t n) {
+    void* p = nullptr;
+    if (cudaMallocHost(&p, n * sizeof(T)) != cudaSuccess) throw std::bad_alloc();
+    return static_cast<T*>(p);
+  }
+  void deallocate(T* p, size_t) { cudaFreeHost(p); }
+  template <class U>
+  bool operator==(const PinnedAlloc<U>&) const { return true; }
+  template <class U>
+  bool operator!=(const PinnedAlloc<U>&) const { return false; }
+};
+
 struct lms_ctx {
   int device = 0;
   int sms = 148;
@@ -206,7 +226,9 @@ struct lms_ctx {
   const double* a = nullptr;
   const double* b = nullptr;
   int64_t nlines = 0;
-  std::vector<double> h_a, h_b;  // host copy: per-fit max |a|, max |b| for the filter margins
+  // host copy (pinned: the upload's DMA reads it asynchronously): per-fit
+  // max |a|, max |b| for the filter margins
+  std::vector<double, PinnedAlloc<double>> h_a, h_b;
   // or, for lines that stay on the device (lms_batched_fit_sets_f64), the
   // per-fit statistics computed there: fit offsets and (alo, ahi, am, bm)
   std::vector<int64_t> ext_off;
@@ -682,15 +704,39 @@ int ctx_upload(lms_ctx* c, const double* a, const double* b, int64_t n) {
   CUDA_TRY(cudaSetDevice(c->device));
   RC_TRY(c->a_own.need(n));
   RC_TRY(c->b_own.need(n));
-  CUDA_TRY(cudaMemcpyAsync(c->a_own.p, a, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
-  CUDA_TRY(cudaMemcpyAsync(c->b_own.p, b, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
-  c->h_a.assign(a, a + n);
-  c->h_b.assign(b, b + n);
+  // the host copy (pinned) and the line statistics in one pass, then two
+  // asynchronous DMAs from it (a pageable source would be staged by the
+  // driver synchronously)
+  try {
+    c->h_a.resize(n);
+    c->h_b.resize(n);
+  } catch (const std::bad_alloc&) {
+    return set_error(LMS_ERR_NOMEM, "pinned host copy of %lld lines", (long long)n);
+  }
+  double* ha = c->h_a.data();
+  double* hb = c->h_b.data();
+  double alo = INFINITY, ahi = -INFINITY, am = 0.0, bm = 0.0;
+#pragma omp simd reduction(min : alo) reduction(max : ahi, am, bm)
+  for (int64_t k = 0; k < n; ++k) {
+    const double x = a[k], y = b[k];
+    ha[k] = x;
+    hb[k] = y;
+    alo = x < alo ? x : alo;
+    ahi = x > ahi ? x : ahi;
+    am = std::fabs(x) > am ? std::fabs(x) : am;
+    bm = std::fabs(y) > bm ? std::fabs(y) : bm;
+  }
+  CUDA_TRY(cudaMemcpyAsync(c->a_own.p, ha, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->b_own.p, hb, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
   c->ext_off.clear();
   c->a = c->a_own.p;
   c->b = c->b_own.p;
   c->nlines = n;
-  cache_line_stats(c);
+  ++c->gen;  // (cache_line_stats, fused into the copy)
+  c->s_alo = alo;
+  c->s_ahi = ahi;
+  c->s_am = am;
+  c->s_bm = bm;
   return LMS_OK;
 }
 
